@@ -1,0 +1,213 @@
+"""TRPL+K CPU oracle -- TEST INFRASTRUCTURE ONLY.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s cpu_baseline /
+``--impl reference`` leg may import this package.  It wraps ``oracle.c`` (plain
+fp64 C + OpenMP, Algorithm 1 of PAPER.md:176-202 with the readings of
+DESIGN.md) via ctypes.  It shares no code with ``paper_1711_10128_b200``.
+
+Pins (tests/test_oracle_*.py): closed-form Laplacian spectra, dense
+``numpy.linalg.eigh`` / ``scipy.linalg.eigh(A, B)`` brute force on tiny
+problems, analytic sine eigenvectors for SpMV, ``math.fsum`` for dots, B-
+orthonormality, eq 3.1 bookkeeping, cross-cycle interlacing, the eq 3.2
+subspace rebuilt densely, LOPCG and TRLan reductions, exact matvec accounting.
+Parity unpinned: the matvec count to convergence (no paper value for these
+synthetic matrices; SURVEY 8(c.4) last row).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "oracle.c")
+_HDR = os.path.join(_HERE, "oracle.h")
+_LIB = os.path.join(_HERE, "liboracle.so")
+
+_P = ctypes.c_void_p
+_I64 = ctypes.c_int64
+
+
+def build(force: bool = False) -> str:
+    newest = max(os.path.getmtime(_SRC), os.path.getmtime(_HDR))
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < newest:
+        subprocess.check_call(["gcc", "-O2", "-fopenmp", "-fPIC", "-shared", "-std=c11",
+                               "-o", _LIB, _SRC, "-lm"])
+    return _LIB
+
+
+class _Problem(ctypes.Structure):
+    _fields_ = [("n", _I64), ("a_rowptr", _P), ("a_col", _P), ("a_val", _P),
+                ("b_rowptr", _P), ("b_col", _P), ("b_val", _P), ("sigma", ctypes.c_double),
+                ("p", ctypes.c_int), ("q", ctypes.c_int), ("l", ctypes.c_int),
+                ("tol", ctypes.c_double), ("tol_mode", ctypes.c_int), ("seed", ctypes.c_uint64),
+                ("max_cycles", ctypes.c_int), ("restart_size", ctypes.c_int),
+                ("lock_mode", ctypes.c_int), ("debug", ctypes.c_int)]
+
+
+class _Report(ctypes.Structure):
+    _fields_ = [("status", ctypes.c_int), ("cycles", ctypes.c_int),
+                ("a_matvecs", _I64), ("b_matvecs", _I64), ("precond_applies", _I64),
+                ("verify_matvecs", _I64), ("inner_steps", _I64), ("random_draws", _I64),
+                ("log_cap", ctypes.c_int), ("log_len", ctypes.c_int),
+                ("log_t", _P), ("log_mv", _P), ("log_theta_t", _P), ("log_res", _P),
+                ("log_k", _P), ("log_nprev", _P), ("log_thetas", _P), ("log_terr", _P),
+                ("log_orth", _P), ("dump_cycles", ctypes.c_int), ("dump_X", _P),
+                ("dump_rho", _P), ("dump_t", _P)]
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        build()
+        L = ctypes.CDLL(_LIB)
+        L.orc_u01.restype = ctypes.c_double
+        L.orc_u01.argtypes = [ctypes.c_uint64] * 3
+        L.orc_spmv.restype = None
+        L.orc_spmv.argtypes = [_I64, _P, _P, _P, _P, _P]
+        L.orc_dot.restype = ctypes.c_double
+        L.orc_dot.argtypes = [_I64, _P, _P]
+        L.orc_frobenius.restype = ctypes.c_double
+        L.orc_frobenius.argtypes = [_I64, _P]
+        L.orc_jacobi_diag.restype = None
+        L.orc_jacobi_diag.argtypes = [_I64, _P, _P, _P, _P, _P, _P, ctypes.c_double,
+                                      ctypes.c_double, _P]
+        L.orc_sym_eig.restype = ctypes.c_int
+        L.orc_sym_eig.argtypes = [ctypes.c_int, _P, _P, _P]
+        L.orc_cgs2.restype = ctypes.c_int
+        L.orc_cgs2.argtypes = [_I64, ctypes.c_int, _P, _P, _P, _P, _P, _P, _P, _P]
+        L.orc_trplk_solve.restype = ctypes.c_int
+        L.orc_trplk_solve.argtypes = [ctypes.POINTER(_Problem), _P, _P, _P, ctypes.POINTER(_Report)]
+        _lib = L
+    return _lib
+
+
+def _ptr(a):
+    return None if a is None else a.ctypes.data
+
+
+def _csr(M):
+    """Accept inputs.CSR or scipy.sparse csr; return (rowptr int64, col int64, val f64)."""
+    if M is None:
+        return None, None, None
+    if hasattr(M, "rowptr"):
+        return (np.ascontiguousarray(M.rowptr, np.int64), np.ascontiguousarray(M.col, np.int64),
+                np.ascontiguousarray(M.val, np.float64))
+    M = M.tocsr()
+    M.sort_indices()
+    return (np.ascontiguousarray(M.indptr, np.int64), np.ascontiguousarray(M.indices, np.int64),
+            np.ascontiguousarray(M.data, np.float64))
+
+
+def u01(seed, stream, index):
+    return lib().orc_u01(seed, stream, index)
+
+
+def spmv(A, x):
+    rp, ci, v = _csr(A)
+    x = np.ascontiguousarray(x, np.float64)
+    n = len(rp) - 1
+    y = np.empty(n, np.float64)
+    lib().orc_spmv(n, _ptr(rp), _ptr(ci), _ptr(v), _ptr(x), _ptr(y))
+    return y
+
+
+def dot(x, y):
+    x = np.ascontiguousarray(x, np.float64)
+    y = np.ascontiguousarray(y, np.float64)
+    return lib().orc_dot(len(x), _ptr(x), _ptr(y))
+
+
+def frobenius(A):
+    _, _, v = _csr(A)
+    return lib().orc_frobenius(len(v), _ptr(v))
+
+
+def jacobi_diag(A, B=None, sigma=0.0, floor_rel=1e-8):
+    ra, ca, va = _csr(A)
+    rb, cb, vb = _csr(B)
+    n = len(ra) - 1
+    M = np.empty(n, np.float64)
+    lib().orc_jacobi_diag(n, _ptr(ra), _ptr(ca), _ptr(va), _ptr(rb), _ptr(cb), _ptr(vb),
+                          sigma, floor_rel, _ptr(M))
+    return M
+
+
+def sym_eig(T):
+    T = np.asfortranarray(T, np.float64)
+    k = T.shape[0]
+    th = np.empty(k, np.float64)
+    Y = np.empty((k, k), np.float64, order="F")
+    sweeps = lib().orc_sym_eig(k, _ptr(T), _ptr(th), _ptr(Y))
+    if sweeps < 0:
+        raise RuntimeError("oracle Jacobi did not converge")
+    return th, Y
+
+
+def cgs2(V, w, B=None):
+    """Returns (w_out unnormalised, h (summed coefficients), beta, breakdown, passes)."""
+    V = np.asfortranarray(V, np.float64)
+    n, k = V.shape
+    w = np.array(w, dtype=np.float64, copy=True)
+    rb, cb, vb = _csr(B)
+    h = np.empty(max(k, 1), np.float64)
+    beta = ctypes.c_double()
+    passes = ctypes.c_int()
+    brk = lib().orc_cgs2(n, k, _ptr(V), _ptr(w), _ptr(rb), _ptr(cb), _ptr(vb), _ptr(h),
+                         ctypes.addressof(beta), ctypes.addressof(passes))
+    return w, h[:k], beta.value, bool(brk), passes.value
+
+
+STATUS = {0: "OK", 1: "EINVAL", 2: "NOT_CONVERGED", 3: "BREAKDOWN"}
+
+
+def solve(A, B=None, p=5, q=20, l=1, tol=1e-8, sigma=0.0, seed=12, max_cycles=5000,
+          tol_mode=0, restart_size=0, lock_mode=0, debug=False, dump_cycles=0,
+          want_vectors=True):
+    """Run Algorithm 1 (TRPL+K).  Returns a dict with eigenvalues, vectors, residuals,
+    counters and the per-cycle log."""
+    ra, ca, va = _csr(A)
+    rb, cb, vb = _csr(B)
+    n = len(ra) - 1
+    ph = restart_size if restart_size > 0 else p
+    prob = _Problem(n, _ptr(ra), _ptr(ca), _ptr(va), _ptr(rb), _ptr(cb), _ptr(vb), sigma,
+                    p, q, l, tol, tol_mode, seed, max_cycles, restart_size, lock_mode,
+                    1 if debug else 0)
+    cap = max_cycles
+    logs = {
+        "t": np.zeros(cap, np.int32), "mv": np.zeros(cap, np.int64),
+        "theta_t": np.zeros(cap), "res": np.zeros(cap), "k": np.zeros(cap, np.int32),
+        "nprev": np.zeros(cap, np.int32), "thetas": np.zeros((cap, ph)),
+        "terr": np.zeros(cap), "orth": np.zeros(cap),
+    }
+    dX = np.zeros((max(dump_cycles, 1), ph, n)) if dump_cycles else None
+    drho = np.zeros(max(dump_cycles, 1))
+    dt = np.zeros(max(dump_cycles, 1), np.int32)
+    rep = _Report(0, 0, 0, 0, 0, 0, 0, 0, cap, 0,
+                  _ptr(logs["t"]), _ptr(logs["mv"]), _ptr(logs["theta_t"]), _ptr(logs["res"]),
+                  _ptr(logs["k"]), _ptr(logs["nprev"]), _ptr(logs["thetas"]), _ptr(logs["terr"]),
+                  _ptr(logs["orth"]), dump_cycles, _ptr(dX), _ptr(drho), _ptr(dt))
+    evals = np.zeros(p)
+    resid = np.zeros(p)
+    evecs = np.zeros((p, n)) if want_vectors else None  # row c = eigenvector c (n contiguous)
+    st = lib().orc_trplk_solve(ctypes.byref(prob), _ptr(evals), _ptr(evecs), _ptr(resid),
+                               ctypes.byref(rep))
+    L = rep.log_len
+    out = {
+        "status": STATUS.get(st, st), "eigenvalues": evals, "residuals": resid,
+        "eigenvectors": None if evecs is None else evecs.T,
+        "cycles": rep.cycles, "a_matvecs": rep.a_matvecs, "b_matvecs": rep.b_matvecs,
+        "precond_applies": rep.precond_applies, "verify_matvecs": rep.verify_matvecs,
+        "inner_steps": rep.inner_steps, "random_draws": rep.random_draws,
+        "log": {k_: v[:L] for k_, v in logs.items()},
+    }
+    if dump_cycles:
+        nd = min(dump_cycles, rep.cycles)
+        out["dump"] = {"X": [dX[i].T.copy() for i in range(nd)], "rho": drho[:nd].copy(),
+                       "t": dt[:nd].copy()}
+    return out

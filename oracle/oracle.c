@@ -1,0 +1,496 @@
+/*
+ * TRPL+K CPU ORACLE -- TEST INFRASTRUCTURE ONLY (see oracle.h).
+ *
+ * Plain fp64 C + OpenMP, no BLAS, no code shared with the CUDA path.
+ * Every function cites the passage it follows.  "P:n" = PAPER.md line n,
+ * "S:n" = SPEC.md line n, "Rn" = reading n of SURVEY.md 8(c.3) / DESIGN.md.
+ *
+ * Determinism: every dot product uses 4096-row blocks summed sequentially and
+ * combined pairwise in a fixed order, so results do not depend on the number
+ * of OpenMP threads.
+ */
+#include "oracle.h"
+
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+
+#define ORC_BLK 4096
+
+/* ---------------------------------------------------------------- RNG (R13) */
+double orc_u01(uint64_t seed, uint64_t stream, uint64_t index) {
+    /* splitmix64 finaliser over (seed, stream, index); identical formula is stated in
+     * written out again here, not shared. */
+    uint64_t key = (seed * 0xD1B54A32D192ED03ULL) ^ (stream * 0xABC98388FB8FAC03ULL);
+    uint64_t z = key + (index + 1ULL) * 0x9E3779B97F4A7C15ULL;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    z ^= z >> 31;
+    return (double)(z >> 11) * (1.0 / 9007199254740992.0);
+}
+
+/* ------------------------------------------------------- sparse / BLAS-1 */
+void orc_spmv(int64_t n, const int64_t* rowptr, const int64_t* col, const double* val,
+              const double* x, double* y) {
+    /* y = A x, row by row (eq 3.1 "z = A G(:,j)"). */
+#pragma omp parallel for schedule(static) if (n > 32768)
+    for (int64_t i = 0; i < n; ++i) {
+        double s = 0.0;
+        for (int64_t p = rowptr[i]; p < rowptr[i + 1]; ++p) s += val[p] * x[col[p]];
+        y[i] = s;
+    }
+}
+
+static double pairwise_sum(const double* s, int64_t nb) {
+    if (nb == 1) return s[0];
+    int64_t h = nb / 2;
+    return pairwise_sum(s, h) + pairwise_sum(s + h, nb - h);
+}
+
+double orc_dot(int64_t n, const double* x, const double* y) {
+    if (n <= 0) return 0.0;
+    int64_t nb = (n + ORC_BLK - 1) / ORC_BLK;
+    double* s = (double*)malloc((size_t)nb * sizeof(double));
+#pragma omp parallel for schedule(static) if (n > 32768)
+    for (int64_t b = 0; b < nb; ++b) {
+        int64_t e = (b + 1) * ORC_BLK < n ? (b + 1) * ORC_BLK : n;
+        double a = 0.0;
+        for (int64_t i = b * ORC_BLK; i < e; ++i) a += x[i] * y[i];
+        s[b] = a;
+    }
+    double r = pairwise_sum(s, nb);
+    free(s);
+    return r;
+}
+
+double orc_frobenius(int64_t nnz, const double* val) {
+    /* eq 5.1: ||A||_F over all stored entries (both triangles) */
+    return sqrt(orc_dot(nnz, val, val));
+}
+
+static void axpy(int64_t n, double a, const double* x, double* y) {
+#pragma omp parallel for schedule(static) if (n > 32768)
+    for (int64_t i = 0; i < n; ++i) y[i] += a * x[i];
+}
+
+static void scal_copy(int64_t n, double a, const double* x, double* y) {
+#pragma omp parallel for schedule(static) if (n > 32768)
+    for (int64_t i = 0; i < n; ++i) y[i] = a * x[i];
+}
+
+void orc_jacobi_diag(int64_t n, const int64_t* a_rowptr, const int64_t* a_col, const double* a_val,
+                     const int64_t* b_rowptr, const int64_t* b_col, const double* b_val,
+                     double sigma, double floor_rel, double* M) {
+    /* d_i = max(|A_ii - sigma B_ii|, eps_d * max_j |A_jj|), M = diag(d)^-1 (R12). */
+    double* ad = (double*)calloc((size_t)n, sizeof(double));
+    double amax = 0.0;
+    for (int64_t i = 0; i < n; ++i) {
+        for (int64_t p = a_rowptr[i]; p < a_rowptr[i + 1]; ++p)
+            if (a_col[p] == i) ad[i] += a_val[p];
+        if (fabs(ad[i]) > amax) amax = fabs(ad[i]);
+    }
+    for (int64_t i = 0; i < n; ++i) {
+        double bd = 1.0;
+        if (b_rowptr) {
+            bd = 0.0;
+            for (int64_t p = b_rowptr[i]; p < b_rowptr[i + 1]; ++p)
+                if (b_col[p] == i) bd += b_val[p];
+        }
+        double d = fabs(ad[i] - sigma * bd);
+        double fl = floor_rel * amax;
+        M[i] = 1.0 / (d > fl ? d : fl);
+    }
+    free(ad);
+}
+
+/* ------------------------------------------------------------ small eig */
+int orc_sym_eig(int k, const double* T, double* theta, double* Y) {
+    /* Cyclic-by-row Jacobi (Golub & Van Loan Alg. 8.5.2/8.5.3) on sym(T).
+     * A rotation (p,q) is skipped when |a_pq| <= eps*sqrt(|a_pp a_qq|) or |a_pq| <= 1e-30||T||_F;
+     * a sweep without rotations ends the iteration. */
+    double* A = (double*)malloc((size_t)k * k * sizeof(double));
+    double* V = (double*)malloc((size_t)k * k * sizeof(double));
+    double fro = 0.0;
+    for (int j = 0; j < k; ++j)
+        for (int i = 0; i < k; ++i) {
+            A[i + (size_t)k * j] = 0.5 * (T[i + (size_t)k * j] + T[j + (size_t)k * i]);
+            V[i + (size_t)k * j] = (i == j) ? 1.0 : 0.0;
+            fro += A[i + (size_t)k * j] * A[i + (size_t)k * j];
+        }
+    fro = sqrt(fro);
+    const double eps = 2.220446049250313e-16;
+    int sweep, rotated = 1;
+    for (sweep = 0; sweep < 100 && rotated; ++sweep) {
+        rotated = 0;
+        for (int p = 0; p < k - 1; ++p)
+            for (int q = p + 1; q < k; ++q) {
+                double apq = A[p + (size_t)k * q];
+                double app = A[p + (size_t)k * p], aqq = A[q + (size_t)k * q];
+                if (fabs(apq) <= eps * sqrt(fabs(app * aqq)) || fabs(apq) <= 1e-30 * fro) continue;
+                rotated = 1;
+                double tau = (aqq - app) / (2.0 * apq);
+                double t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
+                double c = 1.0 / sqrt(1.0 + t * t), s = t * c;
+                for (int i = 0; i < k; ++i) { /* A <- A J */
+                    double aip = A[i + (size_t)k * p], aiq = A[i + (size_t)k * q];
+                    A[i + (size_t)k * p] = c * aip - s * aiq;
+                    A[i + (size_t)k * q] = s * aip + c * aiq;
+                }
+                for (int j = 0; j < k; ++j) { /* A <- J^T A */
+                    double apj = A[p + (size_t)k * j], aqj = A[q + (size_t)k * j];
+                    A[p + (size_t)k * j] = c * apj - s * aqj;
+                    A[q + (size_t)k * j] = s * apj + c * aqj;
+                }
+                A[p + (size_t)k * q] = 0.0;
+                A[q + (size_t)k * p] = 0.0;
+                for (int i = 0; i < k; ++i) { /* V <- V J */
+                    double vip = V[i + (size_t)k * p], viq = V[i + (size_t)k * q];
+                    V[i + (size_t)k * p] = c * vip - s * viq;
+                    V[i + (size_t)k * q] = s * vip + c * viq;
+                }
+            }
+    }
+    /* ascending, stable on ties (R11): insertion sort of indices */
+    int* idx = (int*)malloc((size_t)k * sizeof(int));
+    for (int i = 0; i < k; ++i) idx[i] = i;
+    for (int i = 1; i < k; ++i) {
+        int v = idx[i], j = i - 1;
+        while (j >= 0 && A[idx[j] + (size_t)k * idx[j]] > A[v + (size_t)k * v]) { idx[j + 1] = idx[j]; --j; }
+        idx[j + 1] = v;
+    }
+    for (int c = 0; c < k; ++c) {
+        int src = idx[c];
+        theta[c] = A[src + (size_t)k * src];
+        int imax = 0;
+        double vmax = -1.0;
+        for (int i = 0; i < k; ++i)
+            if (fabs(V[i + (size_t)k * src]) > vmax) { vmax = fabs(V[i + (size_t)k * src]); imax = i; }
+        double sg = V[imax + (size_t)k * src] < 0.0 ? -1.0 : 1.0; /* sign rule (R11) */
+        for (int i = 0; i < k; ++i) Y[i + (size_t)k * c] = sg * V[i + (size_t)k * src];
+    }
+    free(idx);
+    free(A);
+    free(V);
+    return rotated ? -1 : sweep;
+}
+
+/* ------------------------------------------------------------ solver ctx */
+typedef struct {
+    const orc_problem* P;
+    int64_t n;
+    int64_t a_mv, b_mv, prec;
+} ctx_t;
+
+static void applyA(ctx_t* c, const double* x, double* y) {
+    orc_spmv(c->n, c->P->a_rowptr, c->P->a_col, c->P->a_val, x, y);
+    c->a_mv++;
+}
+
+static void applyB(ctx_t* c, const double* x, double* y) {
+    if (c->P->b_rowptr) {
+        orc_spmv(c->n, c->P->b_rowptr, c->P->b_col, c->P->b_val, x, y);
+        c->b_mv++;
+    } else {
+        memcpy(y, x, (size_t)c->n * sizeof(double));
+    }
+}
+
+/* CGS2 in the B-inner product (R3; "orthonormal basis" P:184). */
+static int cgs2_ctx(ctx_t* c, int k, const double* V, double* w, double* Bw, double* h,
+                    double* beta, int* passes) {
+    int64_t n = c->n;
+    applyB(c, w, Bw);
+    double nin = sqrt(orc_dot(n, w, Bw));
+    double* coef = (double*)malloc((size_t)(k > 0 ? k : 1) * sizeof(double));
+    if (h) for (int j = 0; j < k; ++j) h[j] = 0.0;
+    double nprev = nin, nrm = nin;
+    int np = 0;
+    for (int pass = 1; pass <= 3; ++pass) {
+        /* classical GS: all coefficients from the same w, then the update */
+        for (int j = 0; j < k; ++j) coef[j] = orc_dot(n, V + (size_t)n * j, Bw);
+        for (int j = 0; j < k; ++j) axpy(n, -coef[j], V + (size_t)n * j, w);
+        if (h) for (int j = 0; j < k; ++j) h[j] += coef[j];
+        applyB(c, w, Bw);
+        nprev = nrm;
+        nrm = sqrt(orc_dot(n, w, Bw));
+        np = pass;
+        if (pass >= 2 && !(nrm < nprev / sqrt(2.0))) break; /* 3rd pass only if pass 2 dropped >1/sqrt2 */
+    }
+    free(coef);
+    *beta = nrm;
+    if (passes) *passes = np;
+    return (nrm < 1e-14 * nin || nin == 0.0) ? 1 : 0;
+}
+
+int orc_cgs2(int64_t n, int k, const double* V, double* w, const int64_t* b_rowptr,
+             const int64_t* b_col, const double* b_val, double* h, double* beta, int* passes) {
+    orc_problem P;
+    memset(&P, 0, sizeof(P));
+    P.n = n;
+    P.b_rowptr = b_rowptr; P.b_col = b_col; P.b_val = b_val;
+    ctx_t c = {&P, n, 0, 0, 0};
+    double* Bw = (double*)malloc((size_t)n * sizeof(double));
+    int r = cgs2_ctx(&c, k, V, w, Bw, h, beta, passes);
+    free(Bw);
+    return r;
+}
+
+/* random replacement for a dependent vector (R16): stream 2, draw counter d */
+static void draw_random(ctx_t* c, int64_t draw, double* w) {
+    int64_t n = c->n;
+#pragma omp parallel for schedule(static) if (n > 32768)
+    for (int64_t i = 0; i < n; ++i) w[i] = orc_u01(c->P->seed, 2, (uint64_t)draw * (uint64_t)n + (uint64_t)i);
+}
+
+/* r = A x - theta B x ; returns ||r||_2  (Alg. 1 step 12; R15) */
+static double residual(ctx_t* c, const double* x, double theta, double* r, double* tmp) {
+    applyA(c, x, r);
+    applyB(c, x, tmp);
+    axpy(c->n, -theta, tmp, r);
+    return sqrt(orc_dot(c->n, r, r));
+}
+
+/* Xn(:,0:ncol) = U(:,0:k) Y(0:k, 0:ncol)   ("x_i = U Y(:,i)") */
+static void rotate(int64_t n, int k, const double* U, const double* Y, int ldy, int ncol, double* Xn) {
+#pragma omp parallel for schedule(static) if (n > 32768)
+    for (int64_t i = 0; i < n; ++i)
+        for (int cc = 0; cc < ncol; ++cc) {
+            double s = 0.0;
+            for (int j = 0; j < k; ++j) s += U[i + (size_t)n * j] * Y[j + (size_t)ldy * cc];
+            Xn[i + (size_t)n * cc] = s;
+        }
+}
+
+int orc_trplk_solve(const orc_problem* P, double* evals, double* evecs, double* resid, orc_report* rep) {
+    const int64_t n = P->n;
+    const int p = P->p, q = P->q, l = P->l;
+    const int ph = P->restart_size > 0 ? P->restart_size : p; /* R5: p^ = p by default */
+    if (rep) { rep->status = 1; rep->cycles = 0; rep->log_len = 0; }
+    if (n < 1 || p < 1 || l < 0 || ph < p || q - ph - l < 1 || !(P->tol > 0.0) || ph + 1 > n ||
+        P->max_cycles < 1)
+        return 1; /* EINVAL */
+    const int m = q - ph - l; /* inner steps per cycle (R5) */
+
+    ctx_t c = {P, n, 0, 0, 0};
+    int64_t verify_mv = 0, inner_steps = 0, draws = 0;
+
+    double* M = (double*)malloc((size_t)n * sizeof(double));
+    orc_jacobi_diag(n, P->a_rowptr, P->a_col, P->a_val, P->b_rowptr, P->b_col, P->b_val, P->sigma,
+                    1e-8, M);
+    double tau = P->tol;
+    if (P->tol_mode == 1) tau = P->tol * orc_frobenius(P->a_rowptr[n], P->a_val); /* eq 5.1 */
+
+    double* U = (double*)calloc((size_t)n * q, sizeof(double));
+    double* Xn = (double*)malloc((size_t)n * ph * sizeof(double));
+    double* W = (double*)malloc((size_t)n * ph * sizeof(double));
+    double* Xp = (double*)malloc((size_t)n * (l > 0 ? l : 1) * sizeof(double));
+    double* XpN = (double*)malloc((size_t)n * (l > 0 ? l : 1) * sizeof(double));
+    double* w = (double*)malloc((size_t)n * sizeof(double));
+    double* Bw = (double*)malloc((size_t)n * sizeof(double));
+    double* z = (double*)malloc((size_t)n * sizeof(double));
+    double* s = (double*)malloc((size_t)n * sizeof(double));
+    double* r = (double*)malloc((size_t)n * sizeof(double));
+    double* u = (double*)malloc((size_t)n * sizeof(double));
+    double* T = (double*)calloc((size_t)q * q, sizeof(double));
+    double* Tk = (double*)malloc((size_t)q * q * sizeof(double));
+    double* Y = (double*)malloc((size_t)q * q * sizeof(double));
+    double* th = (double*)malloc((size_t)q * sizeof(double));
+    int status = 2, brk;
+    double beta;
+
+    /* ---- Alg. 1 steps 1-2: X = B-orthonormalised rand(n,p^), seed stream 0 (R13) */
+    for (int cc = 0; cc < ph; ++cc) {
+        double* x = U + (size_t)n * cc;
+#pragma omp parallel for schedule(static) if (n > 32768)
+        for (int64_t i = 0; i < n; ++i) x[i] = orc_u01(P->seed, 0, (uint64_t)cc * (uint64_t)n + (uint64_t)i);
+        int tries = 0;
+        while ((brk = cgs2_ctx(&c, cc, U, x, Bw, NULL, &beta, NULL)) && tries < 3) {
+            draw_random(&c, draws++, x);
+            ++tries;
+        }
+        if (brk) { status = 3; goto done_init_fail; }
+        scal_copy(n, 1.0 / beta, x, x);
+    }
+    for (int cc = 0; cc < ph; ++cc) applyA(&c, U + (size_t)n * cc, W + (size_t)n * cc);
+    for (int j = 0; j < ph; ++j)
+        for (int i = 0; i < ph; ++i) Tk[i + (size_t)ph * j] = orc_dot(n, U + (size_t)n * i, W + (size_t)n * j);
+    if (orc_sym_eig(ph, Tk, th, Y) < 0) { status = 3; goto done_init_fail; }
+    rotate(n, ph, U, Y, ph, ph, Xn);
+    memcpy(U, Xn, (size_t)n * ph * sizeof(double));
+    rotate(n, ph, W, Y, ph, ph, Xn); /* W <- W Y (AX of the rotated X) */
+    memcpy(W, Xn, (size_t)n * ph * sizeof(double));
+    memcpy(Xn, U, (size_t)n * ph * sizeof(double));
+    memset(T, 0, (size_t)q * q * sizeof(double));
+    for (int i = 0; i < ph; ++i) T[i + (size_t)q * i] = th[i];
+    int t = 1; /* target, 1-based */
+    double rho = th[0];
+    applyB(&c, U, s);
+    for (int64_t i = 0; i < n; ++i) r[i] = W[i] - rho * s[i];
+    for (int64_t i = 0; i < n; ++i) u[i] = M[i] * r[i];
+    c.prec++;
+    int nprev = 0;
+    int cyc;
+    int all_conv = 0;
+
+    for (cyc = 1; cyc <= P->max_cycles; ++cyc) {
+        if (rep && rep->dump_cycles > cyc - 1 && rep->dump_X) {
+            memcpy(rep->dump_X + (size_t)(cyc - 1) * n * ph, U, (size_t)n * ph * sizeof(double));
+            if (rep->dump_rho) rep->dump_rho[cyc - 1] = rho;
+            if (rep->dump_t) rep->dump_t[cyc - 1] = t;
+        }
+        /* ---- seed u1 = (I - X X^T B) M r_t, normalised (eq 3.2 u1 = C x_t, R4) */
+        memcpy(w, u, (size_t)n * sizeof(double));
+        {
+            int tries = 0;
+            while ((brk = cgs2_ctx(&c, ph, U, w, Bw, NULL, &beta, NULL)) && tries < 3) {
+                draw_random(&c, draws++, w);
+                ++tries;
+            }
+            if (brk) { status = 3; break; }
+        }
+        int k = ph;
+        scal_copy(n, 1.0 / beta, w, U + (size_t)n * k);
+        /* ---- inner projected Lanczos, eq 3.1, R1/R2 */
+        for (int j = 1; j <= m; ++j) {
+            double* g = U + (size_t)n * k;
+            k += 1; /* k = p^ + j */
+            applyA(&c, g, z);
+            ++inner_steps;
+            for (int i = 0; i < k; ++i) {
+                double v = orc_dot(n, U + (size_t)n * i, z);
+                T[i + (size_t)q * (k - 1)] = v;
+                T[(k - 1) + (size_t)q * i] = v;
+            }
+            if (j < m) {
+                applyB(&c, g, s);
+                for (int64_t i = 0; i < n; ++i) w[i] = M[i] * (z[i] - rho * s[i]); /* R1 */
+                c.prec++;
+                brk = cgs2_ctx(&c, k, U, w, Bw, NULL, &beta, NULL);
+                if (brk) break; /* R16: basis ends early */
+                scal_copy(n, 1.0 / beta, w, U + (size_t)n * k);
+            }
+        }
+        /* ---- +K: X^prev appended after G, explicitly orthogonalised, l matvecs (Alg.1 7-8) */
+        int appended = 0;
+        for (int cc = 0; cc < nprev; ++cc) {
+            memcpy(w, Xp + (size_t)n * cc, (size_t)n * sizeof(double));
+            brk = cgs2_ctx(&c, k, U, w, Bw, NULL, &beta, NULL);
+            if (brk) continue; /* dependent: drop (R16) */
+            double* xt = U + (size_t)n * k;
+            scal_copy(n, 1.0 / beta, w, xt);
+            k += 1;
+            applyA(&c, xt, z);
+            for (int i = 0; i < k; ++i) {
+                double v = orc_dot(n, U + (size_t)n * i, z);
+                T[i + (size_t)q * (k - 1)] = v;
+                T[(k - 1) + (size_t)q * i] = v;
+            }
+            ++appended;
+        }
+        /* ---- Alg. 1 step 10: X^prev <- X(:, t : min(t+l-1, p)) before the RR (R6) */
+        int last = t + l - 1 < p ? t + l - 1 : p;
+        int nnew = last - t + 1;
+        if (nnew < 0) nnew = 0;
+        for (int cc = 0; cc < nnew; ++cc)
+            memcpy(XpN + (size_t)n * cc, U + (size_t)n * (t - 1 + cc), (size_t)n * sizeof(double));
+        /* ---- debug bookkeeping checks: T vs U^T A U, U^T B U - I */
+        if (rep && P->debug && rep->log_cap >= cyc) {
+            double terr = 0.0, oerr = 0.0;
+            for (int jj = 0; jj < k; ++jj) {
+                orc_spmv(n, P->a_rowptr, P->a_col, P->a_val, U + (size_t)n * jj, z);
+                if (P->b_rowptr) orc_spmv(n, P->b_rowptr, P->b_col, P->b_val, U + (size_t)n * jj, s);
+                else memcpy(s, U + (size_t)n * jj, (size_t)n * sizeof(double));
+                for (int ii = 0; ii < k; ++ii) {
+                    double e1 = fabs(orc_dot(n, U + (size_t)n * ii, z) - T[ii + (size_t)q * jj]);
+                    double e2 = fabs(orc_dot(n, U + (size_t)n * ii, s) - (ii == jj ? 1.0 : 0.0));
+                    if (e1 > terr) terr = e1;
+                    if (e2 > oerr) oerr = e2;
+                }
+            }
+            if (rep->log_terr) rep->log_terr[cyc - 1] = terr;
+            if (rep->log_orth) rep->log_orth[cyc - 1] = oerr;
+        }
+        /* ---- Alg. 1 step 11: T = Y Theta Y^T, x_i = U Y(:,i) */
+        for (int jj = 0; jj < k; ++jj)
+            for (int ii = 0; ii < k; ++ii) Tk[ii + (size_t)k * jj] = T[ii + (size_t)q * jj];
+        if (orc_sym_eig(k, Tk, th, Y) < 0) { status = 3; break; }
+        rotate(n, k, U, Y, k, ph, Xn);
+        /* ---- Alg. 1 steps 12-14: soft lock (R7 literal IF) */
+        double res = residual(&c, Xn + (size_t)n * (t - 1), th[t - 1], r, s);
+        if (rep && rep->log_cap >= cyc) {
+            if (rep->log_t) rep->log_t[cyc - 1] = t;
+            if (rep->log_theta_t) rep->log_theta_t[cyc - 1] = th[t - 1];
+            if (rep->log_res) rep->log_res[cyc - 1] = res;
+            if (rep->log_k) rep->log_k[cyc - 1] = k;
+            if (rep->log_nprev) rep->log_nprev[cyc - 1] = appended;
+            if (rep->log_thetas) for (int i = 0; i < ph; ++i) rep->log_thetas[(size_t)(cyc - 1) * ph + i] = th[i];
+        }
+        while (res <= tau) {
+            t += 1;
+            if (nnew > 0) { /* remove x1^prev (step 13) */
+                for (int cc = 1; cc < nnew; ++cc)
+                    memcpy(XpN + (size_t)n * (cc - 1), XpN + (size_t)n * cc, (size_t)n * sizeof(double));
+                nnew -= 1;
+            }
+            if (t > p) { all_conv = 1; break; }
+            res = residual(&c, Xn + (size_t)n * (t - 1), th[t - 1], r, s);
+            if (P->lock_mode == 0) break;
+        }
+        /* ---- Alg. 1 step 15: restart.  X = U Y(:,1:p^), T = diag(Theta) (R10) */
+        memcpy(U, Xn, (size_t)n * ph * sizeof(double));
+        memset(T, 0, (size_t)q * q * sizeof(double));
+        for (int i = 0; i < ph; ++i) T[i + (size_t)q * i] = th[i];
+        if (nnew > 0) memcpy(Xp, XpN, (size_t)n * nnew * sizeof(double));
+        nprev = nnew;
+        if (rep && rep->log_cap >= cyc) {
+            if (rep->log_mv) rep->log_mv[cyc - 1] = c.a_mv;
+            rep->log_len = cyc;
+        }
+        if (all_conv) {
+            /* final verification of all p pairs (R9) */
+            int first_fail = -1;
+            for (int i = 0; i < p; ++i) {
+                double ri = residual(&c, Xn + (size_t)n * i, th[i], w, s);
+                verify_mv++;
+                resid[i] = ri;
+                if (ri > tau && first_fail < 0) {
+                    first_fail = i;
+                    memcpy(r, w, (size_t)n * sizeof(double));
+                }
+            }
+            if (first_fail < 0) { status = 0; break; }
+            t = first_fail + 1; /* resume (R9) */
+            all_conv = 0;
+        }
+        rho = th[t - 1];
+        for (int64_t i = 0; i < n; ++i) u[i] = M[i] * r[i];
+        c.prec++;
+    }
+    if (status != 0) {
+        /* NOT_CONVERGED (R19) / BREAKDOWN: report the current best with verified residuals */
+        for (int i = 0; i < p; ++i) {
+            resid[i] = residual(&c, Xn + (size_t)n * i, th[i], w, s);
+            verify_mv++;
+        }
+    }
+    for (int i = 0; i < p; ++i) evals[i] = th[i];
+    if (evecs) memcpy(evecs, Xn, (size_t)n * p * sizeof(double));
+    if (rep) rep->cycles = cyc > P->max_cycles ? P->max_cycles : cyc;
+    goto done;
+
+done_init_fail:
+    for (int i = 0; i < p; ++i) { evals[i] = NAN; resid[i] = NAN; }
+done:
+    if (rep) {
+        rep->status = status;
+        rep->a_matvecs = c.a_mv;
+        rep->b_matvecs = c.b_mv;
+        rep->precond_applies = c.prec;
+        rep->verify_matvecs = verify_mv;
+        rep->inner_steps = inner_steps;
+        rep->random_draws = draws;
+    }
+    free(M); free(U); free(Xn); free(W); free(Xp); free(XpN); free(w); free(Bw); free(z);
+    free(s); free(r); free(u); free(T); free(Tk); free(Y); free(th);
+    return status;
+}

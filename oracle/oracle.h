@@ -1,0 +1,90 @@
+/*
+ * TRPL+K CPU ORACLE -- TEST INFRASTRUCTURE ONLY.
+ *
+ * A plain, slow, obviously correct fp64 implementation of Algorithm 1
+ * (alg:trpl+k) with the readings R1-R20 of SURVEY.md 8(c.3)
+ * and DESIGN.md.  Only tests/, __graft_entry__.smoke() and bench.py's
+ * cpu_baseline / --impl reference leg may load it.  It shares no code with the
+ * CUDA path (paper_1711_10128_b200/csrc) and neither includes the other.
+ *
+ * Parity pins: see tests/test_oracle_*.py and DESIGN.md "Oracle pins".
+ */
+#ifndef TRPLK_ORACLE_H
+#define TRPLK_ORACLE_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Counter-based U[0,1) generator, reading R13 (independent implementation). */
+double orc_u01(uint64_t seed, uint64_t stream, uint64_t index);
+
+/* y = A x, CSR in row order (eq 3.1 first line). */
+void orc_spmv(int64_t n, const int64_t* rowptr, const int64_t* col, const double* val,
+              const double* x, double* y);
+/* x^T y with blocked fixed-order summation (4096-row blocks, pairwise across blocks). */
+double orc_dot(int64_t n, const double* x, const double* y);
+/* sqrt(sum of squares of all stored values) (eq 5.1 ||A||_F). */
+double orc_frobenius(int64_t nnz, const double* val);
+/* Jacobi preconditioner M_i = 1/max(|A_ii - sigma B_ii|, floor*max_j|A_jj|) (R12). */
+void orc_jacobi_diag(int64_t n, const int64_t* a_rowptr, const int64_t* a_col, const double* a_val,
+                     const int64_t* b_rowptr, const int64_t* b_col, const double* b_val,
+                     double sigma, double floor_rel, double* M);
+/* Small symmetric eig by cyclic-by-row Jacobi; T is k x k column-major (lda=k),
+ * symmetrised first.  theta ascending, stable on ties, Y column-major k x k with the
+ * largest-magnitude entry of each column positive (R10, R11). Returns sweeps used, <0 on failure. */
+int orc_sym_eig(int k, const double* T, double* theta, double* Y);
+
+/* CGS2 in the B-inner product (R3): w <- w - V V^T B w twice (+1 pass if the second pass
+ * drops the norm by more than 1/sqrt2).  V is n x k column-major (ld = n).  B may be NULL.
+ * Returns the final B-norm in *beta (w is NOT normalised), the coefficients of the passes
+ * summed into h (k, may be NULL) and 1 on breakdown (final norm < 1e-14 * input norm). */
+int orc_cgs2(int64_t n, int k, const double* V, double* w, const int64_t* b_rowptr,
+             const int64_t* b_col, const double* b_val, double* h, double* beta, int* passes);
+
+typedef struct {
+    int64_t n;
+    const int64_t* a_rowptr; const int64_t* a_col; const double* a_val;
+    const int64_t* b_rowptr; const int64_t* b_col; const double* b_val;  /* all NULL: B = I */
+    double sigma;
+    int p, q, l;            /* wanted pairs, max basis, k_plus */
+    double tol;
+    int tol_mode;           /* 0 ABS: ||r|| <= tol; 1 FROB: ||r|| <= tol*||A||_F (eq 5.1) */
+    uint64_t seed;
+    int max_cycles;
+    int restart_size;       /* p^ (>= p); 0 -> p */
+    int lock_mode;          /* 0 IF (Alg. 1 step 12, R7), 1 WHILE */
+    int debug;              /* 1: log ||T - U^T A U||_max and ||U^T B U - I||_max per cycle */
+} orc_problem;
+
+typedef struct {
+    int status;             /* 0 OK, 2 NOT_CONVERGED, 3 BREAKDOWN, 1 EINVAL */
+    int cycles;
+    int64_t a_matvecs, b_matvecs, precond_applies, verify_matvecs, inner_steps, random_draws;
+    /* per-cycle log; arrays of capacity log_cap (caller-owned, may be NULL) */
+    int log_cap, log_len;
+    int* log_t;             /* target (1-based) at the RR of the cycle */
+    int64_t* log_mv;        /* cumulative A-matvecs at the end of the cycle */
+    double* log_theta_t;    /* theta_t at the RR */
+    double* log_res;        /* ||r_t|| at the RR */
+    int* log_k;             /* basis width at the RR */
+    int* log_nprev;         /* X^prev columns appended this cycle */
+    double* log_thetas;     /* log_cap x p^ Ritz values theta_1..p^ */
+    double* log_terr;       /* debug: max |T - U^T A U| */
+    double* log_orth;       /* debug: max |U^T B U - I| */
+    /* optional dumps for tiny problems: X at the start of cycle c (c < dump_cycles) */
+    int dump_cycles;
+    double* dump_X;         /* dump_cycles x (n x p^) */
+    double* dump_rho;       /* dump_cycles */
+    int* dump_t;            /* dump_cycles */
+} orc_report;
+
+/* Algorithm 1 in full.  evals[p], resid[p] ascending; evecs n x p column-major. */
+int orc_trplk_solve(const orc_problem* prob, double* evals, double* evecs, double* resid,
+                    orc_report* rep);
+
+#ifdef __cplusplus
+}
+#endif
+#endif
