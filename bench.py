@@ -1,0 +1,314 @@
+#!/usr/bin/env python
+"""TRPL+K bench (BASELINE.json metric: matvecs/s & time to p eigenpairs, fp64, HBM GB/s vs peak).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl ours|reference]
+
+A "step" is one full trplk_solve (time to the p smallest eigenpairs) of the
+BASELINE config (default configs[1] = C2, 64^3 7-pt Laplacian + diag(d)),
+inputs resident in HBM (the context is created before the timed region).  The
+L2 (126 MB) is flushed between timed steps by writing a 256 MiB buffer.
+`value` = A-matvecs of the solve / solve time (whole job; max over ranks).
+`e2e` = the same metric through the public API with HOST CSR buffers: create
+(H2D of the CSR + SELL conversion) + solve + D2H of eigenvectors + destroy.
+`roofline` = the inner-step kernel with the largest share of the step, live
+CUDA-event timing over the timed steps (trplk_profile), algorithmic bytes of
+DESIGN.md, against MEASURED_PEAKS.json hbm_gbs.  `cpu_baseline` = the oracle
+(oracle/, plain C + OpenMP) on the host cores, rank 0 at N=1 only.
+
+--impl reference: this tier has no reference implementation; the reference
+arm is the oracle timed as it stands on the host cores (bounded sample).
+For N>1 run under torchrun: one rank per GPU, z-slab row partition, NCCL.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "matvecs/s & time to p eigenpairs (fp64), HBM GB/s vs peak, at 1/2/4/8 B200"
+UNIT = "matvecs/s"
+PROFILES = os.path.join(ROOT, "profiles")
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C2", choices=["C1", "C2", "C3", "C4", "C5"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=20.0, help="oracle sample budget")
+    return ap.parse_args()
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        d = json.load(open(path))
+        return float(d.get("hbm_gbs", 6650.0)), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(index), f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return None
+        self.p.terminate()
+        try:
+            self.p.wait(timeout=5)
+        except Exception:
+            self.p.kill()
+        self.f.flush()
+        rows = []
+        for line in open(self.f.name):
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 7:
+                rows.append(parts)
+        os.unlink(self.f.name)
+        if not rows:
+            return None
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = max(float(r[1]) for r in rows if r[1].replace(".", "").isdigit())
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if "Active" in r[3 + i]})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": reasons,
+                "samples": len(rows)}
+
+
+def plane_of(P):
+    return 1 if P.grid["dim"] == 1 else P.grid["N"] ** 2
+
+
+def cpu_baseline(name, budget_s):
+    """Oracle as it stands on the host cores: the full solve if it fits the budget, else the first
+    cycles (bounded sample)."""
+    import oracle
+    from paper_1711_10128_b200 import inputs
+    P = inputs.make(name)
+    cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
+    # probe: 2 cycles, then scale the cycle count to the budget
+    t0 = time.perf_counter()
+    r = oracle.solve(P.A, P.B, P.p, P.q, P.l, P.tol, P.sigma, max_cycles=2, want_vectors=False)
+    dt = time.perf_counter() - t0
+    per_cycle = max(dt / 2, 1e-6)
+    cyc = max(2, int(budget_s / per_cycle))
+    t0 = time.perf_counter()
+    r = oracle.solve(P.A, P.B, P.p, P.q, P.l, P.tol, P.sigma, max_cycles=min(cyc, 5000), want_vectors=False)
+    dt = time.perf_counter() - t0
+    full = r["status"] == "OK"
+    sample = (f"full oracle solve of {name} ({r['cycles']} cycles, {r['a_matvecs']} A-matvecs)" if full else
+              f"first {r['cycles']} cycles of the {name} oracle solve ({r['a_matvecs']} A-matvecs incl. "
+              f"{P.p} verification)")
+    return {"value": r["a_matvecs"] / dt, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample,
+            "seconds": dt}, r
+
+
+def run_reference(args):
+    """Reference arm = the oracle (this tier has no reference implementation)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    vals, times = [], []
+    from paper_1711_10128_b200 import inputs
+    P = inputs.make(args.config)
+    budget = max(3.0, min(args.cpu_seconds, 150.0 / max(1, args.steps + args.warmup)))
+    cb = None
+    for i in range(args.warmup + args.steps):
+        cb, r = cpu_baseline(args.config, budget)
+        if i >= args.warmup:
+            vals.append(cb["value"])
+            times.append(cb["seconds"])
+    v = statistics.mean(vals)
+    out = {"metric": METRIC, "value": v, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.mean(times),
+           "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic (seeded generator, BASELINE configs)",
+           "config": {"workload": f"{args.config}: {P.desc}; p={P.p}, max_basis={P.q}, k_plus={P.l}, tol={P.tol}",
+                      "l2": "host run"},
+           "cpu_baseline": {**{k: cb[k] for k in ("kind", "cores", "sample")}, "value": v, "unit": UNIT},
+           "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out))
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    group = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        group = dist.group.WORLD
+    from paper_1711_10128_b200 import build
+    build.build()
+    from paper_1711_10128_b200 import inputs, trplk
+
+    dim, N = inputs.CONFIGS[args.config][0], inputs.CONFIGS[args.config][1]
+    n = N if dim == 1 else N ** 3
+    plane = 1 if dim == 1 else N * N
+    rb, re = inputs.slab_rows(n, world, rank, plane)
+    P = inputs.make(args.config, row_begin=rb, row_end=re)
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    ctx = trplk.trplk_create(P.A, P.B, P.sigma, n_global=n, row_begin=rb, row_end=re, group=group)
+    evecs = torch.empty((P.p, ctx.n_local), dtype=torch.float64, device="cuda")
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+
+    def solve(**kw):
+        return trplk.trplk_solve(ctx, P.p, P.q, P.l, P.tol, evecs_out=evecs, **kw)
+
+    for _ in range(args.warmup):
+        ev, _, rs, st = solve()
+    assert st["status"] == "OK", st
+    trplk.trplk_profile(ctx, True)
+    clocks = Clocks(local)
+    times, stats = [], []
+    for _ in range(args.steps):
+        flush.fill_(1.0)
+        barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        ev, _, rs, st = solve()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        times.append(e0.elapsed_time(e1))
+        stats.append(st)
+    ck = clocks.stop()
+    prof = trplk.trplk_profile_read(ctx)
+    trplk.trplk_profile(ctx, False)
+    t_sum = torch.tensor([sum(times)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t_sum, op=dist.ReduceOp.MAX)
+    ms_per_step = t_sum.item() / args.steps
+    mv = stats[-1]["a_matvecs"]
+    assert all(s["a_matvecs"] == mv for s in stats)
+    value = mv / (ms_per_step / 1e3)
+
+    # roofline: inner-step kernel group with the largest share (live CUDA events, per launch)
+    names = ["K1 k_sdots (SpMV+Jacobi+T-col/h1 dots)", "K2 k_upd DOTS (CGS pass 2)", "K3 k_upd FINAL (+fix)"]
+    peak, peak_src = peaks()
+    cnt = max(prof["count"], 1)
+    per_ms = prof["ms"] / cnt
+    per_b = prof["bytes"] / cnt
+    kd = int(np.argmax(per_ms))
+    achieved = per_b[kd] / (per_ms[kd] * 1e-3) / 1e9
+    step_gbs = per_b.sum() / (per_ms.sum() * 1e-3) / 1e9
+    traffic = None
+    tfile = os.path.join(PROFILES, f"traffic_{args.config}.json")
+    if os.path.exists(tfile):
+        traffic = json.load(open(tfile)).get(str(kd))
+    roof = {"bound": "hbm", "kernel": names[kd], "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+            "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_src,
+            "bytes_per_launch": per_b[kd], "ms_per_launch": per_ms[kd],
+            "inner_step": {"achieved": round(step_gbs, 1), "frac": round(step_gbs / peak, 4),
+                           "bytes": per_b.sum(), "ms": per_ms.sum(),
+                           "share_ms": [round(x / per_ms.sum(), 3) for x in per_ms]},
+            "solve_model_gbs": round(stats[-1]["model_bytes"] / (ms_per_step * 1e-3) / 1e9, 1),
+            "samples": prof["count"]}
+
+    # e2e through the public API with host buffers (pinned), every step
+    e2e = None
+    if not args.no_e2e:
+        pin = []
+        for M in (P.A, P.B):
+            if M is None:
+                continue
+            pin += [torch.from_numpy(M.rowptr).pin_memory(), torch.from_numpy(M.col).pin_memory(),
+                    torch.from_numpy(M.val).pin_memory()]
+        host_evecs = torch.empty((P.p, ctx.n_local), dtype=torch.float64).pin_memory()
+
+        class _HostCSR:
+            def __init__(self, rp, c, v, n_):
+                self.rowptr, self.col, self.val, self.n, self.row_begin = rp.numpy(), c.numpy(), v.numpy(), n_, rb
+
+        HA = _HostCSR(*pin[0:3], n)
+        HB = _HostCSR(*pin[3:6], n) if P.B is not None else None
+        h2d = sum(t.numel() * t.element_size() for t in pin)
+        d2h = host_evecs.numel() * 8 + 2 * P.p * 8
+        et = []
+        for _ in range(max(1, min(args.steps, 3))):
+            flush.fill_(1.0)
+            barrier()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            c2 = trplk.trplk_create(HA, HB, P.sigma, n_global=n, row_begin=rb, row_end=re, group=group)
+            ev2, _, rs2, st2 = trplk.trplk_solve(c2, P.p, P.q, P.l, P.tol, evecs_out=host_evecs)
+            c2.close()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            et.append(e0.elapsed_time(e1))
+        te = torch.tensor([statistics.mean(et)], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": st2["a_matvecs"] / (te.item() / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h, "ms_per_step": te.item()}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cb, _ = cpu_baseline(args.config, args.cpu_seconds)
+        cpu = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+
+    if rank == 0:
+        out = {"metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+               "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
+               "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+               "data": "synthetic (seeded generator, BASELINE configs; paper matrices unavailable)",
+               "config": {"workload": f"{args.config}: {P.desc}; p={P.p}, max_basis={P.q}, k_plus={P.l}, "
+                                      f"tol={P.tol}, Jacobi, seed 12",
+                          "n": n, "step": "one full trplk_solve (time to p eigenpairs)",
+                          "a_matvecs_per_solve": mv, "cycles": stats[-1]["cycles"],
+                          "time_to_p_eigenpairs_ms": round(ms_per_step, 4),
+                          "l2": "flushed (256 MiB write) between timed steps",
+                          "parallelism": f"z-slab row partition x{world}"},
+               "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+               "gpu_launches": int(sum(s["kernel_launches"] for s in stats)), "clocks": ck,
+               "eigenvalues": [float(x) for x in ev], "max_residual": float(np.max(rs))}
+        print(json.dumps(out))
+    ctx.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,67 @@
+/*
+ * trplk_kernels.h -- kernel-level entry points of libtrplk.so (parity tests,
+ * diagnostics).  Each call runs exactly the device kernels trplk_solve uses for
+ * that step, on caller-provided device buffers, on the context's stream, and
+ * synchronises before returning host outputs.  Vectors that are multiplied by A
+ * or B (the `x`/`g` arguments) must hold n_local + n_ghost entries: the ghost
+ * tail (global columns owned by other ranks, ascending global id) is filled by
+ * the caller.  U blocks are column-major with leading dimension ldu >= n_local.
+ * Errors: EINVAL on bad sizes (k > TRPLK_MAX_BASIS, ld too small), ECUDA.
+ */
+#ifndef TRPLK_KERNELS_H
+#define TRPLK_KERNELS_H
+
+#include "trplk.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* y = Op x on the local rows, Op = A (which=0) or B (which=1).  S1, eq 3.1 line 1. */
+trplk_status trplk_k_spmv(trplk_ctx* ctx, int which, const double* x, double* y);
+
+/* Fused inner-step kernel K1 (eq 3.1 + preconditioner, reading R1):
+ *   z = A g,  s = B g,  w = M (z - rho s)   -> w (device, n_local)
+ *   tcol[0:k] = U^T z                         (T(1:k, k) of eq 3.1)
+ *   h1[0:k]   = U^T (B w),  wnorm2 = w^T B w  (first CGS2 pass coefficients, R3)
+ * For B != I the B-products come from the second kernel the solver runs (B-SpMV + dots). */
+trplk_status trplk_k_step1(trplk_ctx* ctx, const double* U, int64_t ldu, int k, const double* g,
+                           double rho, double* w, double* tcol, double* h1, double* wnorm2);
+
+/* CGS2 in the B-inner product of w against U(:,0:k) (reading R3), device path:
+ * out = (w - U h)/beta with h the summed pass coefficients (host, k entries), beta the
+ * final B-norm, breakdown = final norm < 1e-14 ||w||_B, passes = 2 or 3.
+ * On breakdown out is left unnormalised. */
+trplk_status trplk_k_cgs2(trplk_ctx* ctx, const double* U, int64_t ldu, int k, const double* w,
+                          double* out, double* h, double* beta, int* breakdown, int* passes);
+
+/* X(:,0:ncol) = U(:,0:k) Y(0:k,0:ncol) with the fp64 DMMA kernel (Alg.1 steps 11/15,
+ * PAPER.md:193,198).  Y host, column-major k x ncol (ncol <= 24). */
+trplk_status trplk_k_rotate(trplk_ctx* ctx, const double* U, int64_t ldu, int k, const double* Y,
+                            int ncol, double* X, int64_t ldx);
+
+/* One-CTA parallel-ordered cyclic Jacobi of sym(T), k x k column-major host arrays
+ * (Alg.1 step 11; R10/R11 ordering and sign rule). */
+trplk_status trplk_k_sym_eig(trplk_ctx* ctx, int k, const double* T, double* theta, double* Y);
+
+/* r = A x - theta B x (Alg.1 step 12), u = M r (step 15 seed), rnorm2 = ||r||^2. */
+trplk_status trplk_k_residual(trplk_ctx* ctx, const double* x, double theta, double* r, double* u,
+                              double* rnorm2);
+
+/* x[i] = U01(seed, stream, col*n_global + global_row(i)) for the local rows (reading R13). */
+trplk_status trplk_k_random(trplk_ctx* ctx, uint64_t seed, uint64_t stream, uint64_t col, double* x);
+
+/* Live profile of the inner step (measurement): while enabled, every
+ * outer cycle records CUDA events around the three kernel groups of its middle inner step
+ *   [0] K1  fused SpMV + preconditioner + T-column/h1 dots
+ *   [1] K2  CGS pass 2 (update + dots; for B != I the B-SpMV dot passes and the update)
+ *   [2] K3  final update + normalisation (+ gated third-pass fix-up)
+ * and accumulates their device milliseconds and algorithmic bytes (byte model of DESIGN.md).
+ * enable=1 clears the accumulators.  read: ms[3], bytes[3] sums over `count` cycles. */
+trplk_status trplk_profile(trplk_ctx* ctx, int enable);
+trplk_status trplk_profile_read(const trplk_ctx* ctx, double* ms, double* bytes, int64_t* count);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

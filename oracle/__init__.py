@@ -81,6 +81,8 @@ def lib():
         L.orc_sym_eig.argtypes = [ctypes.c_int, _P, _P, _P]
         L.orc_cgs2.restype = ctypes.c_int
         L.orc_cgs2.argtypes = [_I64, ctypes.c_int, _P, _P, _P, _P, _P, _P, _P, _P]
+        L.orc_rotate.restype = None
+        L.orc_rotate.argtypes = [_I64, ctypes.c_int, _P, _P, ctypes.c_int, ctypes.c_int, _P]
         L.orc_trplk_solve.restype = ctypes.c_int
         L.orc_trplk_solve.argtypes = [ctypes.POINTER(_Problem), _P, _P, _P, ctypes.POINTER(_Report)]
         _lib = L
@@ -147,6 +149,17 @@ def sym_eig(T):
     if sweeps < 0:
         raise RuntimeError("oracle Jacobi did not converge")
     return th, Y
+
+
+def rotate(U, Y):
+    """X = U Y (n x k times k x ncol), column-major fp64."""
+    U = np.asfortranarray(U, np.float64)
+    Y = np.asfortranarray(Y, np.float64)
+    n, k = U.shape
+    ncol = Y.shape[1]
+    X = np.zeros((n, ncol), order="F")
+    lib().orc_rotate(n, k, _ptr(U), _ptr(Y), Y.shape[0], ncol, _ptr(X))
+    return X
 
 
 def cgs2(V, w, B=None):

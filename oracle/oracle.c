@@ -251,7 +251,7 @@ static double residual(ctx_t* c, const double* x, double theta, double* r, doubl
 }
 
 /* Xn(:,0:ncol) = U(:,0:k) Y(0:k, 0:ncol)   ("x_i = U Y(:,i)") */
-static void rotate(int64_t n, int k, const double* U, const double* Y, int ldy, int ncol, double* Xn) {
+void orc_rotate(int64_t n, int k, const double* U, const double* Y, int ldy, int ncol, double* Xn) {
 #pragma omp parallel for schedule(static) if (n > 32768)
     for (int64_t i = 0; i < n; ++i)
         for (int cc = 0; cc < ncol; ++cc) {
@@ -315,9 +315,9 @@ int orc_trplk_solve(const orc_problem* P, double* evals, double* evecs, double* 
     for (int j = 0; j < ph; ++j)
         for (int i = 0; i < ph; ++i) Tk[i + (size_t)ph * j] = orc_dot(n, U + (size_t)n * i, W + (size_t)n * j);
     if (orc_sym_eig(ph, Tk, th, Y) < 0) { status = 3; goto done_init_fail; }
-    rotate(n, ph, U, Y, ph, ph, Xn);
+    orc_rotate(n, ph, U, Y, ph, ph, Xn);
     memcpy(U, Xn, (size_t)n * ph * sizeof(double));
-    rotate(n, ph, W, Y, ph, ph, Xn); /* W <- W Y (AX of the rotated X) */
+    orc_rotate(n, ph, W, Y, ph, ph, Xn); /* W <- W Y (AX of the rotated X) */
     memcpy(W, Xn, (size_t)n * ph * sizeof(double));
     memcpy(Xn, U, (size_t)n * ph * sizeof(double));
     memset(T, 0, (size_t)q * q * sizeof(double));
@@ -414,7 +414,7 @@ int orc_trplk_solve(const orc_problem* P, double* evals, double* evecs, double* 
         for (int jj = 0; jj < k; ++jj)
             for (int ii = 0; ii < k; ++ii) Tk[ii + (size_t)k * jj] = T[ii + (size_t)q * jj];
         if (orc_sym_eig(k, Tk, th, Y) < 0) { status = 3; break; }
-        rotate(n, k, U, Y, k, ph, Xn);
+        orc_rotate(n, k, U, Y, k, ph, Xn);
         /* ---- Alg. 1 steps 12-14: soft lock (R7 literal IF) */
         double res = residual(&c, Xn + (size_t)n * (t - 1), th[t - 1], r, s);
         if (rep && rep->log_cap >= cyc) {

@@ -43,6 +43,9 @@ int orc_sym_eig(int k, const double* T, double* theta, double* Y);
 int orc_cgs2(int64_t n, int k, const double* V, double* w, const int64_t* b_rowptr,
              const int64_t* b_col, const double* b_val, double* h, double* beta, int* passes);
 
+/* Xn(:,0:ncol) = U(:,0:k) Y(0:k,0:ncol), plain triple loop. Column-major, ld n / ldy. */
+void orc_rotate(int64_t n, int k, const double* U, const double* Y, int ldy, int ncol, double* Xn);
+
 typedef struct {
     int64_t n;
     const int64_t* a_rowptr; const int64_t* a_col; const double* a_val;

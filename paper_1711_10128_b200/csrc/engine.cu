@@ -1,0 +1,1555 @@
+// TRPL+K engine: context creation (CSR -> SELL-32, halo plan, NCCL), Algorithm 1 driven on the
+// device with one CUDA graph per outer cycle, and the C ABI of include/trplk.h /
+// include/trplk_kernels.h.
+//
+// Host control flow mirrors Algorithm 1 with readings R1-R20;
+// all vector work runs in the kernels of kernels.cu.  One host synchronisation per cycle
+// (the soft-locking decision of steps 12-14 needs ||r_t||).
+#include <nccl.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "trplk.h"
+#include "trplk_internal.cuh"
+#include "trplk_kernels.h"
+
+using namespace trplk;
+
+namespace {
+
+struct LogRec {
+    int t;
+    int64_t mv;
+    double theta_t, res;
+    int k, nprev;
+    std::vector<double> thetas;
+};
+
+struct GraphRec {
+    cudaGraphExec_t exec;
+    double bytes;      // algorithmic bytes of one replay
+    int64_t launches;  // kernels of one replay
+};
+
+struct Sizes {  // per-solve parameters that shape the captured graphs
+    int p, q, l, ph, m;
+    bool operator<(const Sizes& o) const {
+        return std::tie(p, q, l, ph, m) < std::tie(o.p, o.q, o.l, o.ph, o.m);
+    }
+    bool operator==(const Sizes& o) const { return !(*this < o) && !(o < *this); }
+};
+
+}  // namespace
+
+struct trplk_ctx {
+    int64_t n_global = 0, n_loc = 0, row_begin = 0, row_end = 0, n_ghost = 0, ld = 0;
+    int rank = 0, nranks = 1;
+    cudaStream_t stream = nullptr;       // internal non-blocking work stream (capturable)
+    cudaStream_t user_stream = nullptr;  // the caller's stream; ordered with `stream` by events
+    cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+    trplk_allocator alloc{};
+    bool has_alloc = false;
+    std::vector<std::pair<void*, size_t>> allocs;
+    bool hasB = false;
+    double sigma = 0.0, mfloor = 0.0, normF = 0.0, amax = 0.0;
+    Sell A, B;
+    int64_t sellA_bytes = 0, sellB_bytes = 0, nnzA = 0, nnzB = 0;
+    // halo plan (nranks > 1): per peer, recv range in the ghost tail and send rows
+    std::vector<int> peers;
+    std::vector<int64_t> recv_off, recv_cnt, send_cnt, send_start;
+    std::vector<int*> send_idx;
+    double* sendbuf = nullptr;
+    ncclComm_t comm = nullptr;
+    // solve buffers
+    int q_alloc = 0, ph_alloc = 0;
+    double* U[2] = {nullptr, nullptr};
+    double *w = nullptr, *w1 = nullptr, *w2 = nullptr, *u = nullptr, *u2 = nullptr, *xk = nullptr;
+    double *T = nullptr, *Yg = nullptr, *part = nullptr, *red_local = nullptr, *red_all = nullptr;
+    double* Wtmp = nullptr;
+    unsigned* counter = nullptr;
+    Ctl* ctl = nullptr;
+    Ctl* ctl_h = nullptr;
+    int maxcta = 0;
+    std::string err;
+    std::vector<LogRec> log;
+    int log_ph = 0;
+    Sizes gsizes{0, 0, 0, 0, 0};
+    std::map<uint64_t, GraphRec> graphs;
+    // counters of the running solve
+    int64_t a_mv = 0, b_mv = 0, prec = 0, inner = 0, verify = 0, draws = 0;
+    double model_bytes = 0.0;
+    int64_t launches = 0;
+    // live profile of the middle inner step (trplk_profile)
+    bool prof_on = false;
+    cudaEvent_t pev[4] = {nullptr, nullptr, nullptr, nullptr};
+    double prof_ms[3] = {0, 0, 0}, prof_bytes[3] = {0, 0, 0};
+    int64_t prof_count = 0;
+    int prof_k = 0;
+};
+
+namespace {
+
+#define CK(call)                                                                       \
+    do {                                                                               \
+        cudaError_t e_ = (call);                                                       \
+        if (e_ != cudaSuccess) {                                                       \
+            ctx->err = std::string(#call) + ": " + cudaGetErrorString(e_);             \
+            return TRPLK_ECUDA;                                                        \
+        }                                                                              \
+    } while (0)
+
+#define NK(call)                                                                       \
+    do {                                                                               \
+        ncclResult_t r_ = (call);                                                      \
+        if (r_ != ncclSuccess) {                                                       \
+            ctx->err = std::string(#call) + ": " + ncclGetErrorString(r_);             \
+            return TRPLK_ENCCL;                                                        \
+        }                                                                              \
+    } while (0)
+
+#define ST(call)                                                                       \
+    do {                                                                               \
+        trplk_status s_ = (call);                                                      \
+        if (s_ != TRPLK_OK) return s_;                                                 \
+    } while (0)
+
+// Order the internal work stream after / before the caller's stream.
+void enter_stream(trplk_ctx* ctx) {
+    if (ctx->user_stream != ctx->stream) {
+        cudaEventRecord(ctx->ev_in, ctx->user_stream);
+        cudaStreamWaitEvent(ctx->stream, ctx->ev_in, 0);
+    }
+}
+
+void leave_stream(trplk_ctx* ctx) {
+    if (ctx->user_stream != ctx->stream) {
+        cudaEventRecord(ctx->ev_out, ctx->stream);
+        cudaStreamWaitEvent(ctx->user_stream, ctx->ev_out, 0);
+    }
+}
+
+trplk_status dev_alloc(trplk_ctx* ctx, void** p, size_t bytes) {
+    if (bytes == 0) bytes = 8;
+    bytes = (bytes + 255) & ~(size_t)255;
+    void* q = nullptr;
+    if (ctx->has_alloc) {
+        q = ctx->alloc.alloc(bytes, ctx->alloc.user);
+        if (!q) {
+            ctx->err = "allocator returned NULL for " + std::to_string(bytes) + " bytes";
+            return TRPLK_ENOMEM;
+        }
+    } else {
+        cudaError_t e = cudaMalloc(&q, bytes);
+        if (e != cudaSuccess) {
+            ctx->err = std::string("cudaMalloc: ") + cudaGetErrorString(e);
+            return e == cudaErrorMemoryAllocation ? TRPLK_ENOMEM : TRPLK_ECUDA;
+        }
+    }
+    ctx->allocs.push_back({q, bytes});
+    *p = q;
+    return TRPLK_OK;
+}
+
+void dev_free(trplk_ctx* ctx, void* p) {
+    if (!p) return;
+    for (size_t i = 0; i < ctx->allocs.size(); ++i)
+        if (ctx->allocs[i].first == p) {
+            if (ctx->has_alloc) ctx->alloc.free(p, ctx->alloc.user);
+            else cudaFree(p);
+            ctx->allocs.erase(ctx->allocs.begin() + (long)i);
+            return;
+        }
+}
+
+template <typename T>
+trplk_status dalloc(trplk_ctx* ctx, T** p, size_t count) {
+    return dev_alloc(ctx, reinterpret_cast<void**>(p), count * sizeof(T));
+}
+
+// ----------------------------------------------------------------- CSR -> SELL-32
+struct HostSell {
+    std::vector<int64_t> sptr;
+    std::vector<int> col;
+    std::vector<double> val;
+};
+
+// Local column id of global column c (owned rows first, then the sorted ghost list).
+inline int64_t local_col(int64_t c, int64_t rb, int64_t re, int64_t n_loc, const std::vector<int64_t>& ghosts) {
+    if (c >= rb && c < re) return c - rb;
+    auto it = std::lower_bound(ghosts.begin(), ghosts.end(), c);
+    return n_loc + (int64_t)(it - ghosts.begin());
+}
+
+trplk_status build_sell(trplk_ctx* ctx, const int64_t* rp, const int64_t* ci, const double* va,
+                        const std::vector<int64_t>& ghosts, HostSell& hs) {
+    const int64_t n = ctx->n_loc, rb = ctx->row_begin, re = ctx->row_end;
+    const int64_t ns = (n + 31) / 32;
+    const int64_t base = rp[0];
+    hs.sptr.assign(ns + 1, 0);
+    std::vector<int> width(ns, 0);
+#pragma omp parallel for schedule(static)
+    for (int64_t s = 0; s < ns; ++s) {
+        int w = 1;
+        for (int64_t r = s * 32; r < std::min(n, s * 32 + 32); ++r) {
+            int64_t cnt = rp[r + 1] - rp[r];
+            bool has_diag = false;
+            for (int64_t p = rp[r] - base; p < rp[r + 1] - base; ++p)
+                if (ci[p] == rb + r) has_diag = true;
+            int wr = (int)(has_diag ? cnt : cnt + 1);
+            w = std::max(w, wr);
+        }
+        width[s] = w;
+    }
+    for (int64_t s = 0; s < ns; ++s) hs.sptr[s + 1] = hs.sptr[s] + 32 * (int64_t)width[s];
+    const int64_t tot = hs.sptr[ns];
+    hs.col.assign(tot, 0);
+    hs.val.assign(tot, 0.0);
+#pragma omp parallel for schedule(static)
+    for (int64_t s = 0; s < ns; ++s) {
+        for (int lane = 0; lane < 32; ++lane) {
+            const int64_t r = s * 32 + lane;
+            const int64_t b = hs.sptr[s] + lane;
+            if (r >= n) {
+                for (int j = 0; j < width[s]; ++j) hs.col[b + 32 * j] = 0;
+                continue;
+            }
+            hs.col[b] = (int)r;  // slot 0: diagonal (explicit zero if not stored)
+            hs.val[b] = 0.0;
+            int j = 1;
+            for (int64_t p = rp[r] - base; p < rp[r + 1] - base; ++p) {
+                if (ci[p] == rb + r) {
+                    hs.val[b] += va[p];
+                } else {
+                    hs.col[b + 32 * j] = (int)local_col(ci[p], rb, re, n, ghosts);
+                    hs.val[b + 32 * j] = va[p];
+                    ++j;
+                }
+            }
+            for (; j < width[s]; ++j) hs.col[b + 32 * j] = (int)r;  // padding: val 0
+        }
+    }
+    return TRPLK_OK;
+}
+
+trplk_status upload_sell(trplk_ctx* ctx, const HostSell& hs, Sell& S, int64_t& bytes) {
+    int64_t* sptr;
+    int* col;
+    double* val;
+    ST(dalloc(ctx, &sptr, hs.sptr.size()));
+    ST(dalloc(ctx, &col, hs.col.size()));
+    ST(dalloc(ctx, &val, hs.val.size()));
+    CK(cudaMemcpyAsync(sptr, hs.sptr.data(), hs.sptr.size() * 8, cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(col, hs.col.data(), hs.col.size() * 4, cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(val, hs.val.data(), hs.val.size() * 8, cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    S.nrows = ctx->n_loc;
+    S.nslices = (int64_t)hs.sptr.size() - 1;
+    S.sptr = sptr;
+    S.col = col;
+    S.val = val;
+    bytes = (int64_t)(hs.sptr.size() * 8 + hs.col.size() * 4 + hs.val.size() * 8);
+    return TRPLK_OK;
+}
+
+trplk_status validate_csr(trplk_ctx* ctx, const char* name, const int64_t* rp, const int64_t* ci) {
+    if (!rp || !ci) {
+        ctx->err = std::string(name) + ": NULL CSR array";
+        return TRPLK_EINVAL;
+    }
+    const int64_t base = rp[0];
+    for (int64_t r = 0; r < ctx->n_loc; ++r) {
+        if (rp[r + 1] < rp[r]) {
+            ctx->err = std::string(name) + ": row pointer decreases at row " + std::to_string(r);
+            return TRPLK_EINVAL;
+        }
+        for (int64_t p = rp[r] - base; p < rp[r + 1] - base; ++p) {
+            if (ci[p] < 0 || ci[p] >= ctx->n_global) {
+                ctx->err = std::string(name) + ": column id out of range in row " + std::to_string(r);
+                return TRPLK_EINVAL;
+            }
+            if (p > rp[r] - base && ci[p] <= ci[p - 1]) {
+                ctx->err = std::string(name) + ": columns not strictly increasing in row " + std::to_string(r);
+                return TRPLK_EINVAL;
+            }
+        }
+    }
+    return TRPLK_OK;
+}
+
+// ----------------------------------------------------------------- halo exchange
+trplk_status halo(trplk_ctx* ctx, const double* xconst) {
+    if (ctx->nranks == 1 || ctx->peers.empty()) return TRPLK_OK;
+    double* x = const_cast<double*>(xconst);
+    int64_t off = 0;
+    for (size_t i = 0; i < ctx->peers.size(); ++i) {
+        if (ctx->send_cnt[i] > 0 && ctx->send_start[i] < 0) {
+            launch_gather(x, ctx->send_idx[i], ctx->send_cnt[i], ctx->sendbuf + off, ctx->stream);
+        }
+        off += ctx->send_cnt[i];
+    }
+    NK(ncclGroupStart());
+    off = 0;
+    for (size_t i = 0; i < ctx->peers.size(); ++i) {
+        const int pr = ctx->peers[i];
+        if (ctx->recv_cnt[i] > 0)
+            NK(ncclRecv(x + ctx->n_loc + ctx->recv_off[i], (size_t)ctx->recv_cnt[i], ncclDouble, pr, ctx->comm,
+                        ctx->stream));
+        if (ctx->send_cnt[i] > 0) {
+            const double* src = ctx->send_start[i] >= 0 ? x + ctx->send_start[i] : ctx->sendbuf + off;
+            NK(ncclSend(src, (size_t)ctx->send_cnt[i], ncclDouble, pr, ctx->comm, ctx->stream));
+        }
+        off += ctx->send_cnt[i];
+    }
+    NK(ncclGroupEnd());
+    return TRPLK_OK;
+}
+
+// ----------------------------------------------------------------- kernel wrappers
+SdotsArgs sd_base(trplk_ctx* ctx) {
+    SdotsArgs a{};
+    a.nrows = ctx->n_loc;
+    a.theta_idx = -1;
+    a.tcol_fixed = -1;
+    a.sigma = ctx->sigma;
+    a.mfloor = ctx->mfloor;
+    a.ctl = ctx->ctl;
+    a.T = ctx->T;
+    a.ldT = QMAX;
+    a.part = ctx->part;
+    a.counter = ctx->counter;
+    a.maxcta = ctx->maxcta;
+    a.ldu = ctx->ld;
+    a.x_ld = ctx->ld;
+    return a;
+}
+
+UpdArgs up_base(trplk_ctx* ctx) {
+    UpdArgs a{};
+    a.nrows = ctx->n_loc;
+    a.ldu = ctx->ld;
+    a.x_ld = ctx->ld;
+    a.ctl = ctx->ctl;
+    a.part = ctx->part;
+    a.counter = ctx->counter;
+    a.maxcta = ctx->maxcta;
+    a.dest_ld = ctx->ld;
+    return a;
+}
+
+double vec_bytes(trplk_ctx* ctx) { return 8.0 * (double)ctx->n_loc; }
+
+double mat_bytes(trplk_ctx* ctx, bool b) {
+    return (double)(b ? ctx->sellB_bytes : ctx->sellA_bytes);
+}
+
+trplk_status run_sdots(trplk_ctx* ctx, SdotsArgs a, int kbytes_cols) {
+    const int grid = sdots_grid(ctx->n_loc);
+    // algorithmic bytes of this launch (DESIGN.md byte model)
+    double by = 0.0;
+    if (a.A.nrows && a.out_mode != 4) by += mat_bytes(ctx, false) + vec_bytes(ctx);
+    if (a.B.nrows) by += mat_bytes(ctx, true);
+    if (!a.A.nrows) by += vec_bytes(ctx);
+    if (a.out) by += vec_bytes(ctx);
+    if (a.uout) by += vec_bytes(ctx);
+    if (a.wext) by += vec_bytes(ctx);
+    by += vec_bytes(ctx) * kbytes_cols;
+    ctx->model_bytes += by;
+    ctx->launches += ctx->nranks > 1 ? 2 : 1;
+    if (ctx->nranks > 1) {
+        a.red_local = ctx->red_local;
+        launch_sdots(a, grid, ctx->stream);
+        NK(ncclAllGather(ctx->red_local, ctx->red_all, NV_MAX, ncclDouble, ctx->comm, ctx->stream));
+        launch_finalize_sdots_multi(a, ctx->red_all, ctx->nranks, NV_MAX, ctx->stream);
+    } else {
+        launch_sdots(a, grid, ctx->stream);
+    }
+    CK(cudaGetLastError());
+    return TRPLK_OK;
+}
+
+trplk_status run_upd(trplk_ctx* ctx, UpdArgs a, int k_nominal) {
+    const int kmax = kmax_bucket(std::max(k_nominal, 1));
+    const int grid = upd_grid(ctx->n_loc, kmax);
+    if (a.mode != 3) ctx->model_bytes += vec_bytes(ctx) * (k_nominal + 2);
+    const bool dots = a.dots && (a.mode == 1 || a.mode == 2);
+    ctx->launches += (ctx->nranks > 1 && dots) ? 2 : 1;
+    if (ctx->nranks > 1 && dots) {
+        a.red_local = ctx->red_local;
+        launch_upd(a, kmax, grid, ctx->stream);
+        NK(ncclAllGather(ctx->red_local, ctx->red_all, NV_MAX, ncclDouble, ctx->comm, ctx->stream));
+        launch_finalize_upd_multi(a, ctx->red_all, ctx->nranks, NV_MAX, ctx->stream);
+    } else {
+        launch_upd(a, kmax, grid, ctx->stream);
+    }
+    CK(cudaGetLastError());
+    return TRPLK_OK;
+}
+
+// CGS2 in the B-inner product (R3) of x against V = Ubase(:, 0:kv) (kv = -1: ctl->k), result
+// normalised into Ubase(:, ctl->k) (dest_dyn) or `dest`, ctl->k += 1 on success.
+struct CgsSpec {
+    const double* x;
+    int x_dyn = 0, x_off = 0;
+    const double* V;
+    int64_t ldv = 0;  // 0 => ctx->ld
+    int kv;          // fixed width or -1 (ctl->k)
+    int k_nominal;   // upper bound for the kernel bucket
+    bool first_done; // B = I: h0 / N_IN2 already computed by the fused K1
+    double* dest;
+    int dest_dyn;
+    double* dest2;
+    unsigned gate, clear;
+    int inc_k;
+    cudaEvent_t mark_final = nullptr;  // profiling: recorded just before the FINAL update
+};
+
+trplk_status cgs2(trplk_ctx* ctx, const CgsSpec& c) {
+    const int kn = std::max(c.k_nominal, 1);
+    const int64_t ldv = c.ldv > 0 ? c.ldv : ctx->ld;
+    // pass 1 coefficients: h0 = V^T B x, N_IN2 = x^T B x
+    if (!c.first_done) {
+        SdotsArgs a = sd_base(ctx);
+        a.x = c.x;
+        a.x_dyn = c.x_dyn;
+        a.x_off = c.x_off;
+        if (ctx->hasB) {
+            a.A = ctx->B;  // z = B x
+            a.set1 = 1;
+            a.norm1 = 2;   // x.z
+            ST(halo(ctx, c.x));
+        } else {
+            a.set1 = 3;    // x
+            a.norm1 = 3;   // x.x
+        }
+        a.U = c.V;
+        a.ldu = ldv;
+        a.k1 = c.kv;
+        a.k_from_ctl = c.kv < 0;
+        a.dest1 = D_H0 + 0;
+        a.nslot1 = N_IN2;
+        a.gate = c.gate;
+        ST(run_sdots(ctx, a, kn));
+    }
+    // pass 2: w1 = x - V h0 (+ B = I: h1 = V^T w1, N_1SQ)
+    {
+        UpdArgs u = up_base(ctx);
+        u.x = c.x;
+        u.x_dyn = c.x_dyn;
+        u.x_off = c.x_off;
+        u.U = c.V;
+        u.ldu = ldv;
+        u.kv = c.kv;
+        u.hslot = 0;
+        u.mode = ctx->hasB ? 0 : 1;
+        u.dots = ctx->hasB ? 0 : 1;
+        u.out = ctx->w1;
+        u.hout = 1;
+        u.gate = c.gate;
+        ST(run_upd(ctx, u, kn));
+    }
+    if (ctx->hasB) {
+        SdotsArgs a = sd_base(ctx);
+        ST(halo(ctx, ctx->w1));
+        a.x = ctx->w1;
+        a.A = ctx->B;
+        a.set1 = 1;
+        a.norm1 = 2;
+        a.U = c.V;
+        a.ldu = ldv;
+        a.k1 = c.kv;
+        a.k_from_ctl = c.kv < 0;
+        a.dest1 = D_H0 + 1;
+        a.nslot1 = N_1SQ;
+        a.gate = c.gate;
+        ST(run_sdots(ctx, a, kn));
+    }
+    // final: y = w1 - V h1, beta from Pythagoras; pass 3 into w2 if the norm dropped > 1/sqrt2
+    if (c.mark_final) CK(cudaEventRecord(c.mark_final, ctx->stream));
+    {
+        UpdArgs u = up_base(ctx);
+        u.x = ctx->w1;
+        u.U = c.V;
+        u.ldu = ldv;
+        u.kv = c.kv;
+        u.hslot = 1;
+        u.mode = 2;
+        u.dots = ctx->hasB ? 0 : 1;
+        u.out = ctx->w2;
+        u.hout = 2;
+        u.dest = c.dest;
+        u.dest_dyn = c.dest_dyn;
+        u.dest2 = c.dest2;
+        u.inc_k = c.inc_k;
+        u.gate = c.gate;
+        u.clear_on_brk = c.clear;
+        ST(run_upd(ctx, u, kn));
+    }
+    if (ctx->hasB) {  // pass-3 dots for B != I (gated on ctl->pass3)
+        SdotsArgs a = sd_base(ctx);
+        ST(halo(ctx, ctx->w2));
+        a.x = ctx->w2;
+        a.A = ctx->B;
+        a.set1 = 1;
+        a.norm1 = 2;
+        a.U = c.V;
+        a.ldu = ldv;
+        a.k1 = c.kv;
+        a.k_from_ctl = c.kv < 0;
+        a.dest1 = D_H0 + 2;
+        a.nslot1 = N_2SQ_EXP;
+        a.gate = c.gate;
+        a.gate_pass3 = 1;
+        const double mb = ctx->model_bytes;
+        ST(run_sdots(ctx, a, 0));
+        ctx->model_bytes = mb;  // rare path, not in the byte model
+    }
+    {
+        UpdArgs u = up_base(ctx);
+        u.x = ctx->w2;
+        u.U = c.V;
+        u.ldu = ldv;
+        u.kv = c.kv;
+        u.hslot = 2;
+        u.mode = 3;
+        u.dest = c.dest;
+        u.dest_dyn = c.dest_dyn;
+        u.dest2 = c.dest2;
+        u.inc_k = c.inc_k;
+        u.gate = c.gate;
+        u.clear_on_brk = c.clear;
+        ST(run_upd(ctx, u, kn));
+    }
+    return TRPLK_OK;
+}
+
+// r = A x - theta B x, u = M r, N_RES2 = ||r||^2  (Alg.1 steps 12/15)
+trplk_status residual(trplk_ctx* ctx, const double* x, int x_dyn, int theta_idx, double* uout, unsigned gate) {
+    if (x_dyn == 0) ST(halo(ctx, x));
+    SdotsArgs a = sd_base(ctx);
+    a.A = ctx->A;
+    if (ctx->hasB) a.B = ctx->B;
+    a.x = x;
+    a.x_dyn = x_dyn;
+    a.out_mode = 3;
+    a.uout = uout;
+    a.norm1 = 1;
+    a.nslot1 = N_RES2;
+    a.theta_idx = theta_idx;
+    a.gate = gate;
+    ST(run_sdots(ctx, a, 0));
+    return TRPLK_OK;
+}
+
+trplk_status ensure_buffers(trplk_ctx* ctx, int q, int ph) {
+    if (ctx->q_alloc >= q && ctx->ph_alloc >= ph) return TRPLK_OK;
+    // release previous solve buffers
+    for (double** b : {&ctx->U[0], &ctx->U[1], &ctx->Wtmp}) {
+        dev_free(ctx, *b);
+        *b = nullptr;
+    }
+    const size_t ld = (size_t)ctx->ld;
+    ST(dalloc(ctx, &ctx->U[0], ld * q));
+    ST(dalloc(ctx, &ctx->U[1], ld * q));
+    ST(dalloc(ctx, &ctx->Wtmp, ld * ph));
+    CK(cudaMemsetAsync(ctx->U[0], 0, ld * q * 8, ctx->stream));
+    CK(cudaMemsetAsync(ctx->U[1], 0, ld * q * 8, ctx->stream));
+    ctx->q_alloc = q;
+    ctx->ph_alloc = ph;
+    for (auto& g : ctx->graphs) cudaGraphExecDestroy(g.second.exec);
+    ctx->graphs.clear();
+    return TRPLK_OK;
+}
+
+trplk_status ctl_push(trplk_ctx* ctx) {
+    CK(cudaMemcpyAsync(ctx->ctl, ctx->ctl_h, offsetof(Ctl, k_rr), cudaMemcpyHostToDevice, ctx->stream));
+    return TRPLK_OK;
+}
+
+trplk_status ctl_pull(trplk_ctx* ctx) {
+    CK(cudaMemcpyAsync(ctx->ctl_h, ctx->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    return TRPLK_OK;
+}
+
+// One outer cycle after the seed vector u is in place: eq 3.1 inner steps, +K, RR, rotation,
+// residual of the target.  Issued eagerly or under stream capture.
+trplk_status issue_cycle(trplk_ctx* ctx, const Sizes& S, int cur, int nprev, int t_static, int xprev_static) {
+    const int oth = 1 - cur;
+    double* Uc = ctx->U[cur];
+    double* Uo = ctx->U[oth];
+    const int64_t ld = ctx->ld;
+    // seed: g_1 = (I - X X^T B) u / beta  (eq 3.2 u1 = C x_t, R4), written to column p^
+    {
+        CgsSpec c{};
+        c.x = ctx->u;
+        c.V = Uc;
+        c.kv = S.ph;
+        c.k_nominal = S.ph;
+        c.first_done = false;
+        c.dest = Uc;
+        c.dest_dyn = 1;
+        c.gate = F_CYCLE;
+        c.clear = F_CYCLE;
+        c.inc_k = 1;
+        ST(cgs2(ctx, c));
+    }
+    // inner steps, eq 3.1
+    const int jmid = std::max(1, std::min(S.m - 1, S.m / 2));
+    for (int j = 1; j <= S.m; ++j) {
+        const int k = S.ph + j;  // nominal width incl. g_j
+        const bool prof = ctx->prof_on && j == jmid && j < S.m;
+        const double* g = Uc + ld * (k - 1);
+        ST(halo(ctx, g));
+        SdotsArgs a = sd_base(ctx);
+        a.A = ctx->A;
+        a.x = g;
+        a.U = Uc;
+        a.k_from_ctl = 1;
+        a.set1 = 1;  // T(1:k,k) = U^T z
+        a.dest1 = D_TCOL;
+        a.gate = F_CYCLE | F_INNER;
+        if (j < S.m) {
+            a.out_mode = 2;  // w = M (z - rho B g)
+            a.out = ctx->w;
+            if (ctx->hasB) {
+                a.B = ctx->B;
+            } else {
+                a.set2 = 2;  // h0 = U^T w
+                a.dest2 = D_H0 + 0;
+                a.norm1 = 1;  // ||w||^2
+                a.nslot1 = N_IN2;
+            }
+            if (prof) CK(cudaEventRecord(ctx->pev[0], ctx->stream));
+            ST(run_sdots(ctx, a, k));
+            if (prof) CK(cudaEventRecord(ctx->pev[1], ctx->stream));
+            CgsSpec c{};
+            if (prof) c.mark_final = ctx->pev[2];
+            c.x = ctx->w;
+            c.V = Uc;
+            c.kv = -1;
+            c.k_nominal = k;
+            c.first_done = !ctx->hasB;
+            c.dest = Uc;
+            c.dest_dyn = 1;
+            c.gate = F_CYCLE | F_INNER;
+            c.clear = F_INNER;
+            c.inc_k = 1;
+            ST(cgs2(ctx, c));
+            if (prof) CK(cudaEventRecord(ctx->pev[3], ctx->stream));
+        } else {
+            ST(run_sdots(ctx, a, k));
+        }
+    }
+    // +K: X^prev appended after G, explicitly orthogonalised, one matvec each
+    for (int jj = 0; jj < nprev; ++jj) {
+        const unsigned kb = F_KCOL0 << jj;
+        CgsSpec c{};
+        if (xprev_static >= 0) {
+            c.x = Uo + ld * (xprev_static + jj);
+        } else {
+            c.x = Uo;
+            c.x_dyn = 2;
+            c.x_off = jj;
+        }
+        c.V = Uc;
+        c.kv = -1;
+        c.k_nominal = S.ph + S.m + jj;
+        c.dest = Uc;
+        c.dest_dyn = 1;
+        c.dest2 = ctx->xk;
+        c.gate = F_CYCLE | kb;
+        c.clear = kb;
+        c.inc_k = 1;
+        ST(cgs2(ctx, c));
+        ST(halo(ctx, ctx->xk));
+        SdotsArgs a = sd_base(ctx);
+        a.A = ctx->A;
+        a.x = ctx->xk;
+        a.U = Uc;
+        a.k_from_ctl = 1;
+        a.set1 = 1;
+        a.dest1 = D_TCOL;
+        a.gate = F_CYCLE | kb;
+        ST(run_sdots(ctx, a, S.ph + S.m + jj + 1));
+    }
+    // Rayleigh-Ritz (step 11) and rotation X = U Y(:,1:p^) into the other buffer
+    launch_eig(ctx->ctl, ctx->T, QMAX, ctx->Yg, QMAX, S.ph, 0, F_CYCLE, ctx->stream);
+    CK(cudaGetLastError());
+    launch_rotate(Uc, ld, ctx->n_loc, ctx->ctl, 0, ctx->Yg, QMAX, S.ph, Uo, ld, F_CYCLE, ctx->stream);
+    ctx->launches += 2;
+    CK(cudaGetLastError());
+    ctx->model_bytes += vec_bytes(ctx) * (S.q + S.ph);
+    // residual of the target, u = M r (steps 12, 15)
+    if (t_static > 0) ST(residual(ctx, Uo + ld * (t_static - 1), 0, -1, ctx->u, F_CYCLE));
+    else ST(residual(ctx, Uo, 1, -1, ctx->u, F_CYCLE));
+    return TRPLK_OK;
+}
+
+trplk_status run_cycle(trplk_ctx* ctx, const Sizes& S, int cur, int nprev, int t, int xprev, bool use_graph) {
+    const bool multi = ctx->nranks > 1;
+    const int ts = multi ? t : -1;  // static addresses are needed for the halo exchange
+    const int xs = multi ? xprev : -1;
+    if (!use_graph) return issue_cycle(ctx, S, cur, nprev, ts, xs);
+    if (!(ctx->gsizes == S)) {
+        for (auto& g : ctx->graphs) cudaGraphExecDestroy(g.second.exec);
+        ctx->graphs.clear();
+        ctx->gsizes = S;
+    }
+    const uint64_t key = ((uint64_t)cur) | ((uint64_t)nprev << 1) | ((uint64_t)(ts + 1) << 8) |
+                         ((uint64_t)(xs + 1) << 24) | ((uint64_t)(ctx->prof_on ? 1 : 0) << 40);
+    auto it = ctx->graphs.find(key);
+    if (it == ctx->graphs.end()) {
+        const double mb0 = ctx->model_bytes;
+        const int64_t l0 = ctx->launches;
+        cudaGraph_t graph;
+        CK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+        trplk_status st = issue_cycle(ctx, S, cur, nprev, ts, xs);
+        cudaError_t e = cudaStreamEndCapture(ctx->stream, &graph);
+        if (st != TRPLK_OK) return st;
+        if (e != cudaSuccess) {
+            ctx->err = std::string("cudaStreamEndCapture: ") + cudaGetErrorString(e);
+            return TRPLK_ECUDA;
+        }
+        GraphRec rec;
+        rec.bytes = ctx->model_bytes - mb0;
+        ctx->model_bytes = mb0;
+        rec.launches = ctx->launches - l0;
+        ctx->launches = l0;
+        CK(cudaGraphInstantiate(&rec.exec, graph, 0));
+        cudaGraphDestroy(graph);
+        it = ctx->graphs.emplace(key, rec).first;
+    }
+    CK(cudaGraphLaunch(it->second.exec, ctx->stream));
+    ctx->model_bytes += it->second.bytes;
+    ctx->launches += it->second.launches;
+    return TRPLK_OK;
+}
+
+}  // namespace
+
+// ======================================================================= ABI
+extern "C" {
+
+void trplk_options_default(trplk_options* opt) {
+    if (!opt) return;
+    opt->seed = 12;
+    opt->max_cycles = 5000;
+    opt->tol_mode = 0;
+    opt->restart_size = 0;
+    opt->lock_mode = 0;
+    opt->debug_checks = 0;
+    opt->use_graphs = 1;
+}
+
+trplk_status trplk_nccl_unique_id(void* out, size_t out_bytes) {
+    if (!out || out_bytes < sizeof(ncclUniqueId)) return TRPLK_EINVAL;
+    ncclUniqueId id;
+    if (ncclGetUniqueId(&id) != ncclSuccess) return TRPLK_ENCCL;
+    memcpy(out, &id, sizeof(id));
+    return TRPLK_OK;
+}
+
+const char* trplk_last_error(const trplk_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+static trplk_status create_impl(trplk_ctx* ctx, int64_t n_global, const int64_t* a_rowptr, const int64_t* a_col,
+                                const double* a_val, const int64_t* b_rowptr, const int64_t* b_col,
+                                const double* b_val, double sigma, const trplk_dist* dist) {
+    ctx->n_global = n_global;
+    ctx->sigma = sigma;
+    if (n_global < 1) {
+        ctx->err = "n_global < 1";
+        return TRPLK_EINVAL;
+    }
+    if (dist) {
+        ctx->rank = dist->rank;
+        ctx->nranks = dist->nranks;
+        ctx->row_begin = dist->row_begin;
+        ctx->row_end = dist->row_end;
+        if (ctx->nranks < 1 || ctx->rank < 0 || ctx->rank >= ctx->nranks || ctx->row_begin < 0 ||
+            ctx->row_end > n_global || ctx->row_end <= ctx->row_begin) {
+            ctx->err = "bad trplk_dist (rank/nranks/row range)";
+            return TRPLK_EINVAL;
+        }
+        if (ctx->nranks > 1 && !dist->nccl_unique_id) {
+            ctx->err = "nranks > 1 needs nccl_unique_id";
+            return TRPLK_EINVAL;
+        }
+    } else {
+        ctx->row_begin = 0;
+        ctx->row_end = n_global;
+    }
+    ctx->n_loc = ctx->row_end - ctx->row_begin;
+    ctx->hasB = b_rowptr != nullptr;
+    if ((b_rowptr == nullptr) != (b_col == nullptr) || (b_rowptr == nullptr) != (b_val == nullptr)) {
+        ctx->err = "B: give all three CSR arrays or none";
+        return TRPLK_EINVAL;
+    }
+    if (!a_val) {
+        ctx->err = "A: NULL values";
+        return TRPLK_EINVAL;
+    }
+    ST(validate_csr(ctx, "A", a_rowptr, a_col));
+    if (ctx->hasB) ST(validate_csr(ctx, "B", b_rowptr, b_col));
+
+    if (ctx->nranks > 1) {
+        ncclUniqueId id;
+        memcpy(&id, dist->nccl_unique_id, sizeof(id));
+        NK(ncclCommInitRank(&ctx->comm, ctx->nranks, id, ctx->rank));
+    }
+    // ghost columns (global ids outside the owned range), sorted
+    std::vector<int64_t> ghosts;
+    {
+        const int64_t nnz_a = a_rowptr[ctx->n_loc] - a_rowptr[0];
+        for (int64_t p = 0; p < nnz_a; ++p)
+            if (a_col[p] < ctx->row_begin || a_col[p] >= ctx->row_end) ghosts.push_back(a_col[p]);
+        if (ctx->hasB) {
+            const int64_t nnz_b = b_rowptr[ctx->n_loc] - b_rowptr[0];
+            for (int64_t p = 0; p < nnz_b; ++p)
+                if (b_col[p] < ctx->row_begin || b_col[p] >= ctx->row_end) ghosts.push_back(b_col[p]);
+        }
+        std::sort(ghosts.begin(), ghosts.end());
+        ghosts.erase(std::unique(ghosts.begin(), ghosts.end()), ghosts.end());
+    }
+    ctx->n_ghost = (int64_t)ghosts.size();
+    if (ctx->n_loc + ctx->n_ghost >= (int64_t)1 << 31) {
+        ctx->err = "local rows + ghosts exceed int32 column ids";
+        return TRPLK_EINVAL;
+    }
+    ctx->ld = ((ctx->n_loc + ctx->n_ghost + 31) / 32) * 32;
+    ctx->nnzA = a_rowptr[ctx->n_loc] - a_rowptr[0];
+    ctx->nnzB = ctx->hasB ? b_rowptr[ctx->n_loc] - b_rowptr[0] : 0;
+
+    // ||A||_F and max |A_jj| (local, then across ranks)
+    double fro2 = 0.0, amax = 0.0;
+    for (int64_t r = 0; r < ctx->n_loc; ++r)
+        for (int64_t p = a_rowptr[r] - a_rowptr[0]; p < a_rowptr[r + 1] - a_rowptr[0]; ++p) {
+            fro2 += a_val[p] * a_val[p];
+            if (a_col[p] == ctx->row_begin + r) amax = std::max(amax, std::fabs(a_val[p]));
+        }
+
+    HostSell hs;
+    ST(build_sell(ctx, a_rowptr, a_col, a_val, ghosts, hs));
+    ST(upload_sell(ctx, hs, ctx->A, ctx->sellA_bytes));
+    if (ctx->hasB) {
+        HostSell hb;
+        ST(build_sell(ctx, b_rowptr, b_col, b_val, ghosts, hb));
+        ST(upload_sell(ctx, hb, ctx->B, ctx->sellB_bytes));
+    }
+
+    // fixed device buffers
+    ctx->maxcta = 148 * 8;
+    {
+        int dev = 0, nsm = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        ctx->maxcta = std::max(nsm * 8, 64);
+    }
+    const size_t ld = (size_t)ctx->ld;
+    ST(dalloc(ctx, &ctx->w, ld));
+    ST(dalloc(ctx, &ctx->w1, ld));
+    ST(dalloc(ctx, &ctx->w2, ld));
+    ST(dalloc(ctx, &ctx->u, ld));
+    ST(dalloc(ctx, &ctx->u2, ld));
+    ST(dalloc(ctx, &ctx->xk, ld));
+    ST(dalloc(ctx, &ctx->T, (size_t)QMAX * QMAX));
+    ST(dalloc(ctx, &ctx->Yg, (size_t)QMAX * QMAX));
+    ST(dalloc(ctx, &ctx->part, (size_t)NV_MAX * ctx->maxcta));
+    ST(dalloc(ctx, &ctx->red_local, (size_t)NV_MAX));
+    ST(dalloc(ctx, &ctx->red_all, (size_t)NV_MAX * ctx->nranks));
+    ST(dalloc(ctx, &ctx->counter, 16));
+    ST(dalloc(ctx, &ctx->ctl, 1));
+    CK(cudaMemsetAsync(ctx->counter, 0, 64, ctx->stream));
+    CK(cudaMemsetAsync(ctx->ctl, 0, sizeof(Ctl), ctx->stream));
+    CK(cudaMemsetAsync(ctx->T, 0, sizeof(double) * QMAX * QMAX, ctx->stream));
+    for (double* v : {ctx->w, ctx->w1, ctx->w2, ctx->u, ctx->u2, ctx->xk})
+        CK(cudaMemsetAsync(v, 0, ld * 8, ctx->stream));
+    CK(cudaMallocHost(&ctx->ctl_h, sizeof(Ctl)));
+    memset(ctx->ctl_h, 0, sizeof(Ctl));
+
+    if (ctx->nranks > 1) {
+        // global ||A||_F^2 and max |A_jj|
+        double* tmp;
+        ST(dalloc(ctx, &tmp, 2));
+        CK(cudaMemcpyAsync(tmp, &fro2, 8, cudaMemcpyHostToDevice, ctx->stream));
+        CK(cudaMemcpyAsync(tmp + 1, &amax, 8, cudaMemcpyHostToDevice, ctx->stream));
+        NK(ncclAllReduce(tmp, tmp, 1, ncclDouble, ncclSum, ctx->comm, ctx->stream));
+        NK(ncclAllReduce(tmp + 1, tmp + 1, 1, ncclDouble, ncclMax, ctx->comm, ctx->stream));
+        CK(cudaMemcpyAsync(&fro2, tmp, 8, cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaMemcpyAsync(&amax, tmp + 1, 8, cudaMemcpyDeviceToHost, ctx->stream));
+        // all row ranges
+        int64_t* ranges;
+        ST(dalloc(ctx, &ranges, 2 * (size_t)ctx->nranks + 2));
+        int64_t mine[2] = {ctx->row_begin, ctx->row_end};
+        CK(cudaMemcpyAsync(ranges + 2 * ctx->nranks, mine, 16, cudaMemcpyHostToDevice, ctx->stream));
+        NK(ncclAllGather(ranges + 2 * ctx->nranks, ranges, 2, ncclInt64, ctx->comm, ctx->stream));
+        std::vector<int64_t> rg(2 * (size_t)ctx->nranks);
+        CK(cudaMemcpyAsync(rg.data(), ranges, 16 * (size_t)ctx->nranks, cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        int64_t tot = 0;
+        for (int r = 0; r < ctx->nranks; ++r) {
+            tot += rg[2 * r + 1] - rg[2 * r];
+            if (r > 0 && rg[2 * r] != rg[2 * r - 1]) {
+                ctx->err = "row ranges do not tile [0, n) in rank order";
+                return TRPLK_EINVAL;
+            }
+        }
+        if (tot != n_global || rg[0] != 0) {
+            ctx->err = "row ranges do not tile [0, n)";
+            return TRPLK_EINVAL;
+        }
+        // recv plan: ghosts grouped by owner (contiguous, since sorted)
+        std::vector<int64_t> need_cnt(ctx->nranks, 0), need_off(ctx->nranks, 0);
+        for (size_t gi = 0; gi < ghosts.size(); ++gi) {
+            int owner = 0;
+            while (owner < ctx->nranks - 1 && ghosts[gi] >= rg[2 * owner + 1]) ++owner;
+            if (need_cnt[owner] == 0) need_off[owner] = (int64_t)gi;
+            need_cnt[owner]++;
+        }
+        // exchange counts (all-to-all through allgather of the count matrix)
+        int64_t* cnts;
+        ST(dalloc(ctx, &cnts, (size_t)ctx->nranks * ctx->nranks + ctx->nranks));
+        CK(cudaMemcpyAsync(cnts + (size_t)ctx->nranks * ctx->nranks, need_cnt.data(), 8 * (size_t)ctx->nranks,
+                           cudaMemcpyHostToDevice, ctx->stream));
+        NK(ncclAllGather(cnts + (size_t)ctx->nranks * ctx->nranks, cnts, ctx->nranks, ncclInt64, ctx->comm,
+                         ctx->stream));
+        std::vector<int64_t> cm((size_t)ctx->nranks * ctx->nranks);
+        CK(cudaMemcpyAsync(cm.data(), cnts, 8 * cm.size(), cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        // exchange the requested global ids
+        int64_t* gdev;
+        ST(dalloc(ctx, &gdev, ghosts.size() + 1));
+        if (!ghosts.empty())
+            CK(cudaMemcpyAsync(gdev, ghosts.data(), 8 * ghosts.size(), cudaMemcpyHostToDevice, ctx->stream));
+        std::vector<int64_t*> req(ctx->nranks, nullptr);
+        NK(ncclGroupStart());
+        for (int s = 0; s < ctx->nranks; ++s) {
+            if (s == ctx->rank) continue;
+            const int64_t they_need = cm[(size_t)s * ctx->nranks + ctx->rank];
+            if (they_need > 0) {
+                ST(dalloc(ctx, &req[s], (size_t)they_need));
+                NK(ncclRecv(req[s], (size_t)they_need, ncclInt64, s, ctx->comm, ctx->stream));
+            }
+            if (need_cnt[s] > 0) NK(ncclSend(gdev + need_off[s], (size_t)need_cnt[s], ncclInt64, s, ctx->comm, ctx->stream));
+        }
+        NK(ncclGroupEnd());
+        CK(cudaStreamSynchronize(ctx->stream));
+        int64_t sendtot = 0;
+        for (int s = 0; s < ctx->nranks; ++s) {
+            if (s == ctx->rank) continue;
+            const int64_t they_need = cm[(size_t)s * ctx->nranks + ctx->rank];
+            if (they_need == 0 && need_cnt[s] == 0) continue;
+            ctx->peers.push_back(s);
+            ctx->recv_off.push_back(need_off[s]);
+            ctx->recv_cnt.push_back(need_cnt[s]);
+            ctx->send_cnt.push_back(they_need);
+            std::vector<int64_t> ids(they_need);
+            if (they_need) CK(cudaMemcpy(ids.data(), req[s], 8 * they_need, cudaMemcpyDeviceToHost));
+            bool contig = true;
+            for (int64_t i = 1; i < they_need; ++i) contig &= ids[i] == ids[i - 1] + 1;
+            if (they_need > 0 && contig) {
+                ctx->send_start.push_back(ids[0] - ctx->row_begin);
+                ctx->send_idx.push_back(nullptr);
+            } else {
+                ctx->send_start.push_back(-1);
+                std::vector<int> loc(they_need);
+                for (int64_t i = 0; i < they_need; ++i) loc[i] = (int)(ids[i] - ctx->row_begin);
+                int* d = nullptr;
+                ST(dalloc(ctx, &d, (size_t)std::max<int64_t>(they_need, 1)));
+                if (they_need) CK(cudaMemcpy(d, loc.data(), 4 * they_need, cudaMemcpyHostToDevice));
+                ctx->send_idx.push_back(d);
+            }
+            sendtot += they_need;
+        }
+        ST(dalloc(ctx, &ctx->sendbuf, (size_t)std::max<int64_t>(sendtot, 1)));
+    }
+    ctx->normF = std::sqrt(fro2);
+    ctx->amax = amax;
+    ctx->mfloor = 1e-8 * amax;  // S:192 floor eps_d * max_j |A_jj| (R12)
+    CK(cudaStreamSynchronize(ctx->stream));
+    return TRPLK_OK;
+}
+
+trplk_status trplk_create(trplk_ctx** out, int64_t n_global, const int64_t* a_rowptr, const int64_t* a_col,
+                          const double* a_val, const int64_t* b_rowptr, const int64_t* b_col, const double* b_val,
+                          double sigma, const trplk_dist* dist, const trplk_allocator* alloc, void* stream) {
+    if (!out) return TRPLK_EINVAL;
+    trplk_ctx* ctx = new trplk_ctx();
+    *out = ctx;
+    ctx->user_stream = (cudaStream_t)stream;
+    if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ctx->ev_in, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ctx->ev_out, cudaEventDisableTiming) != cudaSuccess) {
+        ctx->err = "cannot create the work stream";
+        return TRPLK_ECUDA;
+    }
+    enter_stream(ctx);
+    if (alloc && alloc->alloc && alloc->free) {
+        ctx->alloc = *alloc;
+        ctx->has_alloc = true;
+    }
+    return create_impl(ctx, n_global, a_rowptr, a_col, a_val, b_rowptr, b_col, b_val, sigma, dist);
+}
+
+void trplk_destroy(trplk_ctx* ctx) {
+    if (!ctx) return;
+    if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    if (ctx->user_stream) cudaStreamSynchronize(ctx->user_stream);
+    for (auto& g : ctx->graphs) cudaGraphExecDestroy(g.second.exec);
+    for (auto& a : ctx->allocs) {
+        if (ctx->has_alloc) ctx->alloc.free(a.first, ctx->alloc.user);
+        else cudaFree(a.first);
+    }
+    if (ctx->ctl_h) cudaFreeHost(ctx->ctl_h);
+    if (ctx->ev_in) cudaEventDestroy(ctx->ev_in);
+    for (auto& e : ctx->pev)
+        if (e) cudaEventDestroy(e);
+    if (ctx->ev_out) cudaEventDestroy(ctx->ev_out);
+    if (ctx->stream) cudaStreamDestroy(ctx->stream);
+    if (ctx->comm) ncclCommDestroy(ctx->comm);
+    delete ctx;
+}
+
+trplk_status trplk_info(const trplk_ctx* ctx, int64_t* n_local, int64_t* n_ghost, int* rank, int* nranks,
+                        double* frob_a, int64_t* sell_bytes_a, int64_t* sell_bytes_b) {
+    if (!ctx) return TRPLK_EINVAL;
+    if (n_local) *n_local = ctx->n_loc;
+    if (n_ghost) *n_ghost = ctx->n_ghost;
+    if (rank) *rank = ctx->rank;
+    if (nranks) *nranks = ctx->nranks;
+    if (frob_a) *frob_a = ctx->normF;
+    if (sell_bytes_a) *sell_bytes_a = ctx->sellA_bytes;
+    if (sell_bytes_b) *sell_bytes_b = ctx->sellB_bytes;
+    return TRPLK_OK;
+}
+
+int trplk_get_log(const trplk_ctx* ctx, int cap, int* t, int64_t* mv, double* theta_t, double* res, int* k,
+                  int* nprev, double* thetas) {
+    if (!ctx) return 0;
+    const int n = std::min<int>(cap, (int)ctx->log.size());
+    for (int i = 0; i < n; ++i) {
+        const LogRec& L = ctx->log[i];
+        if (t) t[i] = L.t;
+        if (mv) mv[i] = L.mv;
+        if (theta_t) theta_t[i] = L.theta_t;
+        if (res) res[i] = L.res;
+        if (k) k[i] = L.k;
+        if (nprev) nprev[i] = L.nprev;
+        if (thetas)
+            for (int j = 0; j < ctx->log_ph; ++j) thetas[(size_t)i * ctx->log_ph + j] = L.thetas[j];
+    }
+    return n;
+}
+
+static trplk_status solve_impl(trplk_ctx* ctx, int p, int q, int l, double tol, double* evals, double* evecs,
+                               double* resid, const trplk_options* optin, trplk_stats* stats) {
+    trplk_options opt;
+    trplk_options_default(&opt);
+    if (optin) opt = *optin;
+    const int ph = opt.restart_size > 0 ? opt.restart_size : p;
+    const int m = q - ph - l;
+    if (p < 1 || l < 0 || ph < p || m < 1 || !(tol > 0.0) || q > QMAX || ph + 1 > ctx->n_global ||
+        opt.max_cycles < 1 || l > 16 || ph > 24) {
+        ctx->err = "invalid solve arguments (need p>=1, l>=0, p<=p^<=24, m=q-p^-l>=1, q<=" +
+                   std::to_string(QMAX) + ", tol>0, l<=16)";
+        return TRPLK_EINVAL;
+    }
+    if (!evals || !resid) {
+        ctx->err = "NULL output";
+        return TRPLK_EINVAL;
+    }
+    const Sizes S{p, q, l, ph, m};
+    ST(ensure_buffers(ctx, q, ph));
+    ctx->log.clear();
+    ctx->log_ph = ph;
+    ctx->a_mv = ctx->b_mv = ctx->prec = ctx->inner = ctx->verify = ctx->draws = 0;
+    ctx->model_bytes = 0.0;
+    const double tau = opt.tol_mode == 1 ? tol * ctx->normF : tol;  // eq 5.1 vs Alg.1 step 12 (R8)
+    const int64_t ld = ctx->ld;
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    CK(cudaEventRecord(e0, ctx->stream));
+
+    Ctl& H = *ctx->ctl_h;
+    ST(ctl_pull(ctx));
+    const int p3_start = H.pass3_count;
+    int cur = 0;
+    trplk_status status = TRPLK_NOT_CONVERGED;
+    // ---------------- Alg.1 steps 1-2: X = B-orthonormalised rand(n, p^) (R13)
+    H.k = 0;
+    H.flags = ~0u;
+    H.t = 1;
+    H.pass3 = 0;
+    H.rho = 0.0;
+    H.xprev_col = 0;
+    for (int c = 0; c < ph; ++c) {
+        double* xc = ctx->U[cur] + ld * c;
+        launch_random(xc, ctx->n_loc, ctx->row_begin, ctx->n_global, opt.seed, 0, (uint64_t)c, ctx->stream);
+        int tries = 0;
+        for (;;) {
+            H.k = c;
+            H.flags = ~0u;
+            H.pass3 = 0;
+            ST(ctl_push(ctx));
+            CgsSpec cs{};
+            cs.x = xc;
+            cs.V = ctx->U[cur];
+            cs.kv = c;
+            cs.k_nominal = c;
+            cs.dest = ctx->U[cur];
+            cs.dest_dyn = 1;
+            cs.gate = F_CYCLE;
+            cs.clear = F_CYCLE;
+            cs.inc_k = 1;
+            // orthogonalise a copy: dest column == source column, so route through w
+            launch_copy_cols(xc, ld, ctx->w, ld, ctx->n_loc, 1, ctx->stream);
+            cs.x = ctx->w;
+            ST(cgs2(ctx, cs));
+            ST(ctl_pull(ctx));
+            if (ctx->hasB) ctx->b_mv += 2;
+            if (H.flags & F_CYCLE) break;
+            if (tries++ >= 3) {
+                ctx->err = "start block: dependent columns after 3 random replacements";
+                status = TRPLK_BREAKDOWN;
+                goto finish;
+            }
+            launch_random(xc, ctx->n_loc, ctx->row_begin, ctx->n_global, opt.seed, 2, (uint64_t)ctx->draws++,
+                          ctx->stream);
+        }
+    }
+    {
+        H.k = ph;
+        H.flags = ~0u;
+        H.pass3 = 0;
+        ST(ctl_push(ctx));
+        // W = A X (p^ matvecs), T0 = X^T W (full, symmetrised inside the eig), eig, rotate X and W
+        for (int c = 0; c < ph; ++c) {
+            ST(halo(ctx, ctx->U[cur] + ld * c));
+            SdotsArgs a = sd_base(ctx);
+            a.A = ctx->A;
+            a.x = ctx->U[cur] + ld * c;
+            a.out_mode = 1;
+            a.out = ctx->Wtmp + ld * c;
+            ST(run_sdots(ctx, a, 0));
+            ctx->a_mv++;
+        }
+        for (int c = 0; c < ph; ++c) {
+            SdotsArgs a = sd_base(ctx);
+            a.x = ctx->Wtmp + ld * c;
+            a.set1 = 3;
+            a.U = ctx->U[cur];
+            a.k1 = ph;
+            a.dest1 = D_TCOL;
+            a.tcol_fixed = c;
+            ST(run_sdots(ctx, a, ph));
+        }
+        launch_eig(ctx->ctl, ctx->T, QMAX, ctx->Yg, QMAX, ph, ph, 0, ctx->stream);
+        launch_rotate(ctx->U[cur], ld, ctx->n_loc, ctx->ctl, ph, ctx->Yg, QMAX, ph, ctx->U[1 - cur], ld, 0,
+                      ctx->stream);
+        launch_rotate(ctx->Wtmp, ld, ctx->n_loc, ctx->ctl, ph, ctx->Yg, QMAX, ph, ctx->U[cur], ld, 0, ctx->stream);
+        CK(cudaGetLastError());
+        cur = 1 - cur;  // X in U[cur], A X in U[1-cur]
+        // r = A x_1 - theta_1 B x_1 from W (no matvec), u = M r
+        ST(halo(ctx, ctx->U[cur]));
+        SdotsArgs a = sd_base(ctx);
+        a.A = ctx->A;
+        if (ctx->hasB) a.B = ctx->B;
+        a.x = ctx->U[cur];
+        a.wext = ctx->U[1 - cur];
+        a.out_mode = 4;
+        a.uout = ctx->u;
+        a.norm1 = 1;
+        a.nslot1 = N_RES2;
+        a.theta_idx = 0;
+        ST(run_sdots(ctx, a, 0));
+        if (ctx->hasB) ctx->b_mv++;
+        ctx->prec++;
+        ST(ctl_pull(ctx));
+        ctx->b_mv += ctx->hasB ? H.pass3_count - p3_start : 0;
+    }
+    {
+        int t = 1, nprev = 0, xprev = 0;
+        double rho = H.theta[0];
+        bool all_conv = false;
+        int cyc = 0;
+        int seed_tries = 0;
+        std::vector<double> theta(q);
+        int p3_prev = H.pass3_count;
+        while (cyc < opt.max_cycles) {
+            // -------- one outer cycle on the device
+            H.k = ph;
+            H.flags = ~0u;
+            H.t = t;
+            H.pass3 = 0;
+            H.rho = rho;
+            H.xprev_col = xprev;
+            ST(ctl_push(ctx));
+            ST(run_cycle(ctx, S, cur, nprev, t, xprev, opt.use_graphs != 0));
+            ST(ctl_pull(ctx));
+            if (!(H.flags & F_CYCLE)) {  // seed in span(X): inject a stream-2 random vector (R16)
+                if (seed_tries++ >= 3) {
+                    ctx->err = "seed vector dependent after 3 random replacements";
+                    status = TRPLK_BREAKDOWN;
+                    break;
+                }
+                launch_random(ctx->u, ctx->n_loc, ctx->row_begin, ctx->n_global, opt.seed, 2, (uint64_t)ctx->draws++,
+                              ctx->stream);
+                continue;
+            }
+            seed_tries = 0;
+            ++cyc;
+            const int kr = H.k_rr;
+            int appended = 0;
+            for (int jj = 0; jj < nprev; ++jj) appended += (H.flags & (F_KCOL0 << jj)) ? 1 : 0;
+            const int G = kr - ph - appended;  // inner Lanczos columns built (R16: may stop early)
+            const int ncgs = (H.flags & F_INNER) ? G - 1 : G;
+            ctx->a_mv += G + appended + 1;      // m + |X^prev| + residual
+            ctx->inner += G;
+            ctx->prec += ncgs + 1;
+            if (ctx->hasB) ctx->b_mv += 2 + 3 * ncgs + 2 * nprev + 1 + (H.pass3_count - p3_prev);
+            p3_prev = H.pass3_count;
+            if (ctx->prof_on) {  // live inner-step profile (events recorded inside the cycle)
+                const int jmid = std::max(1, std::min(m - 1, m / 2));
+                if (m >= 2 && G > jmid) {
+                    float e[3];
+                    CK(cudaEventElapsedTime(&e[0], ctx->pev[0], ctx->pev[1]));
+                    CK(cudaEventElapsedTime(&e[1], ctx->pev[1], ctx->pev[2]));
+                    CK(cudaEventElapsedTime(&e[2], ctx->pev[2], ctx->pev[3]));
+                    const double n = (double)ctx->n_loc, k = (double)(ph + jmid);
+                    const double spA = 12.0 * ctx->nnzA + 4.0 * (n + 1), spB = 12.0 * ctx->nnzB + 4.0 * (n + 1);
+                    double b1, b2;
+                    if (ctx->hasB) {
+                        b1 = spA + spB + 8.0 * n * (k + 2);
+                        b2 = 2 * (spB + 8.0 * n * (k + 1)) + 8.0 * n * (k + 2);
+                    } else {
+                        b1 = spA + 8.0 * n * (k + 2);  // A, g, U(:,1:k), w (M folded from diag)
+                        b2 = 8.0 * n * (k + 2);        // U, w, w'
+                    }
+                    const double b3 = 8.0 * n * (k + 2);  // U, w', g_{j+1}
+                    const double bb[3] = {b1, b2, b3};
+                    for (int i = 0; i < 3; ++i) {
+                        ctx->prof_ms[i] += e[i];
+                        ctx->prof_bytes[i] += bb[i];
+                    }
+                    ctx->prof_count++;
+                }
+            }
+            for (int i = 0; i < kr; ++i) theta[i] = H.theta[i];
+            double res = std::sqrt(H.nrm[N_RES2]);
+            LogRec L;
+            L.t = t;
+            L.theta_t = theta[t - 1];
+            L.res = res;
+            L.k = kr;
+            L.nprev = appended;
+            L.thetas.assign(theta.begin(), theta.begin() + ph);
+            // Alg.1 step 10 (before the RR): X^prev <- X(:, t : min(t+l-1, p)) of this cycle's basis
+            int xcol = t - 1;
+            int nnew = std::max(0, std::min(t + l - 1, p) - t + 1);
+            // steps 12-14: soft locking (R7)
+            while (res <= tau) {
+                t += 1;
+                if (nnew > 0) {
+                    xcol++;
+                    nnew--;
+                }
+                if (t > p) {
+                    all_conv = true;
+                    break;
+                }
+                H.t = t;
+                ST(ctl_push(ctx));
+                ST(residual(ctx, ctx->U[1 - cur] + ld * (t - 1), 0, t - 1, ctx->u, 0));
+                ctx->a_mv++;
+                ctx->prec++;
+                if (ctx->hasB) ctx->b_mv++;
+                ST(ctl_pull(ctx));
+                res = std::sqrt(H.nrm[N_RES2]);
+                if (opt.lock_mode == 0) break;
+            }
+            L.mv = ctx->a_mv;
+            ctx->log.push_back(L);
+            cur = 1 - cur;
+            nprev = nnew;
+            xprev = xcol;
+            if (all_conv) {
+                // final verification of all p pairs (R9)
+                int first_fail = -1;
+                for (int i = 0; i < p; ++i) {
+                    ST(residual(ctx, ctx->U[cur] + ld * i, 0, i, ctx->u2, 0));
+                    ctx->verify++;
+                    ctx->a_mv++;
+                    if (ctx->hasB) ctx->b_mv++;
+                    ST(ctl_pull(ctx));
+                    resid[i] = std::sqrt(H.nrm[N_RES2]);
+                    if (resid[i] > tau && first_fail < 0) {
+                        first_fail = i;
+                        CK(cudaMemcpyAsync(ctx->u, ctx->u2, 8 * ctx->n_loc, cudaMemcpyDeviceToDevice, ctx->stream));
+                    }
+                }
+                if (first_fail < 0) {
+                    status = TRPLK_OK;
+                    break;
+                }
+                t = first_fail + 1;
+                all_conv = false;
+            }
+            rho = theta[t - 1];
+            H.t = t;
+        }
+        if (status != TRPLK_OK) {
+            for (int i = 0; i < p; ++i) {
+                ST(residual(ctx, ctx->U[cur] + ld * i, 0, i, nullptr, 0));
+                ctx->verify++;
+                ctx->a_mv++;
+                if (ctx->hasB) ctx->b_mv++;
+                ST(ctl_pull(ctx));
+                resid[i] = std::sqrt(H.nrm[N_RES2]);
+            }
+        }
+        if (stats) stats->cycles = cyc;
+    }
+finish:
+    for (int i = 0; i < p; ++i) evals[i] = H.theta[i];
+    if (evecs) {
+        CK(cudaMemcpy2DAsync(evecs, 8 * ctx->n_loc, ctx->U[cur], 8 * ld, 8 * ctx->n_loc, p, cudaMemcpyDefault,
+                             ctx->stream));
+    }
+    CK(cudaEventRecord(e1, ctx->stream));
+    CK(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    if (stats) {
+        stats->a_matvecs = ctx->a_mv;
+        stats->b_matvecs = ctx->b_mv;
+        stats->precond_applies = ctx->prec;
+        stats->inner_steps = ctx->inner;
+        stats->verify_matvecs = ctx->verify;
+        stats->random_draws = ctx->draws;
+        stats->status = status;
+        stats->solve_seconds = ms * 1e-3;
+        stats->model_bytes = ctx->model_bytes;
+        stats->kernel_launches = ctx->launches;
+    }
+    return status;
+}
+
+trplk_status trplk_solve(trplk_ctx* ctx, int p, int max_basis, int k_plus, double tol, double* eigenvalues,
+                         double* eigenvectors, double* residual_norms, const trplk_options* opt, trplk_stats* stats) {
+    if (!ctx) return TRPLK_EINVAL;
+    enter_stream(ctx);
+    const trplk_status st =
+        solve_impl(ctx, p, max_basis, k_plus, tol, eigenvalues, eigenvectors, residual_norms, opt, stats);
+    leave_stream(ctx);
+    return st;
+}
+
+// ------------------------------------------------------------ kernel-level entry points
+static trplk_status kprep(trplk_ctx* ctx, int k) {
+    if (!ctx) return TRPLK_EINVAL;
+    if (k < 0 || k > QMAX) {
+        ctx->err = "k out of range";
+        return TRPLK_EINVAL;
+    }
+    enter_stream(ctx);
+    Ctl& H = *ctx->ctl_h;
+    H.k = k;
+    H.flags = ~0u;
+    H.t = 1;
+    H.pass3 = 0;
+    H.xprev_col = 0;
+    return ctl_push(ctx);
+}
+
+trplk_status trplk_k_spmv(trplk_ctx* ctx, int which, const double* x, double* y) {
+    ST(kprep(ctx, 0));
+    if (which == 1 && !ctx->hasB) {
+        ctx->err = "no B matrix";
+        return TRPLK_EINVAL;
+    }
+    SdotsArgs a = sd_base(ctx);
+    a.A = which == 1 ? ctx->B : ctx->A;
+    a.x = x;
+    a.out_mode = 1;
+    a.out = y;
+    ST(run_sdots(ctx, a, 0));
+    CK(cudaStreamSynchronize(ctx->stream));
+    return TRPLK_OK;
+}
+
+trplk_status trplk_k_step1(trplk_ctx* ctx, const double* U, int64_t ldu, int k, const double* g, double rho,
+                           double* w, double* tcol, double* h1, double* wnorm2) {
+    ST(kprep(ctx, k));
+    if (ldu < ctx->n_loc || k < 1) {
+        ctx->err = "bad ldu or k";
+        return TRPLK_EINVAL;
+    }
+    ctx->ctl_h->rho = rho;
+    ST(ctl_push(ctx));
+    SdotsArgs a = sd_base(ctx);
+    a.A = ctx->A;
+    a.x = g;
+    a.U = U;
+    a.ldu = ldu;
+    a.k_from_ctl = 1;
+    a.set1 = 1;
+    a.dest1 = D_TCOL;
+    a.out_mode = 2;
+    a.out = w;
+    if (ctx->hasB) {
+        a.B = ctx->B;
+    } else {
+        a.set2 = 2;
+        a.dest2 = D_H0 + 0;
+        a.norm1 = 1;
+        a.nslot1 = N_IN2;
+    }
+    ST(run_sdots(ctx, a, k));
+    if (ctx->hasB) {
+        ST(halo(ctx, w));
+        SdotsArgs b = sd_base(ctx);
+        b.A = ctx->B;
+        b.x = w;
+        b.U = U;
+        b.ldu = ldu;
+        b.k1 = k;
+        b.set1 = 1;
+        b.norm1 = 2;
+        b.dest1 = D_H0 + 0;
+        b.nslot1 = N_IN2;
+        ST(run_sdots(ctx, b, k));
+    }
+    ST(ctl_pull(ctx));
+    if (tcol) CK(cudaMemcpy(tcol, ctx->T + (size_t)(k - 1) * QMAX, 8 * (size_t)k, cudaMemcpyDeviceToHost));
+    if (h1) memcpy(h1, ctx->ctl_h->h[0], 8 * (size_t)k);
+    if (wnorm2) *wnorm2 = ctx->ctl_h->nrm[N_IN2];
+    return TRPLK_OK;
+}
+
+trplk_status trplk_k_cgs2(trplk_ctx* ctx, const double* U, int64_t ldu, int k, const double* w, double* out,
+                          double* h, double* beta, int* breakdown, int* passes) {
+    ST(kprep(ctx, k));
+    if (ldu < ctx->n_loc) {
+        ctx->err = "bad ldu";
+        return TRPLK_EINVAL;
+    }
+    ST(ctl_pull(ctx));
+    const int p3 = ctx->ctl_h->pass3_count;
+    CgsSpec c{};
+    c.x = w;
+    c.V = U;
+    c.ldv = ldu;
+    c.kv = k;
+    c.k_nominal = k;
+    c.dest = out;
+    c.dest_dyn = 0;
+    c.gate = F_CYCLE;
+    c.clear = F_CYCLE;
+    c.inc_k = 0;
+    ST(cgs2(ctx, c));
+    ST(ctl_pull(ctx));
+    const Ctl& H = *ctx->ctl_h;
+    const bool third = H.pass3_count > p3;
+    double hn = 0.0;
+    const int last = third ? 2 : 1;
+    for (int i = 0; i < k; ++i) hn += H.h[last][i] * H.h[last][i];
+    const double b2 = (third ? H.nrm[N_2SQ_EXP] : H.nrm[N_1SQ]) - hn;
+    if (beta) *beta = std::sqrt(b2 > 0 ? b2 : 0.0);
+    if (breakdown) *breakdown = (H.flags & F_CYCLE) ? 0 : 1;
+    if (passes) *passes = third ? 3 : 2;
+    if (h)
+        for (int i = 0; i < k; ++i) h[i] = H.h[0][i] + H.h[1][i] + (third ? H.h[2][i] : 0.0);
+    return TRPLK_OK;
+}
+
+trplk_status trplk_k_rotate(trplk_ctx* ctx, const double* U, int64_t ldu, int k, const double* Y, int ncol,
+                            double* X, int64_t ldx) {
+    ST(kprep(ctx, k));
+    if (k < 1 || ncol < 1 || ncol > 24 || ldu < ctx->n_loc || ldx < ctx->n_loc) {
+        ctx->err = "bad rotate sizes";
+        return TRPLK_EINVAL;
+    }
+    CK(cudaMemcpy2DAsync(ctx->Yg, 8 * QMAX, Y, 8 * (size_t)k, 8 * (size_t)k, ncol, cudaMemcpyHostToDevice,
+                         ctx->stream));
+    launch_rotate(U, ldu, ctx->n_loc, ctx->ctl, k, ctx->Yg, QMAX, ncol, X, ldx, 0, ctx->stream);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(ctx->stream));
+    return TRPLK_OK;
+}
+
+trplk_status trplk_k_sym_eig(trplk_ctx* ctx, int k, const double* T, double* theta, double* Y) {
+    ST(kprep(ctx, k));
+    if (k < 1) {
+        ctx->err = "k < 1";
+        return TRPLK_EINVAL;
+    }
+    double* Td;
+    ST(dalloc(ctx, &Td, (size_t)QMAX * QMAX));
+    CK(cudaMemcpy2DAsync(Td, 8 * QMAX, T, 8 * (size_t)k, 8 * (size_t)k, k, cudaMemcpyHostToDevice, ctx->stream));
+    launch_eig(ctx->ctl, Td, QMAX, ctx->Yg, QMAX, 0, k, 0, ctx->stream);
+    CK(cudaGetLastError());
+    ST(ctl_pull(ctx));
+    if (theta) memcpy(theta, ctx->ctl_h->theta, 8 * (size_t)k);
+    if (Y) CK(cudaMemcpy2D(Y, 8 * (size_t)k, ctx->Yg, 8 * QMAX, 8 * (size_t)k, k, cudaMemcpyDeviceToHost));
+    dev_free(ctx, Td);
+    return TRPLK_OK;
+}
+
+trplk_status trplk_k_residual(trplk_ctx* ctx, const double* x, double theta, double* r, double* u, double* rnorm2) {
+    ST(kprep(ctx, 0));
+    SdotsArgs a = sd_base(ctx);
+    a.A = ctx->A;
+    if (ctx->hasB) a.B = ctx->B;
+    a.x = x;
+    a.out_mode = 3;
+    a.out = r;
+    a.uout = u;
+    a.norm1 = 1;
+    a.nslot1 = N_RES2;
+    a.theta_idx = -2;
+    a.theta_val = theta;
+    ST(run_sdots(ctx, a, 0));
+    ST(ctl_pull(ctx));
+    if (rnorm2) *rnorm2 = ctx->ctl_h->nrm[N_RES2];
+    return TRPLK_OK;
+}
+
+trplk_status trplk_k_random(trplk_ctx* ctx, uint64_t seed, uint64_t stream, uint64_t col, double* x) {
+    if (!ctx) return TRPLK_EINVAL;
+    enter_stream(ctx);
+    launch_random(x, ctx->n_loc, ctx->row_begin, ctx->n_global, seed, stream, col, ctx->stream);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(ctx->stream));
+    return TRPLK_OK;
+}
+
+trplk_status trplk_profile(trplk_ctx* ctx, int enable) {
+    if (!ctx) return TRPLK_EINVAL;
+    if (enable && !ctx->pev[0])
+        for (auto& e : ctx->pev) CK(cudaEventCreate(&e));
+    ctx->prof_on = enable != 0;
+    for (int i = 0; i < 3; ++i) ctx->prof_ms[i] = ctx->prof_bytes[i] = 0.0;
+    ctx->prof_count = 0;
+    return TRPLK_OK;
+}
+
+trplk_status trplk_profile_read(const trplk_ctx* ctx, double* ms, double* bytes, int64_t* count) {
+    if (!ctx) return TRPLK_EINVAL;
+    for (int i = 0; i < 3; ++i) {
+        if (ms) ms[i] = ctx->prof_ms[i];
+        if (bytes) bytes[i] = ctx->prof_bytes[i];
+    }
+    if (count) *count = ctx->prof_count;
+    return TRPLK_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,143 @@
+// Internal declarations of the TRPL+K device path (kernels + engine).
+// Not part of the ABI; see include/trplk.h for the boundary.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace trplk {
+
+constexpr int QMAX = 64;           // TRPLK_MAX_BASIS
+constexpr int NV_MAX = 2 * QMAX + 4; // values of one fused reduction
+constexpr int CTA = 256;           // threads per CTA of the streaming kernels
+constexpr int WARPS = CTA / 32;
+
+// SELL-32 sparse matrix, local rows only.  Slice s holds rows [32s, 32s+32); entry j of
+// lane l sits at sptr[s] + 32*j + l; slot j=0 is the diagonal.  Padding: val 0, col = row.
+// Column ids are local: [0, nrows) owned, [nrows, nrows+nghost) ghost tail.
+struct Sell {
+    int64_t nrows = 0;
+    int64_t nslices = 0;
+    const int64_t* sptr = nullptr;
+    const int* col = nullptr;
+    const double* val = nullptr;
+};
+
+// Gate bits of Ctl::flags
+enum : unsigned {
+    F_CYCLE = 1u,      // seed of this cycle valid
+    F_INNER = 2u,      // inner Lanczos loop still running (no breakdown, R16)
+    F_KCOL0 = 4u,      // +K column j valid: F_KCOL0 << j
+};
+
+// Norm slots of Ctl::nrm
+enum { N_IN2 = 0, N_1SQ = 1, N_2SQ_EXP = 2, N_RES2 = 3, N_AUX = 4, N_SLOTS = 8 };
+
+// Destination codes of a reduction
+enum { D_NONE = 0, D_TCOL = 1, D_H0 = 2 /* D_H0 + slot */ };
+
+// Device control block.  The host writes the head (k .. xprev) before every cycle.
+struct Ctl {
+    int k;            // current basis width
+    unsigned flags;   // gate bits
+    int t;            // target, 1-based
+    int pass3;        // third CGS pass pending (R3)
+    double rho;       // shift of this cycle (Alg.1 step 15)
+    int xprev_col;    // first X^prev column in the previous cycle's buffer (Alg.1 step 10)
+    // ---- device-written from here on (not overwritten by the per-cycle host push)
+    int k_rr;         // width used by the last Rayleigh-Ritz
+    int brk;          // breakdown events (diagnostic, cumulative)
+    int pass3_count;  // third CGS passes taken (cumulative)
+    double nrm[N_SLOTS];
+    double h[4][QMAX];
+    double theta[QMAX];
+};
+
+// Arguments of the fused SpMV + preconditioner + dots kernel (K1 / K7 / Gram).
+struct SdotsArgs {
+    Sell A;            // op1 (A.nrows == 0 => z = x)
+    Sell B;            // op2 (B.nrows == 0 => s = x, i.e. B = I)
+    int64_t nrows;     // local rows
+    const double* x;   // input vector (with ghosts if multiplied)
+    int x_dyn;         // 0: x; 1: x + x_ld*(ctl->t-1+x_off); 2: x + x_ld*(ctl->xprev_col+x_off)
+    int64_t x_ld;
+    int x_off;
+    const double* wext;// RESW: r = wext - theta s
+    int out_mode;      // 0 none, 1 z, 2 PREC w=M(z-rho s), 3 RES r=z-theta s (+u=M r), 4 RESW
+    double* out;       // written if non-null (z / w / r)
+    double* uout;      // RES/RESW: u = M r if non-null
+    const double* U;   // dot block
+    int64_t ldu;
+    int set1;          // vector for dot set 1: 0 none, 1 z, 2 out, 3 x
+    int set2;          // vector for dot set 2 (same U): 0 none, 2 out
+    int k1, k2;        // #columns; <0 => ctl->k + (k+1) ... see k_from_ctl
+    int k_from_ctl;    // 1: k1 = k2-style counts = ctl->k (set2 only if set2 != 0)
+    int norm1, norm2;  // 0 none, 1 out.out, 2 x.z, 3 x.x, 4 z.z
+    int theta_idx;     // RES: theta = ctl->theta[theta_idx] (>=0) or ctl->theta[ctl->t-1] (-1)
+    double theta_val;  // used when theta_idx == -2
+    int dest1, dest2;  // D_TCOL / D_H0+slot / D_NONE
+    int tcol_fixed;    // >=0: T column index for D_TCOL (no mirror); -1: ctl->k-1, mirrored
+    int nslot1, nslot2;
+    unsigned gate;
+    int gate_pass3;
+    double sigma, mfloor;
+    int count_prec;    // reserved
+    Ctl* ctl;
+    double* T;
+    int ldT;
+    double* part;      // [NV_MAX][maxcta]
+    unsigned* counter;
+    int maxcta;
+    double* red_local; // multi-rank: local sums instead of finalize (nullptr => finalize)
+};
+
+// Arguments of the CGS update kernel (K2 / K3 / fix-up).
+struct UpdArgs {
+    int64_t nrows;
+    const double* x;   // vector being orthogonalised
+    int x_dyn;         // as SdotsArgs::x_dyn
+    int64_t x_ld;
+    int x_off;
+    const double* U;   // basis block
+    int64_t ldu;
+    int kv;            // #columns (>=0) or -1 => ctl->k
+    int hslot;         // coefficients ctl->h[hslot]
+    int mode;          // 0 NONE (y = x - U h -> out), 1 DOTS, 2 FINAL, 3 FIX
+    int dots;          // DOTS/FINAL-pass3/FIX?: compute U^T y and y.y (B = I only)
+    double* out;       // y written (NONE/DOTS, FINAL pass-3 path)
+    double* dest;      // FINAL/FIX: normalised vector destination (column base pointer)
+    int64_t dest_ld;   // dest + dest_ld * ctl->k when dest_dyn
+    int dest_dyn;
+    double* dest2;     // optional copy (+K scratch)
+    int hout;          // DOTS: coefficient slot for U^T y; norm -> ctl->nrm[N_1SQ] (or N_2SQ_EXP in FINAL)
+    int inc_k;         // FINAL/FIX: ctl->k += 1 on success
+    unsigned gate;
+    unsigned clear_on_brk;
+    Ctl* ctl;
+    double* part;
+    unsigned* counter;
+    int maxcta;
+    double* red_local;
+};
+
+// Kernel launchers (kernels.cu)
+void launch_sdots(const SdotsArgs& a, int grid, cudaStream_t s);
+void launch_upd(const UpdArgs& a, int kmax, int grid, cudaStream_t s);
+void launch_eig(Ctl* ctl, double* T, int ldT, double* Y, int ldY, int ph, int k_fixed, unsigned gate,
+                cudaStream_t s);
+void launch_rotate(const double* U, int64_t ldu, int64_t nrows, const Ctl* ctl, int k_fixed,
+                   const double* Y, int ldY, int ncol, double* X, int64_t ldx, unsigned gate,
+                   cudaStream_t s);
+void launch_random(double* x, int64_t nrows, int64_t row0, int64_t n_global, uint64_t seed,
+                   uint64_t stream, uint64_t col, cudaStream_t s);
+void launch_finalize_sdots_multi(const SdotsArgs& sd, const double* red_all, int nranks, int stride,
+                                 cudaStream_t s);
+void launch_finalize_upd_multi(const UpdArgs& up, const double* red_all, int nranks, int stride,
+                               cudaStream_t s);
+void launch_gather(const double* x, const int* idx, int64_t n, double* out, cudaStream_t s);
+void launch_copy_cols(const double* src, int64_t lds, double* dst, int64_t ldd, int64_t nrows, int ncols,
+                      cudaStream_t s);
+int sdots_grid(int64_t nrows);
+int upd_grid(int64_t nrows, int kmax);
+int kmax_bucket(int k);
+
+}  // namespace trplk

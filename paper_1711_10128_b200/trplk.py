@@ -1,0 +1,360 @@
+"""Thin Python binding of libtrplk.so (include/trplk.h, include/trplk_kernels.h).
+
+Argument marshalling only: every step of TRPL+K runs in the CUDA kernels of the
+library.  PyTorch provides device memory (the caching allocator, through the
+ABI's trplk_allocator hooks), the stream and the process group used to
+broadcast the NCCL unique id.  There is no CPU fallback: if the library is
+missing this module raises at import time.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Optional
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "lib", "libtrplk.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"libtrplk.so not built ({LIB_PATH}); run `python -m paper_1711_10128_b200.build`")
+
+_lib = ctypes.CDLL(LIB_PATH)
+
+_P = ctypes.c_void_p
+_I64 = ctypes.c_int64
+_D = ctypes.c_double
+_I = ctypes.c_int
+
+STATUS = {0: "OK", 1: "EINVAL", 2: "NOT_CONVERGED", 3: "BREAKDOWN", 4: "ECUDA", 5: "ENCCL", 6: "ENOMEM"}
+MAX_BASIS = 64
+
+_ALLOC_FN = ctypes.CFUNCTYPE(_P, ctypes.c_size_t, _P)
+_FREE_FN = ctypes.CFUNCTYPE(None, _P, _P)
+
+
+class Allocator(ctypes.Structure):
+    _fields_ = [("alloc", _ALLOC_FN), ("free", _FREE_FN), ("user", _P)]
+
+
+class Dist(ctypes.Structure):
+    _fields_ = [("rank", _I), ("nranks", _I), ("row_begin", _I64), ("row_end", _I64),
+                ("nccl_unique_id", _P)]
+
+
+class Options(ctypes.Structure):
+    _fields_ = [("seed", ctypes.c_uint64), ("max_cycles", _I), ("tol_mode", _I),
+                ("restart_size", _I), ("lock_mode", _I), ("debug_checks", _I), ("use_graphs", _I)]
+
+
+class Stats(ctypes.Structure):
+    _fields_ = [("a_matvecs", _I64), ("b_matvecs", _I64), ("precond_applies", _I64),
+                ("cycles", _I64), ("inner_steps", _I64), ("verify_matvecs", _I64),
+                ("random_draws", _I64), ("status", _I), ("solve_seconds", _D), ("model_bytes", _D),
+                ("kernel_launches", _I64)]
+
+    def as_dict(self):
+        d = {k: getattr(self, k) for k, _ in self._fields_}
+        d["status"] = STATUS.get(d["status"], d["status"])
+        return d
+
+
+def _sig(name, res, args):
+    f = getattr(_lib, name)
+    f.restype = res
+    f.argtypes = args
+    return f
+
+
+_sig("trplk_options_default", None, [ctypes.POINTER(Options)])
+_sig("trplk_nccl_unique_id", _I, [_P, ctypes.c_size_t])
+_sig("trplk_create", _I, [ctypes.POINTER(_P), _I64, _P, _P, _P, _P, _P, _P, _D,
+                          ctypes.POINTER(Dist), ctypes.POINTER(Allocator), _P])
+_sig("trplk_solve", _I, [_P, _I, _I, _I, _D, _P, _P, _P, ctypes.POINTER(Options), ctypes.POINTER(Stats)])
+_sig("trplk_get_log", _I, [_P, _I, _P, _P, _P, _P, _P, _P, _P])
+_sig("trplk_info", _I, [_P, _P, _P, _P, _P, _P, _P, _P])
+_sig("trplk_destroy", None, [_P])
+_sig("trplk_last_error", ctypes.c_char_p, [_P])
+_sig("trplk_k_spmv", _I, [_P, _I, _P, _P])
+_sig("trplk_k_step1", _I, [_P, _P, _I64, _I, _P, _D, _P, _P, _P, _P])
+_sig("trplk_k_cgs2", _I, [_P, _P, _I64, _I, _P, _P, _P, _P, _P, _P])
+_sig("trplk_k_rotate", _I, [_P, _P, _I64, _I, _P, _I, _P, _I64])
+_sig("trplk_k_sym_eig", _I, [_P, _I, _P, _P, _P])
+_sig("trplk_k_residual", _I, [_P, _P, _D, _P, _P, _P])
+_sig("trplk_k_random", _I, [_P, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64, _P])
+_sig("trplk_profile", _I, [_P, _I])
+_sig("trplk_profile_read", _I, [_P, _P, _P, ctypes.POINTER(_I64)])
+
+EXPORTED = ["trplk_options_default", "trplk_nccl_unique_id", "trplk_create", "trplk_solve",
+            "trplk_get_log", "trplk_info", "trplk_destroy", "trplk_last_error", "trplk_k_spmv",
+            "trplk_k_step1", "trplk_k_cgs2", "trplk_k_rotate", "trplk_k_sym_eig",
+            "trplk_k_residual", "trplk_k_random", "trplk_profile", "trplk_profile_read"]
+
+
+class TrplkError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = STATUS.get(status, status)
+
+
+def _ptr(a):
+    if a is None:
+        return None
+    if hasattr(a, "data_ptr"):
+        return a.data_ptr()
+    return a.ctypes.data
+
+
+def _csr_arrays(M):
+    if M is None:
+        return None, None, None
+    if hasattr(M, "rowptr"):
+        return (np.ascontiguousarray(M.rowptr, np.int64), np.ascontiguousarray(M.col, np.int64),
+                np.ascontiguousarray(M.val, np.float64))
+    M = M.tocsr()
+    M.sort_indices()
+    return (np.ascontiguousarray(M.indptr, np.int64), np.ascontiguousarray(M.indices, np.int64),
+            np.ascontiguousarray(M.data, np.float64))
+
+
+class Context:
+    """Owns a trplk_ctx*; created by trplk_create()."""
+
+    def __init__(self, handle, stream, keep):
+        self.handle = handle
+        self.stream = stream
+        self._keep = keep
+        n_local, n_ghost, rank, nranks, fro = _I64(), _I64(), _I(), _I(), _D()
+        sa, sb = _I64(), _I64()
+        _lib.trplk_info(handle, ctypes.byref(n_local), ctypes.byref(n_ghost), ctypes.byref(rank),
+                        ctypes.byref(nranks), ctypes.byref(fro), ctypes.byref(sa), ctypes.byref(sb))
+        self.n_local, self.n_ghost = n_local.value, n_ghost.value
+        self.rank, self.nranks = rank.value, nranks.value
+        self.frob_a = fro.value
+        self.sell_bytes_a, self.sell_bytes_b = sa.value, sb.value
+        self.ld = ((self.n_local + self.n_ghost + 31) // 32) * 32
+
+    def last_error(self) -> str:
+        return _lib.trplk_last_error(self.handle).decode()
+
+    def check(self, st):
+        if st != 0:
+            raise TrplkError(st, self.last_error())
+
+    def close(self):
+        if self.handle:
+            _lib.trplk_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def _torch_allocator(device_index, stream_int):
+    import torch
+
+    def _alloc(nbytes, user):
+        try:
+            return torch.cuda.caching_allocator_alloc(nbytes, device_index, stream_int)
+        except Exception:
+            return None
+
+    def _free(ptr, user):
+        torch.cuda.caching_allocator_delete(ptr)
+
+    fa, ff = _ALLOC_FN(_alloc), _FREE_FN(_free)
+    return Allocator(fa, ff, None), (fa, ff)
+
+
+def trplk_nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    st = _lib.trplk_nccl_unique_id(buf, 128)
+    if st != 0:
+        raise TrplkError(st, "ncclGetUniqueId failed")
+    return buf.raw
+
+
+def trplk_create(A, B=None, sigma: float = 0.0, n_global: Optional[int] = None, row_begin: int = 0,
+                 row_end: Optional[int] = None, group=None, stream=None, torch_alloc: bool = True) -> Context:
+    """Create a context.  A/B: inputs.CSR (this rank's rows) or scipy CSR.  For several ranks pass
+    the torch.distributed `group` and this rank's row range; rank 0's NCCL id is broadcast."""
+    import torch
+
+    ra, ca, va = _csr_arrays(A)
+    rb, cb, vb = _csr_arrays(B)
+    if n_global is None:
+        n_global = getattr(A, "n", None) or A.shape[1]
+    rows = len(ra) - 1
+    if row_end is None:
+        row_begin = getattr(A, "row_begin", row_begin)
+        row_end = row_begin + rows
+    dev = torch.cuda.current_device()
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    sptr = stream.cuda_stream
+    keep = [ra, ca, va, rb, cb, vb]
+    dist_p = None
+    if group is not None:
+        import torch.distributed as dist
+        rank, nranks = dist.get_rank(group), dist.get_world_size(group)
+        idt = torch.zeros(128, dtype=torch.uint8)
+        if rank == 0:
+            idt[:] = torch.frombuffer(bytearray(trplk_nccl_unique_id()), dtype=torch.uint8)
+        if dist.get_backend(group) == "nccl":
+            idt = idt.cuda()
+        dist.broadcast(idt, src=dist.get_global_rank(group, 0) if hasattr(dist, "get_global_rank") else 0,
+                       group=group)
+        idb = ctypes.create_string_buffer(bytes(idt.cpu().numpy().tobytes()), 128)
+        keep.append(idb)
+        d = Dist(rank, nranks, row_begin, row_end, ctypes.cast(idb, _P))
+        keep.append(d)
+        dist_p = ctypes.byref(d)
+    elif row_begin != 0 or row_end != n_global:
+        d = Dist(0, 1, row_begin, row_end, None)
+        keep.append(d)
+        dist_p = ctypes.byref(d)
+    alloc_p = None
+    if torch_alloc:
+        al, fns = _torch_allocator(dev, sptr)
+        keep += [al, fns]
+        alloc_p = ctypes.byref(al)
+    h = _P()
+    st = _lib.trplk_create(ctypes.byref(h), n_global, _ptr(ra), _ptr(ca), _ptr(va), _ptr(rb), _ptr(cb),
+                           _ptr(vb), float(sigma), dist_p, alloc_p, sptr)
+    if st != 0:
+        msg = _lib.trplk_last_error(h).decode() if h.value else "create failed"
+        if h.value:
+            _lib.trplk_destroy(h)
+        raise TrplkError(st, msg)
+    return Context(h, stream, keep)
+
+
+def make_options(**kw) -> Options:
+    o = Options()
+    _lib.trplk_options_default(ctypes.byref(o))
+    for k, v in kw.items():
+        if not hasattr(o, k):
+            raise TypeError(f"unknown option {k}")
+        setattr(o, k, v)
+    return o
+
+
+def trplk_solve(ctx: Context, p: int, max_basis: int, k_plus: int, tol: float, evecs_out=None,
+                **options):
+    """Run Algorithm 1.  Returns (eigenvalues np[p], eigenvectors torch.cuda (n_local, p)
+    column-major view, residual norms np[p], stats dict).  Raises on error statuses except
+    NOT_CONVERGED / BREAKDOWN (reported in stats['status'])."""
+    import torch
+
+    opt = make_options(**options)
+    ev = np.zeros(p)
+    rs = np.zeros(p)
+    if evecs_out is None:
+        buf = torch.empty((p, ctx.n_local), dtype=torch.float64, device="cuda")
+        evecs = buf.T
+        ptr = buf.data_ptr()
+    else:
+        evecs = evecs_out
+        ptr = _ptr(evecs_out)
+    stats = Stats()
+    st = _lib.trplk_solve(ctx.handle, p, max_basis, k_plus, tol, _ptr(ev), ptr, _ptr(rs), ctypes.byref(opt),
+                          ctypes.byref(stats))
+    if st not in (0, 2, 3):
+        ctx.check(st)
+    return ev, evecs, rs, stats.as_dict()
+
+
+def trplk_get_log(ctx: Context, cap: int = 100000, ph: Optional[int] = None):
+    cap = int(cap)
+    t = np.zeros(cap, np.int32)
+    mv = np.zeros(cap, np.int64)
+    th = np.zeros(cap)
+    rs = np.zeros(cap)
+    k = np.zeros(cap, np.int32)
+    npv = np.zeros(cap, np.int32)
+    ths = np.zeros((cap, ph)) if ph else None
+    n = _lib.trplk_get_log(ctx.handle, cap, _ptr(t), _ptr(mv), _ptr(th), _ptr(rs), _ptr(k), _ptr(npv),
+                           _ptr(ths))
+    out = {"t": t[:n], "mv": mv[:n], "theta_t": th[:n], "res": rs[:n], "k": k[:n], "nprev": npv[:n]}
+    if ph:
+        out["thetas"] = ths[:n]
+    return out
+
+
+def trplk_destroy(ctx: Context):
+    ctx.close()
+
+
+def trplk_last_error(ctx: Context) -> str:
+    return ctx.last_error()
+
+
+# ------------------------------------------------------------ kernel-level entry points
+def trplk_k_spmv(ctx, which, x, y):
+    ctx.check(_lib.trplk_k_spmv(ctx.handle, which, _ptr(x), _ptr(y)))
+
+
+def trplk_k_step1(ctx, U, ldu, k, g, rho, w):
+    tcol, h1, nrm = np.zeros(k), np.zeros(k), _D()
+    ctx.check(_lib.trplk_k_step1(ctx.handle, _ptr(U), ldu, k, _ptr(g), rho, _ptr(w), _ptr(tcol), _ptr(h1),
+                                 ctypes.byref(nrm)))
+    return tcol, h1, nrm.value
+
+
+def trplk_k_cgs2(ctx, U, ldu, k, w, out):
+    h = np.zeros(max(k, 1))
+    beta, brk, passes = _D(), _I(), _I()
+    ctx.check(_lib.trplk_k_cgs2(ctx.handle, _ptr(U), ldu, k, _ptr(w), _ptr(out), _ptr(h), ctypes.byref(beta),
+                                ctypes.byref(brk), ctypes.byref(passes)))
+    return h[:k], beta.value, bool(brk.value), passes.value
+
+
+def trplk_k_rotate(ctx, U, ldu, k, Y, ncol, X, ldx):
+    Y = np.asfortranarray(Y, np.float64)
+    ctx.check(_lib.trplk_k_rotate(ctx.handle, _ptr(U), ldu, k, _ptr(Y), ncol, _ptr(X), ldx))
+
+
+def trplk_k_sym_eig(ctx, T):
+    T = np.asfortranarray(T, np.float64)
+    k = T.shape[0]
+    th = np.zeros(k)
+    Y = np.zeros((k, k), order="F")
+    ctx.check(_lib.trplk_k_sym_eig(ctx.handle, k, _ptr(T), _ptr(th), _ptr(Y)))
+    return th, Y
+
+
+def trplk_k_residual(ctx, x, theta, r=None, u=None):
+    n2 = _D()
+    ctx.check(_lib.trplk_k_residual(ctx.handle, _ptr(x), theta, _ptr(r), _ptr(u), ctypes.byref(n2)))
+    return n2.value
+
+
+def trplk_k_random(ctx, seed, stream, col, x):
+    ctx.check(_lib.trplk_k_random(ctx.handle, seed, stream, col, _ptr(x)))
+
+
+def trplk_options_default() -> Options:
+    return make_options()
+
+
+def trplk_info(ctx: Context) -> dict:
+    return {"n_local": ctx.n_local, "n_ghost": ctx.n_ghost, "rank": ctx.rank, "nranks": ctx.nranks,
+            "frob_a": ctx.frob_a, "sell_bytes_a": ctx.sell_bytes_a, "sell_bytes_b": ctx.sell_bytes_b}
+
+
+def trplk_profile(ctx: Context, enable: bool = True):
+    ctx.check(_lib.trplk_profile(ctx.handle, 1 if enable else 0))
+
+
+def trplk_profile_read(ctx: Context) -> dict:
+    """Accumulated live inner-step profile: per kernel group (K1, K2, K3) the device ms and
+    algorithmic bytes summed over `count` cycles."""
+    ms = np.zeros(3)
+    by = np.zeros(3)
+    cnt = _I64()
+    ctx.check(_lib.trplk_profile_read(ctx.handle, _ptr(ms), _ptr(by), ctypes.byref(cnt)))
+    return {"ms": ms, "bytes": by, "count": cnt.value}

@@ -1,0 +1,176 @@
+"""Kernel-level parity: each device kernel, called through the C ABI
+(include/trplk_kernels.h), against the oracle's primitive on the same seeded
+inputs (normwise <= 1e-12 for vectors, |d - d_orc| <=
+1e-12 ||u|| ||v|| for dots).  Sizes span several CTAs/tiles and a ragged tail."""
+import numpy as np
+import pytest
+
+from gpu_util import b_orthonormal_block, need_gpu, normwise, to_dev
+
+pytestmark = pytest.mark.gpu
+
+# (config, grid N): 19^3 = 6859 and 9^3 = 729 rows leave ragged 32-row slices; C1 n = 1000
+CASES = [("C2", 19), ("C4", 9), ("C1", None), ("C2", 40)]
+
+
+@pytest.fixture(scope="module")
+def problems(gen):
+    return {f"{c}-{N}": gen.make(c, N=N) for c, N in CASES}
+
+
+def _ctx(trplk, P):
+    return trplk.trplk_create(P.A, P.B)
+
+
+@pytest.mark.parametrize("case", [f"{c}-{N}" for c, N in CASES])
+def test_spmv_A_and_B(orc, problems, case):
+    torch, trplk = need_gpu()
+    P = problems[case]
+    ctx = _ctx(trplk, P)
+    n = P.A.n
+    rng = np.random.default_rng(1)
+    x = rng.standard_normal(n)
+    y = torch.zeros(n, dtype=torch.float64, device="cuda")
+    trplk.trplk_k_spmv(ctx, 0, to_dev(torch, x), y)
+    assert normwise(y.cpu().numpy(), orc.spmv(P.A, x)) <= 1e-13
+    if P.B is not None:
+        trplk.trplk_k_spmv(ctx, 1, to_dev(torch, x), y)
+        assert normwise(y.cpu().numpy(), orc.spmv(P.B, x)) <= 1e-13
+
+
+@pytest.mark.parametrize("case", [f"{c}-{N}" for c, N in CASES])
+@pytest.mark.parametrize("k", [1, 7, 20, 48])
+def test_step1_fused_spmv_precond_dots(orc, problems, case, k):
+    """K1: z = A g, T(1:k,k) = U^T z, w = M (z - rho B g), h1 = U^T B w, ||w||_B^2."""
+    torch, trplk = need_gpu()
+    P = problems[case]
+    n = P.A.n
+    if k >= n:
+        pytest.skip("k >= n")
+    ctx = _ctx(trplk, P)
+    U = b_orthonormal_block(orc, n, k, P.B, seed=k)
+    g = U[:, k - 1]
+    rho = 0.5
+    Ud = to_dev(torch, U, ctx.ld)
+    w = torch.zeros(ctx.ld, dtype=torch.float64, device="cuda")
+    tcol, h1, wn = trplk.trplk_k_step1(ctx, Ud, ctx.ld, k, Ud[k - 1], rho, w)
+    # oracle
+    z = orc.spmv(P.A, g)
+    s = g if P.B is None else orc.spmv(P.B, g)
+    M = orc.jacobi_diag(P.A, P.B)
+    w_o = M * (z - rho * s)
+    Bw = w_o if P.B is None else orc.spmv(P.B, w_o)
+    t_o = np.array([orc.dot(U[:, i], z) for i in range(k)])
+    h_o = np.array([orc.dot(U[:, i], Bw) for i in range(k)])
+    assert normwise(w.cpu().numpy()[:n], w_o) <= 1e-12
+    nz, nBw = np.linalg.norm(z), np.linalg.norm(Bw)
+    un = np.linalg.norm(U, axis=0)
+    assert np.all(np.abs(tcol - t_o) <= 1e-12 * un * nz)
+    assert np.all(np.abs(h1 - h_o) <= 1e-12 * un * nBw)
+    assert abs(wn - orc.dot(w_o, Bw)) <= 1e-12 * np.linalg.norm(w_o) * nBw
+
+
+@pytest.mark.parametrize("case", [f"{c}-{N}" for c, N in CASES])
+@pytest.mark.parametrize("k", [0, 5, 33])
+def test_cgs2_B_inner_product(orc, problems, case, k):
+    torch, trplk = need_gpu()
+    P = problems[case]
+    n = P.A.n
+    ctx = _ctx(trplk, P)
+    U = b_orthonormal_block(orc, n, max(k, 1), P.B, seed=11)[:, :k]
+    rng = np.random.default_rng(k + 3)
+    w0 = rng.standard_normal(n)
+    Ud = to_dev(torch, U if k else np.zeros((n, 1)), ctx.ld)
+    out = torch.zeros(ctx.ld, dtype=torch.float64, device="cuda")
+    h, beta, brk, passes = trplk.trplk_k_cgs2(ctx, Ud, ctx.ld, k, to_dev(torch, w0, ctx.ld), out)
+    w_o, h_o, beta_o, brk_o, passes_o = orc.cgs2(U if k else np.zeros((n, 0)), w0, P.B)
+    assert brk == brk_o is False and passes == passes_o
+    assert abs(beta - beta_o) <= 1e-12 * beta_o
+    assert normwise(out.cpu().numpy()[:n], w_o / beta_o) <= 1e-12
+    assert np.all(np.abs(h - h_o) <= 1e-12 * np.linalg.norm(w0))
+    # dependent vector: both break down (R16)
+    if k:
+        wd = U @ rng.standard_normal(k)
+        _, _, brk, _ = trplk.trplk_k_cgs2(ctx, Ud, ctx.ld, k, to_dev(torch, wd, ctx.ld), out)
+        assert brk and orc.cgs2(U, wd, P.B)[3]
+
+
+@pytest.mark.parametrize("ncol", [1, 5, 8, 10, 20, 24])
+@pytest.mark.parametrize("k", [1, 6, 30, 64])
+def test_rotate_dmma(orc, problems, ncol, k):
+    """K5: X = U Y on fp64 DMMA vs the oracle's triple loop."""
+    torch, trplk = need_gpu()
+    P = problems["C2-19"]
+    n = P.A.n
+    ctx = _ctx(trplk, P)
+    rng = np.random.default_rng(ncol * 100 + k)
+    U = rng.standard_normal((n, k))
+    Y = rng.standard_normal((k, ncol))
+    X = torch.zeros((ncol, ctx.ld), dtype=torch.float64, device="cuda")
+    trplk.trplk_k_rotate(ctx, to_dev(torch, U, ctx.ld), ctx.ld, k, Y, ncol, X, ctx.ld)
+    Xo = orc.rotate(U, Y)
+    assert normwise(X.cpu().numpy()[:, :n].T, Xo) <= 1e-13
+
+
+@pytest.mark.parametrize("k", [1, 2, 5, 20, 31, 48, 64])
+def test_sym_eig_one_cta_jacobi(orc, problems, k):
+    torch, trplk = need_gpu()
+    ctx = _ctx(trplk, problems["C1-None"])
+    rng = np.random.default_rng(k)
+    R = rng.standard_normal((k, k))
+    T = R + R.T
+    th, Y = trplk.trplk_k_sym_eig(ctx, T)
+    th_o, Y_o = orc.sym_eig(T)
+    nT = np.linalg.norm(T, 2)
+    assert np.max(np.abs(th - th_o)) <= 1e-13 * nT
+    assert np.max(np.abs(Y.T @ Y - np.eye(k))) <= 1e-13
+    assert np.max(np.abs(T @ Y - Y * th)) <= 1e-13 * nT
+    gaps = np.min(np.abs(np.subtract.outer(th_o, th_o)) + np.eye(k) * 1e9, axis=1)
+    for c in range(k):  # unique eigenvectors (distinct eigenvalues + sign rule) agree
+        assert np.max(np.abs(Y[:, c] - Y_o[:, c])) <= 1e-13 * nT / gaps[c] + 1e-14
+
+
+def test_sym_eig_degenerate_graded(orc, problems):
+    torch, trplk = need_gpu()
+    ctx = _ctx(trplk, problems["C1-None"])
+    rng = np.random.default_rng(9)
+    Q, _ = np.linalg.qr(rng.standard_normal((24, 24)))
+    lam = np.r_[[1e-5] * 3, 3e-5, [2.0] * 6, np.linspace(0.1, 4, 14)]
+    T = (Q * lam) @ Q.T
+    T = 0.5 * (T + T.T)
+    th, Y = trplk.trplk_k_sym_eig(ctx, T)
+    assert np.max(np.abs(th - np.sort(lam))) <= 1e-14 * 8
+    assert np.max(np.abs(T @ Y - Y * th)) <= 1e-14 * 40
+
+
+@pytest.mark.parametrize("case", [f"{c}-{N}" for c, N in CASES])
+def test_residual_and_seed(orc, problems, case):
+    torch, trplk = need_gpu()
+    P = problems[case]
+    n = P.A.n
+    ctx = _ctx(trplk, P)
+    rng = np.random.default_rng(2)
+    x = rng.standard_normal(n)
+    theta = 0.37
+    r = torch.zeros(ctx.ld, dtype=torch.float64, device="cuda")
+    u = torch.zeros(ctx.ld, dtype=torch.float64, device="cuda")
+    n2 = trplk.trplk_k_residual(ctx, to_dev(torch, x, ctx.ld), theta, r, u)
+    Bx = x if P.B is None else orc.spmv(P.B, x)
+    r_o = orc.spmv(P.A, x) - theta * Bx
+    M = orc.jacobi_diag(P.A, P.B)
+    assert normwise(r.cpu().numpy()[:n], r_o) <= 1e-13
+    assert normwise(u.cpu().numpy()[:n], M * r_o) <= 1e-13
+    assert abs(n2 - orc.dot(r_o, r_o)) <= 1e-12 * orc.dot(r_o, r_o)
+
+
+def test_random_start_block_bit_exact(orc, problems):
+    """Counter-based generator (R13): device draws equal the oracle's bit for bit."""
+    torch, trplk = need_gpu()
+    P = problems["C2-19"]
+    n = P.A.n
+    ctx = _ctx(trplk, P)
+    x = torch.zeros(n, dtype=torch.float64, device="cuda")
+    for stream, col in ((0, 0), (0, 7), (2, 3)):
+        trplk.trplk_k_random(ctx, 12, stream, col, x)
+        ref = np.array([orc.u01(12, stream, col * n + i) for i in range(n)])
+        assert np.array_equal(x.cpu().numpy(), ref)

@@ -1,0 +1,189 @@
+"""End-to-end parity of trplk_solve (C ABI) with the oracle on the same seeded
+inputs (SURVEY 8(c.5) protocol): identical per-cycle trajectory (t, basis
+width, X^prev width) with theta_t within 1e-10 relative -- hence identical
+A-matvec counts -- unless the runs diverge at a near-tie; eigenvalues within
+1e-9 relative; all residuals <= tol; eigenvector subspace angles <= 1e-6 at
+tol_parity, grouped by clusters."""
+import numpy as np
+import pytest
+import scipy.linalg as sla
+
+from gpu_util import need_gpu
+
+pytestmark = pytest.mark.gpu
+
+
+def gpu_solve(trplk, P, tol=None, **opt):
+    ctx = trplk.trplk_create(P.A, P.B, P.sigma)
+    ev, X, rs, st = trplk.trplk_solve(ctx, P.p, P.q, P.l, P.tol if tol is None else tol, **opt)
+    ph = opt.get("restart_size", 0) or P.p
+    log = trplk.trplk_get_log(ctx, ph=ph)
+    Xh = X.cpu().numpy().copy()
+    ctx.close()
+    return {"eigenvalues": ev, "X": Xh, "residuals": rs, "stats": st, "log": log}
+
+
+def oracle_solve(orc, P, tol=None, **opt):
+    return orc.solve(P.A, P.B, P.p, P.q, P.l, P.tol if tol is None else tol, P.sigma, **opt)
+
+
+def norm_inf(P):
+    """max row sum |A| (>= ||A||_2 for symmetric A): scale of rounding errors in Ritz values."""
+    A = P.A.to_scipy()
+    return float(abs(A).sum(axis=1).max())
+
+
+def first_divergence(g, o, nA):
+    """First cycle where (t, width, X^prev width) differ or theta_t differs by more than
+    1e-10 relative + 1e-13 ||A|| (RR is backward stable: absolute errors O(eps ||A||))."""
+    lg, lo = g["log"], o["log"]
+    n = min(len(lg["t"]), len(lo["t"]))
+    for c in range(n):
+        same = (lg["t"][c] == lo["t"][c] and lg["k"][c] == lo["k"][c] and lg["nprev"][c] == lo["nprev"][c]
+                and abs(lg["theta_t"][c] - lo["theta_t"][c]) <= 1e-10 * abs(lo["theta_t"][c]) + 1e-13 * nA)
+        if not same:
+            return c
+    return None if len(lg["t"]) == len(lo["t"]) else n
+
+
+def near_tie(o, c, tol):
+    """Divergence allowed only at a near-tie: Ritz values within 1e-10 rel, or ||r_t|| ~ tau."""
+    th = o["log"]["thetas"][c]
+    close = np.any(np.abs(np.diff(th)) <= 1e-10 * np.abs(th[1:]))
+    res = o["log"]["res"][c]
+    return close or abs(res - tol) <= 1e-2 * tol
+
+
+def subspace_angles_grouped(X, Y, B, lam, tolp):
+    """Max B-principal angle between X and Y over groups of clustered eigenvalues."""
+    groups, cur = [], [0]
+    for i in range(1, len(lam)):
+        if lam[i] - lam[i - 1] < 10 * tolp / 1e-6:
+            cur.append(i)
+        else:
+            groups.append(cur)
+            cur = [i]
+    groups.append(cur)
+    worst = 0.0
+    for g in groups:
+        BY = Y[:, g] if B is None else B @ Y[:, g]
+        s = np.linalg.svd(X[:, g].T @ BY, compute_uv=False)
+        worst = max(worst, float(np.arccos(np.clip(np.min(s), -1, 1))))
+    return worst, groups
+
+
+def check_parity(g, o, P, allow_tie_divergence=False):
+    assert g["stats"]["status"] == o["status"] == "OK"
+    assert np.all(g["residuals"] <= P.tol) and np.all(o["residuals"] <= P.tol)
+    c = first_divergence(g, o, norm_inf(P))
+    if c is None:
+        assert g["stats"]["a_matvecs"] == o["a_matvecs"]
+        assert g["stats"]["cycles"] == o["cycles"]
+    else:
+        lg, lo = g["log"], o["log"]
+        info = {k_: (lg[k_][c], lo[k_][c]) for k_ in ("t", "k", "nprev", "theta_t", "res")}
+        assert allow_tie_divergence and near_tie(o, c, P.tol), f"trajectory diverged at cycle {c}: {info}"
+    rel = np.abs(g["eigenvalues"] - o["eigenvalues"]) / np.abs(o["eigenvalues"])
+    assert np.max(rel) <= 1e-9, rel
+    return c
+
+
+@pytest.mark.parametrize("name,N", [("C1", None), ("C2", 12), ("C2", 24), ("C4", 8), ("C4", 12)])
+def test_solve_parity_small(orc, gen, name, N):
+    torch, trplk = need_gpu()
+    P = gen.make(name, N=N)
+    g = gpu_solve(trplk, P)
+    o = oracle_solve(orc, P)
+    check_parity(g, o, P)
+    # B-orthonormal eigenvectors
+    X = g["X"]
+    BX = X if P.B is None else P.B.to_scipy() @ X
+    assert np.max(np.abs(X.T @ BX - np.eye(P.p))) <= 1e-12
+
+
+def test_solve_clustered_C3_small(orc, gen):
+    """Exact multiplicities (C3 shape, 12^3): several results are correct -- compare complete
+    clusters' subspaces; trajectory may only diverge at a near-tie."""
+    torch, trplk = need_gpu()
+    P = gen.make("C3", N=12, p=10, q=24, l=3)
+    g = gpu_solve(trplk, P)
+    o = oracle_solve(orc, P)
+    check_parity(g, o, P, allow_tie_divergence=True)
+    c = 2 - 2 * np.cos(np.arange(1, 13) * np.pi / 13)
+    ref = np.sort(np.add.outer(np.add.outer(c, c), c).ravel())[:10]
+    assert np.max(np.abs(g["eigenvalues"] - ref) / ref) <= 1e-9
+
+
+@pytest.mark.parametrize("name,N,tolp", [("C1", None, 1e-12), ("C2", 16, 1e-11), ("C4", 8, 1e-11)])
+def test_eigenvector_angles_tol_parity(orc, gen, name, N, tolp):
+    torch, trplk = need_gpu()
+    P = gen.make(name, N=N)
+    g = gpu_solve(trplk, P, tol=tolp)
+    o = oracle_solve(orc, P, tol=tolp)
+    assert g["stats"]["status"] == "OK" and o["status"] == "OK"
+    B = None if P.B is None else P.B.to_scipy()
+    ang, groups = subspace_angles_grouped(g["X"], o["eigenvectors"], B, o["eigenvalues"], tolp)
+    assert ang <= 1e-6, (ang, groups)
+
+
+def test_graph_and_eager_bitwise_equal_and_deterministic(gen):
+    torch, trplk = need_gpu()
+    P = gen.make("C2", N=20)
+    a = gpu_solve(trplk, P, use_graphs=1)
+    b = gpu_solve(trplk, P, use_graphs=0)
+    c = gpu_solve(trplk, P, use_graphs=1)
+    assert np.array_equal(a["eigenvalues"], b["eigenvalues"])
+    assert np.array_equal(a["eigenvalues"], c["eigenvalues"])
+    assert np.array_equal(a["X"], c["X"])
+    assert a["stats"]["a_matvecs"] == b["stats"]["a_matvecs"]
+
+
+def test_matvec_accounting_and_interlacing(gen):
+    torch, trplk = need_gpu()
+    P = gen.make("C2", N=10, p=4, q=12, l=2)
+    g = gpu_solve(trplk, P, tol=1e-10)
+    lg = g["log"]
+    ph, m = 4, 12 - 4 - 2
+    mv = np.r_[ph, lg["mv"]]
+    tt = lg["t"]
+    tnext = np.r_[tt[1:], ph + 1]
+    for c in range(len(tt)):
+        locks = tnext[c] - tt[c]
+        extra = locks if tnext[c] <= ph else locks - 1
+        assert mv[c + 1] - mv[c] == m + lg["nprev"][c] + 1 + extra
+    th = lg["thetas"]
+    assert np.all(th[1:] <= th[:-1] + 1e-14 * np.abs(th[:-1]) + 1e-14)
+
+
+def test_options_restart_size_lock_while_frob(orc, gen):
+    torch, trplk = need_gpu()
+    P = gen.make("C2", N=12)
+    for opt in ({"restart_size": 12}, {"lock_mode": 1}, {"tol_mode": 1}):
+        tol = 1e-12 if opt.get("tol_mode") else P.tol
+        g = gpu_solve(trplk, P, tol=tol, **opt)
+        o = orc.solve(P.A, None, P.p, P.q, P.l, tol, **opt)
+        assert g["stats"]["status"] == "OK"
+        assert g["stats"]["a_matvecs"] == o["a_matvecs"], opt
+        assert np.max(np.abs(g["eigenvalues"] - o["eigenvalues"]) / o["eigenvalues"]) <= 1e-9
+
+
+def test_not_converged_and_einval(gen):
+    torch, trplk = need_gpu()
+    P = gen.make("C2", N=10)
+    ctx = trplk.trplk_create(P.A)
+    ev, X, rs, st = trplk.trplk_solve(ctx, 4, 12, 2, 1e-13, max_cycles=2)
+    assert st["status"] == "NOT_CONVERGED" and st["cycles"] == 2 and np.all(np.isfinite(ev))
+    with pytest.raises(trplk.TrplkError):
+        trplk.trplk_solve(ctx, 4, 6, 2, 1e-8)  # m = 0
+    with pytest.raises(trplk.TrplkError):
+        trplk.trplk_solve(ctx, 4, 65, 2, 1e-8)  # q > TRPLK_MAX_BASIS
+    ctx.close()
+
+
+def test_full_C2_parity(orc, gen):
+    """BASELINE configs[1] at full size, bench launch configuration."""
+    torch, trplk = need_gpu()
+    P = gen.make("C2")
+    g = gpu_solve(trplk, P)
+    o = oracle_solve(orc, P, want_vectors=False)
+    check_parity(g, o, P, allow_tie_divergence=True)
