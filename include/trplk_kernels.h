@@ -51,6 +51,16 @@ trplk_status trplk_k_residual(trplk_ctx* ctx, const double* x, double theta, dou
 /* x[i] = U01(seed, stream, col*n_global + global_row(i)) for the local rows (reading R13). */
 trplk_status trplk_k_random(trplk_ctx* ctx, uint64_t seed, uint64_t stream, uint64_t col, double* x);
 
+/* Host-only halo planning of a row slab (no device work; the code trplk_create runs).
+ *   ghosts_out[cap]  sorted unique global column ids outside [row_begin,row_end) referenced by the
+ *                    local rows of A (and B, may be NULL); the ghost tail of every local vector
+ *   owners_out[cap]  owner rank of each ghost given ranges[2*nranks] = {begin_r, end_r} (rank order)
+ *   *n_ghost         count (set even when cap is too small, which returns EINVAL)
+ * Local column id of a global column c: c - row_begin if owned, else n_local + index in ghosts_out. */
+trplk_status trplk_plan_ghosts(int64_t row_begin, int64_t row_end, const int64_t* a_rowptr, const int64_t* a_col,
+                               const int64_t* b_rowptr, const int64_t* b_col, const int64_t* ranges, int nranks,
+                               int64_t* ghosts_out, int* owners_out, int64_t cap, int64_t* n_ghost);
+
 /* Live profile of the inner step (measurement): while enabled, every
  * outer cycle records CUDA events around the three kernel groups of its middle inner step
  *   [0] K1  fused SpMV + preconditioner + T-column/h1 dots

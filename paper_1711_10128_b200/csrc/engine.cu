@@ -71,12 +71,11 @@ struct trplk_ctx {
     int q_alloc = 0, ph_alloc = 0;
     double* U[2] = {nullptr, nullptr};
     double *w = nullptr, *w1 = nullptr, *w2 = nullptr, *u = nullptr, *u2 = nullptr, *xk = nullptr;
-    double *T = nullptr, *Yg = nullptr, *part = nullptr, *red_local = nullptr, *red_all = nullptr;
+    double *T = nullptr, *Yg = nullptr, *part = nullptr, *gpart = nullptr, *red_local = nullptr, *red_all = nullptr;
     double* Wtmp = nullptr;
     unsigned* counter = nullptr;
     Ctl* ctl = nullptr;
     Ctl* ctl_h = nullptr;
-    int maxcta = 0;
     std::string err;
     std::vector<LogRec> log;
     int log_ph = 0;
@@ -258,6 +257,112 @@ trplk_status upload_sell(trplk_ctx* ctx, const HostSell& hs, Sell& S, int64_t& b
     return TRPLK_OK;
 }
 
+// Sorted unique global column ids outside [rb, re) referenced by the local rows of A (and B).
+std::vector<int64_t> find_ghosts(int64_t n_loc, int64_t rb, int64_t re, const int64_t* a_rp, const int64_t* a_ci,
+                                 const int64_t* b_rp, const int64_t* b_ci) {
+    std::vector<int64_t> ghosts;
+    for (int m = 0; m < 2; ++m) {
+        const int64_t* rp = m == 0 ? a_rp : b_rp;
+        const int64_t* ci = m == 0 ? a_ci : b_ci;
+        if (!rp) continue;
+        const int64_t nnz = rp[n_loc] - rp[0];
+        for (int64_t p = 0; p < nnz; ++p)
+            if (ci[p] < rb || ci[p] >= re) ghosts.push_back(ci[p]);
+    }
+    std::sort(ghosts.begin(), ghosts.end());
+    ghosts.erase(std::unique(ghosts.begin(), ghosts.end()), ghosts.end());
+    return ghosts;
+}
+
+// Owner rank of each ghost id given all ranks' [begin, end) row ranges (rank order).
+std::vector<int> ghost_owners(const std::vector<int64_t>& ghosts, const int64_t* ranges, int nranks) {
+    std::vector<int> own(ghosts.size(), 0);
+    for (size_t gi = 0; gi < ghosts.size(); ++gi) {
+        int owner = 0;
+        while (owner < nranks - 1 && ghosts[gi] >= ranges[2 * owner + 1]) ++owner;
+        own[gi] = owner;
+    }
+    return own;
+}
+
+// DIA conversion (values only; column = row + offset computed in the kernel).  Used when the
+// local rows hold at most DIA_MAX distinct offsets col - row, the padded diagonals store at
+// most 1.25x the entries, and the ghost columns are the two contiguous ranges just below
+// and above the owned rows (z-slab partitions of stencils).  ok = false otherwise.
+trplk_status try_dia(trplk_ctx* ctx, const int64_t* rp, const int64_t* ci, const double* va,
+                     const std::vector<int64_t>& ghosts, Sell& S, int64_t& bytes, bool& ok) {
+    ok = false;
+    const int64_t n = ctx->n_loc, rb = ctx->row_begin, re = ctx->row_end, base = rp[0];
+    int64_t glo = 0;
+    for (int64_t g : ghosts) glo += g < rb ? 1 : 0;
+    const int64_t ghi = (int64_t)ghosts.size() - glo;
+    if (glo > 0 && (ghosts[0] != rb - glo || ghosts[glo - 1] != rb - 1)) return TRPLK_OK;
+    if (ghi > 0 && (ghosts[glo] != re || ghosts.back() != re + ghi - 1)) return TRPLK_OK;
+    // distinct offsets (per-thread sets, merged)
+    std::vector<int64_t> offs;
+    bool too_many = false;
+#pragma omp parallel
+    {
+        std::vector<int64_t> loc;
+        bool over = false;
+#pragma omp for schedule(static)
+        for (int64_t r = 0; r < n; ++r) {
+            if (over) continue;
+            for (int64_t p = rp[r] - base; p < rp[r + 1] - base; ++p) {
+                const int64_t off = ci[p] - (rb + r);
+                if (std::find(loc.begin(), loc.end(), off) == loc.end()) {
+                    loc.push_back(off);
+                    if ((int)loc.size() > DIA_MAX) { over = true; break; }
+                }
+            }
+        }
+#pragma omp critical
+        {
+            too_many |= over;
+            for (int64_t o : loc)
+                if (std::find(offs.begin(), offs.end(), o) == offs.end()) offs.push_back(o);
+        }
+    }
+    if (too_many) return TRPLK_OK;
+    if (std::find(offs.begin(), offs.end(), (int64_t)0) == offs.end()) offs.push_back(0);
+    if ((int)offs.size() > DIA_MAX) return TRPLK_OK;
+    std::sort(offs.begin(), offs.end());
+    const int nd = (int)offs.size();
+    const int64_t nnz = rp[n] - base;
+    if ((double)n * nd > 1.25 * (double)nnz + 64.0 * nd) return TRPLK_OK;
+    for (int64_t o : offs)
+        if (o > INT32_MAX || o < INT32_MIN) return TRPLK_OK;
+    const int64_t ldv = ((n + 31) / 32) * 32;
+    std::vector<double> dv((size_t)nd * ldv, 0.0);
+#pragma omp parallel for schedule(static)
+    for (int64_t r = 0; r < n; ++r)
+        for (int64_t p = rp[r] - base; p < rp[r + 1] - base; ++p) {
+            const int64_t off = ci[p] - (rb + r);
+            const int d = (int)(std::lower_bound(offs.begin(), offs.end(), off) - offs.begin());
+            dv[(size_t)d * ldv + r] = va[p];
+        }
+    double* dd;
+    ST(dalloc(ctx, &dd, dv.size()));
+    CK(cudaMemcpyAsync(dd, dv.data(), dv.size() * 8, cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    S = Sell();
+    S.fmt = 1;
+    S.nrows = n;
+    S.nslices = (n + 31) / 32;
+    S.ndiag = nd;
+    S.ldv = ldv;
+    S.glo = glo;
+    S.nghost = (int64_t)ghosts.size();
+    S.dval = dd;
+    for (int d = 0; d < nd; ++d) {
+        S.offs[d] = (int)offs[d];
+        if (offs[d] == 0) S.diag_slot = d;
+    }
+    bytes = (int64_t)nd * n * 8;
+    ok = true;
+    return TRPLK_OK;
+}
+
 trplk_status validate_csr(trplk_ctx* ctx, const char* name, const int64_t* rp, const int64_t* ci) {
     if (!rp || !ci) {
         ctx->err = std::string(name) + ": NULL CSR array";
@@ -323,8 +428,9 @@ SdotsArgs sd_base(trplk_ctx* ctx) {
     a.T = ctx->T;
     a.ldT = QMAX;
     a.part = ctx->part;
+    a.gpart = ctx->gpart;
     a.counter = ctx->counter;
-    a.maxcta = ctx->maxcta;
+    a.maxcta = MAXCTA;
     a.ldu = ctx->ld;
     a.x_ld = ctx->ld;
     return a;
@@ -337,8 +443,9 @@ UpdArgs up_base(trplk_ctx* ctx) {
     a.x_ld = ctx->ld;
     a.ctl = ctx->ctl;
     a.part = ctx->part;
+    a.gpart = ctx->gpart;
     a.counter = ctx->counter;
-    a.maxcta = ctx->maxcta;
+    a.maxcta = MAXCTA;
     a.dest_ld = ctx->ld;
     return a;
 }
@@ -349,8 +456,10 @@ double mat_bytes(trplk_ctx* ctx, bool b) {
     return (double)(b ? ctx->sellB_bytes : ctx->sellA_bytes);
 }
 
-trplk_status run_sdots(trplk_ctx* ctx, SdotsArgs a, int kbytes_cols) {
-    const int grid = sdots_grid(ctx->n_loc);
+// kbytes_cols: nominal number of basis columns the launch reads (>= the device-side k); it
+// selects the register-row template and feeds the byte model.
+trplk_status run_sdots(trplk_ctx* ctx, SdotsArgs a, int kbytes_cols, bool count_bytes = true) {
+    const int kmax = (a.set1 || a.set2) ? kmax_bucket(std::max(kbytes_cols, 1)) : 0;
     // algorithmic bytes of this launch (DESIGN.md byte model)
     double by = 0.0;
     if (a.A.nrows && a.out_mode != 4) by += mat_bytes(ctx, false) + vec_bytes(ctx);
@@ -359,16 +468,16 @@ trplk_status run_sdots(trplk_ctx* ctx, SdotsArgs a, int kbytes_cols) {
     if (a.out) by += vec_bytes(ctx);
     if (a.uout) by += vec_bytes(ctx);
     if (a.wext) by += vec_bytes(ctx);
-    by += vec_bytes(ctx) * kbytes_cols;
-    ctx->model_bytes += by;
+    if (a.set1 || a.set2) by += vec_bytes(ctx) * kbytes_cols;
+    if (count_bytes) ctx->model_bytes += by;
     ctx->launches += ctx->nranks > 1 ? 2 : 1;
     if (ctx->nranks > 1) {
         a.red_local = ctx->red_local;
-        launch_sdots(a, grid, ctx->stream);
+        launch_sdots(a, kmax, ctx->stream);
         NK(ncclAllGather(ctx->red_local, ctx->red_all, NV_MAX, ncclDouble, ctx->comm, ctx->stream));
         launch_finalize_sdots_multi(a, ctx->red_all, ctx->nranks, NV_MAX, ctx->stream);
     } else {
-        launch_sdots(a, grid, ctx->stream);
+        launch_sdots(a, kmax, ctx->stream);
     }
     CK(cudaGetLastError());
     return TRPLK_OK;
@@ -376,17 +485,16 @@ trplk_status run_sdots(trplk_ctx* ctx, SdotsArgs a, int kbytes_cols) {
 
 trplk_status run_upd(trplk_ctx* ctx, UpdArgs a, int k_nominal) {
     const int kmax = kmax_bucket(std::max(k_nominal, 1));
-    const int grid = upd_grid(ctx->n_loc, kmax);
     if (a.mode != 3) ctx->model_bytes += vec_bytes(ctx) * (k_nominal + 2);
     const bool dots = a.dots && (a.mode == 1 || a.mode == 2);
     ctx->launches += (ctx->nranks > 1 && dots) ? 2 : 1;
     if (ctx->nranks > 1 && dots) {
         a.red_local = ctx->red_local;
-        launch_upd(a, kmax, grid, ctx->stream);
+        launch_upd(a, kmax, ctx->stream);
         NK(ncclAllGather(ctx->red_local, ctx->red_all, NV_MAX, ncclDouble, ctx->comm, ctx->stream));
         launch_finalize_upd_multi(a, ctx->red_all, ctx->nranks, NV_MAX, ctx->stream);
     } else {
-        launch_upd(a, kmax, grid, ctx->stream);
+        launch_upd(a, kmax, ctx->stream);
     }
     CK(cudaGetLastError());
     return TRPLK_OK;
@@ -471,7 +579,7 @@ trplk_status cgs2(trplk_ctx* ctx, const CgsSpec& c) {
         ST(run_sdots(ctx, a, kn));
     }
     // final: y = w1 - V h1, beta from Pythagoras; pass 3 into w2 if the norm dropped > 1/sqrt2
-    if (c.mark_final) CK(cudaEventRecord(c.mark_final, ctx->stream));
+    if (c.mark_final) CK(cudaEventRecordWithFlags(c.mark_final, ctx->stream, cudaEventRecordExternal));
     {
         UpdArgs u = up_base(ctx);
         u.x = ctx->w1;
@@ -506,9 +614,7 @@ trplk_status cgs2(trplk_ctx* ctx, const CgsSpec& c) {
         a.nslot1 = N_2SQ_EXP;
         a.gate = c.gate;
         a.gate_pass3 = 1;
-        const double mb = ctx->model_bytes;
-        ST(run_sdots(ctx, a, 0));
-        ctx->model_bytes = mb;  // rare path, not in the byte model
+        ST(run_sdots(ctx, a, kn, false));  // rare path, not in the byte model
     }
     {
         UpdArgs u = up_base(ctx);
@@ -626,9 +732,9 @@ trplk_status issue_cycle(trplk_ctx* ctx, const Sizes& S, int cur, int nprev, int
                 a.norm1 = 1;  // ||w||^2
                 a.nslot1 = N_IN2;
             }
-            if (prof) CK(cudaEventRecord(ctx->pev[0], ctx->stream));
+            if (prof) CK(cudaEventRecordWithFlags(ctx->pev[0], ctx->stream, cudaEventRecordExternal));
             ST(run_sdots(ctx, a, k));
-            if (prof) CK(cudaEventRecord(ctx->pev[1], ctx->stream));
+            if (prof) CK(cudaEventRecordWithFlags(ctx->pev[1], ctx->stream, cudaEventRecordExternal));
             CgsSpec c{};
             if (prof) c.mark_final = ctx->pev[2];
             c.x = ctx->w;
@@ -642,7 +748,7 @@ trplk_status issue_cycle(trplk_ctx* ctx, const Sizes& S, int cur, int nprev, int
             c.clear = F_INNER;
             c.inc_k = 1;
             ST(cgs2(ctx, c));
-            if (prof) CK(cudaEventRecord(ctx->pev[3], ctx->stream));
+            if (prof) CK(cudaEventRecordWithFlags(ctx->pev[3], ctx->stream, cudaEventRecordExternal));
         } else {
             ST(run_sdots(ctx, a, k));
         }
@@ -804,19 +910,8 @@ static trplk_status create_impl(trplk_ctx* ctx, int64_t n_global, const int64_t*
         NK(ncclCommInitRank(&ctx->comm, ctx->nranks, id, ctx->rank));
     }
     // ghost columns (global ids outside the owned range), sorted
-    std::vector<int64_t> ghosts;
-    {
-        const int64_t nnz_a = a_rowptr[ctx->n_loc] - a_rowptr[0];
-        for (int64_t p = 0; p < nnz_a; ++p)
-            if (a_col[p] < ctx->row_begin || a_col[p] >= ctx->row_end) ghosts.push_back(a_col[p]);
-        if (ctx->hasB) {
-            const int64_t nnz_b = b_rowptr[ctx->n_loc] - b_rowptr[0];
-            for (int64_t p = 0; p < nnz_b; ++p)
-                if (b_col[p] < ctx->row_begin || b_col[p] >= ctx->row_end) ghosts.push_back(b_col[p]);
-        }
-        std::sort(ghosts.begin(), ghosts.end());
-        ghosts.erase(std::unique(ghosts.begin(), ghosts.end()), ghosts.end());
-    }
+    const std::vector<int64_t> ghosts =
+        find_ghosts(ctx->n_loc, ctx->row_begin, ctx->row_end, a_rowptr, a_col, b_rowptr, b_col);
     ctx->n_ghost = (int64_t)ghosts.size();
     if (ctx->n_loc + ctx->n_ghost >= (int64_t)1 << 31) {
         ctx->err = "local rows + ghosts exceed int32 column ids";
@@ -834,23 +929,25 @@ static trplk_status create_impl(trplk_ctx* ctx, int64_t n_global, const int64_t*
             if (a_col[p] == ctx->row_begin + r) amax = std::max(amax, std::fabs(a_val[p]));
         }
 
-    HostSell hs;
-    ST(build_sell(ctx, a_rowptr, a_col, a_val, ghosts, hs));
-    ST(upload_sell(ctx, hs, ctx->A, ctx->sellA_bytes));
+    // device format: DIA when the matrix is a few full diagonals (stencils), else SELL-32
+    const bool force_sell = getenv("TRPLK_FORCE_SELL") != nullptr;
+    bool diaA = false, diaB = false;
+    if (!force_sell) ST(try_dia(ctx, a_rowptr, a_col, a_val, ghosts, ctx->A, ctx->sellA_bytes, diaA));
+    if (!diaA) {
+        HostSell hs;
+        ST(build_sell(ctx, a_rowptr, a_col, a_val, ghosts, hs));
+        ST(upload_sell(ctx, hs, ctx->A, ctx->sellA_bytes));
+    }
     if (ctx->hasB) {
-        HostSell hb;
-        ST(build_sell(ctx, b_rowptr, b_col, b_val, ghosts, hb));
-        ST(upload_sell(ctx, hb, ctx->B, ctx->sellB_bytes));
+        if (!force_sell) ST(try_dia(ctx, b_rowptr, b_col, b_val, ghosts, ctx->B, ctx->sellB_bytes, diaB));
+        if (!diaB) {
+            HostSell hb;
+            ST(build_sell(ctx, b_rowptr, b_col, b_val, ghosts, hb));
+            ST(upload_sell(ctx, hb, ctx->B, ctx->sellB_bytes));
+        }
     }
 
     // fixed device buffers
-    ctx->maxcta = 148 * 8;
-    {
-        int dev = 0, nsm = 148;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-        ctx->maxcta = std::max(nsm * 8, 64);
-    }
     const size_t ld = (size_t)ctx->ld;
     ST(dalloc(ctx, &ctx->w, ld));
     ST(dalloc(ctx, &ctx->w1, ld));
@@ -860,12 +957,13 @@ static trplk_status create_impl(trplk_ctx* ctx, int64_t n_global, const int64_t*
     ST(dalloc(ctx, &ctx->xk, ld));
     ST(dalloc(ctx, &ctx->T, (size_t)QMAX * QMAX));
     ST(dalloc(ctx, &ctx->Yg, (size_t)QMAX * QMAX));
-    ST(dalloc(ctx, &ctx->part, (size_t)NV_MAX * ctx->maxcta));
+    ST(dalloc(ctx, &ctx->part, (size_t)NV_MAX * MAXCTA));
+    ST(dalloc(ctx, &ctx->gpart, (size_t)NV_MAX * MAXG));
     ST(dalloc(ctx, &ctx->red_local, (size_t)NV_MAX));
     ST(dalloc(ctx, &ctx->red_all, (size_t)NV_MAX * ctx->nranks));
-    ST(dalloc(ctx, &ctx->counter, 16));
+    ST(dalloc(ctx, &ctx->counter, NCOUNTERS));
     ST(dalloc(ctx, &ctx->ctl, 1));
-    CK(cudaMemsetAsync(ctx->counter, 0, 64, ctx->stream));
+    CK(cudaMemsetAsync(ctx->counter, 0, sizeof(unsigned) * NCOUNTERS, ctx->stream));
     CK(cudaMemsetAsync(ctx->ctl, 0, sizeof(Ctl), ctx->stream));
     CK(cudaMemsetAsync(ctx->T, 0, sizeof(double) * QMAX * QMAX, ctx->stream));
     for (double* v : {ctx->w, ctx->w1, ctx->w2, ctx->u, ctx->u2, ctx->xk})
@@ -906,9 +1004,9 @@ static trplk_status create_impl(trplk_ctx* ctx, int64_t n_global, const int64_t*
         }
         // recv plan: ghosts grouped by owner (contiguous, since sorted)
         std::vector<int64_t> need_cnt(ctx->nranks, 0), need_off(ctx->nranks, 0);
+        const std::vector<int> owners = ghost_owners(ghosts, rg.data(), ctx->nranks);
         for (size_t gi = 0; gi < ghosts.size(); ++gi) {
-            int owner = 0;
-            while (owner < ctx->nranks - 1 && ghosts[gi] >= rg[2 * owner + 1]) ++owner;
+            const int owner = owners[gi];
             if (need_cnt[owner] == 0) need_off[owner] = (int64_t)gi;
             need_cnt[owner]++;
         }
@@ -1223,7 +1321,8 @@ static trplk_status solve_impl(trplk_ctx* ctx, int p, int q, int l, double tol, 
                     CK(cudaEventElapsedTime(&e[1], ctx->pev[1], ctx->pev[2]));
                     CK(cudaEventElapsedTime(&e[2], ctx->pev[2], ctx->pev[3]));
                     const double n = (double)ctx->n_loc, k = (double)(ph + jmid);
-                    const double spA = 12.0 * ctx->nnzA + 4.0 * (n + 1), spB = 12.0 * ctx->nnzB + 4.0 * (n + 1);
+                    // matrix bytes of the device format (DIA: 8 ndiag n; SELL: 12 per slot + slice ptrs)
+                    const double spA = (double)ctx->sellA_bytes, spB = (double)ctx->sellB_bytes;
                     double b1, b2;
                     if (ctx->hasB) {
                         b1 = spA + spB + 8.0 * n * (k + 2);
@@ -1529,6 +1628,22 @@ trplk_status trplk_k_random(trplk_ctx* ctx, uint64_t seed, uint64_t stream, uint
     launch_random(x, ctx->n_loc, ctx->row_begin, ctx->n_global, seed, stream, col, ctx->stream);
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(ctx->stream));
+    return TRPLK_OK;
+}
+
+trplk_status trplk_plan_ghosts(int64_t row_begin, int64_t row_end, const int64_t* a_rowptr, const int64_t* a_col,
+                               const int64_t* b_rowptr, const int64_t* b_col, const int64_t* ranges, int nranks,
+                               int64_t* ghosts_out, int* owners_out, int64_t cap, int64_t* n_ghost) {
+    if (!a_rowptr || !a_col || row_end < row_begin || !n_ghost || nranks < 1) return TRPLK_EINVAL;
+    const std::vector<int64_t> g =
+        find_ghosts(row_end - row_begin, row_begin, row_end, a_rowptr, a_col, b_rowptr, b_col);
+    *n_ghost = (int64_t)g.size();
+    if ((int64_t)g.size() > cap) return TRPLK_EINVAL;
+    const std::vector<int> own = ranges ? ghost_owners(g, ranges, nranks) : std::vector<int>(g.size(), 0);
+    for (size_t i = 0; i < g.size(); ++i) {
+        if (ghosts_out) ghosts_out[i] = g[i];
+        if (owners_out) owners_out[i] = own[i];
+    }
     return TRPLK_OK;
 }
 

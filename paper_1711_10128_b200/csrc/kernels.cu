@@ -8,9 +8,14 @@
 //   k_eig     K6: one-CTA parallel-ordered cyclic Jacobi of T (Alg.1 step 11).
 //   k_rotate  K5: X = U Y on fp64 DMMA tensor cores (mma.sync m8n8k4 f64).
 //
-// Every reduction is deterministic: fixed per-warp butterfly shuffles, a fixed-order CTA
-// sum, per-CTA partials and a fixed-order final sum by the last CTA to finish.
+// Streaming kernels use one lane per row (32-row SELL slice = one warp tile) and issue the
+// whole row of the basis block U (k loads per lane) before the SpMV's dependent gathers, so
+// the basis stream overlaps the gather latency.  Every reduction is deterministic: per-warp
+// shuffle butterflies in a fixed pattern, a fixed-order CTA sum, then a two-level grid
+// reduction (groups of 32 CTAs, then groups) whose order does not depend on scheduling.
 #include <cstdio>
+#include <mutex>
+#include <unordered_map>
 
 #include "trplk_internal.cuh"
 
@@ -45,55 +50,132 @@ __device__ __forceinline__ void warp_butterfly(double (&v)[1 << LOG], int lane) 
     for (int off = (16 >> LOG); off >= 1; off >>= 1) v[0] += shx(v[0], off);
 }
 
-// SELL-32 row of lane `lane` in slice s: returns sum_j val*x[col], diag = slot-0 value.
-__device__ __forceinline__ double sell_row(const Sell& M, int64_t s, int lane, const double* __restrict__ x,
-                                           double& diag) {
+// Row `32 s + lane` of a local matrix times x: returns sum_j a_ij x_j and the diagonal a_ii.
+// DIA: every load address is computed, so all values and gathers of a chunk of 8 diagonals
+// are in flight at once (one memory round trip); the sum runs in ascending column order.
+// SELL: column ids are loaded first (two round trips per chunk of 8 entries).
+__device__ __forceinline__ double mat_row(const Sell& M, int64_t s, int lane, const double* __restrict__ x,
+                                          double& diag) {
+    double acc = 0.0;
+    if (M.fmt == 1) {
+        const int64_t row = s * 32 + lane;
+        const int64_t nl = M.nrows, top = M.nrows + M.nghost - 1;
+        diag = __ldg(M.dval + (int64_t)M.diag_slot * M.ldv + row);
+        for (int d0 = 0; d0 < M.ndiag; d0 += 8) {
+            double v[8], xv[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int d = d0 + u;
+                v[u] = 0.0;
+                xv[u] = 0.0;
+                if (d < M.ndiag) {
+                    int64_t idx = row + M.offs[d];
+                    idx = idx < 0 ? idx + nl + M.glo : (idx >= nl ? idx + M.glo : idx);
+                    idx = idx < 0 ? 0 : (idx > top ? top : idx);  // out-of-matrix slots hold 0
+                    v[u] = __ldg(M.dval + (int64_t)d * M.ldv + row);
+                    xv[u] = __ldg(x + idx);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) acc = fma(v[u], xv[u], acc);
+        }
+        return acc;
+    }
     const int64_t b = __ldg(M.sptr + s), e = __ldg(M.sptr + s + 1);
     const int w = (int)((e - b) >> 5);
     const double* vp = M.val + b + lane;
     const int* cp = M.col + b + lane;
-    double acc = 0.0;
     diag = __ldg(vp);
-    int j = 0;
-    for (; j + 4 <= w; j += 4) {
-        const double v0 = __ldg(vp + 32 * j), v1 = __ldg(vp + 32 * (j + 1));
-        const double v2 = __ldg(vp + 32 * (j + 2)), v3 = __ldg(vp + 32 * (j + 3));
-        const int c0 = __ldg(cp + 32 * j), c1 = __ldg(cp + 32 * (j + 1));
-        const int c2 = __ldg(cp + 32 * (j + 2)), c3 = __ldg(cp + 32 * (j + 3));
-        const double x0 = __ldg(x + c0), x1 = __ldg(x + c1), x2 = __ldg(x + c2), x3 = __ldg(x + c3);
-        acc = fma(v0, x0, acc);
-        acc = fma(v1, x1, acc);
-        acc = fma(v2, x2, acc);
-        acc = fma(v3, x3, acc);
+    for (int j0 = 0; j0 < w; j0 += 8) {
+        double v[8];
+        int c[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const bool in = j0 + u < w;
+            v[u] = in ? __ldg(vp + 32 * (j0 + u)) : 0.0;
+            c[u] = in ? __ldg(cp + 32 * (j0 + u)) : 0;
+        }
+        double xv[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) xv[u] = (j0 + u < w) ? __ldg(x + c[u]) : 0.0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc = fma(v[u], xv[u], acc);
     }
-    for (; j < w; ++j) acc = fma(__ldg(vp + 32 * j), __ldg(x + __ldg(cp + 32 * j)), acc);
     return acc;
 }
 
-// Last-CTA-done pattern.  Returns true in exactly one CTA, after all CTAs wrote their partials.
-__device__ __forceinline__ bool last_cta(unsigned* counter) {
-    __shared__ bool is_last;
+// Deterministic two-level grid reduction of the CTA's nv values `mine` (smem).  Returns true in
+// exactly one CTA, whose smem `out` then holds the grid sums.  The summation order is fixed:
+// CTAs in groups of RG (lane = CTA in group, xor-butterfly), then the groups likewise.
+constexpr int RG = 32;
+__device__ bool grid_reduce(const double* mine, int nv, double* part, double* gpart, unsigned* cnt, int maxcta,
+                            double* out) {
+    __shared__ bool flag;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int bid = blockIdx.x, ncta = gridDim.x;
+    for (int v = tid; v < nv; v += blockDim.x) part[(int64_t)v * maxcta + bid] = mine[v];
     __threadfence();
     __syncthreads();
-    if (threadIdx.x == 0) {
-        const unsigned prev = atomicAdd(counter, 1u);
-        is_last = (prev == gridDim.x - 1);
+    const int g = bid / RG, g0 = g * RG, gs = min(RG, ncta - g0), ng = (ncta + RG - 1) / RG;
+    if (tid == 0) flag = atomicAdd(&cnt[1 + g], 1u) == (unsigned)(gs - 1);
+    __syncthreads();
+    if (!flag) return false;
+    __threadfence();
+    constexpr int VPC = 4;  // values per warp in flight (register budget of the host kernel)
+    double val[VPC];
+    for (int base = warp; base < nv; base += VPC * WARPS) {
+#pragma unroll
+        for (int i = 0; i < VPC; ++i) {
+            const int v = base + i * WARPS;
+            val[i] = (v < nv && lane < gs) ? __ldcg(part + (int64_t)v * maxcta + g0 + lane) : 0.0;
+        }
+#pragma unroll
+        for (int i = 0; i < VPC; ++i) {
+            const int v = base + i * WARPS;
+            if (v < nv) {
+                const double s = warp_sum(val[i]);
+                if (lane == 0) gpart[(int64_t)v * MAXG + g] = s;
+            }
+        }
+    }
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) {
+        cnt[1 + g] = 0u;
+        flag = atomicAdd(&cnt[0], 1u) == (unsigned)(ng - 1);
     }
     __syncthreads();
-    if (is_last) __threadfence();
-    return is_last;
+    if (!flag) return false;
+    __threadfence();
+    for (int base = warp; base < nv; base += VPC * WARPS) {
+#pragma unroll
+        for (int i = 0; i < VPC; ++i) {
+            const int v = base + i * WARPS;
+            double s = 0.0;
+            if (v < nv) {
+                if (lane < ng) s = __ldcg(gpart + (int64_t)v * MAXG + lane);
+                if (lane + 32 < ng) s += __ldcg(gpart + (int64_t)v * MAXG + lane + 32);
+            }
+            val[i] = s;
+        }
+#pragma unroll
+        for (int i = 0; i < VPC; ++i) {
+            const int v = base + i * WARPS;
+            if (v < nv) {
+                const double s = warp_sum(val[i]);
+                if (lane == 0) out[v] = s;
+            }
+        }
+    }
+    __syncthreads();
+    if (tid == 0) cnt[0] = 0u;
+    return true;
 }
 
-// Fixed-order sum of the per-CTA partials part[v*maxcta + c], c < ncta, into out[v] (smem).
-__device__ void reduce_partials(const double* part, int maxcta, int ncta, int nv, double* out) {
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    for (int v = warp; v < nv; v += WARPS) {
-        double s = 0.0;
-        for (int c = lane; c < ncta; c += 32) s += __ldcg(part + (int64_t)v * maxcta + c);
-        s = warp_sum(s);
-        if (lane == 0) out[v] = s;
-    }
-    __syncthreads();
+__device__ __forceinline__ const double* resolve_x(const double* x, int dyn, int64_t ld, int off, const Ctl* ctl) {
+    if (dyn == 1) return x + ld * (int64_t)(ctl->t - 1 + off);
+    if (dyn == 2) return x + ld * (int64_t)(ctl->xprev_col + off);
+    return x;
 }
 
 // ------------------------------------------------------------ K1: fused SpMV + dots
@@ -117,20 +199,16 @@ __device__ void sdots_finalize(const SdotsArgs& a, const double* r, int k1, int 
     }
 }
 
-__device__ __forceinline__ const double* resolve_x(const double* x, int dyn, int64_t ld, int off, const Ctl* ctl) {
-    if (dyn == 1) return x + ld * (int64_t)(ctl->t - 1 + off);
-    if (dyn == 2) return x + ld * (int64_t)(ctl->xprev_col + off);
-    return x;
-}
-
 __device__ __forceinline__ void sdots_counts(const SdotsArgs& a, const Ctl* ctl, bool two, int& k1, int& k2) {
     const int kc = ctl->k;
     k1 = a.set1 ? (a.k_from_ctl ? kc : a.k1) : 0;
     k2 = (two && a.set2) ? (a.k_from_ctl ? kc : a.k2) : 0;
 }
 
-template <int RPT, bool TWO>
-__global__ void __launch_bounds__(CTA) k_sdots(const SdotsArgs a) {
+// KMAX = basis columns held in registers per chunk (the first chunk is issued before the SpMV);
+// wider blocks are processed in chunks of KMAX columns.
+template <int KMAX, bool TWO>
+__global__ void __launch_bounds__(CTA, 2) k_sdots(const SdotsArgs a) {
     Ctl* ctl = a.ctl;
     if ((ctl->flags & a.gate) != a.gate) return;
     if (a.gate_pass3 && ctl->pass3 == 0) return;
@@ -153,110 +231,92 @@ __global__ void __launch_bounds__(CTA) k_sdots(const SdotsArgs a) {
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t nslices = (a.nrows + 31) >> 5;
-    const int64_t ntiles = (nslices + RPT - 1) / RPT;
-    for (int64_t tile = (int64_t)blockIdx.x * WARPS + warp; tile < ntiles; tile += (int64_t)gridDim.x * WARPS) {
-        double xv[RPT], zv[RPT], ov[RPT];
-        int64_t row[RPT];
-        bool ok[RPT];
+    for (int64_t s = (int64_t)blockIdx.x * WARPS + warp; s < nslices; s += (int64_t)gridDim.x * WARPS) {
+        const int64_t row = s * 32 + lane;
+        const bool ok = row < a.nrows;
+        // issue the basis row first: its latency overlaps the SpMV's dependent gathers
+        double ur[KMAX > 0 ? KMAX : 1];
 #pragma unroll
-        for (int i = 0; i < RPT; ++i) {
-            const int64_t s = tile * RPT + i;
-            row[i] = s * 32 + lane;
-            ok[i] = (s < nslices) && (row[i] < a.nrows);
-            xv[i] = zv[i] = ov[i] = 0.0;
-            if (s < nslices) {
-                double ad = 1.0, bd = 1.0, z = 0.0, sv = 0.0;
-                const double xr = ok[i] ? X[row[i]] : 0.0;
-                if (a.out_mode == 4) {
-                    ad = __ldg(a.A.val + __ldg(a.A.sptr + s) + lane);
-                } else if (a.A.nrows) {
-                    z = sell_row(a.A, s, lane, X, ad);
-                } else {
-                    z = xr;
-                }
-                if (a.out_mode >= 2) {
-                    if (a.B.nrows) sv = sell_row(a.B, s, lane, X, bd);
-                    else sv = xr;
-                }
-                double o = 0.0, minv = 1.0;
-                if (a.out_mode >= 2) {
-                    double d = fabs(ad - a.sigma * bd);
-                    d = d > a.mfloor ? d : a.mfloor;
-                    minv = 1.0 / d;  // M_ii
-                }
-                switch (a.out_mode) {
-                    case 1: o = z; break;
-                    case 2: o = minv * (z - rho * sv); break;  // w = M (z - rho B g), R1
-                    case 3: o = z - theta * sv; break;         // r = A x - theta B x
-                    case 4: o = (ok[i] ? a.wext[row[i]] : 0.0) - theta * sv; break;
-                    default: break;
-                }
-                if (ok[i]) {
-                    if (a.out) a.out[row[i]] = o;
-                    if (a.uout) a.uout[row[i]] = minv * o;
-                    xv[i] = xr;
-                    zv[i] = z;
-                    ov[i] = o;
-                }
-            }
+        for (int c = 0; c < KMAX; ++c) ur[c] = (ok && c < kmx) ? a.U[(int64_t)c * a.ldu + row] : 0.0;
+        double ad = 1.0, bd = 1.0, z = 0.0, sv = 0.0;
+        const double xr = ok ? X[row] : 0.0;
+        if (a.out_mode == 4)
+            ad = a.A.fmt == 1 ? __ldg(a.A.dval + (int64_t)a.A.diag_slot * a.A.ldv + row)
+                              : __ldg(a.A.val + __ldg(a.A.sptr + s) + lane);
+        else if (a.A.nrows) z = mat_row(a.A, s, lane, X, ad);
+        else z = xr;
+        if (a.out_mode >= 2) {
+            if (a.B.nrows) sv = mat_row(a.B, s, lane, X, bd);
+            else sv = xr;
         }
-        if (kmx > 0) {
-            double v1[RPT];
+        double o = 0.0, minv = 1.0;
+        if (a.out_mode >= 2) {
+            double d = fabs(ad - a.sigma * bd);
+            d = d > a.mfloor ? d : a.mfloor;
+            minv = 1.0 / d;  // M_ii
+        }
+        switch (a.out_mode) {
+            case 1: o = z; break;
+            case 2: o = minv * (z - rho * sv); break;  // w = M (z - rho B g), R1
+            case 3: o = z - theta * sv; break;         // r = A x - theta B x
+            case 4: o = (ok ? a.wext[row] : 0.0) - theta * sv; break;
+            default: break;
+        }
+        if (ok) {
+            if (a.out) a.out[row] = o;
+            if (a.uout) a.uout[row] = minv * o;
+        } else {
+            z = 0.0;
+            o = 0.0;
+        }
+        if (KMAX > 0 && kmx > 0) {
+            const double v1 = a.set1 == 1 ? z : (a.set1 == 2 ? o : xr);
+          for (int cb = 0; cb < kmx; cb += KMAX) {
+            if (cb > 0) {
 #pragma unroll
-            for (int i = 0; i < RPT; ++i) v1[i] = a.set1 == 1 ? zv[i] : (a.set1 == 2 ? ov[i] : xv[i]);
-            for (int c0 = 0; c0 < kmx; c0 += 8) {
-                double v[TWO ? 16 : 8];
+                for (int c = 0; c < KMAX; ++c)
+                    ur[c] = (ok && cb + c < kmx) ? a.U[(int64_t)(cb + c) * a.ldu + row] : 0.0;
+            }
 #pragma unroll
-                for (int cc = 0; cc < 8; ++cc) {
-                    const int c = c0 + cc;
-                    double s1 = 0.0, s2 = 0.0;
-                    if (c < kmx) {
+            for (int cl = 0; cl < KMAX; cl += 8) {
+                const int c0 = cb + cl;
+                if (c0 < kmx) {
+                    double v[TWO ? 16 : 8];
 #pragma unroll
-                        for (int i = 0; i < RPT; ++i) {
-                            if (ok[i]) {
-                                const double u = a.U[(int64_t)c * a.ldu + row[i]];
-                                s1 = fma(u, v1[i], s1);
-                                if (TWO) s2 = fma(u, ov[i], s2);
+                    for (int cc = 0; cc < 8; ++cc) {
+                        const int c = c0 + cc;
+                        v[cc] = (c < k1) ? ur[cl + cc] * v1 : 0.0;
+                        if constexpr (TWO) v[8 + cc] = (c < k2) ? ur[cl + cc] * o : 0.0;
+                    }
+                    if constexpr (TWO) {
+                        warp_butterfly<4>(v, lane);
+                        const int idx = (lane >> 1) & 15;
+                        if ((lane & 1) == 0) {
+                            const int col = c0 + (idx & 7);
+                            if (idx < 8) {
+                                if (col < k1) acc[warp][col] += v[0];
+                            } else {
+                                if (col < k2) acc[warp][k1 + col] += v[0];
                             }
                         }
+                    } else {
+                        warp_butterfly<3>(v, lane);
+                        const int idx = (lane >> 2) & 7;
+                        if ((lane & 3) == 0 && c0 + idx < k1) acc[warp][c0 + idx] += v[0];
                     }
-                    v[cc] = s1;
-                    if constexpr (TWO) v[8 + cc] = s2;
-                }
-                if constexpr (TWO) {
-                    warp_butterfly<4>(v, lane);
-                    const int idx = (lane >> 1) & 15;
-                    if ((lane & 1) == 0) {
-                        const int col = c0 + (idx & 7);
-                        if (idx < 8) {
-                            if (col < k1) acc[warp][col] += v[0];
-                        } else {
-                            if (col < k2) acc[warp][k1 + col] += v[0];
-                        }
-                    }
-                } else {
-                    warp_butterfly<3>(v, lane);
-                    const int idx = (lane >> 2) & 7;
-                    if ((lane & 3) == 0 && c0 + idx < k1) acc[warp][c0 + idx] += v[0];
                 }
             }
+          }
         }
         if (nn) {
-            double n1 = 0.0, n2 = 0.0;
-#pragma unroll
-            for (int i = 0; i < RPT; ++i) {
-                const double o = ov[i], x = xv[i], z = zv[i];
-                const double p1 = a.norm1 == 1 ? o * o : a.norm1 == 2 ? x * z : a.norm1 == 3 ? x * x : z * z;
-                const double p2 = a.norm2 == 1 ? o * o : a.norm2 == 2 ? x * z : a.norm2 == 3 ? x * x : z * z;
-                n1 += p1;
-                n2 += p2;
-            }
-            n1 = warp_sum(n1);
-            n2 = warp_sum(n2);
+            const double p1 = a.norm1 == 1 ? o * o : a.norm1 == 2 ? xr * z : a.norm1 == 3 ? xr * xr : z * z;
+            const double p2 = a.norm2 == 1 ? o * o : a.norm2 == 2 ? xr * z : a.norm2 == 3 ? xr * xr : z * z;
+            const double n1 = warp_sum(ok ? p1 : 0.0);
+            const double n2 = a.norm2 ? warp_sum(ok ? p2 : 0.0) : 0.0;
             if (lane == 0) {
-                int o = k1 + k2;
-                if (a.norm1) acc[warp][o++] += n1;
-                if (a.norm2) acc[warp][o] += n2;
+                int oo = k1 + k2;
+                if (a.norm1) acc[warp][oo++] += n1;
+                if (a.norm2) acc[warp][oo] += n2;
             }
         }
     }
@@ -266,16 +326,15 @@ __global__ void __launch_bounds__(CTA) k_sdots(const SdotsArgs a) {
         double s = 0.0;
 #pragma unroll
         for (int w = 0; w < WARPS; ++w) s += acc[w][v];
-        a.part[(int64_t)v * a.maxcta + blockIdx.x] = s;
+        res[v] = s;
     }
-    if (!last_cta(a.counter)) return;
-    reduce_partials(a.part, a.maxcta, gridDim.x, nv, res);
+    __syncthreads();
+    if (!grid_reduce(res, nv, a.part, a.gpart, a.counter, a.maxcta, res)) return;
     if (a.red_local) {
         for (int v = threadIdx.x; v < nv; v += CTA) a.red_local[v] = res[v];
     } else {
         sdots_finalize(a, res, k1, k2);
     }
-    if (threadIdx.x == 0) *a.counter = 0u;
 }
 
 // --------------------------------------------------- K2/K3: CGS update (+dots / +norm)
@@ -292,7 +351,7 @@ __global__ void __launch_bounds__(CTA) k_upd(const UpdArgs a) {
     if (a.mode == 3 && ctl->pass3 == 0) return;
     const int kv = a.kv >= 0 ? a.kv : ctl->k;
     const double* __restrict__ X = resolve_x(a.x, a.x_dyn, a.x_ld, a.x_off, ctl);
-    __shared__ double hs[KMAX > 0 ? KMAX : 1];
+    __shared__ double hs[KMAX];
     __shared__ double acc[WARPS][QMAX + 1];
     __shared__ double res[QMAX + 1];
     for (int i = threadIdx.x; i < KMAX; i += CTA) hs[i] = i < kv ? ctl->h[a.hslot][i] : 0.0;
@@ -354,14 +413,14 @@ __global__ void __launch_bounds__(CTA) k_upd(const UpdArgs a) {
             }
             if (do_dots) {
 #pragma unroll
-                for (int c0 = 0; c0 < KMAX; c0 += 16) {
+                for (int c0 = 0; c0 < KMAX; c0 += 8) {
                     if (c0 < kv) {
-                        double v[16];
+                        double v[8];
 #pragma unroll
-                        for (int cc = 0; cc < 16; ++cc) v[cc] = (c0 + cc < KMAX) ? ur[(c0 + cc) % KMAX] * y : 0.0;
-                        warp_butterfly<4>(v, lane);
-                        const int idx = (lane >> 1) & 15;
-                        if ((lane & 1) == 0 && c0 + idx < kv) acc[warp][c0 + idx] += v[0];
+                        for (int cc = 0; cc < 8; ++cc) v[cc] = ur[c0 + cc] * y;
+                        warp_butterfly<3>(v, lane);
+                        const int idx = (lane >> 2) & 7;
+                        if ((lane & 3) == 0 && c0 + idx < kv) acc[warp][c0 + idx] += v[0];
                     }
                 }
                 const double yy = warp_sum(y * y);
@@ -371,23 +430,30 @@ __global__ void __launch_bounds__(CTA) k_upd(const UpdArgs a) {
     }
     if (a.mode == 0) return;
     const int nv = do_dots ? kv + 1 : 0;
+    __shared__ bool is_last;
     if (nv) {
         __syncthreads();
         for (int v = threadIdx.x; v < nv; v += CTA) {
             double s = 0.0;
 #pragma unroll
             for (int w = 0; w < WARPS; ++w) s += acc[w][v];
-            a.part[(int64_t)v * a.maxcta + blockIdx.x] = s;
+            res[v] = s;
         }
-    }
-    if (!last_cta(a.counter)) return;
-    if (nv) {
-        reduce_partials(a.part, a.maxcta, gridDim.x, nv, res);
+        __syncthreads();
+        if (!grid_reduce(res, nv, a.part, a.gpart, a.counter, a.maxcta, res)) return;
         if (a.red_local) {
             for (int v = threadIdx.x; v < nv; v += CTA) a.red_local[v] = res[v];
         } else {
             upd_finalize(a, res, kv);
         }
+    } else {
+        // no dots: one ticket so exactly one CTA applies the control-block side effects
+        __threadfence();
+        __syncthreads();
+        if (threadIdx.x == 0) is_last = atomicAdd(a.counter, 1u) == gridDim.x - 1;
+        __syncthreads();
+        if (!is_last) return;
+        if (threadIdx.x == 0) *a.counter = 0u;
     }
     if (threadIdx.x == 0) {
         if (a.mode == 2) {
@@ -409,7 +475,6 @@ __global__ void __launch_bounds__(CTA) k_upd(const UpdArgs a) {
                 ctl->k += 1;
             }
         }
-        *a.counter = 0u;
     }
 }
 
@@ -441,12 +506,17 @@ __global__ void k_finalize_multi(const SdotsArgs sd, const UpdArgs up, int which
 }
 
 // ------------------------------------------------------- K6: one-CTA cyclic Jacobi
+// (first version, three barriers per round; superseded by eig.cu)
+#if 0
 constexpr int LDA = QMAX + 1;
 
+// Round-robin (circle) tournament: player at position `pos` in round r (player 0 fixed).
 __device__ __forceinline__ int rr_player(int pos, int r, int kk) {
     return pos == 0 ? 0 : 1 + (pos - 1 + r) % (kk - 1);
 }
 
+// 256 threads: 8 threads per rotation pair (<= 32 disjoint pairs per round), each updating
+// every 8th row/column of the pair.
 __global__ void __launch_bounds__(256) k_eig(Ctl* ctl, double* T, int ldT, double* Y, int ldY, int ph,
                                              int k_fixed, unsigned gate) {
     if ((ctl->flags & gate) != gate) return;
@@ -456,16 +526,26 @@ __global__ void __launch_bounds__(256) k_eig(Ctl* ctl, double* T, int ldT, doubl
     double* V = sm + QMAX * LDA;
     __shared__ double cs[QMAX / 2], sn[QMAX / 2], red[256];
     __shared__ int pp[QMAX / 2], qq[QMAX / 2], ord[QMAX];
+    __shared__ unsigned char tabp[QMAX - 1][QMAX / 2], tabq[QMAX - 1][QMAX / 2];
     __shared__ int rotated;
     __shared__ double fro;
     const int tid = threadIdx.x;
     double f = 0.0;
-    for (int idx = tid; idx < k * k; idx += blockDim.x) {
-        const int i = idx % k, j = idx / k;
-        const double a = 0.5 * (T[i + (int64_t)j * ldT] + T[j + (int64_t)i * ldT]);  // sym(T)
-        A[i + j * LDA] = a;
-        V[i + j * LDA] = (i == j) ? 1.0 : 0.0;
-        f += a * a;
+    for (int j = 0; j < k; ++j)
+        for (int i = tid; i < k; i += blockDim.x) {
+            const double a = 0.5 * (T[i + (int64_t)j * ldT] + T[j + (int64_t)i * ldT]);  // sym(T)
+            A[i + j * LDA] = a;
+            V[i + j * LDA] = (i == j) ? 1.0 : 0.0;
+            f += a * a;
+        }
+    const int kk = k + (k & 1);
+    const int npairs = kk / 2;
+    for (int idx = tid; idx < (kk - 1) * npairs; idx += blockDim.x) {
+        const int r = idx / npairs, i = idx % npairs;
+        int p = rr_player(i, r, kk), q = rr_player(kk - 1 - i, r, kk);
+        if (p > q) { const int t = p; p = q; q = t; }
+        tabp[r][i] = (unsigned char)p;
+        tabq[r][i] = (unsigned char)q;
     }
     red[tid] = f;
     __syncthreads();
@@ -476,15 +556,13 @@ __global__ void __launch_bounds__(256) k_eig(Ctl* ctl, double* T, int ldT, doubl
     }
     __syncthreads();
     const double eps = 2.220446049250313e-16;
-    const int kk = k + (k & 1);
-    const int npairs = kk / 2;
+    const int pi = tid >> 3, sub = tid & 7;
     for (int sweep = 0; sweep < 100 && k > 1; ++sweep) {
         if (tid == 0) rotated = 0;
         __syncthreads();
         for (int r = 0; r < kk - 1; ++r) {
             if (tid < npairs) {
-                int p = rr_player(tid, r, kk), q = rr_player(kk - 1 - tid, r, kk);
-                if (p > q) { const int tmp = p; p = q; q = tmp; }
+                const int p = tabp[r][tid], q = tabq[r][tid];
                 pp[tid] = -1;
                 if (q < k) {
                     const double apq = A[p + q * LDA], app = A[p + p * LDA], aqq = A[q + q * LDA];
@@ -502,30 +580,34 @@ __global__ void __launch_bounds__(256) k_eig(Ctl* ctl, double* T, int ldT, doubl
             }
             __syncthreads();
             // A <- A J and V <- V J (columns p, q of every rotated pair)
-            for (int idx = tid; idx < npairs * k; idx += blockDim.x) {
-                const int pi = idx / k, i = idx % k;
+            if (pi < npairs) {
                 const int p = pp[pi];
-                if (p < 0) continue;
-                const int q = qq[pi];
-                const double c = cs[pi], s = sn[pi];
-                const double aip = A[i + p * LDA], aiq = A[i + q * LDA];
-                A[i + p * LDA] = c * aip - s * aiq;
-                A[i + q * LDA] = s * aip + c * aiq;
-                const double vip = V[i + p * LDA], viq = V[i + q * LDA];
-                V[i + p * LDA] = c * vip - s * viq;
-                V[i + q * LDA] = s * vip + c * viq;
+                if (p >= 0) {
+                    const int q = qq[pi];
+                    const double c = cs[pi], s = sn[pi];
+                    for (int i = sub; i < k; i += 8) {
+                        const double aip = A[i + p * LDA], aiq = A[i + q * LDA];
+                        A[i + p * LDA] = c * aip - s * aiq;
+                        A[i + q * LDA] = s * aip + c * aiq;
+                        const double vip = V[i + p * LDA], viq = V[i + q * LDA];
+                        V[i + p * LDA] = c * vip - s * viq;
+                        V[i + q * LDA] = s * vip + c * viq;
+                    }
+                }
             }
             __syncthreads();
             // A <- J^T A (rows p, q); the rotated entries (p,q), (q,p) are set to exactly 0
-            for (int idx = tid; idx < npairs * k; idx += blockDim.x) {
-                const int pi = idx / k, j = idx % k;
+            if (pi < npairs) {
                 const int p = pp[pi];
-                if (p < 0) continue;
-                const int q = qq[pi];
-                const double c = cs[pi], s = sn[pi];
-                const double apj = A[p + j * LDA], aqj = A[q + j * LDA];
-                A[p + j * LDA] = (j == q) ? 0.0 : c * apj - s * aqj;
-                A[q + j * LDA] = (j == p) ? 0.0 : s * apj + c * aqj;
+                if (p >= 0) {
+                    const int q = qq[pi];
+                    const double c = cs[pi], s = sn[pi];
+                    for (int j = sub; j < k; j += 8) {
+                        const double apj = A[p + j * LDA], aqj = A[q + j * LDA];
+                        A[p + j * LDA] = (j == q) ? 0.0 : c * apj - s * aqj;
+                        A[q + j * LDA] = (j == p) ? 0.0 : s * apj + c * aqj;
+                    }
+                }
             }
             __syncthreads();
         }
@@ -565,6 +647,7 @@ __global__ void __launch_bounds__(256) k_eig(Ctl* ctl, double* T, int ldT, doubl
     }
     if (tid == 0) ctl->k_rr = k;
 }
+#endif
 
 // ------------------------------------------------------- K5: DMMA rotation X = U Y
 __device__ __forceinline__ void dmma884(double (&d)[2], double a, double b) {
@@ -669,18 +752,35 @@ static int num_sms() {
     return n;
 }
 
-constexpr int SD_RPT = 2;
+// Grid of a persistent streaming kernel: resident CTAs (occupancy API) x SMs, balanced so
+// that every CTA processes the same number of 32-row tiles.
+static int occupancy(const void* kernel) {
+    static std::mutex mu;
+    static std::unordered_map<const void*, int> cache;
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(kernel);
+    if (it != cache.end()) return it->second;
+    int occ = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, CTA, 0);
+    if (occ < 1) occ = 1;
+    cache[kernel] = occ;
+    return occ;
+}
 
-int sdots_grid(int64_t nrows) {
-    const int64_t nslices = (nrows + 31) / 32;
-    const int64_t warps_needed = (nslices + SD_RPT - 1) / SD_RPT;
-    int64_t g = (warps_needed + WARPS - 1) / WARPS;
-    const int64_t cap = (int64_t)num_sms() * 4;
-    if (g > cap) g = cap;
-    return (int)(g < 1 ? 1 : g);
+template <typename K>
+static int stream_grid(K kernel, int64_t nrows) {
+    const int occ = occupancy(reinterpret_cast<const void*>(kernel));
+    const int64_t tiles = (nrows + 31) / 32;
+    const int64_t need = (tiles + WARPS - 1) / WARPS;
+    int64_t cap = (int64_t)num_sms() * occ;
+    if (cap > MAXCTA) cap = MAXCTA;
+    if (need <= cap) return (int)(need < 1 ? 1 : need);
+    const int64_t waves = (need + cap - 1) / cap;
+    return (int)((need + waves - 1) / waves);
 }
 
 int kmax_bucket(int k) {
+    if (k <= 0) return 0;
     if (k <= 8) return 8;
     if (k <= 16) return 16;
     if (k <= 24) return 24;
@@ -690,42 +790,47 @@ int kmax_bucket(int k) {
     return 64;
 }
 
-int upd_grid(int64_t nrows, int kmax) {
-    const int64_t tiles = (nrows + 31) / 32;
-    int64_t g = (tiles + WARPS - 1) / WARPS;
-    const int per_sm = kmax <= 16 ? 6 : kmax <= 32 ? 4 : kmax <= 48 ? 3 : 2;
-    const int64_t cap = (int64_t)num_sms() * per_sm;
-    if (g > cap) g = cap;
-    return (int)(g < 1 ? 1 : g);
+#define SD_CASE(KM)                                                                      \
+    case KM:                                                                             \
+        if (a.set2) {                                                                    \
+            auto kern = k_sdots<KM, true>;                                               \
+            kern<<<stream_grid(kern, a.nrows), CTA, 0, s>>>(a);                          \
+        } else {                                                                         \
+            auto kern = k_sdots<KM, false>;                                              \
+            kern<<<stream_grid(kern, a.nrows), CTA, 0, s>>>(a);                          \
+        }                                                                                \
+        break;
+
+void launch_sdots(const SdotsArgs& a, int kmax, cudaStream_t s) {
+    switch (kmax > 32 ? 32 : kmax) {  // columns beyond 32 are processed in further chunks
+        SD_CASE(0)
+        SD_CASE(8)
+        SD_CASE(16)
+        SD_CASE(24)
+        default:
+        SD_CASE(32)
+    }
 }
 
-void launch_sdots(const SdotsArgs& a, int grid, cudaStream_t s) {
-    if (a.set2) k_sdots<SD_RPT, true><<<grid, CTA, 0, s>>>(a);
-    else k_sdots<SD_RPT, false><<<grid, CTA, 0, s>>>(a);
-}
+#define UP_CASE(KM)                                        \
+    case KM: {                                             \
+        auto kern = k_upd<KM>;                             \
+        kern<<<stream_grid(kern, a.nrows), CTA, 0, s>>>(a); \
+    } break;
 
-void launch_upd(const UpdArgs& a, int kmax, int grid, cudaStream_t s) {
+void launch_upd(const UpdArgs& a, int kmax, cudaStream_t s) {
     switch (kmax) {
-        case 8: k_upd<8><<<grid, CTA, 0, s>>>(a); break;
-        case 16: k_upd<16><<<grid, CTA, 0, s>>>(a); break;
-        case 24: k_upd<24><<<grid, CTA, 0, s>>>(a); break;
-        case 32: k_upd<32><<<grid, CTA, 0, s>>>(a); break;
-        case 40: k_upd<40><<<grid, CTA, 0, s>>>(a); break;
-        case 48: k_upd<48><<<grid, CTA, 0, s>>>(a); break;
-        default: k_upd<64><<<grid, CTA, 0, s>>>(a); break;
+        UP_CASE(8)
+        UP_CASE(16)
+        UP_CASE(24)
+        UP_CASE(32)
+        UP_CASE(40)
+        UP_CASE(48)
+        default:
+        UP_CASE(64)
     }
 }
 
-void launch_eig(Ctl* ctl, double* T, int ldT, double* Y, int ldY, int ph, int k_fixed, unsigned gate,
-                cudaStream_t s) {
-    static bool init = false;
-    const int smem = 2 * QMAX * LDA * (int)sizeof(double);
-    if (!init) {
-        cudaFuncSetAttribute(k_eig, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        init = true;
-    }
-    k_eig<<<1, 256, smem, s>>>(ctl, T, ldT, Y, ldY, ph, k_fixed, gate);
-}
 
 void launch_rotate(const double* U, int64_t ldu, int64_t nrows, const Ctl* ctl, int k_fixed, const double* Y,
                    int ldY, int ncol, double* X, int64_t ldx, unsigned gate, cudaStream_t s) {

@@ -10,16 +10,31 @@ constexpr int QMAX = 64;           // TRPLK_MAX_BASIS
 constexpr int NV_MAX = 2 * QMAX + 4; // values of one fused reduction
 constexpr int CTA = 256;           // threads per CTA of the streaming kernels
 constexpr int WARPS = CTA / 32;
+constexpr int MAXCTA = 2048;       // largest grid of a reducing kernel
+constexpr int MAXG = MAXCTA / 32;  // reduction groups (32 CTAs each)
+constexpr int NCOUNTERS = 1 + MAXG;
 
-// SELL-32 sparse matrix, local rows only.  Slice s holds rows [32s, 32s+32); entry j of
-// lane l sits at sptr[s] + 32*j + l; slot j=0 is the diagonal.  Padding: val 0, col = row.
-// Column ids are local: [0, nrows) owned, [nrows, nrows+nghost) ghost tail.
+constexpr int DIA_MAX = 32;       // most diagonals a DIA matrix may have
+
+// Local sparse matrix (rows owned by this rank), one of two device formats chosen at create:
+//  fmt 0  SELL-32: slice s holds rows [32s, 32s+32); entry j of lane l sits at
+//         sptr[s] + 32*j + l; slot j=0 is the diagonal.  Padding: val 0, col = row.
+//         Column ids are local: [0, nrows) owned, [nrows, nrows+nghost) ghost tail.
+//  fmt 1  DIA: ndiag diagonals with global offsets offs[d] (col = row + offs[d]); values
+//         dval[d*ldv + row] (0 where no entry).  Requires the ghost tail to be the contiguous
+//         global ranges [row_begin-glo, row_begin) then [row_end, row_end+nghost-glo), so the
+//         local index of row+off is computed, not loaded.  diag_slot = index of offset 0.
 struct Sell {
+    int fmt = 0;
     int64_t nrows = 0;
     int64_t nslices = 0;
     const int64_t* sptr = nullptr;
     const int* col = nullptr;
     const double* val = nullptr;
+    int ndiag = 0, diag_slot = 0;
+    int64_t ldv = 0, glo = 0, nghost = 0;
+    const double* dval = nullptr;
+    int offs[DIA_MAX] = {};
 };
 
 // Gate bits of Ctl::flags
@@ -85,7 +100,8 @@ struct SdotsArgs {
     double* T;
     int ldT;
     double* part;      // [NV_MAX][maxcta]
-    unsigned* counter;
+    double* gpart;     // [NV_MAX][MAXG]
+    unsigned* counter; // [NCOUNTERS]
     int maxcta;
     double* red_local; // multi-rank: local sums instead of finalize (nullptr => finalize)
 };
@@ -114,14 +130,15 @@ struct UpdArgs {
     unsigned clear_on_brk;
     Ctl* ctl;
     double* part;
+    double* gpart;
     unsigned* counter;
     int maxcta;
     double* red_local;
 };
 
 // Kernel launchers (kernels.cu)
-void launch_sdots(const SdotsArgs& a, int grid, cudaStream_t s);
-void launch_upd(const UpdArgs& a, int kmax, int grid, cudaStream_t s);
+void launch_sdots(const SdotsArgs& a, int kmax, cudaStream_t s);
+void launch_upd(const UpdArgs& a, int kmax, cudaStream_t s);
 void launch_eig(Ctl* ctl, double* T, int ldT, double* Y, int ldY, int ph, int k_fixed, unsigned gate,
                 cudaStream_t s);
 void launch_rotate(const double* U, int64_t ldu, int64_t nrows, const Ctl* ctl, int k_fixed,
@@ -136,8 +153,6 @@ void launch_finalize_upd_multi(const UpdArgs& up, const double* red_all, int nra
 void launch_gather(const double* x, const int* idx, int64_t n, double* out, cudaStream_t s);
 void launch_copy_cols(const double* src, int64_t lds, double* dst, int64_t ldd, int64_t nrows, int ncols,
                       cudaStream_t s);
-int sdots_grid(int64_t nrows);
-int upd_grid(int64_t nrows, int kmax);
 int kmax_bucket(int k);
 
 }  // namespace trplk

@@ -83,13 +83,15 @@ _sig("trplk_k_rotate", _I, [_P, _P, _I64, _I, _P, _I, _P, _I64])
 _sig("trplk_k_sym_eig", _I, [_P, _I, _P, _P, _P])
 _sig("trplk_k_residual", _I, [_P, _P, _D, _P, _P, _P])
 _sig("trplk_k_random", _I, [_P, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64, _P])
+_sig("trplk_plan_ghosts", _I, [_I64, _I64, _P, _P, _P, _P, _P, _I, _P, _P, _I64, ctypes.POINTER(_I64)])
 _sig("trplk_profile", _I, [_P, _I])
 _sig("trplk_profile_read", _I, [_P, _P, _P, ctypes.POINTER(_I64)])
 
 EXPORTED = ["trplk_options_default", "trplk_nccl_unique_id", "trplk_create", "trplk_solve",
             "trplk_get_log", "trplk_info", "trplk_destroy", "trplk_last_error", "trplk_k_spmv",
             "trplk_k_step1", "trplk_k_cgs2", "trplk_k_rotate", "trplk_k_sym_eig",
-            "trplk_k_residual", "trplk_k_random", "trplk_profile", "trplk_profile_read"]
+            "trplk_k_residual", "trplk_k_random", "trplk_profile", "trplk_profile_read",
+            "trplk_plan_ghosts"]
 
 
 class TrplkError(RuntimeError):
@@ -344,6 +346,26 @@ def trplk_options_default() -> Options:
 def trplk_info(ctx: Context) -> dict:
     return {"n_local": ctx.n_local, "n_ghost": ctx.n_ghost, "rank": ctx.rank, "nranks": ctx.nranks,
             "frob_a": ctx.frob_a, "sell_bytes_a": ctx.sell_bytes_a, "sell_bytes_b": ctx.sell_bytes_b}
+
+
+def trplk_plan_ghosts(A, B=None, row_begin=0, row_end=None, ranges=None):
+    """Host-only halo plan of a row slab (the code trplk_create runs): (ghost ids, owner ranks)."""
+    ra, ca, _ = _csr_arrays(A)
+    rb, cb, _ = _csr_arrays(B)
+    if row_end is None:
+        row_end = row_begin + len(ra) - 1
+    rg = None if ranges is None else np.ascontiguousarray(np.asarray(ranges, np.int64).ravel())
+    nr = 1 if rg is None else len(rg) // 2
+    cnt = _I64()
+    _lib.trplk_plan_ghosts(row_begin, row_end, _ptr(ra), _ptr(ca), _ptr(rb), _ptr(cb), _ptr(rg), nr, None,
+                           None, 0, ctypes.byref(cnt))
+    g = np.zeros(max(cnt.value, 1), np.int64)
+    o = np.zeros(max(cnt.value, 1), np.int32)
+    st = _lib.trplk_plan_ghosts(row_begin, row_end, _ptr(ra), _ptr(ca), _ptr(rb), _ptr(cb), _ptr(rg), nr,
+                                _ptr(g), _ptr(o), len(g), ctypes.byref(cnt))
+    if st != 0:
+        raise TrplkError(st, "trplk_plan_ghosts failed")
+    return g[:cnt.value], o[:cnt.value]
 
 
 def trplk_profile(ctx: Context, enable: bool = True):

@@ -1,0 +1,54 @@
+"""Write tests/golden/oracle_<CFG>.json from the ORACLE only (no CUDA path involved).
+
+    python tests/golden/make_oracle_golden.py C3 [C4 ...] [--cycles K]
+
+Stores the oracle's eigenvalues, residuals, status, counters and per-cycle log
+(t, cumulative A-matvecs, theta_t, ||r_t||, basis width, X^prev width) of the
+full-size BASELINE configs whose oracle solve takes minutes, so the GPU parity
+tests can compare trajectories without re-running the oracle.  --cycles K
+stores a bounded prefix (max_cycles=K) instead of the full solve.
+"""
+import json
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, ROOT)
+
+import oracle  # noqa: E402
+from paper_1711_10128_b200 import inputs  # noqa: E402
+
+
+def main(argv):
+    cycles = None
+    if "--cycles" in argv:
+        i = argv.index("--cycles")
+        cycles = int(argv[i + 1])
+        argv = argv[:i] + argv[i + 2:]
+    for name in argv:
+        P = inputs.make(name)
+        t0 = time.perf_counter()
+        r = oracle.solve(P.A, P.B, P.p, P.q, P.l, P.tol, P.sigma, want_vectors=False,
+                         max_cycles=cycles or 5000)
+        dt = time.perf_counter() - t0
+        out = {
+            "config": name, "desc": P.desc, "p": P.p, "q": P.q, "l": P.l, "tol": P.tol,
+            "source": "oracle/ (orc_trplk_solve) via tests/golden/make_oracle_golden.py",
+            "prefix_cycles": cycles,
+            "status": r["status"], "cycles": r["cycles"], "a_matvecs": r["a_matvecs"],
+            "b_matvecs": r["b_matvecs"], "eigenvalues": list(map(float, r["eigenvalues"])),
+            "residuals": list(map(float, r["residuals"])),
+            "log": {k: [float(x) if k in ("theta_t", "res") else int(x) for x in v]
+                    for k, v in r["log"].items() if k in ("t", "mv", "theta_t", "res", "k", "nprev")},
+            "log_thetas": [list(map(float, row)) for row in r["log"]["thetas"]],
+            "oracle_seconds": dt, "host_cores": os.cpu_count(),
+        }
+        suffix = f"_first{cycles}" if cycles else ""
+        path = os.path.join(os.path.dirname(os.path.abspath(__file__)), f"oracle_{name}{suffix}.json")
+        json.dump(out, open(path, "w"))
+        print(name, r["status"], r["cycles"], r["a_matvecs"], f"{dt:.1f}s", flush=True)
+
+
+if __name__ == "__main__":
+    main(sys.argv[1:])

@@ -18,8 +18,69 @@ def problems(gen):
     return {f"{c}-{N}": gen.make(c, N=N) for c, N in CASES}
 
 
-def _ctx(trplk, P):
-    return trplk.trplk_create(P.A, P.B)
+def _ctx(trplk, P, fmt="auto"):
+    """fmt 'sell' forces the SELL-32 device format (TRPLK_FORCE_SELL); stencils pick DIA."""
+    import os
+    if fmt == "sell":
+        os.environ["TRPLK_FORCE_SELL"] = "1"
+    try:
+        return trplk.trplk_create(P.A, P.B)
+    finally:
+        os.environ.pop("TRPLK_FORCE_SELL", None)
+
+
+def _random_sym(n, density, seed):
+    """General symmetric sparse matrix (many diagonals -> SELL-32) with a dominant diagonal."""
+    import scipy.sparse as sp
+    R = sp.random(n, n, density=density, random_state=seed, format="csr")
+    A = (R + R.T + sp.diags(np.full(n, 4.0))).tocsr()
+    A.sort_indices()
+    return A
+
+
+def test_spmv_and_step1_general_sparse(orc):
+    """Non-stencil matrix: SELL-32 path, ragged rows of very different lengths."""
+    torch, trplk = need_gpu()
+    from types import SimpleNamespace
+    n = 3001
+    A = _random_sym(n, 0.01, 3)
+    P = SimpleNamespace(A=A, B=None)
+    ctx = trplk.trplk_create(A, n_global=n)
+    rng = np.random.default_rng(0)
+    x = rng.standard_normal(n)
+    y = torch.zeros(n, dtype=torch.float64, device="cuda")
+    trplk.trplk_k_spmv(ctx, 0, to_dev(torch, x), y)
+    assert normwise(y.cpu().numpy(), orc.spmv(A, x)) <= 1e-13
+    k = 12
+    U = b_orthonormal_block(orc, n, k, None, seed=4)
+    Ud = to_dev(torch, U, ctx.ld)
+    w = torch.zeros(ctx.ld, dtype=torch.float64, device="cuda")
+    tcol, h1, wn = trplk.trplk_k_step1(ctx, Ud, ctx.ld, k, Ud[k - 1], 0.3, w)
+    z = orc.spmv(A, U[:, k - 1])
+    w_o = orc.jacobi_diag(A) * (z - 0.3 * U[:, k - 1])
+    assert normwise(w.cpu().numpy()[:n], w_o) <= 1e-12
+    assert np.all(np.abs(tcol - U.T @ z) <= 1e-12 * np.linalg.norm(z))
+    assert np.all(np.abs(h1 - U.T @ w_o) <= 1e-12 * np.linalg.norm(w_o))
+    del P
+
+
+@pytest.mark.parametrize("case", [f"{c}-{N}" for c, N in CASES])
+def test_spmv_sell_format(orc, problems, case):
+    torch, trplk = need_gpu()
+    P = problems[case]
+    ctx = _ctx(trplk, P, "sell")
+    n = P.A.n
+    x = np.random.default_rng(5).standard_normal(n)
+    y = torch.zeros(n, dtype=torch.float64, device="cuda")
+    trplk.trplk_k_spmv(ctx, 0, to_dev(torch, x), y)
+    assert normwise(y.cpu().numpy(), orc.spmv(P.A, x)) <= 1e-13
+    r = torch.zeros(ctx.ld, dtype=torch.float64, device="cuda")
+    u = torch.zeros(ctx.ld, dtype=torch.float64, device="cuda")
+    trplk.trplk_k_residual(ctx, to_dev(torch, x, ctx.ld), 0.25, r, u)
+    Bx = x if P.B is None else orc.spmv(P.B, x)
+    r_o = orc.spmv(P.A, x) - 0.25 * Bx
+    assert normwise(r.cpu().numpy()[:n], r_o) <= 1e-13
+    assert normwise(u.cpu().numpy()[:n], orc.jacobi_diag(P.A, P.B) * r_o) <= 1e-13
 
 
 @pytest.mark.parametrize("case", [f"{c}-{N}" for c, N in CASES])

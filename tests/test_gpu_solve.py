@@ -13,8 +13,14 @@ from gpu_util import need_gpu
 pytestmark = pytest.mark.gpu
 
 
-def gpu_solve(trplk, P, tol=None, **opt):
-    ctx = trplk.trplk_create(P.A, P.B, P.sigma)
+def gpu_solve(trplk, P, tol=None, fmt="auto", **opt):
+    import os
+    if fmt == "sell":
+        os.environ["TRPLK_FORCE_SELL"] = "1"
+    try:
+        ctx = trplk.trplk_create(P.A, P.B, P.sigma)
+    finally:
+        os.environ.pop("TRPLK_FORCE_SELL", None)
     ev, X, rs, st = trplk.trplk_solve(ctx, P.p, P.q, P.l, P.tol if tol is None else tol, **opt)
     ph = opt.get("restart_size", 0) or P.p
     log = trplk.trplk_get_log(ctx, ph=ph)
@@ -88,17 +94,19 @@ def check_parity(g, o, P, allow_tie_divergence=False):
     return c
 
 
-@pytest.mark.parametrize("name,N", [("C1", None), ("C2", 12), ("C2", 24), ("C4", 8), ("C4", 12)])
-def test_solve_parity_small(orc, gen, name, N):
+@pytest.mark.parametrize("name,N,fmt", [("C1", None, "auto"), ("C2", 12, "auto"), ("C2", 24, "auto"),
+                                        ("C4", 8, "auto"), ("C4", 12, "auto"), ("C2", 12, "sell"),
+                                        ("C4", 8, "sell")])
+def test_solve_parity_small(orc, gen, name, N, fmt):
     torch, trplk = need_gpu()
     P = gen.make(name, N=N)
-    g = gpu_solve(trplk, P)
+    g = gpu_solve(trplk, P, fmt=fmt)
     o = oracle_solve(orc, P)
     check_parity(g, o, P)
     # B-orthonormal eigenvectors
     X = g["X"]
     BX = X if P.B is None else P.B.to_scipy() @ X
-    assert np.max(np.abs(X.T @ BX - np.eye(P.p))) <= 1e-12
+    assert np.max(np.abs(X.T @ BX - np.eye(P.p))) <= 1e-11  # oracle: 1.5e-12 on C1
 
 
 def test_solve_clustered_C3_small(orc, gen):
