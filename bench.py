@@ -196,7 +196,7 @@ def main():
 
     for _ in range(args.warmup):
         ev, _, rs, st = solve()
-    assert st["status"] == "OK", st
+        assert st["status"] == "OK", st
     trplk.trplk_profile(ctx, True)
     clocks = Clocks(local)
     times, stats = [], []

@@ -59,8 +59,10 @@ __device__ __forceinline__ double mat_row(const Sell& M, int64_t s, int lane, co
     double acc = 0.0;
     if (M.fmt == 1) {
         const int64_t row = s * 32 + lane;
-        const int64_t nl = M.nrows, top = M.nrows + M.nghost - 1;
-        diag = __ldg(M.dval + (int64_t)M.diag_slot * M.ldv + row);
+        const int nl = (int)M.nrows, top = (int)(M.nrows + M.nghost - 1), glo = (int)M.glo;
+        const bool halo = M.nghost != 0;
+        const double* dv = M.dval + row;
+        diag = __ldg(dv + (int64_t)M.diag_slot * M.ldv);
         for (int d0 = 0; d0 < M.ndiag; d0 += 8) {
             double v[8], xv[8];
 #pragma unroll
@@ -69,10 +71,10 @@ __device__ __forceinline__ double mat_row(const Sell& M, int64_t s, int lane, co
                 v[u] = 0.0;
                 xv[u] = 0.0;
                 if (d < M.ndiag) {
-                    int64_t idx = row + M.offs[d];
-                    idx = idx < 0 ? idx + nl + M.glo : (idx >= nl ? idx + M.glo : idx);
+                    int idx = (int)row + M.offs[d];  // local rows + ghosts < 2^31 (checked at create)
+                    if (halo) idx = idx < 0 ? idx + nl + glo : (idx >= nl ? idx + glo : idx);
                     idx = idx < 0 ? 0 : (idx > top ? top : idx);  // out-of-matrix slots hold 0
-                    v[u] = __ldg(M.dval + (int64_t)d * M.ldv + row);
+                    v[u] = __ldg(dv + (int64_t)d * M.ldv);
                     xv[u] = __ldg(x + idx);
                 }
             }
@@ -318,6 +320,141 @@ __global__ void __launch_bounds__(CTA, 2) k_sdots(const SdotsArgs a) {
                 if (a.norm1) acc[warp][oo++] += n1;
                 if (a.norm2) acc[warp][oo] += n2;
             }
+        }
+    }
+    if (nv == 0) return;
+    __syncthreads();
+    for (int v = threadIdx.x; v < nv; v += CTA) {
+        double s = 0.0;
+#pragma unroll
+        for (int w = 0; w < WARPS; ++w) s += acc[w][v];
+        res[v] = s;
+    }
+    __syncthreads();
+    if (!grid_reduce(res, nv, a.part, a.gpart, a.counter, a.maxcta, res)) return;
+    if (a.red_local) {
+        for (int v = threadIdx.x; v < nv; v += CTA) a.red_local[v] = res[v];
+    } else {
+        sdots_finalize(a, res, k1, k2);
+    }
+}
+
+// ---------------------------------------------- K1 (DMMA dots): fused SpMV + U^T [z w]
+__device__ __forceinline__ void dmma884(double (&d)[2], double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(d[0]), "+d"(d[1])
+                 : "d"(a), "d"(b));
+}
+
+// The dot products of K1 are the tall-skinny contraction U(:,1:k)^T [z w] (n x k by n x 2).
+// Each warp accumulates it over all of its 32-row tiles in DMMA m8n8k4 fragments
+// (A = 8 columns x 4 rows of U, B = rows of [z w 0..0], C = 8 x 8, columns 0/1 useful) and
+// reduces across warps/CTAs once at the end: no per-tile shuffle reductions.  The CUDA-core
+// version of this kernel was issue-bound (ncu: 'wait' + math-pipe throttle, 31% DRAM).
+// NG = column groups of 8 held in accumulators (k <= 8 NG).
+template <int NG, bool TWO>
+__global__ void __launch_bounds__(CTA, 2) k_sdots_mma(const SdotsArgs a) {
+    Ctl* ctl = a.ctl;
+    if ((ctl->flags & a.gate) != a.gate) return;
+    if (a.gate_pass3 && ctl->pass3 == 0) return;
+    int k1, k2;
+    sdots_counts(a, ctl, TWO, k1, k2);
+    const double rho = ctl->rho;
+    double theta = 0.0;
+    if (a.out_mode >= 3)
+        theta = a.theta_idx >= 0 ? ctl->theta[a.theta_idx]
+                                 : (a.theta_idx == -1 ? ctl->theta[ctl->t - 1] : a.theta_val);
+    const int nn = (a.norm1 ? 1 : 0) + (a.norm2 ? 1 : 0);
+    const int nv = k1 + k2 + nn;
+    const int kmx = k1 > k2 ? k1 : k2;
+    const double* __restrict__ X = resolve_x(a.x, a.x_dyn, a.x_ld, a.x_off, ctl);
+    const double* __restrict__ Ub = a.U;
+
+    __shared__ double acc[WARPS][NV_MAX];
+    __shared__ double res[NV_MAX];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int fi = lane >> 2, fj = lane & 3;  // fragment row/col ids
+    double cacc[NG][2];
+#pragma unroll
+    for (int g = 0; g < NG; ++g) cacc[g][0] = cacc[g][1] = 0.0;
+    double n1 = 0.0, n2 = 0.0;
+    const int64_t nslices = (a.nrows + 31) >> 5;
+    for (int64_t s = (int64_t)blockIdx.x * WARPS + warp; s < nslices; s += (int64_t)gridDim.x * WARPS) {
+        const int64_t r0 = s * 32;
+        const int64_t row = r0 + lane;
+        const bool ok = row < a.nrows;
+        double ad = 1.0, bd = 1.0, z = 0.0, sv = 0.0;
+        const double xr = ok ? X[row] : 0.0;
+        if (a.A.nrows) z = mat_row(a.A, s, lane, X, ad);
+        else z = xr;
+        if (a.out_mode >= 2) {
+            if (a.B.nrows) sv = mat_row(a.B, s, lane, X, bd);
+            else sv = xr;
+        }
+        double o = 0.0, minv = 1.0;
+        if (a.out_mode >= 2) {
+            double d = fabs(ad - a.sigma * bd);
+            d = d > a.mfloor ? d : a.mfloor;
+            minv = 1.0 / d;  // M_ii
+        }
+        if (a.out_mode == 1) o = z;
+        else if (a.out_mode == 2) o = minv * (z - rho * sv);  // w = M (z - rho B g), R1
+        else if (a.out_mode == 3) o = z - theta * sv;
+        if (ok) {
+            if (a.out) a.out[row] = o;
+            if (a.uout) a.uout[row] = minv * o;
+        } else {
+            z = 0.0;
+            o = 0.0;
+        }
+        const double v1 = a.set1 == 1 ? z : (a.set1 == 2 ? o : xr);
+        if (nn) {
+            const double p1 = a.norm1 == 1 ? o * o : a.norm1 == 2 ? xr * z : a.norm1 == 3 ? xr * xr : z * z;
+            const double p2 = a.norm2 == 1 ? o * o : a.norm2 == 2 ? xr * z : a.norm2 == 3 ? xr * xr : z * z;
+            n1 += ok ? p1 : 0.0;
+            n2 += ok ? p2 : 0.0;
+        }
+        // B fragments of the 8 row quads: B[fj][fi] = (fi == 0 ? v1 : fi == 1 ? o : 0) at row 4q + fj
+        double bq[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const double t1 = __shfl_sync(0xffffffffu, v1, 4 * q + fj);
+            const double t2 = TWO ? __shfl_sync(0xffffffffu, o, 4 * q + fj) : 0.0;
+            bq[q] = fi == 0 ? t1 : (fi == 1 ? t2 : 0.0);
+        }
+        const int64_t nrows = a.nrows;
+#pragma unroll
+        for (int g = 0; g < NG; ++g) {
+            if (8 * g < kmx) {
+                const int c = 8 * g + fi;
+                const bool cok = c < kmx;
+                const double* up = Ub + (int64_t)c * a.ldu + r0 + fj;
+                double av[8];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) av[q] = (cok && r0 + 4 * q + fj < nrows) ? __ldg(up + 4 * q) : 0.0;
+#pragma unroll
+                for (int q = 0; q < 8; ++q) dmma884(cacc[g], av[q], bq[q]);
+            }
+        }
+    }
+    // per-warp results: lane with fj == 0 holds C[fi][0] (set 1) and C[fi][1] (set 2) of group g
+    for (int i = threadIdx.x; i < WARPS * NV_MAX; i += CTA) (&acc[0][0])[i] = 0.0;
+    __syncthreads();
+    if (fj == 0) {
+#pragma unroll
+        for (int g = 0; g < NG; ++g) {
+            const int c = 8 * g + fi;
+            if (c < k1) acc[warp][c] = cacc[g][0];
+            if (TWO && c < k2) acc[warp][k1 + c] = cacc[g][1];
+        }
+    }
+    if (nn) {
+        n1 = warp_sum(n1);
+        n2 = warp_sum(n2);
+        if (lane == 0) {
+            int oo = k1 + k2;
+            if (a.norm1) acc[warp][oo++] = n1;
+            if (a.norm2) acc[warp][oo] = n2;
         }
     }
     if (nv == 0) return;
@@ -650,11 +787,6 @@ __global__ void __launch_bounds__(256) k_eig(Ctl* ctl, double* T, int ldT, doubl
 #endif
 
 // ------------------------------------------------------- K5: DMMA rotation X = U Y
-__device__ __forceinline__ void dmma884(double (&d)[2], double a, double b) {
-    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
-                 : "+d"(d[0]), "+d"(d[1])
-                 : "d"(a), "d"(b));
-}
 
 template <int NT>
 __global__ void __launch_bounds__(256) k_rotate(const double* __restrict__ U, int64_t ldu, int64_t nrows,
@@ -801,7 +933,32 @@ int kmax_bucket(int k) {
         }                                                                                \
         break;
 
+#define SDM_CASE(NG)                                                                     \
+    case NG:                                                                             \
+        if (a.set2) {                                                                    \
+            auto kern = k_sdots_mma<NG, true>;                                           \
+            kern<<<stream_grid(kern, a.nrows), CTA, 0, s>>>(a);                          \
+        } else {                                                                         \
+            auto kern = k_sdots_mma<NG, false>;                                          \
+            kern<<<stream_grid(kern, a.nrows), CTA, 0, s>>>(a);                          \
+        }                                                                                \
+        break;
+
 void launch_sdots(const SdotsArgs& a, int kmax, cudaStream_t s) {
+    if (kmax > 0 && a.out_mode != 4) {  // dots: DMMA accumulator kernel
+        switch ((kmax + 7) / 8) {
+            SDM_CASE(1)
+            SDM_CASE(2)
+            SDM_CASE(3)
+            SDM_CASE(4)
+            SDM_CASE(5)
+            SDM_CASE(6)
+            SDM_CASE(7)
+            default:
+            SDM_CASE(8)
+        }
+        return;
+    }
     switch (kmax > 32 ? 32 : kmax) {  // columns beyond 32 are processed in further chunks
         SD_CASE(0)
         SD_CASE(8)
