@@ -588,7 +588,7 @@ trplk_status cgs2(trplk_ctx* ctx, const CgsSpec& c) {
         u.kv = c.kv;
         u.hslot = 1;
         u.mode = 2;
-        u.dots = ctx->hasB ? 0 : 1;
+        u.dots = 0;
         u.out = ctx->w2;
         u.hout = 2;
         u.dest = c.dest;
@@ -599,13 +599,18 @@ trplk_status cgs2(trplk_ctx* ctx, const CgsSpec& c) {
         u.clear_on_brk = c.clear;
         ST(run_upd(ctx, u, kn));
     }
-    if (ctx->hasB) {  // pass-3 dots for B != I (gated on ctl->pass3)
+    {  // third-pass dots h3 = V^T B w2, N_2SQ_EXP = w2^T B w2 (gated on ctl->pass3, normally a no-op)
         SdotsArgs a = sd_base(ctx);
-        ST(halo(ctx, ctx->w2));
         a.x = ctx->w2;
-        a.A = ctx->B;
-        a.set1 = 1;
-        a.norm1 = 2;
+        if (ctx->hasB) {
+            ST(halo(ctx, ctx->w2));
+            a.A = ctx->B;
+            a.set1 = 1;
+            a.norm1 = 2;
+        } else {
+            a.set1 = 3;
+            a.norm1 = 3;
+        }
         a.U = c.V;
         a.ldu = ldv;
         a.k1 = c.kv;

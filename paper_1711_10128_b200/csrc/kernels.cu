@@ -481,8 +481,10 @@ __device__ void upd_finalize(const UpdArgs& a, const double* r, int kv) {
     if (threadIdx.x == 0) ctl->nrm[a.mode == 1 ? N_1SQ : N_2SQ_EXP] = r[kv];
 }
 
-template <int KMAX>
-__global__ void __launch_bounds__(CTA) k_upd(const UpdArgs a) {
+// DOTS = true: mode 1 (update + U^T y dots); DOTS = false: modes 0 / 2 / 3 (no dots; the rare
+// third-pass dots are a separate gated k_sdots launch).
+template <int KMAX, bool DOTS>
+__global__ void __launch_bounds__(CTA, DOTS ? 2 : 3) k_upd(const UpdArgs a) {
     Ctl* ctl = a.ctl;
     if ((ctl->flags & a.gate) != a.gate) return;
     if (a.mode == 3 && ctl->pass3 == 0) return;
@@ -517,7 +519,7 @@ __global__ void __launch_bounds__(CTA) k_upd(const UpdArgs a) {
         }
     }
     const bool write_y = a.mode <= 1 || (a.mode == 2 && pass3);
-    const bool do_dots = a.dots && (a.mode == 1 || (a.mode == 2 && pass3));
+    const bool do_dots = DOTS && a.mode == 1;
     const bool write_dest = (a.mode >= 2) && !pass3 && !brk;
     double* dest = a.dest;
     if (write_dest && a.dest_dyn) dest = a.dest + a.dest_ld * (int64_t)ctl->k;
@@ -528,18 +530,28 @@ __global__ void __launch_bounds__(CTA) k_upd(const UpdArgs a) {
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t ntiles = (a.nrows + 31) >> 5;
+    double dacc[KMAX / 8][2];
+#pragma unroll
+    for (int g = 0; g < KMAX / 8; ++g) dacc[g][0] = dacc[g][1] = 0.0;
+    double yy_acc = 0.0;
     if (write_y || write_dest) {
         for (int64_t tile = (int64_t)blockIdx.x * WARPS + warp; tile < ntiles;
              tile += (int64_t)gridDim.x * WARPS) {
             const int64_t row = tile * 32 + lane;
             const bool ok = row < a.nrows;
-            double ur[KMAX];
-#pragma unroll
-            for (int c = 0; c < KMAX; ++c) ur[c] = (ok && c < kv) ? a.U[(int64_t)c * a.ldu + row] : 0.0;
+            // y = x - U h, columns in order; loads issued in chunks of 8 (the compiler hoists
+            // later chunks as far as the register budget allows)
             double y = ok ? X[row] : 0.0;
+            const double* up = a.U + row;
 #pragma unroll
-            for (int c = 0; c < KMAX; ++c)
-                if (c < kv) y = fma(-hs[c], ur[c], y);  // y = x - U h, columns in order
+            for (int cb = 0; cb < KMAX; cb += 8) {
+                double u8[8];
+#pragma unroll
+                for (int c = 0; c < 8; ++c)
+                    u8[c] = (ok && cb + c < kv) ? __ldg(up + (int64_t)(cb + c) * a.ldu) : 0.0;
+#pragma unroll
+                for (int c = 0; c < 8; ++c) y = fma(-hs[cb + c], u8[c], y);
+            }
             if (ok) {
                 if (write_y && a.out) a.out[row] = y;
                 if (write_dest) {
@@ -548,20 +560,31 @@ __global__ void __launch_bounds__(CTA) k_upd(const UpdArgs a) {
                     if (a.dest2) a.dest2[row] = g;
                 }
             }
-            if (do_dots) {
+            if (DOTS && do_dots) {
+                // U^T y accumulated in DMMA fragments over the warp's tiles: A = y^T (row 0, 4 rows
+                // per quad), B = U(4 rows, 8 columns) re-read in fragment order (cache hits).
+                yy_acc += ok ? y * y : 0.0;
+                const int fi = lane >> 2, fj = lane & 3;
+                double ya[8];
 #pragma unroll
-                for (int c0 = 0; c0 < KMAX; c0 += 8) {
-                    if (c0 < kv) {
-                        double v[8];
+                for (int q = 0; q < 8; ++q) {
+                    const double t = __shfl_sync(0xffffffffu, y, 4 * q + fj);
+                    ya[q] = fi == 0 ? t : 0.0;
+                }
+                const int64_t r0 = tile * 32;
 #pragma unroll
-                        for (int cc = 0; cc < 8; ++cc) v[cc] = ur[c0 + cc] * y;
-                        warp_butterfly<3>(v, lane);
-                        const int idx = (lane >> 2) & 7;
-                        if ((lane & 3) == 0 && c0 + idx < kv) acc[warp][c0 + idx] += v[0];
+                for (int g = 0; g < KMAX / 8; ++g) {
+                    if (8 * g < kv) {
+                        const int c = 8 * g + fi;
+                        const bool cok = c < kv;
+                        const double* up = a.U + (int64_t)c * a.ldu + r0 + fj;
+                        double bu[8];
+#pragma unroll
+                        for (int q = 0; q < 8; ++q) bu[q] = (cok && r0 + 4 * q + fj < a.nrows) ? __ldg(up + 4 * q) : 0.0;
+#pragma unroll
+                        for (int q = 0; q < 8; ++q) dmma884(dacc[g], ya[q], bu[q]);
                     }
                 }
-                const double yy = warp_sum(y * y);
-                if (lane == 0) acc[warp][kv] += yy;
             }
         }
     }
@@ -569,6 +592,19 @@ __global__ void __launch_bounds__(CTA) k_upd(const UpdArgs a) {
     const int nv = do_dots ? kv + 1 : 0;
     __shared__ bool is_last;
     if (nv) {
+        // per-warp results: lane fi == 0 holds D[0][2 fj + e] = dot of column 8g + 2fj + e
+        const int fi = lane >> 2, fj = lane & 3;
+        if (fi == 0) {
+#pragma unroll
+            for (int g = 0; g < KMAX / 8; ++g)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const int c = 8 * g + 2 * fj + e;
+                    if (c < kv) acc[warp][c] = dacc[g][e];
+                }
+        }
+        const double yy = warp_sum(yy_acc);
+        if (lane == 0) acc[warp][kv] = yy;
         __syncthreads();
         for (int v = threadIdx.x; v < nv; v += CTA) {
             double s = 0.0;
@@ -872,7 +908,25 @@ __global__ void k_gather(const double* x, const int* idx, int64_t n, double* out
         out[i] = x[idx[i]];
 }
 
+}  // namespace trplk
+
+#include "staged.cuh"  // TMA-staged K1 / K2 (shares the device helpers above)
+
+namespace trplk {
+
 // ---------------------------------------------------------------- launchers
+// TRPLK_NO_TMA=1 selects the register-streaming K1/K2 (comparison / fallback of the same math)
+// Variant of the K1/K2 dot kernels (same arithmetic): "rs" (default) register stream + smem
+// transpose + DMMA; "tma" bulk-copy staged; "reg" DMMA fragments loaded straight from global.
+static int kvar() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("TRPLK_KVAR");
+        v = (e && !strcmp(e, "tma")) ? 1 : (e && !strcmp(e, "reg")) ? 2 : 0;
+    }
+    return v;
+}
+
 static int num_sms() {
     static int n = 0;
     if (n == 0) {
@@ -945,6 +999,13 @@ int kmax_bucket(int k) {
         break;
 
 void launch_sdots(const SdotsArgs& a, int kmax, cudaStream_t s) {
+    // inner-step K1 (and the T-column-only launches): TMA-staged basis stream
+    const bool k1_shape = a.A.nrows && a.out_mode <= 2 && a.set1 == 1 && (a.set2 == 0 || a.set2 == 2) &&
+                          (a.norm1 == 0 || a.norm1 == 1) && a.norm2 == 0 && a.x_dyn == 0 && a.uout == nullptr;
+    if (kmax > 0 && k1_shape) {
+        if (kvar() == 0 && launch_step1_rs(a, kmax, s)) return;
+        if (kvar() == 1 && launch_step1_tma(a, kmax, s)) return;
+    }
     if (kmax > 0 && a.out_mode != 4) {  // dots: DMMA accumulator kernel
         switch ((kmax + 7) / 8) {
             SDM_CASE(1)
@@ -969,13 +1030,22 @@ void launch_sdots(const SdotsArgs& a, int kmax, cudaStream_t s) {
     }
 }
 
-#define UP_CASE(KM)                                        \
-    case KM: {                                             \
-        auto kern = k_upd<KM>;                             \
-        kern<<<stream_grid(kern, a.nrows), CTA, 0, s>>>(a); \
+#define UP_CASE(KM)                                                \
+    case KM: {                                                     \
+        if (a.mode == 1 && a.dots) {                               \
+            auto kern = k_upd<KM, true>;                           \
+            kern<<<stream_grid(kern, a.nrows), CTA, 0, s>>>(a);    \
+        } else {                                                   \
+            auto kern = k_upd<KM, false>;                          \
+            kern<<<stream_grid(kern, a.nrows), CTA, 0, s>>>(a);    \
+        }                                                          \
     } break;
 
 void launch_upd(const UpdArgs& a, int kmax, cudaStream_t s) {
+    if (a.mode == 1 && a.dots) {
+        if (kvar() == 0 && launch_upd2_rs(a, kmax, s)) return;
+        if (kvar() == 1 && launch_upd2_tma(a, kmax, s)) return;
+    }
     switch (kmax) {
         UP_CASE(8)
         UP_CASE(16)
