@@ -44,6 +44,12 @@ trplk_status trplk_k_rotate(trplk_ctx* ctx, const double* U, int64_t ldu, int k,
  * (Alg.1 step 11; R10/R11 ordering and sign rule). */
 trplk_status trplk_k_sym_eig(trplk_ctx* ctx, int k, const double* T, double* theta, double* Y);
 
+/* Timing of the Rayleigh-Ritz kernel alone (measurement): the one-CTA Jacobi of sym(T) (k x k,
+ * column-major host array) launched `reps` times back to back on the context's stream, timed
+ * with CUDA events.  *ms = average device milliseconds per launch, *sweeps = Jacobi sweeps the
+ * last launch took (nullable).  Errors: EINVAL (k, reps), ECUDA. */
+trplk_status trplk_k_sym_eig_time(trplk_ctx* ctx, int k, const double* T, int reps, double* ms, int* sweeps);
+
 /* r = A x - theta B x (Alg.1 step 12), u = M r (step 15 seed), rnorm2 = ||r||^2. */
 trplk_status trplk_k_residual(trplk_ctx* ctx, const double* x, double theta, double* r, double* u,
                               double* rnorm2);

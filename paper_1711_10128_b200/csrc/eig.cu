@@ -10,6 +10,9 @@
 // ends the iteration); the rotated entry is set to exactly 0.  Output: ascending Theta (stable
 // on ties), Y with the largest-magnitude entry of each column positive (R11); T is then reset
 // to diag(Theta(1:p^)) for the restart (R10).
+#include <cstdlib>
+#include <cstring>
+
 #include "trplk_internal.cuh"
 
 namespace trplk {
@@ -23,7 +26,7 @@ __device__ __forceinline__ int rr_player(int pos, int r, int kk) {
     return pos == 0 ? 0 : 1 + (pos - 1 + r) % (kk - 1);
 }
 
-__global__ void __launch_bounds__(EIG_THREADS) k_eig(Ctl* ctl, double* T, int ldT, double* Y, int ldY, int ph,
+__global__ void __launch_bounds__(EIG_THREADS) k_eig_2b(Ctl* ctl, double* T, int ldT, double* Y, int ldY, int ph,
                                                      int k_fixed, unsigned gate) {
     if ((ctl->flags & gate) != gate) return;
     const int k = k_fixed > 0 ? k_fixed : ctl->k;
@@ -73,7 +76,9 @@ __global__ void __launch_bounds__(EIG_THREADS) k_eig(Ctl* ctl, double* T, int ld
     }
     __syncthreads();
     const double eps = 2.220446049250313e-16;
+    int nsw = 1;
     for (int sweep = 0; sweep < 100 && k > 1; ++sweep) {
+        nsw = sweep + 1;
         if (tid == 0) rotated = 0;
         __syncthreads();
         for (int r = 0; r < kk - 1; ++r) {
@@ -187,18 +192,311 @@ __global__ void __launch_bounds__(EIG_THREADS) k_eig(Ctl* ctl, double* T, int ld
             T[i + (int64_t)j * ldT] = (i == j && i < ph) ? ctl->theta[i] : 0.0;
         }
     }
-    if (tid == 0) ctl->k_rr = k;
+    if (tid == 0) {
+        ctl->k_rr = k;
+        ctl->eig_sweeps = nsw;
+    }
 }
 
+// ------------------------------------------------------------------------------------------
+// One-barrier-per-round variant (default).  A is double-buffered: round r reads A_r and writes
+// A_{r+1}, so within one phase
+//   warp 0      computes the rotation parameters of round r+1: for its pivot (x, y) it forms
+//               the new entry A_{r+1}[x,y] from A_r and the round-r rotations of the two pairs
+//               holding x and y (the same 2x2 formula the block update uses) and takes the new
+//               diagonal entries from the round-r parameter step;
+//   warps 1..7  apply the round-r rotations: 2x2 blocks J_i^T A_r[P_i,P_j] J_j -> A_{r+1}
+//               (every entry of A is in exactly one block) and V <- V J;
+// and a round costs one barrier.  Same rotations in the same order, same skip rule and
+// sweep-end test as k_eig_2b (and the oracle's rule): only the schedule differs.
+constexpr int BLK_WARPS = 7;                         // warps 1..7: 2x2 block updates
+constexpr int EIG1_THREADS = 32 * (1 + BLK_WARPS) + 256;  // + 8 warps: V columns
+
+__device__ __forceinline__ int rr_pos(int x, int r, int kk) {  // position of player x in round r
+    if (x == 0) return 0;
+    const int m = kk - 1;
+    int v = (x - 1 - r) % m;
+    if (v < 0) v += m;
+    return v + 1;
+}
+
+__device__ __forceinline__ int pair_of_pos(int pos, int kk) { return pos < kk / 2 ? pos : kk - 1 - pos; }
+
+// 2x2 block update J_i^T [a b; c d] J_j (rotation (c1,s1) of pair i, (c2,s2) of pair j)
+__device__ __forceinline__ void block22(double a, double b, double c, double d, double c1, double s1, double c2,
+                                        double s2, double& m00, double& m01, double& m10, double& m11) {
+    const double n00 = a * c2 - b * s2, n01 = a * s2 + b * c2;
+    const double n10 = c * c2 - d * s2, n11 = c * s2 + d * c2;
+    m00 = c1 * n00 - s1 * n10;
+    m01 = c1 * n01 - s1 * n11;
+    m10 = s1 * n00 + c1 * n10;
+    m11 = s1 * n01 + c1 * n11;
+}
+
+// Rotation of the pivot (p,q), p < q < k, from a_pp, a_qq, a_pq (skip rule of the oracle:
+// |a_pq| <= eps sqrt|a_pp a_qq| or <= 1e-30 ||T||_F is not rotated); also the new diagonal.
+__device__ __forceinline__ void jacobi_param(double app, double aqq, double apq, double fro, double& c, double& s,
+                                             double& dp, double& dq, int& act) {
+    const double eps = 2.220446049250313e-16;
+    c = 1.0;
+    s = 0.0;
+    dp = app;
+    dq = aqq;
+    act = 0;
+    if (!(fabs(apq) <= eps * sqrt(fabs(app * aqq)) || fabs(apq) <= 1e-30 * fro)) {
+        const double d = aqq - app, b = 2.0 * apq;
+        const double t = ((d == 0.0 || ((d > 0.0) == (b > 0.0))) ? 1.0 : -1.0) * fabs(b) /
+                         (fabs(d) + sqrt(d * d + b * b));
+        c = rsqrt(1.0 + t * t);
+        s = t * c;
+        double m00, m01, m10, m11;
+        block22(app, apq, apq, aqq, c, s, c, s, m00, m01, m10, m11);
+        dp = m00;
+        dq = m11;
+        act = 1;
+    }
+}
+
+__global__ void __launch_bounds__(EIG1_THREADS) k_eig(Ctl* ctl, double* T, int ldT, double* Y, int ldY, int ph,
+                                                      int k_fixed, unsigned gate) {
+    if ((ctl->flags & gate) != gate) return;
+    const int k = k_fixed > 0 ? k_fixed : ctl->k;
+    extern __shared__ double sm[];
+    double* V = sm + 2 * QMAX * ELD;  // A_r, A_{r+1} at sm + (r & 1) * QMAX * ELD
+    __shared__ double pc[2][MAXPAIRS], ps[2][MAXPAIRS], pdp[2][MAXPAIRS], pdq[2][MAXPAIRS];
+    __shared__ int pp[2][MAXPAIRS], pq[2][MAXPAIRS], pact[2][MAXPAIRS];
+    __shared__ double red[EIG1_THREADS];
+    __shared__ int ord[QMAX];
+    __shared__ unsigned char bi[MAXBLK], bj[MAXBLK];
+    __shared__ unsigned char plr[QMAX - 1][QMAX], pairof[QMAX - 1][QMAX];  // player at pos; pair of player
+    __shared__ int rot[101];
+    __shared__ double fro;
+    const int tid = threadIdx.x;
+    double f = 0.0;
+    {
+        const int kk0 = k + (k & 1);
+        for (int idx = tid; idx < (kk0 - 1) * kk0; idx += EIG1_THREADS) {
+            const int r = idx / kk0, pos = idx % kk0;
+            const int x = rr_player(pos, r, kk0);
+            plr[r][pos] = (unsigned char)x;
+            pairof[r][x] = (unsigned char)(pos < kk0 / 2 ? pos : kk0 - 1 - pos);
+        }
+    }
+    for (int idx = tid; idx < k * k; idx += EIG1_THREADS) {
+        const int i = idx % k, j = idx / k;
+        const double a = 0.5 * (T[i + (int64_t)j * ldT] + T[j + (int64_t)i * ldT]);  // sym(T)
+        sm[i + j * ELD] = a;
+        V[i + j * ELD] = (i == j) ? 1.0 : 0.0;
+        f += a * a;
+    }
+    const int kk = k + (k & 1);
+    const int npairs = kk / 2;
+    const int nblk = npairs * (npairs + 1) / 2;
+    const int nr = kk - 1;  // rounds per sweep
+    if (tid == 0) {
+        int b = 0;
+        for (int i = 0; i < npairs; ++i)
+            for (int j = i; j < npairs; ++j) {
+                bi[b] = (unsigned char)i;
+                bj[b] = (unsigned char)j;
+                ++b;
+            }
+    }
+    for (int i = tid; i < 101; i += EIG1_THREADS) rot[i] = 0;
+    red[tid] = f;
+    __syncthreads();
+    if (tid == 0) {
+        double s = 0.0;
+        for (int i = 0; i < EIG1_THREADS; ++i) s += red[i];
+        fro = sqrt(s);
+    }
+    __syncthreads();
+    const int maxsweep = 100;
+    if (k > 1 && tid < npairs) {  // parameters of round 0 of sweep 0
+        int p = rr_player(tid, 0, kk), q = rr_player(kk - 1 - tid, 0, kk);
+        if (p > q) { const int t = p; p = q; q = t; }
+        double c = 1.0, s = 0.0, dp = sm[p + p * ELD], dq = 0.0;
+        int act = 0;
+        if (q < k) jacobi_param(sm[p + p * ELD], sm[q + q * ELD], sm[p + q * ELD], fro, c, s, dp, dq, act);
+        pc[0][tid] = c; ps[0][tid] = s; pdp[0][tid] = dp; pdq[0][tid] = dq;
+        pp[0][tid] = p; pq[0][tid] = q; pact[0][tid] = act;
+        if (act) rot[0] = 1;
+    }
+    __syncthreads();
+    int sweep = 0, r = 0, cur = 0;
+    const int warp = tid >> 5;
+    while (k > 1) {
+        const int nxt = cur ^ 1;
+        const int rn = r + 1 == nr ? 0 : r + 1;
+        const int sn = r + 1 == nr ? sweep + 1 : sweep;
+        const double* __restrict__ Ac = sm + cur * (QMAX * ELD);
+        double* __restrict__ An = sm + nxt * (QMAX * ELD);
+        if (warp == 0) {
+            // rotation parameters of round r+1 (pair m = lane)
+            const int m = tid;
+            if (m < npairs && sn < maxsweep) {
+                int x = plr[rn][m], y = plr[rn][kk - 1 - m];
+                if (x > y) { const int t = x; x = y; y = t; }
+                double c = 1.0, s = 0.0, dx, dy = 0.0;
+                int act = 0;
+                const int i = pairof[r][x];
+                const bool xp = pp[cur][i] == x;
+                dx = xp ? pdp[cur][i] : pdq[cur][i];
+                if (y < k) {
+                    const int j = pairof[r][y];
+                    const bool yp = pp[cur][j] == y;
+                    dy = yp ? pdp[cur][j] : pdq[cur][j];
+                    double axy;
+                    if (i == j) {  // only for k <= 2: the same pair again
+                        axy = pact[cur][i] ? 0.0 : Ac[x + y * ELD];
+                    } else {
+                        // entry (x, y) of J_i^T A_r[P_i, P_j] J_j, x in pair i, y in pair j
+                        const int p1 = pp[cur][i], q1 = pq[cur][i], p2 = pp[cur][j], q2 = pq[cur][j];
+                        const bool q1ok = q1 < k, q2ok = q2 < k;
+                        const double a = Ac[p1 + p2 * ELD];
+                        const double bb = q2ok ? Ac[p1 + q2 * ELD] : 0.0;
+                        const double cc = q1ok ? Ac[q1 + p2 * ELD] : 0.0;
+                        const double dd = (q1ok && q2ok) ? Ac[q1 + q2 * ELD] : 0.0;
+                        double m00, m01, m10, m11;
+                        block22(a, bb, cc, dd, pc[cur][i], ps[cur][i], pc[cur][j], ps[cur][j], m00, m01, m10, m11);
+                        axy = xp ? (yp ? m00 : m01) : (yp ? m10 : m11);
+                    }
+                    jacobi_param(dx, dy, axy, fro, c, s, dx, dy, act);
+                }
+                pc[nxt][m] = c; ps[nxt][m] = s; pdp[nxt][m] = dx; pdq[nxt][m] = dy;
+                pp[nxt][m] = x; pq[nxt][m] = y; pact[nxt][m] = act;
+                if (act) rot[sn] = 1;
+            }
+        } else {
+            if (warp < 1 + BLK_WARPS) {
+                // 2x2 block updates of round r: A_r -> A_{r+1} (A_r and A_{r+1} are distinct
+                // buffers, so the loads of later blocks are not ordered after earlier stores)
+                const int t2 = tid - 32;
+                for (int b = t2; b < nblk; b += 32 * BLK_WARPS) {
+                    const int i = bi[b], j = bj[b];
+                    const int p1 = pp[cur][i], q1 = pq[cur][i], p2 = pp[cur][j], q2 = pq[cur][j];
+                    const bool q1ok = q1 < k, q2ok = q2 < k;
+                    const double a = Ac[p1 + p2 * ELD];
+                    const double bb = q2ok ? Ac[p1 + q2 * ELD] : 0.0;
+                    const double cc = q1ok ? Ac[q1 + p2 * ELD] : 0.0;
+                    const double dd = (q1ok && q2ok) ? Ac[q1 + q2 * ELD] : 0.0;
+                    const int ai = pact[cur][i], aj = pact[cur][j];
+                    double m00 = a, m01 = bb, m10 = cc, m11 = dd;
+                    if (i == j) {
+                        if (ai) {
+                            m00 = pdp[cur][i];
+                            m11 = pdq[cur][i];
+                            m01 = m10 = 0.0;
+                        }
+                    } else if (ai || aj) {
+                        block22(a, bb, cc, dd, pc[cur][i], ps[cur][i], pc[cur][j], ps[cur][j], m00, m01, m10, m11);
+                    }
+                    An[p1 + p2 * ELD] = m00;
+                    An[p2 + p1 * ELD] = m00;
+                    if (q2ok) {
+                        An[p1 + q2 * ELD] = m01;
+                        An[q2 + p1 * ELD] = m01;
+                    }
+                    if (q1ok) {
+                        An[q1 + p2 * ELD] = m10;
+                        An[p2 + q1 * ELD] = m10;
+                    }
+                    if (q1ok && q2ok) {
+                        An[q1 + q2 * ELD] = m11;
+                        An[q2 + q1 * ELD] = m11;
+                    }
+                }
+            } else {
+                // V <- V J for the pairs of round r: thread = (row, pair slot), all loads first
+                const int tv = tid - 32 * (1 + BLK_WARPS);
+                const int row = tv & (QMAX - 1), slot = tv >> 6;  // 4 slots x 64 rows
+                constexpr int NPV = MAXPAIRS / 4;
+                double vp[NPV], vq[NPV], c_[NPV], s_[NPV];
+                int pidx[NPV], qidx[NPV];
+                bool on[NPV];
+#pragma unroll
+                for (int u = 0; u < NPV; ++u) {
+                    const int pi = slot + 4 * u;
+                    on[u] = row < k && pi < npairs && pact[cur][pi];
+                    if (on[u]) {
+                        pidx[u] = row + pp[cur][pi] * ELD;
+                        qidx[u] = row + pq[cur][pi] * ELD;
+                        c_[u] = pc[cur][pi];
+                        s_[u] = ps[cur][pi];
+                        vp[u] = V[pidx[u]];
+                        vq[u] = V[qidx[u]];
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < NPV; ++u) {
+                    if (on[u]) {
+                        V[pidx[u]] = c_[u] * vp[u] - s_[u] * vq[u];
+                        V[qidx[u]] = s_[u] * vp[u] + c_[u] * vq[u];
+                    }
+                }
+            }
+        }
+        __syncthreads();
+        cur = nxt;
+        if (r + 1 == nr) {  // end of a sweep: stop after a sweep without rotations
+            if (!rot[sweep] || sn >= maxsweep) break;
+        }
+        r = rn;
+        sweep = sn;
+    }
+    const double* __restrict__ A = sm + cur * (QMAX * ELD);
+    // ascending order, stable on ties (R11)
+    if (tid < k) {
+        const double ti = A[tid + tid * ELD];
+        int rank = 0;
+        for (int j = 0; j < k; ++j) {
+            const double tj = A[j + j * ELD];
+            rank += (tj < ti) || (tj == ti && j < tid);
+        }
+        ord[rank] = tid;
+    }
+    __syncthreads();
+    if (tid < k) {
+        const int src = ord[tid];
+        int imax = 0;
+        double vmax = -1.0;
+        for (int i = 0; i < k; ++i) {
+            const double a = fabs(V[i + src * ELD]);
+            if (a > vmax) { vmax = a; imax = i; }
+        }
+        const double sg = V[imax + src * ELD] < 0.0 ? -1.0 : 1.0;  // sign rule (R11)
+        for (int i = 0; i < k; ++i) Y[i + (int64_t)tid * ldY] = sg * V[i + src * ELD];
+        ctl->theta[tid] = A[src + src * ELD];
+    }
+    __syncthreads();
+    if (ph > 0) {  // restart: T <- diag(Theta(1:p^)) (R10)
+        for (int idx = tid; idx < QMAX * QMAX; idx += EIG1_THREADS) {
+            const int i = idx % QMAX, j = idx / QMAX;
+            T[i + (int64_t)j * ldT] = (i == j && i < ph) ? ctl->theta[i] : 0.0;
+        }
+    }
+    if (tid == 0) {
+        ctl->k_rr = k;
+        ctl->eig_sweeps = sweep + 1;
+    }
+}
+
+// TRPLK_EIG=2b selects the two-barrier reference variant (same rotations).
 void launch_eig(Ctl* ctl, double* T, int ldT, double* Y, int ldY, int ph, int k_fixed, unsigned gate,
                 cudaStream_t s) {
-    static bool init = false;
+    static int init = 0;
+    static bool two = false;
     const int smem = 2 * QMAX * ELD * (int)sizeof(double);
+    const int smem1 = 3 * QMAX * ELD * (int)sizeof(double);
     if (!init) {
-        cudaFuncSetAttribute(k_eig, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        init = true;
+        cudaFuncSetAttribute(k_eig, cudaFuncAttributeMaxDynamicSharedMemorySize, smem1);
+        cudaFuncSetAttribute(k_eig_2b, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        const char* e = getenv("TRPLK_EIG");
+        two = e && !strcmp(e, "2b");
+        init = 1;
     }
-    k_eig<<<1, EIG_THREADS, smem, s>>>(ctl, T, ldT, Y, ldY, ph, k_fixed, gate);
+    if (two) k_eig_2b<<<1, EIG_THREADS, smem, s>>>(ctl, T, ldT, Y, ldY, ph, k_fixed, gate);
+    else k_eig<<<1, EIG1_THREADS, smem1, s>>>(ctl, T, ldT, Y, ldY, ph, k_fixed, gate);
 }
 
 }  // namespace trplk

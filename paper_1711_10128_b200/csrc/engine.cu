@@ -53,6 +53,8 @@ struct trplk_ctx {
     int rank = 0, nranks = 1;
     cudaStream_t stream = nullptr;       // internal non-blocking work stream (capturable)
     cudaStream_t user_stream = nullptr;  // the caller's stream; ordered with `stream` by events
+    cudaStream_t side = nullptr;         // captures the bodies of conditional graph nodes
+    bool use_cond = false;               // pass-3 kernels in conditional nodes when capturing (1 rank)
     cudaEvent_t ev_in = nullptr, ev_out = nullptr;
     trplk_allocator alloc{};
     bool has_alloc = false;
@@ -578,7 +580,23 @@ trplk_status cgs2(trplk_ctx* ctx, const CgsSpec& c) {
         a.gate = c.gate;
         ST(run_sdots(ctx, a, kn));
     }
-    // final: y = w1 - V h1, beta from Pythagoras; pass 3 into w2 if the norm dropped > 1/sqrt2
+    // final: y = w1 - V h1, beta from Pythagoras; pass 3 into w2 if the norm dropped > 1/sqrt2.
+    // Under graph capture (one rank) the pass-3 kernels go into a conditional node that the
+    // FINAL kernel switches on only when the third pass is needed (normally never), so the
+    // common path launches no gated no-op kernels.
+    cudaGraphConditionalHandle cond = 0;
+    cudaGraph_t capg = nullptr;
+    bool in_cond = false;
+    if (ctx->use_cond && ctx->nranks == 1) {
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        const cudaGraphNode_t* deps = nullptr;
+        size_t ndeps = 0;
+        CK(cudaStreamGetCaptureInfo(ctx->stream, &cs, nullptr, &capg, &deps, &ndeps));
+        if (cs == cudaStreamCaptureStatusActive) {
+            CK(cudaGraphConditionalHandleCreate(&cond, capg, 0, cudaGraphCondAssignDefault));
+            in_cond = true;
+        }
+    }
     if (c.mark_final) CK(cudaEventRecordWithFlags(c.mark_final, ctx->stream, cudaEventRecordExternal));
     {
         UpdArgs u = up_base(ctx);
@@ -597,7 +615,27 @@ trplk_status cgs2(trplk_ctx* ctx, const CgsSpec& c) {
         u.inc_k = c.inc_k;
         u.gate = c.gate;
         u.clear_on_brk = c.clear;
+        u.pass3_cond = in_cond ? (unsigned long long)cond : 0ull;
         ST(run_upd(ctx, u, kn));
+    }
+    cudaStream_t main_stream = ctx->stream;
+    const int64_t launches0 = ctx->launches;
+    if (in_cond) {
+        const cudaGraphNode_t* deps = nullptr;
+        size_t ndeps = 0;
+        cudaStreamCaptureStatus cs;
+        CK(cudaStreamGetCaptureInfo(ctx->stream, &cs, nullptr, &capg, &deps, &ndeps));
+        cudaGraphNodeParams np{};
+        np.type = cudaGraphNodeTypeConditional;
+        np.conditional.handle = cond;
+        np.conditional.type = cudaGraphCondTypeIf;
+        np.conditional.size = 1;
+        cudaGraphNode_t node;
+        CK(cudaGraphAddNode(&node, capg, deps, ndeps, &np));
+        CK(cudaStreamUpdateCaptureDependencies(ctx->stream, &node, 1, cudaStreamSetCaptureDependencies));
+        CK(cudaStreamBeginCaptureToGraph(ctx->side, np.conditional.phGraph_out[0], nullptr, nullptr, 0,
+                                         cudaStreamCaptureModeThreadLocal));
+        ctx->stream = ctx->side;  // the two pass-3 launches below are captured into the body
     }
     {  // third-pass dots h3 = V^T B w2, N_2SQ_EXP = w2^T B w2 (gated on ctl->pass3, normally a no-op)
         SdotsArgs a = sd_base(ctx);
@@ -636,6 +674,12 @@ trplk_status cgs2(trplk_ctx* ctx, const CgsSpec& c) {
         u.gate = c.gate;
         u.clear_on_brk = c.clear;
         ST(run_upd(ctx, u, kn));
+    }
+    if (in_cond) {
+        ctx->stream = main_stream;
+        cudaGraph_t body = nullptr;
+        CK(cudaStreamEndCapture(ctx->side, &body));
+        ctx->launches = launches0;  // the body normally does not run
     }
     return TRPLK_OK;
 }
@@ -793,7 +837,7 @@ trplk_status issue_cycle(trplk_ctx* ctx, const Sizes& S, int cur, int nprev, int
     // Rayleigh-Ritz (step 11) and rotation X = U Y(:,1:p^) into the other buffer
     launch_eig(ctx->ctl, ctx->T, QMAX, ctx->Yg, QMAX, S.ph, 0, F_CYCLE, ctx->stream);
     CK(cudaGetLastError());
-    launch_rotate(Uc, ld, ctx->n_loc, ctx->ctl, 0, ctx->Yg, QMAX, S.ph, Uo, ld, F_CYCLE, ctx->stream);
+    launch_rotate(Uc, ld, ctx->n_loc, ctx->ctl, 0, ctx->Yg, QMAX, S.ph, Uo, ld, F_CYCLE, ctx->stream, S.q);
     ctx->launches += 2;
     CK(cudaGetLastError());
     ctx->model_bytes += vec_bytes(ctx) * (S.q + S.ph);
@@ -1086,7 +1130,13 @@ trplk_status trplk_create(trplk_ctx** out, int64_t n_global, const int64_t* a_ro
     trplk_ctx* ctx = new trplk_ctx();
     *out = ctx;
     ctx->user_stream = (cudaStream_t)stream;
+    {  // measured on B200 (C2): the conditional node costs more than the two no-op launches it
+       // replaces (94.4 vs 81.9 ms per solve), so it is opt-in (TRPLK_COND=1)
+        const char* e = getenv("TRPLK_COND");
+        ctx->use_cond = e && e[0] == '1';
+    }
     if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreateWithFlags(&ctx->ev_in, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&ctx->ev_out, cudaEventDisableTiming) != cudaSuccess) {
         ctx->err = "cannot create the work stream";
@@ -1115,6 +1165,7 @@ void trplk_destroy(trplk_ctx* ctx) {
         if (e) cudaEventDestroy(e);
     if (ctx->ev_out) cudaEventDestroy(ctx->ev_out);
     if (ctx->stream) cudaStreamDestroy(ctx->stream);
+    if (ctx->side) cudaStreamDestroy(ctx->side);
     if (ctx->comm) ncclCommDestroy(ctx->comm);
     delete ctx;
 }
@@ -1255,8 +1306,8 @@ static trplk_status solve_impl(trplk_ctx* ctx, int p, int q, int l, double tol, 
         }
         launch_eig(ctx->ctl, ctx->T, QMAX, ctx->Yg, QMAX, ph, ph, 0, ctx->stream);
         launch_rotate(ctx->U[cur], ld, ctx->n_loc, ctx->ctl, ph, ctx->Yg, QMAX, ph, ctx->U[1 - cur], ld, 0,
-                      ctx->stream);
-        launch_rotate(ctx->Wtmp, ld, ctx->n_loc, ctx->ctl, ph, ctx->Yg, QMAX, ph, ctx->U[cur], ld, 0, ctx->stream);
+                      ctx->stream, ph);
+        launch_rotate(ctx->Wtmp, ld, ctx->n_loc, ctx->ctl, ph, ctx->Yg, QMAX, ph, ctx->U[cur], ld, 0, ctx->stream, ph);
         CK(cudaGetLastError());
         cur = 1 - cur;  // X in U[cur], A X in U[1-cur]
         // r = A x_1 - theta_1 B x_1 from W (no matvec), u = M r
@@ -1584,7 +1635,7 @@ trplk_status trplk_k_rotate(trplk_ctx* ctx, const double* U, int64_t ldu, int k,
     }
     CK(cudaMemcpy2DAsync(ctx->Yg, 8 * QMAX, Y, 8 * (size_t)k, 8 * (size_t)k, ncol, cudaMemcpyHostToDevice,
                          ctx->stream));
-    launch_rotate(U, ldu, ctx->n_loc, ctx->ctl, k, ctx->Yg, QMAX, ncol, X, ldx, 0, ctx->stream);
+    launch_rotate(U, ldu, ctx->n_loc, ctx->ctl, k, ctx->Yg, QMAX, ncol, X, ldx, 0, ctx->stream, k);
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(ctx->stream));
     return TRPLK_OK;
@@ -1604,6 +1655,35 @@ trplk_status trplk_k_sym_eig(trplk_ctx* ctx, int k, const double* T, double* the
     ST(ctl_pull(ctx));
     if (theta) memcpy(theta, ctx->ctl_h->theta, 8 * (size_t)k);
     if (Y) CK(cudaMemcpy2D(Y, 8 * (size_t)k, ctx->Yg, 8 * QMAX, 8 * (size_t)k, k, cudaMemcpyDeviceToHost));
+    dev_free(ctx, Td);
+    return TRPLK_OK;
+}
+
+trplk_status trplk_k_sym_eig_time(trplk_ctx* ctx, int k, const double* T, int reps, double* ms, int* sweeps) {
+    ST(kprep(ctx, k));
+    if (k < 1 || reps < 1) {
+        ctx->err = "k < 1 or reps < 1";
+        return TRPLK_EINVAL;
+    }
+    double* Td;
+    ST(dalloc(ctx, &Td, (size_t)QMAX * QMAX));
+    CK(cudaMemcpy2DAsync(Td, 8 * QMAX, T, 8 * (size_t)k, 8 * (size_t)k, k, cudaMemcpyHostToDevice, ctx->stream));
+    launch_eig(ctx->ctl, Td, QMAX, ctx->Yg, QMAX, 0, k, 0, ctx->stream);  // warm-up
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    CK(cudaEventRecord(e0, ctx->stream));
+    for (int i = 0; i < reps; ++i) launch_eig(ctx->ctl, Td, QMAX, ctx->Yg, QMAX, 0, k, 0, ctx->stream);
+    CK(cudaEventRecord(e1, ctx->stream));
+    CK(cudaEventSynchronize(e1));
+    float t = 0.f;
+    CK(cudaEventElapsedTime(&t, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    CK(cudaGetLastError());
+    ST(ctl_pull(ctx));
+    if (ms) *ms = (double)t / reps;
+    if (sweeps) *sweeps = ctx->ctl_h->eig_sweeps;
     dev_free(ctx, Td);
     return TRPLK_OK;
 }

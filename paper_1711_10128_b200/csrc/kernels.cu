@@ -106,10 +106,14 @@ __device__ __forceinline__ double mat_row(const Sell& M, int64_t s, int lane, co
     return acc;
 }
 
-// Deterministic two-level grid reduction of the CTA's nv values `mine` (smem).  Returns true in
-// exactly one CTA, whose smem `out` then holds the grid sums.  The summation order is fixed:
-// CTAs in groups of RG (lane = CTA in group, xor-butterfly), then the groups likewise.
+// Deterministic grid reduction of the CTA's nv values `mine` (smem).  Returns true in exactly
+// one CTA, whose smem `out` then holds the grid sums.  The summation order is fixed.
+// Grids of <= 1024 CTAs: one level -- the last CTA to arrive sums, per value, CTA partials
+// lane, lane+32, ... in order and then the 32 lanes by an xor butterfly (one global round trip
+// less than two levels).  Larger grids: CTAs in groups of RG (lane = CTA in group, butterfly),
+// then the groups likewise.
 constexpr int RG = 32;
+constexpr int ONE_LEVEL_MAX = 1024;
 __device__ bool grid_reduce(const double* mine, int nv, double* part, double* gpart, unsigned* cnt, int maxcta,
                             double* out) {
     __shared__ bool flag;
@@ -118,6 +122,30 @@ __device__ bool grid_reduce(const double* mine, int nv, double* part, double* gp
     for (int v = tid; v < nv; v += blockDim.x) part[(int64_t)v * maxcta + bid] = mine[v];
     __threadfence();
     __syncthreads();
+    if (ncta <= ONE_LEVEL_MAX) {
+        if (tid == 0) flag = atomicAdd(&cnt[0], 1u) == (unsigned)(ncta - 1);
+        __syncthreads();
+        if (!flag) return false;
+        __threadfence();
+        const int nwarps = blockDim.x >> 5;
+        for (int v = warp; v < nv; v += nwarps) {
+            const double* pv = part + (int64_t)v * maxcta;
+            double s = 0.0;
+            constexpr int U = 8;
+            for (int c0 = lane; c0 < ncta; c0 += 32 * U) {
+                double t[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) t[u] = (c0 + 32 * u < ncta) ? __ldcg(pv + c0 + 32 * u) : 0.0;
+#pragma unroll
+                for (int u = 0; u < U; ++u) s += t[u];
+            }
+            s = warp_sum(s);
+            if (lane == 0) out[v] = s;
+        }
+        __syncthreads();
+        if (tid == 0) cnt[0] = 0u;
+        return true;
+    }
     const int g = bid / RG, g0 = g * RG, gs = min(RG, ncta - g0), ng = (ncta + RG - 1) / RG;
     if (tid == 0) flag = atomicAdd(&cnt[1 + g], 1u) == (unsigned)(gs - 1);
     __syncthreads();
@@ -484,7 +512,7 @@ __device__ void upd_finalize(const UpdArgs& a, const double* r, int kv) {
 // DOTS = true: mode 1 (update + U^T y dots); DOTS = false: modes 0 / 2 / 3 (no dots; the rare
 // third-pass dots are a separate gated k_sdots launch).
 template <int KMAX, bool DOTS>
-__global__ void __launch_bounds__(CTA, DOTS ? 2 : 3) k_upd(const UpdArgs a) {
+__global__ void __launch_bounds__(CTA, DOTS ? 2 : (KMAX <= 16 ? 3 : (KMAX <= 32 ? 2 : 1))) k_upd(const UpdArgs a) {
     Ctl* ctl = a.ctl;
     if ((ctl->flags & a.gate) != a.gate) return;
     if (a.mode == 3 && ctl->pass3 == 0) return;
@@ -539,19 +567,15 @@ __global__ void __launch_bounds__(CTA, DOTS ? 2 : 3) k_upd(const UpdArgs a) {
              tile += (int64_t)gridDim.x * WARPS) {
             const int64_t row = tile * 32 + lane;
             const bool ok = row < a.nrows;
-            // y = x - U h, columns in order; loads issued in chunks of 8 (the compiler hoists
-            // later chunks as far as the register budget allows)
+            // y = x - U h, columns in order; the whole row of U is loaded before the first FMA
+            // (KMAX loads in flight per lane)
             double y = ok ? X[row] : 0.0;
             const double* up = a.U + row;
+            double uk[KMAX];
 #pragma unroll
-            for (int cb = 0; cb < KMAX; cb += 8) {
-                double u8[8];
+            for (int c = 0; c < KMAX; ++c) uk[c] = (ok && c < kv) ? __ldg(up + (int64_t)c * a.ldu) : 0.0;
 #pragma unroll
-                for (int c = 0; c < 8; ++c)
-                    u8[c] = (ok && cb + c < kv) ? __ldg(up + (int64_t)(cb + c) * a.ldu) : 0.0;
-#pragma unroll
-                for (int c = 0; c < 8; ++c) y = fma(-hs[cb + c], u8[c], y);
-            }
+            for (int c = 0; c < KMAX; ++c) y = fma(-hs[c], uk[c], y);
             if (ok) {
                 if (write_y && a.out) a.out[row] = y;
                 if (write_dest) {
@@ -633,6 +657,7 @@ __global__ void __launch_bounds__(CTA, DOTS ? 2 : 3) k_upd(const UpdArgs a) {
             if (pass3) {
                 ctl->pass3 = 1;
                 ctl->pass3_count += 1;
+                if (a.pass3_cond) cudaGraphSetConditional((cudaGraphConditionalHandle)a.pass3_cond, 1u);
             } else if (brk) {
                 ctl->flags &= ~a.clear_on_brk;
                 ctl->brk += 1;
@@ -880,6 +905,74 @@ __global__ void __launch_bounds__(256) k_rotate(const double* __restrict__ U, in
     }
 }
 
+// Transposed-operand DMMA rotation (default): X^T = Y^T U^T, so the A operand (Y^T, p^ x k) is
+// loaded into registers once per warp and reused for every row tile, and the B operand is
+// U^T: lane (kk = l&3, n = l>>2) loads U[row0 + n, 4 ks + kk] -- 4 columns x 8 consecutive rows
+// per instruction, each column's 32 bytes x 4 row blocks of a 32-row tile forming full lines.
+// The accumulator D = X^T (8 output columns x 8 rows) holds 2 consecutive rows per lane,
+// written as one 16-byte store.  NJ = 8-column groups of X (p^ <= 8 NJ), KS4 = k-steps of 4
+// (k <= 4 KS4), RB = 8-row blocks per warp iteration (all RB*KS4 loads issued first).
+constexpr int ROT_CTA = 128;
+template <int NJ, int KS4, int RB>
+__global__ void __launch_bounds__(ROT_CTA, 2) k_rotate_t(const double* __restrict__ U, int64_t ldu, int64_t nrows,
+                                                       const Ctl* ctl, int k_fixed, const double* __restrict__ Y,
+                                                       int ldY, int ncol, double* __restrict__ X, int64_t ldx,
+                                                       unsigned gate) {
+    if ((ctl->flags & gate) != gate) return;
+    const int k = k_fixed > 0 ? k_fixed : ctl->k_rr;
+    const int lane = threadIdx.x & 31;
+    const int lq = lane & 3, lr = lane >> 2;
+    double yf[NJ][KS4];
+#pragma unroll
+    for (int jb = 0; jb < NJ; ++jb)
+#pragma unroll
+        for (int ks = 0; ks < KS4; ++ks) {
+            const int kk = 4 * ks + lq, j = 8 * jb + lr;
+            yf[jb][ks] = (kk < k && j < ncol) ? __ldg(Y + kk + (int64_t)j * ldY) : 0.0;
+        }
+    const int64_t gw = ((int64_t)blockIdx.x * ROT_CTA + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * ROT_CTA) >> 5;
+    const int64_t ntile = (nrows + 8 * RB - 1) / (8 * RB);
+    const bool vec = ((reinterpret_cast<uintptr_t>(X) & 15) == 0) && ((ldx & 1) == 0);
+    for (int64_t tile = gw; tile < ntile; tile += nw) {
+        const int64_t r0 = tile * (8 * RB);
+        double b[RB][KS4];
+#pragma unroll
+        for (int rb = 0; rb < RB; ++rb) {
+            const int64_t row = r0 + 8 * rb + lr;
+#pragma unroll
+            for (int ks = 0; ks < KS4; ++ks) {
+                const int kk = 4 * ks + lq;
+                b[rb][ks] = (row < nrows && kk < k) ? __ldg(U + (int64_t)kk * ldu + row) : 0.0;
+            }
+        }
+#pragma unroll
+        for (int rb = 0; rb < RB; ++rb) {
+            double acc[NJ][2];
+#pragma unroll
+            for (int jb = 0; jb < NJ; ++jb) {
+                acc[jb][0] = acc[jb][1] = 0.0;
+#pragma unroll
+                for (int ks = 0; ks < KS4; ++ks) dmma884(acc[jb], yf[jb][ks], b[rb][ks]);
+            }
+            const int64_t row = r0 + 8 * rb + 2 * lq;
+#pragma unroll
+            for (int jb = 0; jb < NJ; ++jb) {
+                const int j = 8 * jb + lr;
+                if (j < ncol) {
+                    double* xp = X + (int64_t)j * ldx + row;
+                    if (vec && row + 1 < nrows) {
+                        *reinterpret_cast<double2*>(xp) = make_double2(acc[jb][0], acc[jb][1]);
+                    } else {
+                        if (row < nrows) xp[0] = acc[jb][0];
+                        if (row + 1 < nrows) xp[1] = acc[jb][1];
+                    }
+                }
+            }
+        }
+    }
+}
+
 // ---------------------------------------------------------------- small kernels
 __device__ __forceinline__ double u01(uint64_t seed, uint64_t stream, uint64_t index) {
     // counter-based U[0,1): splitmix64 finaliser over (seed, stream, index), reading R13
@@ -910,19 +1003,23 @@ __global__ void k_gather(const double* x, const int* idx, int64_t n, double* out
 
 }  // namespace trplk
 
-#include "staged.cuh"  // TMA-staged K1 / K2 (shares the device helpers above)
+#include "staged.cuh"     // TMA-staged K1 / K2 (shares the device helpers above)
+#include "stream_tp.cuh"   // thread-per-row K1 / K2 (default)
 
 namespace trplk {
 
 // ---------------------------------------------------------------- launchers
 // TRPLK_NO_TMA=1 selects the register-streaming K1/K2 (comparison / fallback of the same math)
-// Variant of the K1/K2 dot kernels (same arithmetic): "rs" (default) register stream + smem
-// transpose + DMMA; "tma" bulk-copy staged; "reg" DMMA fragments loaded straight from global.
+// Variant of the inner-step K1/K2 dot kernels (same outputs): "rs" (default) register stream +
+// smem transpose + DMMA; "tp" thread-per-row register accumulators (stream_tp.cuh); "tma"
+// bulk-copy staged; "reg" DMMA fragments loaded straight from global.  The other dot launches
+// (CGS first pass, +K T columns, residual) use the thread-per-row kernel.  B200 comparison
+// (C2 / C3 inner step): profiles/r01_variants.md.
 static int kvar() {
     static int v = -1;
     if (v < 0) {
         const char* e = getenv("TRPLK_KVAR");
-        v = (e && !strcmp(e, "tma")) ? 1 : (e && !strcmp(e, "reg")) ? 2 : 0;
+        v = (e && !strcmp(e, "tma")) ? 1 : (e && !strcmp(e, "reg")) ? 2 : (e && !strcmp(e, "tp")) ? 0 : 3;
     }
     return v;
 }
@@ -1002,8 +1099,10 @@ void launch_sdots(const SdotsArgs& a, int kmax, cudaStream_t s) {
     // inner-step K1 (and the T-column-only launches): TMA-staged basis stream
     const bool k1_shape = a.A.nrows && a.out_mode <= 2 && a.set1 == 1 && (a.set2 == 0 || a.set2 == 2) &&
                           (a.norm1 == 0 || a.norm1 == 1) && a.norm2 == 0 && a.x_dyn == 0 && a.uout == nullptr;
+    if (kmax > 0 && (kvar() == 0 || (kvar() == 3 && !k1_shape)) && a.out_mode != 4 && launch_step1_tp(a, kmax, s))
+        return;
     if (kmax > 0 && k1_shape) {
-        if (kvar() == 0 && launch_step1_rs(a, kmax, s)) return;
+        if (kvar() == 3 && launch_step1_rs(a, kmax, s)) return;
         if (kvar() == 1 && launch_step1_tma(a, kmax, s)) return;
     }
     if (kmax > 0 && a.out_mode != 4) {  // dots: DMMA accumulator kernel
@@ -1043,7 +1142,8 @@ void launch_sdots(const SdotsArgs& a, int kmax, cudaStream_t s) {
 
 void launch_upd(const UpdArgs& a, int kmax, cudaStream_t s) {
     if (a.mode == 1 && a.dots) {
-        if (kvar() == 0 && launch_upd2_rs(a, kmax, s)) return;
+        if (kvar() == 0 && launch_upd2_tp(a, kmax, s)) return;
+        if (kvar() == 3 && launch_upd2_rs(a, kmax, s)) return;
         if (kvar() == 1 && launch_upd2_tma(a, kmax, s)) return;
     }
     switch (kmax) {
@@ -1059,8 +1159,51 @@ void launch_upd(const UpdArgs& a, int kmax, cudaStream_t s) {
 }
 
 
+template <int NJ, int KS4>
+static void rot_t(const double* U, int64_t ldu, int64_t nrows, const Ctl* ctl, int k_fixed, const double* Y,
+                  int ldY, int ncol, double* X, int64_t ldx, unsigned gate, cudaStream_t s) {
+    constexpr int RB = 2;
+    auto kern = k_rotate_t<NJ, KS4, RB>;
+    int occ = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, ROT_CTA, 0);
+    if (occ < 1) occ = 1;
+    const int64_t tiles = (nrows + 8 * RB - 1) / (8 * RB);
+    int64_t g = (tiles + ROT_CTA / 32 - 1) / (ROT_CTA / 32);
+    const int64_t cap = (int64_t)num_sms() * occ;
+    if (g > cap) g = cap;
+    if (g < 1) g = 1;
+    kern<<<(int)g, ROT_CTA, 0, s>>>(U, ldu, nrows, ctl, k_fixed, Y, ldY, ncol, X, ldx, gate);
+}
+
+template <int NJ>
+static void rot_t_k(int kmax, const double* U, int64_t ldu, int64_t nrows, const Ctl* ctl, int k_fixed,
+                    const double* Y, int ldY, int ncol, double* X, int64_t ldx, unsigned gate, cudaStream_t s) {
+    const int ks4 = (kmax + 3) / 4;
+    if (ks4 <= 2) rot_t<NJ, 2>(U, ldu, nrows, ctl, k_fixed, Y, ldY, ncol, X, ldx, gate, s);
+    else if (ks4 <= 4) rot_t<NJ, 4>(U, ldu, nrows, ctl, k_fixed, Y, ldY, ncol, X, ldx, gate, s);
+    else if (ks4 <= 6) rot_t<NJ, 6>(U, ldu, nrows, ctl, k_fixed, Y, ldY, ncol, X, ldx, gate, s);
+    else if (ks4 <= 8) rot_t<NJ, 8>(U, ldu, nrows, ctl, k_fixed, Y, ldY, ncol, X, ldx, gate, s);
+    else if (ks4 <= 10) rot_t<NJ, 10>(U, ldu, nrows, ctl, k_fixed, Y, ldY, ncol, X, ldx, gate, s);
+    else if (ks4 <= 12) rot_t<NJ, 12>(U, ldu, nrows, ctl, k_fixed, Y, ldY, ncol, X, ldx, gate, s);
+    else rot_t<NJ, 16>(U, ldu, nrows, ctl, k_fixed, Y, ldY, ncol, X, ldx, gate, s);
+}
+
+// kmax: upper bound of the device-side width (k_fixed, or the solve's max basis q).
+// TRPLK_ROT=mma8 selects the row-operand variant k_rotate (8-row tiles, Y in shared memory).
 void launch_rotate(const double* U, int64_t ldu, int64_t nrows, const Ctl* ctl, int k_fixed, const double* Y,
-                   int ldY, int ncol, double* X, int64_t ldx, unsigned gate, cudaStream_t s) {
+                   int ldY, int ncol, double* X, int64_t ldx, unsigned gate, cudaStream_t s, int kmax) {
+    static int var = -1;
+    if (var < 0) {
+        const char* e = getenv("TRPLK_ROT");
+        var = (e && !strcmp(e, "mma8")) ? 1 : 0;
+    }
+    if (k_fixed > 0) kmax = k_fixed;
+    if (var == 0 && kmax <= 64 && ncol <= 24) {
+        if (ncol <= 8) rot_t_k<1>(kmax, U, ldu, nrows, ctl, k_fixed, Y, ldY, ncol, X, ldx, gate, s);
+        else if (ncol <= 16) rot_t_k<2>(kmax, U, ldu, nrows, ctl, k_fixed, Y, ldY, ncol, X, ldx, gate, s);
+        else rot_t_k<3>(kmax, U, ldu, nrows, ctl, k_fixed, Y, ldY, ncol, X, ldx, gate, s);
+        return;
+    }
     const int64_t tiles = (nrows + 7) / 8;
     int64_t g = (tiles + 7) / 8;
     const int64_t cap = (int64_t)num_sms() * 8;

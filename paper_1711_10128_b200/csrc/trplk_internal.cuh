@@ -62,6 +62,7 @@ struct Ctl {
     int k_rr;         // width used by the last Rayleigh-Ritz
     int brk;          // breakdown events (diagnostic, cumulative)
     int pass3_count;  // third CGS passes taken (cumulative)
+    int eig_sweeps;   // Jacobi sweeps of the last Rayleigh-Ritz (diagnostic)
     double nrm[N_SLOTS];
     double h[4][QMAX];
     double theta[QMAX];
@@ -134,6 +135,9 @@ struct UpdArgs {
     unsigned* counter;
     int maxcta;
     double* red_local;
+    // FINAL (mode 2) inside a captured graph: set to 1 when a third CGS pass is needed, so the
+    // conditional node holding the pass-3 kernels runs only then (0 = no conditional node)
+    unsigned long long pass3_cond;
 };
 
 // Kernel launchers (kernels.cu)
@@ -143,7 +147,7 @@ void launch_eig(Ctl* ctl, double* T, int ldT, double* Y, int ldY, int ph, int k_
                 cudaStream_t s);
 void launch_rotate(const double* U, int64_t ldu, int64_t nrows, const Ctl* ctl, int k_fixed,
                    const double* Y, int ldY, int ncol, double* X, int64_t ldx, unsigned gate,
-                   cudaStream_t s);
+                   cudaStream_t s, int kmax);
 void launch_random(double* x, int64_t nrows, int64_t row0, int64_t n_global, uint64_t seed,
                    uint64_t stream, uint64_t col, cudaStream_t s);
 void launch_finalize_sdots_multi(const SdotsArgs& sd, const double* red_all, int nranks, int stride,

@@ -82,6 +82,7 @@ _sig("trplk_k_cgs2", _I, [_P, _P, _I64, _I, _P, _P, _P, _P, _P, _P])
 _sig("trplk_k_rotate", _I, [_P, _P, _I64, _I, _P, _I, _P, _I64])
 _sig("trplk_k_sym_eig", _I, [_P, _I, _P, _P, _P])
 _sig("trplk_k_residual", _I, [_P, _P, _D, _P, _P, _P])
+_sig("trplk_k_sym_eig_time", _I, [_P, _I, _P, _I, _P, _P])
 _sig("trplk_k_random", _I, [_P, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64, _P])
 _sig("trplk_plan_ghosts", _I, [_I64, _I64, _P, _P, _P, _P, _P, _I, _P, _P, _I64, ctypes.POINTER(_I64)])
 _sig("trplk_profile", _I, [_P, _I])
@@ -91,7 +92,7 @@ EXPORTED = ["trplk_options_default", "trplk_nccl_unique_id", "trplk_create", "tr
             "trplk_get_log", "trplk_info", "trplk_destroy", "trplk_last_error", "trplk_k_spmv",
             "trplk_k_step1", "trplk_k_cgs2", "trplk_k_rotate", "trplk_k_sym_eig",
             "trplk_k_residual", "trplk_k_random", "trplk_profile", "trplk_profile_read",
-            "trplk_plan_ghosts"]
+            "trplk_plan_ghosts", "trplk_k_sym_eig_time"]
 
 
 class TrplkError(RuntimeError):
@@ -327,6 +328,16 @@ def trplk_k_sym_eig(ctx, T):
     Y = np.zeros((k, k), order="F")
     ctx.check(_lib.trplk_k_sym_eig(ctx.handle, k, _ptr(T), _ptr(th), _ptr(Y)))
     return th, Y
+
+
+def trplk_k_sym_eig_time(ctx, T, reps=50):
+    """Average device ms per launch of the Rayleigh-Ritz kernel on sym(T), and its sweep count."""
+    T = np.asfortranarray(T, np.float64)
+    ms = _D()
+    sw = ctypes.c_int()
+    ctx.check(_lib.trplk_k_sym_eig_time(ctx.handle, T.shape[0], _ptr(T), int(reps), ctypes.byref(ms),
+                                        ctypes.byref(sw)))
+    return ms.value, sw.value
 
 
 def trplk_k_residual(ctx, x, theta, r=None, u=None):

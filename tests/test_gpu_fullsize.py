@@ -35,6 +35,18 @@ def _near_tie(thetas, res, tol):
     return bool(np.any(np.abs(np.diff(th)) <= 1e-10 * np.abs(th[1:])) or abs(res - tol) <= 1e-2 * tol)
 
 
+def _emergence(log, c):
+    """Cycle c of a run is an emergence event (reading R17): with the target t unchanged, theta_t
+    fell by more than the previous residual ||r_t||, i.e. by more than the distance from the old
+    Ritz value to the nearest eigenvalue, so the Ritz value moved to ANOTHER eigenvalue.  For an
+    exactly degenerate spectrum (C3: multiplicities 3 and 6) the Krylov space grows a new copy of
+    a cluster only from rounding-level components, so when that happens depends on the rounding
+    of the run, not on the method; the trajectories may part there."""
+    if c == 0 or log["t"][c] != log["t"][c - 1]:
+        return False
+    return log["theta_t"][c - 1] - log["theta_t"][c] > log["res"][c - 1]
+
+
 @pytest.mark.parametrize("name", ["C2", "C3", "C4"])
 def test_fullsize_vs_oracle_golden(gen, name):
     torch, trplk = need_gpu()
@@ -54,7 +66,9 @@ def test_fullsize_vs_oracle_golden(gen, name):
         same = (lo["t"][c] == log["t"][c] and lo["k"][c] == log["k"][c] and lo["nprev"][c] == log["nprev"][c]
                 and abs(lo["theta_t"][c] - log["theta_t"][c]) <= 1e-10 * abs(lo["theta_t"][c]) + 1e-13 * nA)
         if not same:
-            assert _near_tie(g["log_thetas"][c], lo["res"][c], P.tol), f"diverged at cycle {c} without a near-tie"
+            ok = _near_tie(g["log_thetas"][c], lo["res"][c], P.tol) or any(
+                _emergence(L, cc) for L in (lo, log) for cc in range(max(c - 1, 1), min(c + 2, n)))
+            assert ok, f"diverged at cycle {c} without a near-tie or an emergence event"
             break
     else:
         assert st["a_matvecs"] == g["a_matvecs"]
