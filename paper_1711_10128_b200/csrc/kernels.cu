@@ -1004,7 +1004,8 @@ __global__ void k_gather(const double* x, const int* idx, int64_t n, double* out
 }  // namespace trplk
 
 #include "staged.cuh"     // TMA-staged K1 / K2 (shares the device helpers above)
-#include "stream_tp.cuh"   // thread-per-row K1 / K2 (default)
+#include "stream_tp.cuh"   // thread-per-row K1 / K2
+#include "stream_cp.cuh"   // cp.async-pipelined K1 / K2
 
 namespace trplk {
 
@@ -1019,7 +1020,8 @@ static int kvar() {
     static int v = -1;
     if (v < 0) {
         const char* e = getenv("TRPLK_KVAR");
-        v = (e && !strcmp(e, "tma")) ? 1 : (e && !strcmp(e, "reg")) ? 2 : (e && !strcmp(e, "tp")) ? 0 : 3;
+        v = (e && !strcmp(e, "tma")) ? 1 : (e && !strcmp(e, "reg")) ? 2 : (e && !strcmp(e, "tp")) ? 0
+          : (e && !strcmp(e, "cp")) ? 4 : 3;
     }
     return v;
 }
@@ -1099,10 +1101,11 @@ void launch_sdots(const SdotsArgs& a, int kmax, cudaStream_t s) {
     // inner-step K1 (and the T-column-only launches): TMA-staged basis stream
     const bool k1_shape = a.A.nrows && a.out_mode <= 2 && a.set1 == 1 && (a.set2 == 0 || a.set2 == 2) &&
                           (a.norm1 == 0 || a.norm1 == 1) && a.norm2 == 0 && a.x_dyn == 0 && a.uout == nullptr;
-    if (kmax > 0 && (kvar() == 0 || (kvar() == 3 && !k1_shape)) && a.out_mode != 4 && launch_step1_tp(a, kmax, s))
+    if (kmax > 0 && (kvar() == 0 || (kvar() >= 3 && !k1_shape)) && a.out_mode != 4 && launch_step1_tp(a, kmax, s))
         return;
     if (kmax > 0 && k1_shape) {
         if (kvar() == 3 && launch_step1_rs(a, kmax, s)) return;
+        if (kvar() == 4 && launch_step1_cp(a, kmax, s)) return;
         if (kvar() == 1 && launch_step1_tma(a, kmax, s)) return;
     }
     if (kmax > 0 && a.out_mode != 4) {  // dots: DMMA accumulator kernel
@@ -1143,6 +1146,7 @@ void launch_sdots(const SdotsArgs& a, int kmax, cudaStream_t s) {
 void launch_upd(const UpdArgs& a, int kmax, cudaStream_t s) {
     if (a.mode == 1 && a.dots) {
         if (kvar() == 0 && launch_upd2_tp(a, kmax, s)) return;
+        if (kvar() == 4 && launch_upd2_cp(a, kmax, s)) return;
         if (kvar() == 3 && launch_upd2_rs(a, kmax, s)) return;
         if (kvar() == 1 && launch_upd2_tma(a, kmax, s)) return;
     }
