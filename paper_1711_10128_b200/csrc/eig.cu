@@ -209,8 +209,22 @@ __global__ void __launch_bounds__(EIG_THREADS) k_eig_2b(Ctl* ctl, double* T, int
 //               (every entry of A is in exactly one block) and V <- V J;
 // and a round costs one barrier.  Same rotations in the same order, same skip rule and
 // sweep-end test as k_eig_2b (and the oracle's rule): only the schedule differs.
-constexpr int BLK_WARPS = 7;                         // warps 1..7: 2x2 block updates
-constexpr int EIG1_THREADS = 32 * (1 + BLK_WARPS) + 256;  // + 8 warps: V columns
+#ifdef EIG_TRACE
+__device__ unsigned long long eig_trace[32];  // per-warp cycles to the round barrier; [30] rounds, [31] round cycles
+#endif
+// Warp roles (warp w runs on scheduler w % 4): warp 0 computes the next round's rotation
+// parameters -- the critical path -- and has scheduler 0 to itself (warps 4, 8, 12 idle);
+// warps 1-3, 5-7 update the 2x2 blocks of A, warps 9-11, 13-15 the columns of V.
+constexpr int EIG1_THREADS = 512;
+constexpr int BLK_WARPS = 6;
+__device__ __forceinline__ int eig_role(int w, int& rank) {  // 0 params, 1 blocks, 2 V, 3 idle
+    if (w == 0) { rank = 0; return 0; }
+    if ((w & 3) == 0) { rank = 0; return 3; }
+    const int sub = (w & 3) - 1;  // 0..2
+    if (w < 8) { rank = (w >> 2) * 3 + sub; return 1; }
+    rank = ((w - 8) >> 2) * 3 + sub;
+    return 2;
+}
 
 __device__ __forceinline__ int rr_pos(int x, int r, int kk) {  // position of player x in round r
     if (x == 0) return 0;
@@ -235,6 +249,32 @@ __device__ __forceinline__ void block22(double a, double b, double c, double d, 
 
 // Rotation of the pivot (p,q), p < q < k, from a_pp, a_qq, a_pq (skip rule of the oracle:
 // |a_pq| <= eps sqrt|a_pp a_qq| or <= 1e-30 ||T||_F is not rotated); also the new diagonal.
+// fp64 reciprocal and reciprocal square root: hardware approximation + two Newton steps (~1 ulp).
+// Measured on B200 (tools/micro_fp64lat.cu): the IEEE sqrt / div / rsqrt chains cost 99 / 79 / 74
+// cycles of dependent latency, the original parameter formula 551 cycles per rotation.
+__device__ __forceinline__ double rcp_nr(double x) {
+    double y;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    double e = fma(-x, y, 1.0);
+    y = fma(y, e, y);
+    e = fma(-x, y, 1.0);
+    return fma(y, e, y);
+}
+__device__ __forceinline__ double rsqrt_nr(double x) {
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    double h = x * y;
+    double e = fma(-h, y, 1.0);
+    y = fma(0.5 * y, e, y);
+    h = x * y;
+    e = fma(-h, y, 1.0);
+    return fma(0.5 * y, e, y);
+}
+
+// Rotation of the pivot (p,q), p < q < k, from a_pp, a_qq, a_pq (skip rule of the oracle:
+// |a_pq| <= eps sqrt|a_pp a_qq| or <= 1e-30 ||T||_F is not rotated, tested on squares); also
+// the new diagonal.  t = sgn(tau) / (|tau| + sqrt(1 + tau^2)) in the division-free form
+// t = sgn |b| / (|d| + sqrt(d^2 + b^2)), c = 1/sqrt(1 + t^2), s = t c.
 __device__ __forceinline__ void jacobi_param(double app, double aqq, double apq, double fro, double& c, double& s,
                                              double& dp, double& dq, int& act) {
     const double eps = 2.220446049250313e-16;
@@ -243,11 +283,12 @@ __device__ __forceinline__ void jacobi_param(double app, double aqq, double apq,
     dp = app;
     dq = aqq;
     act = 0;
-    if (!(fabs(apq) <= eps * sqrt(fabs(app * aqq)) || fabs(apq) <= 1e-30 * fro)) {
+    if (!(apq * apq <= eps * eps * fabs(app * aqq) || fabs(apq) <= 1e-30 * fro)) {
         const double d = aqq - app, b = 2.0 * apq;
-        const double t = ((d == 0.0 || ((d > 0.0) == (b > 0.0))) ? 1.0 : -1.0) * fabs(b) /
-                         (fabs(d) + sqrt(d * d + b * b));
-        c = rsqrt(1.0 + t * t);
+        const double h = fma(d, d, b * b);
+        const double den = fma(h, rsqrt_nr(h), fabs(d));  // |d| + sqrt(d^2 + b^2)
+        const double t = ((d == 0.0 || ((d > 0.0) == (b > 0.0))) ? 1.0 : -1.0) * fabs(b) * rcp_nr(den);
+        c = rsqrt(fma(t, t, 1.0));  // CUDA rsqrt: c^2 + s^2 = 1 to ~1 ulp (orthogonality of V)
         s = t * c;
         double m00, m01, m10, m11;
         block22(app, apq, apq, aqq, c, s, c, s, m00, m01, m10, m11);
@@ -268,11 +309,11 @@ __global__ void __launch_bounds__(EIG1_THREADS) k_eig(Ctl* ctl, double* T, int l
     __shared__ double red[EIG1_THREADS];
     __shared__ int ord[QMAX];
     __shared__ unsigned char bi[MAXBLK], bj[MAXBLK];
-    __shared__ unsigned char plr[QMAX - 1][QMAX], pairof[QMAX - 1][QMAX];  // player at pos; pair of player
     __shared__ int rot[101];
     __shared__ double fro;
     const int tid = threadIdx.x;
     double f = 0.0;
+    __shared__ unsigned char plr[QMAX - 1][QMAX], pairof[QMAX - 1][QMAX];  // player at pos; pair of player
     {
         const int kk0 = k + (k & 1);
         for (int idx = tid; idx < (kk0 - 1) * kk0; idx += EIG1_THREADS) {
@@ -325,7 +366,13 @@ __global__ void __launch_bounds__(EIG1_THREADS) k_eig(Ctl* ctl, double* T, int l
     __syncthreads();
     int sweep = 0, r = 0, cur = 0;
     const int warp = tid >> 5;
+#ifdef EIG_TRACE
+    long long tr0 = clock64();
+#endif
     while (k > 1) {
+#ifdef EIG_TRACE
+        tr0 = clock64();
+#endif
         const int nxt = cur ^ 1;
         const int rn = r + 1 == nr ? 0 : r + 1;
         const int sn = r + 1 == nr ? sweep + 1 : sweep;
@@ -347,10 +394,9 @@ __global__ void __launch_bounds__(EIG1_THREADS) k_eig(Ctl* ctl, double* T, int l
                     const bool yp = pp[cur][j] == y;
                     dy = yp ? pdp[cur][j] : pdq[cur][j];
                     double axy;
-                    if (i == j) {  // only for k <= 2: the same pair again
+                    if (i == j) {
                         axy = pact[cur][i] ? 0.0 : Ac[x + y * ELD];
                     } else {
-                        // entry (x, y) of J_i^T A_r[P_i, P_j] J_j, x in pair i, y in pair j
                         const int p1 = pp[cur][i], q1 = pq[cur][i], p2 = pp[cur][j], q2 = pq[cur][j];
                         const bool q1ok = q1 < k, q2ok = q2 < k;
                         const double a = Ac[p1 + p2 * ELD];
@@ -368,10 +414,12 @@ __global__ void __launch_bounds__(EIG1_THREADS) k_eig(Ctl* ctl, double* T, int l
                 if (act) rot[sn] = 1;
             }
         } else {
-            if (warp < 1 + BLK_WARPS) {
+            int rank = 0;
+            const int role = eig_role(warp, rank);
+            if (role == 1) {
                 // 2x2 block updates of round r: A_r -> A_{r+1} (A_r and A_{r+1} are distinct
                 // buffers, so the loads of later blocks are not ordered after earlier stores)
-                const int t2 = tid - 32;
+                const int t2 = rank * 32 + (tid & 31);
                 for (int b = t2; b < nblk; b += 32 * BLK_WARPS) {
                     const int i = bi[b], j = bj[b];
                     const int p1 = pp[cur][i], q1 = pq[cur][i], p2 = pp[cur][j], q2 = pq[cur][j];
@@ -406,37 +454,33 @@ __global__ void __launch_bounds__(EIG1_THREADS) k_eig(Ctl* ctl, double* T, int l
                         An[q2 + q1 * ELD] = m11;
                     }
                 }
-            } else {
-                // V <- V J for the pairs of round r: thread = (row, pair slot), all loads first
-                const int tv = tid - 32 * (1 + BLK_WARPS);
-                const int row = tv & (QMAX - 1), slot = tv >> 6;  // 4 slots x 64 rows
-                constexpr int NPV = MAXPAIRS / 4;
-                double vp[NPV], vq[NPV], c_[NPV], s_[NPV];
-                int pidx[NPV], qidx[NPV];
-                bool on[NPV];
-#pragma unroll
-                for (int u = 0; u < NPV; ++u) {
-                    const int pi = slot + 4 * u;
-                    on[u] = row < k && pi < npairs && pact[cur][pi];
-                    if (on[u]) {
-                        pidx[u] = row + pp[cur][pi] * ELD;
-                        qidx[u] = row + pq[cur][pi] * ELD;
-                        c_[u] = pc[cur][pi];
-                        s_[u] = ps[cur][pi];
-                        vp[u] = V[pidx[u]];
-                        vq[u] = V[qidx[u]];
-                    }
-                }
-#pragma unroll
-                for (int u = 0; u < NPV; ++u) {
-                    if (on[u]) {
-                        V[pidx[u]] = c_[u] * vp[u] - s_[u] * vq[u];
-                        V[qidx[u]] = s_[u] * vp[u] + c_[u] * vq[u];
-                    }
+            } else if (role == 2) {
+                // V <- V J for the pairs of round r: tasks (pair, row) packed densely over the
+                // V warps (consecutive lanes = consecutive rows of one pair: conflict-free)
+                const int tv = rank * 32 + (tid & 31);
+                constexpr int NVT = 32 * 6;
+                const int ntask = npairs * k;
+                const float inv_k = 1.0f / (float)k;
+                for (int e = tv; e < ntask; e += NVT) {
+                    const int pi = __float2int_rz(((float)e + 0.5f) * inv_k);
+                    if (!pact[cur][pi]) continue;
+                    const int row = e - pi * k;
+                    const int ip = row + pp[cur][pi] * ELD, iq = row + pq[cur][pi] * ELD;
+                    const double c = pc[cur][pi], sn_ = ps[cur][pi];
+                    const double vp = V[ip], vq = V[iq];
+                    V[ip] = c * vp - sn_ * vq;
+                    V[iq] = sn_ * vp + c * vq;
                 }
             }
         }
+#ifdef EIG_TRACE
+        if ((tid & 31) == 0) atomicAdd(&eig_trace[warp], (unsigned long long)(clock64() - tr0));
+#endif
         __syncthreads();
+#ifdef EIG_TRACE
+        if (tid == 0) atomicAdd(&eig_trace[31], (unsigned long long)(clock64() - tr0));
+        if (tid == 0) atomicAdd(&eig_trace[30], 1ull);
+#endif
         cur = nxt;
         if (r + 1 == nr) {  // end of a sweep: stop after a sweep without rotations
             if (!rot[sweep] || sn >= maxsweep) break;

@@ -87,8 +87,9 @@ def test_C3_closed_form_clusters(gen):
     c = 2 - 2 * np.cos(np.arange(1, 129) * np.pi / 129)
     ref = np.sort(np.add.outer(np.add.outer(c[:8], c[:8]), c[:8]).ravel())[:20]
     assert st["status"] == "OK"
-    # a-posteriori: |theta - lambda| <= ||r||^2 / gap with inter-cluster gap >= 5.8e-4
-    assert np.all(np.abs(ev - ref) <= rs ** 2 / 5.8e-4 + 1e-14)
+    # a-posteriori: |theta - lambda| <= ||r||^2 / gap with inter-cluster gap >= 5.8e-4, plus the
+    # rounding floor of a backward-stable Rayleigh-Ritz, O(eps ||A||): 1e-14 ||A||_2 (||A||_2 < 12)
+    assert np.all(np.abs(ev - ref) <= rs ** 2 / 5.8e-4 + 1e-14 * 12.0)
     ctx.close()
 
 
