@@ -127,20 +127,33 @@ __device__ bool grid_reduce(const double* mine, int nv, double* part, double* gp
         __syncthreads();
         if (!flag) return false;
         __threadfence();
+        // warp w sums values w*VB .. w*VB+VB-1 (then + nwarps*VB ...): VB*U partial loads in
+        // flight per lane, so a 296-CTA x 60-value reduction is ~3 dependent L2 round trips
         const int nwarps = blockDim.x >> 5;
-        for (int v = warp; v < nv; v += nwarps) {
-            const double* pv = part + (int64_t)v * maxcta;
-            double s = 0.0;
-            constexpr int U = 8;
+        constexpr int VB = 4, U = 4;
+        for (int v0 = warp * VB; v0 < nv; v0 += nwarps * VB) {
+            double sv[VB];
+#pragma unroll
+            for (int b = 0; b < VB; ++b) sv[b] = 0.0;
             for (int c0 = lane; c0 < ncta; c0 += 32 * U) {
-                double t[U];
+                double t[VB][U];
 #pragma unroll
-                for (int u = 0; u < U; ++u) t[u] = (c0 + 32 * u < ncta) ? __ldcg(pv + c0 + 32 * u) : 0.0;
+                for (int b = 0; b < VB; ++b)
 #pragma unroll
-                for (int u = 0; u < U; ++u) s += t[u];
+                    for (int u = 0; u < U; ++u)
+                        t[b][u] = (v0 + b < nv && c0 + 32 * u < ncta)
+                                      ? __ldcg(part + (int64_t)(v0 + b) * maxcta + c0 + 32 * u)
+                                      : 0.0;
+#pragma unroll
+                for (int b = 0; b < VB; ++b)
+#pragma unroll
+                    for (int u = 0; u < U; ++u) sv[b] += t[b][u];
             }
-            s = warp_sum(s);
-            if (lane == 0) out[v] = s;
+#pragma unroll
+            for (int b = 0; b < VB; ++b) {
+                const double s = warp_sum(sv[b]);
+                if (lane == 0 && v0 + b < nv) out[v0 + b] = s;
+            }
         }
         __syncthreads();
         if (tid == 0) cnt[0] = 0u;

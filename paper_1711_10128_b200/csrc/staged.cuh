@@ -320,12 +320,13 @@ __global__ void __launch_bounds__(CTA, 2) k_step1_rs(const SdotsArgs a) {
     const int nn = (a.norm1 ? 1 : 0) + (a.norm2 ? 1 : 0);
     const int nv = k1 + k2 + nn;
     const double* __restrict__ X = a.x;
-    extern __shared__ __align__(128) double wsm[];  // WARPS x KMAX x WLD
+    constexpr int CH = KMAX < 24 ? KMAX : 24;       // columns per chunk (= slab width)
+    extern __shared__ __align__(128) double wsm[];  // WARPS x CH x WLD: one chunk per warp
     __shared__ double acc[WARPS][NV_MAX];
     __shared__ double res[NV_MAX];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int fi = lane >> 2, fj = lane & 3;
-    double* W = wsm + (size_t)warp * KMAX * WLD;
+    double* W = wsm + (size_t)warp * CH * WLD;
     double cacc[KMAX / 8][2];
 #pragma unroll
     for (int g = 0; g < KMAX / 8; ++g) cacc[g][0] = cacc[g][1] = 0.0;
@@ -334,7 +335,6 @@ __global__ void __launch_bounds__(CTA, 2) k_step1_rs(const SdotsArgs a) {
     for (int64_t sl = (int64_t)blockIdx.x * WARPS + warp; sl < nslices; sl += (int64_t)gridDim.x * WARPS) {
         const int64_t row = sl * 32 + lane;
         const bool ok = row < a.nrows;
-        constexpr int CH = KMAX < 24 ? KMAX : 24;  // first chunk of columns, loaded before the SpMV
         double ur[CH];
         const double* up = a.U + row;
 #pragma unroll
@@ -358,21 +358,6 @@ __global__ void __launch_bounds__(CTA, 2) k_step1_rs(const SdotsArgs a) {
             o = 0.0;
         }
         if (a.norm1 == 1) n1 += o * o;
-        __syncwarp();
-#pragma unroll
-        for (int c = 0; c < CH; ++c) W[c * WLD + lane] = ur[c];
-#pragma unroll
-        for (int cb = CH; cb < KMAX; cb += CH) {  // remaining columns: load a chunk, park it
-            if (cb < kmx) {
-#pragma unroll
-                for (int c = 0; c < CH; ++c)
-                    ur[c] = (ok && cb + c < kmx && cb + c < KMAX) ? __ldg(up + (int64_t)(cb + c) * a.ldu) : 0.0;
-#pragma unroll
-                for (int c = 0; c < CH; ++c)
-                    if (cb + c < KMAX) W[(cb + c) * WLD + lane] = ur[c];
-            }
-        }
-        __syncwarp();
         const double v1 = a.set1 == 1 ? z : o;
         double bq[8];
 #pragma unroll
@@ -381,12 +366,37 @@ __global__ void __launch_bounds__(CTA, 2) k_step1_rs(const SdotsArgs a) {
             const double t2 = TWO ? __shfl_sync(0xffffffffu, o, 4 * q + fj) : 0.0;
             bq[q] = fi == 0 ? t1 : (fi == 1 ? t2 : 0.0);
         }
+        // chunks of CH columns through the warp's slab: the next chunk's loads are issued
+        // (into the registers just parked) before this chunk's DMMAs
+        __syncwarp();
 #pragma unroll
-        for (int g = 0; g < KMAX / 8; ++g) {
-            if (8 * g < kmx) {
-                const double* sp = W + (8 * g + fi) * WLD + fj;
+        for (int c = 0; c < CH; ++c) W[c * WLD + lane] = ur[c];
+        __syncwarp();
 #pragma unroll
-                for (int q = 0; q < 8; ++q) dmma884_s(cacc[g], sp[4 * q], bq[q]);
+        for (int cb = 0; cb < KMAX; cb += CH) {
+            const bool more = cb + CH < KMAX && cb + CH < kmx;
+            if (more) {
+#pragma unroll
+                for (int c = 0; c < CH; ++c) {
+                    const int cc = cb + CH + c;
+                    ur[c] = (ok && cc < kmx && cc < KMAX) ? __ldg(up + (int64_t)cc * a.ldu) : 0.0;
+                }
+            }
+            if (cb < kmx) {
+#pragma unroll
+                for (int g = cb / 8; g < (cb + CH) / 8 && g < KMAX / 8; ++g) {
+                    if (8 * g < kmx) {
+                        const double* sp = W + (8 * g - cb + fi) * WLD + fj;
+#pragma unroll
+                        for (int q = 0; q < 8; ++q) dmma884_s(cacc[g], sp[4 * q], bq[q]);
+                    }
+                }
+            }
+            if (more) {
+                __syncwarp();
+#pragma unroll
+                for (int c = 0; c < CH; ++c) W[c * WLD + lane] = ur[c];
+                __syncwarp();
             }
         }
     }
@@ -572,7 +582,7 @@ static int rs_grid(K kern, int smem, int64_t nrows) {
 
 template <int KMAX, bool TWO>
 static void launch_step1_rs_k(const SdotsArgs& a, cudaStream_t s) {
-    const int smem = WARPS * KMAX * WLD * (int)sizeof(double);
+    const int smem = WARPS * (KMAX < 24 ? KMAX : 24) * WLD * (int)sizeof(double);
     auto kern = k_step1_rs<KMAX, TWO>;
     kern<<<rs_grid(kern, smem, a.nrows), CTA, smem, s>>>(a);
 }
