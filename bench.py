@@ -224,7 +224,8 @@ def main():
     value = mv / (ms_per_step / 1e3)
 
     # roofline: inner-step kernel group with the largest share (live CUDA events, per launch)
-    names = ["K1 k_sdots (SpMV+Jacobi+T-col/h1 dots)", "K2 k_upd DOTS (CGS pass 2)", "K3 k_upd FINAL (+fix)"]
+    names = ["K1 k_step1_rs (SpMV+Jacobi+T-col/h1 dots)", "K2 k_upd2_rs (CGS pass 2 update+dots)",
+             "K3 k_upd FINAL (+gated pass 3)"]
     peak, peak_src = peaks()
     cnt = max(prof["count"], 1)
     per_ms = prof["ms"] / cnt
@@ -232,12 +233,20 @@ def main():
     kd = int(np.argmax(per_ms))
     achieved = per_b[kd] / (per_ms[kd] * 1e-3) / 1e9
     step_gbs = per_b.sum() / (per_ms.sum() * 1e-3) / 1e9
-    traffic = None
+    # ncu DRAM bytes per launch of the same kernel instantiation (profiles/traffic_<cfg>.json,
+    # tools/make_traffic.py): the inner step profiled is j = jmid, k = p^ + jmid
+    traffic, traffic_kernel = None, None
     tfile = os.path.join(PROFILES, f"traffic_{args.config}.json")
     if os.path.exists(tfile):
-        traffic = json.load(open(tfile)).get(str(kd))
+        m = P.q - P.p - P.l
+        jmid = max(1, min(m - 1, m // 2))
+        kk = P.p + jmid
+        bucket = next(b for b in (8, 16, 24, 32, 40, 48, 64) if kk <= b)
+        traffic_kernel = [f"k_step1_rs<{bucket}, 1>", f"k_upd2_rs<{bucket}>", f"k_upd<{bucket}, 0>"][kd]
+        traffic = json.load(open(tfile)).get(traffic_kernel)
     roof = {"bound": "hbm", "kernel": names[kd], "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-            "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_src,
+            "frac": round(achieved / peak, 4), "traffic": traffic, "traffic_kernel": traffic_kernel,
+            "peak_source": peak_src,
             "bytes_per_launch": per_b[kd], "ms_per_launch": per_ms[kd],
             "inner_step": {"achieved": round(step_gbs, 1), "frac": round(step_gbs / peak, 4),
                            "bytes": per_b.sum(), "ms": per_ms.sum(),
