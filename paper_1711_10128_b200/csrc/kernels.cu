@@ -1034,7 +1034,27 @@ static int kvar() {
     if (v < 0) {
         const char* e = getenv("TRPLK_KVAR");
         v = (e && !strcmp(e, "tma")) ? 1 : (e && !strcmp(e, "reg")) ? 2 : (e && !strcmp(e, "tp")) ? 0
-          : (e && !strcmp(e, "cp")) ? 4 : 3;
+          : (e && !strcmp(e, "cp")) ? 4 : (e && !strcmp(e, "wp")) ? 5 : 3;
+    }
+    return v;
+}
+
+// K2 (CGS pass 2 with dots) variant: warp-pair `wp` (default) or TRPLK_K2=rs for the K1-family one
+static int k2var() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("TRPLK_K2");
+        v = (e && !strcmp(e, "rs")) ? 0 : 1;  // default: warp-pair K2 (measured: profiles/r01_variants.md)
+    }
+    return v;
+}
+
+// TRPLK_K1=wp: the warp-group K1 (inner-step shape)
+static int k1var() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("TRPLK_K1");
+        v = (e && !strcmp(e, "wp")) ? 1 : 0;
     }
     return v;
 }
@@ -1117,6 +1137,7 @@ void launch_sdots(const SdotsArgs& a, int kmax, cudaStream_t s) {
     if (kmax > 0 && (kvar() == 0 || (kvar() >= 3 && !k1_shape)) && a.out_mode != 4 && launch_step1_tp(a, kmax, s))
         return;
     if (kmax > 0 && k1_shape) {
+        if (k1var() == 1 && launch_step1_wp(a, kmax, s)) return;
         if (kvar() == 3 && launch_step1_rs(a, kmax, s)) return;
         if (kvar() == 4 && launch_step1_cp(a, kmax, s)) return;
         if (kvar() == 1 && launch_step1_tma(a, kmax, s)) return;
@@ -1160,6 +1181,7 @@ void launch_upd(const UpdArgs& a, int kmax, cudaStream_t s) {
     if (a.mode == 1 && a.dots) {
         if (kvar() == 0 && launch_upd2_tp(a, kmax, s)) return;
         if (kvar() == 4 && launch_upd2_cp(a, kmax, s)) return;
+        if ((kvar() == 5 || k2var() == 1) && launch_upd2_wp(a, kmax, s)) return;
         if (kvar() == 3 && launch_upd2_rs(a, kmax, s)) return;
         if (kvar() == 1 && launch_upd2_tma(a, kmax, s)) return;
     }

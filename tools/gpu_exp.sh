@@ -1,7 +1,8 @@
 mkdir -p gpurun_out/exp
 O=gpurun_out/exp
-timeout 1500 python -m pytest tests -m gpu -q -x -rf --timeout 900 > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+TRPLK_K1=wp timeout 1500 python -m pytest tests/test_gpu_kernels.py tests/test_gpu_solve.py -m gpu -q -x -rf --timeout 900 > $O/pytest_wp.log 2>&1; echo "pytest rc=$?" >> $O/pytest_wp.log
 Q="--steps 3 --warmup 1 --no-e2e --no-cpu-baseline"
-for c in C2 C3 C4; do timeout 600 python bench.py --config $c $Q > $O/b_${c}_def.json 2>&1; done
-TRPLK_NO_CDIA=1 timeout 600 python bench.py --config C2 $Q > $O/b_C2_nocdia.json 2>&1
-timeout 900 python bench.py --config C5 --steps 2 --warmup 1 --no-e2e --no-cpu-baseline > $O/b_C5_def.json 2>&1
+for c in C2 C3; do
+  TRPLK_K1=wp timeout 600 python bench.py --config $c $Q > $O/b_${c}_wp.json 2>&1
+  timeout 600 python bench.py --config $c $Q > $O/b_${c}_def.json 2>&1
+done
