@@ -1,8 +1,8 @@
 mkdir -p gpurun_out/exp
 O=gpurun_out/exp
-TRPLK_K1=wp timeout 1500 python -m pytest tests/test_gpu_kernels.py tests/test_gpu_solve.py -m gpu -q -x -rf --timeout 900 > $O/pytest_wp.log 2>&1; echo "pytest rc=$?" >> $O/pytest_wp.log
+timeout 1500 python -m pytest tests -m gpu -q -x -rf --timeout 900 > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
 Q="--steps 3 --warmup 1 --no-e2e --no-cpu-baseline"
 for c in C2 C3; do
-  TRPLK_K1=wp timeout 600 python bench.py --config $c $Q > $O/b_${c}_wp.json 2>&1
   timeout 600 python bench.py --config $c $Q > $O/b_${c}_def.json 2>&1
+  TRPLK_NO_PDL=1 timeout 600 python bench.py --config $c $Q > $O/b_${c}_nopdl.json 2>&1
 done
