@@ -119,8 +119,12 @@ __device__ bool grid_reduce(const double* mine, int nv, double* part, double* gp
     __shared__ bool flag;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int bid = blockIdx.x, ncta = gridDim.x;
-    for (int v = tid; v < nv; v += blockDim.x) part[(int64_t)v * maxcta + bid] = mine[v];
-    __threadfence();
+    // only the threads that wrote partials fence (a fence waits for ALL of the thread's
+    // outstanding stores, e.g. its rows of the output vector, which need no ordering here)
+    if (tid < nv) {
+        for (int v = tid; v < nv; v += blockDim.x) part[(int64_t)v * maxcta + bid] = mine[v];
+        __threadfence();
+    }
     __syncthreads();
     if (ncta <= ONE_LEVEL_MAX) {
         if (tid == 0) flag = atomicAdd(&cnt[0], 1u) == (unsigned)(ncta - 1);
@@ -657,8 +661,9 @@ __global__ void __launch_bounds__(CTA, DOTS ? 2 : (KMAX <= 16 ? 3 : (KMAX <= 32 
             upd_finalize(a, res, kv);
         }
     } else {
-        // no dots: one ticket so exactly one CTA applies the control-block side effects
-        __threadfence();
+        // no dots: one ticket so exactly one CTA -- the last to finish, after every CTA has
+        // read the control block -- applies the control-block side effects (no data is handed
+        // between CTAs, so no fence)
         __syncthreads();
         if (threadIdx.x == 0) is_last = atomicAdd(a.counter, 1u) == gridDim.x - 1;
         __syncthreads();

@@ -4,5 +4,4 @@ timeout 1500 python -m pytest tests -m gpu -q -x -rf --timeout 900 > gpurun_out/
 Q="--steps 3 --warmup 1 --no-e2e --no-cpu-baseline"
 for c in C2 C3; do
   timeout 600 python bench.py --config $c $Q > $O/b_${c}_def.json 2>&1
-  TRPLK_NO_PDL=1 timeout 600 python bench.py --config $c $Q > $O/b_${c}_nopdl.json 2>&1
 done
