@@ -1024,6 +1024,7 @@ __global__ void k_gather(const double* x, const int* idx, int64_t n, double* out
 #include "staged.cuh"     // TMA-staged K1 / K2 (shares the device helpers above)
 #include "stream_tp.cuh"   // thread-per-row K1 / K2
 #include "stream_cp.cuh"   // cp.async-pipelined K1 / K2
+#include "rotate.cuh"      // shared-memory-staged DMMA rotation (default)
 
 namespace trplk {
 
@@ -1233,16 +1234,23 @@ static void rot_t_k(int kmax, const double* U, int64_t ldu, int64_t nrows, const
 }
 
 // kmax: upper bound of the device-side width (k_fixed, or the solve's max basis q).
-// TRPLK_ROT=mma8 selects the row-operand variant k_rotate (8-row tiles, Y in shared memory).
+// Default: k_rotate_s (rotate.cuh); TRPLK_ROT=t the register-fragment k_rotate_t, TRPLK_ROT=mma8
+// the row-operand k_rotate (8-row tiles, Y in shared memory).
 void launch_rotate(const double* U, int64_t ldu, int64_t nrows, const Ctl* ctl, int k_fixed, const double* Y,
                    int ldY, int ncol, double* X, int64_t ldx, unsigned gate, cudaStream_t s, int kmax) {
     static int var = -1;
     if (var < 0) {
         const char* e = getenv("TRPLK_ROT");
-        var = (e && !strcmp(e, "mma8")) ? 1 : 0;
+        var = (e && !strcmp(e, "mma8")) ? 1 : (e && !strcmp(e, "t")) ? 2 : 0;
     }
     if (k_fixed > 0) kmax = k_fixed;
-    if (var == 0 && kmax <= 64 && ncol <= 24) {
+    if (var == 0 && ncol <= 24) {
+        const bool done = ncol <= 8    ? rot_s_k<1>(kmax, U, ldu, nrows, ctl, k_fixed, Y, ldY, ncol, X, ldx, gate, s)
+                          : ncol <= 16 ? rot_s_k<2>(kmax, U, ldu, nrows, ctl, k_fixed, Y, ldY, ncol, X, ldx, gate, s)
+                                       : rot_s_k<3>(kmax, U, ldu, nrows, ctl, k_fixed, Y, ldY, ncol, X, ldx, gate, s);
+        if (done) return;
+    }
+    if (var == 2 && kmax <= 64 && ncol <= 24) {
         if (ncol <= 8) rot_t_k<1>(kmax, U, ldu, nrows, ctl, k_fixed, Y, ldY, ncol, X, ldx, gate, s);
         else if (ncol <= 16) rot_t_k<2>(kmax, U, ldu, nrows, ctl, k_fixed, Y, ldY, ncol, X, ldx, gate, s);
         else rot_t_k<3>(kmax, U, ldu, nrows, ctl, k_fixed, Y, ldY, ncol, X, ldx, gate, s);
