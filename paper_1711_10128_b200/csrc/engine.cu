@@ -53,8 +53,6 @@ struct trplk_ctx {
     int rank = 0, nranks = 1;
     cudaStream_t stream = nullptr;       // internal non-blocking work stream (capturable)
     cudaStream_t user_stream = nullptr;  // the caller's stream; ordered with `stream` by events
-    cudaStream_t side = nullptr;         // captures the bodies of conditional graph nodes
-    bool use_cond = false;               // pass-3 kernels in conditional nodes when capturing (1 rank)
     cudaEvent_t ev_in = nullptr, ev_out = nullptr;
     trplk_allocator alloc{};
     bool has_alloc = false;
@@ -580,23 +578,7 @@ trplk_status cgs2(trplk_ctx* ctx, const CgsSpec& c) {
         a.gate = c.gate;
         ST(run_sdots(ctx, a, kn));
     }
-    // final: y = w1 - V h1, beta from Pythagoras; pass 3 into w2 if the norm dropped > 1/sqrt2.
-    // Under graph capture (one rank) the pass-3 kernels go into a conditional node that the
-    // FINAL kernel switches on only when the third pass is needed (normally never), so the
-    // common path launches no gated no-op kernels.
-    cudaGraphConditionalHandle cond = 0;
-    cudaGraph_t capg = nullptr;
-    bool in_cond = false;
-    if (ctx->use_cond && ctx->nranks == 1) {
-        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-        const cudaGraphNode_t* deps = nullptr;
-        size_t ndeps = 0;
-        CK(cudaStreamGetCaptureInfo(ctx->stream, &cs, nullptr, &capg, &deps, &ndeps));
-        if (cs == cudaStreamCaptureStatusActive) {
-            CK(cudaGraphConditionalHandleCreate(&cond, capg, 0, cudaGraphCondAssignDefault));
-            in_cond = true;
-        }
-    }
+    // final: y = w1 - V h1, beta from Pythagoras; pass 3 into w2 if the norm dropped > 1/sqrt2
     if (c.mark_final) CK(cudaEventRecordWithFlags(c.mark_final, ctx->stream, cudaEventRecordExternal));
     {
         UpdArgs u = up_base(ctx);
@@ -615,27 +597,7 @@ trplk_status cgs2(trplk_ctx* ctx, const CgsSpec& c) {
         u.inc_k = c.inc_k;
         u.gate = c.gate;
         u.clear_on_brk = c.clear;
-        u.pass3_cond = in_cond ? (unsigned long long)cond : 0ull;
         ST(run_upd(ctx, u, kn));
-    }
-    cudaStream_t main_stream = ctx->stream;
-    const int64_t launches0 = ctx->launches;
-    if (in_cond) {
-        const cudaGraphNode_t* deps = nullptr;
-        size_t ndeps = 0;
-        cudaStreamCaptureStatus cs;
-        CK(cudaStreamGetCaptureInfo(ctx->stream, &cs, nullptr, &capg, &deps, &ndeps));
-        cudaGraphNodeParams np{};
-        np.type = cudaGraphNodeTypeConditional;
-        np.conditional.handle = cond;
-        np.conditional.type = cudaGraphCondTypeIf;
-        np.conditional.size = 1;
-        cudaGraphNode_t node;
-        CK(cudaGraphAddNode(&node, capg, deps, ndeps, &np));
-        CK(cudaStreamUpdateCaptureDependencies(ctx->stream, &node, 1, cudaStreamSetCaptureDependencies));
-        CK(cudaStreamBeginCaptureToGraph(ctx->side, np.conditional.phGraph_out[0], nullptr, nullptr, 0,
-                                         cudaStreamCaptureModeThreadLocal));
-        ctx->stream = ctx->side;  // the two pass-3 launches below are captured into the body
     }
     {  // third-pass dots h3 = V^T B w2, N_2SQ_EXP = w2^T B w2 (gated on ctl->pass3, normally a no-op)
         SdotsArgs a = sd_base(ctx);
@@ -674,12 +636,6 @@ trplk_status cgs2(trplk_ctx* ctx, const CgsSpec& c) {
         u.gate = c.gate;
         u.clear_on_brk = c.clear;
         ST(run_upd(ctx, u, kn));
-    }
-    if (in_cond) {
-        ctx->stream = main_stream;
-        cudaGraph_t body = nullptr;
-        CK(cudaStreamEndCapture(ctx->side, &body));
-        ctx->launches = launches0;  // the body normally does not run
     }
     return TRPLK_OK;
 }
@@ -1130,13 +1086,7 @@ trplk_status trplk_create(trplk_ctx** out, int64_t n_global, const int64_t* a_ro
     trplk_ctx* ctx = new trplk_ctx();
     *out = ctx;
     ctx->user_stream = (cudaStream_t)stream;
-    {  // measured on B200 (C2): the conditional node costs more than the two no-op launches it
-       // replaces (94.4 vs 81.9 ms per solve), so it is opt-in (TRPLK_COND=1)
-        const char* e = getenv("TRPLK_COND");
-        ctx->use_cond = e && e[0] == '1';
-    }
     if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess ||
-        cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreateWithFlags(&ctx->ev_in, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&ctx->ev_out, cudaEventDisableTiming) != cudaSuccess) {
         ctx->err = "cannot create the work stream";
@@ -1165,7 +1115,6 @@ void trplk_destroy(trplk_ctx* ctx) {
         if (e) cudaEventDestroy(e);
     if (ctx->ev_out) cudaEventDestroy(ctx->ev_out);
     if (ctx->stream) cudaStreamDestroy(ctx->stream);
-    if (ctx->side) cudaStreamDestroy(ctx->side);
     if (ctx->comm) ncclCommDestroy(ctx->comm);
     delete ctx;
 }

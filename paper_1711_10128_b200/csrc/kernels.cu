@@ -106,6 +106,12 @@ __device__ __forceinline__ double mat_row(const Sell& M, int64_t s, int lane, co
     return acc;
 }
 
+// Diagonal entry of row 32 s + lane (DIA: the offset-0 array; SELL: slot 0).
+__device__ __forceinline__ double mat_diag(const Sell& M, int64_t s, int lane) {
+    if (M.fmt == 1) return __ldg(M.dval + (int64_t)M.diag_slot * M.ldv + s * 32 + lane);
+    return __ldg(M.val + __ldg(M.sptr + s) + lane);
+}
+
 // Deterministic grid reduction of the CTA's nv values `mine` (smem).  Returns true in exactly
 // one CTA, whose smem `out` then holds the grid sums.  The summation order is fixed.
 // Grids of <= 1024 CTAs: one level -- the last CTA to arrive sums, per value, CTA partials
@@ -381,6 +387,89 @@ __global__ void __launch_bounds__(CTA, 2) k_sdots(const SdotsArgs a) {
         for (int v = threadIdx.x; v < nv; v += CTA) a.red_local[v] = res[v];
     } else {
         sdots_finalize(a, res, k1, k2);
+    }
+}
+
+// -------------------------------------- SpMV-only launches (no basis dots): residual K7 etc.
+// r = A x - theta B x (u = M r), z = A x, w = M (z - rho B x) with up to two norms; R row tiles
+// per warp iteration so R tiles' value loads and gathers are in flight together, norms in
+// per-lane registers (one warp reduction at the end), <= 80 registers for 3 CTAs per SM.
+template <int R>
+__global__ void __launch_bounds__(CTA, 3) k_spmv_nd(const SdotsArgs a) {
+    Ctl* ctl = a.ctl;
+    if ((ctl->flags & a.gate) != a.gate) return;
+    if (a.gate_pass3 && ctl->pass3 == 0) return;
+    double theta = 0.0;
+    if (a.out_mode >= 3)
+        theta = a.theta_idx >= 0 ? ctl->theta[a.theta_idx]
+                                 : (a.theta_idx == -1 ? ctl->theta[ctl->t - 1] : a.theta_val);
+    const double rho = ctl->rho;
+    const int nn = (a.norm1 ? 1 : 0) + (a.norm2 ? 1 : 0);
+    const double* __restrict__ X = resolve_x(a.x, a.x_dyn, a.x_ld, a.x_off, ctl);
+    __shared__ double acc[WARPS][2];
+    __shared__ double res[2];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t nslices = (a.nrows + 31) >> 5;
+    const int64_t stride = (int64_t)gridDim.x * WARPS;
+    double n1 = 0.0, n2 = 0.0;
+    for (int64_t s0 = (int64_t)blockIdx.x * WARPS + warp; s0 < nslices; s0 += stride * R) {
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const int64_t s = s0 + r * stride;
+            if (s >= nslices) break;
+            const int64_t row = s * 32 + lane;
+            const bool ok = row < a.nrows;
+            double ad = 1.0, bd = 1.0, z = 0.0, sv = 0.0, xr = 0.0;
+            if (ok) {
+                xr = X[row];
+                if (a.out_mode == 4) ad = mat_diag(a.A, s, lane);
+                else if (a.A.nrows) z = mat_row(a.A, s, lane, X, ad);
+                else z = xr;
+                if (a.out_mode >= 2) sv = a.B.nrows ? mat_row(a.B, s, lane, X, bd) : xr;
+            }
+            double o = 0.0, minv = 1.0;
+            if (a.out_mode >= 2) {
+                double d = fabs(ad - a.sigma * bd);
+                d = d > a.mfloor ? d : a.mfloor;
+                minv = 1.0 / d;  // M_ii
+            }
+            switch (a.out_mode) {
+                case 1: o = z; break;
+                case 2: o = minv * (z - rho * sv); break;  // w = M (z - rho B g), R1
+                case 3: o = z - theta * sv; break;         // r = A x - theta B x
+                case 4: o = (ok ? a.wext[row] : 0.0) - theta * sv; break;
+                default: break;
+            }
+            if (ok) {
+                if (a.out) a.out[row] = o;
+                if (a.uout) a.uout[row] = minv * o;
+                if (nn) {
+                    n1 += a.norm1 == 1 ? o * o : a.norm1 == 2 ? xr * z : a.norm1 == 3 ? xr * xr : z * z;
+                    if (a.norm2) n2 += a.norm2 == 1 ? o * o : a.norm2 == 2 ? xr * z : a.norm2 == 3 ? xr * xr : z * z;
+                }
+            }
+        }
+    }
+    if (nn == 0) return;
+    n1 = warp_sum(n1);
+    n2 = warp_sum(n2);
+    if (lane == 0) {
+        acc[warp][0] = n1;
+        acc[warp][1] = n2;
+    }
+    __syncthreads();
+    if (threadIdx.x < nn) {
+        double t = 0.0;
+#pragma unroll
+        for (int w = 0; w < WARPS; ++w) t += acc[w][threadIdx.x];
+        res[threadIdx.x] = t;
+    }
+    __syncthreads();
+    if (!grid_reduce(res, nn, a.part, a.gpart, a.counter, a.maxcta, res)) return;
+    if (a.red_local) {
+        for (int v = threadIdx.x; v < nn; v += CTA) a.red_local[v] = res[v];
+    } else {
+        sdots_finalize(a, res, 0, 0);
     }
 }
 
@@ -675,7 +764,6 @@ __global__ void __launch_bounds__(CTA, DOTS ? 2 : (KMAX <= 16 ? 3 : (KMAX <= 32 
             if (pass3) {
                 ctl->pass3 = 1;
                 ctl->pass3_count += 1;
-                if (a.pass3_cond) cudaGraphSetConditional((cudaGraphConditionalHandle)a.pass3_cond, 1u);
             } else if (brk) {
                 ctl->flags &= ~a.clear_on_brk;
                 ctl->brk += 1;
@@ -1160,6 +1248,11 @@ void launch_sdots(const SdotsArgs& a, int kmax, cudaStream_t s) {
             default:
             SDM_CASE(8)
         }
+        return;
+    }
+    if (kmax == 0 && getenv("TRPLK_OLD_ND") == nullptr) {  // SpMV-only launch (residual, plain SpMV)
+        auto kern = k_spmv_nd<2>;
+        kern<<<stream_grid(kern, (a.nrows + 1) / 2), CTA, 0, s>>>(a);
         return;
     }
     switch (kmax > 32 ? 32 : kmax) {  // columns beyond 32 are processed in further chunks

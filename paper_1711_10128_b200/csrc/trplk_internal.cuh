@@ -135,9 +135,6 @@ struct UpdArgs {
     unsigned* counter;
     int maxcta;
     double* red_local;
-    // FINAL (mode 2) inside a captured graph: set to 1 when a third CGS pass is needed, so the
-    // conditional node holding the pass-3 kernels runs only then (0 = no conditional node)
-    unsigned long long pass3_cond;
 };
 
 // Kernel launchers (kernels.cu)
