@@ -68,6 +68,8 @@ typedef struct {
     int rank, nranks;
     int64_t row_begin, row_end;
     const void* nccl_unique_id;
+    void* loopback; /* test infrastructure: an in-process hub (trplk_loopback_create) instead of NCCL,
+                       all ranks of the solve as host threads of one process on one GPU; NULL = NCCL */
 } trplk_dist;
 
 typedef struct {

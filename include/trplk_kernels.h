@@ -67,6 +67,15 @@ trplk_status trplk_plan_ghosts(int64_t row_begin, int64_t row_end, const int64_t
                                const int64_t* b_rowptr, const int64_t* b_col, const int64_t* ranges, int nranks,
                                int64_t* ghosts_out, int* owners_out, int64_t cap, int64_t* n_ghost);
 
+/* In-process loopback hub for nranks ranks (test infrastructure): pass it as
+ * trplk_dist.loopback to every rank's trplk_create, one host thread per rank, all on the same
+ * GPU.  Every exchange (halo planes, reduction partials, create-time plans) becomes a rendezvous
+ * of the rank threads with device-to-device copies on the receiving rank's stream ordered by
+ * CUDA events -- no kernel waits on another rank.  Solves on loopback ranks run eagerly (no
+ * CUDA graphs).  Destroy the hub after every rank's context.  Errors: EINVAL (nranks < 1). */
+trplk_status trplk_loopback_create(int nranks, void** hub);
+void trplk_loopback_destroy(void* hub);
+
 /* Live profile of the inner step (measurement): while enabled, every
  * outer cycle records CUDA events around the three kernel groups of its middle inner step
  *   [0] K1  fused SpMV + preconditioner + T-column/h1 dots

@@ -7,6 +7,8 @@
 // (the soft-locking decision of steps 12-14 needs ||r_t||).
 #include <nccl.h>
 
+#include "comm.cuh"
+
 #include <algorithm>
 #include <chrono>
 #include <cmath>
@@ -66,7 +68,8 @@ struct trplk_ctx {
     std::vector<int64_t> recv_off, recv_cnt, send_cnt, send_start;
     std::vector<int*> send_idx;
     double* sendbuf = nullptr;
-    ncclComm_t comm = nullptr;
+    Comm* cm = nullptr;    // rank exchanges (NCCL, or the in-process loopback hub)
+    bool loopback = false;  // loopback ranks: eager launches (exchanges are host rendezvous)
     // solve buffers
     int q_alloc = 0, ph_alloc = 0;
     double* U[2] = {nullptr, nullptr};
@@ -109,6 +112,14 @@ namespace {
         ncclResult_t r_ = (call);                                                      \
         if (r_ != ncclSuccess) {                                                       \
             ctx->err = std::string(#call) + ": " + ncclGetErrorString(r_);             \
+            return TRPLK_ENCCL;                                                        \
+        }                                                                              \
+    } while (0)
+
+#define CM(call)                                                                       \
+    do {                                                                               \
+        if (!(call)) {                                                                 \
+            ctx->err = std::string(#call) + ": " + ctx->cm->what();                    \
             return TRPLK_ENCCL;                                                        \
         }                                                                              \
     } while (0)
@@ -399,20 +410,18 @@ trplk_status halo(trplk_ctx* ctx, const double* xconst) {
         }
         off += ctx->send_cnt[i];
     }
-    NK(ncclGroupStart());
+    std::vector<Xfer> sends, recvs;
     off = 0;
     for (size_t i = 0; i < ctx->peers.size(); ++i) {
         const int pr = ctx->peers[i];
-        if (ctx->recv_cnt[i] > 0)
-            NK(ncclRecv(x + ctx->n_loc + ctx->recv_off[i], (size_t)ctx->recv_cnt[i], ncclDouble, pr, ctx->comm,
-                        ctx->stream));
+        if (ctx->recv_cnt[i] > 0) recvs.push_back({pr, x + ctx->n_loc + ctx->recv_off[i], (size_t)ctx->recv_cnt[i]});
         if (ctx->send_cnt[i] > 0) {
-            const double* src = ctx->send_start[i] >= 0 ? x + ctx->send_start[i] : ctx->sendbuf + off;
-            NK(ncclSend(src, (size_t)ctx->send_cnt[i], ncclDouble, pr, ctx->comm, ctx->stream));
+            double* src = ctx->send_start[i] >= 0 ? x + ctx->send_start[i] : ctx->sendbuf + off;
+            sends.push_back({pr, src, (size_t)ctx->send_cnt[i]});
         }
         off += ctx->send_cnt[i];
     }
-    NK(ncclGroupEnd());
+    CM(ctx->cm->sendrecv(sends, recvs, 8, ctx->stream));
     return TRPLK_OK;
 }
 
@@ -474,7 +483,7 @@ trplk_status run_sdots(trplk_ctx* ctx, SdotsArgs a, int kbytes_cols, bool count_
     if (ctx->nranks > 1) {
         a.red_local = ctx->red_local;
         launch_sdots(a, kmax, ctx->stream);
-        NK(ncclAllGather(ctx->red_local, ctx->red_all, NV_MAX, ncclDouble, ctx->comm, ctx->stream));
+        CM(ctx->cm->allgather(ctx->red_local, ctx->red_all, NV_MAX, 8, ctx->stream));
         launch_finalize_sdots_multi(a, ctx->red_all, ctx->nranks, NV_MAX, ctx->stream);
     } else {
         launch_sdots(a, kmax, ctx->stream);
@@ -491,7 +500,7 @@ trplk_status run_upd(trplk_ctx* ctx, UpdArgs a, int k_nominal) {
     if (ctx->nranks > 1 && dots) {
         a.red_local = ctx->red_local;
         launch_upd(a, kmax, ctx->stream);
-        NK(ncclAllGather(ctx->red_local, ctx->red_all, NV_MAX, ncclDouble, ctx->comm, ctx->stream));
+        CM(ctx->cm->allgather(ctx->red_local, ctx->red_all, NV_MAX, 8, ctx->stream));
         launch_finalize_upd_multi(a, ctx->red_all, ctx->nranks, NV_MAX, ctx->stream);
     } else {
         launch_upd(a, kmax, ctx->stream);
@@ -804,6 +813,7 @@ trplk_status issue_cycle(trplk_ctx* ctx, const Sizes& S, int cur, int nprev, int
 }
 
 trplk_status run_cycle(trplk_ctx* ctx, const Sizes& S, int cur, int nprev, int t, int xprev, bool use_graph) {
+    if (ctx->loopback) use_graph = false;  // loopback exchanges are host rendezvous: eager only
     const bool multi = ctx->nranks > 1;
     const int ts = multi ? t : -1;  // static addresses are needed for the halo exchange
     const int xs = multi ? xprev : -1;
@@ -888,8 +898,8 @@ static trplk_status create_impl(trplk_ctx* ctx, int64_t n_global, const int64_t*
             ctx->err = "bad trplk_dist (rank/nranks/row range)";
             return TRPLK_EINVAL;
         }
-        if (ctx->nranks > 1 && !dist->nccl_unique_id) {
-            ctx->err = "nranks > 1 needs nccl_unique_id";
+        if (ctx->nranks > 1 && !dist->nccl_unique_id && !dist->loopback) {
+            ctx->err = "nranks > 1 needs nccl_unique_id (or a loopback hub)";
             return TRPLK_EINVAL;
         }
     } else {
@@ -910,9 +920,21 @@ static trplk_status create_impl(trplk_ctx* ctx, int64_t n_global, const int64_t*
     if (ctx->hasB) ST(validate_csr(ctx, "B", b_rowptr, b_col));
 
     if (ctx->nranks > 1) {
-        ncclUniqueId id;
-        memcpy(&id, dist->nccl_unique_id, sizeof(id));
-        NK(ncclCommInitRank(&ctx->comm, ctx->nranks, id, ctx->rank));
+        if (dist->loopback) {
+            LoopHub* hub = static_cast<LoopHub*>(dist->loopback);
+            if (hub->n != ctx->nranks) {
+                ctx->err = "loopback hub size != nranks";
+                return TRPLK_EINVAL;
+            }
+            ctx->cm = new LoopComm(hub, ctx->rank);
+            ctx->loopback = true;
+        } else {
+            NcclComm* c = new NcclComm();
+            ctx->cm = c;
+            ncclUniqueId id;
+            memcpy(&id, dist->nccl_unique_id, sizeof(id));
+            NK(ncclCommInitRank(&c->comm, ctx->nranks, id, ctx->rank));
+        }
     }
     // ghost columns (global ids outside the owned range), sorted
     const std::vector<int64_t> ghosts =
@@ -979,19 +1001,15 @@ static trplk_status create_impl(trplk_ctx* ctx, int64_t n_global, const int64_t*
     if (ctx->nranks > 1) {
         // global ||A||_F^2 and max |A_jj|
         double* tmp;
-        ST(dalloc(ctx, &tmp, 2));
-        CK(cudaMemcpyAsync(tmp, &fro2, 8, cudaMemcpyHostToDevice, ctx->stream));
-        CK(cudaMemcpyAsync(tmp + 1, &amax, 8, cudaMemcpyHostToDevice, ctx->stream));
-        NK(ncclAllReduce(tmp, tmp, 1, ncclDouble, ncclSum, ctx->comm, ctx->stream));
-        NK(ncclAllReduce(tmp + 1, tmp + 1, 1, ncclDouble, ncclMax, ctx->comm, ctx->stream));
-        CK(cudaMemcpyAsync(&fro2, tmp, 8, cudaMemcpyDeviceToHost, ctx->stream));
-        CK(cudaMemcpyAsync(&amax, tmp + 1, 8, cudaMemcpyDeviceToHost, ctx->stream));
+        ST(dalloc(ctx, &tmp, 2 + 2 * (size_t)ctx->nranks));
+        CM(ctx->cm->allreduce_host(&fro2, 1, 0, ctx->stream, tmp));
+        CM(ctx->cm->allreduce_host(&amax, 1, 1, ctx->stream, tmp));
         // all row ranges
         int64_t* ranges;
         ST(dalloc(ctx, &ranges, 2 * (size_t)ctx->nranks + 2));
         int64_t mine[2] = {ctx->row_begin, ctx->row_end};
         CK(cudaMemcpyAsync(ranges + 2 * ctx->nranks, mine, 16, cudaMemcpyHostToDevice, ctx->stream));
-        NK(ncclAllGather(ranges + 2 * ctx->nranks, ranges, 2, ncclInt64, ctx->comm, ctx->stream));
+        CM(ctx->cm->allgather(ranges + 2 * ctx->nranks, ranges, 2, 8, ctx->stream));
         std::vector<int64_t> rg(2 * (size_t)ctx->nranks);
         CK(cudaMemcpyAsync(rg.data(), ranges, 16 * (size_t)ctx->nranks, cudaMemcpyDeviceToHost, ctx->stream));
         CK(cudaStreamSynchronize(ctx->stream));
@@ -1020,8 +1038,7 @@ static trplk_status create_impl(trplk_ctx* ctx, int64_t n_global, const int64_t*
         ST(dalloc(ctx, &cnts, (size_t)ctx->nranks * ctx->nranks + ctx->nranks));
         CK(cudaMemcpyAsync(cnts + (size_t)ctx->nranks * ctx->nranks, need_cnt.data(), 8 * (size_t)ctx->nranks,
                            cudaMemcpyHostToDevice, ctx->stream));
-        NK(ncclAllGather(cnts + (size_t)ctx->nranks * ctx->nranks, cnts, ctx->nranks, ncclInt64, ctx->comm,
-                         ctx->stream));
+        CM(ctx->cm->allgather(cnts + (size_t)ctx->nranks * ctx->nranks, cnts, ctx->nranks, 8, ctx->stream));
         std::vector<int64_t> cm((size_t)ctx->nranks * ctx->nranks);
         CK(cudaMemcpyAsync(cm.data(), cnts, 8 * cm.size(), cudaMemcpyDeviceToHost, ctx->stream));
         CK(cudaStreamSynchronize(ctx->stream));
@@ -1031,17 +1048,17 @@ static trplk_status create_impl(trplk_ctx* ctx, int64_t n_global, const int64_t*
         if (!ghosts.empty())
             CK(cudaMemcpyAsync(gdev, ghosts.data(), 8 * ghosts.size(), cudaMemcpyHostToDevice, ctx->stream));
         std::vector<int64_t*> req(ctx->nranks, nullptr);
-        NK(ncclGroupStart());
+        std::vector<Xfer> sends, recvs;
         for (int s = 0; s < ctx->nranks; ++s) {
             if (s == ctx->rank) continue;
             const int64_t they_need = cm[(size_t)s * ctx->nranks + ctx->rank];
             if (they_need > 0) {
                 ST(dalloc(ctx, &req[s], (size_t)they_need));
-                NK(ncclRecv(req[s], (size_t)they_need, ncclInt64, s, ctx->comm, ctx->stream));
+                recvs.push_back({s, req[s], (size_t)they_need});
             }
-            if (need_cnt[s] > 0) NK(ncclSend(gdev + need_off[s], (size_t)need_cnt[s], ncclInt64, s, ctx->comm, ctx->stream));
+            if (need_cnt[s] > 0) sends.push_back({s, gdev + need_off[s], (size_t)need_cnt[s]});
         }
-        NK(ncclGroupEnd());
+        CM(ctx->cm->sendrecv(sends, recvs, 8, ctx->stream));
         CK(cudaStreamSynchronize(ctx->stream));
         int64_t sendtot = 0;
         for (int s = 0; s < ctx->nranks; ++s) {
@@ -1115,7 +1132,7 @@ void trplk_destroy(trplk_ctx* ctx) {
         if (e) cudaEventDestroy(e);
     if (ctx->ev_out) cudaEventDestroy(ctx->ev_out);
     if (ctx->stream) cudaStreamDestroy(ctx->stream);
-    if (ctx->comm) ncclCommDestroy(ctx->comm);
+    delete ctx->cm;
     delete ctx;
 }
 
@@ -1173,6 +1190,7 @@ static trplk_status solve_impl(trplk_ctx* ctx, int p, int q, int l, double tol, 
     ctx->log_ph = ph;
     ctx->a_mv = ctx->b_mv = ctx->prec = ctx->inner = ctx->verify = ctx->draws = 0;
     ctx->model_bytes = 0.0;
+    ctx->launches = 0;  // per-solve count (stats->kernel_launches)
     const double tau = opt.tol_mode == 1 ? tol * ctx->normF : tol;  // eq 5.1 vs Alg.1 step 12 (R8)
     const int64_t ld = ctx->ld;
     cudaEvent_t e0, e1;
@@ -1636,6 +1654,14 @@ trplk_status trplk_k_sym_eig_time(trplk_ctx* ctx, int k, const double* T, int re
     dev_free(ctx, Td);
     return TRPLK_OK;
 }
+
+trplk_status trplk_loopback_create(int nranks, void** hub) {
+    if (nranks < 1 || !hub) return TRPLK_EINVAL;
+    *hub = new LoopHub(nranks);
+    return TRPLK_OK;
+}
+
+void trplk_loopback_destroy(void* hub) { delete static_cast<LoopHub*>(hub); }
 
 trplk_status trplk_k_residual(trplk_ctx* ctx, const double* x, double theta, double* r, double* u, double* rnorm2) {
     ST(kprep(ctx, 0));

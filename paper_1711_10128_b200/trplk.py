@@ -40,7 +40,7 @@ class Allocator(ctypes.Structure):
 
 class Dist(ctypes.Structure):
     _fields_ = [("rank", _I), ("nranks", _I), ("row_begin", _I64), ("row_end", _I64),
-                ("nccl_unique_id", _P)]
+                ("nccl_unique_id", _P), ("loopback", _P)]
 
 
 class Options(ctypes.Structure):
@@ -83,6 +83,8 @@ _sig("trplk_k_rotate", _I, [_P, _P, _I64, _I, _P, _I, _P, _I64])
 _sig("trplk_k_sym_eig", _I, [_P, _I, _P, _P, _P])
 _sig("trplk_k_residual", _I, [_P, _P, _D, _P, _P, _P])
 _sig("trplk_k_sym_eig_time", _I, [_P, _I, _P, _I, _P, _P])
+_sig("trplk_loopback_create", _I, [_I, ctypes.POINTER(_P)])
+_sig("trplk_loopback_destroy", None, [_P])
 _sig("trplk_k_random", _I, [_P, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64, _P])
 _sig("trplk_plan_ghosts", _I, [_I64, _I64, _P, _P, _P, _P, _P, _I, _P, _P, _I64, ctypes.POINTER(_I64)])
 _sig("trplk_profile", _I, [_P, _I])
@@ -92,7 +94,7 @@ EXPORTED = ["trplk_options_default", "trplk_nccl_unique_id", "trplk_create", "tr
             "trplk_get_log", "trplk_info", "trplk_destroy", "trplk_last_error", "trplk_k_spmv",
             "trplk_k_step1", "trplk_k_cgs2", "trplk_k_rotate", "trplk_k_sym_eig",
             "trplk_k_residual", "trplk_k_random", "trplk_profile", "trplk_profile_read",
-            "trplk_plan_ghosts", "trplk_k_sym_eig_time"]
+            "trplk_plan_ghosts", "trplk_k_sym_eig_time", "trplk_loopback_create", "trplk_loopback_destroy"]
 
 
 class TrplkError(RuntimeError):
@@ -181,10 +183,25 @@ def trplk_nccl_unique_id() -> bytes:
     return buf.raw
 
 
+def trplk_loopback_create(nranks: int):
+    """In-process loopback hub (test infrastructure): ranks of one solve as threads on one GPU."""
+    h = _P()
+    st = _lib.trplk_loopback_create(int(nranks), ctypes.byref(h))
+    if st != 0:
+        raise TrplkError(st, "trplk_loopback_create failed")
+    return h
+
+
+def trplk_loopback_destroy(hub):
+    _lib.trplk_loopback_destroy(hub)
+
+
 def trplk_create(A, B=None, sigma: float = 0.0, n_global: Optional[int] = None, row_begin: int = 0,
-                 row_end: Optional[int] = None, group=None, stream=None, torch_alloc: bool = True) -> Context:
+                 row_end: Optional[int] = None, group=None, stream=None, torch_alloc: bool = True,
+                 loopback=None) -> Context:
     """Create a context.  A/B: inputs.CSR (this rank's rows) or scipy CSR.  For several ranks pass
-    the torch.distributed `group` and this rank's row range; rank 0's NCCL id is broadcast."""
+    the torch.distributed `group` and this rank's row range; rank 0's NCCL id is broadcast.
+    loopback=(hub, rank, nranks): the rank of an in-process loopback solve (tests only)."""
     import torch
 
     ra, ca, va = _csr_arrays(A)
@@ -213,11 +230,16 @@ def trplk_create(A, B=None, sigma: float = 0.0, n_global: Optional[int] = None, 
                        group=group)
         idb = ctypes.create_string_buffer(bytes(idt.cpu().numpy().tobytes()), 128)
         keep.append(idb)
-        d = Dist(rank, nranks, row_begin, row_end, ctypes.cast(idb, _P))
+        d = Dist(rank, nranks, row_begin, row_end, ctypes.cast(idb, _P), None)
+        keep.append(d)
+        dist_p = ctypes.byref(d)
+    elif loopback is not None:
+        hub, rank, nranks = loopback
+        d = Dist(rank, nranks, row_begin, row_end, None, hub)
         keep.append(d)
         dist_p = ctypes.byref(d)
     elif row_begin != 0 or row_end != n_global:
-        d = Dist(0, 1, row_begin, row_end, None)
+        d = Dist(0, 1, row_begin, row_end, None, None)
         keep.append(d)
         dist_p = ctypes.byref(d)
     alloc_p = None

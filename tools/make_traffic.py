@@ -20,17 +20,16 @@ acc = {}
 for r in rows[2:]:
     d = dict(zip(hdr, r))
     name = d.get("Kernel Name", "")
-    try:
-        rd = float(d["dram__bytes_read.sum"].replace(",", ""))
-        wr = float(d["dram__bytes_write.sum"].replace(",", ""))
+    SC = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "MB": 1e6, "GB": 1e9}
+    try:  # each column has its own unit (second header row)
+        rd = float(d["dram__bytes_read.sum"].replace(",", "")) * SC.get(rows[1][hdr.index("dram__bytes_read.sum")], 1)
+        wr = float(d["dram__bytes_write.sum"].replace(",", "")) * SC.get(rows[1][hdr.index("dram__bytes_write.sum")], 1)
     except (KeyError, ValueError):
         continue
-    unit = rows[1][hdr.index("dram__bytes_read.sum")]
-    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1)
     key = name.replace("void ", "").split("(")[0]
-    if rd * scale < 1e6:  # gated no-op launches
+    if rd < 1e6:  # gated no-op launches
         continue
-    acc.setdefault(key, []).append((rd + wr) * scale)
+    acc.setdefault(key, []).append(rd + wr)
 res = {k: sum(v) / len(v) for k, v in acc.items()}
 res["source"] = f"ncu --set full (cold cache) of bench.py --config {cfg}; DRAM read+write bytes per launch, " \
     "averaged over the captured launches of each kernel instantiation: " + ", ".join(f"{k}:{len(v)}" for k, v in acc.items())

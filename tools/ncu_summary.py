@@ -10,7 +10,7 @@ import subprocess
 import sys
 
 KEYS = {
-    "gpu__time_duration.sum": "duration_ns",
+    "gpu__time_duration.sum": "duration_us",
     "dram__bytes_read.sum": "dram_read_B",
     "dram__bytes_write.sum": "dram_write_B",
     "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed": "dram_pct",
@@ -24,10 +24,14 @@ KEYS = {
 STALL = "smsp__average_warps_issue_stalled_"
 
 
+SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-3, "usecond": 1, "msecond": 1e3}
+
+
 def raw(rep):
+    """Per launch: durations in microseconds, DRAM bytes in bytes (each column's unit applied)."""
     out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
-    hdr = rows[0]
+    hdr, units = rows[0], dict(zip(rows[0], rows[1]))
     res = []
     for r in rows[2:]:
         d = dict(zip(hdr, r))
@@ -35,7 +39,7 @@ def raw(rep):
         for k, v in KEYS.items():
             if k in d:
                 try:
-                    rec[v] = float(d[k].replace(",", ""))
+                    rec[v] = float(d[k].replace(",", "")) * SCALE.get(units.get(k, ""), 1)
                 except ValueError:
                     rec[v] = d[k]
         stalls = {}
