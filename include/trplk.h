@@ -79,7 +79,7 @@ typedef struct {
                            1 FROB: <= tol*||A||_F (eq 5.1); R8 */
     int restart_size;   /* p^ >= p kept at restart; 0 => p (R5) */
     int lock_mode;      /* 0 IF (one lock per cycle, Alg.1 step 12, R7); 1 WHILE */
-    int debug_checks;   /* reserved (0) */
+    int debug_checks;   /* bit 1 (value 2): force the third CGS pass (R3) -- tests of that path */
     int use_graphs;     /* 1 (default): one CUDA graph per cycle; 0: eager launches */
 } trplk_options;
 

@@ -67,6 +67,12 @@ trplk_status trplk_plan_ghosts(int64_t row_begin, int64_t row_end, const int64_t
                                const int64_t* b_rowptr, const int64_t* b_col, const int64_t* ranges, int nranks,
                                int64_t* ghosts_out, int* owners_out, int64_t cap, int64_t* n_ghost);
 
+/* Debug switches of the context (tests of rare paths).  Bit 0: take the third CGS pass
+ * (reading R3) in every CGS2 even when the second pass kept more than 1/sqrt2 of the norm -- the
+ * same arithmetic as a genuine third pass, so its kernels can be checked against the oracle.
+ * trplk_options.debug_checks bit 1 does the same for one solve.  Errors: EINVAL (ctx NULL). */
+trplk_status trplk_set_debug(trplk_ctx* ctx, int flags);
+
 /* In-process loopback hub for nranks ranks (test infrastructure): pass it as
  * trplk_dist.loopback to every rank's trplk_create, one host thread per rank, all on the same
  * GPU.  Every exchange (halo planes, reduction partials, create-time plans) becomes a rendezvous

@@ -407,7 +407,14 @@ __global__ void __launch_bounds__(EIG1_THREADS) k_eig(Ctl* ctl, double* T, int l
                         block22(a, bb, cc, dd, pc[cur][i], ps[cur][i], pc[cur][j], ps[cur][j], m00, m01, m10, m11);
                         axy = xp ? (yp ? m00 : m01) : (yp ? m10 : m11);
                     }
+#ifdef EIG_TRACE
+                    long long tb = clock64();
+                    if (m == 0) atomicAdd(&eig_trace[16], (unsigned long long)(tb - tr0));
+#endif
                     jacobi_param(dx, dy, axy, fro, c, s, dx, dy, act);
+#ifdef EIG_TRACE
+                    if (m == 0) atomicAdd(&eig_trace[17], (unsigned long long)(clock64() - tb));
+#endif
                 }
                 pc[nxt][m] = c; ps[nxt][m] = s; pdp[nxt][m] = dx; pdq[nxt][m] = dy;
                 pp[nxt][m] = x; pq[nxt][m] = y; pact[nxt][m] = act;

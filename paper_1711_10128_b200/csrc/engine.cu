@@ -69,6 +69,7 @@ struct trplk_ctx {
     std::vector<int*> send_idx;
     double* sendbuf = nullptr;
     Comm* cm = nullptr;    // rank exchanges (NCCL, or the in-process loopback hub)
+    int force3 = 0;        // debug: force the third CGS pass (trplk_set_debug / options.debug_checks & 2)
     bool loopback = false;  // loopback ranks: eager launches (exchanges are host rendezvous)
     // solve buffers
     int q_alloc = 0, ph_alloc = 0;
@@ -509,6 +510,26 @@ trplk_status run_upd(trplk_ctx* ctx, UpdArgs a, int k_nominal) {
     return TRPLK_OK;
 }
 
+// One rank and B = I: the FINAL kernel is launched cooperatively and runs a third pass itself
+// (grid barrier), so the two gated pass-3 launches (~2.5 us each, normally no-ops) disappear
+// from every CGS2.  TRPLK_NO_COOP3=1 keeps the gated launches.
+// The debug switch changes the captured kernels' arguments: drop the cached graphs.
+void set_force3(trplk_ctx* ctx, int v) {
+    if (ctx->force3 == v) return;
+    ctx->force3 = v;
+    for (auto& g : ctx->graphs) cudaGraphExecDestroy(g.second.exec);
+    ctx->graphs.clear();
+}
+
+bool coop3(const trplk_ctx* ctx) {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("TRPLK_NO_COOP3");
+        v = (e && e[0] == '1') ? 0 : 1;
+    }
+    return v == 1 && ctx->nranks == 1 && !ctx->hasB;
+}
+
 // CGS2 in the B-inner product (R3) of x against V = Ubase(:, 0:kv) (kv = -1: ctl->k), result
 // normalised into Ubase(:, ctl->k) (dest_dyn) or `dest`, ctl->k += 1 on success.
 struct CgsSpec {
@@ -606,7 +627,10 @@ trplk_status cgs2(trplk_ctx* ctx, const CgsSpec& c) {
         u.inc_k = c.inc_k;
         u.gate = c.gate;
         u.clear_on_brk = c.clear;
+        u.force3 = ctx->force3;
+        u.coop = coop3(ctx);
         ST(run_upd(ctx, u, kn));
+        if (u.coop) return TRPLK_OK;  // the third pass, when needed, ran inside the FINAL kernel
     }
     {  // third-pass dots h3 = V^T B w2, N_2SQ_EXP = w2^T B w2 (gated on ctl->pass3, normally a no-op)
         SdotsArgs a = sd_base(ctx);
@@ -1191,6 +1215,7 @@ static trplk_status solve_impl(trplk_ctx* ctx, int p, int q, int l, double tol, 
     ctx->a_mv = ctx->b_mv = ctx->prec = ctx->inner = ctx->verify = ctx->draws = 0;
     ctx->model_bytes = 0.0;
     ctx->launches = 0;  // per-solve count (stats->kernel_launches)
+
     const double tau = opt.tol_mode == 1 ? tol * ctx->normF : tol;  // eq 5.1 vs Alg.1 step 12 (R8)
     const int64_t ld = ctx->ld;
     cudaEvent_t e0, e1;
@@ -1468,11 +1493,21 @@ finish:
 trplk_status trplk_solve(trplk_ctx* ctx, int p, int max_basis, int k_plus, double tol, double* eigenvalues,
                          double* eigenvectors, double* residual_norms, const trplk_options* opt, trplk_stats* stats) {
     if (!ctx) return TRPLK_EINVAL;
+    const int f3 = ctx->force3;
+    const int f3_solve = f3 | ((opt && (opt->debug_checks & 2)) ? 1 : 0);
+    if (f3_solve != f3) set_force3(ctx, f3_solve);
     enter_stream(ctx);
     const trplk_status st =
         solve_impl(ctx, p, max_basis, k_plus, tol, eigenvalues, eigenvectors, residual_norms, opt, stats);
     leave_stream(ctx);
+    if (f3_solve != f3) set_force3(ctx, f3);
     return st;
+}
+
+trplk_status trplk_set_debug(trplk_ctx* ctx, int flags) {
+    if (!ctx) return TRPLK_EINVAL;
+    set_force3(ctx, flags & 1);
+    return TRPLK_OK;
 }
 
 // ------------------------------------------------------------ kernel-level entry points

@@ -17,6 +17,8 @@
 #include <mutex>
 #include <unordered_map>
 
+#include <cooperative_groups.h>
+
 #include "trplk_internal.cuh"
 
 namespace trplk {
@@ -615,6 +617,66 @@ __device__ void upd_finalize(const UpdArgs& a, const double* r, int kv) {
     if (threadIdx.x == 0) ctl->nrm[a.mode == 1 ? N_1SQ : N_2SQ_EXP] = r[kv];
 }
 
+// Third CGS pass inside a cooperatively launched FINAL kernel (reading R3; one rank, B = I):
+// w2 = w1 - U h2 is already in a.out for this CTA's rows; h3 = U^T w2 and ||w2||^2 are reduced
+// over the grid (per-CTA partials, grid barrier, the same fixed-order sum in every CTA), then
+// g = (w2 - U h3) / beta3 with beta3^2 = ||w2||^2 - ||h3||^2.  Rare path (a second pass that
+// loses more than half the norm): written for few registers, not speed.  Returns breakdown.
+__device__ __noinline__ bool final_pass3_coop(const UpdArgs& a, int kv, double nin, double* dest, double* sred) {
+    namespace cg = cooperative_groups;
+    __shared__ double acc3[WARPS][QMAX + 1];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int i = threadIdx.x; i < WARPS * (QMAX + 1); i += CTA) (&acc3[0][0])[i] = 0.0;
+    __syncthreads();
+    const int64_t ntiles = (a.nrows + 31) >> 5;
+    double yy = 0.0;
+    for (int64_t tile = (int64_t)blockIdx.x * WARPS + warp; tile < ntiles; tile += (int64_t)gridDim.x * WARPS) {
+        const int64_t row = tile * 32 + lane;
+        const bool ok = row < a.nrows;
+        const double y = ok ? a.out[row] : 0.0;
+        yy += y * y;
+        for (int c = 0; c < kv; ++c) {
+            const double v = warp_sum(ok ? __ldg(a.U + (int64_t)c * a.ldu + row) * y : 0.0);
+            if (lane == 0) acc3[warp][c] += v;
+        }
+    }
+    yy = warp_sum(yy);
+    if (lane == 0) acc3[warp][kv] = yy;
+    __syncthreads();
+    for (int v = threadIdx.x; v <= kv; v += CTA) {
+        double t = 0.0;
+        for (int w = 0; w < WARPS; ++w) t += acc3[w][v];
+        a.part[(int64_t)v * a.maxcta + blockIdx.x] = t;
+    }
+    __threadfence();
+    cg::this_grid().sync();
+    for (int v = threadIdx.x; v <= kv; v += CTA) {  // every CTA: the same fixed-order sum
+        double t = 0.0;
+        for (int c = 0; c < (int)gridDim.x; ++c) t += __ldcg(a.part + (int64_t)v * a.maxcta + c);
+        sred[v] = t;
+    }
+    __syncthreads();
+    double hn = 0.0;
+    for (int i = 0; i < kv; ++i) hn += sred[i] * sred[i];
+    const double n3sq = sred[kv] - hn;
+    const double b = sqrt(n3sq > 0.0 ? n3sq : 0.0);
+    const bool brk = !(b >= 1e-14 * nin) || nin == 0.0;
+    if (!brk) {
+        const double binv = 1.0 / b;
+        for (int64_t tile = (int64_t)blockIdx.x * WARPS + warp; tile < ntiles; tile += (int64_t)gridDim.x * WARPS) {
+            const int64_t row = tile * 32 + lane;
+            if (row >= a.nrows) continue;
+            double y = a.out[row];
+            for (int c = 0; c < kv; ++c) y = fma(-sred[c], __ldg(a.U + (int64_t)c * a.ldu + row), y);
+            const double g = y * binv;
+            dest[row] = g;
+            if (a.dest2) a.dest2[row] = g;
+        }
+    }
+    cg::this_grid().sync();  // the partials buffer is free again before any CTA leaves
+    return brk;
+}
+
 // DOTS = true: mode 1 (update + U^T y dots); DOTS = false: modes 0 / 2 / 3 (no dots; the rare
 // third-pass dots are a separate gated k_sdots launch).
 template <int KMAX, bool DOTS>
@@ -641,7 +703,7 @@ __global__ void __launch_bounds__(CTA, DOTS ? 2 : (KMAX <= 16 ? 3 : (KMAX <= 32 
         if (a.mode == 2) {
             const double n1sq = ctl->nrm[N_1SQ];
             const double n2sq = n1sq - hn;    // ||w''||^2 = ||w'||^2 - ||h2||^2 (U B-orthonormal)
-            pass3 = !(n2sq >= 0.5 * n1sq);    // second pass dropped the norm by > 1/sqrt2
+            pass3 = !(n2sq >= 0.5 * n1sq) || a.force3;  // second pass dropped the norm by > 1/sqrt2
             b = sqrt(n2sq > 0.0 ? n2sq : 0.0);
         } else {
             const double n3sq = ctl->nrm[N_2SQ_EXP] - hn;
@@ -719,6 +781,13 @@ __global__ void __launch_bounds__(CTA, DOTS ? 2 : (KMAX <= 16 ? 3 : (KMAX <= 32 
         }
     }
     if (a.mode == 0) return;
+    bool brk3 = false, done3 = false;
+    if (a.mode == 2 && pass3 && a.coop) {
+        __syncthreads();
+        double* d3 = a.dest_dyn ? a.dest + a.dest_ld * (int64_t)ctl->k : a.dest;
+        brk3 = final_pass3_coop(a, kv, sqrt(ctl->nrm[N_IN2]), d3, res);
+        done3 = true;
+    }
     const int nv = do_dots ? kv + 1 : 0;
     __shared__ bool is_last;
     if (nv) {
@@ -760,7 +829,17 @@ __global__ void __launch_bounds__(CTA, DOTS ? 2 : (KMAX <= 16 ? 3 : (KMAX <= 32 
         if (threadIdx.x == 0) *a.counter = 0u;
     }
     if (threadIdx.x == 0) {
-        if (a.mode == 2) {
+        if (a.mode == 2 && done3) {  // third pass done in this kernel
+            for (int i = 0; i < kv; ++i) ctl->h[2][i] = res[i];  // h3 and ||w2||^2 (reported by the API)
+            ctl->nrm[N_2SQ_EXP] = res[kv];
+            ctl->pass3_count += 1;
+            if (brk3) {
+                ctl->flags &= ~a.clear_on_brk;
+                ctl->brk += 1;
+            } else if (a.inc_k) {
+                ctl->k += 1;
+            }
+        } else if (a.mode == 2) {
             if (pass3) {
                 ctl->pass3 = 1;
                 ctl->pass3_count += 1;
@@ -1153,6 +1232,15 @@ static int k1var() {
     return v;
 }
 
+static bool coop_final() {  // experiment: FINAL as a cooperative launch (TRPLK_COOP=1)
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("TRPLK_COOP");
+        v = (e && e[0] == '1') ? 1 : 0;
+    }
+    return v == 1;
+}
+
 static int num_sms() {
     static int n = 0;
     if (n == 0) {
@@ -1272,7 +1360,20 @@ void launch_sdots(const SdotsArgs& a, int kmax, cudaStream_t s) {
             kern<<<stream_grid(kern, a.nrows), CTA, 0, s>>>(a);    \
         } else {                                                   \
             auto kern = k_upd<KM, false>;                          \
-            kern<<<stream_grid(kern, a.nrows), CTA, 0, s>>>(a);    \
+            if (a.mode == 2 && (a.coop || coop_final())) {         \
+                cudaLaunchConfig_t cfg{};                          \
+                cfg.gridDim = stream_grid(kern, a.nrows);          \
+                cfg.blockDim = CTA;                                \
+                cfg.stream = s;                                    \
+                cudaLaunchAttribute at[1];                         \
+                at[0].id = cudaLaunchAttributeCooperative;         \
+                at[0].val.cooperative = 1;                         \
+                cfg.attrs = at;                                    \
+                cfg.numAttrs = 1;                                  \
+                cudaLaunchKernelEx(&cfg, kern, a);                 \
+            } else {                                               \
+                kern<<<stream_grid(kern, a.nrows), CTA, 0, s>>>(a); \
+            }                                                      \
         }                                                          \
     } break;
 

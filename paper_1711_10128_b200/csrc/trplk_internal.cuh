@@ -135,6 +135,8 @@ struct UpdArgs {
     unsigned* counter;
     int maxcta;
     double* red_local;
+    int coop;   // FINAL launched cooperatively: a third pass (R3) runs inside the kernel (1 rank, B = I)
+    int force3; // debug: take the third CGS pass unconditionally (tests of the pass-3 path)
 };
 
 // Kernel launchers (kernels.cu)

@@ -84,6 +84,7 @@ _sig("trplk_k_sym_eig", _I, [_P, _I, _P, _P, _P])
 _sig("trplk_k_residual", _I, [_P, _P, _D, _P, _P, _P])
 _sig("trplk_k_sym_eig_time", _I, [_P, _I, _P, _I, _P, _P])
 _sig("trplk_loopback_create", _I, [_I, ctypes.POINTER(_P)])
+_sig("trplk_set_debug", _I, [_P, _I])
 _sig("trplk_loopback_destroy", None, [_P])
 _sig("trplk_k_random", _I, [_P, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64, _P])
 _sig("trplk_plan_ghosts", _I, [_I64, _I64, _P, _P, _P, _P, _P, _I, _P, _P, _I64, ctypes.POINTER(_I64)])
@@ -94,7 +95,8 @@ EXPORTED = ["trplk_options_default", "trplk_nccl_unique_id", "trplk_create", "tr
             "trplk_get_log", "trplk_info", "trplk_destroy", "trplk_last_error", "trplk_k_spmv",
             "trplk_k_step1", "trplk_k_cgs2", "trplk_k_rotate", "trplk_k_sym_eig",
             "trplk_k_residual", "trplk_k_random", "trplk_profile", "trplk_profile_read",
-            "trplk_plan_ghosts", "trplk_k_sym_eig_time", "trplk_loopback_create", "trplk_loopback_destroy"]
+            "trplk_plan_ghosts", "trplk_k_sym_eig_time", "trplk_loopback_create", "trplk_loopback_destroy",
+            "trplk_set_debug"]
 
 
 class TrplkError(RuntimeError):
@@ -194,6 +196,11 @@ def trplk_loopback_create(nranks: int):
 
 def trplk_loopback_destroy(hub):
     _lib.trplk_loopback_destroy(hub)
+
+
+def trplk_set_debug(ctx, flags: int):
+    """Debug switches (bit 0: force the third CGS pass)."""
+    ctx.check(_lib.trplk_set_debug(ctx.handle, int(flags)))
 
 
 def trplk_create(A, B=None, sigma: float = 0.0, n_global: Optional[int] = None, row_begin: int = 0,

@@ -156,6 +156,31 @@ def test_cgs2_B_inner_product(orc, problems, case, k):
         assert brk and orc.cgs2(U, wd, P.B)[3]
 
 
+@pytest.mark.parametrize("case", ["C2-19", "C4-9"])
+@pytest.mark.parametrize("k", [5, 33])
+def test_cgs2_forced_third_pass(orc, problems, case, k):
+    """Reading R3's third pass, forced (trplk_set_debug): B = I runs it inside the cooperatively
+    launched FINAL kernel, B != I through the gated pass-3 launches.  A third projection of a
+    vector already B-orthogonal to U changes it only at rounding level, so the result must still
+    equal the oracle's two-pass CGS2 (normwise 1e-12) and report 3 passes."""
+    torch, trplk = need_gpu()
+    P = problems[case]
+    n = P.A.n
+    ctx = _ctx(trplk, P)
+    trplk.trplk_set_debug(ctx, 1)
+    U = b_orthonormal_block(orc, n, k, P.B, seed=13)
+    w0 = np.random.default_rng(k + 7).standard_normal(n)
+    out = torch.zeros(ctx.ld, dtype=torch.float64, device="cuda")
+    h, beta, brk, passes = trplk.trplk_k_cgs2(ctx, to_dev(torch, U, ctx.ld), ctx.ld, k, to_dev(torch, w0, ctx.ld),
+                                              out)
+    w_o, h_o, beta_o, brk_o, passes_o = orc.cgs2(U, w0, P.B)
+    assert passes == 3 and not brk and not brk_o
+    assert abs(beta - beta_o) <= 1e-12 * beta_o
+    assert normwise(out.cpu().numpy()[:n], w_o / beta_o) <= 1e-12
+    assert np.all(np.abs(h - h_o) <= 1e-12 * np.linalg.norm(w0))
+    trplk.trplk_set_debug(ctx, 0)
+
+
 @pytest.mark.parametrize("ncol", [1, 5, 8, 10, 20, 24])
 @pytest.mark.parametrize("k", [1, 6, 30, 64])
 def test_rotate_dmma(orc, problems, ncol, k):

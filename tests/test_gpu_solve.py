@@ -195,3 +195,18 @@ def test_full_C2_parity(orc, gen):
     g = gpu_solve(trplk, P)
     o = oracle_solve(orc, P, want_vectors=False)
     check_parity(g, o, P, allow_tie_divergence=True)
+
+
+@pytest.mark.parametrize("name,N", [("C2", 12), ("C4", 8)])
+def test_solve_with_forced_third_pass(orc, gen, name, N):
+    """Every CGS2 of the solve takes the third pass (options.debug_checks bit 1): the same
+    trajectory as the oracle's two-pass run (the third projection is rounding-level), so the
+    A-matvec count and the eigenvalues agree."""
+    torch, trplk = need_gpu()
+    P = gen.make(name, N=N)
+    g = gpu_solve(trplk, P, debug_checks=2)
+    o = oracle_solve(orc, P, want_vectors=False)
+    assert g["stats"]["status"] == "OK"
+    assert g["stats"]["a_matvecs"] == o["a_matvecs"]
+    assert np.max(np.abs(g["eigenvalues"] - o["eigenvalues"]) / np.abs(o["eigenvalues"])) <= 1e-9
+    assert np.all(g["residuals"] <= P.tol)

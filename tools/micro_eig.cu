@@ -48,5 +48,7 @@ int main(int argc, char** argv) {
     printf("k=%d  %.1f us/launch  sweeps %d  rounds/launch %.0f  cycles/round %.0f (%s)\n", k, 1e3 * ms / reps,
            hh.eig_sweeps, rounds / reps, t[31] / rounds, cudaGetErrorString(cudaGetLastError()));
     for (int w = 0; w < EIG1_THREADS / 32; ++w) printf("  warp %2d: %.0f cycles to barrier\n", w, t[w] / rounds);
+    printf("  warp 0 lane 0: %.0f cycles to the pivot entry, %.0f in the rotation parameters\n", t[16] / rounds,
+           t[17] / rounds);
     return 0;
 }
