@@ -313,14 +313,24 @@ __global__ void __launch_bounds__(EIG1_THREADS) k_eig(Ctl* ctl, double* T, int l
     __shared__ double fro;
     const int tid = threadIdx.x;
     double f = 0.0;
-    __shared__ unsigned char plr[QMAX - 1][QMAX], pairof[QMAX - 1][QMAX];  // player at pos; pair of player
+    // Static schedule table for the parameter warp: for round r and pair m of round r+1,
+    // .x = players x < y of that pair and the round-r pairs i, j holding them, .y = the players
+    // (p1 < q1) of pair i and (p2 < q2) of pair j -- so the pivot's operands are one table load
+    // away instead of a chain of dependent index loads.
+    __shared__ uint2 nxtab[QMAX - 1][MAXPAIRS];
     {
-        const int kk0 = k + (k & 1);
-        for (int idx = tid; idx < (kk0 - 1) * kk0; idx += EIG1_THREADS) {
-            const int r = idx / kk0, pos = idx % kk0;
-            const int x = rr_player(pos, r, kk0);
-            plr[r][pos] = (unsigned char)x;
-            pairof[r][x] = (unsigned char)(pos < kk0 / 2 ? pos : kk0 - 1 - pos);
+        const int kk0 = k + (k & 1), nr0 = kk0 - 1, np0 = kk0 / 2;
+        for (int idx = tid; idx < nr0 * np0; idx += EIG1_THREADS) {
+            const int r = idx / np0, m = idx % np0, rn = r + 1 == nr0 ? 0 : r + 1;
+            int x = rr_player(m, rn, kk0), y = rr_player(kk0 - 1 - m, rn, kk0);
+            if (x > y) { const int t = x; x = y; y = t; }
+            const int i = pair_of_pos(rr_pos(x, r, kk0), kk0), j = pair_of_pos(rr_pos(y, r, kk0), kk0);
+            int p1 = rr_player(i, r, kk0), q1 = rr_player(kk0 - 1 - i, r, kk0);
+            int p2 = rr_player(j, r, kk0), q2 = rr_player(kk0 - 1 - j, r, kk0);
+            if (p1 > q1) { const int t = p1; p1 = q1; q1 = t; }
+            if (p2 > q2) { const int t = p2; p2 = q2; q2 = t; }
+            nxtab[r][m] = make_uint2((unsigned)x | (unsigned)y << 8 | (unsigned)i << 16 | (unsigned)j << 24,
+                                     (unsigned)p1 | (unsigned)q1 << 8 | (unsigned)p2 << 16 | (unsigned)q2 << 24);
         }
     }
     for (int idx = tid; idx < k * k; idx += EIG1_THREADS) {
@@ -382,22 +392,20 @@ __global__ void __launch_bounds__(EIG1_THREADS) k_eig(Ctl* ctl, double* T, int l
             // rotation parameters of round r+1 (pair m = lane)
             const int m = tid;
             if (m < npairs && sn < maxsweep) {
-                int x = plr[rn][m], y = plr[rn][kk - 1 - m];
-                if (x > y) { const int t = x; x = y; y = t; }
+                const uint2 tb = nxtab[r][m];
+                const int x = tb.x & 255, y = (tb.x >> 8) & 255, i = (tb.x >> 16) & 255, j = tb.x >> 24;
+                const int p1 = tb.y & 255, q1 = (tb.y >> 8) & 255, p2 = (tb.y >> 16) & 255, q2 = tb.y >> 24;
                 double c = 1.0, s = 0.0, dx, dy = 0.0;
                 int act = 0;
-                const int i = pairof[r][x];
-                const bool xp = pp[cur][i] == x;
+                const bool xp = p1 == x;
                 dx = xp ? pdp[cur][i] : pdq[cur][i];
                 if (y < k) {
-                    const int j = pairof[r][y];
-                    const bool yp = pp[cur][j] == y;
+                    const bool yp = p2 == y;
                     dy = yp ? pdp[cur][j] : pdq[cur][j];
                     double axy;
                     if (i == j) {
                         axy = pact[cur][i] ? 0.0 : Ac[x + y * ELD];
                     } else {
-                        const int p1 = pp[cur][i], q1 = pq[cur][i], p2 = pp[cur][j], q2 = pq[cur][j];
                         const bool q1ok = q1 < k, q2ok = q2 < k;
                         const double a = Ac[p1 + p2 * ELD];
                         const double bb = q2ok ? Ac[p1 + q2 * ELD] : 0.0;
