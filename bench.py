@@ -224,8 +224,9 @@ def main():
     value = mv / (ms_per_step / 1e3)
 
     # roofline: inner-step kernel group with the largest share (live CUDA events, per launch)
-    names = ["K1 k_step1_rs (SpMV+Jacobi+T-col/h1 dots)", "K2 k_upd2_rs (CGS pass 2 update+dots)",
-             "K3 k_upd FINAL (+gated pass 3)"]
+    names = ["K1 (k_step1_rs: SpMV + Jacobi + T-column / h1 dots)",
+             "K2 (CGS pass 2: k_upd2_wp update + dots; B != I: the B-SpMV dot passes too)",
+             "K3 (k_upd FINAL update + normalisation)"]
     peak, peak_src = peaks()
     cnt = max(prof["count"], 1)
     per_ms = prof["ms"] / cnt
