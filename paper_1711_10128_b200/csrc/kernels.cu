@@ -1192,6 +1192,7 @@ __global__ void k_gather(const double* x, const int* idx, int64_t n, double* out
 #include "stream_tp.cuh"   // thread-per-row K1 / K2
 #include "stream_cp.cuh"   // cp.async-pipelined K1 / K2
 #include "rotate.cuh"      // shared-memory-staged DMMA rotation (default)
+#include "k1_pipe.cuh"     // software-pipelined K1 (DIA, B = I, k <= 24)
 
 namespace trplk {
 
@@ -1227,7 +1228,7 @@ static int k1var() {
     static int v = -1;
     if (v < 0) {
         const char* e = getenv("TRPLK_K1");
-        v = (e && !strcmp(e, "wp")) ? 1 : 0;
+        v = (e && !strcmp(e, "wp")) ? 1 : (e && !strcmp(e, "pipe")) ? 2 : 0;
     }
     return v;
 }
@@ -1320,6 +1321,11 @@ void launch_sdots(const SdotsArgs& a, int kmax, cudaStream_t s) {
         return;
     if (kmax > 0 && k1_shape) {
         if (k1var() == 1 && launch_step1_wp(a, kmax, s)) return;
+        // pipelined K1: measured faster on long tile loops with a register-resident row (C5,
+        // k <= 16: 10.98 vs 11.53 ms per inner step); equal or slower elsewhere
+        if ((k1var() == 2 || (k1var() == 0 && kmax <= 16 && a.nrows >= (int64_t)1 << 24)) &&
+            launch_step1_pipe(a, kmax, s))
+            return;
         if (kvar() == 3 && launch_step1_rs(a, kmax, s)) return;
         if (kvar() == 4 && launch_step1_cp(a, kmax, s)) return;
         if (kvar() == 1 && launch_step1_tma(a, kmax, s)) return;
