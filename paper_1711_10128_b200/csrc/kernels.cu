@@ -1316,7 +1316,7 @@ int kmax_bucket(int k) {
 void launch_sdots(const SdotsArgs& a, int kmax, cudaStream_t s) {
     // inner-step K1 (and the T-column-only launches): TMA-staged basis stream
     const bool k1_shape = a.A.nrows && a.out_mode <= 2 && a.set1 == 1 && (a.set2 == 0 || a.set2 == 2) &&
-                          (a.norm1 == 0 || a.norm1 == 1) && a.norm2 == 0 && a.x_dyn == 0 && a.uout == nullptr;
+                          (a.norm1 >= 0 && a.norm1 <= 2) && a.norm2 == 0 && a.x_dyn == 0 && a.uout == nullptr;
     if (kmax > 0 && (kvar() == 0 || (kvar() >= 3 && !k1_shape)) && a.out_mode != 4 && launch_step1_tp(a, kmax, s))
         return;
     if (kmax > 0 && k1_shape) {

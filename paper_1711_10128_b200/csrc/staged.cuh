@@ -358,6 +358,7 @@ __global__ void __launch_bounds__(CTA, 2) k_step1_rs(const SdotsArgs a) {
             o = 0.0;
         }
         if (a.norm1 == 1) n1 += o * o;
+        else if (a.norm1 == 2) n1 += xr * z;  // x^T B x of a CGS first pass (z = B x)
         const double v1 = a.set1 == 1 ? z : o;
         double bq[8];
 #pragma unroll
