@@ -243,8 +243,16 @@ def main():
         jmid = max(1, min(m - 1, m // 2))
         kk = P.p + jmid
         bucket = next(b for b in (8, 16, 24, 32, 40, 48, 64) if kk <= b)
-        traffic_kernel = [f"k_step1_rs<{bucket}, 1>", f"k_upd2_rs<{bucket}>", f"k_upd<{bucket}, 0>"][kd]
-        traffic = json.load(open(tfile)).get(traffic_kernel)
+        tj = json.load(open(tfile))
+        # K1 runs k_step1_rs (or the pipelined k_step1_pipe on long slabs), K2 the warp-group
+        # k_upd2_wp<KS, G>, K3 k_upd<KMAX, 0>
+        want = [(f"k_step1_rs<{bucket}, 1>", f"k_step1_pipe<{bucket}, 1>"), ("k_upd2_wp<",),
+                (f"k_upd<{bucket}, 0>",)][kd]
+        for key in tj:
+            if key != "source" and any(key.startswith(w) for w in want):
+                if kd != 1 or int(key.split("<")[1].split(",")[0]) * int(key.split(",")[1].strip(" >")) >= bucket:
+                    traffic_kernel, traffic = key, tj[key]
+                    break
     roof = {"bound": "hbm", "kernel": names[kd], "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
             "frac": round(achieved / peak, 4), "traffic": traffic, "traffic_kernel": traffic_kernel,
             "peak_source": peak_src,
