@@ -622,21 +622,23 @@ __device__ void upd_finalize(const UpdArgs& a, const double* r, int kv) {
 // over the grid (per-CTA partials, grid barrier, the same fixed-order sum in every CTA), then
 // g = (w2 - U h3) / beta3 with beta3^2 = ||w2||^2 - ||h3||^2.  Rare path (a second pass that
 // loses more than half the norm): written for few registers, not speed.  Returns breakdown.
-__device__ __noinline__ bool final_pass3_coop(const UpdArgs& a, int kv, double nin, double* dest, double* sred) {
+__device__ __noinline__ bool final_pass3_coop(const double* __restrict__ U, int64_t ldu, int64_t nrows, const double* w2,
+                                              double* part, int maxcta, double* dest2, int kv, double nin, double* dest,
+                                              double* sred) {
     namespace cg = cooperative_groups;
     __shared__ double acc3[WARPS][QMAX + 1];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (int i = threadIdx.x; i < WARPS * (QMAX + 1); i += CTA) (&acc3[0][0])[i] = 0.0;
     __syncthreads();
-    const int64_t ntiles = (a.nrows + 31) >> 5;
+    const int64_t ntiles = (nrows + 31) >> 5;
     double yy = 0.0;
     for (int64_t tile = (int64_t)blockIdx.x * WARPS + warp; tile < ntiles; tile += (int64_t)gridDim.x * WARPS) {
         const int64_t row = tile * 32 + lane;
-        const bool ok = row < a.nrows;
-        const double y = ok ? a.out[row] : 0.0;
+        const bool ok = row < nrows;
+        const double y = ok ? w2[row] : 0.0;
         yy += y * y;
         for (int c = 0; c < kv; ++c) {
-            const double v = warp_sum(ok ? __ldg(a.U + (int64_t)c * a.ldu + row) * y : 0.0);
+            const double v = warp_sum(ok ? __ldg(U + (int64_t)c * ldu + row) * y : 0.0);
             if (lane == 0) acc3[warp][c] += v;
         }
     }
@@ -646,13 +648,13 @@ __device__ __noinline__ bool final_pass3_coop(const UpdArgs& a, int kv, double n
     for (int v = threadIdx.x; v <= kv; v += CTA) {
         double t = 0.0;
         for (int w = 0; w < WARPS; ++w) t += acc3[w][v];
-        a.part[(int64_t)v * a.maxcta + blockIdx.x] = t;
+        part[(int64_t)v * maxcta + blockIdx.x] = t;
     }
     __threadfence();
     cg::this_grid().sync();
     for (int v = threadIdx.x; v <= kv; v += CTA) {  // every CTA: the same fixed-order sum
         double t = 0.0;
-        for (int c = 0; c < (int)gridDim.x; ++c) t += __ldcg(a.part + (int64_t)v * a.maxcta + c);
+        for (int c = 0; c < (int)gridDim.x; ++c) t += __ldcg(part + (int64_t)v * maxcta + c);
         sred[v] = t;
     }
     __syncthreads();
@@ -665,12 +667,12 @@ __device__ __noinline__ bool final_pass3_coop(const UpdArgs& a, int kv, double n
         const double binv = 1.0 / b;
         for (int64_t tile = (int64_t)blockIdx.x * WARPS + warp; tile < ntiles; tile += (int64_t)gridDim.x * WARPS) {
             const int64_t row = tile * 32 + lane;
-            if (row >= a.nrows) continue;
-            double y = a.out[row];
-            for (int c = 0; c < kv; ++c) y = fma(-sred[c], __ldg(a.U + (int64_t)c * a.ldu + row), y);
+            if (row >= nrows) continue;
+            double y = w2[row];
+            for (int c = 0; c < kv; ++c) y = fma(-sred[c], __ldg(U + (int64_t)c * ldu + row), y);
             const double g = y * binv;
             dest[row] = g;
-            if (a.dest2) a.dest2[row] = g;
+            if (dest2) dest2[row] = g;
         }
     }
     cg::this_grid().sync();  // the partials buffer is free again before any CTA leaves
@@ -785,7 +787,8 @@ __global__ void __launch_bounds__(CTA, DOTS ? 2 : (KMAX <= 16 ? 3 : (KMAX <= 32 
     if (a.mode == 2 && pass3 && a.coop) {
         __syncthreads();
         double* d3 = a.dest_dyn ? a.dest + a.dest_ld * (int64_t)ctl->k : a.dest;
-        brk3 = final_pass3_coop(a, kv, sqrt(ctl->nrm[N_IN2]), d3, res);
+        brk3 = final_pass3_coop(a.U, a.ldu, a.nrows, a.out, a.part, a.maxcta, a.dest2, kv, sqrt(ctl->nrm[N_IN2]), d3,
+                                res);
         done3 = true;
     }
     const int nv = do_dots ? kv + 1 : 0;
