@@ -510,6 +510,17 @@ trplk_status run_upd(trplk_ctx* ctx, UpdArgs a, int k_nominal) {
     return TRPLK_OK;
 }
 
+// Small-n latency path: one CTA runs the whole inner loop (small.cuh) when the local problem
+// is a few rows per thread, one rank, B = I and q <= 24.  TRPLK_NO_SMALL=1 disables it.
+bool small_path(const trplk_ctx* ctx, const Sizes& S) {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("TRPLK_NO_SMALL");
+        v = (e && e[0] == '1') ? 0 : 1;
+    }
+    return v == 1 && ctx->nranks == 1 && !ctx->hasB && ctx->n_loc <= SMALL_NMAX && S.q <= 24;
+}
+
 // One rank and B = I: the FINAL kernel is launched cooperatively and runs a third pass itself
 // (grid barrier), so the two gated pass-3 launches (~2.5 us each, normally no-ops) disappear
 // from every CGS2.  TRPLK_NO_COOP3=1 keeps the gated launches.
@@ -746,7 +757,37 @@ trplk_status issue_cycle(trplk_ctx* ctx, const Sizes& S, int cur, int nprev, int
     }
     // inner steps, eq 3.1
     const int jmid = std::max(1, std::min(S.m - 1, S.m / 2));
-    for (int j = 1; j <= S.m; ++j) {
+    if (small_path(ctx, S)) {  // one CTA runs all m steps (latency path, small.cuh)
+        SmallArgs sa{};
+        sa.A = ctx->A;
+        sa.nrows = ctx->n_loc;
+        sa.U = Uc;
+        sa.ldu = ld;
+        sa.w = ctx->w;
+        sa.w1 = ctx->w1;
+        sa.w2 = ctx->w2;
+        sa.ctl = ctx->ctl;
+        sa.T = ctx->T;
+        sa.ldT = QMAX;
+        sa.m = S.m;
+        sa.sigma = ctx->sigma;
+        sa.mfloor = ctx->mfloor;
+        sa.gate = F_CYCLE | F_INNER;
+        sa.clear = F_INNER;
+        sa.force3 = ctx->force3;
+        if (ctx->prof_on) CK(cudaEventRecordWithFlags(ctx->pev[0], ctx->stream, cudaEventRecordExternal));
+        launch_inner_small(sa, S.q, ctx->stream);
+        CK(cudaGetLastError());
+        if (ctx->prof_on)
+            for (int e = 1; e < 4; ++e) CK(cudaEventRecordWithFlags(ctx->pev[e], ctx->stream, cudaEventRecordExternal));
+        ctx->launches += 1;
+        for (int j = 1; j <= S.m; ++j) {  // byte model of the m steps (as the multi-kernel path)
+            const int k = S.ph + j;
+            ctx->model_bytes += mat_bytes(ctx, false) + vec_bytes(ctx) * (k + 2);
+            if (j < S.m) ctx->model_bytes += 2 * vec_bytes(ctx) * (k + 2);
+        }
+    }
+    for (int j = 1; j <= S.m && !small_path(ctx, S); ++j) {
         const int k = S.ph + j;  // nominal width incl. g_j
         const bool prof = ctx->prof_on && j == jmid && j < S.m;
         const double* g = Uc + ld * (k - 1);
@@ -1368,6 +1409,7 @@ static trplk_status solve_impl(trplk_ctx* ctx, int p, int q, int l, double tol, 
                     CK(cudaEventElapsedTime(&e[0], ctx->pev[0], ctx->pev[1]));
                     CK(cudaEventElapsedTime(&e[1], ctx->pev[1], ctx->pev[2]));
                     CK(cudaEventElapsedTime(&e[2], ctx->pev[2], ctx->pev[3]));
+                    if (small_path(ctx, S)) e[0] /= (float)std::max(G, 1);  // one kernel for all steps
                     const double n = (double)ctx->n_loc, k = (double)(ph + jmid);
                     // matrix bytes of the device format (DIA: 8 ndiag n; SELL: 12 per slot + slice ptrs)
                     const double spA = (double)ctx->sellA_bytes, spB = (double)ctx->sellB_bytes;

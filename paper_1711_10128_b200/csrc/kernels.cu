@@ -1196,6 +1196,7 @@ __global__ void k_gather(const double* x, const int* idx, int64_t n, double* out
 #include "stream_cp.cuh"   // cp.async-pipelined K1 / K2
 #include "rotate.cuh"      // shared-memory-staged DMMA rotation (default)
 #include "k1_pipe.cuh"     // software-pipelined K1 (DIA, B = I, k <= 24)
+#include "small.cuh"       // single-CTA inner loop for small n (latency path)
 
 namespace trplk {
 

@@ -139,7 +139,27 @@ struct UpdArgs {
     int force3; // debug: take the third CGS pass unconditionally (tests of the pass-3 path)
 };
 
+// Single-CTA inner loop of the small-n latency path (small.cuh)
+constexpr int SMALL_NMAX = 8192;  // rows handled by the small path (32 per thread)
+
+struct SmallArgs {
+    Sell A;
+    int64_t nrows;
+    double* U;  // current basis block (column k-1 = g_1 on entry)
+    int64_t ldu;
+    double *w, *w1, *w2;
+    Ctl* ctl;
+    double* T;
+    int ldT;
+    int m;  // inner steps of the cycle
+    double sigma, mfloor;
+    unsigned gate, clear;
+    int force3;
+};
+
+
 // Kernel launchers (kernels.cu)
+bool launch_inner_small(const SmallArgs& a, int kmax, cudaStream_t s);
 void launch_sdots(const SdotsArgs& a, int kmax, cudaStream_t s);
 void launch_upd(const UpdArgs& a, int kmax, cudaStream_t s);
 void launch_eig(Ctl* ctl, double* T, int ldT, double* Y, int ldY, int ph, int k_fixed, unsigned gate,
