@@ -499,6 +499,23 @@ __global__ void __launch_bounds__(EIG1_THREADS) k_eig(Ctl* ctl, double* T, int l
         cur = nxt;
         if (r + 1 == nr) {  // end of a sweep: stop after a sweep without rotations
             if (!rot[sweep] || sn >= maxsweep) break;
+            // ... or when no pivot passes the skip rule any more: the next sweep would rotate
+            // nothing (no entry changes without a rotation), so stopping here gives the same A, V
+            const double* __restrict__ Ar = sm + cur * (QMAX * ELD);
+            const double eps2 = 2.220446049250313e-16 * 2.220446049250313e-16;
+            int live = 0;
+            for (int idx = tid; idx < k * k; idx += EIG1_THREADS) {
+                const int pr = idx % k, qr = idx / k;
+                if (pr < qr) {
+                    const double apq = Ar[pr + qr * ELD];
+                    if (!(apq * apq <= eps2 * fabs(Ar[pr + pr * ELD] * Ar[qr + qr * ELD]) || fabs(apq) <= 1e-30 * fro))
+                        live = 1;
+                }
+            }
+            if (!__syncthreads_or(live)) {
+                ++sweep;  // report the sweep the test replaced
+                break;
+            }
         }
         r = rn;
         sweep = sn;

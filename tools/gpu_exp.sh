@@ -1,6 +1,6 @@
 mkdir -p gpurun_out/exp
 O=gpurun_out/exp
-timeout 1500 python -m pytest tests -m gpu -q -rf --timeout 900 > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+timeout 120 python tools/eig_time.py > $O/eig_1b.txt 2>&1
+timeout 1500 python -m pytest tests -m gpu -q -x -rf --timeout 900 > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
 Q="--steps 3 --warmup 3 --no-e2e --no-cpu-baseline"
-timeout 600 python bench.py --config C1 $Q > $O/b_C1_def.json 2>&1
-TRPLK_NO_SMALL=1 timeout 600 python bench.py --config C1 $Q > $O/b_C1_nosmall.json 2>&1
+timeout 600 python bench.py --config C2 $Q > $O/b_C2_def.json 2>&1
