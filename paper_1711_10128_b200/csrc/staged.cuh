@@ -307,6 +307,10 @@ __global__ void __launch_bounds__(CTA, 1) k_upd2_tma(const UpdArgs a) {
 // U is read from HBM/L2 exactly once; no block-level barriers in the main loop.
 constexpr int WLD = 36;
 
+// Slab width of k_step1_rs: 24 columns up to k = 32; 16 beyond, where 24 registers of the basis
+// row plus 2 k/8 DMMA accumulators no longer fit 128 registers without spilling.
+__host__ __device__ constexpr int rs_chunk(int kmax) { return kmax < 24 ? kmax : (kmax > 32 ? 16 : 24); }
+
 template <int KMAX, bool TWO>
 __global__ void __launch_bounds__(CTA, 2) k_step1_rs(const SdotsArgs a) {
     Ctl* ctl = a.ctl;
@@ -320,7 +324,7 @@ __global__ void __launch_bounds__(CTA, 2) k_step1_rs(const SdotsArgs a) {
     const int nn = (a.norm1 ? 1 : 0) + (a.norm2 ? 1 : 0);
     const int nv = k1 + k2 + nn;
     const double* __restrict__ X = a.x;
-    constexpr int CH = KMAX < 24 ? KMAX : 24;       // columns per chunk (= slab width)
+    constexpr int CH = rs_chunk(KMAX);               // columns per chunk (= slab width)
     extern __shared__ __align__(128) double wsm[];  // WARPS x CH x WLD: one chunk per warp
     __shared__ double acc[WARPS][NV_MAX];
     __shared__ double res[NV_MAX];
@@ -583,7 +587,7 @@ static int rs_grid(K kern, int smem, int64_t nrows) {
 
 template <int KMAX, bool TWO>
 static void launch_step1_rs_k(const SdotsArgs& a, cudaStream_t s) {
-    const int smem = WARPS * (KMAX < 24 ? KMAX : 24) * WLD * (int)sizeof(double);
+    const int smem = WARPS * rs_chunk(KMAX) * WLD * (int)sizeof(double);
     auto kern = k_step1_rs<KMAX, TWO>;
     kern<<<rs_grid(kern, smem, a.nrows), CTA, smem, s>>>(a);
 }
