@@ -210,3 +210,17 @@ def test_solve_with_forced_third_pass(orc, gen, name, N):
     assert g["stats"]["a_matvecs"] == o["a_matvecs"]
     assert np.max(np.abs(g["eigenvalues"] - o["eigenvalues"]) / np.abs(o["eigenvalues"])) <= 1e-9
     assert np.all(g["residuals"] <= P.tol)
+
+
+@pytest.mark.parametrize("q", [49, 64])
+def test_widest_basis(orc, gen, q):
+    """max_basis up to TRPLK_MAX_BASIS = 64: the k > 48 kernel instantiations (DMMA-fragment K1,
+    4-warp K2 groups, 3-group rotation) against the oracle's trajectory and eigenvalues."""
+    torch, trplk = need_gpu()
+    P = gen.make("C2", N=14, q=q)
+    g = gpu_solve(trplk, P)
+    o = oracle_solve(orc, P, want_vectors=False)
+    assert g["stats"]["status"] == "OK" and o["status"] == "OK"
+    assert g["stats"]["a_matvecs"] == o["a_matvecs"]
+    assert np.max(np.abs(g["eigenvalues"] - o["eigenvalues"]) / np.abs(o["eigenvalues"])) <= 1e-9
+    assert np.all(g["residuals"] <= P.tol)
