@@ -8,8 +8,9 @@ BASELINE config (default configs[1] = C2, 64^3 7-pt Laplacian + diag(d)),
 inputs resident in HBM (the context is created before the timed region).  The
 L2 (126 MB) is flushed between timed steps by writing a 256 MiB buffer.
 `value` = A-matvecs of the solve / solve time (whole job; max over ranks).
-`e2e` = the same metric through the public API with HOST CSR buffers: create
-(H2D of the CSR + SELL conversion) + solve + D2H of eigenvectors + destroy.
+`e2e` = the same metric through the public API with HOST CSR buffers (pinned): create
+(validation scan, H2D of the CSR, DIA/SELL conversion) + solve + D2H of eigenvectors +
+destroy, after min(W, 3) untimed create/solve/destroy rounds.
 `roofline` = the inner-step kernel with the largest share of the step, live
 CUDA-event timing over the timed steps (trplk_profile), algorithmic bytes of
 DESIGN.md, against MEASURED_PEAKS.json hbm_gbs.  `cpu_baseline` = the oracle
@@ -283,7 +284,8 @@ def main():
         h2d = sum(t.numel() * t.element_size() for t in pin)
         d2h = host_evecs.numel() * 8 + 2 * P.p * 8
         et = []
-        for _ in range(max(1, min(args.steps, 3))):
+        ne_warm = max(1, min(args.warmup, 3))
+        for it in range(ne_warm + max(1, min(args.steps, 5))):
             flush.fill_(1.0)
             barrier()
             torch.cuda.synchronize()
@@ -294,7 +296,8 @@ def main():
             c2.close()
             e1.record(stream)
             torch.cuda.synchronize()
-            et.append(e0.elapsed_time(e1))
+            if it >= ne_warm:  # untimed warm-up: first-touch allocator growth, lazy module loads
+                et.append(e0.elapsed_time(e1))
         te = torch.tensor([statistics.mean(et)], dtype=torch.float64, device="cuda")
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)

@@ -15,6 +15,8 @@
 #include <cstdio>
 #include <cstring>
 #include <map>
+#include <memory>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -146,6 +148,64 @@ void leave_stream(trplk_ctx* ctx) {
     }
 }
 
+// Device memory without a caller allocator comes from a process-wide stream-ordered pool per
+// device (cudaMallocFromPoolAsync on the work stream): a create/solve/destroy sequence -- the
+// e2e path -- re-uses the previous context's memory instead of paying cudaMalloc/cudaFree each
+// time.  trplk_destroy trims the pool back to POOL_KEEP bytes (TRPLK_POOL_KEEP_MB, default 8 GB)
+// so a finished large solve does not keep its footprint reserved.
+static std::mutex g_pool_mu;
+static std::map<int, cudaMemPool_t> g_pools;
+
+static cudaMemPool_t device_pool() {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    auto it = g_pools.find(dev);
+    if (it != g_pools.end()) return it->second;
+    cudaMemPoolProps pr{};
+    pr.allocType = cudaMemAllocationTypePinned;
+    pr.handleTypes = cudaMemHandleTypeNone;
+    pr.location.type = cudaMemLocationTypeDevice;
+    pr.location.id = dev;
+    cudaMemPool_t pool = nullptr;
+    if (cudaMemPoolCreate(&pool, &pr) != cudaSuccess) return nullptr;
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    g_pools[dev] = pool;
+    return pool;
+}
+
+static void trim_pool() {
+    cudaMemPool_t pool = device_pool();
+    if (!pool) return;
+    const char* e = getenv("TRPLK_POOL_KEEP_MB");
+    const size_t keep = (e ? (size_t)atoll(e) : (size_t)8192) << 20;
+    cudaMemPoolTrimTo(pool, keep);
+}
+
+// Pinned host blocks for the Ctl mirror, recycled across contexts (cudaMallocHost costs ~ms).
+static std::vector<Ctl*> g_ctl_free;
+
+static Ctl* ctl_host_alloc() {
+    {
+        std::lock_guard<std::mutex> lk(g_pool_mu);
+        if (!g_ctl_free.empty()) {
+            Ctl* c = g_ctl_free.back();
+            g_ctl_free.pop_back();
+            return c;
+        }
+    }
+    Ctl* c = nullptr;
+    if (cudaMallocHost(&c, sizeof(Ctl)) != cudaSuccess) return nullptr;
+    return c;
+}
+
+static void ctl_host_free(Ctl* c) {
+    if (!c) return;
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    g_ctl_free.push_back(c);
+}
+
 trplk_status dev_alloc(trplk_ctx* ctx, void** p, size_t bytes) {
     if (bytes == 0) bytes = 8;
     bytes = (bytes + 255) & ~(size_t)255;
@@ -157,9 +217,10 @@ trplk_status dev_alloc(trplk_ctx* ctx, void** p, size_t bytes) {
             return TRPLK_ENOMEM;
         }
     } else {
-        cudaError_t e = cudaMalloc(&q, bytes);
+        cudaMemPool_t pool = device_pool();
+        cudaError_t e = pool ? cudaMallocFromPoolAsync(&q, bytes, pool, ctx->stream) : cudaMalloc(&q, bytes);
         if (e != cudaSuccess) {
-            ctx->err = std::string("cudaMalloc: ") + cudaGetErrorString(e);
+            ctx->err = std::string("device allocation: ") + cudaGetErrorString(e);
             return e == cudaErrorMemoryAllocation ? TRPLK_ENOMEM : TRPLK_ECUDA;
         }
     }
@@ -168,12 +229,17 @@ trplk_status dev_alloc(trplk_ctx* ctx, void** p, size_t bytes) {
     return TRPLK_OK;
 }
 
+static void dev_release(trplk_ctx* ctx, void* p) {
+    if (ctx->has_alloc) ctx->alloc.free(p, ctx->alloc.user);
+    else if (device_pool()) cudaFreeAsync(p, ctx->stream);
+    else cudaFree(p);
+}
+
 void dev_free(trplk_ctx* ctx, void* p) {
     if (!p) return;
     for (size_t i = 0; i < ctx->allocs.size(); ++i)
         if (ctx->allocs[i].first == p) {
-            if (ctx->has_alloc) ctx->alloc.free(p, ctx->alloc.user);
-            else cudaFree(p);
+            dev_release(ctx, p);
             ctx->allocs.erase(ctx->allocs.begin() + (long)i);
             return;
         }
@@ -297,12 +363,122 @@ std::vector<int> ghost_owners(const std::vector<int64_t>& ghosts, const int64_t*
     return own;
 }
 
+// One parallel pass over a local CSR block (rows [rb, re) of the global matrix): validation,
+// the out-of-slab column ids (ghosts), the distinct diagonal offsets col - row (stops counting
+// past DIA_MAX) and, when values are given, the squared Frobenius norm and max |A_jj|.  The
+// sums are per 4096-row block, combined in block order: independent of the thread count.
+struct CsrScan {
+    std::vector<int64_t> ghosts;  // unsorted, may repeat
+    std::vector<int64_t> offs;    // sorted distinct offsets (meaningful when !too_many)
+    bool too_many = false;
+    double fro2 = 0.0, amax = 0.0;
+};
+
+trplk_status scan_csr(trplk_ctx* ctx, const char* name, const int64_t* rp, const int64_t* ci, const double* va,
+                      CsrScan& out) {
+    if (!rp || !ci) {
+        ctx->err = std::string(name) + ": NULL CSR array";
+        return TRPLK_EINVAL;
+    }
+    const int64_t n = ctx->n_loc, rb = ctx->row_begin, re = ctx->row_end, ng = ctx->n_global, base = rp[0];
+    constexpr int64_t BLK = 4096;
+    const int64_t nb = (n + BLK - 1) / BLK;
+    std::vector<double> bf((size_t)nb, 0.0), ba((size_t)nb, 0.0);
+    std::vector<int64_t> bad((size_t)nb, -1);
+    std::vector<int> badk((size_t)nb, 0);
+#pragma omp parallel
+    {
+        std::vector<int64_t> gl, ol;
+        bool over = false;
+#pragma omp for schedule(static)
+        for (int64_t b = 0; b < nb; ++b) {
+            double f = 0.0, a = 0.0;
+            const int64_t r1 = std::min(n, (b + 1) * BLK);
+            for (int64_t r = b * BLK; r < r1 && bad[b] < 0; ++r) {
+                if (rp[r + 1] < rp[r]) {
+                    bad[b] = r, badk[b] = 1;
+                    break;
+                }
+                int64_t prev = -1;
+                size_t hint = 0;
+                for (int64_t p = rp[r] - base; p < rp[r + 1] - base; ++p) {
+                    const int64_t c = ci[p];
+                    if (c < 0 || c >= ng) {
+                        bad[b] = r, badk[b] = 2;
+                        break;
+                    }
+                    if (c <= prev) {
+                        bad[b] = r, badk[b] = 3;
+                        break;
+                    }
+                    prev = c;
+                    if (va) {
+                        f += va[p] * va[p];
+                        if (c == rb + r) a = std::max(a, std::fabs(va[p]));
+                    }
+                    if (c < rb || c >= re) gl.push_back(c);
+                    if (!over) {
+                        const int64_t off = c - (rb + r);
+                        // offsets of consecutive entries of a row come in the same order row to row
+                        if (hint < ol.size() && ol[hint] == off) {
+                            ++hint;
+                        } else {
+                            auto it = std::find(ol.begin(), ol.end(), off);
+                            if (it == ol.end()) {
+                                ol.push_back(off);
+                                hint = ol.size();
+                                over = ol.size() > (size_t)DIA_MAX;
+                            } else {
+                                hint = (size_t)(it - ol.begin()) + 1;
+                            }
+                        }
+                    }
+                }
+            }
+            bf[b] = f;
+            ba[b] = a;
+        }
+#pragma omp critical
+        {
+            out.ghosts.insert(out.ghosts.end(), gl.begin(), gl.end());
+            out.too_many |= over;
+            for (int64_t o : ol)
+                if (std::find(out.offs.begin(), out.offs.end(), o) == out.offs.end()) out.offs.push_back(o);
+        }
+    }
+    for (int64_t b = 0; b < nb; ++b)
+        if (bad[b] >= 0) {
+            static const char* what[] = {"", "row pointer decreases at row ", "column id out of range in row ",
+                                         "columns not strictly increasing in row "};
+            ctx->err = std::string(name) + ": " + what[badk[b]] + std::to_string(bad[b]);
+            return TRPLK_EINVAL;
+        }
+    for (int64_t b = 0; b < nb; ++b) {
+        out.fro2 += bf[b];
+        out.amax = std::max(out.amax, ba[b]);
+    }
+    if (out.offs.size() > (size_t)DIA_MAX) out.too_many = true;
+    std::sort(out.offs.begin(), out.offs.end());
+    return TRPLK_OK;
+}
+
+static bool host_pinned(const void* p) {
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return at.type == cudaMemoryTypeHost;
+}
+
 // DIA conversion (values only; column = row + offset computed in the kernel).  Used when the
-// local rows hold at most DIA_MAX distinct offsets col - row, the padded diagonals store at
-// most 1.25x the entries, and the ghost columns are the two contiguous ranges just below
-// and above the owned rows (z-slab partitions of stencils).  ok = false otherwise.
+// local rows hold at most DIA_MAX distinct offsets col - row (from scan_csr), the padded
+// diagonals store at most 1.25x the entries, and the ghost columns are the two contiguous
+// ranges just below and above the owned rows (z-slab partitions of stencils).  ok = false
+// otherwise.  Pinned host CSR arrays are copied to the device and scattered there
+// (launch_csr_to_dia); pageable ones are scattered on the host and copied.
 trplk_status try_dia(trplk_ctx* ctx, const int64_t* rp, const int64_t* ci, const double* va,
-                     const std::vector<int64_t>& ghosts, Sell& S, int64_t& bytes, bool& ok) {
+                     const std::vector<int64_t>& ghosts, const CsrScan& sc, Sell& S, int64_t& bytes, bool& ok) {
     ok = false;
     const int64_t n = ctx->n_loc, rb = ctx->row_begin, re = ctx->row_end, base = rp[0];
     int64_t glo = 0;
@@ -310,32 +486,8 @@ trplk_status try_dia(trplk_ctx* ctx, const int64_t* rp, const int64_t* ci, const
     const int64_t ghi = (int64_t)ghosts.size() - glo;
     if (glo > 0 && (ghosts[0] != rb - glo || ghosts[glo - 1] != rb - 1)) return TRPLK_OK;
     if (ghi > 0 && (ghosts[glo] != re || ghosts.back() != re + ghi - 1)) return TRPLK_OK;
-    // distinct offsets (per-thread sets, merged)
-    std::vector<int64_t> offs;
-    bool too_many = false;
-#pragma omp parallel
-    {
-        std::vector<int64_t> loc;
-        bool over = false;
-#pragma omp for schedule(static)
-        for (int64_t r = 0; r < n; ++r) {
-            if (over) continue;
-            for (int64_t p = rp[r] - base; p < rp[r + 1] - base; ++p) {
-                const int64_t off = ci[p] - (rb + r);
-                if (std::find(loc.begin(), loc.end(), off) == loc.end()) {
-                    loc.push_back(off);
-                    if ((int)loc.size() > DIA_MAX) { over = true; break; }
-                }
-            }
-        }
-#pragma omp critical
-        {
-            too_many |= over;
-            for (int64_t o : loc)
-                if (std::find(offs.begin(), offs.end(), o) == offs.end()) offs.push_back(o);
-        }
-    }
-    if (too_many) return TRPLK_OK;
+    if (sc.too_many) return TRPLK_OK;
+    std::vector<int64_t> offs = sc.offs;
     if (std::find(offs.begin(), offs.end(), (int64_t)0) == offs.end()) offs.push_back(0);
     if ((int)offs.size() > DIA_MAX) return TRPLK_OK;
     std::sort(offs.begin(), offs.end());
@@ -345,19 +497,40 @@ trplk_status try_dia(trplk_ctx* ctx, const int64_t* rp, const int64_t* ci, const
     for (int64_t o : offs)
         if (o > INT32_MAX || o < INT32_MIN) return TRPLK_OK;
     const int64_t ldv = ((n + 31) / 32) * 32;
-    std::vector<double> dv((size_t)nd * ldv, 0.0);
-#pragma omp parallel for schedule(static)
-    for (int64_t r = 0; r < n; ++r)
-        for (int64_t p = rp[r] - base; p < rp[r + 1] - base; ++p) {
-            const int64_t off = ci[p] - (rb + r);
-            const int d = (int)(std::lower_bound(offs.begin(), offs.end(), off) - offs.begin());
-            dv[(size_t)d * ldv + r] = va[p];
-        }
     double* dd;
-    ST(dalloc(ctx, &dd, dv.size()));
-    CK(cudaMemcpyAsync(dd, dv.data(), dv.size() * 8, cudaMemcpyHostToDevice, ctx->stream));
-    CK(cudaStreamSynchronize(ctx->stream));
+    ST(dalloc(ctx, &dd, (size_t)nd * ldv));
     S = Sell();
+    for (int d = 0; d < nd; ++d) S.offs[d] = (int)offs[d];
+    if (host_pinned(rp) && host_pinned(ci) && host_pinned(va)) {
+        int64_t *rpd, *cid;
+        double* vad;
+        ST(dalloc(ctx, &rpd, (size_t)n + 1));
+        ST(dalloc(ctx, &cid, (size_t)std::max<int64_t>(nnz, 1)));
+        ST(dalloc(ctx, &vad, (size_t)std::max<int64_t>(nnz, 1)));
+        CK(cudaMemcpyAsync(rpd, rp, 8 * ((size_t)n + 1), cudaMemcpyHostToDevice, ctx->stream));
+        CK(cudaMemcpyAsync(cid, ci, 8 * (size_t)nnz, cudaMemcpyHostToDevice, ctx->stream));
+        CK(cudaMemcpyAsync(vad, va, 8 * (size_t)nnz, cudaMemcpyHostToDevice, ctx->stream));
+        CK(cudaMemsetAsync(dd, 0, 8 * (size_t)nd * ldv, ctx->stream));
+        launch_csr_to_dia(rpd, cid, vad, n, rb, S.offs, nd, ldv, dd, ctx->stream);
+        CK(cudaGetLastError());
+        dev_free(ctx, rpd);
+        dev_free(ctx, cid);
+        dev_free(ctx, vad);
+    } else {
+        std::unique_ptr<double[]> dv(new double[(size_t)nd * ldv]);
+#pragma omp parallel for schedule(static)
+        for (int64_t r = 0; r < ldv; ++r) {
+            for (int d = 0; d < nd; ++d) dv[(size_t)d * ldv + r] = 0.0;
+            if (r >= n) continue;
+            for (int64_t p = rp[r] - base; p < rp[r + 1] - base; ++p) {
+                const int64_t off = ci[p] - (rb + r);
+                const int d = (int)(std::lower_bound(offs.begin(), offs.end(), off) - offs.begin());
+                dv[(size_t)d * ldv + r] = va[p];
+            }
+        }
+        CK(cudaMemcpyAsync(dd, dv.get(), 8 * (size_t)nd * ldv, cudaMemcpyHostToDevice, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+    }
     S.fmt = 1;
     S.nrows = n;
     S.nslices = (n + 31) / 32;
@@ -366,37 +539,10 @@ trplk_status try_dia(trplk_ctx* ctx, const int64_t* rp, const int64_t* ci, const
     S.glo = glo;
     S.nghost = (int64_t)ghosts.size();
     S.dval = dd;
-    for (int d = 0; d < nd; ++d) {
-        S.offs[d] = (int)offs[d];
+    for (int d = 0; d < nd; ++d)
         if (offs[d] == 0) S.diag_slot = d;
-    }
     bytes = (int64_t)nd * n * 8;
     ok = true;
-    return TRPLK_OK;
-}
-
-trplk_status validate_csr(trplk_ctx* ctx, const char* name, const int64_t* rp, const int64_t* ci) {
-    if (!rp || !ci) {
-        ctx->err = std::string(name) + ": NULL CSR array";
-        return TRPLK_EINVAL;
-    }
-    const int64_t base = rp[0];
-    for (int64_t r = 0; r < ctx->n_loc; ++r) {
-        if (rp[r + 1] < rp[r]) {
-            ctx->err = std::string(name) + ": row pointer decreases at row " + std::to_string(r);
-            return TRPLK_EINVAL;
-        }
-        for (int64_t p = rp[r] - base; p < rp[r + 1] - base; ++p) {
-            if (ci[p] < 0 || ci[p] >= ctx->n_global) {
-                ctx->err = std::string(name) + ": column id out of range in row " + std::to_string(r);
-                return TRPLK_EINVAL;
-            }
-            if (p > rp[r] - base && ci[p] <= ci[p - 1]) {
-                ctx->err = std::string(name) + ": columns not strictly increasing in row " + std::to_string(r);
-                return TRPLK_EINVAL;
-            }
-        }
-    }
     return TRPLK_OK;
 }
 
@@ -944,11 +1090,27 @@ trplk_status trplk_nccl_unique_id(void* out, size_t out_bytes) {
 
 const char* trplk_last_error(const trplk_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
 
+// TRPLK_TIMING=1: host wall time of the create phases on stderr (tools/e2e_breakdown.py).
+struct PhaseTimer {
+    const char* what;
+    bool on;
+    std::chrono::steady_clock::time_point t;
+    explicit PhaseTimer(const char* w) : what(w), on(getenv("TRPLK_TIMING") != nullptr), t(std::chrono::steady_clock::now()) {}
+    void mark(const char* phase) {
+        if (!on) return;
+        auto now = std::chrono::steady_clock::now();
+        fprintf(stderr, "[trplk %s] %-10s %8.3f ms\n", what, phase,
+                std::chrono::duration<double, std::milli>(now - t).count());
+        t = now;
+    }
+};
+
 static trplk_status create_impl(trplk_ctx* ctx, int64_t n_global, const int64_t* a_rowptr, const int64_t* a_col,
                                 const double* a_val, const int64_t* b_rowptr, const int64_t* b_col,
                                 const double* b_val, double sigma, const trplk_dist* dist) {
     ctx->n_global = n_global;
     ctx->sigma = sigma;
+    PhaseTimer pt("create");
     if (n_global < 1) {
         ctx->err = "n_global < 1";
         return TRPLK_EINVAL;
@@ -981,8 +1143,11 @@ static trplk_status create_impl(trplk_ctx* ctx, int64_t n_global, const int64_t*
         ctx->err = "A: NULL values";
         return TRPLK_EINVAL;
     }
-    ST(validate_csr(ctx, "A", a_rowptr, a_col));
-    if (ctx->hasB) ST(validate_csr(ctx, "B", b_rowptr, b_col));
+    // validation, ghosts, DIA offsets and norms in one parallel pass per matrix
+    CsrScan scA, scB;
+    ST(scan_csr(ctx, "A", a_rowptr, a_col, a_val, scA));
+    if (ctx->hasB) ST(scan_csr(ctx, "B", b_rowptr, b_col, nullptr, scB));
+    pt.mark("scan");
 
     if (ctx->nranks > 1) {
         if (dist->loopback) {
@@ -1002,8 +1167,10 @@ static trplk_status create_impl(trplk_ctx* ctx, int64_t n_global, const int64_t*
         }
     }
     // ghost columns (global ids outside the owned range), sorted
-    const std::vector<int64_t> ghosts =
-        find_ghosts(ctx->n_loc, ctx->row_begin, ctx->row_end, a_rowptr, a_col, b_rowptr, b_col);
+    std::vector<int64_t> ghosts = std::move(scA.ghosts);
+    ghosts.insert(ghosts.end(), scB.ghosts.begin(), scB.ghosts.end());
+    std::sort(ghosts.begin(), ghosts.end());
+    ghosts.erase(std::unique(ghosts.begin(), ghosts.end()), ghosts.end());
     ctx->n_ghost = (int64_t)ghosts.size();
     if (ctx->n_loc + ctx->n_ghost >= (int64_t)1 << 31) {
         ctx->err = "local rows + ghosts exceed int32 column ids";
@@ -1014,24 +1181,19 @@ static trplk_status create_impl(trplk_ctx* ctx, int64_t n_global, const int64_t*
     ctx->nnzB = ctx->hasB ? b_rowptr[ctx->n_loc] - b_rowptr[0] : 0;
 
     // ||A||_F and max |A_jj| (local, then across ranks)
-    double fro2 = 0.0, amax = 0.0;
-    for (int64_t r = 0; r < ctx->n_loc; ++r)
-        for (int64_t p = a_rowptr[r] - a_rowptr[0]; p < a_rowptr[r + 1] - a_rowptr[0]; ++p) {
-            fro2 += a_val[p] * a_val[p];
-            if (a_col[p] == ctx->row_begin + r) amax = std::max(amax, std::fabs(a_val[p]));
-        }
+    double fro2 = scA.fro2, amax = scA.amax;
 
     // device format: DIA when the matrix is a few full diagonals (stencils), else SELL-32
     const bool force_sell = getenv("TRPLK_FORCE_SELL") != nullptr;
     bool diaA = false, diaB = false;
-    if (!force_sell) ST(try_dia(ctx, a_rowptr, a_col, a_val, ghosts, ctx->A, ctx->sellA_bytes, diaA));
+    if (!force_sell) ST(try_dia(ctx, a_rowptr, a_col, a_val, ghosts, scA, ctx->A, ctx->sellA_bytes, diaA));
     if (!diaA) {
         HostSell hs;
         ST(build_sell(ctx, a_rowptr, a_col, a_val, ghosts, hs));
         ST(upload_sell(ctx, hs, ctx->A, ctx->sellA_bytes));
     }
     if (ctx->hasB) {
-        if (!force_sell) ST(try_dia(ctx, b_rowptr, b_col, b_val, ghosts, ctx->B, ctx->sellB_bytes, diaB));
+        if (!force_sell) ST(try_dia(ctx, b_rowptr, b_col, b_val, ghosts, scB, ctx->B, ctx->sellB_bytes, diaB));
         if (!diaB) {
             HostSell hb;
             ST(build_sell(ctx, b_rowptr, b_col, b_val, ghosts, hb));
@@ -1039,6 +1201,7 @@ static trplk_status create_impl(trplk_ctx* ctx, int64_t n_global, const int64_t*
         }
     }
 
+    pt.mark("format");
     // fixed device buffers
     const size_t ld = (size_t)ctx->ld;
     ST(dalloc(ctx, &ctx->w, ld));
@@ -1060,8 +1223,13 @@ static trplk_status create_impl(trplk_ctx* ctx, int64_t n_global, const int64_t*
     CK(cudaMemsetAsync(ctx->T, 0, sizeof(double) * QMAX * QMAX, ctx->stream));
     for (double* v : {ctx->w, ctx->w1, ctx->w2, ctx->u, ctx->u2, ctx->xk})
         CK(cudaMemsetAsync(v, 0, ld * 8, ctx->stream));
-    CK(cudaMallocHost(&ctx->ctl_h, sizeof(Ctl)));
+    ctx->ctl_h = ctl_host_alloc();
+    if (!ctx->ctl_h) {
+        ctx->err = "cudaMallocHost (control block)";
+        return TRPLK_ENOMEM;
+    }
     memset(ctx->ctl_h, 0, sizeof(Ctl));
+    pt.mark("buffers");
 
     if (ctx->nranks > 1) {
         // global ||A||_F^2 and max |A_jj|
@@ -1147,7 +1315,10 @@ static trplk_status create_impl(trplk_ctx* ctx, int64_t n_global, const int64_t*
                 for (int64_t i = 0; i < they_need; ++i) loc[i] = (int)(ids[i] - ctx->row_begin);
                 int* d = nullptr;
                 ST(dalloc(ctx, &d, (size_t)std::max<int64_t>(they_need, 1)));
-                if (they_need) CK(cudaMemcpy(d, loc.data(), 4 * they_need, cudaMemcpyHostToDevice));
+                if (they_need) {
+                    CK(cudaMemcpyAsync(d, loc.data(), 4 * they_need, cudaMemcpyHostToDevice, ctx->stream));
+                    CK(cudaStreamSynchronize(ctx->stream));  // loc is a local
+                }
                 ctx->send_idx.push_back(d);
             }
             sendtot += they_need;
@@ -1158,6 +1329,7 @@ static trplk_status create_impl(trplk_ctx* ctx, int64_t n_global, const int64_t*
     ctx->amax = amax;
     ctx->mfloor = 1e-8 * amax;  // S:192 floor eps_d * max_j |A_jj| (R12)
     CK(cudaStreamSynchronize(ctx->stream));
+    pt.mark("halo+sync");
     return TRPLK_OK;
 }
 
@@ -1187,11 +1359,10 @@ void trplk_destroy(trplk_ctx* ctx) {
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     if (ctx->user_stream) cudaStreamSynchronize(ctx->user_stream);
     for (auto& g : ctx->graphs) cudaGraphExecDestroy(g.second.exec);
-    for (auto& a : ctx->allocs) {
-        if (ctx->has_alloc) ctx->alloc.free(a.first, ctx->alloc.user);
-        else cudaFree(a.first);
-    }
-    if (ctx->ctl_h) cudaFreeHost(ctx->ctl_h);
+    for (auto& a : ctx->allocs) dev_release(ctx, a.first);
+    if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    if (!ctx->has_alloc) trim_pool();
+    ctl_host_free(ctx->ctl_h);
     if (ctx->ev_in) cudaEventDestroy(ctx->ev_in);
     for (auto& e : ctx->pev)
         if (e) cudaEventDestroy(e);
@@ -1250,7 +1421,9 @@ static trplk_status solve_impl(trplk_ctx* ctx, int p, int q, int l, double tol, 
         return TRPLK_EINVAL;
     }
     const Sizes S{p, q, l, ph, m};
+    PhaseTimer pt("solve");
     ST(ensure_buffers(ctx, q, ph));
+    pt.mark("buffers");
     ctx->log.clear();
     ctx->log_ph = ph;
     ctx->a_mv = ctx->b_mv = ctx->prec = ctx->inner = ctx->verify = ctx->draws = 0;
@@ -1506,6 +1679,7 @@ static trplk_status solve_impl(trplk_ctx* ctx, int p, int q, int l, double tol, 
         if (stats) stats->cycles = cyc;
     }
 finish:
+    pt.mark("cycles");
     for (int i = 0; i < p; ++i) evals[i] = H.theta[i];
     if (evecs) {
         CK(cudaMemcpy2DAsync(evecs, 8 * ctx->n_loc, ctx->U[cur], 8 * ld, 8 * ctx->n_loc, p, cudaMemcpyDefault,
@@ -1513,6 +1687,7 @@ finish:
     }
     CK(cudaEventRecord(e1, ctx->stream));
     CK(cudaEventSynchronize(e1));
+    pt.mark("d2h");
     float ms = 0.f;
     CK(cudaEventElapsedTime(&ms, e0, e1));
     cudaEventDestroy(e0);

@@ -1486,6 +1486,36 @@ void launch_copy_cols(const double* src, int64_t lds, double* dst, int64_t ldd, 
     k_copy_cols<<<dim3((unsigned)g, (unsigned)ncols), 256, 0, s>>>(src, lds, dst, ldd, nrows, ncols);
 }
 
+struct DiaOffs {
+    int o[DIA_MAX];
+};
+
+// create-time CSR -> DIA scatter (rows of a local block; ci holds global column ids)
+__global__ void k_csr_to_dia(const int64_t* __restrict__ rp, const int64_t* __restrict__ ci,
+                             const double* __restrict__ va, int64_t nrows, int64_t row0, DiaOffs offs, int nd,
+                             int64_t ldv, double* __restrict__ dval) {
+    const int64_t base = rp[0];
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < nrows; r += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t p1 = rp[r + 1] - base;
+        for (int64_t p = rp[r] - base; p < p1; ++p) {
+            const int64_t off = ci[p] - (row0 + r);
+            int d = 0;
+            while (d < nd - 1 && offs.o[d] != off) ++d;
+            dval[(int64_t)d * ldv + r] = va[p];
+        }
+    }
+}
+
+void launch_csr_to_dia(const int64_t* rp, const int64_t* ci, const double* va, int64_t nrows, int64_t row0,
+                       const int* offs, int nd, int64_t ldv, double* dval, cudaStream_t s) {
+    DiaOffs o{};
+    for (int d = 0; d < nd && d < DIA_MAX; ++d) o.o[d] = offs[d];
+    int64_t g = (nrows + 255) / 256;
+    if (g > 148 * 16) g = 148 * 16;
+    if (g < 1) g = 1;
+    k_csr_to_dia<<<(int)g, 256, 0, s>>>(rp, ci, va, nrows, row0, o, nd, ldv, dval);
+}
+
 void launch_gather(const double* x, const int* idx, int64_t n, double* out, cudaStream_t s) {
     int64_t g = (n + 255) / 256;
     if (g > 1024) g = 1024;

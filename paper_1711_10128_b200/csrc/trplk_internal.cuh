@@ -176,6 +176,10 @@ void launch_finalize_upd_multi(const UpdArgs& up, const double* red_all, int nra
 void launch_gather(const double* x, const int* idx, int64_t n, double* out, cudaStream_t s);
 void launch_copy_cols(const double* src, int64_t lds, double* dst, int64_t ldd, int64_t nrows, int ncols,
                       cudaStream_t s);
+// CSR (device copies of the caller's pinned arrays) -> DIA values, one thread per row; dval
+// must be zeroed.  offs: the nd sorted diagonal offsets.
+void launch_csr_to_dia(const int64_t* rp, const int64_t* ci, const double* va, int64_t nrows, int64_t row0,
+                       const int* offs, int nd, int64_t ldv, double* dval, cudaStream_t s);
 int kmax_bucket(int k);
 
 }  // namespace trplk

@@ -224,3 +224,37 @@ def test_widest_basis(orc, gen, q):
     assert g["stats"]["a_matvecs"] == o["a_matvecs"]
     assert np.max(np.abs(g["eigenvalues"] - o["eigenvalues"]) / np.abs(o["eigenvalues"])) <= 1e-9
     assert np.all(g["residuals"] <= P.tol)
+
+
+class _Csr:
+    def __init__(self, rowptr, col, val, n):
+        self.rowptr, self.col, self.val, self.n, self.row_begin = rowptr, col, val, n, 0
+
+
+@pytest.mark.parametrize("name,N,torch_alloc", [("C2", 16, True), ("C4", 10, True), ("C2", 16, False)])
+def test_pinned_host_csr(gen, name, N, torch_alloc):
+    """Pinned host CSR arrays take the device-side CSR -> DIA scatter (k_csr_to_dia), pageable
+    ones the host scatter: the same device matrix, so the same solve bit for bit.  With
+    torch_alloc=False the library's own stream-ordered memory pool serves every buffer."""
+    torch, trplk = need_gpu()
+    P = gen.make(name, N=N)
+
+    def pinned(M):
+        if M is None:
+            return None
+        t = [torch.from_numpy(a).pin_memory() for a in (M.rowptr, M.col, M.val)]
+        return _Csr(*(x.numpy() for x in t), M.n), t
+
+    pa = pinned(P.A)
+    pb = pinned(P.B)
+    out = []
+    for A, B in ((P.A, P.B), (pa[0], None if pb is None else pb[0])):
+        ctx = trplk.trplk_create(A, B, P.sigma, torch_alloc=torch_alloc)
+        info = trplk.trplk_info(ctx)
+        ev, X, rs, st = trplk.trplk_solve(ctx, P.p, P.q, P.l, P.tol)
+        out.append((ev, X.cpu().numpy().copy(), st["a_matvecs"], info))
+        ctx.close()
+    assert out[0][3] == out[1][3]
+    assert out[0][2] == out[1][2]
+    assert np.array_equal(out[0][0], out[1][0])
+    assert np.array_equal(out[0][1], out[1][1])
