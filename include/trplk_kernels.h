@@ -70,7 +70,11 @@ trplk_status trplk_plan_ghosts(int64_t row_begin, int64_t row_end, const int64_t
 /* Debug switches of the context (tests of rare paths).  Bit 0: take the third CGS pass
  * (reading R3) in every CGS2 even when the second pass kept more than 1/sqrt2 of the norm -- the
  * same arithmetic as a genuine third pass, so its kernels can be checked against the oracle.
- * trplk_options.debug_checks bit 1 does the same for one solve.  Errors: EINVAL (ctx NULL). */
+ * trplk_options.debug_checks bit 1 does the same for one solve.  Bit 1: run the m inner steps
+ * of every cycle as ONE cooperative grid-wide kernel (inner_grid.cuh; one CTA per SM, grid
+ * barriers and all-reduces instead of kernel boundaries) where it applies -- one rank, B = I,
+ * max_basis <= 32, n above the single-CTA small path; also enabled by the environment variable
+ * TRPLK_GRID=1.  Same readings (R1, R3, R16) as the multi-kernel step.  Errors: EINVAL (ctx NULL). */
 trplk_status trplk_set_debug(trplk_ctx* ctx, int flags);
 
 /* In-process loopback hub for nranks ranks (test infrastructure): pass it as

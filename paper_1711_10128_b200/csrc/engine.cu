@@ -72,12 +72,15 @@ struct trplk_ctx {
     double* sendbuf = nullptr;
     Comm* cm = nullptr;    // rank exchanges (NCCL, or the in-process loopback hub)
     int force3 = 0;        // debug: force the third CGS pass (trplk_set_debug / options.debug_checks & 2)
+    int grid_on = -1;      // grid-wide inner loop: -1 = TRPLK_GRID env, else trplk_set_debug bit 1
     bool loopback = false;  // loopback ranks: eager launches (exchanges are host rendezvous)
     // solve buffers
     int q_alloc = 0, ph_alloc = 0;
     double* U[2] = {nullptr, nullptr};
     double *w = nullptr, *w1 = nullptr, *w2 = nullptr, *u = nullptr, *u2 = nullptr, *xk = nullptr;
     double *T = nullptr, *Yg = nullptr, *part = nullptr, *gpart = nullptr, *red_local = nullptr, *red_all = nullptr;
+    double* gridpart = nullptr;
+    unsigned long long* gtrace = nullptr;  // TRPLK_GRID_TRACE: per-step phase timestamps  // all-reduce partials of the grid-wide inner loop (2 x GRID_MAXCTA x GRID_NVP)
     double* Wtmp = nullptr;
     unsigned* counter = nullptr;
     Ctl* ctl = nullptr;
@@ -667,6 +670,20 @@ bool small_path(const trplk_ctx* ctx, const Sizes& S) {
     return v == 1 && ctx->nranks == 1 && !ctx->hasB && ctx->n_loc <= SMALL_NMAX && S.q <= 24;
 }
 
+// Mid-size latency path: one cooperative grid-wide kernel runs all m steps (inner_grid.cuh) for
+// one rank, B = I, q <= 32 and n above the single-CTA range.  Opt-in (TRPLK_GRID=1 or
+// trplk_set_debug bit 1): at C2 it measured 40 us per inner step against ~37 us for the
+// multi-kernel step, whose launches overlap in the graph (profiles/r01_variants.md).
+bool grid_path(const trplk_ctx* ctx, const Sizes& S) {
+    static int env = -1;
+    if (env < 0) {
+        const char* e = getenv("TRPLK_GRID");
+        env = (e && e[0] == '1') ? 1 : 0;
+    }
+    const bool on = ctx->grid_on < 0 ? env == 1 : ctx->grid_on == 1;
+    return on && !small_path(ctx, S) && ctx->nranks == 1 && !ctx->hasB && S.q <= 32 && ctx->gridpart != nullptr;
+}
+
 // One rank and B = I: the FINAL kernel is launched cooperatively and runs a third pass itself
 // (grid barrier), so the two gated pass-3 launches (~2.5 us each, normally no-ops) disappear
 // from every CGS2.  TRPLK_NO_COOP3=1 keeps the gated launches.
@@ -903,7 +920,8 @@ trplk_status issue_cycle(trplk_ctx* ctx, const Sizes& S, int cur, int nprev, int
     }
     // inner steps, eq 3.1
     const int jmid = std::max(1, std::min(S.m - 1, S.m / 2));
-    if (small_path(ctx, S)) {  // one CTA runs all m steps (latency path, small.cuh)
+    const bool fused = small_path(ctx, S) || grid_path(ctx, S);
+    if (fused) {  // one kernel runs all m steps (latency paths, small.cuh / inner_grid.cuh)
         SmallArgs sa{};
         sa.A = ctx->A;
         sa.nrows = ctx->n_loc;
@@ -922,7 +940,20 @@ trplk_status issue_cycle(trplk_ctx* ctx, const Sizes& S, int cur, int nprev, int
         sa.clear = F_INNER;
         sa.force3 = ctx->force3;
         if (ctx->prof_on) CK(cudaEventRecordWithFlags(ctx->pev[0], ctx->stream, cudaEventRecordExternal));
-        launch_inner_small(sa, S.q, ctx->stream);
+        if (small_path(ctx, S)) {
+            launch_inner_small(sa, S.q, ctx->stream);
+        } else {
+            GridArgs ga{sa, ctx->gridpart, nullptr};
+            static const bool trace = getenv("TRPLK_GRID_TRACE") != nullptr;
+            if (trace) {
+                if (!ctx->gtrace) ST(dalloc(ctx, &ctx->gtrace, 8 * 64));
+                ga.trace = ctx->gtrace;
+            }
+            if (!launch_inner_grid(ga, S.q, ctx->stream)) {
+                ctx->err = "cooperative launch of the grid-wide inner loop failed";
+                return TRPLK_ECUDA;
+            }
+        }
         CK(cudaGetLastError());
         if (ctx->prof_on)
             for (int e = 1; e < 4; ++e) CK(cudaEventRecordWithFlags(ctx->pev[e], ctx->stream, cudaEventRecordExternal));
@@ -933,7 +964,7 @@ trplk_status issue_cycle(trplk_ctx* ctx, const Sizes& S, int cur, int nprev, int
             if (j < S.m) ctx->model_bytes += 2 * vec_bytes(ctx) * (k + 2);
         }
     }
-    for (int j = 1; j <= S.m && !small_path(ctx, S); ++j) {
+    for (int j = 1; j <= S.m && !fused; ++j) {
         const int k = S.ph + j;  // nominal width incl. g_j
         const bool prof = ctx->prof_on && j == jmid && j < S.m;
         const double* g = Uc + ld * (k - 1);
@@ -1217,6 +1248,7 @@ static trplk_status create_impl(trplk_ctx* ctx, int64_t n_global, const int64_t*
     ST(dalloc(ctx, &ctx->red_local, (size_t)NV_MAX));
     ST(dalloc(ctx, &ctx->red_all, (size_t)NV_MAX * ctx->nranks));
     ST(dalloc(ctx, &ctx->counter, NCOUNTERS));
+    if (ctx->nranks == 1 && !ctx->hasB) ST(dalloc(ctx, &ctx->gridpart, (size_t)2 * GRID_MAXCTA * GRID_NVP));
     ST(dalloc(ctx, &ctx->ctl, 1));
     CK(cudaMemsetAsync(ctx->counter, 0, sizeof(unsigned) * NCOUNTERS, ctx->stream));
     CK(cudaMemsetAsync(ctx->ctl, 0, sizeof(Ctl), ctx->stream));
@@ -1582,7 +1614,7 @@ static trplk_status solve_impl(trplk_ctx* ctx, int p, int q, int l, double tol, 
                     CK(cudaEventElapsedTime(&e[0], ctx->pev[0], ctx->pev[1]));
                     CK(cudaEventElapsedTime(&e[1], ctx->pev[1], ctx->pev[2]));
                     CK(cudaEventElapsedTime(&e[2], ctx->pev[2], ctx->pev[3]));
-                    if (small_path(ctx, S)) e[0] /= (float)std::max(G, 1);  // one kernel for all steps
+                    const bool fused = small_path(ctx, S) || grid_path(ctx, S);
                     const double n = (double)ctx->n_loc, k = (double)(ph + jmid);
                     // matrix bytes of the device format (DIA: 8 ndiag n; SELL: 12 per slot + slice ptrs)
                     const double spA = (double)ctx->sellA_bytes, spB = (double)ctx->sellB_bytes;
@@ -1595,7 +1627,18 @@ static trplk_status solve_impl(trplk_ctx* ctx, int p, int q, int l, double tol, 
                         b2 = 8.0 * n * (k + 2);        // U, w, w'
                     }
                     const double b3 = 8.0 * n * (k + 2);  // U, w', g_{j+1}
-                    const double bb[3] = {b1, b2, b3};
+                    double bb[3] = {b1, b2, b3};
+                    if (fused) {  // one launch for all G steps: its time, the bytes of all G steps
+                        double tot = 0.0;
+                        for (int j = 1; j <= G; ++j) {
+                            const double kj = (double)(ph + j);
+                            tot += (double)ctx->sellA_bytes + 8.0 * n * (kj + 2);
+                            if (j < m) tot += 2 * 8.0 * n * (kj + 2);
+                        }
+                        bb[0] = tot;
+                        bb[1] = bb[2] = 0.0;
+                        e[1] = e[2] = 0.0f;
+                    }
                     for (int i = 0; i < 3; ++i) {
                         ctx->prof_ms[i] += e[i];
                         ctx->prof_bytes[i] += bb[i];
@@ -1680,6 +1723,17 @@ static trplk_status solve_impl(trplk_ctx* ctx, int p, int q, int l, double tol, 
     }
 finish:
     pt.mark("cycles");
+    if (ctx->gtrace) {  // TRPLK_GRID_TRACE: phase durations (us) of the last grid-path cycle, per step
+        unsigned long long tr[64];
+        cudaStreamSynchronize(ctx->stream);
+        cudaMemcpy(tr, ctx->gtrace, sizeof(tr), cudaMemcpyDeviceToHost);
+        for (int j = 0; j < 8 && tr[j * 8 + 6] > tr[j * 8]; ++j)
+            fprintf(stderr, "[grid step %d] p1 %.2f red %.2f p2 %.2f red %.2f fin %.2f sync %.2f total %.2f\n", j + 1,
+                    (tr[j * 8 + 1] - tr[j * 8]) * 1e-3, (tr[j * 8 + 2] - tr[j * 8 + 1]) * 1e-3,
+                    (tr[j * 8 + 3] - tr[j * 8 + 2]) * 1e-3, (tr[j * 8 + 4] - tr[j * 8 + 3]) * 1e-3,
+                    (tr[j * 8 + 5] - tr[j * 8 + 4]) * 1e-3, (tr[j * 8 + 6] - tr[j * 8 + 5]) * 1e-3,
+                    (tr[j * 8 + 6] - tr[j * 8]) * 1e-3);
+    }
     for (int i = 0; i < p; ++i) evals[i] = H.theta[i];
     if (evecs) {
         CK(cudaMemcpy2DAsync(evecs, 8 * ctx->n_loc, ctx->U[cur], 8 * ld, 8 * ctx->n_loc, p, cudaMemcpyDefault,
@@ -1724,6 +1778,12 @@ trplk_status trplk_solve(trplk_ctx* ctx, int p, int max_basis, int k_plus, doubl
 trplk_status trplk_set_debug(trplk_ctx* ctx, int flags) {
     if (!ctx) return TRPLK_EINVAL;
     set_force3(ctx, flags & 1);
+    const int g = (flags & 2) ? 1 : -1;
+    if (g != ctx->grid_on) {  // the captured cycle graphs hold the other inner-loop kernels
+        ctx->grid_on = g;
+        for (auto& e : ctx->graphs) cudaGraphExecDestroy(e.second.exec);
+        ctx->graphs.clear();
+    }
     return TRPLK_OK;
 }
 

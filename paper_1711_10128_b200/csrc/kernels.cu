@@ -56,6 +56,9 @@ __device__ __forceinline__ void warp_butterfly(double (&v)[1 << LOG], int lane) 
 // DIA: every load address is computed, so all values and gathers of a chunk of 8 diagonals
 // are in flight at once (one memory round trip); the sum runs in ascending column order.
 // SELL: column ids are loaded first (two round trips per chunk of 8 entries).
+// XNC = false: x is gathered with ld.global.cg (L2) instead of the read-only path -- for
+// kernels that read x after other CTAs wrote it inside the same launch (inner_grid.cuh).
+template <bool XNC = true>
 __device__ __forceinline__ double mat_row(const Sell& M, int64_t s, int lane, const double* __restrict__ x,
                                           double& diag) {
     double acc = 0.0;
@@ -77,7 +80,7 @@ __device__ __forceinline__ double mat_row(const Sell& M, int64_t s, int lane, co
                     if (halo) idx = idx < 0 ? idx + nl + glo : (idx >= nl ? idx + glo : idx);
                     idx = idx < 0 ? 0 : (idx > top ? top : idx);  // out-of-matrix slots hold 0
                     v[u] = __ldg(dv + (int64_t)d * M.ldv);
-                    xv[u] = __ldg(x + idx);
+                    xv[u] = XNC ? __ldg(x + idx) : __ldcg(x + idx);
                 }
             }
 #pragma unroll
@@ -101,7 +104,7 @@ __device__ __forceinline__ double mat_row(const Sell& M, int64_t s, int lane, co
         }
         double xv[8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) xv[u] = (j0 + u < w) ? __ldg(x + c[u]) : 0.0;
+        for (int u = 0; u < 8; ++u) xv[u] = (j0 + u < w) ? (XNC ? __ldg(x + c[u]) : __ldcg(x + c[u])) : 0.0;
 #pragma unroll
         for (int u = 0; u < 8; ++u) acc = fma(v[u], xv[u], acc);
     }
@@ -1197,6 +1200,7 @@ __global__ void k_gather(const double* x, const int* idx, int64_t n, double* out
 #include "rotate.cuh"      // shared-memory-staged DMMA rotation (default)
 #include "k1_pipe.cuh"     // software-pipelined K1 (DIA, B = I, k <= 24)
 #include "small.cuh"       // single-CTA inner loop for small n (latency path)
+#include "inner_grid.cuh"  // cooperative grid-wide inner loop for mid-size n (latency path)
 
 namespace trplk {
 

@@ -578,6 +578,12 @@ static int rs_grid(K kern, int smem, int64_t nrows) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, CTA, smem);
     if (occ < 1) occ = 1;
     const int64_t need = ((nrows + 31) / 32 + WARPS - 1) / WARPS;
+    static const int spw = getenv("TRPLK_RS_SPW") ? atoi(getenv("TRPLK_RS_SPW")) : 0;  // experiment knob
+    if (spw > 0) {
+        int64_t g = (need + spw - 1) / spw;
+        if (g > MAXCTA) g = MAXCTA;
+        return (int)(g < 1 ? 1 : g);
+    }
     int64_t cap = (int64_t)nsm_s() * occ;
     if (cap > MAXCTA) cap = MAXCTA;
     if (need <= cap) return (int)(need < 1 ? 1 : need);

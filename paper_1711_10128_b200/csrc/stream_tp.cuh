@@ -268,6 +268,12 @@ static int tp_grid(K kern, int64_t nrows, int tr) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, CTA, 0);
     if (occ < 1) occ = 1;
     const int64_t need = ((nrows + tr - 1) / tr + WARPS - 1) / WARPS;
+    static const int spw = getenv("TRPLK_TP_SPW") ? atoi(getenv("TRPLK_TP_SPW")) : 0;  // experiment knob
+    if (spw > 0) {
+        int64_t g = (need + spw - 1) / spw;
+        if (g > MAXCTA) g = MAXCTA;
+        return (int)(g < 1 ? 1 : g);
+    }
     int64_t cap = (int64_t)nsm * occ;
     if (cap > MAXCTA) cap = MAXCTA;
     if (need <= cap) return (int)(need < 1 ? 1 : need);

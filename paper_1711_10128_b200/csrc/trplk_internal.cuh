@@ -158,8 +158,19 @@ struct SmallArgs {
 };
 
 
+// Grid-wide persistent inner loop (inner_grid.cuh): SmallArgs plus the all-reduce buffer.
+constexpr int GRID_NVP = 72;       // stride of one CTA's partial sums
+constexpr int GRID_MAXCTA = 1024;  // partial buffer: 2 x GRID_MAXCTA x GRID_NVP doubles
+struct GridArgs {
+    SmallArgs s;
+    double* part;
+    unsigned long long* trace;  // optional (TRPLK_GRID_TRACE): phase timestamps of CTA 0, per step
+};
+
 // Kernel launchers (kernels.cu)
 bool launch_inner_small(const SmallArgs& a, int kmax, cudaStream_t s);
+// false: not applicable (kmax > 32 or no co-resident grid); nothing launched
+bool launch_inner_grid(const GridArgs& a, int kmax, cudaStream_t s);
 void launch_sdots(const SdotsArgs& a, int kmax, cudaStream_t s);
 void launch_upd(const UpdArgs& a, int kmax, cudaStream_t s);
 void launch_eig(Ctl* ctl, double* T, int ldT, double* Y, int ldY, int ph, int k_fixed, unsigned gate,

@@ -199,7 +199,7 @@ def trplk_loopback_destroy(hub):
 
 
 def trplk_set_debug(ctx, flags: int):
-    """Debug switches (bit 0: force the third CGS pass)."""
+    """Debug switches (bit 0: force the third CGS pass; bit 1: grid-wide cooperative inner loop)."""
     ctx.check(_lib.trplk_set_debug(ctx.handle, int(flags)))
 
 
