@@ -58,6 +58,23 @@ class _Report(ctypes.Structure):
                 ("dump_rho", _P), ("dump_t", _P)]
 
 
+class _Pl1Problem(ctypes.Structure):
+    _fields_ = [("n", _I64), ("a_rowptr", _P), ("a_col", _P), ("a_val", _P),
+                ("b_rowptr", _P), ("b_col", _P), ("b_val", _P), ("sigma", ctypes.c_double),
+                ("use_precond", ctypes.c_int), ("m", ctypes.c_int), ("tol", ctypes.c_double),
+                ("seed", ctypes.c_uint64), ("x0", _P), ("max_cycles", ctypes.c_int),
+                ("variant", ctypes.c_int)]
+
+
+class _Pl1Report(ctypes.Structure):
+    _fields_ = [("status", ctypes.c_int), ("cycles", ctypes.c_int),
+                ("a_matvecs", _I64), ("b_matvecs", _I64),
+                ("rho", ctypes.c_double), ("resid", ctypes.c_double),
+                ("log_cap", ctypes.c_int), ("log_len", ctypes.c_int),
+                ("log_rho", _P), ("log_res", _P), ("log_conj", _P), ("log_ritz", _P),
+                ("log_mg", _P), ("log_nq", _P)]
+
+
 _lib = None
 
 
@@ -85,6 +102,8 @@ def lib():
         L.orc_rotate.argtypes = [_I64, ctypes.c_int, _P, _P, ctypes.c_int, ctypes.c_int, _P]
         L.orc_trplk_solve.restype = ctypes.c_int
         L.orc_trplk_solve.argtypes = [ctypes.POINTER(_Problem), _P, _P, _P, ctypes.POINTER(_Report)]
+        L.orc_pl1_solve.restype = ctypes.c_int
+        L.orc_pl1_solve.argtypes = [ctypes.POINTER(_Pl1Problem), _P, ctypes.POINTER(_Pl1Report)]
         _lib = L
     return _lib
 
@@ -224,3 +243,26 @@ def solve(A, B=None, p=5, q=20, l=1, tol=1e-8, sigma=0.0, seed=12, max_cycles=50
         out["dump"] = {"X": [dX[i].T.copy() for i in range(nd)], "rho": drho[:nd].copy(),
                        "t": dt[:nd].copy()}
     return out
+
+
+def pl1_solve(A, B=None, m=4, tol=1e-8, sigma=0.0, seed=12, x0=None, max_cycles=2000, variant=0,
+              use_precond=True):
+    """Run Algorithm 2 (PL+1) for the lowest eigenpair of (A, B), readings P1-P6.  Returns a dict
+    with rho, x (B-normalised), residual norm, counters and the per-iteration log."""
+    ra, ca, va = _csr(A)
+    rb, cb, vb = _csr(B)
+    n = len(ra) - 1
+    x0a = None if x0 is None else np.ascontiguousarray(x0, np.float64)
+    prob = _Pl1Problem(n, _ptr(ra), _ptr(ca), _ptr(va), _ptr(rb), _ptr(cb), _ptr(vb), sigma,
+                       1 if use_precond else 0, m, tol, seed, _ptr(x0a), max_cycles, variant)
+    cap = max_cycles + 1
+    logs = {"rho": np.zeros(cap), "res": np.zeros(cap), "conj": np.zeros(cap), "ritz": np.zeros(cap),
+            "mg": np.zeros(cap, np.int32), "nq": np.zeros(cap, np.int32)}
+    rep = _Pl1Report(0, 0, 0, 0, 0.0, 0.0, cap, 0, _ptr(logs["rho"]), _ptr(logs["res"]),
+                     _ptr(logs["conj"]), _ptr(logs["ritz"]), _ptr(logs["mg"]), _ptr(logs["nq"]))
+    x = np.zeros(n)
+    st = lib().orc_pl1_solve(ctypes.byref(prob), _ptr(x), ctypes.byref(rep))
+    L = rep.log_len
+    return {"status": STATUS.get(st, st), "rho": rep.rho, "x": x, "residual": rep.resid,
+            "cycles": rep.cycles, "a_matvecs": rep.a_matvecs, "b_matvecs": rep.b_matvecs,
+            "log": {k_: v[:L].copy() for k_, v in logs.items()}}

@@ -494,3 +494,231 @@ done:
     free(s); free(r); free(u); free(T); free(Tk); free(Y); free(th);
     return status;
 }
+
+/* =====================================================================================
+ * PL+1, Algorithm 2 (alg:pl+1) -- NEXT-1 of SURVEY 8(f).
+ * Readings:
+ *  P1 step 4: G_k = B-orthonormal basis of span{M(A-rho_k B)x_k, ..., [M(A-rho_k B)]^m x_k}
+ *     built as v_1 = M r_k, v_{j+1} = M(A - rho_k B) g_j, each v CGS2-orthogonalised (B-inner
+ *     product, R3) against g_1..g_{j-1} only (x_k and p_{k-1} are not projected out: step 5
+ *     solves the pencil (Q^T A Q, Q^T B Q)); a breakdown (R16 threshold) ends G_k early.
+ *  P2 step 5: lowest eigenpair of the projected pencil by Cholesky reduction S = L L^T,
+ *     C = L^-1 H L^-T and the Jacobi eig; w = L^-T y_1 (w^T S w = 1), sign fixed
+ *     so that w(1) >= 0 (the coefficient of x_k).
+ *  P3 a Cholesky pivot d_j <= 1e-24 S_jj (component of the column outside the span of the
+ *     previous ones below 1e-12 relative) drops p_{k-1} from Q_k (SPEC "columns dropped");
+ *     if the failing column is not p_{k-1}: BREAKDOWN.
+ *  P4 step 7: rho_{k-1} = rho(x_{k-1}), the Rayleigh quotient of the previous iterate (the
+ *     shift of iteration k-1; Lemma 8's proof uses p_{k-1}^T(A - rho(x_{k-1})B)p_k = 0);
+ *     |p_{k-1}^T(A - rho_{k-1}B)p_{k-1}| <= 1e-14 ||A||_F -> coefficient 0 (SPEC fallback).
+ *  P5 step 6: rho_{k+1} and r_{k+1} from explicit products A x_{k+1}, B x_{k+1}; A p_{k-1} by an
+ *     explicit product when Q_k is formed.  A-matvecs: 1 (x_0) + per iteration m (A g_j) +
+ *     1 (A x_{k+1}) + [k > 0] (A p_{k-1}).
+ *  P6 x_0(i) = u01(seed, 3, i) (R13 generator, stream 3), then B-normalised (step 2).
+ * ===================================================================================== */
+
+/* S = L L^T in place (lower triangle of L, column-major nq x nq); returns the index of the
+ * first pivot that fails the P3 test, or -1. */
+static int pl1_chol(int nq, const double* S, double* L) {
+    for (int i = 0; i < nq * nq; ++i) L[i] = 0.0;
+    for (int j = 0; j < nq; ++j) {
+        double d = S[j + nq * j];
+        for (int k = 0; k < j; ++k) d -= L[j + nq * k] * L[j + nq * k];
+        if (!(d > 1e-24 * S[j + nq * j])) return j;
+        const double ljj = sqrt(d);
+        L[j + nq * j] = ljj;
+        for (int i = j + 1; i < nq; ++i) {
+            double s = S[i + nq * j];
+            for (int k = 0; k < j; ++k) s -= L[i + nq * k] * L[j + nq * k];
+            L[i + nq * j] = s / ljj;
+        }
+    }
+    return -1;
+}
+
+int orc_pl1_solve(const orc_pl1_problem* P, double* x_out, orc_pl1_report* rep) {
+    const int64_t n = P->n;
+    const int m = P->m;
+    if (rep) { rep->status = 1; rep->cycles = 0; rep->log_len = 0; rep->a_matvecs = rep->b_matvecs = 0; }
+    if (n < 2 || m < 1 || m > 32 || !(P->tol > 0.0) || P->max_cycles < 1) return 1;
+    orc_problem Q;
+    memset(&Q, 0, sizeof(Q));
+    Q.n = n;
+    Q.a_rowptr = P->a_rowptr; Q.a_col = P->a_col; Q.a_val = P->a_val;
+    Q.b_rowptr = P->b_rowptr; Q.b_col = P->b_col; Q.b_val = P->b_val;
+    Q.seed = P->seed;
+    ctx_t c = {&Q, n, 0, 0, 0};
+    const size_t nb = (size_t)n * sizeof(double);
+    double* M = (double*)malloc(nb);
+    if (P->use_precond)
+        orc_jacobi_diag(n, P->a_rowptr, P->a_col, P->a_val, P->b_rowptr, P->b_col, P->b_val, P->sigma, 1e-8, M);
+    else
+        for (int64_t i = 0; i < n; ++i) M[i] = 1.0;
+    const double normF = orc_frobenius(P->a_rowptr[n] - P->a_rowptr[0], P->a_val + 0);
+    double *x = malloc(nb), *Ax = malloc(nb), *Bx = malloc(nb), *r = malloc(nb);
+    double *p = malloc(nb), *Ap = malloc(nb), *Bp = malloc(nb);
+    double *v = malloc(nb), *tmp = malloc(nb), *g = malloc(nb), *xt = malloc(nb), *d = malloc(nb);
+    double *G = malloc(nb * m), *AG = malloc(nb * m), *BG = malloc(nb * m);
+    const int qmax = m + 2;
+    double H[34 * 34], S[34 * 34], L[34 * 34], C[34 * 34], Y[34 * 34], th[34], w[34];
+    const double* Qc[34];
+    const double* AQc[34];
+    const double* BQc[34];
+    int status = 2, has_p = 0, k = 0;
+    double beta;
+
+    /* step 2: x_0 with ||x_0||_B = 1, rho_0, r_0 */
+    for (int64_t i = 0; i < n; ++i) x[i] = P->x0 ? P->x0[i] : orc_u01(P->seed, 3, (uint64_t)i);
+    applyB(&c, x, Bx);
+    double nx = sqrt(orc_dot(n, x, Bx));
+    for (int64_t i = 0; i < n; ++i) x[i] /= nx;
+    applyA(&c, x, Ax);
+    applyB(&c, x, Bx);
+    double rho = orc_dot(n, x, Ax) / orc_dot(n, x, Bx);
+    for (int64_t i = 0; i < n; ++i) r[i] = Ax[i] - rho * Bx[i];
+    double res = sqrt(orc_dot(n, r, r));
+    double rho_prev = rho;  /* rho(x_{k-1}) for step 7 (P4) */
+    double conj_next = 0.0;
+
+    for (k = 0;; ++k) {
+        if (rep && k < rep->log_cap) {
+            rep->log_rho[k] = rho;
+            rep->log_res[k] = res;
+            rep->log_conj[k] = conj_next;
+            rep->log_ritz[k] = 0.0;
+            rep->log_mg[k] = 0;
+            rep->log_nq[k] = 0;
+            rep->log_len = k + 1;
+        }
+        if (res <= P->tol) { status = 0; break; }  /* step 3 */
+        if (k >= P->max_cycles) { status = 2; break; }
+        /* step 4 (P1): G_k */
+        int mg = 0;
+        for (int j = 0; j < m; ++j) {
+            if (j == 0)
+                for (int64_t i = 0; i < n; ++i) v[i] = M[i] * r[i];  /* M (A - rho_k B) x_k */
+            else
+                for (int64_t i = 0; i < n; ++i)
+                    v[i] = M[i] * (AG[i + (size_t)n * (j - 1)] - rho * BG[i + (size_t)n * (j - 1)]);
+            if (cgs2_ctx(&c, mg, G, v, tmp, NULL, &beta, NULL)) break;  /* breakdown: G_k ends */
+            double* gj = G + (size_t)n * mg;
+            for (int64_t i = 0; i < n; ++i) gj[i] = v[i] / beta;
+            applyA(&c, gj, AG + (size_t)n * mg);
+            applyB(&c, gj, BG + (size_t)n * mg);
+            ++mg;
+        }
+        /* step 5: Q_k = [x_k, G_k, p_{k-1}], RR on the projected pencil (P2, P3) */
+        int nq = 1 + mg;
+        Qc[0] = x; AQc[0] = Ax; BQc[0] = Bx;
+        for (int j = 0; j < mg; ++j) {
+            Qc[1 + j] = G + (size_t)n * j;
+            AQc[1 + j] = AG + (size_t)n * j;
+            BQc[1 + j] = BG + (size_t)n * j;
+        }
+        if (has_p) {
+            applyA(&c, p, Ap);
+            applyB(&c, p, Bp);
+            Qc[nq] = p; AQc[nq] = Ap; BQc[nq] = Bp;
+            ++nq;
+        }
+        int use_p = has_p, fail;
+        for (;;) {
+            for (int i = 0; i < nq; ++i)
+                for (int jj = 0; jj < nq; ++jj) {
+                    H[i + nq * jj] = orc_dot(n, Qc[i], AQc[jj]);
+                    S[i + nq * jj] = orc_dot(n, Qc[i], BQc[jj]);
+                }
+            for (int i = 0; i < nq; ++i)
+                for (int jj = 0; jj < i; ++jj) {
+                    const double h = 0.5 * (H[i + nq * jj] + H[jj + nq * i]);
+                    const double s = 0.5 * (S[i + nq * jj] + S[jj + nq * i]);
+                    H[i + nq * jj] = H[jj + nq * i] = h;
+                    S[i + nq * jj] = S[jj + nq * i] = s;
+                }
+            fail = pl1_chol(nq, S, L);
+            if (fail < 0) break;
+            if (use_p && fail == nq - 1) { use_p = 0; --nq; continue; }  /* P3: drop p_{k-1} */
+            break;
+        }
+        if (fail >= 0) { status = 3; break; }
+        /* C = L^-1 H L^-T: forward substitution on the columns, then on the rows */
+        for (int jj = 0; jj < nq; ++jj)
+            for (int i = 0; i < nq; ++i) {
+                double s = H[i + nq * jj];
+                for (int t = 0; t < i; ++t) s -= L[i + nq * t] * C[t + nq * jj];
+                C[i + nq * jj] = s / L[i + nq * i];
+            }  /* C = L^-1 H */
+        for (int i = 0; i < nq; ++i)
+            for (int jj = 0; jj < nq; ++jj) {
+                double s = C[i + nq * jj];
+                for (int t = 0; t < jj; ++t) s -= L[jj + nq * t] * Y[i + nq * t];
+                Y[i + nq * jj] = s / L[jj + nq * jj];
+            }  /* Y = (L^-1 H) L^-T */
+        memcpy(C, Y, sizeof(double) * nq * nq);
+        if (orc_sym_eig(nq, C, th, Y) < 0) { status = 3; break; }
+        for (int i = nq - 1; i >= 0; --i) {  /* w = L^-T y_1 */
+            double s = Y[i];
+            for (int t = i + 1; t < nq; ++t) s -= L[t + nq * i] * w[t];
+            w[i] = s / L[i + nq * i];
+        }
+        if (w[0] < 0.0)
+            for (int i = 0; i < nq; ++i) w[i] = -w[i];
+        if (rep && k < rep->log_cap) {
+            rep->log_ritz[k] = th[0];
+            rep->log_mg[k] = mg;
+            rep->log_nq[k] = nq;
+        }
+        /* step 6: g_k, x~_{k+1}, x_{k+1}, rho_{k+1}, r_{k+1} (P5) */
+        for (int64_t i = 0; i < n; ++i) {
+            double s = 0.0;
+            for (int j = 0; j < mg; ++j) s += w[1 + j] * G[i + (size_t)n * j];
+            g[i] = s;
+            xt[i] = w[0] * x[i] + s + (use_p ? w[nq - 1] * p[i] : 0.0);
+        }
+        applyB(&c, xt, tmp);
+        const double nxt = sqrt(orc_dot(n, xt, tmp));
+        const double rho_k = rho;
+        for (int64_t i = 0; i < n; ++i) x[i] = xt[i] / nxt;
+        applyA(&c, x, Ax);
+        applyB(&c, x, Bx);
+        rho = orc_dot(n, x, Ax) / orc_dot(n, x, Bx);
+        for (int64_t i = 0; i < n; ++i) r[i] = Ax[i] - rho * Bx[i];
+        res = sqrt(orc_dot(n, r, r));
+        /* step 7 (P4): p~_k and p_k */
+        conj_next = 0.0;
+        if (!has_p) {
+            memcpy(v, g, nb);
+        } else if (P->variant == 1) {
+            const double wp = use_p ? w[nq - 1] : 0.0;
+            for (int64_t i = 0; i < n; ++i) v[i] = g[i] + wp * p[i];
+        } else {
+            for (int64_t i = 0; i < n; ++i) d[i] = Ap[i] - rho_prev * Bp[i];  /* (A - rho_{k-1} B) p_{k-1} */
+            const double num = orc_dot(n, d, g), den = orc_dot(n, d, p);
+            const double coef = fabs(den) <= 1e-14 * normF ? 0.0 : num / den;
+            for (int64_t i = 0; i < n; ++i) v[i] = g[i] - coef * p[i];
+        }
+        applyB(&c, v, tmp);
+        const double np_ = sqrt(orc_dot(n, v, tmp));
+        if (np_ > 0.0) {
+            if (has_p && P->variant == 0) conj_next = orc_dot(n, d, v) / np_ / normF;
+            for (int64_t i = 0; i < n; ++i) p[i] = v[i] / np_;
+            has_p = 1;
+        } else {
+            has_p = 0;
+        }
+        rho_prev = rho_k;
+    }
+    if (x_out) memcpy(x_out, x, nb);
+    if (rep) {
+        rep->status = status;
+        rep->cycles = k;
+        rep->a_matvecs = c.a_mv;
+        rep->b_matvecs = c.b_mv;
+        rep->rho = rho;
+        rep->resid = res;
+    }
+    (void)qmax;
+    free(M); free(x); free(Ax); free(Bx); free(r); free(p); free(Ap); free(Bp); free(v); free(tmp);
+    free(g); free(xt); free(d); free(G); free(AG); free(BG);
+    return status;
+}

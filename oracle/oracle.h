@@ -87,6 +87,41 @@ typedef struct {
 int orc_trplk_solve(const orc_problem* prob, double* evals, double* evecs, double* resid,
                     orc_report* rep);
 
+/* ------------------------------------------------------------------ PL+1 (Algorithm 2)
+ * Preconditioned Lanczos+1 for the lowest eigenpair of (A, B) (alg:pl+1),
+ * readings P1-P6 of DESIGN.md section 2 (NEXT-1 of SURVEY 8(f)). */
+typedef struct {
+    int64_t n;
+    const int64_t* a_rowptr; const int64_t* a_col; const double* a_val;
+    const int64_t* b_rowptr; const int64_t* b_col; const double* b_val;  /* all NULL: B = I */
+    double sigma;           /* M = Jacobi of A - sigma B (R1, R12 floor) */
+    int use_precond;        /* 0: M = I */
+    int m;                  /* Krylov block size (step 4), 1..32 */
+    double tol;             /* delta: stop when ||r_k||_2 <= delta (step 3) */
+    uint64_t seed;          /* x_0(i) = u01(seed, 3, i) when x0 is NULL (P6) */
+    const double* x0;       /* optional start vector (n) */
+    int max_cycles;
+    int variant;            /* 0: step-7 conjugation (paper); 1: practical p = g + p w(m+2) */
+} orc_pl1_problem;
+
+typedef struct {
+    int status;             /* 0 OK, 2 NOT_CONVERGED, 3 BREAKDOWN, 1 EINVAL */
+    int cycles;             /* outer iterations performed */
+    int64_t a_matvecs, b_matvecs;
+    double rho, resid;      /* final rho_k and ||r_k||_2 */
+    int log_cap, log_len;   /* per-iteration log, entry k = state at the top of iteration k */
+    double* log_rho;        /* rho_k = rho(x_k) */
+    double* log_res;        /* ||r_k||_2 */
+    double* log_conj;       /* p_{k-1}^T (A - rho_{k-1} B) p_k / ||A||_F of the step-7 update that
+                               produced p_k (entry k+1 holds iteration k's); 0 where undefined */
+    double* log_ritz;       /* lowest Ritz value of step 5 at iteration k (entry k), or 0 */
+    int* log_mg;            /* columns of G_k built at iteration k (entry k; < m after a breakdown) */
+    int* log_nq;            /* columns of Q_k used in the RR at iteration k (p dropped if dependent) */
+} orc_pl1_report;
+
+/* Algorithm 2.  x_out (n, may be NULL): the final B-normalised iterate. */
+int orc_pl1_solve(const orc_pl1_problem* prob, double* x_out, orc_pl1_report* rep);
+
 #ifdef __cplusplus
 }
 #endif
