@@ -128,6 +128,29 @@ trplk_status trplk_solve(trplk_ctx* ctx, int p, int max_basis, int k_plus, doubl
                          double* eigenvalues, double* eigenvectors, double* residual_norms,
                          const trplk_options* opt, trplk_stats* stats);
 
+/* PL+1, Algorithm 2 (alg:pl+1) for the LOWEST eigenpair
+ * of the context's pencil with the context's Jacobi preconditioner M ~ (A - sigma B)^-1 (or
+ * M = I when use_precond = 0), readings P1-P6 of DESIGN.md section 2:
+ *   step 4  G_k: B-orthonormal (CGS2) basis of span{M(A-rho_k B)x_k, ..., [M(A-rho_k B)]^m x_k}
+ *   step 5  lowest primitive Ritz pair of (Q^T A Q, Q^T B Q), Q = [x_k, G_k, p_{k-1}], by
+ *           Cholesky reduction + the Jacobi eig (p_{k-1} dropped when numerically dependent)
+ *   step 6  x_{k+1} = Q w / ||Q w||_B, rho_{k+1} = x^T A x / x^T B x, r_{k+1} = (A - rho B) x
+ *   step 7  p_k = B-normalised g_k - [p^T(A - rho_{k-1}B)g_k / p^T(A - rho_{k-1}B)p] p_{k-1}
+ *           (variant 0, the paper's), or g_k + w(m+2) p_{k-1} (variant 1)
+ * until ||r_k||_2 <= tol or max_iter iterations.  One rank (nranks == 1), 1 <= m <= 32.
+ *   x0          start vector [n_local] (device or host), NULL: x0(i) = u01(seed, 3, i) (R13)
+ *   rho         host: final rho_k;  resid: host ||r_k||_2;  x_out [n_local] device or host
+ *               (cudaMemcpyDefault) or NULL: the B-normalised x_k
+ *   log_*       host arrays of capacity log_cap (any NULL): rho_k, ||r_k||, and the step-7
+ *               defect p_{k-1}^T(A - rho_{k-1}B)p_k / ||A||_F of the update that produced p_k
+ *               (entry k+1), per iteration; *log_len = entries written
+ * stats: a_matvecs, b_matvecs, cycles (= iterations), status, solve_seconds are filled.
+ * Returns OK, NOT_CONVERGED, BREAKDOWN (Cholesky of Q^T B Q failed on x_k or G_k), EINVAL. */
+trplk_status trplk_pl1_solve(trplk_ctx* ctx, int m, double tol, int variant, int use_precond, int max_iter,
+                             uint64_t seed, const double* x0, double* rho, double* resid, double* x_out,
+                             int log_cap, double* log_rho, double* log_res, double* log_conj, int* log_len,
+                             trplk_stats* stats);
+
 /* Per-cycle log of the last solve (SURVEY 8(c.2) "Log per cycle"); any pointer may be NULL.
  * Arrays have capacity cap (thetas: cap x p^, row-major).  Returns the number of cycles logged. */
 int trplk_get_log(const trplk_ctx* ctx, int cap, int* t, int64_t* mv, double* theta_t,

@@ -1787,6 +1787,267 @@ trplk_status trplk_set_debug(trplk_ctx* ctx, int flags) {
     return TRPLK_OK;
 }
 
+// ------------------------------------------------------------ PL+1 (Algorithm 2, NEXT-1)
+// Readings P1-P6; the oracle's orc_pl1_solve follows the same steps.
+// Q = [x, g_1..g_m, p] lives in one block of m+2 columns (ld = ctx->ld) so that the Gram
+// columns Q^T (A q_j), Q^T (B q_j) come from the fused dot kernel (set1 = x, D_TCOL) and the
+// combination G w from the DMMA rotation; A Q and B Q are kept as blocks of the same shape.
+static trplk_status pl1_impl(trplk_ctx* ctx, int m, double tol, int variant, int use_precond, int max_iter,
+                             uint64_t seed, const double* x0, double* rho_out, double* resid_out, double* x_out,
+                             int log_cap, double* log_rho, double* log_res, double* log_conj, int* log_len,
+                             trplk_stats* stats) {
+    const int64_t n = ctx->n_loc, ld = ctx->ld;
+    const int nc = m + 2;
+    cudaStream_t st = ctx->stream;
+    double *Q, *AQ, *BQ, *r, *xt, *g, *pt, *v, *tmp, *Hq, *Sq, *part;
+    Pl1Dev* dv;
+    ST(dalloc(ctx, &Q, (size_t)ld * nc));
+    ST(dalloc(ctx, &AQ, (size_t)ld * nc));
+    BQ = Q;
+    if (ctx->hasB) ST(dalloc(ctx, &BQ, (size_t)ld * nc));
+    for (double** b : {&r, &xt, &g, &pt, &v, &tmp}) ST(dalloc(ctx, b, (size_t)ld));
+    ST(dalloc(ctx, &Hq, (size_t)nc * nc));
+    ST(dalloc(ctx, &Sq, (size_t)nc * nc));
+    ST(dalloc(ctx, &part, (size_t)PL1_PART));
+    ST(dalloc(ctx, &dv, 1));
+    CK(cudaMemsetAsync(Q, 0, 8 * (size_t)ld * nc, st));
+    CK(cudaMemsetAsync(AQ, 0, 8 * (size_t)ld * nc, st));
+    if (ctx->hasB) CK(cudaMemsetAsync(BQ, 0, 8 * (size_t)ld * nc, st));
+    for (double* b : {r, xt, g, pt, v, tmp}) CK(cudaMemsetAsync(b, 0, 8 * (size_t)ld, st));
+    CK(cudaMemsetAsync(dv, 0, sizeof(Pl1Dev), st));
+    double* x = Q;
+    double* G = Q + ld;
+    double* p = Q + ld * (m + 1);
+    double *Ax = AQ, *AG = AQ + ld, *Ap = AQ + ld * (m + 1);
+    double *Bx = BQ, *BG = BQ + ld, *Bp = BQ + ld * (m + 1);
+    double* sc = dv->sc;
+    int64_t amv = 0, bmv = 0;
+    ctx->launches = 0;
+    auto spmv = [&](bool useB, const double* xin, double* out) -> trplk_status {
+        ST(halo(ctx, xin));
+        SdotsArgs a = sd_base(ctx);
+        a.A = useB ? ctx->B : ctx->A;
+        a.x = xin;
+        a.out_mode = 1;
+        a.out = out;
+        ST(run_sdots(ctx, a, 0));
+        if (useB) bmv++;
+        else amv++;
+        return TRPLK_OK;
+    };
+    auto dots = [&](std::initializer_list<std::pair<std::pair<const double*, const double*>, int>> L) {
+        Pl1Pairs P{};
+        for (auto& e : L) {
+            P.a[P.np] = e.first.first;
+            P.b[P.np] = e.first.second;
+            P.slot[P.np] = e.second;
+            P.np++;
+        }
+        pl1_dots(P, n, part, sc, st);
+        ctx->launches += 2;
+    };
+    double h[16];
+    auto read_sc = [&]() -> trplk_status {
+        CK(cudaMemcpyAsync(h, sc, sizeof(h), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        return TRPLK_OK;
+    };
+    Ctl& H = *ctx->ctl_h;
+    ST(ctl_pull(ctx));
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    CK(cudaEventRecord(e0, st));
+    // step 2: x_0 (P6), ||x_0||_B = 1, rho_0, r_0
+    if (x0) CK(cudaMemcpyAsync(x, x0, 8 * (size_t)n, cudaMemcpyDefault, st));
+    else launch_random(x, n, ctx->row_begin, ctx->n_global, seed, 3, 0, st);
+    const double* Bxin = x;
+    if (ctx->hasB) {
+        ST(spmv(true, x, tmp));
+        Bxin = tmp;
+    }
+    dots({{{x, Bxin}, 0}});
+    pl1_scale(n, x, sc + 0, x, st);
+    ST(spmv(false, x, Ax));
+    if (ctx->hasB) ST(spmv(true, x, Bx));
+    dots({{{x, Ax}, 1}, {{x, Bx}, 2}});
+    pl1_res(n, Ax, Bx, sc + 1, sc + 2, r, st);
+    dots({{{r, r}, 3}});
+    ST(read_sc());
+    double rho = h[1] / h[2], res = std::sqrt(h[3]);
+    double rho_prev = rho, conj_next = 0.0;
+    int has_p = 0, k = 0;
+    trplk_status status = TRPLK_NOT_CONVERGED;
+    int nlog = 0;
+    for (k = 0;; ++k) {
+        if (k < log_cap) {
+            if (log_rho) log_rho[k] = rho;
+            if (log_res) log_res[k] = res;
+            if (log_conj) log_conj[k] = conj_next;
+            nlog = k + 1;
+        }
+        if (res <= tol) {  // step 3
+            status = TRPLK_OK;
+            break;
+        }
+        if (k >= max_iter) break;
+        // step 4 (P1): G_k, each new vector CGS2-orthogonalised against the previous ones
+        int mg = 0;
+        for (int j = 0; j < m; ++j) {
+            if (j == 0) pl1_prec(ctx->A, ctx->B, n, ctx->sigma, ctx->mfloor, r, r, 0.0, v, use_precond, st);
+            else pl1_prec(ctx->A, ctx->B, n, ctx->sigma, ctx->mfloor, AG + ld * (j - 1), BG + ld * (j - 1), rho, v,
+                          use_precond, st);
+            ctx->launches++;
+            H.k = mg;
+            H.flags = ~0u;
+            H.pass3 = 0;
+            ST(ctl_push(ctx));
+            CgsSpec cs{};
+            cs.x = v;
+            cs.V = G;
+            cs.kv = mg;
+            cs.k_nominal = mg;
+            cs.dest = G;
+            cs.dest_dyn = 1;
+            cs.gate = F_CYCLE;
+            cs.clear = F_CYCLE;
+            cs.inc_k = 1;
+            const int p3 = H.pass3_count;
+            ST(cgs2(ctx, cs));
+            ST(ctl_pull(ctx));
+            if (ctx->hasB) bmv += 2 + (H.pass3_count - p3);
+            if (!(H.flags & F_CYCLE)) break;  // breakdown: G_k ends with mg columns
+            ST(spmv(false, G + ld * mg, AG + ld * mg));
+            if (ctx->hasB) ST(spmv(true, G + ld * mg, BG + ld * mg));
+            ++mg;
+        }
+        for (int j = mg; j < m; ++j) {  // unused slots stay zero (they enter G w with weight 0)
+            CK(cudaMemsetAsync(G + ld * j, 0, 8 * (size_t)ld, st));
+            CK(cudaMemsetAsync(AG + ld * j, 0, 8 * (size_t)ld, st));
+            if (ctx->hasB) CK(cudaMemsetAsync(BG + ld * j, 0, 8 * (size_t)ld, st));
+        }
+        // step 5 (P2, P3): Gram columns of Q_k = [x_k, G_k, p_{k-1}], reduced pencil, eig
+        if (has_p) {
+            ST(spmv(false, p, Ap));
+            if (ctx->hasB) ST(spmv(true, p, Bp));
+        }
+        for (int j = 0; j < nc; ++j) {
+            if (j > mg && !(j == m + 1 && has_p)) continue;
+            for (int which = 0; which < 2; ++which) {
+                SdotsArgs a = sd_base(ctx);
+                a.x = (which == 0 ? AQ : BQ) + ld * j;
+                a.set1 = 3;
+                a.U = Q;
+                a.k1 = nc;
+                a.dest1 = D_TCOL;
+                a.tcol_fixed = j;
+                a.T = which == 0 ? Hq : Sq;
+                a.ldT = nc;
+                ST(run_sdots(ctx, a, nc));
+            }
+        }
+        pl1_reduce(Hq, Sq, nc, m, mg, has_p, ctx->T, QMAX, dv, st);
+        int nqf[2];
+        CK(cudaMemcpyAsync(nqf, &dv->nq, sizeof(nqf), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        if (nqf[1] >= 0) {
+            ctx->err = "PL+1: Q_k^T B Q_k not positive definite on [x_k, G_k] (P3)";
+            status = TRPLK_BREAKDOWN;
+            break;
+        }
+        launch_eig(ctx->ctl, ctx->T, QMAX, ctx->Yg, QMAX, 0, nqf[0], 0, st);
+        pl1_back(ctx->Yg, QMAX, m, dv, st);
+        ctx->launches += 3;
+        // step 6 (P5): g_k = G w(2:m+1), x~ = w(1) x + g + w(m+2) p, x_{k+1}, rho_{k+1}, r_{k+1}
+        launch_rotate(G, ld, n, ctx->ctl, m, dv->w + 1, PL1_QP, 1, g, ld, 0, st, m);
+        pl1_xt(n, x, g, p, dv, m, xt, st);
+        const double* Bxt = xt;
+        if (ctx->hasB) {
+            ST(spmv(true, xt, tmp));
+            Bxt = tmp;
+        }
+        dots({{{xt, Bxt}, 0}});
+        pl1_scale(n, xt, sc + 0, x, st);
+        ST(spmv(false, x, Ax));
+        if (ctx->hasB) ST(spmv(true, x, Bx));
+        dots({{{x, Ax}, 1}, {{x, Bx}, 2}});
+        pl1_res(n, Ax, Bx, sc + 1, sc + 2, r, st);
+        dots({{{r, r}, 3}});
+        ctx->launches += 5;
+        // step 7 (P4): p~_k and p_k
+        const bool conj = has_p && variant == 0;
+        if (!has_p) {
+            CK(cudaMemcpyAsync(pt, g, 8 * (size_t)n, cudaMemcpyDeviceToDevice, st));
+        } else if (variant == 1) {
+            pl1_pt(n, g, p, sc + 4, sc + 5, 0.0, 1, dv, m, pt, st);
+        } else {
+            pl1_axpby(n, 1.0, Ap, -rho_prev, Bp, v, st);  // d = (A - rho_{k-1} B) p_{k-1}
+            dots({{{v, g}, 4}, {{v, p}, 5}});
+            pl1_pt(n, g, p, sc + 4, sc + 5, 1e-14 * ctx->normF, 0, dv, m, pt, st);
+        }
+        const double* Bpt = pt;
+        if (ctx->hasB) {
+            ST(spmv(true, pt, tmp));
+            Bpt = tmp;
+        }
+        dots({{{pt, Bpt}, 6}});
+        ST(read_sc());
+        if (h[6] > 0.0) {
+            pl1_scale(n, pt, sc + 6, p, st);
+            if (conj) dots({{{v, p}, 7}});
+            has_p = 1;
+        } else {
+            has_p = 0;
+        }
+        ST(read_sc());
+        conj_next = conj && has_p ? h[7] / ctx->normF : 0.0;
+        rho_prev = rho;
+        rho = h[1] / h[2];
+        res = std::sqrt(h[3]);
+    }
+    CK(cudaEventRecord(e1, st));
+    CK(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    if (x_out) CK(cudaMemcpyAsync(x_out, x, 8 * (size_t)n, cudaMemcpyDefault, st));
+    CK(cudaStreamSynchronize(st));
+    if (rho_out) *rho_out = rho;
+    if (resid_out) *resid_out = res;
+    if (log_len) *log_len = nlog;
+    if (stats) {
+        memset(stats, 0, sizeof(*stats));
+        stats->a_matvecs = amv;
+        stats->b_matvecs = bmv;
+        stats->cycles = k;
+        stats->status = status;
+        stats->solve_seconds = ms * 1e-3;
+        stats->kernel_launches = ctx->launches;
+    }
+    for (void* b : {(void*)Q, (void*)AQ, (void*)r, (void*)xt, (void*)g, (void*)pt, (void*)v, (void*)tmp, (void*)Hq,
+                    (void*)Sq, (void*)part, (void*)dv})
+        dev_free(ctx, b);
+    if (ctx->hasB) dev_free(ctx, BQ);
+    return status;
+}
+
+trplk_status trplk_pl1_solve(trplk_ctx* ctx, int m, double tol, int variant, int use_precond, int max_iter,
+                             uint64_t seed, const double* x0, double* rho, double* resid, double* x_out,
+                             int log_cap, double* log_rho, double* log_res, double* log_conj, int* log_len,
+                             trplk_stats* stats) {
+    if (!ctx) return TRPLK_EINVAL;
+    if (ctx->nranks != 1 || m < 1 || m > 32 || !(tol > 0.0) || max_iter < 0 || (variant != 0 && variant != 1)) {
+        ctx->err = "PL+1: needs one rank, 1 <= m <= 32, tol > 0, max_iter >= 0, variant 0/1";
+        return TRPLK_EINVAL;
+    }
+    enter_stream(ctx);
+    const trplk_status s = pl1_impl(ctx, m, tol, variant, use_precond, max_iter, seed, x0, rho, resid, x_out,
+                                    log_cap, log_rho, log_res, log_conj, log_len, stats);
+    leave_stream(ctx);
+    return s;
+}
+
 // ------------------------------------------------------------ kernel-level entry points
 static trplk_status kprep(trplk_ctx* ctx, int k) {
     if (!ctx) return TRPLK_EINVAL;

@@ -1201,6 +1201,7 @@ __global__ void k_gather(const double* x, const int* idx, int64_t n, double* out
 #include "k1_pipe.cuh"     // software-pipelined K1 (DIA, B = I, k <= 24)
 #include "small.cuh"       // single-CTA inner loop for small n (latency path)
 #include "inner_grid.cuh"  // cooperative grid-wide inner loop for mid-size n (latency path)
+#include "pl1.cuh"         // PL+1 (Algorithm 2) small kernels
 
 namespace trplk {
 

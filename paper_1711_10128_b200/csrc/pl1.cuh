@@ -1,0 +1,247 @@
+// Small kernels of PL+1 (Algorithm 2; NEXT-1 of SURVEY 8(f)), readings P1-P6
+// of DESIGN.md section 2.  The n-length work reuses the TRPL+K kernels (SpMV, CGS2 in the
+// B-inner product, Gram columns by the fused dot kernel, the DMMA rotation, the Jacobi eig);
+// these add the projected-pencil reduction of step 5 and the vector updates of steps 4, 6, 7.
+// Included by kernels.cu (mat_diag, warp_sum).
+#pragma once
+
+namespace trplk {
+
+// v = M (z - rho s), M = Jacobi of A - sigma B (R1, floor R12); s = x when B = I.
+__global__ void k_pl1_prec(const Sell A, const Sell B, int64_t n, double sigma, double mfloor, const double* z,
+                           const double* s, double rho, double* v, int prec) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        if (!prec) {  // M = I
+            v[i] = z[i] - rho * s[i];
+            continue;
+        }
+        const double ad = mat_diag(A, i >> 5, (int)(i & 31));
+        const double bd = B.nrows ? mat_diag(B, i >> 5, (int)(i & 31)) : 1.0;
+        double d = fabs(ad - sigma * bd);
+        d = d > mfloor ? d : mfloor;
+        v[i] = (1.0 / d) * (z[i] - rho * s[i]);
+    }
+}
+
+// Deterministic dot products of up to 4 vector pairs (Pl1Pairs): CTA partials, then one CTA
+// sums them in CTA order (k_pl1_dots_fin).  out[slot[t]] = a_t . b_t.
+constexpr int PL1_DOT_CTAS = 296;
+
+__global__ void __launch_bounds__(256) k_pl1_dots(Pl1Pairs P, int64_t n, double* part) {
+    __shared__ double sw[8][4];
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+#pragma unroll
+        for (int t = 0; t < 4; ++t)
+            if (t < P.np) acc[t] = fma(P.a[t][i], P.b[t][i], acc[t]);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+        double v = acc[t];
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0) sw[warp][t] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < 4) {
+        double s = 0.0;
+        for (int w = 0; w < 8; ++w) s += sw[w][threadIdx.x];
+        part[(int64_t)blockIdx.x * 4 + threadIdx.x] = s;
+    }
+}
+
+__global__ void k_pl1_dots_fin(Pl1Pairs P, const double* part, int nblk, double* out) {
+    const int t = threadIdx.x;
+    if (t >= P.np) return;
+    double s = 0.0;
+    for (int b = 0; b < nblk; ++b) s += part[b * 4 + t];
+    out[P.slot[t]] = s;
+}
+
+// Step 5 (P2, P3): compact the Gram columns of Q = [x, G(:, 0:mg), p] out of the (m+2)-wide
+// H = Q^T A Q and S = Q^T B Q (column-major, ld = ldq), symmetrise, Cholesky S = L L^T with the
+// P3 pivot test (a failing p column is dropped), C = L^-1 H L^-T into T (ld ldT).  One CTA.
+__global__ void k_pl1_reduce(const double* Hq, const double* Sq, int ldq, int m, int mg, int has_p, double* T,
+                             int ldT, Pl1Dev* d) {
+    __shared__ double H[PL1_QP * PL1_QP], S[PL1_QP * PL1_QP], L[PL1_QP * PL1_QP], C[PL1_QP * PL1_QP];
+    __shared__ int cols[PL1_QP];
+    __shared__ int snq, sfail;
+    const int tid = threadIdx.x;
+    if (tid == 0) {
+        int nq = 0;
+        cols[nq++] = 0;
+        for (int j = 0; j < mg; ++j) cols[nq++] = 1 + j;
+        if (has_p) cols[nq++] = m + 1;
+        snq = nq;
+        sfail = -1;
+    }
+    __syncthreads();
+    int nq = snq;
+    for (int idx = tid; idx < nq * nq; idx += blockDim.x) {
+        const int i = idx % nq, j = idx / nq;
+        const int ci = cols[i], cj = cols[j];
+        H[i + PL1_QP * j] = 0.5 * (Hq[ci + (int64_t)ldq * cj] + Hq[cj + (int64_t)ldq * ci]);
+        S[i + PL1_QP * j] = 0.5 * (Sq[ci + (int64_t)ldq * cj] + Sq[cj + (int64_t)ldq * ci]);
+        L[i + PL1_QP * j] = 0.0;
+    }
+    __syncthreads();
+    for (int j = 0; j < nq; ++j) {
+        if (tid == 0) {
+            double dd = S[j + PL1_QP * j];
+            for (int k = 0; k < j; ++k) dd -= L[j + PL1_QP * k] * L[j + PL1_QP * k];
+            if (!(dd > 1e-24 * S[j + PL1_QP * j])) {
+                if (has_p && j == nq - 1) snq = nq - 1;  // P3: drop p_{k-1}
+                else sfail = j;
+            } else {
+                L[j + PL1_QP * j] = sqrt(dd);
+            }
+        }
+        __syncthreads();
+        if (sfail >= 0 || snq < nq) break;
+        const double ljj = L[j + PL1_QP * j];
+        for (int i = j + 1 + tid; i < nq; i += blockDim.x) {
+            double s = S[i + PL1_QP * j];
+            for (int k = 0; k < j; ++k) s -= L[i + PL1_QP * k] * L[j + PL1_QP * k];
+            L[i + PL1_QP * j] = s / ljj;
+        }
+        __syncthreads();
+    }
+    nq = snq;
+    if (sfail >= 0) {
+        if (tid == 0) {
+            d->nq = nq;
+            d->fail = sfail;
+        }
+        return;
+    }
+    // C = L^-1 H (forward substitution, one column per thread), then (L^-1 H) L^-T (one row per thread)
+    for (int j = tid; j < nq; j += blockDim.x)
+        for (int i = 0; i < nq; ++i) {
+            double s = H[i + PL1_QP * j];
+            for (int t = 0; t < i; ++t) s -= L[i + PL1_QP * t] * C[t + PL1_QP * j];
+            C[i + PL1_QP * j] = s / L[i + PL1_QP * i];
+        }
+    __syncthreads();
+    for (int i = tid; i < nq; i += blockDim.x)
+        for (int j = 0; j < nq; ++j) {
+            double s = C[i + PL1_QP * j];
+            for (int t = 0; t < j; ++t) s -= L[j + PL1_QP * t] * H[i + PL1_QP * t];  // H reused as Y
+            H[i + PL1_QP * j] = s / L[j + PL1_QP * j];
+        }
+    __syncthreads();
+    for (int idx = tid; idx < nq * nq; idx += blockDim.x) {
+        const int i = idx % nq, j = idx / nq;
+        T[i + (int64_t)ldT * j] = H[i + PL1_QP * j];
+        d->L[i + PL1_QP * j] = L[i + PL1_QP * j];
+    }
+    if (tid < PL1_QP) d->cols[tid] = tid < nq ? cols[tid] : -1;
+    if (tid == 0) {
+        d->nq = nq;
+        d->fail = -1;
+    }
+}
+
+// w = L^-T y_1 (y_1 = column 0 of Y, ld ldY), sign w(1) >= 0 (P2), scattered to the m+2 slots of
+// Q (zeros for unused slots) in d->w.  One thread.
+__global__ void k_pl1_back(const double* Y, int ldY, int m, Pl1Dev* d) {
+    if (threadIdx.x != 0) return;
+    const int nq = d->nq;
+    double w[PL1_QP];
+    for (int i = nq - 1; i >= 0; --i) {
+        double s = Y[i];
+        for (int t = i + 1; t < nq; ++t) s -= d->L[t + PL1_QP * i] * w[t];
+        w[i] = s / d->L[i + PL1_QP * i];
+    }
+    const double sg = w[0] < 0.0 ? -1.0 : 1.0;
+    for (int i = 0; i < m + 2; ++i) d->w[i] = 0.0;
+    for (int i = 0; i < nq; ++i) d->w[d->cols[i]] = sg * w[i];
+}
+
+// xt = w(1) x + g + w(m+2) p (step 6)
+__global__ void k_pl1_xt(int64_t n, const double* x, const double* g, const double* p, const Pl1Dev* d, int m,
+                         double* xt) {
+    const double a = d->w[0], b = d->w[m + 1];
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        xt[i] = a * x[i] + g[i] + b * p[i];
+}
+
+// y = x / sqrt(*nrm2)
+__global__ void k_pl1_scale(int64_t n, const double* x, const double* nrm2, double* y) {
+    const double s = sqrt(*nrm2);
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        y[i] = x[i] / s;
+}
+
+// r = Ax - rho Bx with rho = xAx / xBx from the device scalars (step 6)
+__global__ void k_pl1_res(int64_t n, const double* Ax, const double* Bx, const double* xAx, const double* xBx,
+                          double* r) {
+    const double rho = *xAx / *xBx;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        r[i] = Ax[i] - rho * Bx[i];
+}
+
+// y = a x + b z (host scalars)
+__global__ void k_pl1_axpby(int64_t n, double a, const double* x, double b, const double* z, double* y) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        y[i] = a * x[i] + b * z[i];
+}
+
+// step 7 (P4): pt = g - (num/den) p, coefficient 0 when |den| <= 1e-14 ||A||_F; variant 1: g + w(m+2) p
+__global__ void k_pl1_pt(int64_t n, const double* g, const double* p, const double* num, const double* den,
+                         double den_floor, int variant, const Pl1Dev* d, int m, double* pt) {
+    double c;
+    if (variant == 1) c = d->w[m + 1];
+    else c = fabs(*den) <= den_floor ? 0.0 : -(*num / *den);
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        pt[i] = g[i] + c * p[i];
+}
+
+static int pl1_grid(int64_t n) {
+    int64_t g = (n + 255) / 256;
+    if (g > 148 * 8) g = 148 * 8;
+    return (int)(g < 1 ? 1 : g);
+}
+
+void pl1_prec(const Sell& A, const Sell& B, int64_t n, double sigma, double mfloor, const double* z,
+              const double* s, double rho, double* v, int prec, cudaStream_t st) {
+    k_pl1_prec<<<pl1_grid(n), 256, 0, st>>>(A, B, n, sigma, mfloor, z, s, rho, v, prec);
+}
+
+void pl1_dots(const Pl1Pairs& P, int64_t n, double* part, double* out, cudaStream_t st) {
+    int g = (int)std::min<int64_t>(PL1_DOT_CTAS, (n + 255) / 256);
+    if (g < 1) g = 1;
+    k_pl1_dots<<<g, 256, 0, st>>>(P, n, part);
+    k_pl1_dots_fin<<<1, 32, 0, st>>>(P, part, g, out);
+}
+
+void pl1_reduce(const double* Hq, const double* Sq, int ldq, int m, int mg, int has_p, double* T, int ldT,
+                Pl1Dev* d, cudaStream_t st) {
+    k_pl1_reduce<<<1, 64, 0, st>>>(Hq, Sq, ldq, m, mg, has_p, T, ldT, d);
+}
+
+void pl1_back(const double* Y, int ldY, int m, Pl1Dev* d, cudaStream_t st) { k_pl1_back<<<1, 32, 0, st>>>(Y, ldY, m, d); }
+
+void pl1_xt(int64_t n, const double* x, const double* g, const double* p, const Pl1Dev* d, int m, double* xt,
+            cudaStream_t st) {
+    k_pl1_xt<<<pl1_grid(n), 256, 0, st>>>(n, x, g, p, d, m, xt);
+}
+
+void pl1_scale(int64_t n, const double* x, const double* nrm2, double* y, cudaStream_t st) {
+    k_pl1_scale<<<pl1_grid(n), 256, 0, st>>>(n, x, nrm2, y);
+}
+
+void pl1_res(int64_t n, const double* Ax, const double* Bx, const double* xAx, const double* xBx, double* r,
+             cudaStream_t st) {
+    k_pl1_res<<<pl1_grid(n), 256, 0, st>>>(n, Ax, Bx, xAx, xBx, r);
+}
+
+void pl1_axpby(int64_t n, double a, const double* x, double b, const double* z, double* y, cudaStream_t st) {
+    k_pl1_axpby<<<pl1_grid(n), 256, 0, st>>>(n, a, x, b, z, y);
+}
+
+void pl1_pt(int64_t n, const double* g, const double* p, const double* num, const double* den, double den_floor,
+            int variant, const Pl1Dev* d, int m, double* pt, cudaStream_t st) {
+    k_pl1_pt<<<pl1_grid(n), 256, 0, st>>>(n, g, p, num, den, den_floor, variant, d, m, pt);
+}
+
+}  // namespace trplk

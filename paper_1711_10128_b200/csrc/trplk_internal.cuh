@@ -167,6 +167,37 @@ struct GridArgs {
     unsigned long long* trace;  // optional (TRPLK_GRID_TRACE): phase timestamps of CTA 0, per step
 };
 
+// PL+1 (pl1.cuh): device scratch of the projected pencil of step 5 and the dot-pair list.
+constexpr int PL1_QP = 34;  // Q_k columns: x, m <= 32 Krylov vectors, p
+struct Pl1Dev {
+    double L[PL1_QP * PL1_QP];  // Cholesky factor of Q^T B Q (compacted columns)
+    double w[PL1_QP];           // primitive Ritz vector in Q's m+2 slots (zeros: unused)
+    double sc[16];              // scalars written by pl1_dots
+    int cols[PL1_QP];           // compact column -> Q slot
+    int nq, fail;
+};
+struct Pl1Pairs {
+    const double* a[4];
+    const double* b[4];
+    int slot[4];
+    int np;
+};
+constexpr int PL1_PART = 296 * 4;  // partials of pl1_dots
+void pl1_prec(const Sell& A, const Sell& B, int64_t n, double sigma, double mfloor, const double* z,
+              const double* s, double rho, double* v, int prec, cudaStream_t st);
+void pl1_dots(const Pl1Pairs& P, int64_t n, double* part, double* out, cudaStream_t st);
+void pl1_reduce(const double* Hq, const double* Sq, int ldq, int m, int mg, int has_p, double* T, int ldT,
+                Pl1Dev* d, cudaStream_t st);
+void pl1_back(const double* Y, int ldY, int m, Pl1Dev* d, cudaStream_t st);
+void pl1_xt(int64_t n, const double* x, const double* g, const double* p, const Pl1Dev* d, int m, double* xt,
+            cudaStream_t st);
+void pl1_scale(int64_t n, const double* x, const double* nrm2, double* y, cudaStream_t st);
+void pl1_res(int64_t n, const double* Ax, const double* Bx, const double* xAx, const double* xBx, double* r,
+             cudaStream_t st);
+void pl1_axpby(int64_t n, double a, const double* x, double b, const double* z, double* y, cudaStream_t st);
+void pl1_pt(int64_t n, const double* g, const double* p, const double* num, const double* den, double den_floor,
+            int variant, const Pl1Dev* d, int m, double* pt, cudaStream_t st);
+
 // Kernel launchers (kernels.cu)
 bool launch_inner_small(const SmallArgs& a, int kmax, cudaStream_t s);
 // false: not applicable (kmax > 32 or no co-resident grid); nothing launched

@@ -90,13 +90,15 @@ _sig("trplk_k_random", _I, [_P, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint6
 _sig("trplk_plan_ghosts", _I, [_I64, _I64, _P, _P, _P, _P, _P, _I, _P, _P, _I64, ctypes.POINTER(_I64)])
 _sig("trplk_profile", _I, [_P, _I])
 _sig("trplk_profile_read", _I, [_P, _P, _P, ctypes.POINTER(_I64)])
+_sig("trplk_pl1_solve", _I, [_P, _I, _D, _I, _I, _I, ctypes.c_uint64, _P, _P, _P, _P, _I, _P, _P, _P, _P,
+                             ctypes.POINTER(Stats)])
 
 EXPORTED = ["trplk_options_default", "trplk_nccl_unique_id", "trplk_create", "trplk_solve",
             "trplk_get_log", "trplk_info", "trplk_destroy", "trplk_last_error", "trplk_k_spmv",
             "trplk_k_step1", "trplk_k_cgs2", "trplk_k_rotate", "trplk_k_sym_eig",
             "trplk_k_residual", "trplk_k_random", "trplk_profile", "trplk_profile_read",
             "trplk_plan_ghosts", "trplk_k_sym_eig_time", "trplk_loopback_create", "trplk_loopback_destroy",
-            "trplk_set_debug"]
+            "trplk_set_debug", "trplk_pl1_solve"]
 
 
 class TrplkError(RuntimeError):
@@ -298,6 +300,31 @@ def trplk_solve(ctx: Context, p: int, max_basis: int, k_plus: int, tol: float, e
     if st not in (0, 2, 3):
         ctx.check(st)
     return ev, evecs, rs, stats.as_dict()
+
+
+def trplk_pl1_solve(ctx: Context, m: int, tol: float, variant: int = 0, use_precond: bool = True,
+                    max_iter: int = 2000, seed: int = 12, x0=None, x_out=None):
+    """PL+1 (Algorithm 2) for the lowest eigenpair.  Returns (rho, residual, x torch.cuda (n_local,)
+    or x_out, stats dict, log dict {rho, res, conj})."""
+    import torch
+
+    x = torch.empty(ctx.n_local, dtype=torch.float64, device="cuda") if x_out is None else x_out
+    cap = int(max_iter) + 1
+    lr, ls, lc = np.zeros(cap), np.zeros(cap), np.zeros(cap)
+    nlog = _I(0)
+    rho, res = _D(0.0), _D(0.0)
+    stats = Stats()
+    x0p = None
+    if x0 is not None:
+        x0 = np.ascontiguousarray(x0, np.float64) if not hasattr(x0, "data_ptr") else x0
+        x0p = _ptr(x0)
+    st = _lib.trplk_pl1_solve(ctx.handle, int(m), float(tol), int(variant), 1 if use_precond else 0, int(max_iter),
+                              int(seed), x0p, ctypes.byref(rho), ctypes.byref(res), _ptr(x), cap, _ptr(lr),
+                              _ptr(ls), _ptr(lc), ctypes.byref(nlog), ctypes.byref(stats))
+    if st not in (0, 2, 3):
+        ctx.check(st)
+    L = nlog.value
+    return rho.value, res.value, x, stats.as_dict(), {"rho": lr[:L], "res": ls[:L], "conj": lc[:L]}
 
 
 def trplk_get_log(ctx: Context, cap: int = 100000, ph: Optional[int] = None):
