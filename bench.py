@@ -51,6 +51,9 @@ def parse():
                     help="kernel-profile events on every timed step (default: the last one)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=20.0, help="oracle sample budget")
+    ap.add_argument("--method", default="trplk", choices=["trplk", "pl1"],
+                    help="pl1: PL+1 (Algorithm 2, NEXT-1) for the lowest eigenpair, one GPU")
+    ap.add_argument("--pl1-m", type=int, default=4, help="PL+1 Krylov block size m")
     return ap.parse_args()
 
 
@@ -159,10 +162,96 @@ def run_reference(args):
     return 0
 
 
+def run_pl1(args):
+    """PL+1 (Algorithm 2) on one GPU: a step = one trplk_pl1_solve to tol (time to the lowest
+    eigenpair).  value = A-matvecs / device solve time; roofline = the solve's algorithmic bytes
+    (every launch of the iteration, DESIGN.md byte model) / solve time; e2e = create from pinned
+    host CSR + solve + D2H of x + destroy; cpu_baseline = the oracle's orc_pl1_solve."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    import torch
+    from paper_1711_10128_b200 import build
+    build.build()
+    from paper_1711_10128_b200 import inputs, trplk
+    P = inputs.make(args.config)
+    m, tol = args.pl1_m, P.tol
+    ctx = trplk.trplk_create(P.A, P.B, P.sigma)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+    for _ in range(args.warmup):
+        trplk.trplk_pl1_solve(ctx, m, tol)
+    clocks = Clocks(int(os.environ.get("LOCAL_RANK", "0")))
+    times, sts = [], []
+    for _ in range(args.steps):
+        flush.fill_(1.0)
+        torch.cuda.synchronize()
+        rho, res, x, st, log = trplk.trplk_pl1_solve(ctx, m, tol)
+        torch.cuda.synchronize()
+        assert st["status"] == "OK", st
+        times.append(st["solve_seconds"] * 1e3)
+        sts.append(st)
+    ck = clocks.stop()
+    ms = statistics.mean(times)
+    mv = sts[-1]["a_matvecs"]
+    peak, peak_src = peaks()
+    ach = sts[-1]["model_bytes"] / (ms * 1e-3) / 1e9
+    # e2e: pinned host CSR -> create -> PL+1 -> x to pinned host -> destroy
+    pin = [torch.from_numpy(a).pin_memory() for M in (P.A, P.B) if M is not None for a in (M.rowptr, M.col, M.val)]
+
+    class _H:
+        def __init__(self, rp, c, v):
+            self.rowptr, self.col, self.val, self.n, self.row_begin = rp.numpy(), c.numpy(), v.numpy(), P.A.n, 0
+
+    HA = _H(*pin[0:3])
+    HB = _H(*pin[3:6]) if P.B is not None else None
+    xh = torch.empty(P.A.n, dtype=torch.float64).pin_memory()
+    et = []
+    stream = torch.cuda.current_stream()
+    for it in range(1 + max(1, min(args.steps, 3))):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        c2 = trplk.trplk_create(HA, HB, P.sigma)
+        trplk.trplk_pl1_solve(c2, m, tol, x_out=xh)
+        c2.close()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        if it:
+            et.append(e0.elapsed_time(e1))
+    cpu = None
+    if not args.no_cpu_baseline:
+        import oracle
+        oracle.build()
+        t0 = time.perf_counter()
+        o = oracle.pl1_solve(P.A, P.B, m=m, tol=tol, sigma=P.sigma)
+        dt = time.perf_counter() - t0
+        cpu = {"value": o["a_matvecs"] / dt, "unit": UNIT, "cores": int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1)),
+               "kind": "oracle", "sample": f"full oracle PL+1 solve of {args.config} (m={m}, {o['cycles']} iterations)"}
+    out = {"metric": "PL+1 A-matvecs/s to the lowest eigenpair (fp64)", "value": round(mv / (ms * 1e-3), 2),
+           "unit": UNIT, "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+           "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic (seeded generator, BASELINE configs; paper matrices unavailable)",
+           "config": {"workload": f"{args.config}: {P.desc}; PL+1 m={m}, tol={tol}, Jacobi, seed 12",
+                      "n": P.A.n, "iterations": sts[-1]["cycles"], "a_matvecs_per_solve": mv,
+                      "rho": rho, "l2": "flushed (256 MiB write) between timed steps"},
+           "roofline": {"bound": "hbm", "kernel": "whole PL+1 iteration (all launches, model bytes)",
+                        "achieved": round(ach, 1), "peak": peak, "unit": "GB/s", "frac": round(ach / peak, 4),
+                        "traffic": None, "peak_source": peak_src},
+           "cpu_baseline": cpu,
+           "e2e": {"value": mv / (statistics.mean(et) * 1e-3), "unit": UNIT,
+                   "h2d_bytes_per_step": sum(t.numel() * t.element_size() for t in pin),
+                   "d2h_bytes_per_step": P.A.n * 8, "ms_per_step": statistics.mean(et)},
+           "gpu_launches": sts[-1]["kernel_launches"], "clocks": ck}
+    ctx.close()
+    print(json.dumps(out))
+    return 0
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
+    if args.method == "pl1":
+        return run_pl1(args)
     import numpy as np
     import torch
     import torch.distributed as dist

@@ -1823,6 +1823,8 @@ static trplk_status pl1_impl(trplk_ctx* ctx, int m, double tol, int variant, int
     double* sc = dv->sc;
     int64_t amv = 0, bmv = 0;
     ctx->launches = 0;
+    ctx->model_bytes = 0.0;
+    const double vb = 8.0 * (double)n;  // bytes of one n-vector (DESIGN.md byte model)
     auto spmv = [&](bool useB, const double* xin, double* out) -> trplk_status {
         ST(halo(ctx, xin));
         SdotsArgs a = sd_base(ctx);
@@ -1845,6 +1847,7 @@ static trplk_status pl1_impl(trplk_ctx* ctx, int m, double tol, int variant, int
         }
         pl1_dots(P, n, part, sc, st);
         ctx->launches += 2;
+        ctx->model_bytes += 2.0 * vb * P.np;
     };
     double h[16];
     auto read_sc = [&]() -> trplk_status {
@@ -1898,6 +1901,7 @@ static trplk_status pl1_impl(trplk_ctx* ctx, int m, double tol, int variant, int
             else pl1_prec(ctx->A, ctx->B, n, ctx->sigma, ctx->mfloor, AG + ld * (j - 1), BG + ld * (j - 1), rho, v,
                           use_precond, st);
             ctx->launches++;
+            ctx->model_bytes += (j == 0 ? 2.0 : 3.0) * vb + (double)ctx->sellA_bytes / 8.0;  // z, s, v + diag
             H.k = mg;
             H.flags = ~0u;
             H.pass3 = 0;
@@ -1961,6 +1965,7 @@ static trplk_status pl1_impl(trplk_ctx* ctx, int m, double tol, int variant, int
         // step 6 (P5): g_k = G w(2:m+1), x~ = w(1) x + g + w(m+2) p, x_{k+1}, rho_{k+1}, r_{k+1}
         launch_rotate(G, ld, n, ctx->ctl, m, dv->w + 1, PL1_QP, 1, g, ld, 0, st, m);
         pl1_xt(n, x, g, p, dv, m, xt, st);
+        ctx->model_bytes += vb * (m + 1) + 4.0 * vb + 2.0 * vb + 3.0 * vb;  // rotation, xt, scale, res
         const double* Bxt = xt;
         if (ctx->hasB) {
             ST(spmv(true, xt, tmp));
@@ -1982,10 +1987,12 @@ static trplk_status pl1_impl(trplk_ctx* ctx, int m, double tol, int variant, int
             pl1_pt(n, g, p, sc + 4, sc + 5, 0.0, 1, dv, m, pt, st);
         } else {
             pl1_axpby(n, 1.0, Ap, -rho_prev, Bp, v, st);  // d = (A - rho_{k-1} B) p_{k-1}
+            ctx->model_bytes += 3.0 * vb;
             dots({{{v, g}, 4}, {{v, p}, 5}});
             pl1_pt(n, g, p, sc + 4, sc + 5, 1e-14 * ctx->normF, 0, dv, m, pt, st);
         }
         const double* Bpt = pt;
+        ctx->model_bytes += 3.0 * vb + 2.0 * vb;  // p~, scale
         if (ctx->hasB) {
             ST(spmv(true, pt, tmp));
             Bpt = tmp;
@@ -2024,6 +2031,7 @@ static trplk_status pl1_impl(trplk_ctx* ctx, int m, double tol, int variant, int
         stats->status = status;
         stats->solve_seconds = ms * 1e-3;
         stats->kernel_launches = ctx->launches;
+        stats->model_bytes = ctx->model_bytes;
     }
     for (void* b : {(void*)Q, (void*)AQ, (void*)r, (void*)xt, (void*)g, (void*)pt, (void*)v, (void*)tmp, (void*)Hq,
                     (void*)Sq, (void*)part, (void*)dv})
