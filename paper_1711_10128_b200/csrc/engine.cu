@@ -1894,49 +1894,41 @@ static trplk_status pl1_impl(trplk_ctx* ctx, int m, double tol, int variant, int
             break;
         }
         if (k >= max_iter) break;
-        // step 4 (P1): G_k, each new vector CGS2-orthogonalised against the previous ones
-        int mg = 0;
+        // step 4 (P1): G_k, each new vector CGS2-orthogonalised against the previous ones.  The
+        // CGS2 kernels append at column ctl->k and clear F_CYCLE on a breakdown (R16), which
+        // gates the remaining CGS2 launches of the block: no host round trip inside step 4.
+        H.k = 0;
+        H.flags = ~0u;
+        H.pass3 = 0;
+        ST(ctl_push(ctx));
         for (int j = 0; j < m; ++j) {
             if (j == 0) pl1_prec(ctx->A, ctx->B, n, ctx->sigma, ctx->mfloor, r, r, 0.0, v, use_precond, st);
             else pl1_prec(ctx->A, ctx->B, n, ctx->sigma, ctx->mfloor, AG + ld * (j - 1), BG + ld * (j - 1), rho, v,
                           use_precond, st);
             ctx->launches++;
             ctx->model_bytes += (j == 0 ? 2.0 : 3.0) * vb + (double)ctx->sellA_bytes / 8.0;  // z, s, v + diag
-            H.k = mg;
-            H.flags = ~0u;
-            H.pass3 = 0;
-            ST(ctl_push(ctx));
             CgsSpec cs{};
             cs.x = v;
             cs.V = G;
-            cs.kv = mg;
-            cs.k_nominal = mg;
+            cs.kv = -1;
+            cs.k_nominal = j;
             cs.dest = G;
             cs.dest_dyn = 1;
             cs.gate = F_CYCLE;
             cs.clear = F_CYCLE;
             cs.inc_k = 1;
-            const int p3 = H.pass3_count;
             ST(cgs2(ctx, cs));
-            ST(ctl_pull(ctx));
-            if (ctx->hasB) bmv += 2 + (H.pass3_count - p3);
-            if (!(H.flags & F_CYCLE)) break;  // breakdown: G_k ends with mg columns
-            ST(spmv(false, G + ld * mg, AG + ld * mg));
-            if (ctx->hasB) ST(spmv(true, G + ld * mg, BG + ld * mg));
-            ++mg;
+            ST(spmv(false, G + ld * j, AG + ld * j));  // counted for the columns actually built below
+            if (ctx->hasB) ST(spmv(true, G + ld * j, BG + ld * j));
         }
-        for (int j = mg; j < m; ++j) {  // unused slots stay zero (they enter G w with weight 0)
-            CK(cudaMemsetAsync(G + ld * j, 0, 8 * (size_t)ld, st));
-            CK(cudaMemsetAsync(AG + ld * j, 0, 8 * (size_t)ld, st));
-            if (ctx->hasB) CK(cudaMemsetAsync(BG + ld * j, 0, 8 * (size_t)ld, st));
-        }
-        // step 5 (P2, P3): Gram columns of Q_k = [x_k, G_k, p_{k-1}], reduced pencil, eig
+        // step 5 (P2, P3): Gram columns of Q_k = [x_k, G_k, p_{k-1}], reduced pencil, eig.  Columns
+        // past a breakdown hold finite stale data; the reduction ignores them, w weighs them 0.
         if (has_p) {
             ST(spmv(false, p, Ap));
             if (ctx->hasB) ST(spmv(true, p, Bp));
         }
         for (int j = 0; j < nc; ++j) {
-            if (j > mg && !(j == m + 1 && has_p)) continue;
+            if (j == m + 1 && !has_p) continue;
             for (int which = 0; which < 2; ++which) {
                 SdotsArgs a = sd_base(ctx);
                 a.x = (which == 0 ? AQ : BQ) + ld * j;
@@ -1950,16 +1942,8 @@ static trplk_status pl1_impl(trplk_ctx* ctx, int m, double tol, int variant, int
                 ST(run_sdots(ctx, a, nc));
             }
         }
-        pl1_reduce(Hq, Sq, nc, m, mg, has_p, ctx->T, QMAX, dv, st);
-        int nqf[2];
-        CK(cudaMemcpyAsync(nqf, &dv->nq, sizeof(nqf), cudaMemcpyDeviceToHost, st));
-        CK(cudaStreamSynchronize(st));
-        if (nqf[1] >= 0) {
-            ctx->err = "PL+1: Q_k^T B Q_k not positive definite on [x_k, G_k] (P3)";
-            status = TRPLK_BREAKDOWN;
-            break;
-        }
-        launch_eig(ctx->ctl, ctx->T, QMAX, ctx->Yg, QMAX, 0, nqf[0], 0, st);
+        pl1_reduce(Hq, Sq, nc, m, ctx->ctl, has_p, ctx->T, QMAX, dv, st);
+        launch_eig(ctx->ctl, ctx->T, QMAX, ctx->Yg, QMAX, 0, 0, 0, st);  // k = ctl->k = nq
         pl1_back(ctx->Yg, QMAX, m, dv, st);
         ctx->launches += 3;
         // step 6 (P5): g_k = G w(2:m+1), x~ = w(1) x + g + w(m+2) p, x_{k+1}, rho_{k+1}, r_{k+1}
@@ -1998,15 +1982,23 @@ static trplk_status pl1_impl(trplk_ctx* ctx, int m, double tol, int variant, int
             Bpt = tmp;
         }
         dots({{{pt, Bpt}, 6}});
-        ST(read_sc());
-        if (h[6] > 0.0) {
-            pl1_scale(n, pt, sc + 6, p, st);
-            if (conj) dots({{{v, p}, 7}});
-            has_p = 1;
-        } else {
-            has_p = 0;
+        pl1_scale_p(n, pt, sc + 6, p, dv, st);
+        if (conj) dots({{{v, p}, 7}});
+        // the one host round trip of the iteration: scalars, step-5 status, G_k width, CGS2 passes
+        int info[4];
+        CK(cudaMemcpyAsync(h, sc, sizeof(h), cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(info, &dv->nq, sizeof(info), cudaMemcpyDeviceToHost, st));
+        const int p3 = H.pass3_count;
+        ST(ctl_pull(ctx));
+        const int mg = info[2];
+        if (ctx->hasB) bmv += 2 * std::min(mg + 1, m) + (H.pass3_count - p3) - (m - mg);  // B SpMVs of unbuilt columns
+        amv -= (m - mg);  // SpMVs of columns past a breakdown are not the algorithm's
+        if (info[1] >= 0) {
+            ctx->err = "PL+1: Q_k^T B Q_k not positive definite on [x_k, G_k] (P3)";
+            status = TRPLK_BREAKDOWN;
+            break;
         }
-        ST(read_sc());
+        has_p = info[3];
         conj_next = conj && has_p ? h[7] / ctx->normF : 0.0;
         rho_prev = rho;
         rho = h[1] / h[2];

@@ -61,8 +61,10 @@ __global__ void k_pl1_dots_fin(Pl1Pairs P, const double* part, int nblk, double*
 // Step 5 (P2, P3): compact the Gram columns of Q = [x, G(:, 0:mg), p] out of the (m+2)-wide
 // H = Q^T A Q and S = Q^T B Q (column-major, ld = ldq), symmetrise, Cholesky S = L L^T with the
 // P3 pivot test (a failing p column is dropped), C = L^-1 H L^-T into T (ld ldT).  One CTA.
-__global__ void k_pl1_reduce(const double* Hq, const double* Sq, int ldq, int m, int mg, int has_p, double* T,
+// mg = ctl->k (columns CGS2 appended in step 4); on exit ctl->k = nq for the eig kernel.
+__global__ void k_pl1_reduce(const double* Hq, const double* Sq, int ldq, int m, Ctl* ctl, int has_p, double* T,
                              int ldT, Pl1Dev* d) {
+    const int mg = ctl->k;
     __shared__ double H[PL1_QP * PL1_QP], S[PL1_QP * PL1_QP], L[PL1_QP * PL1_QP], C[PL1_QP * PL1_QP];
     __shared__ int cols[PL1_QP];
     __shared__ int snq, sfail;
@@ -111,6 +113,8 @@ __global__ void k_pl1_reduce(const double* Hq, const double* Sq, int ldq, int m,
         if (tid == 0) {
             d->nq = nq;
             d->fail = sfail;
+            d->mg = mg;
+            ctl->k = 1;  // keep the (discarded) eig of this iteration well defined
         }
         return;
     }
@@ -138,6 +142,8 @@ __global__ void k_pl1_reduce(const double* Hq, const double* Sq, int ldq, int m,
     if (tid == 0) {
         d->nq = nq;
         d->fail = -1;
+        d->mg = mg;
+        ctl->k = nq;
     }
 }
 
@@ -168,6 +174,16 @@ __global__ void k_pl1_xt(int64_t n, const double* x, const double* g, const doub
 // y = x / sqrt(*nrm2)
 __global__ void k_pl1_scale(int64_t n, const double* x, const double* nrm2, double* y) {
     const double s = sqrt(*nrm2);
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        y[i] = x[i] / s;
+}
+
+// p_k = p~_k / ||p~_k||_B, or (zero norm: g_k = 0) no search direction for the next iteration
+__global__ void k_pl1_scale_p(int64_t n, const double* x, const double* nrm2, double* y, Pl1Dev* d) {
+    const double q = *nrm2;
+    if (blockIdx.x == 0 && threadIdx.x == 0) d->has_p = q > 0.0 ? 1 : 0;
+    if (!(q > 0.0)) return;
+    const double s = sqrt(q);
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
         y[i] = x[i] / s;
 }
@@ -214,9 +230,13 @@ void pl1_dots(const Pl1Pairs& P, int64_t n, double* part, double* out, cudaStrea
     k_pl1_dots_fin<<<1, 32, 0, st>>>(P, part, g, out);
 }
 
-void pl1_reduce(const double* Hq, const double* Sq, int ldq, int m, int mg, int has_p, double* T, int ldT,
+void pl1_reduce(const double* Hq, const double* Sq, int ldq, int m, Ctl* ctl, int has_p, double* T, int ldT,
                 Pl1Dev* d, cudaStream_t st) {
-    k_pl1_reduce<<<1, 64, 0, st>>>(Hq, Sq, ldq, m, mg, has_p, T, ldT, d);
+    k_pl1_reduce<<<1, 64, 0, st>>>(Hq, Sq, ldq, m, ctl, has_p, T, ldT, d);
+}
+
+void pl1_scale_p(int64_t n, const double* x, const double* nrm2, double* y, Pl1Dev* d, cudaStream_t st) {
+    k_pl1_scale_p<<<pl1_grid(n), 256, 0, st>>>(n, x, nrm2, y, d);
 }
 
 void pl1_back(const double* Y, int ldY, int m, Pl1Dev* d, cudaStream_t st) { k_pl1_back<<<1, 32, 0, st>>>(Y, ldY, m, d); }

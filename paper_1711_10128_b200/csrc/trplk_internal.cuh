@@ -174,7 +174,9 @@ struct Pl1Dev {
     double w[PL1_QP];           // primitive Ritz vector in Q's m+2 slots (zeros: unused)
     double sc[16];              // scalars written by pl1_dots
     int cols[PL1_QP];           // compact column -> Q slot
-    int nq, fail;
+    int nq, fail;               // read together by the host
+    int mg;                     // G_k columns built (ctl->k after step 4)
+    int has_p;                  // p_k formed (||p~_k||_B > 0)
 };
 struct Pl1Pairs {
     const double* a[4];
@@ -186,8 +188,9 @@ constexpr int PL1_PART = 296 * 4;  // partials of pl1_dots
 void pl1_prec(const Sell& A, const Sell& B, int64_t n, double sigma, double mfloor, const double* z,
               const double* s, double rho, double* v, int prec, cudaStream_t st);
 void pl1_dots(const Pl1Pairs& P, int64_t n, double* part, double* out, cudaStream_t st);
-void pl1_reduce(const double* Hq, const double* Sq, int ldq, int m, int mg, int has_p, double* T, int ldT,
+void pl1_reduce(const double* Hq, const double* Sq, int ldq, int m, Ctl* ctl, int has_p, double* T, int ldT,
                 Pl1Dev* d, cudaStream_t st);
+void pl1_scale_p(int64_t n, const double* x, const double* nrm2, double* y, Pl1Dev* d, cudaStream_t st);
 void pl1_back(const double* Y, int ldY, int m, Pl1Dev* d, cudaStream_t st);
 void pl1_xt(int64_t n, const double* x, const double* g, const double* p, const Pl1Dev* d, int m, double* xt,
             cudaStream_t st);
