@@ -1876,12 +1876,16 @@ static trplk_status pl1_impl(trplk_ctx* ctx, int m, double tol, int variant, int
     dots({{{x, Ax}, 1}, {{x, Bx}, 2}});
     pl1_res(n, Ax, Bx, sc + 1, sc + 2, r, st);
     dots({{{r, r}, 3}});
+    pl1_shift_rho(dv, sc, st);  // rho_cur = rho_0
     ST(read_sc());
     double rho = h[1] / h[2], res = std::sqrt(h[3]);
     double rho_prev = rho, conj_next = 0.0;
     int has_p = 0, k = 0;
     trplk_status status = TRPLK_NOT_CONVERGED;
     int nlog = 0;
+    cudaGraphExec_t gexec[2] = {nullptr, nullptr};
+    double gbytes[2] = {0.0, 0.0};
+    int64_t glaunch[2] = {0, 0}, gamv[2] = {0, 0}, gbmv[2] = {0, 0};
     for (k = 0;; ++k) {
         if (k < log_cap) {
             if (log_rho) log_rho[k] = rho;
@@ -1894,16 +1898,14 @@ static trplk_status pl1_impl(trplk_ctx* ctx, int m, double tol, int variant, int
             break;
         }
         if (k >= max_iter) break;
+        auto issue_iter = [&](int has_p) -> trplk_status {
         // step 4 (P1): G_k, each new vector CGS2-orthogonalised against the previous ones.  The
         // CGS2 kernels append at column ctl->k and clear F_CYCLE on a breakdown (R16), which
         // gates the remaining CGS2 launches of the block: no host round trip inside step 4.
-        H.k = 0;
-        H.flags = ~0u;
-        H.pass3 = 0;
-        ST(ctl_push(ctx));
+        pl1_begin(ctx->ctl, st);
         for (int j = 0; j < m; ++j) {
-            if (j == 0) pl1_prec(ctx->A, ctx->B, n, ctx->sigma, ctx->mfloor, r, r, 0.0, v, use_precond, st);
-            else pl1_prec(ctx->A, ctx->B, n, ctx->sigma, ctx->mfloor, AG + ld * (j - 1), BG + ld * (j - 1), rho, v,
+            if (j == 0) pl1_prec(ctx->A, ctx->B, n, ctx->sigma, ctx->mfloor, r, r, nullptr, v, use_precond, st);
+            else pl1_prec(ctx->A, ctx->B, n, ctx->sigma, ctx->mfloor, AG + ld * (j - 1), BG + ld * (j - 1), &dv->rho_cur, v,
                           use_precond, st);
             ctx->launches++;
             ctx->model_bytes += (j == 0 ? 2.0 : 3.0) * vb + (double)ctx->sellA_bytes / 8.0;  // z, s, v + diag
@@ -1965,12 +1967,13 @@ static trplk_status pl1_impl(trplk_ctx* ctx, int m, double tol, int variant, int
         ctx->launches += 5;
         // step 7 (P4): p~_k and p_k
         const bool conj = has_p && variant == 0;
+        (void)conj;
         if (!has_p) {
             CK(cudaMemcpyAsync(pt, g, 8 * (size_t)n, cudaMemcpyDeviceToDevice, st));
         } else if (variant == 1) {
             pl1_pt(n, g, p, sc + 4, sc + 5, 0.0, 1, dv, m, pt, st);
         } else {
-            pl1_axpby(n, 1.0, Ap, -rho_prev, Bp, v, st);  // d = (A - rho_{k-1} B) p_{k-1}
+            pl1_dvec(n, Ap, Bp, dv, v, st);  // d = (A - rho_{k-1} B) p_{k-1}
             ctx->model_bytes += 3.0 * vb;
             dots({{{v, g}, 4}, {{v, p}, 5}});
             pl1_pt(n, g, p, sc + 4, sc + 5, 1e-14 * ctx->normF, 0, dv, m, pt, st);
@@ -1984,6 +1987,41 @@ static trplk_status pl1_impl(trplk_ctx* ctx, int m, double tol, int variant, int
         dots({{{pt, Bpt}, 6}});
         pl1_scale_p(n, pt, sc + 6, p, dv, st);
         if (conj) dots({{{v, p}, 7}});
+        pl1_shift_rho(dv, sc, st);
+        ctx->launches += 1;
+            return TRPLK_OK;
+        };
+        // one CUDA graph per has_p (the only host-side branch of an iteration); counters and
+        // byte model recorded at capture and re-added per launch
+        const int gi = has_p ? 1 : 0;
+        if (!gexec[gi]) {
+            const double mb0 = ctx->model_bytes;
+            const int64_t l0 = ctx->launches, a0 = amv, b0 = bmv;
+            cudaGraph_t graph;
+            CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+            trplk_status cs_ = issue_iter(has_p);
+            cudaError_t e = cudaStreamEndCapture(st, &graph);
+            if (cs_ != TRPLK_OK) return cs_;
+            if (e != cudaSuccess) {
+                ctx->err = std::string("cudaStreamEndCapture: ") + cudaGetErrorString(e);
+                return TRPLK_ECUDA;
+            }
+            CK(cudaGraphInstantiate(&gexec[gi], graph, 0));
+            cudaGraphDestroy(graph);
+            gbytes[gi] = ctx->model_bytes - mb0;
+            glaunch[gi] = ctx->launches - l0;
+            gamv[gi] = amv - a0;
+            gbmv[gi] = bmv - b0;
+            ctx->model_bytes = mb0;
+            ctx->launches = l0;
+            amv = a0;
+            bmv = b0;
+        }
+        CK(cudaGraphLaunch(gexec[gi], st));
+        ctx->model_bytes += gbytes[gi];
+        ctx->launches += glaunch[gi];
+        amv += gamv[gi];
+        bmv += gbmv[gi];
         // the one host round trip of the iteration: scalars, step-5 status, G_k width, CGS2 passes
         int info[4];
         CK(cudaMemcpyAsync(h, sc, sizeof(h), cudaMemcpyDeviceToHost, st));
@@ -1998,8 +2036,8 @@ static trplk_status pl1_impl(trplk_ctx* ctx, int m, double tol, int variant, int
             status = TRPLK_BREAKDOWN;
             break;
         }
+        conj_next = (has_p && variant == 0 && info[3]) ? h[7] / ctx->normF : 0.0;
         has_p = info[3];
-        conj_next = conj && has_p ? h[7] / ctx->normF : 0.0;
         rho_prev = rho;
         rho = h[1] / h[2];
         res = std::sqrt(h[3]);
@@ -2010,6 +2048,8 @@ static trplk_status pl1_impl(trplk_ctx* ctx, int m, double tol, int variant, int
     CK(cudaEventElapsedTime(&ms, e0, e1));
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
+    for (auto& ge : gexec)
+        if (ge) cudaGraphExecDestroy(ge);
     if (x_out) CK(cudaMemcpyAsync(x_out, x, 8 * (size_t)n, cudaMemcpyDefault, st));
     CK(cudaStreamSynchronize(st));
     if (rho_out) *rho_out = rho;

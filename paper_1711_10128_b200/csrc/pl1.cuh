@@ -9,7 +9,8 @@ namespace trplk {
 
 // v = M (z - rho s), M = Jacobi of A - sigma B (R1, floor R12); s = x when B = I.
 __global__ void k_pl1_prec(const Sell A, const Sell B, int64_t n, double sigma, double mfloor, const double* z,
-                           const double* s, double rho, double* v, int prec) {
+                           const double* s, const double* rhop, double* v, int prec) {
+    const double rho = rhop ? *rhop : 0.0;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         if (!prec) {  // M = I
             v[i] = z[i] - rho * s[i];
@@ -219,8 +220,32 @@ static int pl1_grid(int64_t n) {
 }
 
 void pl1_prec(const Sell& A, const Sell& B, int64_t n, double sigma, double mfloor, const double* z,
-              const double* s, double rho, double* v, int prec, cudaStream_t st) {
+              const double* s, const double* rho, double* v, int prec, cudaStream_t st) {
     k_pl1_prec<<<pl1_grid(n), 256, 0, st>>>(A, B, n, sigma, mfloor, z, s, rho, v, prec);
+}
+
+__global__ void k_pl1_begin(Ctl* ctl) {
+    ctl->k = 0;
+    ctl->flags = ~0u;
+    ctl->pass3 = 0;
+}
+
+__global__ void k_pl1_shift_rho(Pl1Dev* d, const double* sc) {
+    d->rho_prev = d->rho_cur;
+    d->rho_cur = sc[1] / sc[2];
+}
+
+// v = (A - rho_{k-1} B) p_{k-1} from the stored products (P4)
+__global__ void k_pl1_dvec(int64_t n, const double* Ap, const double* Bp, const Pl1Dev* d, double* v) {
+    const double r = d->rho_prev;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        v[i] = Ap[i] - r * Bp[i];
+}
+
+void pl1_begin(Ctl* ctl, cudaStream_t st) { k_pl1_begin<<<1, 1, 0, st>>>(ctl); }
+void pl1_shift_rho(Pl1Dev* d, const double* sc, cudaStream_t st) { k_pl1_shift_rho<<<1, 1, 0, st>>>(d, sc); }
+void pl1_dvec(int64_t n, const double* Ap, const double* Bp, const Pl1Dev* d, double* v, cudaStream_t st) {
+    k_pl1_dvec<<<pl1_grid(n), 256, 0, st>>>(n, Ap, Bp, d, v);
 }
 
 void pl1_dots(const Pl1Pairs& P, int64_t n, double* part, double* out, cudaStream_t st) {

@@ -177,6 +177,7 @@ struct Pl1Dev {
     int nq, fail;               // read together by the host
     int mg;                     // G_k columns built (ctl->k after step 4)
     int has_p;                  // p_k formed (||p~_k||_B > 0)
+    double rho_cur, rho_prev;   // rho(x_k), rho(x_{k-1}) (device copies, so an iteration is a graph)
 };
 struct Pl1Pairs {
     const double* a[4];
@@ -186,7 +187,10 @@ struct Pl1Pairs {
 };
 constexpr int PL1_PART = 296 * 4;  // partials of pl1_dots
 void pl1_prec(const Sell& A, const Sell& B, int64_t n, double sigma, double mfloor, const double* z,
-              const double* s, double rho, double* v, int prec, cudaStream_t st);
+              const double* s, const double* rho, double* v, int prec, cudaStream_t st);
+void pl1_begin(Ctl* ctl, cudaStream_t st);                         // ctl->k = 0, flags = ~0, pass3 = 0
+void pl1_shift_rho(Pl1Dev* d, const double* sc, cudaStream_t st);  // rho_prev = rho_cur; rho_cur = sc1/sc2
+void pl1_dvec(int64_t n, const double* Ap, const double* Bp, const Pl1Dev* d, double* v, cudaStream_t st);
 void pl1_dots(const Pl1Pairs& P, int64_t n, double* part, double* out, cudaStream_t st);
 void pl1_reduce(const double* Hq, const double* Sq, int ldq, int m, Ctl* ctl, int has_p, double* T, int ldT,
                 Pl1Dev* d, cudaStream_t st);
