@@ -80,7 +80,10 @@ struct trplk_ctx {
     double *w = nullptr, *w1 = nullptr, *w2 = nullptr, *u = nullptr, *u2 = nullptr, *xk = nullptr;
     double *T = nullptr, *Yg = nullptr, *part = nullptr, *gpart = nullptr, *red_local = nullptr, *red_all = nullptr;
     double* gridpart = nullptr;
-    unsigned long long* gtrace = nullptr;  // TRPLK_GRID_TRACE: per-step phase timestamps  // all-reduce partials of the grid-wide inner loop (2 x GRID_MAXCTA x GRID_NVP)
+    unsigned long long* gtrace = nullptr;  // TRPLK_GRID_TRACE: per-step phase timestamps
+    cudaEvent_t ctev[2] = {nullptr, nullptr};  // TRPLK_CYCLE_TRACE
+    double ctrace_busy = 0.0;
+    int ctrace_n = 0;  // all-reduce partials of the grid-wide inner loop (2 x GRID_MAXCTA x GRID_NVP)
     double* Wtmp = nullptr;
     unsigned* counter = nullptr;
     Ctl* ctl = nullptr;
@@ -1583,8 +1586,23 @@ static trplk_status solve_impl(trplk_ctx* ctx, int p, int q, int l, double tol, 
             H.rho = rho;
             H.xprev_col = xprev;
             ST(ctl_push(ctx));
+            static const bool ctrace = getenv("TRPLK_CYCLE_TRACE") != nullptr;  // GPU busy vs idle per cycle
+            if (ctrace) {
+                if (!ctx->ctev[0]) {
+                    CK(cudaEventCreate(&ctx->ctev[0]));
+                    CK(cudaEventCreate(&ctx->ctev[1]));
+                }
+                CK(cudaEventRecord(ctx->ctev[0], ctx->stream));
+            }
             ST(run_cycle(ctx, S, cur, nprev, t, xprev, opt.use_graphs != 0));
+            if (ctrace) CK(cudaEventRecord(ctx->ctev[1], ctx->stream));
             ST(ctl_pull(ctx));
+            if (ctrace) {
+                float cms = 0.f;
+                CK(cudaEventElapsedTime(&cms, ctx->ctev[0], ctx->ctev[1]));
+                ctx->ctrace_busy += cms;
+                ctx->ctrace_n++;
+            }
             if (!(H.flags & F_CYCLE)) {  // seed in span(X): inject a stream-2 random vector (R16)
                 if (seed_tries++ >= 3) {
                     ctx->err = "seed vector dependent after 3 random replacements";
@@ -1723,6 +1741,12 @@ static trplk_status solve_impl(trplk_ctx* ctx, int p, int q, int l, double tol, 
     }
 finish:
     pt.mark("cycles");
+    if (ctx->ctrace_n) {
+        fprintf(stderr, "[cycle trace] %d cycles, graph time %.3f ms (%.1f us per cycle)\n", ctx->ctrace_n,
+                ctx->ctrace_busy, 1e3 * ctx->ctrace_busy / ctx->ctrace_n);
+        ctx->ctrace_busy = 0.0;
+        ctx->ctrace_n = 0;
+    }
     if (ctx->gtrace) {  // TRPLK_GRID_TRACE: phase durations (us) of the last grid-path cycle, per step
         unsigned long long tr[64];
         cudaStreamSynchronize(ctx->stream);
