@@ -571,7 +571,12 @@ void launch_eig(Ctl* ctl, double* T, int ldT, double* Y, int ldY, int ph, int k_
         two = e && !strcmp(e, "2b");
         init = 1;
     }
-    if (two) k_eig_2b<<<1, EIG_THREADS, smem, s>>>(ctl, T, ldT, Y, ldY, ph, k_fixed, gate);
+    static const int tri = [] {
+        const char* e = getenv("TRPLK_EIG");
+        return e && !strcmp(e, "tri") ? 1 : 0;
+    }();
+    if (tri) launch_eig_tri(ctl, T, ldT, Y, ldY, ph, k_fixed, ph, gate, s);  // ph > 0: only p^ pairs needed
+    else if (two) k_eig_2b<<<1, EIG_THREADS, smem, s>>>(ctl, T, ldT, Y, ldY, ph, k_fixed, gate);
     else k_eig<<<1, EIG1_THREADS, smem1, s>>>(ctl, T, ldT, Y, ldY, ph, k_fixed, gate);
 }
 

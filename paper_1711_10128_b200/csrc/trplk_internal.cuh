@@ -213,6 +213,10 @@ void launch_sdots(const SdotsArgs& a, int kmax, cudaStream_t s);
 void launch_upd(const UpdArgs& a, int kmax, cudaStream_t s);
 void launch_eig(Ctl* ctl, double* T, int ldT, double* Y, int ldY, int ph, int k_fixed, unsigned gate,
                 cudaStream_t s);
+// TRPLK_EIG=tri: tridiagonalisation + multisection + inverse iteration for the nev lowest pairs
+// (eig_tri.cu); nev <= 0: all k
+void launch_eig_tri(Ctl* ctl, double* T, int ldT, double* Y, int ldY, int ph, int k_fixed, int nev, unsigned gate,
+                    cudaStream_t s);
 void launch_rotate(const double* U, int64_t ldu, int64_t nrows, const Ctl* ctl, int k_fixed,
                    const double* Y, int ldY, int ncol, double* X, int64_t ldx, unsigned gate,
                    cudaStream_t s, int kmax);
