@@ -1,4 +1,3 @@
 mkdir -p gpurun_out/exp
 O=gpurun_out/exp
-TRPLK_EIG=tri TRPLK_EIG_NEV=10 python tools/eig_time.py > $O/eig_tri_clk.txt 2>&1
-TRPLK_EIG=tri python tools/eig_time.py > $O/eig_tri_full.txt 2>&1
+timeout 900 python -m pytest tests/test_gpu_eig_tri.py -m gpu -q -rf --timeout 600 > $O/pytest_tri.log 2>&1; echo "rc=$?" >> $O/pytest_tri.log
