@@ -1953,7 +1953,12 @@ static trplk_status pl1_impl(trplk_ctx* ctx, int m, double tol, int variant, int
             ST(spmv(false, p, Ap));
             if (ctx->hasB) ST(spmv(true, p, Bp));
         }
-        for (int j = 0; j < nc; ++j) {
+        const bool gram1 = pl1_gram(nc, Q, AQ, ctx->hasB ? BQ : nullptr, ld, n, part, Hq, Sq, st);
+        if (gram1) {
+            ctx->launches += 2;
+            ctx->model_bytes += vb * nc * (ctx->hasB ? 3.0 : 2.0);
+        }
+        for (int j = 0; j < nc && !gram1; ++j) {
             if (j == m + 1 && !has_p) continue;
             for (int which = 0; which < 2; ++which) {
                 SdotsArgs a = sd_base(ctx);

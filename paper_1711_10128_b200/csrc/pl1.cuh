@@ -59,6 +59,79 @@ __global__ void k_pl1_dots_fin(Pl1Pairs P, const double* part, int nblk, double*
     out[P.slot[t]] = s;
 }
 
+// Step 5 Gram matrices in one pass: H = Q^T (A Q), S = Q^T (B Q) for the NC columns of Q (upper
+// triangles, thread-per-row register accumulators, fixed-order CTA then grid sums).  BQ = NULL:
+// B = I.  Columns of Q past a breakdown hold finite stale data (their entries are ignored).
+template <int NC>
+__global__ void __launch_bounds__(256) k_pl1_gram(const double* __restrict__ Q, const double* __restrict__ AQ,
+                                                  const double* __restrict__ BQ, int64_t ld, int64_t n,
+                                                  double* part) {
+    constexpr int NT = NC * (NC + 1) / 2;
+    __shared__ double sw[8][2 * NT];
+    double h[NT], s[NT];
+#pragma unroll
+    for (int t = 0; t < NT; ++t) h[t] = s[t] = 0.0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        double q[NC], a[NC], b[NC];
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+            q[c] = Q[i + c * ld];
+            a[c] = AQ[i + c * ld];
+            b[c] = BQ ? BQ[i + c * ld] : q[c];
+        }
+        int t = 0;
+#pragma unroll
+        for (int r = 0; r < NC; ++r)
+#pragma unroll
+            for (int c = r; c < NC; ++c, ++t) {
+                h[t] = fma(q[r], a[c], h[t]);
+                s[t] = fma(q[r], b[c], s[t]);
+            }
+    }
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+    for (int t = 0; t < NT; ++t) {
+        double x = h[t], y = s[t];
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1) {
+            x += __shfl_xor_sync(0xffffffffu, x, o);
+            y += __shfl_xor_sync(0xffffffffu, y, o);
+        }
+        if (lane == 0) {
+            sw[warp][t] = x;
+            sw[warp][NT + t] = y;
+        }
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < 2 * NT; t += blockDim.x) {
+        double x = 0.0;
+        for (int w = 0; w < 8; ++w) x += sw[w][t];
+        part[(int64_t)blockIdx.x * 2 * NT + t] = x;
+    }
+}
+
+// grid sums in CTA order -> H, S (nc x nc, ld nc, mirrored)
+template <int NC>
+__global__ void k_pl1_gram_fin(const double* part, int nblk, double* H, double* S) {
+    constexpr int NT = NC * (NC + 1) / 2;
+    const int t = threadIdx.x;
+    if (t >= 2 * NT) return;
+    double x = 0.0;
+    for (int b = 0; b < nblk; ++b) x += part[(int64_t)b * 2 * NT + t];
+    const int tt = t < NT ? t : t - NT;
+    int r = 0, c = 0, u = 0;
+    for (r = 0; r < NC; ++r) {
+        if (tt < u + NC - r) {
+            c = r + (tt - u);
+            break;
+        }
+        u += NC - r;
+    }
+    double* M = t < NT ? H : S;
+    M[r + NC * c] = x;
+    M[c + NC * r] = x;
+}
+
 // Step 5 (P2, P3): compact the Gram columns of Q = [x, G(:, 0:mg), p] out of the (m+2)-wide
 // H = Q^T A Q and S = Q^T B Q (column-major, ld = ldq), symmetrise, Cholesky S = L L^T with the
 // P3 pivot test (a failing p column is dropped), C = L^-1 H L^-T into T (ld ldT).  One CTA.
@@ -262,6 +335,30 @@ void pl1_reduce(const double* Hq, const double* Sq, int ldq, int m, Ctl* ctl, in
 
 void pl1_scale_p(int64_t n, const double* x, const double* nrm2, double* y, Pl1Dev* d, cudaStream_t st) {
     k_pl1_scale_p<<<pl1_grid(n), 256, 0, st>>>(n, x, nrm2, y, d);
+}
+
+template <int NC>
+static void pl1_gram_k(const double* Q, const double* AQ, const double* BQ, int64_t ld, int64_t n, double* part,
+                       double* H, double* S, cudaStream_t st) {
+    constexpr int NT = NC * (NC + 1) / 2;
+    int g = (int)std::min<int64_t>(PL1_PART / (2 * NT), (n + 255) / 256);
+    if (g > 296) g = 296;
+    if (g < 1) g = 1;
+    k_pl1_gram<NC><<<g, 256, 0, st>>>(Q, AQ, BQ, ld, n, part);
+    k_pl1_gram_fin<NC><<<1, 2 * NT <= 32 ? 32 : ((2 * NT + 31) / 32) * 32, 0, st>>>(part, g, H, S);
+}
+
+bool pl1_gram(int nc, const double* Q, const double* AQ, const double* BQ, int64_t ld, int64_t n, double* part,
+              double* H, double* S, cudaStream_t st) {
+    switch (nc) {
+        case 3: pl1_gram_k<3>(Q, AQ, BQ, ld, n, part, H, S, st); return true;
+        case 4: pl1_gram_k<4>(Q, AQ, BQ, ld, n, part, H, S, st); return true;
+        case 5: pl1_gram_k<5>(Q, AQ, BQ, ld, n, part, H, S, st); return true;
+        case 6: pl1_gram_k<6>(Q, AQ, BQ, ld, n, part, H, S, st); return true;
+        case 7: pl1_gram_k<7>(Q, AQ, BQ, ld, n, part, H, S, st); return true;
+        case 8: pl1_gram_k<8>(Q, AQ, BQ, ld, n, part, H, S, st); return true;
+        default: return false;
+    }
 }
 
 void pl1_back(const double* Y, int ldY, int m, Pl1Dev* d, cudaStream_t st) { k_pl1_back<<<1, 32, 0, st>>>(Y, ldY, m, d); }

@@ -185,7 +185,7 @@ struct Pl1Pairs {
     int slot[4];
     int np;
 };
-constexpr int PL1_PART = 296 * 4;  // partials of pl1_dots
+constexpr int PL1_PART = 296 * 72;  // partials of pl1_dots / pl1_gram (296 CTAs x 2 NT, NC <= 8)
 void pl1_prec(const Sell& A, const Sell& B, int64_t n, double sigma, double mfloor, const double* z,
               const double* s, const double* rho, double* v, int prec, cudaStream_t st);
 void pl1_begin(Ctl* ctl, cudaStream_t st);                         // ctl->k = 0, flags = ~0, pass3 = 0
@@ -196,6 +196,9 @@ void pl1_reduce(const double* Hq, const double* Sq, int ldq, int m, Ctl* ctl, in
                 Pl1Dev* d, cudaStream_t st);
 void pl1_scale_p(int64_t n, const double* x, const double* nrm2, double* y, Pl1Dev* d, cudaStream_t st);
 void pl1_back(const double* Y, int ldY, int m, Pl1Dev* d, cudaStream_t st);
+// H = Q^T A Q, S = Q^T B Q (nc x nc, ld nc) in one pass for 3 <= nc <= 8; false: not handled
+bool pl1_gram(int nc, const double* Q, const double* AQ, const double* BQ, int64_t ld, int64_t n, double* part,
+              double* H, double* S, cudaStream_t st);
 void pl1_xt(int64_t n, const double* x, const double* g, const double* p, const Pl1Dev* d, int m, double* xt,
             cudaStream_t st);
 void pl1_scale(int64_t n, const double* x, const double* nrm2, double* y, cudaStream_t st);
