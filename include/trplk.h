@@ -137,7 +137,9 @@ trplk_status trplk_solve(trplk_ctx* ctx, int p, int max_basis, int k_plus, doubl
  *   step 6  x_{k+1} = Q w / ||Q w||_B, rho_{k+1} = x^T A x / x^T B x, r_{k+1} = (A - rho B) x
  *   step 7  p_k = B-normalised g_k - [p^T(A - rho_{k-1}B)g_k / p^T(A - rho_{k-1}B)p] p_{k-1}
  *           (variant 0, the paper's), or g_k + w(m+2) p_{k-1} (variant 1)
- * until ||r_k||_2 <= tol or max_iter iterations.  One rank (nranks == 1), 1 <= m <= 32.
+ * until ||r_k||_2 <= tol or max_iter iterations.  1 <= m <= 32.  Several ranks: the context's
+ * row slabs, halo exchanges and rank-ordered reductions as trplk_solve (same result on every
+ * rank; x_out holds this rank's rows).
  *   x0          start vector [n_local] (device or host), NULL: x0(i) = u01(seed, 3, i) (R13)
  *   rho         host: final rho_k;  resid: host ||r_k||_2;  x_out [n_local] device or host
  *               (cudaMemcpyDefault) or NULL: the B-normalised x_k

@@ -1861,7 +1861,9 @@ static trplk_status pl1_impl(trplk_ctx* ctx, int m, double tol, int variant, int
         else amv++;
         return TRPLK_OK;
     };
-    auto dots = [&](std::initializer_list<std::pair<std::pair<const double*, const double*>, int>> L) {
+    // several ranks: local sums into red_local (same slots), allgather, rank-ordered sums into sc
+    auto dots = [&](std::initializer_list<std::pair<std::pair<const double*, const double*>, int>> L)
+        -> trplk_status {
         Pl1Pairs P{};
         for (auto& e : L) {
             P.a[P.np] = e.first.first;
@@ -1869,9 +1871,17 @@ static trplk_status pl1_impl(trplk_ctx* ctx, int m, double tol, int variant, int
             P.slot[P.np] = e.second;
             P.np++;
         }
-        pl1_dots(P, n, part, sc, st);
         ctx->launches += 2;
         ctx->model_bytes += 2.0 * vb * P.np;
+        if (ctx->nranks == 1) {
+            pl1_dots(P, n, part, sc, st);
+            return TRPLK_OK;
+        }
+        pl1_dots(P, n, part, ctx->red_local, st);
+        CM(ctx->cm->allgather(ctx->red_local, ctx->red_all, 16, 8, st));
+        pl1_dots_ranks(P, ctx->red_all, ctx->nranks, 16, sc, st);
+        ctx->launches += 1;
+        return TRPLK_OK;
     };
     double h[16];
     auto read_sc = [&]() -> trplk_status {
@@ -1893,13 +1903,13 @@ static trplk_status pl1_impl(trplk_ctx* ctx, int m, double tol, int variant, int
         ST(spmv(true, x, tmp));
         Bxin = tmp;
     }
-    dots({{{x, Bxin}, 0}});
+    ST(dots({{{x, Bxin}, 0}}));
     pl1_scale(n, x, sc + 0, x, st);
     ST(spmv(false, x, Ax));
     if (ctx->hasB) ST(spmv(true, x, Bx));
-    dots({{{x, Ax}, 1}, {{x, Bx}, 2}});
+    ST(dots({{{x, Ax}, 1}, {{x, Bx}, 2}}));
     pl1_res(n, Ax, Bx, sc + 1, sc + 2, r, st);
-    dots({{{r, r}, 3}});
+    ST(dots({{{r, r}, 3}}));
     pl1_shift_rho(dv, sc, st);  // rho_cur = rho_0
     ST(read_sc());
     double rho = h[1] / h[2], res = std::sqrt(h[3]);
@@ -1953,7 +1963,7 @@ static trplk_status pl1_impl(trplk_ctx* ctx, int m, double tol, int variant, int
             ST(spmv(false, p, Ap));
             if (ctx->hasB) ST(spmv(true, p, Bp));
         }
-        const bool gram1 = pl1_gram(nc, Q, AQ, ctx->hasB ? BQ : nullptr, ld, n, part, Hq, Sq, st);
+        const bool gram1 = ctx->nranks == 1 && pl1_gram(nc, Q, AQ, ctx->hasB ? BQ : nullptr, ld, n, part, Hq, Sq, st);
         if (gram1) {
             ctx->launches += 2;
             ctx->model_bytes += vb * nc * (ctx->hasB ? 3.0 : 2.0);
@@ -1986,13 +1996,13 @@ static trplk_status pl1_impl(trplk_ctx* ctx, int m, double tol, int variant, int
             ST(spmv(true, xt, tmp));
             Bxt = tmp;
         }
-        dots({{{xt, Bxt}, 0}});
+        ST(dots({{{xt, Bxt}, 0}}));
         pl1_scale(n, xt, sc + 0, x, st);
         ST(spmv(false, x, Ax));
         if (ctx->hasB) ST(spmv(true, x, Bx));
-        dots({{{x, Ax}, 1}, {{x, Bx}, 2}});
+        ST(dots({{{x, Ax}, 1}, {{x, Bx}, 2}}));
         pl1_res(n, Ax, Bx, sc + 1, sc + 2, r, st);
-        dots({{{r, r}, 3}});
+        ST(dots({{{r, r}, 3}}));
         ctx->launches += 5;
         // step 7 (P4): p~_k and p_k
         const bool conj = has_p && variant == 0;
@@ -2004,7 +2014,7 @@ static trplk_status pl1_impl(trplk_ctx* ctx, int m, double tol, int variant, int
         } else {
             pl1_dvec(n, Ap, Bp, dv, v, st);  // d = (A - rho_{k-1} B) p_{k-1}
             ctx->model_bytes += 3.0 * vb;
-            dots({{{v, g}, 4}, {{v, p}, 5}});
+            ST(dots({{{v, g}, 4}, {{v, p}, 5}}));
             pl1_pt(n, g, p, sc + 4, sc + 5, 1e-14 * ctx->normF, 0, dv, m, pt, st);
         }
         const double* Bpt = pt;
@@ -2013,9 +2023,9 @@ static trplk_status pl1_impl(trplk_ctx* ctx, int m, double tol, int variant, int
             ST(spmv(true, pt, tmp));
             Bpt = tmp;
         }
-        dots({{{pt, Bpt}, 6}});
+        ST(dots({{{pt, Bpt}, 6}}));
         pl1_scale_p(n, pt, sc + 6, p, dv, st);
-        if (conj) dots({{{v, p}, 7}});
+        if (conj) ST(dots({{{v, p}, 7}}));
         pl1_shift_rho(dv, sc, st);
         ctx->launches += 1;
             return TRPLK_OK;
@@ -2023,7 +2033,9 @@ static trplk_status pl1_impl(trplk_ctx* ctx, int m, double tol, int variant, int
         // one CUDA graph per has_p (the only host-side branch of an iteration); counters and
         // byte model recorded at capture and re-added per launch
         const int gi = has_p ? 1 : 0;
-        if (!gexec[gi]) {
+        if (ctx->loopback) {  // loopback exchanges are host rendezvous: eager only
+            ST(issue_iter(has_p));
+        } else if (!gexec[gi]) {
             const double mb0 = ctx->model_bytes;
             const int64_t l0 = ctx->launches, a0 = amv, b0 = bmv;
             cudaGraph_t graph;
@@ -2046,11 +2058,13 @@ static trplk_status pl1_impl(trplk_ctx* ctx, int m, double tol, int variant, int
             amv = a0;
             bmv = b0;
         }
-        CK(cudaGraphLaunch(gexec[gi], st));
-        ctx->model_bytes += gbytes[gi];
-        ctx->launches += glaunch[gi];
-        amv += gamv[gi];
-        bmv += gbmv[gi];
+        if (!ctx->loopback) {
+            CK(cudaGraphLaunch(gexec[gi], st));
+            ctx->model_bytes += gbytes[gi];
+            ctx->launches += glaunch[gi];
+            amv += gamv[gi];
+            bmv += gbmv[gi];
+        }
         // the one host round trip of the iteration: scalars, step-5 status, G_k width, CGS2 passes
         int info[4];
         CK(cudaMemcpyAsync(h, sc, sizeof(h), cudaMemcpyDeviceToHost, st));
@@ -2106,8 +2120,8 @@ trplk_status trplk_pl1_solve(trplk_ctx* ctx, int m, double tol, int variant, int
                              int log_cap, double* log_rho, double* log_res, double* log_conj, int* log_len,
                              trplk_stats* stats) {
     if (!ctx) return TRPLK_EINVAL;
-    if (ctx->nranks != 1 || m < 1 || m > 32 || !(tol > 0.0) || max_iter < 0 || (variant != 0 && variant != 1)) {
-        ctx->err = "PL+1: needs one rank, 1 <= m <= 32, tol > 0, max_iter >= 0, variant 0/1";
+    if (m < 1 || m > 32 || !(tol > 0.0) || max_iter < 0 || (variant != 0 && variant != 1)) {
+        ctx->err = "PL+1: needs 1 <= m <= 32, tol > 0, max_iter >= 0, variant 0/1";
         return TRPLK_EINVAL;
     }
     enter_stream(ctx);

@@ -59,6 +59,15 @@ __global__ void k_pl1_dots_fin(Pl1Pairs P, const double* part, int nblk, double*
     out[P.slot[t]] = s;
 }
 
+// several ranks: out[slot] = sum over ranks (in rank order) of the gathered local sums
+__global__ void k_pl1_dots_ranks(Pl1Pairs P, const double* all, int nranks, int stride, double* out) {
+    const int t = threadIdx.x;
+    if (t >= P.np) return;
+    double s = 0.0;
+    for (int r = 0; r < nranks; ++r) s += all[(int64_t)r * stride + P.slot[t]];
+    out[P.slot[t]] = s;
+}
+
 // Step 5 Gram matrices in one pass: H = Q^T (A Q), S = Q^T (B Q) for the NC columns of Q (upper
 // triangles, thread-per-row register accumulators, fixed-order CTA then grid sums).  BQ = NULL:
 // B = I.  Columns of Q past a breakdown hold finite stale data (their entries are ignored).
@@ -326,6 +335,10 @@ void pl1_dots(const Pl1Pairs& P, int64_t n, double* part, double* out, cudaStrea
     if (g < 1) g = 1;
     k_pl1_dots<<<g, 256, 0, st>>>(P, n, part);
     k_pl1_dots_fin<<<1, 32, 0, st>>>(P, part, g, out);
+}
+
+void pl1_dots_ranks(const Pl1Pairs& P, const double* all, int nranks, int stride, double* out, cudaStream_t st) {
+    k_pl1_dots_ranks<<<1, 32, 0, st>>>(P, all, nranks, stride, out);
 }
 
 void pl1_reduce(const double* Hq, const double* Sq, int ldq, int m, Ctl* ctl, int has_p, double* T, int ldT,

@@ -192,6 +192,7 @@ void pl1_begin(Ctl* ctl, cudaStream_t st);                         // ctl->k = 0
 void pl1_shift_rho(Pl1Dev* d, const double* sc, cudaStream_t st);  // rho_prev = rho_cur; rho_cur = sc1/sc2
 void pl1_dvec(int64_t n, const double* Ap, const double* Bp, const Pl1Dev* d, double* v, cudaStream_t st);
 void pl1_dots(const Pl1Pairs& P, int64_t n, double* part, double* out, cudaStream_t st);
+void pl1_dots_ranks(const Pl1Pairs& P, const double* all, int nranks, int stride, double* out, cudaStream_t st);
 void pl1_reduce(const double* Hq, const double* Sq, int ldq, int m, Ctl* ctl, int has_p, double* T, int ldT,
                 Pl1Dev* d, cudaStream_t st);
 void pl1_scale_p(int64_t n, const double* x, const double* nrm2, double* y, Pl1Dev* d, cudaStream_t st);

@@ -98,3 +98,54 @@ def test_loopback_ranks_match_one_rank(gen, orc, name, N, nranks):
         M = X[:, g].T @ (X1h[:, g] if B is None else B @ X1h[:, g])
         s = np.linalg.svd(M, compute_uv=False)
         assert np.min(s) >= 1 - 1e-8, (g, s)
+
+
+def _pl1_rank(trplk, inputs, name, N, hub, rank, nranks, out, m):
+    import torch
+    torch.cuda.set_device(0)
+    P0 = inputs.make(name, N=N)
+    n = P0.A.n
+    plane = 1 if P0.grid["dim"] == 1 else N * N
+    rb, re = inputs.slab_rows(n, nranks, rank, plane)
+    P = inputs.make(name, N=N, row_begin=rb, row_end=re)
+    try:
+        ctx = trplk.trplk_create(P.A, P.B, P.sigma, n_global=n, row_begin=rb, row_end=re,
+                                 loopback=(hub, rank, nranks))
+        rho, res, x, st, log = trplk.trplk_pl1_solve(ctx, m, P.tol)
+        out[rank] = {"rho": rho, "res": res, "x": x.cpu().numpy().copy(), "st": st, "log": log}
+        ctx.close()
+    except Exception as e:  # reported by the main thread
+        out[rank] = e
+
+
+@pytest.mark.parametrize("name,N,nranks", [("C2", 16, 2), ("C4", 10, 2), ("C2", 16, 4)])
+def test_pl1_loopback_ranks(gen, orc, name, N, nranks):
+    """PL+1 on z-slab ranks (loopback hub): every rank reports the same rho / iterations; the
+    same iteration and A-matvec counts as the oracle; gathered x = the oracle's x."""
+    torch, trplk = need_gpu()
+    m = 4
+    hub = trplk.trplk_loopback_create(nranks)
+    out = [None] * nranks
+    th = [threading.Thread(target=_pl1_rank, args=(trplk, gen, name, N, hub, r, nranks, out, m))
+          for r in range(nranks)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=600)
+    assert not any(t.is_alive() for t in th)
+    trplk.trplk_loopback_destroy(hub)
+    for o in out:
+        if isinstance(o, Exception):
+            raise o
+    for o in out[1:]:
+        assert o["rho"] == out[0]["rho"] and o["st"]["cycles"] == out[0]["st"]["cycles"]
+    P = gen.make(name, N=N)
+    r = orc.pl1_solve(P.A, P.B, m=m, tol=P.tol, sigma=P.sigma)
+    o0 = out[0]
+    assert o0["st"]["status"] == "OK" and r["status"] == "OK"
+    assert o0["st"]["cycles"] == r["cycles"] and o0["st"]["a_matvecs"] == r["a_matvecs"]
+    assert abs(o0["rho"] - r["rho"]) <= 1e-12 * abs(r["rho"])
+    x = np.concatenate([o["x"] for o in out])
+    B = None if P.B is None else P.B.to_scipy()
+    Bx = x if B is None else B @ x
+    assert abs(abs(Bx @ r["x"]) - 1) <= 1e-8
