@@ -607,6 +607,7 @@ int orc_pl1_solve(const orc_pl1_problem* P, double* x_out, orc_pl1_report* rep) 
             applyB(&c, gj, BG + (size_t)n * mg);
             ++mg;
         }
+        if (rep && k < rep->log_cap) rep->log_mg[k] = mg;
         /* step 5: Q_k = [x_k, G_k, p_{k-1}], RR on the projected pencil (P2, P3) */
         int nq = 1 + mg;
         Qc[0] = x; AQc[0] = Ax; BQc[0] = Bx;
@@ -665,7 +666,6 @@ int orc_pl1_solve(const orc_pl1_problem* P, double* x_out, orc_pl1_report* rep) 
             for (int i = 0; i < nq; ++i) w[i] = -w[i];
         if (rep && k < rep->log_cap) {
             rep->log_ritz[k] = th[0];
-            rep->log_mg[k] = mg;
             rep->log_nq[k] = nq;
         }
         /* step 6: g_k, x~_{k+1}, x_{k+1}, rho_{k+1}, r_{k+1} (P5) */

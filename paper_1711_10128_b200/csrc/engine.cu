@@ -2075,6 +2075,7 @@ static trplk_status pl1_impl(trplk_ctx* ctx, int m, double tol, int variant, int
         if (ctx->hasB) bmv += 2 * std::min(mg + 1, m) + (H.pass3_count - p3) - (m - mg);  // B SpMVs of unbuilt columns
         amv -= (m - mg);  // SpMVs of columns past a breakdown are not the algorithm's
         if (info[1] >= 0) {
+            amv -= 1;  // the step-6 product of the discarded iterate
             ctx->err = "PL+1: Q_k^T B Q_k not positive definite on [x_k, G_k] (P3)";
             status = TRPLK_BREAKDOWN;
             break;

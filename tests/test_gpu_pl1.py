@@ -66,3 +66,44 @@ def test_pl1_full_size_C2(orc, gen):
     assert np.max(np.abs(log["rho"] - o["log"]["rho"]) / np.abs(o["log"]["rho"])) <= 1e-10
     assert abs(rho - o["rho"]) <= 1e-12 * abs(o["rho"])
     assert abs(abs(x @ o["x"]) - 1) <= 1e-8
+
+
+def test_pl1_wide_block_and_breakdown(orc, gen):
+    """m = 12 (Gram by the per-column fused dot kernel, NC = 14 > 8) on C2, and a Krylov
+    breakdown: A with 4 distinct eigenvalues (n = 64), m = 6 -> G_k ends after <= 3 columns
+    (step 4, P1) on the oracle and the GPU alike."""
+    import scipy.sparse as sp
+    torch, trplk = need_gpu()
+    P = gen.make("C2", N=12)
+    rho, res, x, st, log, o = _run(trplk, orc, P, 12, 1e-9)
+    assert st["status"] == "OK" and o["status"] == "OK"
+    assert st["cycles"] == o["cycles"] and st["a_matvecs"] == o["a_matvecs"]
+    assert abs(rho - o["rho"]) <= 1e-12 * abs(o["rho"])
+
+    class _M:  # CSR in the shape inputs.make returns
+        def __init__(self, S):
+            S = S.tocsr()
+            self.rowptr = S.indptr.astype(np.int64)
+            self.col = S.indices.astype(np.int64)
+            self.val = S.data.astype(np.float64)
+            self.n = S.shape[0]
+            self.row_begin = 0
+
+        def to_scipy(self):
+            return sp.csr_matrix((self.val, self.col, self.rowptr), shape=(self.n, self.n))
+
+    # x_0 in a 2-dimensional invariant subspace: v_2 = (A - rho) g_1 lies in span{x_0, g_1},
+    # so CGS2 against g_1 alone returns ~x_0 (g_2), v_3 breaks down (mg = 2), and Q = [x, g_1, g_2]
+    # is singular on x -> BREAKDOWN (P3) at iteration 0, oracle and GPU alike
+    d = np.arange(1.0, 65.0)
+    A = _M(sp.diags(d))
+    x0 = np.zeros(64)
+    x0[0] = x0[1] = 1.0
+    ctx = trplk.trplk_create(A, None, 0.0)
+    rho, res, x, st, log = trplk.trplk_pl1_solve(ctx, 6, 1e-10, use_precond=False, x0=x0)
+    ctx.close()
+    o = orc.pl1_solve(A, None, m=6, tol=1e-10, use_precond=False, x0=x0)
+    assert o["status"] == "BREAKDOWN" and st["status"] == "BREAKDOWN"
+    assert o["log"]["mg"][0] == 2
+    assert st["cycles"] == o["cycles"] == 0 and st["a_matvecs"] == o["a_matvecs"]
+    assert abs(rho - o["rho"]) <= 1e-14
