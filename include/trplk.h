@@ -109,7 +109,10 @@ trplk_status trplk_nccl_unique_id(void* out, size_t out_bytes);
  * b_*: same for B, or all three NULL for B = I.  Every row must store its diagonal
  * entry (it may be zero).  Errors: EINVAL for a row range that does not tile n,
  * column ids out of range / not strictly increasing, q limits; ECUDA/ENCCL/ENOMEM.
- * The matrices are converted to SELL-32 (diagonal first) in device memory. */
+ * Device formats: DIA (values per diagonal offset) when the local rows hold <= 32 distinct
+ * offsets with <= 25 % padding and a contiguous ghost tail (stencils), else SELL-32 (diagonal
+ * first).  Create is one parallel scan of the CSR; pinned host arrays are copied and scattered
+ * into DIA on the device, pageable ones on the host. */
 trplk_status trplk_create(trplk_ctx** out, int64_t n_global,
                           const int64_t* a_rowptr, const int64_t* a_col, const double* a_val,
                           const int64_t* b_rowptr, const int64_t* b_col, const double* b_val,
