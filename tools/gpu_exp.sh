@@ -1,3 +1,6 @@
 mkdir -p gpurun_out/exp
 O=gpurun_out/exp
-timeout 900 python -m pytest tests/test_gpu_pl1.py -m gpu -q -rf --timeout 300 -k wide > $O/pytest_pl1w.log 2>&1; echo "pytest rc=$?" >> $O/pytest_pl1w.log
+timeout 1800 python -m pytest tests -m gpu -q -rf --timeout 600 > $O/pytest_all.log 2>&1; echo "pytest rc=$?" >> $O/pytest_all.log
+python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke rc=$?" >> $O/smoke.log
+python bench.py > $O/bench_default.json 2> $O/bench_default.err
+python bench.py --method pl1 > $O/bench_pl1_C2.json 2> $O/bench_pl1.err
