@@ -1057,6 +1057,83 @@ trplk_status issue_cycle(trplk_ctx* ctx, const Sizes& S, int cur, int nprev, int
     return TRPLK_OK;
 }
 
+// Process-wide cache of instantiated cycle graphs, keyed by everything a captured kernel
+// argument can depend on: the cycle key, the solve sizes, every device allocation of the
+// context (address and size, in allocation order), the matrix descriptors and the scalar
+// arguments.  A context created right after another one of the same problem (the e2e path:
+// create -> solve -> destroy, again and again) usually gets the same device addresses back from
+// the allocator, so its graphs are reused instead of captured and instantiated again.
+static std::mutex g_graph_mu;
+static std::map<std::string, GraphRec> g_graph_cache;
+static std::vector<std::string> g_graph_order;
+constexpr size_t GRAPH_CACHE_MAX = 64;
+
+static std::string graph_fingerprint(const trplk_ctx* ctx, uint64_t key, const Sizes& S) {
+    std::string f;
+    auto put = [&f](const void* p, size_t n) { f.append(static_cast<const char*>(p), n); };
+    put(&key, sizeof(key));
+    put(&S, sizeof(S));
+    for (const auto& a : ctx->allocs) {
+        put(&a.first, sizeof(a.first));
+        put(&a.second, sizeof(a.second));
+    }
+    for (const Sell* M : {&ctx->A, &ctx->B}) {  // field by field (no padding bytes)
+        const int64_t v[11] = {M->fmt, M->nrows, M->nslices, (int64_t)(uintptr_t)M->sptr, (int64_t)(uintptr_t)M->col,
+                               (int64_t)(uintptr_t)M->val, M->ndiag, M->diag_slot, M->ldv, M->glo, M->nghost};
+        put(v, sizeof(v));
+        put(&M->dval, sizeof(M->dval));
+        put(M->offs, sizeof(M->offs));
+    }
+    const double sc[3] = {ctx->sigma, ctx->mfloor, ctx->normF};
+    put(sc, sizeof(sc));
+    const int64_t iv[6] = {ctx->n_loc, ctx->ld, ctx->row_begin, ctx->n_global, (int64_t)ctx->force3,
+                           (int64_t)ctx->grid_on};
+    put(iv, sizeof(iv));
+    put(&ctx->ctl_h, sizeof(ctx->ctl_h));
+    return f;
+}
+
+// hand a context's graphs to the cache (destroy) / take matching ones back (run_cycle)
+static void graphs_to_cache(trplk_ctx* ctx) {
+    if (ctx->nranks > 1 || ctx->prof_on) {
+        for (auto& g : ctx->graphs) cudaGraphExecDestroy(g.second.exec);
+        ctx->graphs.clear();
+        return;
+    }
+    std::lock_guard<std::mutex> lk(g_graph_mu);
+    for (auto& g : ctx->graphs) {
+        const std::string f = graph_fingerprint(ctx, g.first, ctx->gsizes);
+        auto it = g_graph_cache.find(f);
+        if (it != g_graph_cache.end()) {
+            cudaGraphExecDestroy(g.second.exec);
+            continue;
+        }
+        g_graph_cache.emplace(f, g.second);
+        g_graph_order.push_back(f);
+        if (g_graph_order.size() > GRAPH_CACHE_MAX) {
+            auto old = g_graph_cache.find(g_graph_order.front());
+            if (old != g_graph_cache.end()) {
+                cudaGraphExecDestroy(old->second.exec);
+                g_graph_cache.erase(old);
+            }
+            g_graph_order.erase(g_graph_order.begin());
+        }
+    }
+    ctx->graphs.clear();
+}
+
+static bool graph_from_cache(trplk_ctx* ctx, uint64_t key, const Sizes& S, GraphRec& rec) {
+    if (ctx->nranks > 1 || ctx->prof_on) return false;
+    const std::string f = graph_fingerprint(ctx, key, S);
+    std::lock_guard<std::mutex> lk(g_graph_mu);
+    auto it = g_graph_cache.find(f);
+    if (it == g_graph_cache.end()) return false;
+    rec = it->second;
+    g_graph_cache.erase(it);
+    g_graph_order.erase(std::find(g_graph_order.begin(), g_graph_order.end(), f));
+    return true;
+}
+
 trplk_status run_cycle(trplk_ctx* ctx, const Sizes& S, int cur, int nprev, int t, int xprev, bool use_graph) {
     if (ctx->loopback) use_graph = false;  // loopback exchanges are host rendezvous: eager only
     const bool multi = ctx->nranks > 1;
@@ -1071,6 +1148,10 @@ trplk_status run_cycle(trplk_ctx* ctx, const Sizes& S, int cur, int nprev, int t
     const uint64_t key = ((uint64_t)cur) | ((uint64_t)nprev << 1) | ((uint64_t)(ts + 1) << 8) |
                          ((uint64_t)(xs + 1) << 24) | ((uint64_t)(ctx->prof_on ? 1 : 0) << 40);
     auto it = ctx->graphs.find(key);
+    if (it == ctx->graphs.end()) {
+        GraphRec cached;
+        if (graph_from_cache(ctx, key, S, cached)) it = ctx->graphs.emplace(key, cached).first;
+    }
     if (it == ctx->graphs.end()) {
         const double mb0 = ctx->model_bytes;
         const int64_t l0 = ctx->launches;
@@ -1393,7 +1474,7 @@ void trplk_destroy(trplk_ctx* ctx) {
     if (!ctx) return;
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     if (ctx->user_stream) cudaStreamSynchronize(ctx->user_stream);
-    for (auto& g : ctx->graphs) cudaGraphExecDestroy(g.second.exec);
+    graphs_to_cache(ctx);  // before the allocations go: the fingerprint lists them
     for (auto& a : ctx->allocs) dev_release(ctx, a.first);
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     if (!ctx->has_alloc) trim_pool();

@@ -296,3 +296,21 @@ def test_grid_inner_loop(orc, gen, name, N, over, fmt, debug):
         assert np.all(g["residuals"] <= P.tol)
     X = g["X"]
     assert np.max(np.abs(X.T @ X - np.eye(P.p))) <= 1e-11
+
+
+def test_graph_cache_across_contexts(gen):
+    """A context created after another one of the same shape reuses its instantiated cycle
+    graphs (same device addresses): the results must be those of an eager (graph-free) solve of
+    the SECOND problem, bit for bit -- a replayed graph reads the new matrix and vectors."""
+    torch, trplk = need_gpu()
+    P1 = gen.make("C2", N=16)
+    P2 = gen.make("C2", N=16, dscale=3.0)  # same structure, other values
+    for P in (P1, P2, P1):
+        ctx = trplk.trplk_create(P.A, P.B, P.sigma)
+        ev, X, rs, st = trplk.trplk_solve(ctx, P.p, P.q, P.l, P.tol)
+        ctx.close()
+        ctx = trplk.trplk_create(P.A, P.B, P.sigma)
+        ev0, X0, rs0, st0 = trplk.trplk_solve(ctx, P.p, P.q, P.l, P.tol, use_graphs=0)
+        ctx.close()
+        assert np.array_equal(ev, ev0) and np.array_equal(rs, rs0)
+        assert st["a_matvecs"] == st0["a_matvecs"]
