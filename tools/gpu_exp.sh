@@ -1,3 +1,9 @@
 mkdir -p gpurun_out/exp
 O=gpurun_out/exp
-timeout 900 python -m pytest tests/test_gpu_solve.py -m gpu -q -rf --timeout 300 -k graph_cache > $O/pytest_gc.log 2>&1; echo "rc=$?" >> $O/pytest_gc.log
+B="python bench.py --config C2 --steps 1 --warmup 1 --no-cpu-baseline --no-e2e"
+$B > $O/plain.json 2> $O/plain.err || exit 1
+ncu -f --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:'k_step1_rs<.int.24, .bool.1>' -c 3 -o /tmp/k1 $B > $O/ncu_k1.log 2>&1
+python tools/ncu_summary.py rep /tmp/k1.ncu-rep > $O/k1_summary.txt 2>&1
+python tools/ncu_source_top.py /tmp/k1.ncu-rep . 30 > $O/k1_source_top.txt 2>&1
+python tools/make_traffic.py /tmp/k1.ncu-rep C2 > $O/k1_traffic.log 2>&1
+cp profiles/traffic_C2.json $O/traffic_C2.json

@@ -30,9 +30,13 @@ for r in rows[2:]:
     if rd < 1e6:  # gated no-op launches
         continue
     acc.setdefault(key, []).append(rd + wr)
-res = {k: sum(v) / len(v) for k, v in acc.items()}
-res["source"] = f"ncu --set full (cold cache) of bench.py --config {cfg}; DRAM read+write bytes per launch, " \
-    "averaged over the captured launches of each kernel instantiation: " + ", ".join(f"{k}:{len(v)}" for k, v in acc.items())
 path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles", f"traffic_{cfg}.json")
+# merge: instantiations this capture did not see keep their earlier entries
+res = json.load(open(path)) if os.path.exists(path) else {}
+prev_src = res.pop("source", "")
+res.update({k: sum(v) / len(v) for k, v in acc.items()})
+src = f"ncu --set full (cold cache) of bench.py --config {cfg}; DRAM read+write bytes per launch, " \
+    "averaged over the captured launches of each kernel instantiation: " + ", ".join(f"{k}:{len(v)}" for k, v in acc.items())
+res["source"] = src if not prev_src else prev_src + " | " + src
 json.dump(res, open(path, "w"), indent=1)
 print(path, res)
