@@ -1,6 +1,8 @@
 mkdir -p gpurun_out/exp
 O=gpurun_out/exp
-for E in TRPLK_NO_COOP3=1 TRPLK_NO_SMALL=1 TRPLK_GRID=1 TRPLK_KVAR=tp TRPLK_K2=rs; do
-  echo "== $E" >> $O/alt.log
-  env $E timeout 900 python -m pytest tests/test_gpu_solve.py tests/test_gpu_multirank.py -m gpu -q -x --timeout 300 2>&1 | tail -2 >> $O/alt.log
+rm -f $O/var.txt
+for i in 1 2 3 4 5; do
+python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-e2e 2>/dev/null | python -c "
+import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); r=d['roofline']
+print(d['ms_per_step'], d['value'], r['ms_per_launch']*1e3, r['frac'], d['clocks']['sm_mhz'])" >> $O/var.txt
 done
