@@ -1649,6 +1649,7 @@ static trplk_status solve_impl(trplk_ctx* ctx, int p, int q, int l, double tol, 
         ctx->prec++;
         ST(ctl_pull(ctx));
         ctx->b_mv += ctx->hasB ? H.pass3_count - p3_start : 0;
+        pt.mark("start block");
     }
     {
         int t = 1, nprev = 0, xprev = 0;
