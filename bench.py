@@ -324,7 +324,7 @@ def main():
     value = mv / (ms_per_step / 1e3)
 
     # roofline: inner-step kernel group with the largest share (live CUDA events, per launch)
-    names = ["K1 (k_step1_rs: SpMV + Jacobi + T-column / h1 dots)",
+    names = ["K1 (k_step1_rs2: SpMV + Jacobi + T-column / h1 dots)",
              "K2 (CGS pass 2: k_upd2_wp update + dots; B != I: the B-SpMV dot passes too)",
              "K3 (k_upd FINAL update + normalisation)"]
     peak, peak_src = peaks()
@@ -346,7 +346,7 @@ def main():
         tj = json.load(open(tfile))
         # K1 runs k_step1_rs (or the pipelined k_step1_pipe on long slabs), K2 the warp-group
         # k_upd2_wp<KS, G>, K3 k_upd<KMAX, 0>
-        want = [(f"k_step1_rs<{bucket}, 1>", f"k_step1_pipe<{bucket}, 1>"), ("k_upd2_wp<",),
+        want = [(f"k_step1_rs2<{bucket}, 1>", f"k_step1_pipe<{bucket}, 1>"), ("k_upd2_wp<",),
                 (f"k_upd<{bucket}, 0>",)][kd]
         for key in tj:
             if key != "source" and any(key.startswith(w) for w in want):

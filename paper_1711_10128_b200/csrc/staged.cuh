@@ -436,6 +436,159 @@ __global__ void __launch_bounds__(CTA, 2) k_step1_rs(const SdotsArgs a) {
     }
 }
 
+// K1 with two 32-row tiles per warp per iteration (default; TRPLK_RS1=1 selects the one-tile
+// k_step1_rs): the loads of both tiles (basis rows, DIA values, gathers) are in flight
+// together, so a warp walks half as many dependent load round trips; 8-column slab chunks,
+// one slab per tile.  C2: K1 24.5 -> 22.6 us, solve -2.7 %; C3: K1 145 -> 135 us, -2.9 %.
+template <int KMAX, bool TWO>
+__global__ void __launch_bounds__(CTA, 2) k_step1_rs2(const SdotsArgs a) {
+    Ctl* ctl = a.ctl;
+    if ((ctl->flags & a.gate) != a.gate) return;
+    if (a.gate_pass3 && ctl->pass3 == 0) return;
+    const int kc = ctl->k;
+    const int k1 = a.set1 ? (a.k_from_ctl ? kc : a.k1) : 0;
+    const int k2 = (TWO && a.set2) ? (a.k_from_ctl ? kc : a.k2) : 0;
+    const int kmx = k1 > k2 ? k1 : k2;
+    const double rho = ctl->rho;
+    const int nn = (a.norm1 ? 1 : 0) + (a.norm2 ? 1 : 0);
+    const int nv = k1 + k2 + nn;
+    const double* __restrict__ X = a.x;
+    constexpr int CH = 8;
+    extern __shared__ __align__(128) double wsm[];  // WARPS x 2 x CH x WLD
+    __shared__ double acc[WARPS][NV_MAX];
+    __shared__ double res[NV_MAX];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int fi = lane >> 2, fj = lane & 3;
+    double* W0 = wsm + (size_t)warp * 2 * CH * WLD;
+    double* W1 = W0 + CH * WLD;
+    double cacc[KMAX / 8][2];
+#pragma unroll
+    for (int g = 0; g < KMAX / 8; ++g) cacc[g][0] = cacc[g][1] = 0.0;
+    double n1 = 0.0;
+    const int64_t nslices = (a.nrows + 31) >> 5;
+    const int64_t npairs = (nslices + 1) >> 1;
+    auto tile = [&](int64_t sl, bool live, double& v1, double& o) {
+        const int64_t row = sl * 32 + lane;
+        const bool ok = live && row < a.nrows;
+        double z = 0.0, ad = 1.0, bd = 1.0, sv = 0.0;
+        o = 0.0;
+        const double xr = ok ? X[row] : 0.0;
+        if (live) {
+            z = mat_row(a.A, sl, lane, X, ad);
+            if (a.out_mode == 2) {
+                if (a.B.nrows) sv = mat_row(a.B, sl, lane, X, bd);
+                else sv = xr;
+                double d = fabs(ad - a.sigma * bd);
+                d = d > a.mfloor ? d : a.mfloor;
+                o = (1.0 / d) * (z - rho * sv);  // w = M (z - rho B g), R1
+            } else if (a.out_mode == 1) {
+                o = z;
+            }
+        }
+        if (ok) {
+            if (a.out) a.out[row] = o;
+        } else {
+            z = 0.0;
+            o = 0.0;
+        }
+        if (a.norm1 == 1) n1 += o * o;
+        else if (a.norm1 == 2) n1 += xr * z;
+        v1 = a.set1 == 1 ? z : o;
+    };
+    for (int64_t pr = (int64_t)blockIdx.x * WARPS + warp; pr < npairs; pr += (int64_t)gridDim.x * WARPS) {
+        const int64_t s0 = 2 * pr, s1 = 2 * pr + 1;
+        const bool has1 = s1 < nslices;
+        const int64_t r0 = s0 * 32 + lane, r1 = s1 * 32 + lane;
+        const bool ok0 = r0 < a.nrows, ok1 = has1 && r1 < a.nrows;
+        const double* up0 = a.U + r0;
+        const double* up1 = a.U + r1;
+        double u0[CH], u1[CH];
+#pragma unroll
+        for (int c = 0; c < CH; ++c) {
+            u0[c] = (ok0 && c < kmx) ? __ldg(up0 + (int64_t)c * a.ldu) : 0.0;
+            u1[c] = (ok1 && c < kmx) ? __ldg(up1 + (int64_t)c * a.ldu) : 0.0;
+        }
+        double va, oa, vb, ob;
+        tile(s0, true, va, oa);
+        tile(s1, has1, vb, ob);
+        double bq0[8], bq1[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const double t1 = __shfl_sync(0xffffffffu, va, 4 * q + fj);
+            const double t2 = TWO ? __shfl_sync(0xffffffffu, oa, 4 * q + fj) : 0.0;
+            bq0[q] = fi == 0 ? t1 : (fi == 1 ? t2 : 0.0);
+            const double t3 = __shfl_sync(0xffffffffu, vb, 4 * q + fj);
+            const double t4 = TWO ? __shfl_sync(0xffffffffu, ob, 4 * q + fj) : 0.0;
+            bq1[q] = fi == 0 ? t3 : (fi == 1 ? t4 : 0.0);
+        }
+        __syncwarp();
+#pragma unroll
+        for (int c = 0; c < CH; ++c) {
+            W0[c * WLD + lane] = u0[c];
+            W1[c * WLD + lane] = u1[c];
+        }
+        __syncwarp();
+#pragma unroll
+        for (int cb = 0; cb < KMAX; cb += CH) {
+            const bool more = cb + CH < KMAX && cb + CH < kmx;
+            if (more) {
+#pragma unroll
+                for (int c = 0; c < CH; ++c) {
+                    const int cc = cb + CH + c;
+                    u0[c] = (ok0 && cc < kmx) ? __ldg(up0 + (int64_t)cc * a.ldu) : 0.0;
+                    u1[c] = (ok1 && cc < kmx) ? __ldg(up1 + (int64_t)cc * a.ldu) : 0.0;
+                }
+            }
+            if (cb < kmx) {
+                const double* sp0 = W0 + fi * WLD + fj;
+                const double* sp1 = W1 + fi * WLD + fj;
+#pragma unroll
+                for (int q = 0; q < 8; ++q) dmma884_s(cacc[cb / 8], sp0[4 * q], bq0[q]);
+#pragma unroll
+                for (int q = 0; q < 8; ++q) dmma884_s(cacc[cb / 8], sp1[4 * q], bq1[q]);
+            }
+            if (more) {
+                __syncwarp();
+#pragma unroll
+                for (int c = 0; c < CH; ++c) {
+                    W0[c * WLD + lane] = u0[c];
+                    W1[c * WLD + lane] = u1[c];
+                }
+                __syncwarp();
+            }
+        }
+    }
+    for (int i = threadIdx.x; i < WARPS * NV_MAX; i += CTA) (&acc[0][0])[i] = 0.0;
+    __syncthreads();
+    if (fj == 0) {
+#pragma unroll
+        for (int g = 0; g < KMAX / 8; ++g) {
+            const int c = 8 * g + fi;
+            if (c < k1) acc[warp][c] = cacc[g][0];
+            if (TWO && c < k2) acc[warp][k1 + c] = cacc[g][1];
+        }
+    }
+    if (nn) {
+        const double s1 = warp_sum_s(n1);
+        if (lane == 0) acc[warp][k1 + k2] = s1;
+    }
+    if (nv == 0) return;
+    __syncthreads();
+    for (int v = threadIdx.x; v < nv; v += CTA) {
+        double s = 0.0;
+#pragma unroll
+        for (int w = 0; w < WARPS; ++w) s += acc[w][v];
+        res[v] = s;
+    }
+    __syncthreads();
+    if (!grid_reduce(res, nv, a.part, a.gpart, a.counter, a.maxcta, res)) return;
+    if (a.red_local) {
+        for (int v = threadIdx.x; v < nv; v += CTA) a.red_local[v] = res[v];
+    } else {
+        sdots_finalize(a, res, k1, k2);
+    }
+}
+
 template <int KMAX>
 __global__ void __launch_bounds__(CTA, 2) k_upd2_rs(const UpdArgs a) {
     Ctl* ctl = a.ctl;
@@ -593,6 +746,13 @@ static int rs_grid(K kern, int smem, int64_t nrows) {
 
 template <int KMAX, bool TWO>
 static void launch_step1_rs_k(const SdotsArgs& a, cudaStream_t s) {
+    static const bool two_tiles = !(getenv("TRPLK_RS1") && getenv("TRPLK_RS1")[0] == '1');
+    if (two_tiles) {
+        const int smem2 = WARPS * 2 * 8 * WLD * (int)sizeof(double);
+        auto kern2 = k_step1_rs2<KMAX, TWO>;
+        kern2<<<rs_grid(kern2, smem2, (a.nrows + 1) / 2), CTA, smem2, s>>>(a);
+        return;
+    }
     const int smem = WARPS * rs_chunk(KMAX) * WLD * (int)sizeof(double);
     auto kern = k_step1_rs<KMAX, TWO>;
     kern<<<rs_grid(kern, smem, a.nrows), CTA, smem, s>>>(a);
