@@ -431,8 +431,111 @@ __global__ void __launch_bounds__(CTA, 2) k_upd2_wp(const UpdArgs a) {
     }
 }
 
+// k_upd2_wp with two 32-row tiles per warp-group iteration (default; TRPLK_WP1=1 for one):
+// both tiles' column loads in flight together, one group barrier for both, half the dependent
+// load round trips per warp (as k_step1_rs2 for K1).
+template <int KS, int G>
+__global__ void __launch_bounds__(CTA, 2) k_upd2_wp2(const UpdArgs a) {
+    constexpr int NGR = WARPS / G;
+    Ctl* ctl = a.ctl;
+    if ((ctl->flags & a.gate) != a.gate) return;
+    const int kv = a.kv >= 0 ? a.kv : ctl->k;
+    const double* __restrict__ X = resolve_x(a.x, a.x_dyn, a.x_ld, a.x_off, ctl);
+    __shared__ double hs[G * KS];
+    __shared__ double sb[2][NGR][G][64];
+    __shared__ double acc[WARPS][QMAX + 1];
+    __shared__ double res[QMAX + 1];
+    for (int i = threadIdx.x; i < G * KS; i += CTA) hs[i] = i < kv ? ctl->h[a.hslot][i] : 0.0;
+    for (int i = threadIdx.x; i < WARPS * (QMAX + 1); i += CTA) (&acc[0][0])[i] = 0.0;
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int grp = warp / G, wg = warp % G;
+    const int c0 = wg * KS;
+    double d[KS];
+#pragma unroll
+    for (int c = 0; c < KS; ++c) d[c] = 0.0;
+    double yy = 0.0;
+    const int64_t ntile = (a.nrows + 31) >> 5;
+    const int64_t npair = (ntile + 1) >> 1;
+    const double* ub = a.U + (int64_t)c0 * a.ldu;
+    int par = 0;
+    for (int64_t tp = (int64_t)blockIdx.x * NGR + grp; tp < npair; tp += (int64_t)gridDim.x * NGR) {
+        const int64_t r0 = (2 * tp) * 32 + lane, r1 = r0 + 32;
+        const bool ok0 = r0 < a.nrows, ok1 = r1 < a.nrows;
+        double u0[KS], u1[KS];
+#pragma unroll
+        for (int c = 0; c < KS; ++c) {
+            const bool cv = c0 + c < kv;
+            u0[c] = (ok0 && cv) ? __ldg(ub + (int64_t)c * a.ldu + r0) : 0.0;
+            u1[c] = (ok1 && cv) ? __ldg(ub + (int64_t)c * a.ldu + r1) : 0.0;
+        }
+        const double x0 = ok0 ? X[r0] : 0.0, x1 = ok1 ? X[r1] : 0.0;
+        double sp0 = 0.0, sp1 = 0.0;
+#pragma unroll
+        for (int c = 0; c < KS; ++c) {
+            sp0 = fma(hs[c0 + c], u0[c], sp0);
+            sp1 = fma(hs[c0 + c], u1[c], sp1);
+        }
+        sb[par][grp][wg][lane] = sp0;
+        sb[par][grp][wg][32 + lane] = sp1;
+        asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "r"(32 * G) : "memory");
+        double s0 = sb[par][grp][0][lane], s1 = sb[par][grp][0][32 + lane];
+#pragma unroll
+        for (int w = 1; w < G; ++w) {
+            s0 += sb[par][grp][w][lane];
+            s1 += sb[par][grp][w][32 + lane];
+        }
+        par ^= 1;
+        const double y0 = ok0 ? x0 - s0 : 0.0, y1 = ok1 ? x1 - s1 : 0.0;
+        if (wg == 0) {
+            if (a.out) {
+                if (ok0) a.out[r0] = y0;
+                if (ok1) a.out[r1] = y1;
+            }
+            yy = fma(y0, y0, yy);
+            yy = fma(y1, y1, yy);
+        }
+#pragma unroll
+        for (int c = 0; c < KS; ++c) d[c] = fma(u1[c], y1, fma(u0[c], y0, d[c]));
+    }
+#pragma unroll
+    for (int c = 0; c < KS; ++c) {
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) d[c] += __shfl_xor_sync(0xffffffffu, d[c], off);
+    }
+    if (lane == 0) {
+#pragma unroll
+        for (int c = 0; c < KS; ++c)
+            if (c0 + c < kv) acc[warp][c0 + c] = d[c];
+    }
+    const double ys = warp_sum(yy);
+    __syncthreads();
+    if (lane == 0 && wg == 0) acc[warp][kv] = ys;
+    __syncthreads();
+    const int nv = kv + 1;
+    for (int v = threadIdx.x; v < nv; v += CTA) {
+        double sum = 0.0;
+#pragma unroll
+        for (int w = 0; w < WARPS; ++w) sum += acc[w][v];
+        res[v] = sum;
+    }
+    __syncthreads();
+    if (!grid_reduce(res, nv, a.part, a.gpart, a.counter, a.maxcta, res)) return;
+    if (a.red_local) {
+        for (int v = threadIdx.x; v < nv; v += CTA) a.red_local[v] = res[v];
+    } else {
+        upd_finalize(a, res, kv);
+    }
+}
+
 template <int KS, int G>
 static void launch_upd2_wp_k(const UpdArgs& a, cudaStream_t s) {
+    static const bool one = getenv("TRPLK_WP1") && getenv("TRPLK_WP1")[0] == '1';
+    if (!one) {
+        auto kern2 = k_upd2_wp2<KS, G>;
+        kern2<<<tp_grid(kern2, (a.nrows + 1) / 2, 8 * G), CTA, 0, s>>>(a);
+        return;
+    }
     auto kern = k_upd2_wp<KS, G>;
     kern<<<tp_grid(kern, a.nrows, 8 * G), CTA, 0, s>>>(a);  // WARPS/G tiles of 32 rows per CTA at a time
 }

@@ -1,13 +1,10 @@
 mkdir -p gpurun_out/exp
 O=gpurun_out/exp
-B="python bench.py --config C2 --steps 1 --warmup 1 --no-cpu-baseline --no-e2e"
-$B > $O/plain.json 2> $O/plain.err || exit 1
-ncu -f --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:'k_step1_rs2<.int.24, .bool.1>' -c 3 -o /tmp/k1 $B > $O/ncu_k1.log 2>&1
-python tools/ncu_summary.py rep /tmp/k1.ncu-rep > $O/k1_summary.txt 2>&1
-python tools/ncu_source_top.py /tmp/k1.ncu-rep . 30 > $O/k1_source_top.txt 2>&1
-python tools/make_traffic.py /tmp/k1.ncu-rep C2 > $O/k1_traffic.log 2>&1
-B3="python bench.py --config C3 --steps 1 --warmup 1 --no-cpu-baseline --no-e2e"
-ncu -f --set full --clock-control none --kernel-name-base demangled -k regex:'k_step1_rs2<.int.32, .bool.1>' -s 20 -c 3 -o /tmp/k3 $B3 > $O/ncu_k3.log 2>&1
-python tools/make_traffic.py /tmp/k3.ncu-rep C3 > $O/k3_traffic.log 2>&1
-python tools/ncu_summary.py rep /tmp/k3.ncu-rep > $O/k3_summary.txt 2>&1
-cp profiles/traffic_C2.json profiles/traffic_C3.json $O/
+rm -f $O/sweep.txt
+for E in TRPLK_WP1=1 X=0; do for C in C2 C3; do
+echo "== $E $C" >> $O/sweep.txt
+env $E python bench.py --config $C --steps 3 --warmup 2 --no-cpu-baseline --no-e2e 2>>$O/sweep.txt | python -c "
+import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); r=d['roofline']
+print(d['ms_per_step'], d['config']['a_matvecs_per_solve'], 'K1 us', round(r['ms_per_launch']*1e3,2), 'frac', r['frac'], 'inner us', round(r['inner_step']['ms']*1e3,2), r['inner_step']['share_ms'])" >> $O/sweep.txt
+done; done
+timeout 1800 python -m pytest tests -m gpu -q -x --timeout 600 > $O/pytest_wp2.log 2>&1; echo "rc=$?" >> $O/pytest_wp2.log
