@@ -632,7 +632,10 @@ __device__ __noinline__ bool final_pass3_coop(const double* __restrict__ U, int6
     __shared__ double acc3[WARPS][QMAX + 1];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (int i = threadIdx.x; i < WARPS * (QMAX + 1); i += CTA) (&acc3[0][0])[i] = 0.0;
-    __syncthreads();
+    // w2 was written by the two-tile loop, whose row mapping is not this pass's: every CTA's
+    // rows must be visible before they are read back (only on the rare third pass)
+    __threadfence();
+    cg::this_grid().sync();
     const int64_t ntiles = (nrows + 31) >> 5;
     double yy = 0.0;
     for (int64_t tile = (int64_t)blockIdx.x * WARPS + warp; tile < ntiles; tile += (int64_t)gridDim.x * WARPS) {
@@ -685,7 +688,7 @@ __device__ __noinline__ bool final_pass3_coop(const double* __restrict__ U, int6
 // DOTS = true: mode 1 (update + U^T y dots); DOTS = false: modes 0 / 2 / 3 (no dots; the rare
 // third-pass dots are a separate gated k_sdots launch).
 template <int KMAX, bool DOTS>
-__global__ void __launch_bounds__(CTA, DOTS ? 2 : (KMAX <= 16 ? 3 : (KMAX <= 32 ? 2 : 1))) k_upd(const UpdArgs a) {
+__global__ void __launch_bounds__(CTA, DOTS ? 2 : (KMAX <= 32 ? 2 : 1)) k_upd(const UpdArgs a) {
     Ctl* ctl = a.ctl;
     if ((ctl->flags & a.gate) != a.gate) return;
     if (a.mode == 3 && ctl->pass3 == 0) return;
@@ -735,7 +738,44 @@ __global__ void __launch_bounds__(CTA, DOTS ? 2 : (KMAX <= 16 ? 3 : (KMAX <= 32 
 #pragma unroll
     for (int g = 0; g < KMAX / 8; ++g) dacc[g][0] = dacc[g][1] = 0.0;
     double yy_acc = 0.0;
-    if (write_y || write_dest) {
+    static_assert(KMAX > 0, "");
+    if constexpr (!DOTS && KMAX <= 24) {
+        // two 32-row tiles per warp iteration (as k_step1_rs2 / k_upd2_wp2): both rows of U in
+        // flight together, half the dependent load round trips per warp
+        const int64_t npair = (ntiles + 1) >> 1;
+        if (write_y || write_dest) {
+            for (int64_t tp = (int64_t)blockIdx.x * WARPS + warp; tp < npair; tp += (int64_t)gridDim.x * WARPS) {
+                const int64_t r0 = (2 * tp) * 32 + lane, r1 = r0 + 32;
+                const bool ok0 = r0 < a.nrows, ok1 = r1 < a.nrows;
+                double y0 = ok0 ? X[r0] : 0.0, y1 = ok1 ? X[r1] : 0.0;
+                double u0[KMAX], u1[KMAX];
+#pragma unroll
+                for (int c = 0; c < KMAX; ++c) {
+                    u0[c] = (ok0 && c < kv) ? __ldg(a.U + (int64_t)c * a.ldu + r0) : 0.0;
+                    u1[c] = (ok1 && c < kv) ? __ldg(a.U + (int64_t)c * a.ldu + r1) : 0.0;
+                }
+#pragma unroll
+                for (int c = 0; c < KMAX; ++c) {
+                    y0 = fma(-hs[c], u0[c], y0);
+                    y1 = fma(-hs[c], u1[c], y1);
+                }
+                if (ok0) {
+                    if (write_y && a.out) a.out[r0] = y0;
+                    if (write_dest) {
+                        dest[r0] = y0 * binv;
+                        if (a.dest2) a.dest2[r0] = y0 * binv;
+                    }
+                }
+                if (ok1) {
+                    if (write_y && a.out) a.out[r1] = y1;
+                    if (write_dest) {
+                        dest[r1] = y1 * binv;
+                        if (a.dest2) a.dest2[r1] = y1 * binv;
+                    }
+                }
+            }
+        }
+    } else if (write_y || write_dest) {
         for (int64_t tile = (int64_t)blockIdx.x * WARPS + warp; tile < ntiles;
              tile += (int64_t)gridDim.x * WARPS) {
             const int64_t row = tile * 32 + lane;
