@@ -1,23 +1,30 @@
 #!/usr/bin/env python
 """TRPL+K bench (BASELINE.json metric: matvecs/s & time to p eigenpairs, fp64, HBM GB/s vs peak).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C5] [--impl ours|reference]
 
-A "step" is one full trplk_solve (time to the p smallest eigenpairs) of the
-BASELINE config (default configs[1] = C2, 64^3 7-pt Laplacian + diag(d)),
-inputs resident in HBM (the context is created before the timed region).  The
-L2 (126 MB) is flushed between timed steps by writing a 256 MiB buffer.
+A "step" is one full trplk_solve (time to the p smallest eigenpairs) of the BASELINE config.
+Default: C5 = configs[4] (512^3 7-pt Laplacian + diag(d), n = 1.34e8) -- BASELINE's metric names
+no config, so the bench runs the largest single-GPU configuration (the one north_star's HBM and
+scaling targets are stated on); --config C1..C4 runs the others.  Inputs are resident in HBM
+(the context is created before the timed region); the inputs are far larger than the 126 MB L2
+at C3-C5 and a 256 MiB buffer is written between timed steps in any case.
 `value` = A-matvecs of the solve / solve time (whole job; max over ranks).
 `e2e` = the same metric through the public API with HOST CSR buffers (pinned): create
 (validation scan, H2D of the CSR, DIA/SELL conversion) + solve + D2H of eigenvectors +
-destroy, after min(W, 3) untimed create/solve/destroy rounds.
-`roofline` = the inner-step kernel with the largest share of the step, live
-CUDA-event timing on the last timed step (trplk_profile), algorithmic bytes of
-DESIGN.md, against MEASURED_PEAKS.json hbm_gbs.  `cpu_baseline` = the oracle
-(oracle/, plain C + OpenMP) on the host cores, rank 0 at N=1 only.
+destroy, after untimed create/solve/destroy rounds.
+`roofline` = the inner-step kernel with the largest share of the step: live CUDA events around
+the three kernel groups of the middle inner step of every cycle of every timed solve
+(trplk_profile; the event nodes serialise that step's kernels, so the timed solves carry their
+cost), algorithmic bytes of DESIGN.md / event time, against MEASURED_PEAKS.json hbm_gbs; the
+kernel named is the instantiation the library launched (trplk_profile_kernels) and `traffic` its
+ncu DRAM bytes per launch (profiles/traffic_<cfg>.json).  `cpu_baseline` = the oracle
+(oracle/, plain C + OpenMP) on the host cores, rank 0 at N=1 only: the full solve where it takes
+seconds (C1, C2), else a bounded sample of oracle inner steps at the config's full size (see
+oracle_sample).
 
---impl reference: this tier has no reference implementation; the reference
-arm is the oracle timed as it stands on the host cores (bounded sample).
+--impl reference: this tier has no reference implementation; the reference arm is the oracle
+timed as it stands on the host cores, each step one bounded sample of the same workload.
 For N>1 run under torchrun: one rank per GPU, z-slab row partition, NCCL.
 """
 from __future__ import annotations
@@ -44,17 +51,23 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="C2", choices=["C1", "C2", "C3", "C4", "C5"])
+    ap.add_argument("--config", default="C5", choices=["C1", "C2", "C3", "C4", "C5"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--profile-all-steps", action="store_true",
-                    help="kernel-profile events on every timed step (default: the last one)")
+    ap.add_argument("--profile-last-only", action="store_true",
+                    help="kernel-profile events on the last timed step only (default: every timed step)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=20.0, help="oracle sample budget")
     ap.add_argument("--method", default="trplk", choices=["trplk", "pl1"],
                     help="pl1: PL+1 (Algorithm 2, NEXT-1) for the lowest eigenpair, one GPU")
     ap.add_argument("--pl1-m", type=int, default=4, help="PL+1 Krylov block size m")
     return ap.parse_args()
+
+
+def ncu_name(demangled):
+    """'void trplk::k_step1_pipe<16, true>(trplk::SdotsArgs)' -> 'k_step1_pipe<16, 1>' (ncu's form)."""
+    x = demangled.replace("void ", "").replace("trplk::", "").split("(")[0].strip()
+    return x.replace("true", "1").replace("false", "0")
 
 
 def peaks():
@@ -110,53 +123,112 @@ def plane_of(P):
     return 1 if P.grid["dim"] == 1 else P.grid["N"] ** 2
 
 
-def cpu_baseline(name, budget_s):
-    """Oracle as it stands on the host cores: the full solve if it fits the budget, else the first
-    cycles (bounded sample)."""
-    import oracle
-    from paper_1711_10128_b200 import inputs
-    P = inputs.make(name)
-    cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
-    # probe: 2 cycles, then scale the cycle count to the budget
-    t0 = time.perf_counter()
-    r = oracle.solve(P.A, P.B, P.p, P.q, P.l, P.tol, P.sigma, max_cycles=2, want_vectors=False)
-    dt = time.perf_counter() - t0
-    per_cycle = max(dt / 2, 1e-6)
-    cyc = max(2, int(budget_s / per_cycle))
-    t0 = time.perf_counter()
-    r = oracle.solve(P.A, P.B, P.p, P.q, P.l, P.tol, P.sigma, max_cycles=min(cyc, 5000), want_vectors=False)
-    dt = time.perf_counter() - t0
-    full = r["status"] == "OK"
-    sample = (f"full oracle solve of {name} ({r['cycles']} cycles, {r['a_matvecs']} A-matvecs)" if full else
-              f"first {r['cycles']} cycles of the {name} oracle solve ({r['a_matvecs']} A-matvecs incl. "
-              f"{P.p} verification)")
-    return {"value": r["a_matvecs"] / dt, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample,
-            "seconds": dt}, r
+FULL_SOLVE_CFGS = ("C1", "C2")  # oracle full solve in seconds; C3/C4 take 20-30 min, C5 hours
+
+
+def static_config(name, P, n, world):
+    """The `config` object of both arms (identical keys and values)."""
+    return {"workload": f"{name}: {P.desc}; p={P.p}, max_basis={P.q}, k_plus={P.l}, tol={P.tol}, Jacobi, seed 12",
+            "n": n, "step": "one full trplk_solve (time to p eigenpairs)",
+            "l2": "inputs larger than L2 at C3-C5; a 256 MiB buffer is written between timed steps",
+            "parallelism": f"z-slab row partition x{world}"}
+
+
+class OracleSample:
+    """The oracle as it stands (oracle/, plain C + OpenMP) on a bounded sample of the workload.
+
+    C1, C2: the full oracle solve (seconds).  C3-C5 (a full oracle solve takes 20 min to hours):
+    orc_inner_steps -- the code orc_trplk_solve runs for one inner step of eq 3.1 (z = A g, the
+    T column U^T z, w = M (z - rho g), CGS2 of w against the basis, g_next = w / beta) -- on the
+    config's full-size matrix with a basis of the cycle-average width k = p^ + (m+1)/2 (unit
+    vectors: orthonormal; every page written before timing so the reads are real DRAM reads).
+    One inner step = one A-matvec; the +K, Rayleigh-Ritz, rotation and residual work of a cycle
+    (about 10-15 % of its bytes in DESIGN.md's model) is not in the sample, so the sample's
+    matvecs/s is an upper bound of the oracle's full-solve rate."""
+
+    def __init__(self, name, P=None):
+        import numpy as np
+        import oracle
+        from paper_1711_10128_b200 import inputs
+        oracle.build()
+        self.name = name
+        self.P = P if P is not None else inputs.make(name)
+        self.cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
+        self.full = name in FULL_SOLVE_CFGS
+        if not self.full:
+            P = self.P
+            n = P.A.n
+            m = P.q - P.p - P.l
+            self.k0 = P.p + (m + 1) // 2
+            self.U = np.empty((n, self.k0 + 1), order="F")
+            self.U[:] = 0.0
+            for c in range(self.k0):
+                self.U[(c * 7919) % n, c] = 1.0
+            self.work = np.empty(4 * n)
+            self.work[:] = 0.0
+            self.M = oracle.jacobi_diag(P.A, P.B, P.sigma)
+            self.T = np.zeros((self.k0 + 1, self.k0 + 1), order="F")
+
+    def step(self):
+        """One sample; returns (A-matvecs, seconds)."""
+        import oracle
+        P = self.P
+        if self.full:
+            t0 = time.perf_counter()
+            r = oracle.solve(P.A, P.B, P.p, P.q, P.l, P.tol, P.sigma, want_vectors=False)
+            return r["a_matvecs"], time.perf_counter() - t0
+        t0 = time.perf_counter()
+        done, _ = oracle.inner_steps(P.A, P.B, self.M, 1.0, self.U, self.k0, 1, self.T, self.work)
+        return done, time.perf_counter() - t0
+
+    def describe(self, steps):
+        P = self.P
+        if self.full:
+            return f"full oracle solve of {self.name}"
+        return (f"{steps} oracle inner step(s) of eq 3.1 (orc_inner_steps: SpMV, T column, Jacobi, CGS2) at "
+                f"full {self.name} size (n={P.A.n}) with basis width k={self.k0} (cycle average); "
+                f"+K/RR/rotation/residual work not sampled (upper bound of the full-solve rate)")
+
+
+def cpu_baseline(name, budget_s, P=None):
+    """rank 0 at N=1: the oracle sample repeated until ~budget_s seconds of host work."""
+    smp = OracleSample(name, P)
+    mv = 0
+    dt = 0.0
+    steps = 0
+    while True:
+        a, t = smp.step()
+        mv += a
+        dt += t
+        steps += 1
+        if dt >= budget_s:
+            break
+    return {"value": mv / dt, "unit": UNIT, "cores": smp.cores, "kind": "oracle", "sample": smp.describe(steps),
+            "seconds": dt}
 
 
 def run_reference(args):
-    """Reference arm = the oracle (this tier has no reference implementation)."""
+    """Reference arm = the oracle (this tier has no reference implementation), each step one
+    OracleSample of the same workload as our arm."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    vals, times = [], []
-    from paper_1711_10128_b200 import inputs
-    P = inputs.make(args.config)
-    budget = max(3.0, min(args.cpu_seconds, 150.0 / max(1, args.steps + args.warmup)))
-    cb = None
+    smp = OracleSample(args.config)
+    P = smp.P
+    mvs, times = [], []
     for i in range(args.warmup + args.steps):
-        cb, r = cpu_baseline(args.config, budget)
+        a, t = smp.step()
         if i >= args.warmup:
-            vals.append(cb["value"])
-            times.append(cb["seconds"])
-    v = statistics.mean(vals)
+            mvs.append(a)
+            times.append(t)
+    v = sum(mvs) / sum(times)
     out = {"metric": METRIC, "value": v, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.mean(times),
            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-           "data": "synthetic (seeded generator, BASELINE configs)",
-           "config": {"workload": f"{args.config}: {P.desc}; p={P.p}, max_basis={P.q}, k_plus={P.l}, tol={P.tol}",
-                      "l2": "host run"},
-           "cpu_baseline": {**{k: cb[k] for k in ("kind", "cores", "sample")}, "value": v, "unit": UNIT},
+           "data": "synthetic (seeded generator, BASELINE configs; paper matrices unavailable)",
+           "config": static_config(args.config, P, P.A.n, args.gpus),
+           "cpu_baseline": {"kind": "oracle", "cores": smp.cores, "sample": smp.describe(1) + " per step",
+                            "value": v, "unit": UNIT},
            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out))
     return 0
@@ -297,9 +369,9 @@ def main():
     times, stats = [], []
     for it in range(args.steps):
         # the live kernel profile (CUDA event nodes around the middle inner step of every cycle)
-        # serialises that step's kernels; it runs on the last timed step only (all of them if
-        # --profile-all-steps), so the other K-1 steps are unperturbed
-        if it == (0 if args.profile_all_steps else args.steps - 1):
+        # serialises that step's kernels; it runs on every timed step (the headline carries its
+        # cost: +2 % at C2, below 0.1 % at C5), or on the last one with --profile-last-only
+        if it == (args.steps - 1 if args.profile_last_only else 0):
             trplk.trplk_profile(ctx, True)
         flush.fill_(1.0)
         barrier()
@@ -314,6 +386,7 @@ def main():
         stats.append(st)
     ck = clocks.stop()
     prof = trplk.trplk_profile_read(ctx)
+    kern_names = trplk.trplk_profile_kernels(ctx)
     trplk.trplk_profile(ctx, False)
     t_sum = torch.tensor([sum(times)], dtype=torch.float64, device="cuda")
     if world > 1:
@@ -324,9 +397,8 @@ def main():
     value = mv / (ms_per_step / 1e3)
 
     # roofline: inner-step kernel group with the largest share (live CUDA events, per launch)
-    names = ["K1 (k_step1_rs2: SpMV + Jacobi + T-column / h1 dots)",
-             "K2 (CGS pass 2: k_upd2_wp update + dots; B != I: the B-SpMV dot passes too)",
-             "K3 (k_upd FINAL update + normalisation)"]
+    groups = ["K1 (SpMV + Jacobi + T-column / h1 dots)", "K2 (CGS pass 2: update + dots)",
+              "K3 (CGS final update + normalisation)"]
     peak, peak_src = peaks()
     cnt = max(prof["count"], 1)
     per_ms = prof["ms"] / cnt
@@ -334,28 +406,17 @@ def main():
     kd = int(np.argmax(per_ms))
     achieved = per_b[kd] / (per_ms[kd] * 1e-3) / 1e9
     step_gbs = per_b.sum() / (per_ms.sum() * 1e-3) / 1e9
+    kname = ncu_name(kern_names[kd]) if kd < len(kern_names) else ""
     # ncu DRAM bytes per launch of the same kernel instantiation (profiles/traffic_<cfg>.json,
-    # tools/make_traffic.py): the inner step profiled is j = jmid, k = p^ + jmid
-    traffic, traffic_kernel = None, None
+    # tools/make_traffic.py, cold cache)
+    traffic = None
     tfile = os.path.join(PROFILES, f"traffic_{args.config}.json")
-    if os.path.exists(tfile):
-        m = P.q - P.p - P.l
-        jmid = max(1, min(m - 1, m // 2))
-        kk = P.p + jmid
-        bucket = next(b for b in (8, 16, 24, 32, 40, 48, 64) if kk <= b)
-        tj = json.load(open(tfile))
-        # K1 runs k_step1_rs (or the pipelined k_step1_pipe on long slabs), K2 the warp-group
-        # k_upd2_wp<KS, G>, K3 k_upd<KMAX, 0>
-        want = [(f"k_step1_rs2<{bucket}, 1>", f"k_step1_pipe<{bucket}, 1>"), ("k_upd2_wp<",),
-                (f"k_upd<{bucket}, 0>",)][kd]
-        for key in tj:
-            if key != "source" and any(key.startswith(w) for w in want):
-                if kd != 1 or int(key.split("<")[1].split(",")[0]) * int(key.split(",")[1].strip(" >")) >= bucket:
-                    traffic_kernel, traffic = key, tj[key]
-                    break
-    roof = {"bound": "hbm", "kernel": names[kd], "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-            "frac": round(achieved / peak, 4), "traffic": traffic, "traffic_kernel": traffic_kernel,
-            "peak_source": peak_src,
+    if os.path.exists(tfile) and kname:
+        traffic = json.load(open(tfile)).get(kname)
+    roof = {"bound": "hbm", "kernel": f"{groups[kd]}: {kname}", "achieved": round(achieved, 1), "peak": peak,
+            "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
+            "traffic_source": f"profiles/traffic_{args.config}.json[{kname!r}]" if traffic else None,
+            "peak_source": peak_src, "kernels": [ncu_name(x) for x in kern_names],
             "bytes_per_launch": per_b[kd], "ms_per_launch": per_ms[kd],
             "inner_step": {"achieved": round(step_gbs, 1), "frac": round(step_gbs / peak, 4),
                            "bytes": per_b.sum(), "ms": per_ms.sum(),
@@ -383,8 +444,9 @@ def main():
         h2d = sum(t.numel() * t.element_size() for t in pin)
         d2h = host_evecs.numel() * 8 + 2 * P.p * 8
         et = []
-        ne_warm = max(1, min(args.warmup, 3))
-        for it in range(ne_warm + max(1, min(args.steps, 5))):
+        big = n > 50_000_000  # C5: each e2e round is a full create + 20 s solve
+        ne_warm = 1 if big else max(1, min(args.warmup, 3))
+        for it in range(ne_warm + (max(1, min(args.steps, 2)) if big else max(1, min(args.steps, 5)))):
             flush.fill_(1.0)
             barrier()
             torch.cuda.synchronize()
@@ -405,7 +467,9 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cb, _ = cpu_baseline(args.config, args.cpu_seconds)
+        if not args.no_e2e:
+            del pin, HA, HB, host_evecs  # release the pinned host copies before the oracle sample
+        cb = cpu_baseline(args.config, args.cpu_seconds, P)
         cpu = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
 
     if rank == 0:
@@ -413,13 +477,10 @@ def main():
                "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
                "scaling": "strong", "vs_baseline": None, "dtype": "f64",
                "data": "synthetic (seeded generator, BASELINE configs; paper matrices unavailable)",
-               "config": {"workload": f"{args.config}: {P.desc}; p={P.p}, max_basis={P.q}, k_plus={P.l}, "
-                                      f"tol={P.tol}, Jacobi, seed 12",
-                          "n": n, "step": "one full trplk_solve (time to p eigenpairs)",
-                          "a_matvecs_per_solve": mv, "cycles": stats[-1]["cycles"],
-                          "time_to_p_eigenpairs_ms": round(ms_per_step, 4),
-                          "l2": "flushed (256 MiB write) between timed steps",
-                          "parallelism": f"z-slab row partition x{world}"},
+               "config": static_config(args.config, P, n, world),
+               "solve": {"a_matvecs_per_solve": mv, "cycles": stats[-1]["cycles"],
+                         "time_to_p_eigenpairs_ms": round(ms_per_step, 4),
+                         "status": stats[-1]["status"]},
                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
                "gpu_launches": int(sum(s["kernel_launches"] for s in stats)), "clocks": ck,
                "eigenvalues": [float(x) for x in ev], "max_residual": float(np.max(rs))}

@@ -95,6 +95,10 @@ void trplk_loopback_destroy(void* hub);
  * enable=1 clears the accumulators.  read: ms[3], bytes[3] sums over `count` cycles. */
 trplk_status trplk_profile(trplk_ctx* ctx, int enable);
 trplk_status trplk_profile_read(const trplk_ctx* ctx, double* ms, double* bytes, int64_t* count);
+/* Demangled names of the kernels that ran the three profiled groups (K1;K2;K3, ';'-separated;
+ * an empty field where the group is fused into K1), written NUL-terminated into buf[len].
+ * Errors: EINVAL (NULL ctx/buf or len too small). */
+trplk_status trplk_profile_kernels(const trplk_ctx* ctx, char* buf, size_t len);
 
 #ifdef __cplusplus
 }

@@ -55,7 +55,8 @@ class _Report(ctypes.Structure):
                 ("log_t", _P), ("log_mv", _P), ("log_theta_t", _P), ("log_res", _P),
                 ("log_k", _P), ("log_nprev", _P), ("log_thetas", _P), ("log_terr", _P),
                 ("log_orth", _P), ("dump_cycles", ctypes.c_int), ("dump_X", _P),
-                ("dump_rho", _P), ("dump_t", _P)]
+                ("dump_rho", _P), ("dump_t", _P), ("n_sample", ctypes.c_int),
+                ("sample_rows", _P), ("sample_vals", _P), ("verbose", ctypes.c_int)]
 
 
 class _Pl1Problem(ctypes.Structure):
@@ -102,6 +103,9 @@ def lib():
         L.orc_rotate.argtypes = [_I64, ctypes.c_int, _P, _P, ctypes.c_int, ctypes.c_int, _P]
         L.orc_trplk_solve.restype = ctypes.c_int
         L.orc_trplk_solve.argtypes = [ctypes.POINTER(_Problem), _P, _P, _P, ctypes.POINTER(_Report)]
+        L.orc_inner_steps.restype = ctypes.c_int
+        L.orc_inner_steps.argtypes = [ctypes.POINTER(_Problem), _P, ctypes.c_double, _P, ctypes.c_int,
+                                      ctypes.c_int, _P, ctypes.c_int, _P]
         L.orc_pl1_solve.restype = ctypes.c_int
         L.orc_pl1_solve.argtypes = [ctypes.POINTER(_Pl1Problem), _P, ctypes.POINTER(_Pl1Report)]
         _lib = L
@@ -200,7 +204,7 @@ STATUS = {0: "OK", 1: "EINVAL", 2: "NOT_CONVERGED", 3: "BREAKDOWN"}
 
 def solve(A, B=None, p=5, q=20, l=1, tol=1e-8, sigma=0.0, seed=12, max_cycles=5000,
           tol_mode=0, restart_size=0, lock_mode=0, debug=False, dump_cycles=0,
-          want_vectors=True):
+          want_vectors=True, sample_rows=None, verbose=False):
     """Run Algorithm 1 (TRPL+K).  Returns a dict with eigenvalues, vectors, residuals,
     counters and the per-cycle log."""
     ra, ca, va = _csr(A)
@@ -220,10 +224,13 @@ def solve(A, B=None, p=5, q=20, l=1, tol=1e-8, sigma=0.0, seed=12, max_cycles=50
     dX = np.zeros((max(dump_cycles, 1), ph, n)) if dump_cycles else None
     drho = np.zeros(max(dump_cycles, 1))
     dt = np.zeros(max(dump_cycles, 1), np.int32)
+    srows = None if sample_rows is None else np.ascontiguousarray(sample_rows, np.int64)
+    svals = None if srows is None else np.zeros((p, len(srows)))
     rep = _Report(0, 0, 0, 0, 0, 0, 0, 0, cap, 0,
                   _ptr(logs["t"]), _ptr(logs["mv"]), _ptr(logs["theta_t"]), _ptr(logs["res"]),
                   _ptr(logs["k"]), _ptr(logs["nprev"]), _ptr(logs["thetas"]), _ptr(logs["terr"]),
-                  _ptr(logs["orth"]), dump_cycles, _ptr(dX), _ptr(drho), _ptr(dt))
+                  _ptr(logs["orth"]), dump_cycles, _ptr(dX), _ptr(drho), _ptr(dt),
+                  0 if srows is None else len(srows), _ptr(srows), _ptr(svals), 1 if verbose else 0)
     evals = np.zeros(p)
     resid = np.zeros(p)
     evecs = np.zeros((p, n)) if want_vectors else None  # row c = eigenvector c (n contiguous)
@@ -237,12 +244,33 @@ def solve(A, B=None, p=5, q=20, l=1, tol=1e-8, sigma=0.0, seed=12, max_cycles=50
         "precond_applies": rep.precond_applies, "verify_matvecs": rep.verify_matvecs,
         "inner_steps": rep.inner_steps, "random_draws": rep.random_draws,
         "log": {k_: v[:L] for k_, v in logs.items()},
+        "samples": None if svals is None else svals.T,  # [n_sample, p]
     }
     if dump_cycles:
         nd = min(dump_cycles, rep.cycles)
         out["dump"] = {"X": [dX[i].T.copy() for i in range(nd)], "rho": drho[:nd].copy(),
                        "t": dt[:nd].copy()}
     return out
+
+
+def inner_steps(A, B, M, rho, U, k0, nsteps, T=None, work=None):
+    """Run `nsteps` inner steps of eq 3.1 (orc_inner_steps) on the Fortran-ordered basis U
+    (n x (k0+nsteps), orthonormal first k0 columns); fills U's next columns and T in place.
+    work: optional scratch of 4n doubles (pre-touched by the caller)."""
+    ra, ca, va = _csr(A)
+    rb, cb, vb = _csr(B)
+    n = len(ra) - 1
+    assert U.flags["F_CONTIGUOUS"] and U.dtype == np.float64 and U.shape[1] >= k0 + nsteps
+    q = U.shape[1]
+    T = np.zeros((q, q), order="F") if T is None else T
+    prob = _Problem(n, _ptr(ra), _ptr(ca), _ptr(va), _ptr(rb), _ptr(cb), _ptr(vb), 0.0,
+                    1, q, 0, 1.0, 0, 12, 1, 0, 0, 0)
+    M = np.ascontiguousarray(M, np.float64)
+    if work is not None:
+        assert work.dtype == np.float64 and work.size >= 4 * n and work.flags["C_CONTIGUOUS"]
+    done = lib().orc_inner_steps(ctypes.byref(prob), _ptr(M), float(rho), _ptr(U), k0, nsteps, _ptr(T), q,
+                                 _ptr(work))
+    return done, T
 
 
 def pl1_solve(A, B=None, m=4, tol=1e-8, sigma=0.0, seed=12, x0=None, max_cycles=2000, variant=0,

@@ -12,6 +12,7 @@
 #include "oracle.h"
 
 #include <math.h>
+#include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
 
@@ -261,6 +262,63 @@ void orc_rotate(int64_t n, int k, const double* U, const double* Y, int ldy, int
         }
 }
 
+/* The same sums as orc_rotate, written back into U(:,0:ncol) row by row (each row's k inputs are
+ * read before any of its outputs is stored; ncol <= k). */
+static void rotate_rows_inplace(int64_t n, int k, double* U, const double* Y, int ldy, int ncol) {
+#pragma omp parallel if (n > 32768)
+    {
+        double* row = (double*)malloc((size_t)ncol * sizeof(double));
+#pragma omp for schedule(static)
+        for (int64_t i = 0; i < n; ++i) {
+            for (int cc = 0; cc < ncol; ++cc) {
+                double s = 0.0;
+                for (int j = 0; j < k; ++j) s += U[i + (size_t)n * j] * Y[j + (size_t)ldy * cc];
+                row[cc] = s;
+            }
+            for (int cc = 0; cc < ncol; ++cc) U[i + (size_t)n * cc] = row[cc];
+        }
+        free(row);
+    }
+}
+
+/* One inner step of eq 3.1 on the basis U(:,0:k), g_j = U(:,k-1):
+ *   z = A g_j;  T(1:k,k) = U^T z (mirrored);  if `next`: w = M(z - rho B g_j) (R1), CGS2_B of w
+ *   against U(:,0:k) (R2, R3) and g_{j+1} = w/beta into U(:,k).  Returns 1 on a breakdown (R16). */
+static int inner_step(ctx_t* c, const double* M, double rho, int next, double* U, int k, double* T, int q,
+                      double* z, double* s, double* w, double* Bw) {
+    const int64_t n = c->n;
+    double* g = U + (size_t)n * (k - 1);
+    double beta;
+    applyA(c, g, z);
+    for (int i = 0; i < k; ++i) {
+        double v = orc_dot(n, U + (size_t)n * i, z);
+        T[i + (size_t)q * (k - 1)] = v;
+        T[(k - 1) + (size_t)q * i] = v;
+    }
+    if (!next) return 0;
+    applyB(c, g, s);
+    for (int64_t i = 0; i < n; ++i) w[i] = M[i] * (z[i] - rho * s[i]); /* R1 */
+    c->prec++;
+    if (cgs2_ctx(c, k, U, w, Bw, NULL, &beta, NULL)) return 1;
+    scal_copy(n, 1.0 / beta, w, U + (size_t)n * k);
+    return 0;
+}
+
+int orc_inner_steps(const orc_problem* P, const double* M, double rho, double* U, int k0, int nsteps,
+                    double* T, int ldT, double* work) {
+    const int64_t n = P->n;
+    ctx_t c = {P, n, 0, 0, 0};
+    double* wk = work ? work : (double*)malloc((size_t)4 * n * sizeof(double));
+    double *z = wk, *s = wk + n, *w = wk + 2 * n, *Bw = wk + 3 * n;
+    int done = 0;
+    for (int j = 0; j < nsteps; ++j) {
+        ++done;
+        if (inner_step(&c, M, rho, 1, U, k0 + j, T, ldT, z, s, w, Bw)) break;
+    }
+    if (!work) free(wk);
+    return done;
+}
+
 int orc_trplk_solve(const orc_problem* P, double* evals, double* evecs, double* resid, orc_report* rep) {
     const int64_t n = P->n;
     const int p = P->p, q = P->q, l = P->l;
@@ -280,11 +338,14 @@ int orc_trplk_solve(const orc_problem* P, double* evals, double* evecs, double* 
     double tau = P->tol;
     if (P->tol_mode == 1) tau = P->tol * orc_frobenius(P->a_rowptr[n], P->a_val); /* eq 5.1 */
 
+    /* Storage (no arithmetic depends on it): the rotation X = U Y(:,1:p^) is written row by row
+     * into U's first p^ columns (rotate_rows_inplace, same sums as orc_rotate), so X lives in
+     * U(:,1:p^) and no separate n x p^ block is kept; W = AX exists only during start-up; X^prev
+     * is captured straight into Xp, whose previous contents were consumed by this cycle's +K
+     * step.  This keeps the 512^3 config (C5) within a 62 GB host. */
     double* U = (double*)calloc((size_t)n * q, sizeof(double));
-    double* Xn = (double*)malloc((size_t)n * ph * sizeof(double));
-    double* W = (double*)malloc((size_t)n * ph * sizeof(double));
-    double* Xp = (double*)malloc((size_t)n * (l > 0 ? l : 1) * sizeof(double));
-    double* XpN = (double*)malloc((size_t)n * (l > 0 ? l : 1) * sizeof(double));
+    double* W = NULL;
+    double* Xp = NULL;
     double* w = (double*)malloc((size_t)n * sizeof(double));
     double* Bw = (double*)malloc((size_t)n * sizeof(double));
     double* z = (double*)malloc((size_t)n * sizeof(double));
@@ -311,15 +372,13 @@ int orc_trplk_solve(const orc_problem* P, double* evals, double* evecs, double* 
         if (brk) { status = 3; goto done_init_fail; }
         scal_copy(n, 1.0 / beta, x, x);
     }
+    W = (double*)malloc((size_t)n * ph * sizeof(double));
     for (int cc = 0; cc < ph; ++cc) applyA(&c, U + (size_t)n * cc, W + (size_t)n * cc);
     for (int j = 0; j < ph; ++j)
         for (int i = 0; i < ph; ++i) Tk[i + (size_t)ph * j] = orc_dot(n, U + (size_t)n * i, W + (size_t)n * j);
     if (orc_sym_eig(ph, Tk, th, Y) < 0) { status = 3; goto done_init_fail; }
-    orc_rotate(n, ph, U, Y, ph, ph, Xn);
-    memcpy(U, Xn, (size_t)n * ph * sizeof(double));
-    orc_rotate(n, ph, W, Y, ph, ph, Xn); /* W <- W Y (AX of the rotated X) */
-    memcpy(W, Xn, (size_t)n * ph * sizeof(double));
-    memcpy(Xn, U, (size_t)n * ph * sizeof(double));
+    rotate_rows_inplace(n, ph, U, Y, ph, ph); /* X <- X Y */
+    rotate_rows_inplace(n, ph, W, Y, ph, ph); /* W <- W Y (AX of the rotated X) */
     memset(T, 0, (size_t)q * q * sizeof(double));
     for (int i = 0; i < ph; ++i) T[i + (size_t)q * i] = th[i];
     int t = 1; /* target, 1-based */
@@ -328,6 +387,9 @@ int orc_trplk_solve(const orc_problem* P, double* evals, double* evecs, double* 
     for (int64_t i = 0; i < n; ++i) r[i] = W[i] - rho * s[i];
     for (int64_t i = 0; i < n; ++i) u[i] = M[i] * r[i];
     c.prec++;
+    free(W);
+    W = NULL;
+    Xp = (double*)malloc((size_t)n * (l > 0 ? l : 1) * sizeof(double));
     int nprev = 0;
     int cyc;
     int all_conv = 0;
@@ -352,23 +414,9 @@ int orc_trplk_solve(const orc_problem* P, double* evals, double* evecs, double* 
         scal_copy(n, 1.0 / beta, w, U + (size_t)n * k);
         /* ---- inner projected Lanczos, eq 3.1, R1/R2 */
         for (int j = 1; j <= m; ++j) {
-            double* g = U + (size_t)n * k;
             k += 1; /* k = p^ + j */
-            applyA(&c, g, z);
             ++inner_steps;
-            for (int i = 0; i < k; ++i) {
-                double v = orc_dot(n, U + (size_t)n * i, z);
-                T[i + (size_t)q * (k - 1)] = v;
-                T[(k - 1) + (size_t)q * i] = v;
-            }
-            if (j < m) {
-                applyB(&c, g, s);
-                for (int64_t i = 0; i < n; ++i) w[i] = M[i] * (z[i] - rho * s[i]); /* R1 */
-                c.prec++;
-                brk = cgs2_ctx(&c, k, U, w, Bw, NULL, &beta, NULL);
-                if (brk) break; /* R16: basis ends early */
-                scal_copy(n, 1.0 / beta, w, U + (size_t)n * k);
-            }
+            if (inner_step(&c, M, rho, j < m, U, k, T, q, z, s, w, Bw)) break; /* R16: basis ends early */
         }
         /* ---- +K: X^prev appended after G, explicitly orthogonalised, l matvecs (Alg.1 7-8) */
         int appended = 0;
@@ -391,8 +439,8 @@ int orc_trplk_solve(const orc_problem* P, double* evals, double* evecs, double* 
         int last = t + l - 1 < p ? t + l - 1 : p;
         int nnew = last - t + 1;
         if (nnew < 0) nnew = 0;
-        for (int cc = 0; cc < nnew; ++cc)
-            memcpy(XpN + (size_t)n * cc, U + (size_t)n * (t - 1 + cc), (size_t)n * sizeof(double));
+        for (int cc = 0; cc < nnew; ++cc) /* Xp was consumed by the +K step above */
+            memcpy(Xp + (size_t)n * cc, U + (size_t)n * (t - 1 + cc), (size_t)n * sizeof(double));
         /* ---- debug bookkeeping checks: T vs U^T A U, U^T B U - I */
         if (rep && P->debug && rep->log_cap >= cyc) {
             double terr = 0.0, oerr = 0.0;
@@ -414,9 +462,9 @@ int orc_trplk_solve(const orc_problem* P, double* evals, double* evecs, double* 
         for (int jj = 0; jj < k; ++jj)
             for (int ii = 0; ii < k; ++ii) Tk[ii + (size_t)k * jj] = T[ii + (size_t)q * jj];
         if (orc_sym_eig(k, Tk, th, Y) < 0) { status = 3; break; }
-        orc_rotate(n, k, U, Y, k, ph, Xn);
+        rotate_rows_inplace(n, k, U, Y, k, ph); /* U(:,1:p^) <- X_new = U Y(:,1:p^) */
         /* ---- Alg. 1 steps 12-14: soft lock (R7 literal IF) */
-        double res = residual(&c, Xn + (size_t)n * (t - 1), th[t - 1], r, s);
+        double res = residual(&c, U + (size_t)n * (t - 1), th[t - 1], r, s);
         if (rep && rep->log_cap >= cyc) {
             if (rep->log_t) rep->log_t[cyc - 1] = t;
             if (rep->log_theta_t) rep->log_theta_t[cyc - 1] = th[t - 1];
@@ -429,28 +477,30 @@ int orc_trplk_solve(const orc_problem* P, double* evals, double* evecs, double* 
             t += 1;
             if (nnew > 0) { /* remove x1^prev (step 13) */
                 for (int cc = 1; cc < nnew; ++cc)
-                    memcpy(XpN + (size_t)n * (cc - 1), XpN + (size_t)n * cc, (size_t)n * sizeof(double));
+                    memcpy(Xp + (size_t)n * (cc - 1), Xp + (size_t)n * cc, (size_t)n * sizeof(double));
                 nnew -= 1;
             }
             if (t > p) { all_conv = 1; break; }
-            res = residual(&c, Xn + (size_t)n * (t - 1), th[t - 1], r, s);
+            res = residual(&c, U + (size_t)n * (t - 1), th[t - 1], r, s);
             if (P->lock_mode == 0) break;
         }
-        /* ---- Alg. 1 step 15: restart.  X = U Y(:,1:p^), T = diag(Theta) (R10) */
-        memcpy(U, Xn, (size_t)n * ph * sizeof(double));
+        /* ---- Alg. 1 step 15: restart.  X = U Y(:,1:p^) (already in U), T = diag(Theta)
+         * (R10), X^prev = Xp(:,1:nnew) */
         memset(T, 0, (size_t)q * q * sizeof(double));
         for (int i = 0; i < ph; ++i) T[i + (size_t)q * i] = th[i];
-        if (nnew > 0) memcpy(Xp, XpN, (size_t)n * nnew * sizeof(double));
         nprev = nnew;
         if (rep && rep->log_cap >= cyc) {
             if (rep->log_mv) rep->log_mv[cyc - 1] = c.a_mv;
             rep->log_len = cyc;
         }
+        if (rep && rep->verbose)
+            fprintf(stderr, "oracle cycle %d t=%d k=%d mv=%lld theta=%.16e\n", cyc, t, k, (long long)c.a_mv,
+                    th[t - 1 <= ph - 1 ? t - 1 : ph - 1]);
         if (all_conv) {
             /* final verification of all p pairs (R9) */
             int first_fail = -1;
             for (int i = 0; i < p; ++i) {
-                double ri = residual(&c, Xn + (size_t)n * i, th[i], w, s);
+                double ri = residual(&c, U + (size_t)n * i, th[i], w, s);
                 verify_mv++;
                 resid[i] = ri;
                 if (ri > tau && first_fail < 0) {
@@ -469,12 +519,16 @@ int orc_trplk_solve(const orc_problem* P, double* evals, double* evecs, double* 
     if (status != 0) {
         /* NOT_CONVERGED (R19) / BREAKDOWN: report the current best with verified residuals */
         for (int i = 0; i < p; ++i) {
-            resid[i] = residual(&c, Xn + (size_t)n * i, th[i], w, s);
+            resid[i] = residual(&c, U + (size_t)n * i, th[i], w, s);
             verify_mv++;
         }
     }
     for (int i = 0; i < p; ++i) evals[i] = th[i];
-    if (evecs) memcpy(evecs, Xn, (size_t)n * p * sizeof(double));
+    if (evecs) memcpy(evecs, U, (size_t)n * p * sizeof(double));
+    if (rep && rep->n_sample > 0 && rep->sample_rows && rep->sample_vals)
+        for (int cc = 0; cc < p; ++cc)
+            for (int i = 0; i < rep->n_sample; ++i)
+                rep->sample_vals[i + (size_t)rep->n_sample * cc] = U[rep->sample_rows[i] + (size_t)n * cc];
     if (rep) rep->cycles = cyc > P->max_cycles ? P->max_cycles : cyc;
     goto done;
 
@@ -490,7 +544,7 @@ done:
         rep->inner_steps = inner_steps;
         rep->random_draws = draws;
     }
-    free(M); free(U); free(Xn); free(W); free(Xp); free(XpN); free(w); free(Bw); free(z);
+    free(M); free(U); free(W); free(Xp); free(w); free(Bw); free(z);
     free(s); free(r); free(u); free(T); free(Tk); free(Y); free(th);
     return status;
 }

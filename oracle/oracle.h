@@ -81,7 +81,21 @@ typedef struct {
     double* dump_X;         /* dump_cycles x (n x p^) */
     double* dump_rho;       /* dump_cycles */
     int* dump_t;            /* dump_cycles */
+    /* optional samples of the returned eigenvectors (large problems): sample_vals[i + n_sample*c]
+     * = x_c(sample_rows[i]) for c < p */
+    int n_sample;
+    const int64_t* sample_rows;
+    double* sample_vals;
+    int verbose;            /* 1: one progress line per cycle on stderr */
 } orc_report;
+
+/* Inner steps of eq 3.1 alone (the code orc_trplk_solve runs for step j < m): for j < nsteps,
+ * g = U(:,k0+j-1): z = A g, T(0:k0+j, k0+j-1) = U^T z (mirrored, ldT), w = M(z - rho B g), CGS2_B of w
+ * against U(:,0:k0+j), U(:,k0+j) = w/beta.  U is n x (k0+nsteps) column-major with orthonormal
+ * U(:,0:k0); M the Jacobi diagonal; work: caller scratch of 4n doubles (NULL: allocated here).  Returns the steps run (fewer after a breakdown).  Used by
+ * bench.py to time a bounded sample of the oracle at sizes where a full solve takes hours. */
+int orc_inner_steps(const orc_problem* P, const double* M, double rho, double* U, int k0, int nsteps,
+                    double* T, int ldT, double* work /* 4n scratch, or NULL */);
 
 /* Algorithm 1 in full.  evals[p], resid[p] ascending; evecs n x p column-major. */
 int orc_trplk_solve(const orc_problem* prob, double* evals, double* evecs, double* resid,

@@ -5,6 +5,7 @@
 // Host control flow mirrors Algorithm 1 with readings R1-R20;
 // all vector work runs in the kernels of kernels.cu.  One host synchronisation per cycle
 // (the soft-locking decision of steps 12-14 needs ||r_t||).
+#include <cxxabi.h>
 #include <nccl.h>
 
 #include "comm.cuh"
@@ -102,6 +103,7 @@ struct trplk_ctx {
     cudaEvent_t pev[4] = {nullptr, nullptr, nullptr, nullptr};
     double prof_ms[3] = {0, 0, 0}, prof_bytes[3] = {0, 0, 0};
     int64_t prof_count = 0;
+    const void* prof_kern[3] = {nullptr, nullptr, nullptr};  // kernels of the profiled groups K1, K2, K3
     int prof_k = 0;
 };
 
@@ -768,6 +770,7 @@ trplk_status cgs2(trplk_ctx* ctx, const CgsSpec& c) {
         u.hout = 1;
         u.gate = c.gate;
         ST(run_upd(ctx, u, kn));
+        if (c.mark_final) ctx->prof_kern[1] = g_last_kern;
     }
     if (ctx->hasB) {
         SdotsArgs a = sd_base(ctx);
@@ -807,6 +810,7 @@ trplk_status cgs2(trplk_ctx* ctx, const CgsSpec& c) {
         u.force3 = ctx->force3;
         u.coop = coop3(ctx);
         ST(run_upd(ctx, u, kn));
+        if (c.mark_final) ctx->prof_kern[2] = g_last_kern;
         if (u.coop) return TRPLK_OK;  // the third pass, when needed, ran inside the FINAL kernel
     }
     {  // third-pass dots h3 = V^T B w2, N_2SQ_EXP = w2^T B w2 (gated on ctl->pass3, normally a no-op)
@@ -945,6 +949,7 @@ trplk_status issue_cycle(trplk_ctx* ctx, const Sizes& S, int cur, int nprev, int
         if (ctx->prof_on) CK(cudaEventRecordWithFlags(ctx->pev[0], ctx->stream, cudaEventRecordExternal));
         if (small_path(ctx, S)) {
             launch_inner_small(sa, S.q, ctx->stream);
+            ctx->prof_kern[0] = g_last_kern;
         } else {
             GridArgs ga{sa, ctx->gridpart, nullptr};
             static const bool trace = getenv("TRPLK_GRID_TRACE") != nullptr;
@@ -956,6 +961,7 @@ trplk_status issue_cycle(trplk_ctx* ctx, const Sizes& S, int cur, int nprev, int
                 ctx->err = "cooperative launch of the grid-wide inner loop failed";
                 return TRPLK_ECUDA;
             }
+            ctx->prof_kern[0] = g_last_kern;
         }
         CK(cudaGetLastError());
         if (ctx->prof_on)
@@ -993,6 +999,7 @@ trplk_status issue_cycle(trplk_ctx* ctx, const Sizes& S, int cur, int nprev, int
             }
             if (prof) CK(cudaEventRecordWithFlags(ctx->pev[0], ctx->stream, cudaEventRecordExternal));
             ST(run_sdots(ctx, a, k));
+            if (prof) ctx->prof_kern[0] = g_last_kern;
             if (prof) CK(cudaEventRecordWithFlags(ctx->pev[1], ctx->stream, cudaEventRecordExternal));
             CgsSpec c{};
             if (prof) c.mark_final = ctx->pev[2];
@@ -2453,6 +2460,27 @@ trplk_status trplk_profile(trplk_ctx* ctx, int enable) {
     ctx->prof_on = enable != 0;
     for (int i = 0; i < 3; ++i) ctx->prof_ms[i] = ctx->prof_bytes[i] = 0.0;
     ctx->prof_count = 0;
+    return TRPLK_OK;
+}
+
+trplk_status trplk_profile_kernels(const trplk_ctx* ctx, char* buf, size_t len) {
+    if (!ctx || !buf || len == 0) return TRPLK_EINVAL;
+    std::string out;
+    for (int i = 0; i < 3; ++i) {
+        const char* name = nullptr;
+        if (ctx->prof_kern[i] && cudaFuncGetName(&name, ctx->prof_kern[i]) != cudaSuccess) name = nullptr;
+        std::string nm = name ? name : "";
+        if (name) {
+            int stt = 0;
+            char* dm = abi::__cxa_demangle(name, nullptr, nullptr, &stt);
+            if (dm && stt == 0) nm = dm;
+            free(dm);
+        }
+        out += nm;
+        if (i < 2) out += ";";
+    }
+    if (out.size() + 1 > len) return TRPLK_EINVAL;
+    memcpy(buf, out.c_str(), out.size() + 1);
     return TRPLK_OK;
 }
 

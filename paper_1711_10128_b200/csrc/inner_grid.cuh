@@ -13,11 +13,11 @@
 //   final     g_{j+1} = (w' - U h) / beta                                      -> grid barrier
 // Every CTA sums the CTA partials in the same fixed order, so all CTAs hold bit-identical
 // totals and take the same third-pass / breakdown decisions without a broadcast.  The dot
-// products use the DMMA fragment scheme of k_step1_rs (staged.cuh): each warp parks its
+// products use the DMMA fragment scheme of k_step1_rs2 (stream_rs.cuh): each warp parks its
 // 32-row tile of U in a shared-memory slab (row layout in registers -> fragment order).
 // Vectors written inside the launch (w, w', the new basis columns, the partials) are read
 // with ld.global.cg, never through the read-only path.  One rank, B = I, k <= 32.
-// Included by kernels.cu after staged.cuh (mat_row, dmma884_s, WLD, rs_chunk, warp_sum_s).
+// Included by kernels.cu after stream_rs.cuh (mat_row, dmma884_s, WLD, rs_chunk, warp_sum_s).
 #pragma once
 
 namespace trplk {
@@ -356,6 +356,7 @@ static bool launch_grid_k(const GridArgs& a, cudaStream_t s) {
     at[0].val.cooperative = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
+    NOTE_KERN(kern);
     return cudaLaunchKernelEx(&cfg, kern, a) == cudaSuccess;
 }
 

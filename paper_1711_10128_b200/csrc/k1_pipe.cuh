@@ -1,11 +1,11 @@
 // Software-pipelined K1 for DIA matrices with <= 8 diagonals and B = I (C2, C3, C5 shapes):
 //   z = A g, w = M (z - rho g) (eq 3.1 + R1), T(1:k,k) = U^T z, h1 = U^T w, ||w||^2.
-// Same per-tile arithmetic and summation order as k_step1_rs (staged.cuh), but a warp issues the
+// Same per-tile arithmetic and summation order as k_step1_rs2 (stream_rs.cuh), but a warp issues the
 // basis-row loads AND the DIA value / gather loads of its NEXT tile before it contracts the
 // current one (DMMA from the shared-memory slab), so the SpMV's dependent gathers -- the top
 // stall of k_step1_rs at C5 in ncu -- overlap a whole tile of work.
 // k <= 24 (one slab chunk); wider blocks use k_step1_rs.  Included by kernels.cu after
-// staged.cuh (WLD, dmma884_s, warp_sum_s).
+// stream_rs.cuh (WLD, dmma884_s, warp_sum_s).
 #pragma once
 
 namespace trplk {
@@ -145,6 +145,7 @@ template <int KMAX, bool TWO>
 static void launch_step1_pipe_k(const SdotsArgs& a, cudaStream_t s) {
     const int smem = WARPS * KMAX * WLD * (int)sizeof(double);
     auto kern = k_step1_pipe<KMAX, TWO>;
+    NOTE_KERN(kern);
     kern<<<rs_grid(kern, smem, a.nrows), CTA, smem, s>>>(a);
 }
 

@@ -1,12 +1,13 @@
 // Device kernels of the TRPL+K hot path, hand-written for sm_100a (B200).
 //
-//   k_sdots   K1/K7/K4: SELL-32 SpMV with A (and B) fused with the Jacobi preconditioner
-//             (or the residual) and with the dot products of a basis block against the
-//             result -- eq 3.1, R1, Alg.1 steps 12-15.
+//   k_sdots_mma / k_spmv_nd  K1/K7/K4 fallbacks: SpMV with A (and B) fused with the Jacobi
+//             preconditioner (or the residual) and the dot products of a basis block against
+//             the result -- eq 3.1, R1, Alg.1 steps 12-15 (the default K1
+//             kernels are in stream_rs.cuh / k1_pipe.cuh, the other dot launches stream_tp.cuh).
 //   k_upd     K2/K3: classical Gram-Schmidt update y = x - U h fused with the next pass's
 //             dots, or with the final normalisation (reading R3).
-//   k_eig     K6: one-CTA parallel-ordered cyclic Jacobi of T (Alg.1 step 11).
-//   k_rotate  K5: X = U Y on fp64 DMMA tensor cores (mma.sync m8n8k4 f64).
+//   k_rotate_t K5 for 48 < k <= 64: X = U Y on fp64 DMMA tensor cores (mma.sync m8n8k4 f64;
+//             P:193); k <= 48 uses k_rotate_s (rotate.cuh).  K6 (the RR eig) is eig.cu.
 //
 // Streaming kernels use one lane per row (32-row SELL slice = one warp tile) and issue the
 // whole row of the basis block U (k loads per lane) before the SpMV's dependent gathers, so
@@ -22,6 +23,8 @@
 #include "trplk_internal.cuh"
 
 namespace trplk {
+
+thread_local const void* g_last_kern = nullptr;
 
 // ------------------------------------------------------------------ helpers
 __device__ __forceinline__ double shx(double v, int m) { return __shfl_xor_sync(0xffffffffu, v, m); }
@@ -265,136 +268,6 @@ __device__ __forceinline__ void sdots_counts(const SdotsArgs& a, const Ctl* ctl,
 
 // KMAX = basis columns held in registers per chunk (the first chunk is issued before the SpMV);
 // wider blocks are processed in chunks of KMAX columns.
-template <int KMAX, bool TWO>
-__global__ void __launch_bounds__(CTA, 2) k_sdots(const SdotsArgs a) {
-    Ctl* ctl = a.ctl;
-    if ((ctl->flags & a.gate) != a.gate) return;
-    if (a.gate_pass3 && ctl->pass3 == 0) return;
-    int k1, k2;
-    sdots_counts(a, ctl, TWO, k1, k2);
-    double theta = 0.0;
-    if (a.out_mode >= 3)
-        theta = a.theta_idx >= 0 ? ctl->theta[a.theta_idx]
-                                 : (a.theta_idx == -1 ? ctl->theta[ctl->t - 1] : a.theta_val);
-    const double rho = ctl->rho;
-    const int nn = (a.norm1 ? 1 : 0) + (a.norm2 ? 1 : 0);
-    const int nv = k1 + k2 + nn;
-    const int kmx = k1 > k2 ? k1 : k2;
-    const double* __restrict__ X = resolve_x(a.x, a.x_dyn, a.x_ld, a.x_off, ctl);
-
-    __shared__ double acc[WARPS][NV_MAX];
-    __shared__ double res[NV_MAX];
-    for (int i = threadIdx.x; i < WARPS * NV_MAX; i += CTA) (&acc[0][0])[i] = 0.0;
-    __syncthreads();
-
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int64_t nslices = (a.nrows + 31) >> 5;
-    for (int64_t s = (int64_t)blockIdx.x * WARPS + warp; s < nslices; s += (int64_t)gridDim.x * WARPS) {
-        const int64_t row = s * 32 + lane;
-        const bool ok = row < a.nrows;
-        // issue the basis row first: its latency overlaps the SpMV's dependent gathers
-        double ur[KMAX > 0 ? KMAX : 1];
-#pragma unroll
-        for (int c = 0; c < KMAX; ++c) ur[c] = (ok && c < kmx) ? a.U[(int64_t)c * a.ldu + row] : 0.0;
-        double ad = 1.0, bd = 1.0, z = 0.0, sv = 0.0;
-        const double xr = ok ? X[row] : 0.0;
-        if (a.out_mode == 4)
-            ad = a.A.fmt == 1 ? __ldg(a.A.dval + (int64_t)a.A.diag_slot * a.A.ldv + row)
-                              : __ldg(a.A.val + __ldg(a.A.sptr + s) + lane);
-        else if (a.A.nrows) z = mat_row(a.A, s, lane, X, ad);
-        else z = xr;
-        if (a.out_mode >= 2) {
-            if (a.B.nrows) sv = mat_row(a.B, s, lane, X, bd);
-            else sv = xr;
-        }
-        double o = 0.0, minv = 1.0;
-        if (a.out_mode >= 2) {
-            double d = fabs(ad - a.sigma * bd);
-            d = d > a.mfloor ? d : a.mfloor;
-            minv = 1.0 / d;  // M_ii
-        }
-        switch (a.out_mode) {
-            case 1: o = z; break;
-            case 2: o = minv * (z - rho * sv); break;  // w = M (z - rho B g), R1
-            case 3: o = z - theta * sv; break;         // r = A x - theta B x
-            case 4: o = (ok ? a.wext[row] : 0.0) - theta * sv; break;
-            default: break;
-        }
-        if (ok) {
-            if (a.out) a.out[row] = o;
-            if (a.uout) a.uout[row] = minv * o;
-        } else {
-            z = 0.0;
-            o = 0.0;
-        }
-        if (KMAX > 0 && kmx > 0) {
-            const double v1 = a.set1 == 1 ? z : (a.set1 == 2 ? o : xr);
-          for (int cb = 0; cb < kmx; cb += KMAX) {
-            if (cb > 0) {
-#pragma unroll
-                for (int c = 0; c < KMAX; ++c)
-                    ur[c] = (ok && cb + c < kmx) ? a.U[(int64_t)(cb + c) * a.ldu + row] : 0.0;
-            }
-#pragma unroll
-            for (int cl = 0; cl < KMAX; cl += 8) {
-                const int c0 = cb + cl;
-                if (c0 < kmx) {
-                    double v[TWO ? 16 : 8];
-#pragma unroll
-                    for (int cc = 0; cc < 8; ++cc) {
-                        const int c = c0 + cc;
-                        v[cc] = (c < k1) ? ur[cl + cc] * v1 : 0.0;
-                        if constexpr (TWO) v[8 + cc] = (c < k2) ? ur[cl + cc] * o : 0.0;
-                    }
-                    if constexpr (TWO) {
-                        warp_butterfly<4>(v, lane);
-                        const int idx = (lane >> 1) & 15;
-                        if ((lane & 1) == 0) {
-                            const int col = c0 + (idx & 7);
-                            if (idx < 8) {
-                                if (col < k1) acc[warp][col] += v[0];
-                            } else {
-                                if (col < k2) acc[warp][k1 + col] += v[0];
-                            }
-                        }
-                    } else {
-                        warp_butterfly<3>(v, lane);
-                        const int idx = (lane >> 2) & 7;
-                        if ((lane & 3) == 0 && c0 + idx < k1) acc[warp][c0 + idx] += v[0];
-                    }
-                }
-            }
-          }
-        }
-        if (nn) {
-            const double p1 = a.norm1 == 1 ? o * o : a.norm1 == 2 ? xr * z : a.norm1 == 3 ? xr * xr : z * z;
-            const double p2 = a.norm2 == 1 ? o * o : a.norm2 == 2 ? xr * z : a.norm2 == 3 ? xr * xr : z * z;
-            const double n1 = warp_sum(ok ? p1 : 0.0);
-            const double n2 = a.norm2 ? warp_sum(ok ? p2 : 0.0) : 0.0;
-            if (lane == 0) {
-                int oo = k1 + k2;
-                if (a.norm1) acc[warp][oo++] += n1;
-                if (a.norm2) acc[warp][oo] += n2;
-            }
-        }
-    }
-    if (nv == 0) return;
-    __syncthreads();
-    for (int v = threadIdx.x; v < nv; v += CTA) {
-        double s = 0.0;
-#pragma unroll
-        for (int w = 0; w < WARPS; ++w) s += acc[w][v];
-        res[v] = s;
-    }
-    __syncthreads();
-    if (!grid_reduce(res, nv, a.part, a.gpart, a.counter, a.maxcta, res)) return;
-    if (a.red_local) {
-        for (int v = threadIdx.x; v < nv; v += CTA) a.red_local[v] = res[v];
-    } else {
-        sdots_finalize(a, res, k1, k2);
-    }
-}
-
 // -------------------------------------- SpMV-only launches (no basis dots): residual K7 etc.
 // r = A x - theta B x (u = M r), z = A x, w = M (z - rho B x) with up to two norms; R row tiles
 // per warp iteration so R tiles' value loads and gathers are in flight together, norms in
@@ -934,207 +807,7 @@ __global__ void k_finalize_multi(const SdotsArgs sd, const UpdArgs up, int which
     else upd_finalize(up, res, k1);
 }
 
-// ------------------------------------------------------- K6: one-CTA cyclic Jacobi
-// (first version, three barriers per round; superseded by eig.cu)
-#if 0
-constexpr int LDA = QMAX + 1;
-
-// Round-robin (circle) tournament: player at position `pos` in round r (player 0 fixed).
-__device__ __forceinline__ int rr_player(int pos, int r, int kk) {
-    return pos == 0 ? 0 : 1 + (pos - 1 + r) % (kk - 1);
-}
-
-// 256 threads: 8 threads per rotation pair (<= 32 disjoint pairs per round), each updating
-// every 8th row/column of the pair.
-__global__ void __launch_bounds__(256) k_eig(Ctl* ctl, double* T, int ldT, double* Y, int ldY, int ph,
-                                             int k_fixed, unsigned gate) {
-    if ((ctl->flags & gate) != gate) return;
-    const int k = k_fixed > 0 ? k_fixed : ctl->k;
-    extern __shared__ double sm[];
-    double* A = sm;
-    double* V = sm + QMAX * LDA;
-    __shared__ double cs[QMAX / 2], sn[QMAX / 2], red[256];
-    __shared__ int pp[QMAX / 2], qq[QMAX / 2], ord[QMAX];
-    __shared__ unsigned char tabp[QMAX - 1][QMAX / 2], tabq[QMAX - 1][QMAX / 2];
-    __shared__ int rotated;
-    __shared__ double fro;
-    const int tid = threadIdx.x;
-    double f = 0.0;
-    for (int j = 0; j < k; ++j)
-        for (int i = tid; i < k; i += blockDim.x) {
-            const double a = 0.5 * (T[i + (int64_t)j * ldT] + T[j + (int64_t)i * ldT]);  // sym(T)
-            A[i + j * LDA] = a;
-            V[i + j * LDA] = (i == j) ? 1.0 : 0.0;
-            f += a * a;
-        }
-    const int kk = k + (k & 1);
-    const int npairs = kk / 2;
-    for (int idx = tid; idx < (kk - 1) * npairs; idx += blockDim.x) {
-        const int r = idx / npairs, i = idx % npairs;
-        int p = rr_player(i, r, kk), q = rr_player(kk - 1 - i, r, kk);
-        if (p > q) { const int t = p; p = q; q = t; }
-        tabp[r][i] = (unsigned char)p;
-        tabq[r][i] = (unsigned char)q;
-    }
-    red[tid] = f;
-    __syncthreads();
-    if (tid == 0) {
-        double s = 0.0;
-        for (int i = 0; i < (int)blockDim.x; ++i) s += red[i];
-        fro = sqrt(s);
-    }
-    __syncthreads();
-    const double eps = 2.220446049250313e-16;
-    const int pi = tid >> 3, sub = tid & 7;
-    for (int sweep = 0; sweep < 100 && k > 1; ++sweep) {
-        if (tid == 0) rotated = 0;
-        __syncthreads();
-        for (int r = 0; r < kk - 1; ++r) {
-            if (tid < npairs) {
-                const int p = tabp[r][tid], q = tabq[r][tid];
-                pp[tid] = -1;
-                if (q < k) {
-                    const double apq = A[p + q * LDA], app = A[p + p * LDA], aqq = A[q + q * LDA];
-                    if (!(fabs(apq) <= eps * sqrt(fabs(app * aqq)) || fabs(apq) <= 1e-30 * fro)) {
-                        const double tau = (aqq - app) / (2.0 * apq);
-                        const double t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
-                        const double c = 1.0 / sqrt(1.0 + t * t);
-                        cs[tid] = c;
-                        sn[tid] = t * c;
-                        pp[tid] = p;
-                        qq[tid] = q;
-                        rotated = 1;
-                    }
-                }
-            }
-            __syncthreads();
-            // A <- A J and V <- V J (columns p, q of every rotated pair)
-            if (pi < npairs) {
-                const int p = pp[pi];
-                if (p >= 0) {
-                    const int q = qq[pi];
-                    const double c = cs[pi], s = sn[pi];
-                    for (int i = sub; i < k; i += 8) {
-                        const double aip = A[i + p * LDA], aiq = A[i + q * LDA];
-                        A[i + p * LDA] = c * aip - s * aiq;
-                        A[i + q * LDA] = s * aip + c * aiq;
-                        const double vip = V[i + p * LDA], viq = V[i + q * LDA];
-                        V[i + p * LDA] = c * vip - s * viq;
-                        V[i + q * LDA] = s * vip + c * viq;
-                    }
-                }
-            }
-            __syncthreads();
-            // A <- J^T A (rows p, q); the rotated entries (p,q), (q,p) are set to exactly 0
-            if (pi < npairs) {
-                const int p = pp[pi];
-                if (p >= 0) {
-                    const int q = qq[pi];
-                    const double c = cs[pi], s = sn[pi];
-                    for (int j = sub; j < k; j += 8) {
-                        const double apj = A[p + j * LDA], aqj = A[q + j * LDA];
-                        A[p + j * LDA] = (j == q) ? 0.0 : c * apj - s * aqj;
-                        A[q + j * LDA] = (j == p) ? 0.0 : s * apj + c * aqj;
-                    }
-                }
-            }
-            __syncthreads();
-        }
-        if (!rotated) break;
-        __syncthreads();
-    }
-    // ascending order, stable on ties (R11)
-    if (tid < k) {
-        const double ti = A[tid + tid * LDA];
-        int rank = 0;
-        for (int j = 0; j < k; ++j) {
-            const double tj = A[j + j * LDA];
-            rank += (tj < ti) || (tj == ti && j < tid);
-        }
-        ord[rank] = tid;
-    }
-    __syncthreads();
-    if (tid < k) {
-        const int src = ord[tid];
-        int imax = 0;
-        double vmax = -1.0;
-        for (int i = 0; i < k; ++i) {
-            const double a = fabs(V[i + src * LDA]);
-            if (a > vmax) { vmax = a; imax = i; }
-        }
-        const double sg = V[imax + src * LDA] < 0.0 ? -1.0 : 1.0;  // sign rule (R11)
-        for (int i = 0; i < k; ++i) Y[i + (int64_t)tid * ldY] = sg * V[i + src * LDA];
-        ctl->theta[tid] = A[src + src * LDA];
-    }
-    __syncthreads();
-    // restart: T <- diag(Theta(1:p^)) (R10)
-    if (ph > 0) {
-        for (int idx = tid; idx < QMAX * QMAX; idx += blockDim.x) {
-            const int i = idx % QMAX, j = idx / QMAX;
-            T[i + (int64_t)j * ldT] = (i == j && i < ph) ? ctl->theta[i] : 0.0;
-        }
-    }
-    if (tid == 0) ctl->k_rr = k;
-}
-#endif
-
 // ------------------------------------------------------- K5: DMMA rotation X = U Y
-
-template <int NT>
-__global__ void __launch_bounds__(256) k_rotate(const double* __restrict__ U, int64_t ldu, int64_t nrows,
-                                                const Ctl* ctl, int k_fixed, const double* __restrict__ Y,
-                                                int ldY, int ncol, double* __restrict__ X, int64_t ldx,
-                                                unsigned gate) {
-    if ((ctl->flags & gate) != gate) return;
-    const int k = k_fixed > 0 ? k_fixed : ctl->k_rr;
-    const int ksteps = (k + 3) >> 2;
-    __shared__ double Ys[QMAX][8 * NT + 1];
-    for (int idx = threadIdx.x; idx < QMAX * 8 * NT; idx += blockDim.x) {
-        const int kk = idx / (8 * NT), j = idx % (8 * NT);
-        Ys[kk][j] = (kk < k && j < ncol) ? Y[kk + (int64_t)j * ldY] : 0.0;
-    }
-    __syncthreads();
-    const int lane = threadIdx.x & 31;
-    const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    const int64_t ntile = (nrows + 7) >> 3;
-    const int ar = lane >> 2, ac = lane & 3;
-    for (int64_t tile = gw; tile < ntile; tile += nw) {
-        const int64_t r = tile * 8 + ar;
-        const bool ok = r < nrows;
-        double acc[NT][2];
-#pragma unroll
-        for (int nt = 0; nt < NT; ++nt) acc[nt][0] = acc[nt][1] = 0.0;
-        int ks = 0;
-        for (; ks + 4 <= ksteps; ks += 4) {
-            double av[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const int kk = 4 * (ks + u) + ac;
-                av[u] = (ok && kk < k) ? U[(int64_t)kk * ldu + r] : 0.0;
-            }
-#pragma unroll
-            for (int u = 0; u < 4; ++u)
-#pragma unroll
-                for (int nt = 0; nt < NT; ++nt) dmma884(acc[nt], av[u], Ys[4 * (ks + u) + ac][8 * nt + ar]);
-        }
-        for (; ks < ksteps; ++ks) {
-            const int kk = 4 * ks + ac;
-            const double av = (ok && kk < k) ? U[(int64_t)kk * ldu + r] : 0.0;
-#pragma unroll
-            for (int nt = 0; nt < NT; ++nt) dmma884(acc[nt], av, Ys[4 * ks + ac][8 * nt + ar]);
-        }
-        if (ok) {
-#pragma unroll
-            for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-                for (int e = 0; e < 2; ++e) {
-                    const int col = 8 * nt + 2 * ac + e;
-                    if (col < ncol) X[(int64_t)col * ldx + r] = acc[nt][e];
-                }
-        }
-    }
-}
 
 // Transposed-operand DMMA rotation (default): X^T = Y^T U^T, so the A operand (Y^T, p^ x k) is
 // loaded into registers once per warp and reused for every row tile, and the B operand is
@@ -1234,9 +907,8 @@ __global__ void k_gather(const double* x, const int* idx, int64_t n, double* out
 
 }  // namespace trplk
 
-#include "staged.cuh"     // TMA-staged K1 / K2 (shares the device helpers above)
+#include "stream_rs.cuh"  // register-stream + DMMA K1 (shares the device helpers above)
 #include "stream_tp.cuh"   // thread-per-row K1 / K2
-#include "stream_cp.cuh"   // cp.async-pipelined K1 / K2
 #include "rotate.cuh"      // shared-memory-staged DMMA rotation (default)
 #include "k1_pipe.cuh"     // software-pipelined K1 (DIA, B = I, k <= 24)
 #include "small.cuh"       // single-CTA inner loop for small n (latency path)
@@ -1246,49 +918,16 @@ __global__ void k_gather(const double* x, const int* idx, int64_t n, double* out
 namespace trplk {
 
 // ---------------------------------------------------------------- launchers
-// TRPLK_NO_TMA=1 selects the register-streaming K1/K2 (comparison / fallback of the same math)
-// Variant of the inner-step K1/K2 dot kernels (same outputs): "rs" (default) register stream +
-// smem transpose + DMMA; "tp" thread-per-row register accumulators (stream_tp.cuh); "tma"
-// bulk-copy staged; "reg" DMMA fragments loaded straight from global.  The other dot launches
-// (CGS first pass, +K T columns, residual) use the thread-per-row kernel.  B200 comparison
-// (C2 / C3 inner step): profiles/r01_variants.md.
-static int kvar() {
-    static int v = -1;
-    if (v < 0) {
-        const char* e = getenv("TRPLK_KVAR");
-        v = (e && !strcmp(e, "tma")) ? 1 : (e && !strcmp(e, "reg")) ? 2 : (e && !strcmp(e, "tp")) ? 0
-          : (e && !strcmp(e, "cp")) ? 4 : (e && !strcmp(e, "wp")) ? 5 : 3;
-    }
-    return v;
-}
-
-// K2 (CGS pass 2 with dots) variant: warp-pair `wp` (default) or TRPLK_K2=rs for the K1-family one
-static int k2var() {
-    static int v = -1;
-    if (v < 0) {
-        const char* e = getenv("TRPLK_K2");
-        v = (e && !strcmp(e, "rs")) ? 0 : 1;  // default: warp-pair K2 (measured: profiles/r01_variants.md)
-    }
-    return v;
-}
-
-// TRPLK_K1=wp: the warp-group K1 (inner-step shape)
+// K1 variant: default = the pipelined kernel (k1_pipe.cuh) for k <= 16 on slabs of >= 2^24 rows
+// (the C5 steps), else the two-tile register-stream kernel (stream_rs.cuh).  TRPLK_K1=pipe /
+// TRPLK_K1=rs force one of them wherever it applies (parity tests of both on every shape).
 static int k1var() {
     static int v = -1;
     if (v < 0) {
         const char* e = getenv("TRPLK_K1");
-        v = (e && !strcmp(e, "wp")) ? 1 : (e && !strcmp(e, "pipe")) ? 2 : 0;
+        v = (e && !strcmp(e, "pipe")) ? 2 : (e && !strcmp(e, "rs")) ? 1 : 0;
     }
     return v;
-}
-
-static bool coop_final() {  // experiment: FINAL as a cooperative launch (TRPLK_COOP=1)
-    static int v = -1;
-    if (v < 0) {
-        const char* e = getenv("TRPLK_COOP");
-        v = (e && e[0] == '1') ? 1 : 0;
-    }
-    return v == 1;
 }
 
 static int num_sms() {
@@ -1340,46 +979,34 @@ int kmax_bucket(int k) {
     return 64;
 }
 
-#define SD_CASE(KM)                                                                      \
-    case KM:                                                                             \
-        if (a.set2) {                                                                    \
-            auto kern = k_sdots<KM, true>;                                               \
-            kern<<<stream_grid(kern, a.nrows), CTA, 0, s>>>(a);                          \
-        } else {                                                                         \
-            auto kern = k_sdots<KM, false>;                                              \
-            kern<<<stream_grid(kern, a.nrows), CTA, 0, s>>>(a);                          \
-        }                                                                                \
-        break;
-
 #define SDM_CASE(NG)                                                                     \
     case NG:                                                                             \
         if (a.set2) {                                                                    \
             auto kern = k_sdots_mma<NG, true>;                                           \
+            NOTE_KERN(kern);                                                             \
             kern<<<stream_grid(kern, a.nrows), CTA, 0, s>>>(a);                          \
         } else {                                                                         \
             auto kern = k_sdots_mma<NG, false>;                                          \
+            NOTE_KERN(kern);                                                             \
             kern<<<stream_grid(kern, a.nrows), CTA, 0, s>>>(a);                          \
         }                                                                                \
         break;
 
 void launch_sdots(const SdotsArgs& a, int kmax, cudaStream_t s) {
-    // inner-step K1 (and the T-column-only launches): TMA-staged basis stream
+    // inner-step K1 shape: z = A g, w = M (z - rho B g), U^T z (+ U^T w, ||w||^2)
     const bool k1_shape = a.A.nrows && a.out_mode <= 2 && a.set1 == 1 && (a.set2 == 0 || a.set2 == 2) &&
                           (a.norm1 >= 0 && a.norm1 <= 2) && a.norm2 == 0 && a.x_dyn == 0 && a.uout == nullptr;
-    if (kmax > 0 && (kvar() == 0 || (kvar() >= 3 && !k1_shape)) && a.out_mode != 4 && launch_step1_tp(a, kmax, s))
-        return;
     if (kmax > 0 && k1_shape) {
-        if (k1var() == 1 && launch_step1_wp(a, kmax, s)) return;
         // pipelined K1: measured faster on long tile loops with a register-resident row (C5,
         // k <= 16: 10.98 vs 11.53 ms per inner step); equal or slower elsewhere
         if ((k1var() == 2 || (k1var() == 0 && kmax <= 16 && a.nrows >= (int64_t)1 << 24)) &&
             launch_step1_pipe(a, kmax, s))
             return;
-        if (kvar() == 3 && launch_step1_rs(a, kmax, s)) return;
-        if (kvar() == 4 && launch_step1_cp(a, kmax, s)) return;
-        if (kvar() == 1 && launch_step1_tma(a, kmax, s)) return;
+        if (launch_step1_rs(a, kmax, s)) return;
     }
-    if (kmax > 0 && a.out_mode != 4) {  // dots: DMMA accumulator kernel
+    // every other dot launch (CGS first pass, +K T columns, start-block Gram): thread-per-row
+    if (kmax > 0 && a.out_mode != 4 && launch_step1_tp(a, kmax, s)) return;
+    if (kmax > 0 && a.out_mode != 4) {  // dots beyond the bucketed widths: DMMA accumulator kernel
         switch ((kmax + 7) / 8) {
             SDM_CASE(1)
             SDM_CASE(2)
@@ -1393,29 +1020,22 @@ void launch_sdots(const SdotsArgs& a, int kmax, cudaStream_t s) {
         }
         return;
     }
-    if (kmax == 0 && getenv("TRPLK_OLD_ND") == nullptr) {  // SpMV-only launch (residual, plain SpMV)
-        auto kern = k_spmv_nd<2>;
-        kern<<<stream_grid(kern, (a.nrows + 1) / 2), CTA, 0, s>>>(a);
-        return;
-    }
-    switch (kmax > 32 ? 32 : kmax) {  // columns beyond 32 are processed in further chunks
-        SD_CASE(0)
-        SD_CASE(8)
-        SD_CASE(16)
-        SD_CASE(24)
-        default:
-        SD_CASE(32)
-    }
+    // SpMV-only launch (residual, plain SpMV, start-block residual from W)
+    auto kern = k_spmv_nd<2>;
+    NOTE_KERN(kern);
+    kern<<<stream_grid(kern, (a.nrows + 1) / 2), CTA, 0, s>>>(a);
 }
 
 #define UP_CASE(KM)                                                \
     case KM: {                                                     \
         if (a.mode == 1 && a.dots) {                               \
             auto kern = k_upd<KM, true>;                           \
+            NOTE_KERN(kern);                                       \
             kern<<<stream_grid(kern, a.nrows), CTA, 0, s>>>(a);    \
         } else {                                                   \
             auto kern = k_upd<KM, false>;                          \
-            if (a.mode == 2 && (a.coop || coop_final())) {         \
+            NOTE_KERN(kern);                                       \
+            if (a.mode == 2 && a.coop) {                           \
                 cudaLaunchConfig_t cfg{};                          \
                 cfg.gridDim = stream_grid(kern, a.nrows);          \
                 cfg.blockDim = CTA;                                \
@@ -1433,13 +1053,8 @@ void launch_sdots(const SdotsArgs& a, int kmax, cudaStream_t s) {
     } break;
 
 void launch_upd(const UpdArgs& a, int kmax, cudaStream_t s) {
-    if (a.mode == 1 && a.dots) {
-        if (kvar() == 0 && launch_upd2_tp(a, kmax, s)) return;
-        if (kvar() == 4 && launch_upd2_cp(a, kmax, s)) return;
-        if ((kvar() == 5 || k2var() == 1) && launch_upd2_wp(a, kmax, s)) return;
-        if (kvar() == 3 && launch_upd2_rs(a, kmax, s)) return;
-        if (kvar() == 1 && launch_upd2_tma(a, kmax, s)) return;
-    }
+    // CGS pass 2 with dots: warp-group two-tile kernel (stream_tp.cuh)
+    if (a.mode == 1 && a.dots && launch_upd2_wp(a, kmax, s)) return;
     switch (kmax) {
         UP_CASE(8)
         UP_CASE(16)
@@ -1472,47 +1087,23 @@ static void rot_t(const double* U, int64_t ldu, int64_t nrows, const Ctl* ctl, i
 template <int NJ>
 static void rot_t_k(int kmax, const double* U, int64_t ldu, int64_t nrows, const Ctl* ctl, int k_fixed,
                     const double* Y, int ldY, int ncol, double* X, int64_t ldx, unsigned gate, cudaStream_t s) {
-    const int ks4 = (kmax + 3) / 4;
-    if (ks4 <= 2) rot_t<NJ, 2>(U, ldu, nrows, ctl, k_fixed, Y, ldY, ncol, X, ldx, gate, s);
-    else if (ks4 <= 4) rot_t<NJ, 4>(U, ldu, nrows, ctl, k_fixed, Y, ldY, ncol, X, ldx, gate, s);
-    else if (ks4 <= 6) rot_t<NJ, 6>(U, ldu, nrows, ctl, k_fixed, Y, ldY, ncol, X, ldx, gate, s);
-    else if (ks4 <= 8) rot_t<NJ, 8>(U, ldu, nrows, ctl, k_fixed, Y, ldY, ncol, X, ldx, gate, s);
-    else if (ks4 <= 10) rot_t<NJ, 10>(U, ldu, nrows, ctl, k_fixed, Y, ldY, ncol, X, ldx, gate, s);
-    else if (ks4 <= 12) rot_t<NJ, 12>(U, ldu, nrows, ctl, k_fixed, Y, ldY, ncol, X, ldx, gate, s);
-    else rot_t<NJ, 16>(U, ldu, nrows, ctl, k_fixed, Y, ldY, ncol, X, ldx, gate, s);
+    (void)kmax;  // only 48 < k <= 64 comes here
+    rot_t<NJ, 16>(U, ldu, nrows, ctl, k_fixed, Y, ldY, ncol, X, ldx, gate, s);
 }
 
 // kmax: upper bound of the device-side width (k_fixed, or the solve's max basis q).
-// Default: k_rotate_s (rotate.cuh); TRPLK_ROT=t the register-fragment k_rotate_t, TRPLK_ROT=mma8
-// the row-operand k_rotate (8-row tiles, Y in shared memory).
+// k <= 48: k_rotate_s (rotate.cuh, U tile staged in shared memory); 48 < k <= 64: the
+// register-fragment k_rotate_t (the shared-memory slab of 64 columns would leave one CTA per SM).
 void launch_rotate(const double* U, int64_t ldu, int64_t nrows, const Ctl* ctl, int k_fixed, const double* Y,
                    int ldY, int ncol, double* X, int64_t ldx, unsigned gate, cudaStream_t s, int kmax) {
-    static int var = -1;
-    if (var < 0) {
-        const char* e = getenv("TRPLK_ROT");
-        var = (e && !strcmp(e, "mma8")) ? 1 : (e && !strcmp(e, "t")) ? 2 : 0;
-    }
     if (k_fixed > 0) kmax = k_fixed;
-    if (var == 0 && ncol <= 24) {
-        const bool done = ncol <= 8    ? rot_s_k<1>(kmax, U, ldu, nrows, ctl, k_fixed, Y, ldY, ncol, X, ldx, gate, s)
-                          : ncol <= 16 ? rot_s_k<2>(kmax, U, ldu, nrows, ctl, k_fixed, Y, ldY, ncol, X, ldx, gate, s)
-                                       : rot_s_k<3>(kmax, U, ldu, nrows, ctl, k_fixed, Y, ldY, ncol, X, ldx, gate, s);
-        if (done) return;
-    }
-    if (var == 2 && kmax <= 64 && ncol <= 24) {
-        if (ncol <= 8) rot_t_k<1>(kmax, U, ldu, nrows, ctl, k_fixed, Y, ldY, ncol, X, ldx, gate, s);
-        else if (ncol <= 16) rot_t_k<2>(kmax, U, ldu, nrows, ctl, k_fixed, Y, ldY, ncol, X, ldx, gate, s);
-        else rot_t_k<3>(kmax, U, ldu, nrows, ctl, k_fixed, Y, ldY, ncol, X, ldx, gate, s);
-        return;
-    }
-    const int64_t tiles = (nrows + 7) / 8;
-    int64_t g = (tiles + 7) / 8;
-    const int64_t cap = (int64_t)num_sms() * 8;
-    if (g > cap) g = cap;
-    if (g < 1) g = 1;
-    if (ncol <= 8) k_rotate<1><<<(int)g, 256, 0, s>>>(U, ldu, nrows, ctl, k_fixed, Y, ldY, ncol, X, ldx, gate);
-    else if (ncol <= 16) k_rotate<2><<<(int)g, 256, 0, s>>>(U, ldu, nrows, ctl, k_fixed, Y, ldY, ncol, X, ldx, gate);
-    else k_rotate<3><<<(int)g, 256, 0, s>>>(U, ldu, nrows, ctl, k_fixed, Y, ldY, ncol, X, ldx, gate);
+    const bool done = ncol <= 8    ? rot_s_k<1>(kmax, U, ldu, nrows, ctl, k_fixed, Y, ldY, ncol, X, ldx, gate, s)
+                      : ncol <= 16 ? rot_s_k<2>(kmax, U, ldu, nrows, ctl, k_fixed, Y, ldY, ncol, X, ldx, gate, s)
+                                   : rot_s_k<3>(kmax, U, ldu, nrows, ctl, k_fixed, Y, ldY, ncol, X, ldx, gate, s);
+    if (done) return;
+    if (ncol <= 8) rot_t_k<1>(kmax, U, ldu, nrows, ctl, k_fixed, Y, ldY, ncol, X, ldx, gate, s);
+    else if (ncol <= 16) rot_t_k<2>(kmax, U, ldu, nrows, ctl, k_fixed, Y, ldY, ncol, X, ldx, gate, s);
+    else rot_t_k<3>(kmax, U, ldu, nrows, ctl, k_fixed, Y, ldY, ncol, X, ldx, gate, s);
 }
 
 void launch_random(double* x, int64_t nrows, int64_t row0, int64_t n_global, uint64_t seed, uint64_t stream,

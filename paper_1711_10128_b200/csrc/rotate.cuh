@@ -9,7 +9,7 @@
 // the slab, and the accumulator holds 2 consecutive rows of one output column per lane,
 // written as one 16-byte store.  The ncu capture of the register-fragment version at C5 showed
 // lg_throttle + long_scoreboard stalls: its loads touched 4 columns x 64 bytes per instruction.
-// Included by kernels.cu after staged.cuh (WLD, dmma884_s).
+// Included by kernels.cu after stream_rs.cuh (WLD, dmma884_s).
 #pragma once
 
 namespace trplk {
@@ -90,6 +90,7 @@ static void rot_s(const double* U, int64_t ldu, int64_t nrows, const Ctl* ctl, i
     int64_t g = (int64_t)nsm * occ;
     if (need < g) g = need;
     if (g < 1) g = 1;
+    NOTE_KERN(kern);
     kern<<<(int)g, CTA, smem, s>>>(U, ldu, nrows, ctl, k_fixed, Y, ldY, ncol, X, ldx, gate);
 }
 

@@ -185,6 +185,7 @@ __global__ void __launch_bounds__(SMALL_CTA, 1) k_inner_small(const SmallArgs a)
 
 template <int KMAX>
 static void launch_small_k(const SmallArgs& a, cudaStream_t s) {
+    NOTE_KERN(k_inner_small<KMAX>);
     k_inner_small<KMAX><<<1, SMALL_CTA, 0, s>>>(a);
 }
 

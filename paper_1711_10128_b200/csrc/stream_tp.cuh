@@ -1,10 +1,10 @@
-// Thread-per-row streaming variants of the two dot-product kernels of the inner step.
+// Streaming dot kernels of the solver besides the inner-step K1 (stream_rs.cuh / k1_pipe.cuh):
 //
-//   k_step1_tp  K1: z = A g, w = M (z - rho B g), T(1:k,k) = U^T z, h1 = U^T w, ||w||^2
-//               (eq 3.1, with the preconditioner of P:143 as reading R1);
-//               every other dot launch of the solver too (CGS first pass U^T B x, +K T columns,
-//               residual r = A x - theta B x with u = M r): all modes of SdotsArgs.
-//   k_upd2_tp   K2: w' = w - U h1, h2 = U^T w', ||w'||^2   (CGS pass 2, reading R3)
+//   k_step1_tp  thread-per-row: every dot launch that is not the inner-step K1 -- the CGS first
+//               pass U^T B x of the seed and +K vectors (reading R3), the +K T columns
+//               (Alg. 1 step 8), the start-block Gram -- all modes of
+//               SdotsArgs (z = A x, w = M (z - rho B x), residual r = A x - theta B x, u = M r).
+//   k_upd2_wp2  K2, warp-group: w' = w - U h1, h2 = U^T w', ||w'||^2  (CGS pass 2, reading R3)
 //
 // Layout: a warp tile is TR = 32/S consecutive rows; the k basis columns are split over the S
 // lane groups (group g owns columns [g*KS, g*KS+KS)), so each lane keeps its KS values of U
@@ -158,102 +158,6 @@ __global__ void __launch_bounds__(CTA, 1) k_step1_tp(const SdotsArgs a) {
     }
 }
 
-template <int KS, int S, bool PF>
-__global__ void __launch_bounds__(CTA, 1) k_upd2_tp(const UpdArgs a) {
-    constexpr int TR = 32 / S;
-    Ctl* ctl = a.ctl;
-    if ((ctl->flags & a.gate) != a.gate) return;
-    const int kv = a.kv >= 0 ? a.kv : ctl->k;
-    const double* __restrict__ X = resolve_x(a.x, a.x_dyn, a.x_ld, a.x_off, ctl);
-    __shared__ double hs[S * KS];
-    __shared__ double acc[WARPS][QMAX + 1];
-    __shared__ double res[QMAX + 1];
-    for (int i = threadIdx.x; i < S * KS; i += CTA) hs[i] = i < kv ? ctl->h[a.hslot][i] : 0.0;
-    __syncthreads();
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int grp = lane / TR, rr = lane % TR;
-    const int c0 = grp * KS;
-    double hr[KS], d[KS];
-#pragma unroll
-    for (int c = 0; c < KS; ++c) {
-        hr[c] = hs[c0 + c];
-        d[c] = 0.0;
-    }
-    double yy = 0.0;
-    const int64_t ntile = (a.nrows + TR - 1) / TR;
-    const double* ub = a.U + (int64_t)c0 * a.ldu;
-    const int64_t tstride = (int64_t)gridDim.x * WARPS;
-    double un[PF ? KS : 1];
-    double xn = 0.0;
-    if (PF) {
-        const int64_t row = ((int64_t)blockIdx.x * WARPS + warp) * TR + rr;
-#pragma unroll
-        for (int c = 0; c < KS; ++c)
-            un[c] = (row < a.nrows && c0 + c < kv) ? __ldg(ub + (int64_t)c * a.ldu + row) : 0.0;
-        xn = row < a.nrows ? X[row] : 0.0;
-    }
-    for (int64_t t = (int64_t)blockIdx.x * WARPS + warp; t < ntile; t += tstride) {
-        const int64_t row = t * TR + rr;
-        const bool ok = row < a.nrows;
-        double u[KS];
-        double xv;
-        if (PF) {
-            const int64_t rn = row + tstride * TR;
-#pragma unroll
-            for (int c = 0; c < KS; ++c) {
-                u[c] = un[c];
-                un[c] = (rn < a.nrows && c0 + c < kv) ? __ldg(ub + (int64_t)c * a.ldu + rn) : 0.0;
-            }
-            xv = xn;
-            xn = rn < a.nrows ? X[rn] : 0.0;
-        } else {
-#pragma unroll
-            for (int c = 0; c < KS; ++c) u[c] = (ok && c0 + c < kv) ? __ldg(ub + (int64_t)c * a.ldu + row) : 0.0;
-            xv = ok ? X[row] : 0.0;
-        }
-        // y = x - U h: columns in order inside a group, groups combined low to high
-        double s = 0.0;
-#pragma unroll
-        for (int c = 0; c < KS; ++c) s = fma(hr[c], u[c], s);
-        if (S == 2) {
-            const double o = __shfl_xor_sync(0xffffffffu, s, TR);
-            s = grp == 0 ? s + o : o + s;
-        }
-        const double y = ok ? xv - s : 0.0;
-        if (ok && grp == 0 && a.out) a.out[row] = y;
-        if (grp == 0) yy = fma(y, y, yy);
-#pragma unroll
-        for (int c = 0; c < KS; ++c) d[c] = fma(u[c], y, d[c]);
-    }
-#pragma unroll
-    for (int c = 0; c < KS; ++c) {
-#pragma unroll
-        for (int off = 1; off < TR; off <<= 1) d[c] += __shfl_xor_sync(0xffffffffu, d[c], off);
-    }
-    if (rr == 0) {
-#pragma unroll
-        for (int c = 0; c < KS; ++c)
-            if (c0 + c < kv) acc[warp][c0 + c] = d[c];
-    }
-    const double ys = warp_sum(yy);
-    if (lane == 0) acc[warp][kv] = ys;
-    __syncthreads();
-    const int nv = kv + 1;
-    for (int v = threadIdx.x; v < nv; v += CTA) {
-        double s = 0.0;
-#pragma unroll
-        for (int w = 0; w < WARPS; ++w) s += acc[w][v];
-        res[v] = s;
-    }
-    __syncthreads();
-    if (!grid_reduce(res, nv, a.part, a.gpart, a.counter, a.maxcta, res)) return;
-    if (a.red_local) {
-        for (int v = threadIdx.x; v < nv; v += CTA) a.red_local[v] = res[v];
-    } else {
-        upd_finalize(a, res, kv);
-    }
-}
-
 // ------------------------------------------------------------------ launchers
 template <typename K>
 static int tp_grid(K kern, int64_t nrows, int tr) {
@@ -268,12 +172,6 @@ static int tp_grid(K kern, int64_t nrows, int tr) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, CTA, 0);
     if (occ < 1) occ = 1;
     const int64_t need = ((nrows + tr - 1) / tr + WARPS - 1) / WARPS;
-    static const int spw = getenv("TRPLK_TP_SPW") ? atoi(getenv("TRPLK_TP_SPW")) : 0;  // experiment knob
-    if (spw > 0) {
-        int64_t g = (need + spw - 1) / spw;
-        if (g > MAXCTA) g = MAXCTA;
-        return (int)(g < 1 ? 1 : g);
-    }
     int64_t cap = (int64_t)nsm * occ;
     if (cap > MAXCTA) cap = MAXCTA;
     if (need <= cap) return (int)(need < 1 ? 1 : need);
@@ -281,37 +179,11 @@ static int tp_grid(K kern, int64_t nrows, int tr) {
     return (int)((need + waves - 1) / waves);
 }
 
-// TRPLK_TP_PF=1: prefetch variants (next tile's U row loaded during the current tile)
-static bool tp_pf() {
-    static int v = -1;
-    if (v < 0) {
-        const char* e = getenv("TRPLK_TP_PF");
-        v = (e && e[0] == '1') ? 1 : 0;
-    }
-    return v == 1;
-}
-
 template <int KS, int S, bool TWO>
 static void launch_step1_tp_k(const SdotsArgs& a, cudaStream_t s) {
-    constexpr bool PFOK = TWO ? KS <= 16 : KS <= 24;
-    if (PFOK && tp_pf()) {
-        auto kern = k_step1_tp<KS, S, TWO, PFOK>;
-        kern<<<tp_grid(kern, a.nrows, 32 / S), CTA, 0, s>>>(a);
-    } else {
-        auto kern = k_step1_tp<KS, S, TWO, false>;
-        kern<<<tp_grid(kern, a.nrows, 32 / S), CTA, 0, s>>>(a);
-    }
-}
-
-template <int KS, int S>
-static void launch_upd2_tp_k(const UpdArgs& a, cudaStream_t s) {
-    if (tp_pf()) {
-        auto kern = k_upd2_tp<KS, S, true>;
-        kern<<<tp_grid(kern, a.nrows, 32 / S), CTA, 0, s>>>(a);
-    } else {
-        auto kern = k_upd2_tp<KS, S, false>;
-        kern<<<tp_grid(kern, a.nrows, 32 / S), CTA, 0, s>>>(a);
-    }
+    auto kern = k_step1_tp<KS, S, TWO, false>;
+    NOTE_KERN(kern);
+    kern<<<tp_grid(kern, a.nrows, 32 / S), CTA, 0, s>>>(a);
 }
 
 // Column split by width: k <= 24 one group of KS columns (S = 1); k <= 64 two groups (S = 2).
@@ -332,108 +204,15 @@ bool launch_step1_tp(const SdotsArgs& a, int kmax, cudaStream_t s) {
     return true;
 }
 
-bool launch_upd2_tp(const UpdArgs& a, int kmax, cudaStream_t s) {
-    switch (kmax) {
-        case 8: launch_upd2_tp_k<8, 1>(a, s); break;
-        case 16: launch_upd2_tp_k<16, 1>(a, s); break;
-        case 24: launch_upd2_tp_k<24, 1>(a, s); break;
-        case 32: launch_upd2_tp_k<16, 2>(a, s); break;
-        case 40: launch_upd2_tp_k<20, 2>(a, s); break;
-        case 48: launch_upd2_tp_k<24, 2>(a, s); break;
-        case 64: launch_upd2_tp_k<32, 2>(a, s); break;
-        default: return false;
-    }
-    return true;
-}
-
-
-// K2 with the columns split over a group of G = 2 (k <= 32) or 4 warps ("wp"): warp w of a group
+// K2 (CGS pass 2 with dots) with the columns split over a group of G = 2 (k <= 32) or 4 warps ("wp"): warp w of a group
 // owns columns [w*KS, w*KS+KS) of the same 32-row tile (lane = row, every column read a full 256-byte
 // segment), keeps its KS values of U and KS dot accumulators in registers, and the two halves
 // parts of y = x - U h are combined through shared memory behind a group barrier (bar.sync,
 // 32 G threads).  All k column loads of a tile are in flight at once with <= 128 registers, so
 // k <= 48 runs 2 CTAs (16 warps) per SM -- the register budget the single-warp `tp` misses.
-template <int KS, int G>
-__global__ void __launch_bounds__(CTA, 2) k_upd2_wp(const UpdArgs a) {
-    constexpr int NGR = WARPS / G;
-    Ctl* ctl = a.ctl;
-    if ((ctl->flags & a.gate) != a.gate) return;
-    const int kv = a.kv >= 0 ? a.kv : ctl->k;
-    const double* __restrict__ X = resolve_x(a.x, a.x_dyn, a.x_ld, a.x_off, ctl);
-    __shared__ double hs[G * KS];
-    __shared__ double sb[2][NGR][G][32];
-    __shared__ double acc[WARPS][QMAX + 1];
-    __shared__ double res[QMAX + 1];
-    for (int i = threadIdx.x; i < G * KS; i += CTA) hs[i] = i < kv ? ctl->h[a.hslot][i] : 0.0;
-    for (int i = threadIdx.x; i < WARPS * (QMAX + 1); i += CTA) (&acc[0][0])[i] = 0.0;
-    __syncthreads();
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int grp = warp / G, wg = warp % G;
-    const int c0 = wg * KS;
-    double d[KS];
-#pragma unroll
-    for (int c = 0; c < KS; ++c) d[c] = 0.0;
-    double yy = 0.0;
-    const int64_t ntile = (a.nrows + 31) >> 5;
-    const double* ub = a.U + (int64_t)c0 * a.ldu;
-    int par = 0;
-    for (int64_t t = (int64_t)blockIdx.x * NGR + grp; t < ntile; t += (int64_t)gridDim.x * NGR) {
-        const int64_t row = t * 32 + lane;
-        const bool ok = row < a.nrows;
-        double u[KS];
-#pragma unroll
-        for (int c = 0; c < KS; ++c) u[c] = (ok && c0 + c < kv) ? __ldg(ub + (int64_t)c * a.ldu + row) : 0.0;
-        const double xv = ok ? X[row] : 0.0;
-        double sp = 0.0;
-#pragma unroll
-        for (int c = 0; c < KS; ++c) sp = fma(hs[c0 + c], u[c], sp);
-        sb[par][grp][wg][lane] = sp;
-        asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "r"(32 * G) : "memory");
-        double s = sb[par][grp][0][lane];
-#pragma unroll
-        for (int w = 1; w < G; ++w) s += sb[par][grp][w][lane];
-        par ^= 1;
-        const double y = ok ? xv - s : 0.0;
-        if (wg == 0) {
-            if (ok && a.out) a.out[row] = y;
-            yy = fma(y, y, yy);
-        }
-#pragma unroll
-        for (int c = 0; c < KS; ++c) d[c] = fma(u[c], y, d[c]);
-    }
-#pragma unroll
-    for (int c = 0; c < KS; ++c) {
-#pragma unroll
-        for (int off = 1; off < 32; off <<= 1) d[c] += __shfl_xor_sync(0xffffffffu, d[c], off);
-    }
-    if (lane == 0) {
-#pragma unroll
-        for (int c = 0; c < KS; ++c)
-            if (c0 + c < kv) acc[warp][c0 + c] = d[c];
-    }
-    const double ys = warp_sum(yy);
-    __syncthreads();
-    if (lane == 0 && wg == 0) acc[warp][kv] = ys;
-    __syncthreads();
-    const int nv = kv + 1;
-    for (int v = threadIdx.x; v < nv; v += CTA) {
-        double sum = 0.0;
-#pragma unroll
-        for (int w = 0; w < WARPS; ++w) sum += acc[w][v];
-        res[v] = sum;
-    }
-    __syncthreads();
-    if (!grid_reduce(res, nv, a.part, a.gpart, a.counter, a.maxcta, res)) return;
-    if (a.red_local) {
-        for (int v = threadIdx.x; v < nv; v += CTA) a.red_local[v] = res[v];
-    } else {
-        upd_finalize(a, res, kv);
-    }
-}
-
-// k_upd2_wp with two 32-row tiles per warp-group iteration (default; TRPLK_WP1=1 for one):
-// both tiles' column loads in flight together, one group barrier for both, half the dependent
-// load round trips per warp (as k_step1_rs2 for K1).
+// Two 32-row tiles per warp-group iteration: both tiles' column loads in flight together, one
+// group barrier for both, half the dependent load round trips per warp (as k_step1_rs2 for K1;
+// the one-tile kernel measured slower and was removed).
 template <int KS, int G>
 __global__ void __launch_bounds__(CTA, 2) k_upd2_wp2(const UpdArgs a) {
     constexpr int NGR = WARPS / G;
@@ -530,14 +309,9 @@ __global__ void __launch_bounds__(CTA, 2) k_upd2_wp2(const UpdArgs a) {
 
 template <int KS, int G>
 static void launch_upd2_wp_k(const UpdArgs& a, cudaStream_t s) {
-    static const bool one = getenv("TRPLK_WP1") && getenv("TRPLK_WP1")[0] == '1';
-    if (!one) {
-        auto kern2 = k_upd2_wp2<KS, G>;
-        kern2<<<tp_grid(kern2, (a.nrows + 1) / 2, 8 * G), CTA, 0, s>>>(a);
-        return;
-    }
-    auto kern = k_upd2_wp<KS, G>;
-    kern<<<tp_grid(kern, a.nrows, 8 * G), CTA, 0, s>>>(a);  // WARPS/G tiles of 32 rows per CTA at a time
+    auto kern2 = k_upd2_wp2<KS, G>;
+    NOTE_KERN(kern2);
+    kern2<<<tp_grid(kern2, (a.nrows + 1) / 2, 8 * G), CTA, 0, s>>>(a);
 }
 
 bool launch_upd2_wp(const UpdArgs& a, int kmax, cudaStream_t s) {
@@ -551,126 +325,6 @@ bool launch_upd2_wp(const UpdArgs& a, int kmax, cudaStream_t s) {
         case 64: launch_upd2_wp_k<16, 4>(a, s); break;
         default: return false;
     }
-    return true;
-}
-
-
-// K1 with the columns split over a group of G warps ("wp"): every warp of the group computes
-// the SpMV + preconditioner of the same 32 rows (the value/gather loads of the G warps coincide
-// in L1), keeps KS columns of U and 2 KS dot accumulators in registers, so k <= 48 fits 2 CTAs
-// per SM with all of a tile's column loads in flight.  Inner-step shape only (z = A g,
-// out_mode <= 2, dot sets {z, w}, norm w.w); other dot launches use k_step1_tp.
-template <int KS, int G, bool TWO>
-__global__ void __launch_bounds__(CTA, 2) k_step1_wp(const SdotsArgs a) {
-    constexpr int NGR = WARPS / G;
-    Ctl* ctl = a.ctl;
-    if ((ctl->flags & a.gate) != a.gate) return;
-    if (a.gate_pass3 && ctl->pass3 == 0) return;
-    int k1, k2;
-    sdots_counts(a, ctl, TWO, k1, k2);
-    const int kmx = k1 > k2 ? k1 : k2;
-    const double rho = ctl->rho;
-    const int nn = a.norm1 ? 1 : 0;
-    const int nv = k1 + k2 + nn;
-    const double* __restrict__ X = a.x;
-    __shared__ double acc[WARPS][NV_MAX];
-    __shared__ double res[NV_MAX];
-    for (int i = threadIdx.x; i < WARPS * NV_MAX; i += CTA) (&acc[0][0])[i] = 0.0;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int grp = warp / G, wg = warp % G;
-    const int c0 = wg * KS;
-    double a1[KS], a2[TWO ? KS : 1];
-#pragma unroll
-    for (int c = 0; c < KS; ++c) {
-        a1[c] = 0.0;
-        if (TWO) a2[c] = 0.0;
-    }
-    double n1 = 0.0;
-    const int64_t ntile = (a.nrows + 31) >> 5;
-    const double* ub = a.U + (int64_t)c0 * a.ldu;
-    for (int64_t t = (int64_t)blockIdx.x * NGR + grp; t < ntile; t += (int64_t)gridDim.x * NGR) {
-        const int64_t row = t * 32 + lane;
-        const bool ok = row < a.nrows;
-        double u[KS];
-#pragma unroll
-        for (int c = 0; c < KS; ++c) u[c] = (ok && c0 + c < kmx) ? __ldg(ub + (int64_t)c * a.ldu + row) : 0.0;
-        double z = 0.0, o = 0.0;
-        if (ok) {
-            double ad = 1.0, bd = 1.0, sv;
-            z = mat_row(a.A, t, lane, X, ad);
-            if (a.out_mode == 2) {
-                sv = a.B.nrows ? mat_row(a.B, t, lane, X, bd) : X[row];
-                double d = fabs(ad - a.sigma * bd);
-                d = d > a.mfloor ? d : a.mfloor;
-                o = (1.0 / d) * (z - rho * sv);  // w = M (z - rho B g), R1
-            } else if (a.out_mode == 1) {
-                o = z;
-            }
-            if (wg == 0 && a.out) a.out[row] = o;
-        }
-        if (wg == 0 && a.norm1 == 1) n1 = fma(o, o, n1);
-        const double v1 = a.set1 == 1 ? z : o;
-#pragma unroll
-        for (int c = 0; c < KS; ++c) {
-            a1[c] = fma(u[c], v1, a1[c]);
-            if (TWO) a2[c] = fma(u[c], o, a2[c]);
-        }
-    }
-#pragma unroll
-    for (int c = 0; c < KS; ++c) {
-#pragma unroll
-        for (int off = 1; off < 32; off <<= 1) {
-            a1[c] += __shfl_xor_sync(0xffffffffu, a1[c], off);
-            if (TWO) a2[c] += __shfl_xor_sync(0xffffffffu, a2[c], off);
-        }
-    }
-    n1 = warp_sum(n1);
-    __syncthreads();
-    if (lane == 0) {
-#pragma unroll
-        for (int c = 0; c < KS; ++c) {
-            if (c0 + c < k1) acc[warp][c0 + c] = a1[c];
-            if (TWO && c0 + c < k2) acc[warp][k1 + c0 + c] = a2[c];
-        }
-        if (nn && wg == 0) acc[warp][k1 + k2] = n1;
-    }
-    if (nv == 0) return;
-    __syncthreads();
-    for (int v = threadIdx.x; v < nv; v += CTA) {
-        double sum = 0.0;
-#pragma unroll
-        for (int w = 0; w < WARPS; ++w) sum += acc[w][v];
-        res[v] = sum;
-    }
-    __syncthreads();
-    if (!grid_reduce(res, nv, a.part, a.gpart, a.counter, a.maxcta, res)) return;
-    if (a.red_local) {
-        for (int v = threadIdx.x; v < nv; v += CTA) a.red_local[v] = res[v];
-    } else {
-        sdots_finalize(a, res, k1, k2);
-    }
-}
-
-template <int KS, int G, bool TWO>
-static void launch_step1_wp_k(const SdotsArgs& a, cudaStream_t s) {
-    auto kern = k_step1_wp<KS, G, TWO>;
-    kern<<<tp_grid(kern, a.nrows, 8 * G), CTA, 0, s>>>(a);
-}
-
-bool launch_step1_wp(const SdotsArgs& a, int kmax, cudaStream_t s) {
-    const bool two = a.set2 != 0;
-#define WP1(KS, G) two ? launch_step1_wp_k<KS, G, true>(a, s) : launch_step1_wp_k<KS, G, false>(a, s)
-    switch (kmax) {
-        case 8: WP1(4, 2); break;
-        case 16: WP1(8, 2); break;
-        case 24: WP1(6, 4); break;
-        case 32: WP1(8, 4); break;
-        case 40: WP1(10, 4); break;
-        case 48: WP1(12, 4); break;
-        case 64: WP1(16, 4); break;
-        default: return false;
-    }
-#undef WP1
     return true;
 }
 

@@ -210,6 +210,11 @@ void pl1_pt(int64_t n, const double* g, const double* p, const double* num, cons
             int variant, const Pl1Dev* d, int m, double* pt, cudaStream_t st);
 
 // Kernel launchers (kernels.cu)
+// The kernel function most recently launched by this host thread (measurement: bench.py and the
+// live profile name the instantiation that ran, trplk_profile_kernels).
+extern thread_local const void* g_last_kern;
+#define NOTE_KERN(k) (::trplk::g_last_kern = reinterpret_cast<const void*>(k))
+
 bool launch_inner_small(const SmallArgs& a, int kmax, cudaStream_t s);
 // false: not applicable (kmax > 32 or no co-resident grid); nothing launched
 bool launch_inner_grid(const GridArgs& a, int kmax, cudaStream_t s);

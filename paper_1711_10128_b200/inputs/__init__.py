@@ -160,3 +160,10 @@ def slab_rows(n: int, nranks: int, rank: int, plane: int = 1) -> tuple:
     b = (planes * rank) // nranks
     e = (planes * (rank + 1)) // nranks
     return b * plane, (e * plane if rank < nranks - 1 else n)
+
+
+def sample_rows(n: int, count: int = 2048, seed: int = SEED) -> np.ndarray:
+    """Sorted distinct rows floor(U(seed, stream 8, i) * n), i < count: where full-size parity
+    tests compare eigenvector entries with the oracle's (tests/golden/oracle_<cfg>.json)."""
+    r = np.floor(u01(seed, 8, 0, count) * n).astype(np.int64)
+    return np.unique(np.clip(r, 0, n - 1))

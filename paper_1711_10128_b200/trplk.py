@@ -90,6 +90,7 @@ _sig("trplk_k_random", _I, [_P, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint6
 _sig("trplk_plan_ghosts", _I, [_I64, _I64, _P, _P, _P, _P, _P, _I, _P, _P, _I64, ctypes.POINTER(_I64)])
 _sig("trplk_profile", _I, [_P, _I])
 _sig("trplk_profile_read", _I, [_P, _P, _P, ctypes.POINTER(_I64)])
+_sig("trplk_profile_kernels", _I, [_P, ctypes.c_char_p, ctypes.c_size_t])
 _sig("trplk_pl1_solve", _I, [_P, _I, _D, _I, _I, _I, ctypes.c_uint64, _P, _P, _P, _P, _I, _P, _P, _P, _P,
                              ctypes.POINTER(Stats)])
 
@@ -98,7 +99,7 @@ EXPORTED = ["trplk_options_default", "trplk_nccl_unique_id", "trplk_create", "tr
             "trplk_k_step1", "trplk_k_cgs2", "trplk_k_rotate", "trplk_k_sym_eig",
             "trplk_k_residual", "trplk_k_random", "trplk_profile", "trplk_profile_read",
             "trplk_plan_ghosts", "trplk_k_sym_eig_time", "trplk_loopback_create", "trplk_loopback_destroy",
-            "trplk_set_debug", "trplk_pl1_solve"]
+            "trplk_set_debug", "trplk_pl1_solve", "trplk_profile_kernels"]
 
 
 class TrplkError(RuntimeError):
@@ -447,3 +448,11 @@ def trplk_profile_read(ctx: Context) -> dict:
     cnt = _I64()
     ctx.check(_lib.trplk_profile_read(ctx.handle, _ptr(ms), _ptr(by), ctypes.byref(cnt)))
     return {"ms": ms, "bytes": by, "count": cnt.value}
+
+
+def trplk_profile_kernels(ctx: Context) -> list:
+    """Names of the kernel instantiations that ran the profiled groups K1, K2, K3 ('' where a
+    group is fused into K1), as the library launched them (demangled)."""
+    buf = ctypes.create_string_buffer(4096)
+    ctx.check(_lib.trplk_profile_kernels(ctx.handle, buf, len(buf)))
+    return buf.value.decode().split(";")

@@ -1,12 +1,14 @@
-"""Write tests/golden/oracle_<CFG>.json from the ORACLE only (no CUDA path involved).
+"""Write tests/golden/oracle_<CFG>[_tolX][_firstK].json from the ORACLE only (no CUDA path involved).
 
-    python tests/golden/make_oracle_golden.py C3 [C4 ...] [--cycles K]
+    python tests/golden/make_oracle_golden.py C3 [C4 ...] [--cycles K] [--tol TOL] [--verbose]
 
 Stores the oracle's eigenvalues, residuals, status, counters and per-cycle log
 (t, cumulative A-matvecs, theta_t, ||r_t||, basis width, X^prev width) of the
-full-size BASELINE configs whose oracle solve takes minutes, so the GPU parity
-tests can compare trajectories without re-running the oracle.  --cycles K
-stores a bounded prefix (max_cycles=K) instead of the full solve.
+full-size BASELINE configs whose oracle solve takes minutes to hours, so the GPU parity
+tests can compare trajectories without re-running the oracle, plus the eigenvectors'
+entries at the seeded rows inputs.sample_rows(n) (the full vectors are 0.3-8.6 GB).
+--cycles K stores a bounded prefix (max_cycles=K) instead of the full solve; --tol runs at a
+tighter residual tolerance (the eigenvector-parity runs of SURVEY 8(c.5) step 3).
 """
 import json
 import os
@@ -20,17 +22,29 @@ import oracle  # noqa: E402
 from paper_1711_10128_b200 import inputs  # noqa: E402
 
 
+def _opt(argv, flag, conv):
+    if flag in argv:
+        i = argv.index(flag)
+        v = conv(argv[i + 1])
+        del argv[i:i + 2]
+        return v
+    return None
+
+
 def main(argv):
-    cycles = None
-    if "--cycles" in argv:
-        i = argv.index("--cycles")
-        cycles = int(argv[i + 1])
-        argv = argv[:i] + argv[i + 2:]
+    argv = list(argv)
+    cycles = _opt(argv, "--cycles", int)
+    tol = _opt(argv, "--tol", float)
+    verbose = "--verbose" in argv
+    argv = [a for a in argv if a != "--verbose"]
     for name in argv:
         P = inputs.make(name)
+        if tol is not None:
+            P.tol = tol
+        rows = inputs.sample_rows(P.A.n)
         t0 = time.perf_counter()
         r = oracle.solve(P.A, P.B, P.p, P.q, P.l, P.tol, P.sigma, want_vectors=False,
-                         max_cycles=cycles or 5000)
+                         max_cycles=cycles or 5000, sample_rows=rows, verbose=verbose)
         dt = time.perf_counter() - t0
         out = {
             "config": name, "desc": P.desc, "p": P.p, "q": P.q, "l": P.l, "tol": P.tol,
@@ -42,9 +56,12 @@ def main(argv):
             "log": {k: [float(x) if k in ("theta_t", "res") else int(x) for x in v]
                     for k, v in r["log"].items() if k in ("t", "mv", "theta_t", "res", "k", "nprev")},
             "log_thetas": [list(map(float, row)) for row in r["log"]["thetas"]],
+            "sample_rows": [int(x) for x in rows],
+            "sample_vectors": [list(map(float, r["samples"][:, c])) for c in range(P.p)],
             "oracle_seconds": dt, "host_cores": os.cpu_count(),
+            "omp_threads": int(os.environ.get("OMP_NUM_THREADS", os.cpu_count())),
         }
-        suffix = f"_first{cycles}" if cycles else ""
+        suffix = (f"_tol{tol:.0e}" if tol is not None else "") + (f"_first{cycles}" if cycles else "")
         path = os.path.join(os.path.dirname(os.path.abspath(__file__)), f"oracle_{name}{suffix}.json")
         json.dump(out, open(path, "w"))
         print(name, r["status"], r["cycles"], r["a_matvecs"], f"{dt:.1f}s", flush=True)
