@@ -43,9 +43,19 @@ def main(argv):
             P.tol = tol
         rows = inputs.sample_rows(P.A.n)
         t0 = time.perf_counter()
-        r = oracle.solve(P.A, P.B, P.p, P.q, P.l, P.tol, P.sigma, want_vectors=False,
+        exact = name == "C3"  # d = 0 Laplacian: compare the full vectors with the exact eigenspaces
+        r = oracle.solve(P.A, P.B, P.p, P.q, P.l, P.tol, P.sigma, want_vectors=exact,
                          max_cycles=cycles or 5000, sample_rows=rows, verbose=verbose)
         dt = time.perf_counter() - t0
+        extra = {}
+        if exact:
+            sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+            from closed_form import laplace3d_lowest, sin_angle
+            lam, V, groups = laplace3d_lowest(P.grid["N"], P.p)
+            X = r["eigenvectors"]
+            extra = {"exact_groups": groups,
+                     "exact_sin_angle": [sin_angle(X[:, g], V[:, g]) for g in groups],
+                     "exact_eigenvalues": list(map(float, lam))}
         out = {
             "config": name, "desc": P.desc, "p": P.p, "q": P.q, "l": P.l, "tol": P.tol,
             "source": "oracle/ (orc_trplk_solve) via tests/golden/make_oracle_golden.py",
@@ -58,6 +68,7 @@ def main(argv):
             "log_thetas": [list(map(float, row)) for row in r["log"]["thetas"]],
             "sample_rows": [int(x) for x in rows],
             "sample_vectors": [list(map(float, r["samples"][:, c])) for c in range(P.p)],
+            **extra,
             "oracle_seconds": dt, "host_cores": os.cpu_count(),
             "omp_threads": int(os.environ.get("OMP_NUM_THREADS", os.cpu_count())),
         }

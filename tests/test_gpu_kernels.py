@@ -260,3 +260,33 @@ def test_random_start_block_bit_exact(orc, problems):
         trplk.trplk_k_random(ctx, 12, stream, col, x)
         ref = np.array([orc.u01(12, stream, col * n + i) for i in range(n)])
         assert np.array_equal(x.cpu().numpy(), ref)
+
+
+@pytest.mark.parametrize("k", [8, 13, 16])
+def test_step1_pipe_full_slab(orc, gen, k):
+    """The K1 that C5 runs (k_step1_pipe: DIA, B = I, k <= 16, selected by default on slabs of
+    >= 2^24 rows) at a size that selects it: 257^3 = 16,974,593 rows (ragged last 32-row tile),
+    C5's matrix shape (7-pt + diag(d), d~U[0,10)).  Every output against the oracle's SpMV and
+    blocked dots over all rows: w normwise <= 1e-12, dots <= 1e-12 ||u|| ||v||."""
+    torch, trplk = need_gpu()
+    P = gen.make("C5", N=257)
+    n = P.A.n
+    assert n >= 1 << 24
+    ctx = trplk.trplk_create(P.A, P.B)
+    rng = np.random.default_rng(100 + k)
+    U = np.asfortranarray(rng.standard_normal((n, k)) / np.sqrt(n))
+    g = U[:, k - 1]
+    rho = 2.75
+    Ud = to_dev(torch, U, ctx.ld)
+    w = torch.zeros(ctx.ld, dtype=torch.float64, device="cuda")
+    tcol, h1, wn = trplk.trplk_k_step1(ctx, Ud, ctx.ld, k, Ud[k - 1], rho, w)
+    z = orc.spmv(P.A, g)
+    w_o = orc.jacobi_diag(P.A) * (z - rho * g)
+    assert normwise(w.cpu().numpy()[:n], w_o) <= 1e-12
+    un, nz, nw = np.linalg.norm(U, axis=0), np.linalg.norm(z), np.linalg.norm(w_o)
+    t_o = np.array([orc.dot(U[:, i], z) for i in range(k)])
+    h_o = np.array([orc.dot(U[:, i], w_o) for i in range(k)])
+    assert np.all(np.abs(tcol - t_o) <= 1e-12 * un * nz)
+    assert np.all(np.abs(h1 - h_o) <= 1e-12 * un * nw)
+    assert abs(wn - orc.dot(w_o, w_o)) <= 1e-12 * nw * nw
+    ctx.close()

@@ -261,3 +261,19 @@ def test_determinism_thread_count(tmp_path):
         subprocess.check_call([sys.executable, "-c", code, f], env=env)
         outs.append(np.load(f))
     assert np.array_equal(outs[0], outs[1])
+
+
+def test_closed_form_laplace_basis(gen):
+    """tests/closed_form.py (the exact eigenspaces the C3 eigenvector parity is measured against)
+    is itself right: A V = V Lambda and V^T V = I on a 12^3 grid, clusters of the sine basis."""
+    import sys
+    import os
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    from closed_form import laplace3d_lowest
+    P = gen.make("C3", N=12)
+    lam, V, groups = laplace3d_lowest(12, 10)
+    A = P.A.to_scipy()
+    assert np.max(np.abs(A @ V - V * lam)) <= 1e-14
+    assert np.max(np.abs(V.T @ V - np.eye(10))) <= 1e-14
+    assert groups == [[0], [1, 2, 3], [4, 5, 6], [7, 8, 9]]
+    assert np.allclose(lam, np.linalg.eigvalsh(A.toarray())[:10], rtol=0, atol=1e-13)
