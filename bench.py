@@ -54,6 +54,12 @@ def parse():
     ap.add_argument("--config", default="C5", choices=["C1", "C2", "C3", "C4", "C5"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--comm", default="nccl", choices=["nccl", "host"],
+                    help="N>1 exchanges: nccl (production) or host (host-staged through a gloo group; "
+                         "lets several ranks share one GPU -- tests of the multi-process path only)")
+    ap.add_argument("--precond", default="jacobi", choices=["jacobi", "none"],
+                    help="none: M = I (with --k-plus 0: the thick-restart Lanczos baseline, eq 2.1)")
+    ap.add_argument("--k-plus", type=int, default=None, help="override the config's k_plus (l)")
     ap.add_argument("--profile-last-only", action="store_true",
                     help="kernel-profile events on the last timed step only (default: every timed step)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -126,12 +132,13 @@ def plane_of(P):
 FULL_SOLVE_CFGS = ("C1", "C2")  # oracle full solve in seconds; C3/C4 take 20-30 min, C5 hours
 
 
-def static_config(name, P, n, world):
+def static_config(name, P, n, world, precond="Jacobi", comm="nccl"):
     """The `config` object of both arms (identical keys and values)."""
-    return {"workload": f"{name}: {P.desc}; p={P.p}, max_basis={P.q}, k_plus={P.l}, tol={P.tol}, Jacobi, seed 12",
+    return {"workload": f"{name}: {P.desc}; p={P.p}, max_basis={P.q}, k_plus={P.l}, tol={P.tol}, "
+                        f"{precond} preconditioner, seed 12",
             "n": n, "step": "one full trplk_solve (time to p eigenpairs)",
             "l2": "inputs larger than L2 at C3-C5; a 256 MiB buffer is written between timed steps",
-            "parallelism": f"z-slab row partition x{world}"}
+            "parallelism": f"z-slab row partition x{world}" + (" (host-staged gloo exchanges)" if comm == "host" else "")}
 
 
 class OracleSample:
@@ -331,11 +338,15 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
+    torch.cuda.set_device(local % torch.cuda.device_count())
     group = None
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.comm == "host":
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         group = dist.group.WORLD
+    red_dev = "cpu" if args.comm == "host" else "cuda"  # max over ranks
     from paper_1711_10128_b200 import build
     build.build()
     from paper_1711_10128_b200 import inputs, trplk
@@ -345,18 +356,22 @@ def main():
     plane = 1 if dim == 1 else N * N
     rb, re = inputs.slab_rows(n, world, rank, plane)
     P = inputs.make(args.config, row_begin=rb, row_end=re)
+    if args.k_plus is not None:
+        P.l = args.k_plus
+    prec = 1 if args.precond == "none" else 0
     stream = torch.cuda.current_stream()
 
     def barrier():
         if world > 1:
             dist.barrier()
 
-    ctx = trplk.trplk_create(P.A, P.B, P.sigma, n_global=n, row_begin=rb, row_end=re, group=group)
+    ctx = trplk.trplk_create(P.A, P.B, P.sigma, n_global=n, row_begin=rb, row_end=re, group=group,
+                             comm=args.comm)
     evecs = torch.empty((P.p, ctx.n_local), dtype=torch.float64, device="cuda")
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
 
     def solve(**kw):
-        return trplk.trplk_solve(ctx, P.p, P.q, P.l, P.tol, evecs_out=evecs, **kw)
+        return trplk.trplk_solve(ctx, P.p, P.q, P.l, P.tol, evecs_out=evecs, precond=prec, **kw)
 
     for w in range(args.warmup):
         # the last warm-up solve runs with the profile on too, so the timed region finds the
@@ -387,8 +402,9 @@ def main():
     ck = clocks.stop()
     prof = trplk.trplk_profile_read(ctx)
     kern_names = trplk.trplk_profile_kernels(ctx)
+    phases = trplk.trplk_profile_phases(ctx)
     trplk.trplk_profile(ctx, False)
-    t_sum = torch.tensor([sum(times)], dtype=torch.float64, device="cuda")
+    t_sum = torch.tensor([sum(times)], dtype=torch.float64, device=red_dev)
     if world > 1:
         dist.all_reduce(t_sum, op=dist.ReduceOp.MAX)
     ms_per_step = t_sum.item() / args.steps
@@ -421,6 +437,9 @@ def main():
             "inner_step": {"achieved": round(step_gbs, 1), "frac": round(step_gbs / peak, 4),
                            "bytes": per_b.sum(), "ms": per_ms.sum(),
                            "share_ms": [round(x / per_ms.sum(), 3) for x in per_ms]},
+            "cycle_phases_ms": {nm: round(v / max(phases["count"], 1), 4) for nm, v in zip(phases["phases"], phases["ms"])},
+            "cycle_phase_share": {nm: round(v / max(phases["ms"].sum(), 1e-30), 4)
+                                  for nm, v in zip(phases["phases"], phases["ms"])},
             "solve_model_gbs": round(stats[-1]["model_bytes"] / (ms_per_step * 1e-3) / 1e9, 1),
             "samples": prof["count"]}
 
@@ -452,14 +471,15 @@ def main():
             torch.cuda.synchronize()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            c2 = trplk.trplk_create(HA, HB, P.sigma, n_global=n, row_begin=rb, row_end=re, group=group)
-            ev2, _, rs2, st2 = trplk.trplk_solve(c2, P.p, P.q, P.l, P.tol, evecs_out=host_evecs)
+            c2 = trplk.trplk_create(HA, HB, P.sigma, n_global=n, row_begin=rb, row_end=re, group=group,
+                                    comm=args.comm)
+            ev2, _, rs2, st2 = trplk.trplk_solve(c2, P.p, P.q, P.l, P.tol, evecs_out=host_evecs, precond=prec)
             c2.close()
             e1.record(stream)
             torch.cuda.synchronize()
             if it >= ne_warm:  # untimed warm-up: first-touch allocator growth, lazy module loads
                 et.append(e0.elapsed_time(e1))
-        te = torch.tensor([statistics.mean(et)], dtype=torch.float64, device="cuda")
+        te = torch.tensor([statistics.mean(et)], dtype=torch.float64, device=red_dev)
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         e2e = {"value": st2["a_matvecs"] / (te.item() / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
@@ -477,7 +497,7 @@ def main():
                "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
                "scaling": "strong", "vs_baseline": None, "dtype": "f64",
                "data": "synthetic (seeded generator, BASELINE configs; paper matrices unavailable)",
-               "config": static_config(args.config, P, n, world),
+               "config": static_config(args.config, P, n, world, "no (M = I)" if prec else "Jacobi", args.comm),
                "solve": {"a_matvecs_per_solve": mv, "cycles": stats[-1]["cycles"],
                          "time_to_p_eigenpairs_ms": round(ms_per_step, 4),
                          "status": stats[-1]["status"]},

@@ -39,7 +39,7 @@
 extern "C" {
 #endif
 
-#define TRPLK_ABI_VERSION 1
+#define TRPLK_ABI_VERSION 2
 #define TRPLK_MAX_BASIS 64 /* largest max_basis (q) supported by the device kernels */
 
 typedef enum {
@@ -68,8 +68,6 @@ typedef struct {
     int rank, nranks;
     int64_t row_begin, row_end;
     const void* nccl_unique_id;
-    void* loopback; /* test infrastructure: an in-process hub (trplk_loopback_create) instead of NCCL,
-                       all ranks of the solve as host threads of one process on one GPU; NULL = NCCL */
 } trplk_dist;
 
 typedef struct {
@@ -81,6 +79,9 @@ typedef struct {
     int lock_mode;      /* 0 IF (one lock per cycle, Alg.1 step 12, R7); 1 WHILE */
     int debug_checks;   /* bit 1 (value 2): force the third CGS pass (R3) -- tests of that path */
     int use_graphs;     /* 1 (default): one CUDA graph per cycle; 0: eager launches */
+    int precond;        /* 0 (default): Jacobi M on A - sigma B (R12); 1: none, M = I -- with
+                           k_plus = 0 the thick-restart Lanczos baseline (eq 2.1, PAPER.md:77-80,
+                           "cannot use preconditioning directly"), with m = 1, p = k_plus = 1 LOPCG */
 } trplk_options;
 
 typedef struct {

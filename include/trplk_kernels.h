@@ -77,8 +77,32 @@ trplk_status trplk_plan_ghosts(int64_t row_begin, int64_t row_end, const int64_t
  * TRPLK_GRID=1.  Same readings (R1, R3, R16) as the multi-kernel step.  Errors: EINVAL (ctx NULL). */
 trplk_status trplk_set_debug(trplk_ctx* ctx, int flags);
 
-/* In-process loopback hub for nranks ranks (test infrastructure): pass it as
- * trplk_dist.loopback to every rank's trplk_create, one host thread per rank, all on the same
+/* Host-staged rank exchanges (test infrastructure and single-GPU multi-process runs): collective
+ * callbacks every rank calls in the same order on HOST buffers; each returns 0 on success.
+ *   allgather  recv[r*bytes .. (r+1)*bytes) <- rank r's send, for every rank r
+ *   sendrecv   grouped point-to-point: send_buf[i] (send_bytes[i]) to send_peer[i], recv_buf[j]
+ *              (recv_bytes[j]) from recv_peer[j]; every send matches the peer's recv of the same size
+ *   allreduce  v[0:count] <- elementwise sum (op 0) or max (op 1) over ranks (create time only) */
+typedef struct {
+    int (*allgather)(const void* send, void* recv, size_t bytes, void* user);
+    int (*sendrecv)(int nsend, const int* send_peer, const void* const* send_buf, const size_t* send_bytes,
+                    int nrecv, const int* recv_peer, void* const* recv_buf, const size_t* recv_bytes, void* user);
+    int (*allreduce)(double* v, int count, int op, void* user);
+    void* user;
+} trplk_host_comm;
+
+/* trplk_create whose row-partition exchanges go through an in-process loopback hub
+ * (loopback_hub, from trplk_loopback_create) or host callbacks (host_comm) instead of NCCL; exactly
+ * one of the two must be non-NULL, dist must be given (dist->nccl_unique_id is ignored).  Solves on
+ * such contexts run eagerly (no CUDA graphs: the exchanges are host rendezvous).  Otherwise the
+ * arguments, ownership and errors of trplk_create. */
+trplk_status trplk_create_ex(trplk_ctx** out, int64_t n_global, const int64_t* a_rowptr, const int64_t* a_col,
+                             const double* a_val, const int64_t* b_rowptr, const int64_t* b_col, const double* b_val,
+                             double sigma, const trplk_dist* dist, void* loopback_hub,
+                             const trplk_host_comm* host_comm, const trplk_allocator* alloc, void* stream);
+
+/* In-process loopback hub for nranks ranks (test infrastructure): pass it to
+ * every rank's trplk_create_ex, one host thread per rank, all on the same
  * GPU.  Every exchange (halo planes, reduction partials, create-time plans) becomes a rendezvous
  * of the rank threads with device-to-device copies on the receiving rank's stream ordered by
  * CUDA events -- no kernel waits on another rank.  Solves on loopback ranks run eagerly (no
@@ -95,6 +119,11 @@ void trplk_loopback_destroy(void* hub);
  * enable=1 clears the accumulators.  read: ms[3], bytes[3] sums over `count` cycles. */
 trplk_status trplk_profile(trplk_ctx* ctx, int enable);
 trplk_status trplk_profile_read(const trplk_ctx* ctx, double* ms, double* bytes, int64_t* count);
+/* Cycle-phase breakdown of the live profile: device ms summed over `count` profiled cycles of
+ *   [0] seed CGS2 (R4)  [1] the m inner steps (eq 3.1)  [2] +K (Alg.1 steps 6-8)
+ *   [3] Rayleigh-Ritz eig (step 11)  [4] rotation U Y (steps 11/15)  [5] residual of the target
+ * (events at the phase boundaries inside every cycle).  Errors: EINVAL (ctx NULL). */
+trplk_status trplk_profile_phases(const trplk_ctx* ctx, double* ms, int64_t* count);
 /* Demangled names of the kernels that ran the three profiled groups (K1;K2;K3, ';'-separated;
  * an empty field where the group is fused into K1), written NUL-terminated into buf[len].
  * Errors: EINVAL (NULL ctx/buf or len too small). */

@@ -335,6 +335,8 @@ int orc_trplk_solve(const orc_problem* P, double* evals, double* evecs, double* 
     double* M = (double*)malloc((size_t)n * sizeof(double));
     orc_jacobi_diag(n, P->a_rowptr, P->a_col, P->a_val, P->b_rowptr, P->b_col, P->b_val, P->sigma,
                     1e-8, M);
+    if (P->precond == 1) /* no preconditioning: the TRLan / LOPCG baselines of PAPER.md:77-95 */
+        for (int64_t i = 0; i < n; ++i) M[i] = 1.0;
     double tau = P->tol;
     if (P->tol_mode == 1) tau = P->tol * orc_frobenius(P->a_rowptr[n], P->a_val); /* eq 5.1 */
 

@@ -59,6 +59,8 @@ typedef struct {
     int restart_size;       /* p^ (>= p); 0 -> p */
     int lock_mode;          /* 0 IF (Alg. 1 step 12, R7), 1 WHILE */
     int debug;              /* 1: log ||T - U^T A U||_max and ||U^T B U - I||_max per cycle */
+    int precond;            /* 0 Jacobi (R12); 1 none, M = I: with l = 0 thick-restart Lanczos (eq 2.1,
+                               PAPER.md:77-80), with m = p = l = 1 LOPCG (eq 2.2 with p = 1) */
 } orc_problem;
 
 typedef struct {

@@ -11,6 +11,8 @@
 #include <cuda_runtime.h>
 #include <nccl.h>
 
+#include "trplk_kernels.h"
+
 namespace trplk {
 
 struct Xfer {  // one point-to-point transfer of `count` elements of `elsize` bytes
@@ -163,6 +165,67 @@ public:
         return true;
     }
     const char* what() const override { return cudaGetErrorString(last); }
+};
+
+// ---------------------------------------------------------------- host callbacks (one GPU, N processes)
+// Exchanges staged through host memory and handed to the caller's callbacks (the Python binding
+// routes them to a torch.distributed gloo group): device -> host copy, callback, host -> device
+// copy, each synchronous on the rank's stream, so no kernel ever waits on another process and
+// several processes can share one GPU (tests of the multi-process bootstrap; bench.py --comm host).
+class HostComm : public Comm {
+public:
+    trplk_host_comm cb;
+    cudaError_t lastc = cudaSuccess;
+    int lastcb = 0;
+    std::vector<char> hs, hr;
+    explicit HostComm(const trplk_host_comm& c) : cb(c) {}
+    bool cu(cudaError_t e) { return (lastc = e) == cudaSuccess; }
+    bool allgather(const void* send, void* recv, size_t count, size_t elsize, cudaStream_t s) override {
+        const size_t b = count * elsize;
+        hs.resize(b);
+        if (!cu(cudaMemcpyAsync(hs.data(), send, b, cudaMemcpyDeviceToHost, s)) || !cu(cudaStreamSynchronize(s)))
+            return false;
+        hr.resize(b * (size_t)nranks);
+        if ((lastcb = cb.allgather(hs.data(), hr.data(), b, cb.user)) != 0) return false;
+        return cu(cudaMemcpyAsync(recv, hr.data(), hr.size(), cudaMemcpyHostToDevice, s)) && cu(cudaStreamSynchronize(s));
+    }
+    bool sendrecv(const std::vector<Xfer>& sends, const std::vector<Xfer>& recvs, size_t elsize,
+                  cudaStream_t s) override {
+        std::vector<std::vector<char>> sb(sends.size()), rb(recvs.size());
+        std::vector<int> sp, rp;
+        std::vector<const void*> spt;
+        std::vector<void*> rpt;
+        std::vector<size_t> sn, rn;
+        for (size_t i = 0; i < sends.size(); ++i) {
+            sb[i].resize(sends[i].count * elsize);
+            if (!sb[i].empty() && !cu(cudaMemcpyAsync(sb[i].data(), sends[i].ptr, sb[i].size(), cudaMemcpyDeviceToHost, s)))
+                return false;
+            sp.push_back(sends[i].peer);
+            spt.push_back(sb[i].data());
+            sn.push_back(sb[i].size());
+        }
+        for (size_t i = 0; i < recvs.size(); ++i) {
+            rb[i].resize(recvs[i].count * elsize);
+            rp.push_back(recvs[i].peer);
+            rpt.push_back(rb[i].data());
+            rn.push_back(rb[i].size());
+        }
+        if (!cu(cudaStreamSynchronize(s))) return false;
+        if ((lastcb = cb.sendrecv((int)sp.size(), sp.data(), spt.data(), sn.data(), (int)rp.size(), rp.data(),
+                                  rpt.data(), rn.data(), cb.user)) != 0)
+            return false;
+        for (size_t i = 0; i < recvs.size(); ++i)
+            if (!rb[i].empty() && !cu(cudaMemcpyAsync(recvs[i].ptr, rb[i].data(), rb[i].size(), cudaMemcpyHostToDevice, s)))
+                return false;
+        return cu(cudaStreamSynchronize(s));
+    }
+    bool allreduce_host(double* v, int count, int op, cudaStream_t s, double* tmp) override {
+        (void)s;
+        (void)tmp;
+        return (lastcb = cb.allreduce(v, count, op, cb.user)) == 0;
+    }
+    const char* what() const override { return lastcb ? "host exchange callback failed" : cudaGetErrorString(lastc); }
+    int nranks = 1;
 };
 
 }  // namespace trplk

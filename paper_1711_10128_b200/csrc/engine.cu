@@ -45,8 +45,9 @@ struct GraphRec {
 
 struct Sizes {  // per-solve parameters that shape the captured graphs
     int p, q, l, ph, m;
+    int prec;  // trplk_options.precond (0 Jacobi, 1 M = I)
     bool operator<(const Sizes& o) const {
-        return std::tie(p, q, l, ph, m) < std::tie(o.p, o.q, o.l, o.ph, o.m);
+        return std::tie(p, q, l, ph, m, prec) < std::tie(o.p, o.q, o.l, o.ph, o.m, o.prec);
     }
     bool operator==(const Sizes& o) const { return !(*this < o) && !(o < *this); }
 };
@@ -64,6 +65,7 @@ struct trplk_ctx {
     std::vector<std::pair<void*, size_t>> allocs;
     bool hasB = false;
     double sigma = 0.0, mfloor = 0.0, normF = 0.0, amax = 0.0;
+    double mfloor_solve = 0.0;  // the value kernels get: mfloor, or -1 for M = I (options.precond = 1)
     Sell A, B;
     int64_t sellA_bytes = 0, sellB_bytes = 0, nnzA = 0, nnzB = 0;
     // halo plan (nranks > 1): per peer, recv range in the ghost tail and send rows
@@ -74,7 +76,7 @@ struct trplk_ctx {
     Comm* cm = nullptr;    // rank exchanges (NCCL, or the in-process loopback hub)
     int force3 = 0;        // debug: force the third CGS pass (trplk_set_debug / options.debug_checks & 2)
     int grid_on = -1;      // grid-wide inner loop: -1 = TRPLK_GRID env, else trplk_set_debug bit 1
-    bool loopback = false;  // loopback ranks: eager launches (exchanges are host rendezvous)
+    bool loopback = false;  // loopback hub / host callbacks: eager launches (exchanges are host rendezvous)
     // solve buffers
     int q_alloc = 0, ph_alloc = 0;
     double* U[2] = {nullptr, nullptr};
@@ -104,6 +106,10 @@ struct trplk_ctx {
     double prof_ms[3] = {0, 0, 0}, prof_bytes[3] = {0, 0, 0};
     int64_t prof_count = 0;
     const void* prof_kern[3] = {nullptr, nullptr, nullptr};  // kernels of the profiled groups K1, K2, K3
+    // cycle phases (profile on): seed CGS2, inner steps, +K, Rayleigh-Ritz eig, rotation, residual
+    cudaEvent_t phev[7] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+    double phase_ms[6] = {0, 0, 0, 0, 0, 0};
+    int64_t phase_count = 0;
     int prof_k = 0;
 };
 
@@ -587,7 +593,7 @@ SdotsArgs sd_base(trplk_ctx* ctx) {
     a.theta_idx = -1;
     a.tcol_fixed = -1;
     a.sigma = ctx->sigma;
-    a.mfloor = ctx->mfloor;
+    a.mfloor = ctx->mfloor_solve;
     a.ctl = ctx->ctl;
     a.T = ctx->T;
     a.ldT = QMAX;
@@ -903,6 +909,12 @@ trplk_status ctl_pull(trplk_ctx* ctx) {
     return TRPLK_OK;
 }
 
+// phase boundary event of the live cycle profile (trplk_profile_phases)
+static trplk_status phase_mark(trplk_ctx* ctx, int i) {
+    if (ctx->prof_on) CK(cudaEventRecordWithFlags(ctx->phev[i], ctx->stream, cudaEventRecordExternal));
+    return TRPLK_OK;
+}
+
 // One outer cycle after the seed vector u is in place: eq 3.1 inner steps, +K, RR, rotation,
 // residual of the target.  Issued eagerly or under stream capture.
 trplk_status issue_cycle(trplk_ctx* ctx, const Sizes& S, int cur, int nprev, int t_static, int xprev_static) {
@@ -911,6 +923,7 @@ trplk_status issue_cycle(trplk_ctx* ctx, const Sizes& S, int cur, int nprev, int
     double* Uo = ctx->U[oth];
     const int64_t ld = ctx->ld;
     // seed: g_1 = (I - X X^T B) u / beta  (eq 3.2 u1 = C x_t, R4), written to column p^
+    ST(phase_mark(ctx, 0));
     {
         CgsSpec c{};
         c.x = ctx->u;
@@ -926,6 +939,7 @@ trplk_status issue_cycle(trplk_ctx* ctx, const Sizes& S, int cur, int nprev, int
         ST(cgs2(ctx, c));
     }
     // inner steps, eq 3.1
+    ST(phase_mark(ctx, 1));
     const int jmid = std::max(1, std::min(S.m - 1, S.m / 2));
     const bool fused = small_path(ctx, S) || grid_path(ctx, S);
     if (fused) {  // one kernel runs all m steps (latency paths, small.cuh / inner_grid.cuh)
@@ -942,7 +956,7 @@ trplk_status issue_cycle(trplk_ctx* ctx, const Sizes& S, int cur, int nprev, int
         sa.ldT = QMAX;
         sa.m = S.m;
         sa.sigma = ctx->sigma;
-        sa.mfloor = ctx->mfloor;
+        sa.mfloor = ctx->mfloor_solve;
         sa.gate = F_CYCLE | F_INNER;
         sa.clear = F_INNER;
         sa.force3 = ctx->force3;
@@ -1020,6 +1034,7 @@ trplk_status issue_cycle(trplk_ctx* ctx, const Sizes& S, int cur, int nprev, int
         }
     }
     // +K: X^prev appended after G, explicitly orthogonalised, one matvec each
+    ST(phase_mark(ctx, 2));
     for (int jj = 0; jj < nprev; ++jj) {
         const unsigned kb = F_KCOL0 << jj;
         CgsSpec c{};
@@ -1052,15 +1067,19 @@ trplk_status issue_cycle(trplk_ctx* ctx, const Sizes& S, int cur, int nprev, int
         ST(run_sdots(ctx, a, S.ph + S.m + jj + 1));
     }
     // Rayleigh-Ritz (step 11) and rotation X = U Y(:,1:p^) into the other buffer
+    ST(phase_mark(ctx, 3));
     launch_eig(ctx->ctl, ctx->T, QMAX, ctx->Yg, QMAX, S.ph, 0, F_CYCLE, ctx->stream);
     CK(cudaGetLastError());
+    ST(phase_mark(ctx, 4));
     launch_rotate(Uc, ld, ctx->n_loc, ctx->ctl, 0, ctx->Yg, QMAX, S.ph, Uo, ld, F_CYCLE, ctx->stream, S.q);
     ctx->launches += 2;
     CK(cudaGetLastError());
     ctx->model_bytes += vec_bytes(ctx) * (S.q + S.ph);
     // residual of the target, u = M r (steps 12, 15)
+    ST(phase_mark(ctx, 5));
     if (t_static > 0) ST(residual(ctx, Uo + ld * (t_static - 1), 0, -1, ctx->u, F_CYCLE));
     else ST(residual(ctx, Uo, 1, -1, ctx->u, F_CYCLE));
+    ST(phase_mark(ctx, 6));
     return TRPLK_OK;
 }
 
@@ -1091,7 +1110,7 @@ static std::string graph_fingerprint(const trplk_ctx* ctx, uint64_t key, const S
         put(&M->dval, sizeof(M->dval));
         put(M->offs, sizeof(M->offs));
     }
-    const double sc[3] = {ctx->sigma, ctx->mfloor, ctx->normF};
+    const double sc[4] = {ctx->sigma, ctx->mfloor, ctx->normF, ctx->mfloor_solve};
     put(sc, sizeof(sc));
     const int64_t iv[6] = {ctx->n_loc, ctx->ld, ctx->row_begin, ctx->n_global, (int64_t)ctx->force3,
                            (int64_t)ctx->grid_on};
@@ -1200,6 +1219,7 @@ void trplk_options_default(trplk_options* opt) {
     opt->lock_mode = 0;
     opt->debug_checks = 0;
     opt->use_graphs = 1;
+    opt->precond = 0;
 }
 
 trplk_status trplk_nccl_unique_id(void* out, size_t out_bytes) {
@@ -1229,7 +1249,8 @@ struct PhaseTimer {
 
 static trplk_status create_impl(trplk_ctx* ctx, int64_t n_global, const int64_t* a_rowptr, const int64_t* a_col,
                                 const double* a_val, const int64_t* b_rowptr, const int64_t* b_col,
-                                const double* b_val, double sigma, const trplk_dist* dist) {
+                                const double* b_val, double sigma, const trplk_dist* dist, void* hubp,
+                                const trplk_host_comm* hc) {
     ctx->n_global = n_global;
     ctx->sigma = sigma;
     PhaseTimer pt("create");
@@ -1247,8 +1268,8 @@ static trplk_status create_impl(trplk_ctx* ctx, int64_t n_global, const int64_t*
             ctx->err = "bad trplk_dist (rank/nranks/row range)";
             return TRPLK_EINVAL;
         }
-        if (ctx->nranks > 1 && !dist->nccl_unique_id && !dist->loopback) {
-            ctx->err = "nranks > 1 needs nccl_unique_id (or a loopback hub)";
+        if (ctx->nranks > 1 && !dist->nccl_unique_id && !hubp && !hc) {
+            ctx->err = "nranks > 1 needs nccl_unique_id (trplk_create_ex: a loopback hub or host callbacks)";
             return TRPLK_EINVAL;
         }
     } else {
@@ -1272,14 +1293,23 @@ static trplk_status create_impl(trplk_ctx* ctx, int64_t n_global, const int64_t*
     pt.mark("scan");
 
     if (ctx->nranks > 1) {
-        if (dist->loopback) {
-            LoopHub* hub = static_cast<LoopHub*>(dist->loopback);
+        if (hubp) {
+            LoopHub* hub = static_cast<LoopHub*>(hubp);
             if (hub->n != ctx->nranks) {
                 ctx->err = "loopback hub size != nranks";
                 return TRPLK_EINVAL;
             }
             ctx->cm = new LoopComm(hub, ctx->rank);
             ctx->loopback = true;
+        } else if (hc) {
+            if (!hc->allgather || !hc->sendrecv || !hc->allreduce) {
+                ctx->err = "trplk_host_comm: NULL callback";
+                return TRPLK_EINVAL;
+            }
+            HostComm* h = new HostComm(*hc);
+            h->nranks = ctx->nranks;
+            ctx->cm = h;
+            ctx->loopback = true;  // host rendezvous: eager launches
         } else {
             NcclComm* c = new NcclComm();
             ctx->cm = c;
@@ -1459,7 +1489,19 @@ static trplk_status create_impl(trplk_ctx* ctx, int64_t n_global, const int64_t*
 trplk_status trplk_create(trplk_ctx** out, int64_t n_global, const int64_t* a_rowptr, const int64_t* a_col,
                           const double* a_val, const int64_t* b_rowptr, const int64_t* b_col, const double* b_val,
                           double sigma, const trplk_dist* dist, const trplk_allocator* alloc, void* stream) {
+    return trplk_create_ex(out, n_global, a_rowptr, a_col, a_val, b_rowptr, b_col, b_val, sigma, dist, nullptr,
+                           nullptr, alloc, stream);
+}
+
+trplk_status trplk_create_ex(trplk_ctx** out, int64_t n_global, const int64_t* a_rowptr, const int64_t* a_col,
+                             const double* a_val, const int64_t* b_rowptr, const int64_t* b_col, const double* b_val,
+                             double sigma, const trplk_dist* dist, void* loopback_hub,
+                             const trplk_host_comm* host_comm, const trplk_allocator* alloc, void* stream) {
     if (!out) return TRPLK_EINVAL;
+    if ((loopback_hub || host_comm) && (!dist || (loopback_hub && host_comm))) {
+        *out = nullptr;
+        return TRPLK_EINVAL;
+    }
     trplk_ctx* ctx = new trplk_ctx();
     *out = ctx;
     ctx->user_stream = (cudaStream_t)stream;
@@ -1474,7 +1516,8 @@ trplk_status trplk_create(trplk_ctx** out, int64_t n_global, const int64_t* a_ro
         ctx->alloc = *alloc;
         ctx->has_alloc = true;
     }
-    return create_impl(ctx, n_global, a_rowptr, a_col, a_val, b_rowptr, b_col, b_val, sigma, dist);
+    return create_impl(ctx, n_global, a_rowptr, a_col, a_val, b_rowptr, b_col, b_val, sigma, dist, loopback_hub,
+                       host_comm);
 }
 
 void trplk_destroy(trplk_ctx* ctx) {
@@ -1488,6 +1531,8 @@ void trplk_destroy(trplk_ctx* ctx) {
     ctl_host_free(ctx->ctl_h);
     if (ctx->ev_in) cudaEventDestroy(ctx->ev_in);
     for (auto& e : ctx->pev)
+        if (e) cudaEventDestroy(e);
+    for (auto& e : ctx->phev)
         if (e) cudaEventDestroy(e);
     if (ctx->ev_out) cudaEventDestroy(ctx->ev_out);
     if (ctx->stream) cudaStreamDestroy(ctx->stream);
@@ -1543,7 +1588,12 @@ static trplk_status solve_impl(trplk_ctx* ctx, int p, int q, int l, double tol, 
         ctx->err = "NULL output";
         return TRPLK_EINVAL;
     }
-    const Sizes S{p, q, l, ph, m};
+    if (opt.precond != 0 && opt.precond != 1) {
+        ctx->err = "options.precond must be 0 (Jacobi) or 1 (none)";
+        return TRPLK_EINVAL;
+    }
+    ctx->mfloor_solve = opt.precond == 1 ? -1.0 : ctx->mfloor;
+    const Sizes S{p, q, l, ph, m, opt.precond};
     PhaseTimer pt("solve");
     ST(ensure_buffers(ctx, q, ph));
     pt.mark("buffers");
@@ -1714,6 +1764,14 @@ static trplk_status solve_impl(trplk_ctx* ctx, int p, int q, int l, double tol, 
             ctx->prec += ncgs + 1;
             if (ctx->hasB) ctx->b_mv += 2 + 3 * ncgs + 2 * nprev + 1 + (H.pass3_count - p3_prev);
             p3_prev = H.pass3_count;
+            if (ctx->prof_on) {  // live cycle-phase profile
+                for (int i = 0; i < 6; ++i) {
+                    float pm = 0.f;
+                    CK(cudaEventElapsedTime(&pm, ctx->phev[i], ctx->phev[i + 1]));
+                    ctx->phase_ms[i] += pm;
+                }
+                ctx->phase_count++;
+            }
             if (ctx->prof_on) {  // live inner-step profile (events recorded inside the cycle)
                 const int jmid = std::max(1, std::min(m - 1, m / 2));
                 if (m >= 2 && G > jmid) {
@@ -2455,11 +2513,23 @@ trplk_status trplk_plan_ghosts(int64_t row_begin, int64_t row_end, const int64_t
 
 trplk_status trplk_profile(trplk_ctx* ctx, int enable) {
     if (!ctx) return TRPLK_EINVAL;
-    if (enable && !ctx->pev[0])
+    if (enable && !ctx->pev[0]) {
         for (auto& e : ctx->pev) CK(cudaEventCreate(&e));
+        for (auto& e : ctx->phev) CK(cudaEventCreate(&e));
+    }
     ctx->prof_on = enable != 0;
     for (int i = 0; i < 3; ++i) ctx->prof_ms[i] = ctx->prof_bytes[i] = 0.0;
     ctx->prof_count = 0;
+    for (int i = 0; i < 6; ++i) ctx->phase_ms[i] = 0.0;
+    ctx->phase_count = 0;
+    return TRPLK_OK;
+}
+
+trplk_status trplk_profile_phases(const trplk_ctx* ctx, double* ms, int64_t* count) {
+    if (!ctx) return TRPLK_EINVAL;
+    for (int i = 0; i < 6; ++i)
+        if (ms) ms[i] = ctx->phase_ms[i];
+    if (count) *count = ctx->phase_count;
     return TRPLK_OK;
 }
 

@@ -82,9 +82,7 @@ __global__ void __launch_bounds__(CTA, 2) k_step1_rs2(const SdotsArgs a) {
             if (a.out_mode == 2) {
                 if (a.B.nrows) sv = mat_row(a.B, sl, lane, X, bd);
                 else sv = xr;
-                double d = fabs(ad - a.sigma * bd);
-                d = d > a.mfloor ? d : a.mfloor;
-                o = (1.0 / d) * (z - rho * sv);  // w = M (z - rho B g), R1
+                o = jacobi_minv(ad, bd, a.sigma, a.mfloor) * (z - rho * sv);  // w = M (z - rho B g), R1
             } else if (a.out_mode == 1) {
                 o = z;
             }

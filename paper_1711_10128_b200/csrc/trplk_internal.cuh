@@ -210,6 +210,16 @@ void pl1_pt(int64_t n, const double* g, const double* p, const double* num, cons
             int variant, const Pl1Dev* d, int m, double* pt, cudaStream_t st);
 
 // Kernel launchers (kernels.cu)
+// Jacobi preconditioner entry M_ii = 1 / max(|A_ii - sigma B_ii|, mfloor) (reading R12);
+// mfloor < 0 encodes M = I (trplk_options.precond = 1: no preconditioning, the thick-restart
+// Lanczos reduction of eq 2.1, when k_plus = 0).
+__device__ __forceinline__ double jacobi_minv(double ad, double bd, double sigma, double mfloor) {
+    if (mfloor < 0.0) return 1.0;
+    double d = fabs(ad - sigma * bd);
+    d = d > mfloor ? d : mfloor;
+    return 1.0 / d;
+}
+
 // The kernel function most recently launched by this host thread (measurement: bench.py and the
 // live profile name the instantiation that ran, trplk_profile_kernels).
 extern thread_local const void* g_last_kern;

@@ -40,12 +40,23 @@ class Allocator(ctypes.Structure):
 
 class Dist(ctypes.Structure):
     _fields_ = [("rank", _I), ("nranks", _I), ("row_begin", _I64), ("row_end", _I64),
-                ("nccl_unique_id", _P), ("loopback", _P)]
+                ("nccl_unique_id", _P)]
+
+
+_AG_FN = ctypes.CFUNCTYPE(_I, _P, _P, ctypes.c_size_t, _P)
+_SR_FN = ctypes.CFUNCTYPE(_I, _I, ctypes.POINTER(_I), ctypes.POINTER(_P), ctypes.POINTER(ctypes.c_size_t),
+                          _I, ctypes.POINTER(_I), ctypes.POINTER(_P), ctypes.POINTER(ctypes.c_size_t), _P)
+_AR_FN = ctypes.CFUNCTYPE(_I, ctypes.POINTER(_D), _I, _I, _P)
+
+
+class HostCommS(ctypes.Structure):
+    _fields_ = [("allgather", _AG_FN), ("sendrecv", _SR_FN), ("allreduce", _AR_FN), ("user", _P)]
 
 
 class Options(ctypes.Structure):
     _fields_ = [("seed", ctypes.c_uint64), ("max_cycles", _I), ("tol_mode", _I),
-                ("restart_size", _I), ("lock_mode", _I), ("debug_checks", _I), ("use_graphs", _I)]
+                ("restart_size", _I), ("lock_mode", _I), ("debug_checks", _I), ("use_graphs", _I),
+                ("precond", _I)]
 
 
 class Stats(ctypes.Structure):
@@ -84,6 +95,7 @@ _sig("trplk_k_sym_eig", _I, [_P, _I, _P, _P, _P])
 _sig("trplk_k_residual", _I, [_P, _P, _D, _P, _P, _P])
 _sig("trplk_k_sym_eig_time", _I, [_P, _I, _P, _I, _P, _P])
 _sig("trplk_loopback_create", _I, [_I, ctypes.POINTER(_P)])
+_sig("trplk_create_ex", _I, [ctypes.POINTER(_P), _I64, _P, _P, _P, _P, _P, _P, _D, _P, _P, _P, _P, _P])
 _sig("trplk_set_debug", _I, [_P, _I])
 _sig("trplk_loopback_destroy", None, [_P])
 _sig("trplk_k_random", _I, [_P, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64, _P])
@@ -91,6 +103,7 @@ _sig("trplk_plan_ghosts", _I, [_I64, _I64, _P, _P, _P, _P, _P, _I, _P, _P, _I64,
 _sig("trplk_profile", _I, [_P, _I])
 _sig("trplk_profile_read", _I, [_P, _P, _P, ctypes.POINTER(_I64)])
 _sig("trplk_profile_kernels", _I, [_P, ctypes.c_char_p, ctypes.c_size_t])
+_sig("trplk_profile_phases", _I, [_P, _P, ctypes.POINTER(_I64)])
 _sig("trplk_pl1_solve", _I, [_P, _I, _D, _I, _I, _I, ctypes.c_uint64, _P, _P, _P, _P, _I, _P, _P, _P, _P,
                              ctypes.POINTER(Stats)])
 
@@ -99,7 +112,8 @@ EXPORTED = ["trplk_options_default", "trplk_nccl_unique_id", "trplk_create", "tr
             "trplk_k_step1", "trplk_k_cgs2", "trplk_k_rotate", "trplk_k_sym_eig",
             "trplk_k_residual", "trplk_k_random", "trplk_profile", "trplk_profile_read",
             "trplk_plan_ghosts", "trplk_k_sym_eig_time", "trplk_loopback_create", "trplk_loopback_destroy",
-            "trplk_set_debug", "trplk_pl1_solve", "trplk_profile_kernels"]
+            "trplk_set_debug", "trplk_pl1_solve", "trplk_profile_kernels", "trplk_create_ex",
+            "trplk_profile_phases"]
 
 
 class TrplkError(RuntimeError):
@@ -206,12 +220,74 @@ def trplk_set_debug(ctx, flags: int):
     ctx.check(_lib.trplk_set_debug(ctx.handle, int(flags)))
 
 
+def host_comm(group):
+    """trplk_host_comm callbacks over a torch.distributed process group (gloo): the row-partition
+    exchanges staged through host memory (several processes may then share one GPU)."""
+    import traceback
+
+    import torch
+    import torch.distributed as dist
+
+    nr = dist.get_world_size(group)
+    grank = (lambda r: dist.get_global_rank(group, r)) if group is not dist.group.WORLD else (lambda r: r)
+
+    def _view(addr, nbytes):
+        return torch.from_numpy(np.ctypeslib.as_array((ctypes.c_uint8 * nbytes).from_address(addr)))
+
+    def ag(send, recv, nbytes, user):
+        try:
+            src = _view(send, nbytes).clone() if nbytes else torch.empty(0, dtype=torch.uint8)
+            outs = [torch.empty(nbytes, dtype=torch.uint8) for _ in range(nr)]
+            dist.all_gather(outs, src, group=group)
+            if nbytes:
+                _view(recv, nbytes * nr).copy_(torch.cat(outs))
+            return 0
+        except Exception:
+            traceback.print_exc()
+            return 1
+
+    def sr(ns, sp, sb, sn, nrv, rp, rb, rn, user):
+        try:
+            reqs, bufs = [], []
+            for j in range(nrv):
+                if rn[j]:
+                    t = torch.empty(rn[j], dtype=torch.uint8)
+                    bufs.append((t, rb[j], rn[j]))
+                    reqs.append(dist.irecv(t, src=grank(rp[j]), group=group))
+            for i in range(ns):
+                if sn[i]:
+                    reqs.append(dist.isend(_view(sb[i], sn[i]).clone(), dst=grank(sp[i]), group=group))
+            for q in reqs:
+                q.wait()
+            for t, addr, nb in bufs:
+                _view(addr, nb).copy_(t)
+            return 0
+        except Exception:
+            traceback.print_exc()
+            return 1
+
+    def ar(v, count, op, user):
+        try:
+            t = torch.from_numpy(np.ctypeslib.as_array(v, shape=(count,)).copy())
+            dist.all_reduce(t, op=dist.ReduceOp.SUM if op == 0 else dist.ReduceOp.MAX, group=group)
+            np.ctypeslib.as_array(v, shape=(count,))[:] = t.numpy()
+            return 0
+        except Exception:
+            traceback.print_exc()
+            return 1
+
+    fns = (_AG_FN(ag), _SR_FN(sr), _AR_FN(ar))
+    return HostCommS(fns[0], fns[1], fns[2], None), fns
+
+
 def trplk_create(A, B=None, sigma: float = 0.0, n_global: Optional[int] = None, row_begin: int = 0,
                  row_end: Optional[int] = None, group=None, stream=None, torch_alloc: bool = True,
-                 loopback=None) -> Context:
+                 loopback=None, comm: str = "nccl") -> Context:
     """Create a context.  A/B: inputs.CSR (this rank's rows) or scipy CSR.  For several ranks pass
-    the torch.distributed `group` and this rank's row range; rank 0's NCCL id is broadcast.
-    loopback=(hub, rank, nranks): the rank of an in-process loopback solve (tests only)."""
+    the torch.distributed `group` and this rank's row range: comm="nccl" (production: rank 0's NCCL
+    id is broadcast) or comm="host" (host-staged exchanges through the group's own collectives,
+    e.g. gloo; processes may share one GPU).  loopback=(hub, rank, nranks): the rank of an
+    in-process loopback solve (tests only)."""
     import torch
 
     ra, ca, va = _csr_arrays(A)
@@ -228,7 +304,17 @@ def trplk_create(A, B=None, sigma: float = 0.0, n_global: Optional[int] = None, 
     sptr = stream.cuda_stream
     keep = [ra, ca, va, rb, cb, vb]
     dist_p = None
-    if group is not None:
+    hub_p, hc_p = None, None
+    if group is not None and comm == "host":
+        import torch.distributed as dist
+        rank, nranks = dist.get_rank(group), dist.get_world_size(group)
+        hc, fns = host_comm(group)
+        keep += [hc, fns]
+        hc_p = ctypes.byref(hc)
+        d = Dist(rank, nranks, row_begin, row_end, None)
+        keep.append(d)
+        dist_p = ctypes.byref(d)
+    elif group is not None:
         import torch.distributed as dist
         rank, nranks = dist.get_rank(group), dist.get_world_size(group)
         idt = torch.zeros(128, dtype=torch.uint8)
@@ -240,16 +326,17 @@ def trplk_create(A, B=None, sigma: float = 0.0, n_global: Optional[int] = None, 
                        group=group)
         idb = ctypes.create_string_buffer(bytes(idt.cpu().numpy().tobytes()), 128)
         keep.append(idb)
-        d = Dist(rank, nranks, row_begin, row_end, ctypes.cast(idb, _P), None)
+        d = Dist(rank, nranks, row_begin, row_end, ctypes.cast(idb, _P))
         keep.append(d)
         dist_p = ctypes.byref(d)
     elif loopback is not None:
         hub, rank, nranks = loopback
-        d = Dist(rank, nranks, row_begin, row_end, None, hub)
+        d = Dist(rank, nranks, row_begin, row_end, None)
         keep.append(d)
         dist_p = ctypes.byref(d)
+        hub_p = hub
     elif row_begin != 0 or row_end != n_global:
-        d = Dist(0, 1, row_begin, row_end, None, None)
+        d = Dist(0, 1, row_begin, row_end, None)
         keep.append(d)
         dist_p = ctypes.byref(d)
     alloc_p = None
@@ -258,8 +345,12 @@ def trplk_create(A, B=None, sigma: float = 0.0, n_global: Optional[int] = None, 
         keep += [al, fns]
         alloc_p = ctypes.byref(al)
     h = _P()
-    st = _lib.trplk_create(ctypes.byref(h), n_global, _ptr(ra), _ptr(ca), _ptr(va), _ptr(rb), _ptr(cb),
-                           _ptr(vb), float(sigma), dist_p, alloc_p, sptr)
+    if hub_p is None and hc_p is None:
+        st = _lib.trplk_create(ctypes.byref(h), n_global, _ptr(ra), _ptr(ca), _ptr(va), _ptr(rb), _ptr(cb),
+                               _ptr(vb), float(sigma), dist_p, alloc_p, sptr)
+    else:
+        st = _lib.trplk_create_ex(ctypes.byref(h), n_global, _ptr(ra), _ptr(ca), _ptr(va), _ptr(rb), _ptr(cb),
+                                  _ptr(vb), float(sigma), dist_p, hub_p, hc_p, alloc_p, sptr)
     if st != 0:
         msg = _lib.trplk_last_error(h).decode() if h.value else "create failed"
         if h.value:
@@ -456,3 +547,22 @@ def trplk_profile_kernels(ctx: Context) -> list:
     buf = ctypes.create_string_buffer(4096)
     ctx.check(_lib.trplk_profile_kernels(ctx.handle, buf, len(buf)))
     return buf.value.decode().split(";")
+
+
+def trplk_create_ex(A, B=None, sigma: float = 0.0, **kw) -> Context:
+    """trplk_create with the exchanges through a loopback hub (loopback=(hub, rank, nranks)) or a
+    host-staged process group (group=..., comm="host"): the C entry trplk_create_ex."""
+    if kw.get("loopback") is None and kw.get("comm", "nccl") != "host":
+        raise TypeError("trplk_create_ex needs loopback=(hub, rank, nranks) or group=..., comm='host'")
+    return trplk_create(A, B, sigma, **kw)
+
+
+PHASES = ["seed CGS2", "inner steps", "+K", "RR eig", "rotation", "residual"]
+
+
+def trplk_profile_phases(ctx: Context) -> dict:
+    """Live cycle-phase profile: device ms per phase summed over `count` profiled cycles."""
+    ms = np.zeros(6)
+    cnt = _I64()
+    ctx.check(_lib.trplk_profile_phases(ctx.handle, _ptr(ms), ctypes.byref(cnt)))
+    return {"phases": PHASES, "ms": ms, "count": cnt.value}

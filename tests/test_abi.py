@@ -47,7 +47,8 @@ def test_options_defaults_via_abi():
     build.build()
     from paper_1711_10128_b200 import trplk
     o = trplk.make_options()
-    assert (o.seed, o.max_cycles, o.tol_mode, o.restart_size, o.lock_mode, o.use_graphs) == (12, 5000, 0, 0, 0, 1)
+    assert (o.seed, o.max_cycles, o.tol_mode, o.restart_size, o.lock_mode, o.use_graphs, o.precond) == (
+        12, 5000, 0, 0, 0, 1, 0)
 
 
 def test_library_links_sm100a_code():

@@ -115,3 +115,66 @@ def test_slab_partition_world2(cfg, N):
     for r in res:
         assert r[1] == "ok", r
     assert all(r[2] > 0 for r in res)  # each slab has a halo
+
+
+def _hostcomm_worker(rank, world, port, q):
+    """The host-staged exchange callbacks (trplk.host_comm: what trplk_create_ex calls for
+    comm='host') over a world-size-2 gloo group, called through their C function pointers exactly
+    as the library calls them: allgather in rank order, grouped send/recv with per-peer sizes, and
+    the create-time sum / max allreduce."""
+    import ctypes
+    import sys
+    sys.path.insert(0, ROOT)
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1711_10128_b200 import trplk
+        hc, fns = trplk.host_comm(dist.group.WORLD)
+        # allgather: 5 doubles per rank -> rank-ordered concatenation
+        send = np.arange(5, dtype=np.float64) + 100 * rank
+        recv = np.zeros(5 * world)
+        assert hc.allgather(send.ctypes.data, recv.ctypes.data, send.nbytes, None) == 0
+        assert np.array_equal(recv, np.concatenate([np.arange(5) + 100 * r for r in range(world)]))
+        # sendrecv: a halo-like exchange with different sizes per direction (int64 and fp64 payloads)
+        peer = 1 - rank
+        out = np.arange(3 + rank, dtype=np.int64) * (rank + 1)
+        inn = np.zeros(3 + peer, dtype=np.int64)
+        sp = (ctypes.c_int * 1)(peer)
+        sb = (ctypes.c_void_p * 1)(out.ctypes.data)
+        sn = (ctypes.c_size_t * 1)(out.nbytes)
+        rb_ = (ctypes.c_void_p * 1)(inn.ctypes.data)
+        rn = (ctypes.c_size_t * 1)(inn.nbytes)
+        assert hc.sendrecv(1, sp, sb, sn, 1, sp, rb_, rn, None) == 0
+        assert np.array_equal(inn, np.arange(3 + peer) * (peer + 1))
+        # allreduce: sum and max of host doubles (create: ||A||_F^2, max |A_jj|)
+        v = np.array([1.5 + rank, -2.0 * rank])
+        assert hc.allreduce(v.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), 2, 0, None) == 0
+        assert np.array_equal(v, [1.5 + 2.5, -2.0])
+        w = np.array([3.0 * rank, 7.0 - rank])
+        assert hc.allreduce(w.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), 2, 1, None) == 0
+        assert np.array_equal(w, [3.0, 7.0])
+        q.put((rank, "ok", None))
+    except Exception:  # pragma: no cover - reported to the parent
+        import traceback
+        q.put((rank, "fail", traceback.format_exc()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_host_comm_callbacks_world2():
+    import torch.multiprocessing as mp
+    from paper_1711_10128_b200 import build
+    build.build()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_hostcomm_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=240) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    for r in res:
+        assert r[1] == "ok", r

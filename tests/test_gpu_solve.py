@@ -314,3 +314,19 @@ def test_graph_cache_across_contexts(gen):
         ctx.close()
         assert np.array_equal(ev, ev0) and np.array_equal(rs, rs0)
         assert st["a_matvecs"] == st0["a_matvecs"]
+
+
+@pytest.mark.parametrize("name,N,l", [("C2", 12, 0), ("C2", 24, 0), ("C4", 8, 0), ("C1", None, 0), ("C2", 16, 2)])
+def test_no_preconditioner_trlan_baseline(orc, gen, name, N, l):
+    """options.precond = 1 (M = I): with k_plus = 0 the thick-restart Lanczos baseline of eq 2.1
+    (NEXT-4; the oracle pins its space per cycle in test_oracle_solver.py), the same parity as
+    the preconditioned solve against the oracle run with precond = 1.  C1 (n = 1000) runs the
+    single-CTA path, C2-24 the multi-kernel one, C4 the pencil."""
+    torch, trplk = need_gpu()
+    P = gen.make(name, N=N)
+    P.l = l
+    P.q = P.q if name != "C1" else 12
+    g = gpu_solve(trplk, P, precond=1)
+    o = oracle_solve(orc, P, precond=1)
+    check_parity(g, o, P)
+    assert g["stats"]["precond_applies"] >= 0

@@ -277,3 +277,43 @@ def test_closed_form_laplace_basis(gen):
     assert np.max(np.abs(V.T @ V - np.eye(10))) <= 1e-14
     assert groups == [[0], [1, 2, 3], [4, 5, 6], [7, 8, 9]]
     assert np.allclose(lam, np.linalg.eigvalsh(A.toarray())[:10], rtol=0, atol=1e-13)
+
+
+def test_trlan_baseline_m_identity(orc, gen):
+    """NEXT-4 baseline: precond = none sets M = I (no other change).  With l = 0 and p = 1 the RR
+    space of every cycle is thick-restart Lanczos's, eq 2.1: span{x, r, A r, ..,
+    A^{m-1} r} -- explicit powers of A, on a NON-constant diagonal (where the Jacobi M would differ
+    from I).  With a random block start (p = 3, the paper's rand(n, k)) the Ritz residuals
+    are not collinear, so the space is eq 3.2 with M = I: span{X, u1, C u1, ..}, C = (I - X X^T B)
+    (A - rho B) -- pinned densely per cycle, also for the pencil C4."""
+    P = gen.make("C2", N=5)
+    A, _ = _dense_pencil(P)
+    m = 4
+    r = orc.solve(P.A, None, 1, 1 + m, 0, 1e-13, dump_cycles=6, max_cycles=6, precond=1)
+    d = r["dump"]
+    for c in range(len(d["rho"])):
+        x, rho = d["X"][c][:, 0], d["rho"][c]
+        v = A @ x - rho * x
+        cols = [x[:, None]]
+        for _ in range(m):
+            cols.append((v / np.linalg.norm(v))[:, None])
+            v = A @ cols[-1][:, 0]
+        th = _rr_dense(A, None, np.hstack(cols), 1)
+        assert abs(th[0] - r["log"]["thetas"][c][0]) <= 1e-10 * abs(th[0]), c
+    for name in ("C2", "C4"):
+        P = gen.make(name, N=5)
+        A, B = _dense_pencil(P)
+        Bm = np.eye(A.shape[0]) if B is None else B
+        p = 3
+        r = orc.solve(P.A, P.B, p, p + m, 0, 1e-13, dump_cycles=6, max_cycles=6, precond=1)
+        d = r["dump"]
+        for c in range(len(d["rho"])):
+            X, rho, t = d["X"][c], d["rho"][c], d["t"][c]
+            C = (np.eye(len(Bm)) - X @ X.T @ Bm) @ (A - rho * Bm)
+            cols = [X]
+            v = C @ X[:, t - 1]
+            for _ in range(m):
+                cols.append((v / np.linalg.norm(v))[:, None])
+                v = C @ cols[-1][:, 0]
+            th = _rr_dense(A, B, np.hstack(cols), p)
+            assert np.max(np.abs(th - r["log"]["thetas"][c][:p]) / np.abs(th)) <= 1e-10, (name, c)
