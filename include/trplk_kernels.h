@@ -35,6 +35,18 @@ trplk_status trplk_k_step1(trplk_ctx* ctx, const double* U, int64_t ldu, int k, 
 trplk_status trplk_k_cgs2(trplk_ctx* ctx, const double* U, int64_t ldu, int k, const double* w,
                           double* out, double* h, double* beta, int* breakdown, int* passes);
 
+/* Block kernel of the +K augmentation (block.cuh; Alg.1 steps 6-8), c <= 8
+ * vectors against U(:,0:k) in one pass over U:
+ *   mode 0 GRAM  HV = U^T Y (k x c),            G = Y^T Y (c x c)
+ *   mode 1 UPD   Q = Y Rinv (Rinv: c x c upper triangle, NULL = I), Y' = Q - U H -> Yout (device,
+ *                may alias Y), HV = U^T Y', G = Y'^T Y'      (H: k x c host, required)
+ *   mode 2 SPMM  HV = U^T (A Y)   (Y with ghost tails; G not written)
+ * Host matrices column-major with leading dimension = their row count (HV: k, G/Rinv: c, H: k).
+ * Errors: EINVAL (c outside 1..8, k > 64, lds, missing H/Yout for UPD), ECUDA. */
+trplk_status trplk_k_block(trplk_ctx* ctx, int mode, const double* U, int64_t ldu, int k, const double* Y,
+                           int64_t ldy, int c, const double* Rinv, const double* H, double* Yout, int64_t ldyo,
+                           double* HV, double* G);
+
 /* X(:,0:ncol) = U(:,0:k) Y(0:k,0:ncol) with the fp64 DMMA kernel (Alg.1 steps 11/15,
  * PAPER.md:193,198).  Y host, column-major k x ncol (ncol <= 24). */
 trplk_status trplk_k_rotate(trplk_ctx* ctx, const double* U, int64_t ldu, int k, const double* Y,

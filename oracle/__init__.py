@@ -44,7 +44,8 @@ class _Problem(ctypes.Structure):
                 ("p", ctypes.c_int), ("q", ctypes.c_int), ("l", ctypes.c_int),
                 ("tol", ctypes.c_double), ("tol_mode", ctypes.c_int), ("seed", ctypes.c_uint64),
                 ("max_cycles", ctypes.c_int), ("restart_size", ctypes.c_int),
-                ("lock_mode", ctypes.c_int), ("debug", ctypes.c_int), ("precond", ctypes.c_int)]
+                ("lock_mode", ctypes.c_int), ("debug", ctypes.c_int), ("precond", ctypes.c_int),
+                ("block", ctypes.c_int)]
 
 
 class _Report(ctypes.Structure):
@@ -204,7 +205,7 @@ STATUS = {0: "OK", 1: "EINVAL", 2: "NOT_CONVERGED", 3: "BREAKDOWN"}
 
 def solve(A, B=None, p=5, q=20, l=1, tol=1e-8, sigma=0.0, seed=12, max_cycles=5000,
           tol_mode=0, restart_size=0, lock_mode=0, debug=False, dump_cycles=0,
-          want_vectors=True, sample_rows=None, verbose=False, precond=0):
+          want_vectors=True, sample_rows=None, verbose=False, precond=0, block=1):
     """Run Algorithm 1 (TRPL+K).  Returns a dict with eigenvalues, vectors, residuals,
     counters and the per-cycle log."""
     ra, ca, va = _csr(A)
@@ -213,7 +214,7 @@ def solve(A, B=None, p=5, q=20, l=1, tol=1e-8, sigma=0.0, seed=12, max_cycles=50
     ph = restart_size if restart_size > 0 else p
     prob = _Problem(n, _ptr(ra), _ptr(ca), _ptr(va), _ptr(rb), _ptr(cb), _ptr(vb), sigma,
                     p, q, l, tol, tol_mode, seed, max_cycles, restart_size, lock_mode,
-                    1 if debug else 0, precond)
+                    1 if debug else 0, precond, block)
     cap = max_cycles
     logs = {
         "t": np.zeros(cap, np.int32), "mv": np.zeros(cap, np.int64),
@@ -264,7 +265,7 @@ def inner_steps(A, B, M, rho, U, k0, nsteps, T=None, work=None):
     q = U.shape[1]
     T = np.zeros((q, q), order="F") if T is None else T
     prob = _Problem(n, _ptr(ra), _ptr(ca), _ptr(va), _ptr(rb), _ptr(cb), _ptr(vb), 0.0,
-                    1, q, 0, 1.0, 0, 12, 1, 0, 0, 0, 0)
+                    1, q, 0, 1.0, 0, 12, 1, 0, 0, 0, 0, 1)
     M = np.ascontiguousarray(M, np.float64)
     if work is not None:
         assert work.dtype == np.float64 and work.size >= 4 * n and work.flags["C_CONTIGUOUS"]

@@ -284,16 +284,18 @@ static void rotate_rows_inplace(int64_t n, int k, double* U, const double* Y, in
 /* One inner step of eq 3.1 on the basis U(:,0:k), g_j = U(:,k-1):
  *   z = A g_j;  T(1:k,k) = U^T z (mirrored);  if `next`: w = M(z - rho B g_j) (R1), CGS2_B of w
  *   against U(:,0:k) (R2, R3) and g_{j+1} = w/beta into U(:,k).  Returns 1 on a breakdown (R16). */
-static int inner_step(ctx_t* c, const double* M, double rho, int next, double* U, int k, double* T, int q,
-                      double* z, double* s, double* w, double* Bw) {
+static int inner_step_at(ctx_t* c, const double* M, double rho, int next, double* U, int k, int gpos, double* T,
+                         int q, double* z, double* s, double* w, double* Bw) {
+    /* g = U(:, gpos) of a basis of width k; its T column covers rows 0..k-1 (mirrored), its
+     * preconditioned image is CGS2-orthogonalised against all k columns and appended at k */
     const int64_t n = c->n;
-    double* g = U + (size_t)n * (k - 1);
+    double* g = U + (size_t)n * gpos;
     double beta;
     applyA(c, g, z);
     for (int i = 0; i < k; ++i) {
         double v = orc_dot(n, U + (size_t)n * i, z);
-        T[i + (size_t)q * (k - 1)] = v;
-        T[(k - 1) + (size_t)q * i] = v;
+        T[i + (size_t)q * gpos] = v;
+        T[gpos + (size_t)q * i] = v;
     }
     if (!next) return 0;
     applyB(c, g, s);
@@ -302,6 +304,11 @@ static int inner_step(ctx_t* c, const double* M, double rho, int next, double* U
     if (cgs2_ctx(c, k, U, w, Bw, NULL, &beta, NULL)) return 1;
     scal_copy(n, 1.0 / beta, w, U + (size_t)n * k);
     return 0;
+}
+
+static int inner_step(ctx_t* c, const double* M, double rho, int next, double* U, int k, double* T, int q,
+                      double* z, double* s, double* w, double* Bw) {
+    return inner_step_at(c, M, rho, next, U, k, k - 1, T, q, z, s, w, Bw);
 }
 
 int orc_inner_steps(const orc_problem* P, const double* M, double rho, double* U, int k0, int nsteps,
@@ -325,7 +332,7 @@ int orc_trplk_solve(const orc_problem* P, double* evals, double* evecs, double* 
     const int ph = P->restart_size > 0 ? P->restart_size : p; /* R5: p^ = p by default */
     if (rep) { rep->status = 1; rep->cycles = 0; rep->log_len = 0; }
     if (n < 1 || p < 1 || l < 0 || ph < p || q - ph - l < 1 || !(P->tol > 0.0) || ph + 1 > n ||
-        P->max_cycles < 1)
+        P->max_cycles < 1 || P->block > 8 || q > 64)
         return 1; /* EINVAL */
     const int m = q - ph - l; /* inner steps per cycle (R5) */
 
@@ -389,6 +396,20 @@ int orc_trplk_solve(const orc_problem* P, double* evals, double* evecs, double* 
     for (int64_t i = 0; i < n; ++i) r[i] = W[i] - rho * s[i];
     for (int64_t i = 0; i < n; ++i) u[i] = M[i] * r[i];
     c.prec++;
+    /* block TRPL+K (NEXT-3; reading B1): seeds M r_{t+i} of the next b-1 targets too */
+    const int b = P->block > 1 ? P->block : 1;
+    double* ub = b > 1 ? (double*)malloc((size_t)n * (b - 1) * sizeof(double)) : NULL;
+    int nub = 0;
+    if (b > 1) {
+        nub = b - 1 < ph - 1 ? b - 1 : ph - 1;
+        if (nub > m - 1) nub = m - 1 > 0 ? m - 1 : 0;
+        for (int i = 1; i <= nub; ++i) { /* r_i = A x_i - theta_i B x_i from W (no matvec) */
+            double* ui = ub + (size_t)n * (i - 1);
+            applyB(&c, U + (size_t)n * i, s);
+            for (int64_t j = 0; j < n; ++j) ui[j] = M[j] * (W[j + (size_t)n * i] - th[i] * s[j]);
+            c.prec++;
+        }
+    }
     free(W);
     W = NULL;
     Xp = (double*)malloc((size_t)n * (l > 0 ? l : 1) * sizeof(double));
@@ -414,11 +435,32 @@ int orc_trplk_solve(const orc_problem* P, double* evals, double* evecs, double* 
         }
         int k = ph;
         scal_copy(n, 1.0 / beta, w, U + (size_t)n * k);
-        /* ---- inner projected Lanczos, eq 3.1, R1/R2 */
-        for (int j = 1; j <= m; ++j) {
-            k += 1; /* k = p^ + j */
-            ++inner_steps;
-            if (inner_step(&c, M, rho, j < m, U, k, T, q, z, s, w, Bw)) break; /* R16: basis ends early */
+        if (b == 1) {
+            /* ---- inner projected Lanczos, eq 3.1, R1/R2 */
+            for (int j = 1; j <= m; ++j) {
+                k += 1; /* k = p^ + j */
+                ++inner_steps;
+                if (inner_step(&c, M, rho, j < m, U, k, T, q, z, s, w, Bw)) break; /* R16: basis ends early */
+            }
+        } else {
+            /* ---- block version (B1): seeds M r_{t+i}, i < b_e, CGS2_B against [X, earlier seeds]
+             * (a dependent one is dropped), then every column's image M (A - rho B) g under the
+             * cycle's ONE shift rho = theta_t (eq 3.2's operator C), CGS2_B against the whole basis
+             * and appended, in column order, until the basis has p^ + m columns: span{X} plus the
+             * block Krylov space of C from the seed block, independent of the Gram-Schmidt order */
+            int width = ph + 1;
+            for (int i = 1; i <= nub && width < ph + m; ++i) {
+                memcpy(w, ub + (size_t)n * (i - 1), (size_t)n * sizeof(double));
+                if (cgs2_ctx(&c, width, U, w, Bw, NULL, &beta, NULL)) continue;
+                scal_copy(n, 1.0 / beta, w, U + (size_t)n * width);
+                ++width;
+            }
+            for (int next = ph; next < width; ++next) {
+                ++inner_steps;
+                const int produce = width < ph + m;
+                if (!inner_step_at(&c, M, rho, produce, U, width, next, T, q, z, s, w, Bw) && produce) ++width;
+            }
+            k = width;
         }
         /* ---- +K: X^prev appended after G, explicitly orthogonalised, l matvecs (Alg.1 7-8) */
         int appended = 0;
@@ -517,6 +559,16 @@ int orc_trplk_solve(const orc_problem* P, double* evals, double* evecs, double* 
         rho = th[t - 1];
         for (int64_t i = 0; i < n; ++i) u[i] = M[i] * r[i];
         c.prec++;
+        if (b > 1) { /* residuals of the next targets: one A-matvec each (B1) */
+            nub = b - 1 < ph - t ? b - 1 : ph - t;
+            if (nub > m - 1) nub = m - 1 > 0 ? m - 1 : 0;
+            for (int i = 1; i <= nub; ++i) {
+                double* ui = ub + (size_t)n * (i - 1);
+                residual(&c, U + (size_t)n * (t - 1 + i), th[t - 1 + i], w, s);
+                for (int64_t j = 0; j < n; ++j) ui[j] = M[j] * w[j];
+                c.prec++;
+            }
+        }
     }
     if (status != 0) {
         /* NOT_CONVERGED (R19) / BREAKDOWN: report the current best with verified residuals */
@@ -546,6 +598,7 @@ done:
         rep->inner_steps = inner_steps;
         rep->random_draws = draws;
     }
+    free(ub);
     free(M); free(U); free(W); free(Xp); free(w); free(Bw); free(z);
     free(s); free(r); free(u); free(T); free(Tk); free(Y); free(th);
     return status;

@@ -46,8 +46,9 @@ struct GraphRec {
 struct Sizes {  // per-solve parameters that shape the captured graphs
     int p, q, l, ph, m;
     int prec;  // trplk_options.precond (0 Jacobi, 1 M = I)
+    int blk;   // trplk_options.block (<= 1: Algorithm 1)
     bool operator<(const Sizes& o) const {
-        return std::tie(p, q, l, ph, m, prec) < std::tie(o.p, o.q, o.l, o.ph, o.m, o.prec);
+        return std::tie(p, q, l, ph, m, prec, blk) < std::tie(o.p, o.q, o.l, o.ph, o.m, o.prec, o.blk);
     }
     bool operator==(const Sizes& o) const { return !(*this < o) && !(o < *this); }
 };
@@ -82,6 +83,12 @@ struct trplk_ctx {
     double* U[2] = {nullptr, nullptr};
     double *w = nullptr, *w1 = nullptr, *w2 = nullptr, *u = nullptr, *u2 = nullptr, *xk = nullptr;
     double *T = nullptr, *Yg = nullptr, *part = nullptr, *gpart = nullptr, *red_local = nullptr, *red_all = nullptr;
+    // block +K (block.cuh): control, the block being orthogonalised, the accepted vectors, reductions
+    BlkCtl* blk = nullptr;
+    double *wblk = nullptr, *xkb = nullptr, *sblk = nullptr, *bpart = nullptr, *bgpart = nullptr, *bred_local = nullptr,
+           *bred_all = nullptr;
+    unsigned* bcounter = nullptr;
+    int blk_cols = 0;  // columns of wblk / xkb
     double* gridpart = nullptr;
     unsigned long long* gtrace = nullptr;  // TRPLK_GRID_TRACE: per-step phase timestamps
     cudaEvent_t ctev[2] = {nullptr, nullptr};  // TRPLK_CYCLE_TRACE
@@ -715,6 +722,15 @@ bool coop3(const trplk_ctx* ctx) {
     return v == 1 && ctx->nranks == 1 && !ctx->hasB;
 }
 
+// profile events inside a cycle: external event nodes under stream capture, plain records when
+// the cycle is issued eagerly (loopback / host-exchange contexts, use_graphs = 0)
+static cudaError_t record_event(trplk_ctx* ctx, cudaEvent_t ev) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(ctx->stream, &cs);
+    return cs == cudaStreamCaptureStatusActive ? cudaEventRecordWithFlags(ev, ctx->stream, cudaEventRecordExternal)
+                                               : cudaEventRecord(ev, ctx->stream);
+}
+
 // CGS2 in the B-inner product (R3) of x against V = Ubase(:, 0:kv) (kv = -1: ctl->k), result
 // normalised into Ubase(:, ctl->k) (dest_dyn) or `dest`, ctl->k += 1 on success.
 struct CgsSpec {
@@ -795,7 +811,7 @@ trplk_status cgs2(trplk_ctx* ctx, const CgsSpec& c) {
         ST(run_sdots(ctx, a, kn));
     }
     // final: y = w1 - V h1, beta from Pythagoras; pass 3 into w2 if the norm dropped > 1/sqrt2
-    if (c.mark_final) CK(cudaEventRecordWithFlags(c.mark_final, ctx->stream, cudaEventRecordExternal));
+    if (c.mark_final) CK(record_event(ctx, c.mark_final));
     {
         UpdArgs u = up_base(ctx);
         u.x = ctx->w1;
@@ -878,6 +894,25 @@ trplk_status residual(trplk_ctx* ctx, const double* x, int x_dyn, int theta_idx,
     return TRPLK_OK;
 }
 
+trplk_status ensure_block_buffers(trplk_ctx* ctx, int c) {
+    if (ctx->blk_cols >= c) return TRPLK_OK;
+    dev_free(ctx, ctx->wblk);
+    dev_free(ctx, ctx->xkb);
+    dev_free(ctx, ctx->sblk);
+    ctx->wblk = ctx->xkb = ctx->sblk = nullptr;
+    const size_t ld = (size_t)ctx->ld;
+    ST(dalloc(ctx, &ctx->wblk, ld * c));
+    ST(dalloc(ctx, &ctx->xkb, ld * c));
+    ST(dalloc(ctx, &ctx->sblk, ld * c));
+    CK(cudaMemsetAsync(ctx->wblk, 0, ld * c * 8, ctx->stream));
+    CK(cudaMemsetAsync(ctx->xkb, 0, ld * c * 8, ctx->stream));
+    CK(cudaMemsetAsync(ctx->sblk, 0, ld * c * 8, ctx->stream));
+    ctx->blk_cols = c;
+    for (auto& g : ctx->graphs) cudaGraphExecDestroy(g.second.exec);
+    ctx->graphs.clear();
+    return TRPLK_OK;
+}
+
 trplk_status ensure_buffers(trplk_ctx* ctx, int q, int ph) {
     if (ctx->q_alloc >= q && ctx->ph_alloc >= ph) return TRPLK_OK;
     // release previous solve buffers
@@ -909,22 +944,215 @@ trplk_status ctl_pull(trplk_ctx* ctx) {
     return TRPLK_OK;
 }
 
+// One block-kernel launch (block.cuh); several ranks: local sums, allgather, rank-ordered finalize.
+trplk_status run_block(trplk_ctx* ctx, BlkArgs a, int kmax, double bytes) {
+    a.part = ctx->bpart;
+    a.gpart = ctx->bgpart;
+    a.counter = ctx->bcounter;
+    a.maxcta = MAXCTA;
+    a.ctl = ctx->ctl;
+    ctx->model_bytes += bytes;
+    ctx->launches += ctx->nranks > 1 ? 2 : 1;
+    if (ctx->nranks > 1) {
+        a.red_local = ctx->bred_local;
+        if (!launch_block(a, kmax, ctx->stream)) {
+            ctx->err = "block kernel: unsupported width";
+            return TRPLK_EINVAL;
+        }
+        CM(ctx->cm->allgather(ctx->bred_local, ctx->bred_all, BLK_NV, 8, ctx->stream));
+        launch_blk_finalize_multi(a, ctx->bred_all, ctx->nranks, BLK_NV, ctx->stream);
+    } else if (!launch_block(a, kmax, ctx->stream)) {
+        ctx->err = "block kernel: unsupported width";
+        return TRPLK_EINVAL;
+    }
+    CK(cudaGetLastError());
+    return TRPLK_OK;
+}
+
+// +K as one block (B = I): block CGS2 of the c = nprev X^prev columns against U with Cholesky-QR
+// inside the block (BCGS2, third pass gated by R3's rule, dependent columns dropped by R16's
+// threshold), the accepted vectors appended, then one SpMM for their T columns (eq 3.1).  Four
+// passes over U for the whole block instead of four per column.  TRPLK_KPLUS=col: per column.
+bool block_kplus(const trplk_ctx* ctx, int nprev) {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("TRPLK_KPLUS");
+        v = (e && !strcmp(e, "col")) ? 0 : 1;
+    }
+    return v == 1 && !ctx->hasB && nprev >= 1 && nprev <= BC;
+}
+
+// Block CGS2 (BCGS2 with Cholesky-QR inside the block) of the c vectors Y against the current basis
+// Uc(:, 0:ctl->k): two projections (a third gated by R3's rule), dependent vectors dropped (R16),
+// the accepted ones appended at Uc(:, ctl->k ..) and copied to the static block xkb; ctl->k grows.
+// first_done: the first pass (U^T Y, Y^T Y) is already in blk->HV[0] / blk->G[0] (the fused SpMM).
+// c_dyn: the vector count lives on the device (static c is the upper bound for the byte model).
+trplk_status bcgs2_blk(trplk_ctx* ctx, double* Uc, int kn, const double* Y, int y_dyn, int c, const int* c_dyn,
+                       bool first_done, int seed) {
+    const int64_t ld = ctx->ld;
+    const double vb = vec_bytes(ctx);
+    BlkArgs b{};
+    b.nrows = ctx->n_loc;
+    b.U = Uc;
+    b.ldu = ld;
+    b.k_from_ctl = 1;
+    b.c = c;
+    b.c_dyn = c_dyn;
+    b.gate = F_CYCLE;
+    if (!first_done) {  // pass 1: H0 = U^T Y, G0 = Y^T Y
+        BlkArgs g = b;
+        g.mode = BM_GRAM;
+        g.Y = Y;
+        g.y_dyn = y_dyn;
+        g.ldy = ld;
+        g.HV = ctx->blk->HV[0];
+        g.G = ctx->blk->G[0];
+        ST(run_block(ctx, g, kn, vb * (kn + c)));
+    }
+    // pass 2: W1 = Y - U H0, U^T W1, W1^T W1
+    BlkArgs u1 = b;
+    u1.mode = BM_UPD;
+    u1.Y = Y;
+    u1.y_dyn = y_dyn;
+    u1.ldy = ld;
+    u1.H = ctx->blk->HV[0];
+    u1.Yout = ctx->wblk;
+    u1.ldyo = ld;
+    u1.HV = ctx->blk->HV[1];
+    u1.G = ctx->blk->G[1];
+    ST(run_block(ctx, u1, kn, vb * (kn + 2 * c)));
+    launch_blk_ctl(ctx->blk, ctx->ctl, 1, c, c_dyn, seed, F_CYCLE, ctx->stream);
+    // pass 3: W2 = W1 R1^-1 - U (U^T W1 R1^-1) in place, U^T W2, W2^T W2
+    BlkArgs u2 = b;
+    u2.mode = BM_UPD;
+    u2.Y = ctx->wblk;
+    u2.ldy = ld;
+    u2.Rinv = ctx->blk->Rinv;
+    u2.H = ctx->blk->Hs;
+    u2.Yout = ctx->wblk;
+    u2.ldyo = ld;
+    u2.HV = ctx->blk->HV[2];
+    u2.G = ctx->blk->G[2];
+    ST(run_block(ctx, u2, kn, vb * (kn + 2 * c)));
+    launch_blk_ctl(ctx->blk, ctx->ctl, 2, c, c_dyn, seed, F_CYCLE, ctx->stream);
+    // gated third pass (R3)
+    BlkArgs u3 = u2;
+    u3.gate = F_CYCLE | F_BPASS3;
+    u3.HV = ctx->blk->HV[3];
+    u3.G = ctx->blk->G[3];
+    ST(run_block(ctx, u3, kn, 0.0));
+    launch_blk_ctl(ctx->blk, ctx->ctl, 3, c, c_dyn, seed, F_CYCLE | F_BPASS3, ctx->stream);
+    // accepted vectors Q = W R^-1 into U(:, k0 ..) and the scratch block; ctl->k += accepted
+    launch_blk_place(ctx->wblk, ld, ctx->blk, ctx->ctl, Uc, ld, ctx->xkb, ld, ctx->n_loc, 0, F_CYCLE, ctx->stream);
+    ctx->launches += 4;
+    ctx->model_bytes += vb * 3 * c;
+    return TRPLK_OK;
+}
+
+// T columns of the block just appended (xkb, blk->acc vectors at blk->k0): T(1:k, k0 + j) = U^T A x~_j
+// (eq 3.1), one SpMM.  With W: also W = M (A x~ - rho x~) -> wblk and U^T W, W^T W (the first
+// pass of the next block CGS2), SpMM-with-preconditioner of the block inner step (reading B1).
+trplk_status block_spmm(trplk_ctx* ctx, double* Uc, int kn, int cmax, bool with_w) {
+    const int64_t ld = ctx->ld;
+    for (int j = 0; j < cmax; ++j) ST(halo(ctx, ctx->xkb + ld * j));
+    BlkArgs sp{};
+    sp.nrows = ctx->n_loc;
+    sp.U = Uc;
+    sp.ldu = ld;
+    sp.k_from_ctl = 1;
+    sp.mode = with_w ? BM_SPMW : BM_SPMM;
+    sp.A = ctx->A;
+    sp.sigma = ctx->sigma;
+    sp.mfloor = ctx->mfloor_solve;
+    sp.Y = ctx->xkb;
+    sp.ldy = ld;
+    sp.c = cmax;
+    sp.c_dyn = &ctx->blk->acc;
+    sp.T = ctx->T;
+    sp.ldT = QMAX;
+    sp.k0p = &ctx->blk->k0;
+    sp.gate = F_CYCLE;
+    if (with_w) {
+        sp.Yout = ctx->wblk;
+        sp.ldyo = ld;
+        sp.HV = ctx->blk->HV[0];
+        sp.G = ctx->blk->G[0];
+    }
+    const double vb = vec_bytes(ctx);
+    return run_block(ctx, sp, kn, mat_bytes(ctx, false) + vb * (kn + (with_w ? 3 : 1) * cmax));
+}
+
+trplk_status kplus_block(trplk_ctx* ctx, const Sizes& S, double* Uc, const double* Uo, int nprev, int xprev_static) {
+    const int64_t ld = ctx->ld;
+    const int kn = S.ph + S.m + nprev;  // widest basis of the cycle
+    const double* Y = xprev_static >= 0 ? Uo + ld * xprev_static : Uo;
+    ST(bcgs2_blk(ctx, Uc, kn, Y, xprev_static >= 0 ? 0 : 2, nprev, nullptr, false, 0));
+    return block_spmm(ctx, Uc, kn, nprev, false);
+}
+
+// Block inner loop (trplk_options.block = b > 1, reading B1): seeds M r_{t+i}, i < be, block CGS2
+// against X; then per group G_j of the block Krylov space of eq 3.2's C: one SpMM with the
+// preconditioner (T columns of G_j and W = M (A - rho B) G_j with its first-pass dots), a block
+// CGS2 of the images that still fit the basis (p^ + m columns), appended as G_{j+1}.
+trplk_status inner_block(trplk_ctx* ctx, const Sizes& S, double* Uc, int be, int extras) {
+    const int64_t ld = ctx->ld;
+    const int kn = S.ph + S.m;
+    if (extras)  // residuals of the next targets (the cycle's first is ctx->u): one A-matvec each
+        for (int i = 1; i < be; ++i) {
+            SdotsArgs a = sd_base(ctx);
+            a.A = ctx->A;
+            a.x = Uc;
+            a.x_dyn = 1;
+            a.x_off = i;
+            a.out_mode = 3;
+            a.uout = ctx->sblk + ld * i;
+            a.norm1 = 1;
+            a.nslot1 = N_AUX;
+            a.theta_idx = -1;
+            a.gate = F_CYCLE;
+            if (ctx->nranks > 1) {
+                ctx->err = "block inner loop: one rank only";
+                return TRPLK_EINVAL;
+            }
+            ST(run_sdots(ctx, a, 0));
+        }
+    launch_copy_cols(ctx->u, ld, ctx->sblk, ld, ctx->n_loc, 1, ctx->stream);
+    ctx->launches += 1;
+    ST(bcgs2_blk(ctx, Uc, kn, ctx->sblk, 0, be, nullptr, false, 1));
+    const int steps = (S.m + be - 1) / be;
+    for (int s = 1; s <= steps; ++s) {
+        if (s < steps) {
+            ST(block_spmm(ctx, Uc, kn, be, true));
+            launch_blk_room(ctx->blk, ctx->ctl, S.ph + S.m, F_CYCLE, ctx->stream);
+            ctx->launches += 1;
+            ST(bcgs2_blk(ctx, Uc, kn, ctx->wblk, 0, be, &ctx->blk->cin, true, 0));
+        } else {
+            ST(block_spmm(ctx, Uc, kn, be, false));
+        }
+    }
+    return TRPLK_OK;
+}
+
 // phase boundary event of the live cycle profile (trplk_profile_phases)
 static trplk_status phase_mark(trplk_ctx* ctx, int i) {
-    if (ctx->prof_on) CK(cudaEventRecordWithFlags(ctx->phev[i], ctx->stream, cudaEventRecordExternal));
+    if (ctx->prof_on) CK(record_event(ctx, ctx->phev[i]));
     return TRPLK_OK;
 }
 
 // One outer cycle after the seed vector u is in place: eq 3.1 inner steps, +K, RR, rotation,
 // residual of the target.  Issued eagerly or under stream capture.
-trplk_status issue_cycle(trplk_ctx* ctx, const Sizes& S, int cur, int nprev, int t_static, int xprev_static) {
+trplk_status issue_cycle(trplk_ctx* ctx, const Sizes& S, int cur, int nprev, int t_static, int xprev_static,
+                         int be, int extras) {
     const int oth = 1 - cur;
     double* Uc = ctx->U[cur];
     double* Uo = ctx->U[oth];
     const int64_t ld = ctx->ld;
     // seed: g_1 = (I - X X^T B) u / beta  (eq 3.2 u1 = C x_t, R4), written to column p^
     ST(phase_mark(ctx, 0));
-    {
+    if (be > 1) {  // block TRPL+K (reading B1): seeds, block inner loop
+        ST(phase_mark(ctx, 1));
+        ST(inner_block(ctx, S, Uc, be, extras));
+    } else {
         CgsSpec c{};
         c.x = ctx->u;
         c.V = Uc;
@@ -937,7 +1165,6 @@ trplk_status issue_cycle(trplk_ctx* ctx, const Sizes& S, int cur, int nprev, int
         c.clear = F_CYCLE;
         c.inc_k = 1;
         ST(cgs2(ctx, c));
-    }
     // inner steps, eq 3.1
     ST(phase_mark(ctx, 1));
     const int jmid = std::max(1, std::min(S.m - 1, S.m / 2));
@@ -960,7 +1187,7 @@ trplk_status issue_cycle(trplk_ctx* ctx, const Sizes& S, int cur, int nprev, int
         sa.gate = F_CYCLE | F_INNER;
         sa.clear = F_INNER;
         sa.force3 = ctx->force3;
-        if (ctx->prof_on) CK(cudaEventRecordWithFlags(ctx->pev[0], ctx->stream, cudaEventRecordExternal));
+        if (ctx->prof_on) CK(record_event(ctx, ctx->pev[0]));
         if (small_path(ctx, S)) {
             launch_inner_small(sa, S.q, ctx->stream);
             ctx->prof_kern[0] = g_last_kern;
@@ -979,7 +1206,7 @@ trplk_status issue_cycle(trplk_ctx* ctx, const Sizes& S, int cur, int nprev, int
         }
         CK(cudaGetLastError());
         if (ctx->prof_on)
-            for (int e = 1; e < 4; ++e) CK(cudaEventRecordWithFlags(ctx->pev[e], ctx->stream, cudaEventRecordExternal));
+            for (int e = 1; e < 4; ++e) CK(record_event(ctx, ctx->pev[e]));
         ctx->launches += 1;
         for (int j = 1; j <= S.m; ++j) {  // byte model of the m steps (as the multi-kernel path)
             const int k = S.ph + j;
@@ -1011,10 +1238,10 @@ trplk_status issue_cycle(trplk_ctx* ctx, const Sizes& S, int cur, int nprev, int
                 a.norm1 = 1;  // ||w||^2
                 a.nslot1 = N_IN2;
             }
-            if (prof) CK(cudaEventRecordWithFlags(ctx->pev[0], ctx->stream, cudaEventRecordExternal));
+            if (prof) CK(record_event(ctx, ctx->pev[0]));
             ST(run_sdots(ctx, a, k));
             if (prof) ctx->prof_kern[0] = g_last_kern;
-            if (prof) CK(cudaEventRecordWithFlags(ctx->pev[1], ctx->stream, cudaEventRecordExternal));
+            if (prof) CK(record_event(ctx, ctx->pev[1]));
             CgsSpec c{};
             if (prof) c.mark_final = ctx->pev[2];
             c.x = ctx->w;
@@ -1028,14 +1255,16 @@ trplk_status issue_cycle(trplk_ctx* ctx, const Sizes& S, int cur, int nprev, int
             c.clear = F_INNER;
             c.inc_k = 1;
             ST(cgs2(ctx, c));
-            if (prof) CK(cudaEventRecordWithFlags(ctx->pev[3], ctx->stream, cudaEventRecordExternal));
+            if (prof) CK(record_event(ctx, ctx->pev[3]));
         } else {
             ST(run_sdots(ctx, a, k));
         }
     }
+    }  // seed + inner loop of Algorithm 1
     // +K: X^prev appended after G, explicitly orthogonalised, one matvec each
     ST(phase_mark(ctx, 2));
-    for (int jj = 0; jj < nprev; ++jj) {
+    if (block_kplus(ctx, nprev)) ST(kplus_block(ctx, S, Uc, Uo, nprev, xprev_static));
+    for (int jj = 0; jj < nprev && !block_kplus(ctx, nprev); ++jj) {
         const unsigned kb = F_KCOL0 << jj;
         CgsSpec c{};
         if (xprev_static >= 0) {
@@ -1160,19 +1389,21 @@ static bool graph_from_cache(trplk_ctx* ctx, uint64_t key, const Sizes& S, Graph
     return true;
 }
 
-trplk_status run_cycle(trplk_ctx* ctx, const Sizes& S, int cur, int nprev, int t, int xprev, bool use_graph) {
+trplk_status run_cycle(trplk_ctx* ctx, const Sizes& S, int cur, int nprev, int t, int xprev, bool use_graph, int be,
+                       int extras) {
     if (ctx->loopback) use_graph = false;  // loopback exchanges are host rendezvous: eager only
     const bool multi = ctx->nranks > 1;
     const int ts = multi ? t : -1;  // static addresses are needed for the halo exchange
     const int xs = multi ? xprev : -1;
-    if (!use_graph) return issue_cycle(ctx, S, cur, nprev, ts, xs);
+    if (!use_graph) return issue_cycle(ctx, S, cur, nprev, ts, xs, be, extras);
     if (!(ctx->gsizes == S)) {
         for (auto& g : ctx->graphs) cudaGraphExecDestroy(g.second.exec);
         ctx->graphs.clear();
         ctx->gsizes = S;
     }
     const uint64_t key = ((uint64_t)cur) | ((uint64_t)nprev << 1) | ((uint64_t)(ts + 1) << 8) |
-                         ((uint64_t)(xs + 1) << 24) | ((uint64_t)(ctx->prof_on ? 1 : 0) << 40);
+                         ((uint64_t)(xs + 1) << 24) | ((uint64_t)(ctx->prof_on ? 1 : 0) << 40) |
+                         ((uint64_t)be << 44) | ((uint64_t)(extras ? 1 : 0) << 52);
     auto it = ctx->graphs.find(key);
     if (it == ctx->graphs.end()) {
         GraphRec cached;
@@ -1183,7 +1414,7 @@ trplk_status run_cycle(trplk_ctx* ctx, const Sizes& S, int cur, int nprev, int t
         const int64_t l0 = ctx->launches;
         cudaGraph_t graph;
         CK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
-        trplk_status st = issue_cycle(ctx, S, cur, nprev, ts, xs);
+        trplk_status st = issue_cycle(ctx, S, cur, nprev, ts, xs, be, extras);
         cudaError_t e = cudaStreamEndCapture(ctx->stream, &graph);
         if (st != TRPLK_OK) return st;
         if (e != cudaSuccess) {
@@ -1220,6 +1451,7 @@ void trplk_options_default(trplk_options* opt) {
     opt->debug_checks = 0;
     opt->use_graphs = 1;
     opt->precond = 0;
+    opt->block = 1;
 }
 
 trplk_status trplk_nccl_unique_id(void* out, size_t out_bytes) {
@@ -1369,6 +1601,14 @@ static trplk_status create_impl(trplk_ctx* ctx, int64_t n_global, const int64_t*
     ST(dalloc(ctx, &ctx->red_local, (size_t)NV_MAX));
     ST(dalloc(ctx, &ctx->red_all, (size_t)NV_MAX * ctx->nranks));
     ST(dalloc(ctx, &ctx->counter, NCOUNTERS));
+    ST(dalloc(ctx, &ctx->blk, 1));
+    ST(dalloc(ctx, &ctx->bpart, (size_t)BLK_NV * MAXCTA));
+    ST(dalloc(ctx, &ctx->bgpart, (size_t)BLK_NV * MAXG));
+    ST(dalloc(ctx, &ctx->bcounter, NCOUNTERS));
+    ST(dalloc(ctx, &ctx->bred_local, (size_t)BLK_NV));
+    ST(dalloc(ctx, &ctx->bred_all, (size_t)BLK_NV * ctx->nranks));
+    CK(cudaMemsetAsync(ctx->bcounter, 0, sizeof(unsigned) * NCOUNTERS, ctx->stream));
+    CK(cudaMemsetAsync(ctx->blk, 0, sizeof(BlkCtl), ctx->stream));
     if (ctx->nranks == 1 && !ctx->hasB) ST(dalloc(ctx, &ctx->gridpart, (size_t)2 * GRID_MAXCTA * GRID_NVP));
     ST(dalloc(ctx, &ctx->ctl, 1));
     CK(cudaMemsetAsync(ctx->counter, 0, sizeof(unsigned) * NCOUNTERS, ctx->stream));
@@ -1593,9 +1833,16 @@ static trplk_status solve_impl(trplk_ctx* ctx, int p, int q, int l, double tol, 
         return TRPLK_EINVAL;
     }
     ctx->mfloor_solve = opt.precond == 1 ? -1.0 : ctx->mfloor;
-    const Sizes S{p, q, l, ph, m, opt.precond};
+    const int blk = opt.block > 1 ? opt.block : 1;
+    if (blk > 1 && (blk > BC || ctx->hasB || ctx->nranks > 1)) {
+        ctx->err = "options.block: 1..8, B = I and one rank on the device";
+        return TRPLK_EINVAL;
+    }
+    const Sizes S{p, q, l, ph, m, opt.precond, blk};
     PhaseTimer pt("solve");
     ST(ensure_buffers(ctx, q, ph));
+    if (!ctx->hasB && std::max(l <= BC ? l : 0, blk > 1 ? blk : 0) > 0)
+        ST(ensure_block_buffers(ctx, std::max(l <= BC ? l : 0, blk > 1 ? blk : 0)));
     pt.mark("buffers");
     ctx->log.clear();
     ctx->log_ph = ph;
@@ -1704,6 +1951,18 @@ static trplk_status solve_impl(trplk_ctx* ctx, int p, int q, int l, double tol, 
         ST(run_sdots(ctx, a, 0));
         if (ctx->hasB) ctx->b_mv++;
         ctx->prec++;
+        // block (B1): seeds of targets 2 .. b_e from A X as well (no matvec)
+        const int be0 = std::min(blk, std::min(ph, m));
+        for (int i = 1; i < be0; ++i) {
+            SdotsArgs e2 = a;
+            e2.x = ctx->U[cur] + ld * i;
+            e2.wext = ctx->U[1 - cur] + ld * i;
+            e2.uout = ctx->sblk + ld * i;
+            e2.nslot1 = N_AUX;
+            e2.theta_idx = i;
+            ST(run_sdots(ctx, e2, 0));
+            ctx->prec++;
+        }
         ST(ctl_pull(ctx));
         ctx->b_mv += ctx->hasB ? H.pass3_count - p3_start : 0;
         pt.mark("start block");
@@ -1733,7 +1992,13 @@ static trplk_status solve_impl(trplk_ctx* ctx, int p, int q, int l, double tol, 
                 }
                 CK(cudaEventRecord(ctx->ctev[0], ctx->stream));
             }
-            ST(run_cycle(ctx, S, cur, nprev, t, xprev, opt.use_graphs != 0));
+            const int be = blk > 1 ? std::min(blk, std::min(ph - t + 1, m)) : 1;
+            const int extras = (be > 1 && cyc > 0) ? 1 : 0;  // cycle 1's came from A X at start-up
+            ST(run_cycle(ctx, S, cur, nprev, t, xprev, opt.use_graphs != 0, be, extras));
+            if (extras) {
+                ctx->a_mv += be - 1;
+                ctx->prec += be - 1;
+            }
             if (ctrace) CK(cudaEventRecord(ctx->ctev[1], ctx->stream));
             ST(ctl_pull(ctx));
             if (ctrace) {
@@ -2394,6 +2659,58 @@ trplk_status trplk_k_cgs2(trplk_ctx* ctx, const double* U, int64_t ldu, int k, c
     if (passes) *passes = third ? 3 : 2;
     if (h)
         for (int i = 0; i < k; ++i) h[i] = H.h[0][i] + H.h[1][i] + (third ? H.h[2][i] : 0.0);
+    return TRPLK_OK;
+}
+
+trplk_status trplk_k_block(trplk_ctx* ctx, int mode, const double* U, int64_t ldu, int k, const double* Y,
+                           int64_t ldy, int c, const double* Rinv, const double* H, double* Yout, int64_t ldyo,
+                           double* HV, double* G) {
+    ST(kprep(ctx, k));
+    if (c < 1 || c > BC || mode < BM_GRAM || mode > BM_SPMM || ldu < ctx->n_loc || ldy < ctx->n_loc ||
+        (mode == BM_UPD && (!H || !Yout || ldyo < ctx->n_loc))) {
+        ctx->err = "trplk_k_block: bad arguments";
+        return TRPLK_EINVAL;
+    }
+    std::vector<double> hb((size_t)QMAX * BC, 0.0), rb((size_t)BC * BC, 0.0);
+    if (H)
+        for (int j = 0; j < c; ++j)
+            for (int i = 0; i < k; ++i) hb[i + (size_t)QMAX * j] = H[i + (size_t)k * j];
+    if (Rinv)
+        for (int j = 0; j < c; ++j)
+            for (int i = 0; i < c; ++i) rb[i + (size_t)BC * j] = Rinv[i + (size_t)c * j];
+    CK(cudaMemcpyAsync(ctx->blk->Hs, hb.data(), hb.size() * 8, cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(ctx->blk->Rinv, rb.data(), rb.size() * 8, cudaMemcpyHostToDevice, ctx->stream));
+    if (mode == BM_SPMM) {
+        for (int j = 0; j < c; ++j) ST(halo(ctx, Y + ldy * j));
+    }
+    BlkArgs a{};
+    a.nrows = ctx->n_loc;
+    a.U = U;
+    a.ldu = ldu;
+    a.k = k;
+    a.Y = Y;
+    a.ldy = ldy;
+    a.c = c;
+    a.mode = mode;
+    a.A = ctx->A;
+    a.Rinv = Rinv ? ctx->blk->Rinv : nullptr;
+    a.H = ctx->blk->Hs;
+    a.Yout = Yout;
+    a.ldyo = ldyo;
+    a.HV = ctx->blk->HV[0];
+    a.G = ctx->blk->G[0];
+    a.gate = F_CYCLE;
+    ST(run_block(ctx, a, std::max(k, 1), 0.0));
+    std::vector<double> hv((size_t)QMAX * BC), g((size_t)BC * BC);
+    CK(cudaMemcpyAsync(hv.data(), ctx->blk->HV[0], hv.size() * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaMemcpyAsync(g.data(), ctx->blk->G[0], g.size() * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    if (HV)
+        for (int j = 0; j < c; ++j)
+            for (int i = 0; i < k; ++i) HV[i + (size_t)k * j] = hv[i + (size_t)QMAX * j];
+    if (G && mode != BM_SPMM)
+        for (int j = 0; j < c; ++j)
+            for (int i = 0; i < c; ++i) G[i + (size_t)c * j] = g[i + (size_t)BC * j];
     return TRPLK_OK;
 }
 

@@ -280,7 +280,7 @@ __global__ void __launch_bounds__(CTA, 3) k_spmv_nd(const SdotsArgs a) {
     double theta = 0.0;
     if (a.out_mode >= 3)
         theta = a.theta_idx >= 0 ? ctl->theta[a.theta_idx]
-                                 : (a.theta_idx == -1 ? ctl->theta[ctl->t - 1] : a.theta_val);
+                                 : (a.theta_idx == -1 ? ctl->theta[ctl->t - 1 + (a.x_dyn == 1 ? a.x_off : 0)] : a.theta_val);
     const double rho = ctl->rho;
     const int nn = (a.norm1 ? 1 : 0) + (a.norm2 ? 1 : 0);
     const double* __restrict__ X = resolve_x(a.x, a.x_dyn, a.x_ld, a.x_off, ctl);
@@ -373,7 +373,7 @@ __global__ void __launch_bounds__(CTA, 2) k_sdots_mma(const SdotsArgs a) {
     double theta = 0.0;
     if (a.out_mode >= 3)
         theta = a.theta_idx >= 0 ? ctl->theta[a.theta_idx]
-                                 : (a.theta_idx == -1 ? ctl->theta[ctl->t - 1] : a.theta_val);
+                                 : (a.theta_idx == -1 ? ctl->theta[ctl->t - 1 + (a.x_dyn == 1 ? a.x_off : 0)] : a.theta_val);
     const int nn = (a.norm1 ? 1 : 0) + (a.norm2 ? 1 : 0);
     const int nv = k1 + k2 + nn;
     const int kmx = k1 > k2 ? k1 : k2;
@@ -906,6 +906,7 @@ __global__ void k_gather(const double* x, const int* idx, int64_t n, double* out
 #include "stream_rs.cuh"  // register-stream + DMMA K1 (shares the device helpers above)
 #include "stream_tp.cuh"   // thread-per-row K1 / K2
 #include "rotate.cuh"      // shared-memory-staged DMMA rotation (default)
+#include "block.cuh"       // multi-vector Gram / update / SpMM (block +K)
 #include "k1_pipe.cuh"     // software-pipelined K1 (DIA, B = I, k <= 24)
 #include "small.cuh"       // single-CTA inner loop for small n (latency path)
 #include "inner_grid.cuh"  // cooperative grid-wide inner loop for mid-size n (latency path)
@@ -916,12 +917,13 @@ namespace trplk {
 // ---------------------------------------------------------------- launchers
 // K1 variant: default = the pipelined kernel (k1_pipe.cuh) for k <= 16 on slabs of >= 2^24 rows
 // (the C5 steps), else the two-tile register-stream kernel (stream_rs.cuh).  TRPLK_K1=pipe /
-// TRPLK_K1=rs force one of them wherever it applies (parity tests of both on every shape).
+// TRPLK_K1=rs force one of them wherever it applies (parity tests of both on every shape);
+// TRPLK_K1=tpdots keeps the first-pass CGS dots on the thread-per-row kernel.
 static int k1var() {
     static int v = -1;
     if (v < 0) {
         const char* e = getenv("TRPLK_K1");
-        v = (e && !strcmp(e, "pipe")) ? 2 : (e && !strcmp(e, "rs")) ? 1 : 0;
+        v = (e && !strcmp(e, "pipe")) ? 2 : (e && !strcmp(e, "rs")) ? 1 : (e && !strcmp(e, "tpdots")) ? 3 : 0;
     }
     return v;
 }
@@ -1000,7 +1002,18 @@ void launch_sdots(const SdotsArgs& a, int kmax, cudaStream_t s) {
             return;
         if (launch_step1_rs(a, kmax, s)) return;
     }
-    // every other dot launch (CGS first pass, +K T columns, start-block Gram): thread-per-row
+    // first-pass CGS dots U^T x, x^T x (seed, +K; B = I): the register-stream DMMA kernel with A
+    // absent (measured at C5, k = 24: the thread-per-row kernel streamed at 0.66 of DRAM peak with
+    // 192 registers and one CTA per SM)
+    const bool xdots = a.A.nrows == 0 && a.B.nrows == 0 && a.set1 == 3 && a.set2 == 0 && a.out_mode == 0 &&
+                       (a.norm1 == 0 || a.norm1 == 3) && a.norm2 == 0 && a.uout == nullptr && a.out == nullptr;
+    if (kmax > 0 && xdots && k1var() != 3) {
+        SdotsArgs b = a;
+        b.set1 = 1;                          // z = x when A is absent
+        b.norm1 = a.norm1 == 3 ? 2 : 0;      // x.z = x.x
+        if (launch_step1_rs(b, kmax, s)) return;
+    }
+    // every other dot launch (+K T columns with B != I, start-block Gram, ...): thread-per-row
     if (kmax > 0 && a.out_mode != 4 && launch_step1_tp(a, kmax, s)) return;
     if (kmax > 0 && a.out_mode != 4) {  // dots beyond the bucketed widths: DMMA accumulator kernel
         switch ((kmax + 7) / 8) {

@@ -3,7 +3,8 @@
 //
 //   k_step1_rs2  z = A g, w = M (z - rho B g), T(1:k,k) = U^T z, h1 = U^T w, ||w||^2
 //                (eq 3.1; the preconditioned next vector of P:143 as reading R1;
-//                the first CGS2 pass coefficients of reading R3)
+//                the first CGS2 pass coefficients of reading R3); with A absent the first-pass
+//                dots U^T x, x^T x of every other CGS2 (seed, +K: reading R3)
 //
 // A warp owns two 32-row tiles per iteration (lane = row): it issues the loads of both tiles'
 // basis rows, DIA values and gathers together, parks the rows in a private shared-memory slab
@@ -56,7 +57,7 @@ __global__ void __launch_bounds__(CTA, 2) k_step1_rs2(const SdotsArgs a) {
     const double rho = ctl->rho;
     const int nn = (a.norm1 ? 1 : 0) + (a.norm2 ? 1 : 0);
     const int nv = k1 + k2 + nn;
-    const double* __restrict__ X = a.x;
+    const double* __restrict__ X = resolve_x(a.x, a.x_dyn, a.x_ld, a.x_off, ctl);
     constexpr int CH = 8;
     extern __shared__ __align__(128) double wsm[];  // WARPS x 2 x CH x WLD
     __shared__ double acc[WARPS][NV_MAX];
@@ -78,7 +79,7 @@ __global__ void __launch_bounds__(CTA, 2) k_step1_rs2(const SdotsArgs a) {
         o = 0.0;
         const double xr = ok ? X[row] : 0.0;
         if (live) {
-            z = mat_row(a.A, sl, lane, X, ad);
+            z = a.A.nrows ? mat_row(a.A, sl, lane, X, ad) : xr;  // A absent: dots of x itself
             if (a.out_mode == 2) {
                 if (a.B.nrows) sv = mat_row(a.B, sl, lane, X, bd);
                 else sv = xr;

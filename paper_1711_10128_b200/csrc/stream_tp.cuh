@@ -42,7 +42,7 @@ __global__ void __launch_bounds__(CTA, 1) k_step1_tp(const SdotsArgs a) {
     double theta = 0.0;
     if (a.out_mode >= 3)
         theta = a.theta_idx >= 0 ? ctl->theta[a.theta_idx]
-                                 : (a.theta_idx == -1 ? ctl->theta[ctl->t - 1] : a.theta_val);
+                                 : (a.theta_idx == -1 ? ctl->theta[ctl->t - 1 + (a.x_dyn == 1 ? a.x_off : 0)] : a.theta_val);
     const int nn = (a.norm1 ? 1 : 0) + (a.norm2 ? 1 : 0);
     const int nv = k1 + k2 + nn;
     const double* __restrict__ X = resolve_x(a.x, a.x_dyn, a.x_ld, a.x_off, ctl);

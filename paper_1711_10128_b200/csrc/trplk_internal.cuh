@@ -42,6 +42,7 @@ enum : unsigned {
     F_CYCLE = 1u,      // seed of this cycle valid
     F_INNER = 2u,      // inner Lanczos loop still running (no breakdown, R16)
     F_KCOL0 = 4u,      // +K column j valid: F_KCOL0 << j
+    F_BPASS3 = 1u << 30,  // block +K: third BCGS pass needed (R3); F_KCOL0 << j uses bits 2..17
 };
 
 // Norm slots of Ctl::nrm
@@ -139,6 +140,61 @@ struct UpdArgs {
     int force3; // debug: take the third CGS pass unconditionally (tests of the pass-3 path)
 };
 
+// ------------------------------------------------------------- block kernels (block.cuh)
+constexpr int BC = 8;                                // vectors per block launch (DMMA n = 8)
+constexpr int BLK_NV = 2 * QMAX * BC + BC * BC;      // reduction values of one block launch
+enum { BM_GRAM = 0, BM_UPD = 1, BM_SPMM = 2, BM_SPMW = 3 };
+
+// Device state of one block CGS2 (+K augmentation): pass results and the small c x c factors.
+struct BlkCtl {
+    double HV[4][QMAX * BC];  // U^T V of the GRAM / UPD passes (ld QMAX)
+    double G[4][BC * BC];     // V^T V of the passes (ld BC)
+    double Hs[QMAX * BC];     // coefficients of the next UPD: (U^T W) Rinv
+    double Rinv[BC * BC];     // upper triangle applied before the next update / the placement
+    double lprod[BC];         // product of the Cholesky pivots so far (norm left of input vector j)
+    double g0[BC];            // input squared norms (breakdown test, R3/R16)
+    int c;                    // vectors in the block
+    int acc;                  // accepted (not dependent) vectors
+    int drop[BC];             // 1: vector j dependent (dropped, R16)
+    int pos[BC];              // compacted position of accepted vector j
+    int k0;                   // basis width before the block was appended
+    int pass3;                // third pass pending (R3)
+    int cin;                  // vectors entering the next block CGS2 (block inner loop: fit the basis)
+};
+
+struct BlkArgs {
+    int64_t nrows;
+    const double* U;
+    int64_t ldu;
+    int k;            // basis columns (k_from_ctl: ctl->k + k_off)
+    int k_from_ctl, k_off;
+    const double* Y;  // input vectors (ld ldy; SPMM: with ghost tails)
+    int64_t ldy;
+    int y_dyn;        // 2: Y + ldy * ctl->xprev_col (the X^prev columns of the previous block)
+    int c;            // vectors (<= BC), or *c_dyn
+    const int* c_dyn;
+    const int* c_cap;    // non-null: c = min(c, *c_cap) (room left in the basis)
+    const double* Rinv;  // UPD: optional c x c upper triangle (ld BC): Q = Y Rinv
+    const double* H;     // UPD: k x c (ld QMAX): Y' = Q - U H
+    double* Yout;        // UPD: Y' (may alias Y)
+    int64_t ldyo;
+    Sell A;              // SPMM / SPMW: Z = A Y
+    double sigma, mfloor;  // SPMW: W = M (Z - rho Y) (rho = ctl->rho, Jacobi M of A - sigma I) -> Yout
+    int mode;            // BM_GRAM / BM_UPD / BM_SPMM / BM_SPMW
+    double* HV;          // result U^T V (ld QMAX); SPMW: U^T W
+    double* G;           // result V^T V (ld BC)
+    double* T;           // SPMM: T(i, k0 + j) = (U^T Z)(i, j), mirrored; k0 = *k0p
+    int ldT;
+    const int* k0p;
+    unsigned gate;
+    Ctl* ctl;
+    double* part;
+    double* gpart;
+    unsigned* counter;
+    int maxcta;
+    double* red_local;
+};
+
 // Single-CTA inner loop of the small-n latency path (small.cuh)
 constexpr int SMALL_NMAX = 8192;  // rows handled by the small path (32 per thread)
 
@@ -226,6 +282,17 @@ extern thread_local const void* g_last_kern;
 #define NOTE_KERN(k) (::trplk::g_last_kern = reinterpret_cast<const void*>(k))
 
 bool launch_inner_small(const SmallArgs& a, int kmax, cudaStream_t s);
+bool launch_block(const BlkArgs& a, int kmax, cudaStream_t s);
+void launch_blk_finalize_multi(const BlkArgs& a, const double* red_all, int nranks, int stride, cudaStream_t s);
+// BCGS2 control of a +K block (one small kernel per stage): stage 0 after the GRAM pass, 1 after
+// the first UPD (Cholesky-QR, drops), 2 after the second UPD (Cholesky-QR, third-pass test),
+// 3 after the gated third UPD; stage 2/3 also place the accepted vectors (ctl->k += acc).
+void launch_blk_ctl(BlkCtl* b, Ctl* ctl, int stage, int c, const int* c_dyn, int seed, unsigned gate,
+                    cudaStream_t s);
+void launch_blk_room(BlkCtl* b, const Ctl* ctl, int kcap, unsigned gate, cudaStream_t s);
+// Q(:, pos_j) = (W Rinv)(:, j) for accepted j into U(:, k0 + pos_j) and xk(:, pos_j); c = 0: b->c
+void launch_blk_place(const double* W, int64_t ldw, const BlkCtl* b, const Ctl* ctl, double* U, int64_t ldu,
+                      double* xk, int64_t ldx, int64_t nrows, int c, unsigned gate, cudaStream_t s);
 // false: not applicable (kmax > 32 or no co-resident grid); nothing launched
 bool launch_inner_grid(const GridArgs& a, int kmax, cudaStream_t s);
 void launch_sdots(const SdotsArgs& a, int kmax, cudaStream_t s);

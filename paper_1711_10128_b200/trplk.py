@@ -56,7 +56,7 @@ class HostCommS(ctypes.Structure):
 class Options(ctypes.Structure):
     _fields_ = [("seed", ctypes.c_uint64), ("max_cycles", _I), ("tol_mode", _I),
                 ("restart_size", _I), ("lock_mode", _I), ("debug_checks", _I), ("use_graphs", _I),
-                ("precond", _I)]
+                ("precond", _I), ("block", _I)]
 
 
 class Stats(ctypes.Structure):
@@ -104,6 +104,7 @@ _sig("trplk_profile", _I, [_P, _I])
 _sig("trplk_profile_read", _I, [_P, _P, _P, ctypes.POINTER(_I64)])
 _sig("trplk_profile_kernels", _I, [_P, ctypes.c_char_p, ctypes.c_size_t])
 _sig("trplk_profile_phases", _I, [_P, _P, ctypes.POINTER(_I64)])
+_sig("trplk_k_block", _I, [_P, _I, _P, _I64, _I, _P, _I64, _I, _P, _P, _P, _I64, _P, _P])
 _sig("trplk_pl1_solve", _I, [_P, _I, _D, _I, _I, _I, ctypes.c_uint64, _P, _P, _P, _P, _I, _P, _P, _P, _P,
                              ctypes.POINTER(Stats)])
 
@@ -113,7 +114,7 @@ EXPORTED = ["trplk_options_default", "trplk_nccl_unique_id", "trplk_create", "tr
             "trplk_k_residual", "trplk_k_random", "trplk_profile", "trplk_profile_read",
             "trplk_plan_ghosts", "trplk_k_sym_eig_time", "trplk_loopback_create", "trplk_loopback_destroy",
             "trplk_set_debug", "trplk_pl1_solve", "trplk_profile_kernels", "trplk_create_ex",
-            "trplk_profile_phases"]
+            "trplk_profile_phases", "trplk_k_block"]
 
 
 class TrplkError(RuntimeError):
@@ -566,3 +567,15 @@ def trplk_profile_phases(ctx: Context) -> dict:
     cnt = _I64()
     ctx.check(_lib.trplk_profile_phases(ctx.handle, _ptr(ms), ctypes.byref(cnt)))
     return {"phases": PHASES, "ms": ms, "count": cnt.value}
+
+
+def trplk_k_block(ctx, mode, U, ldu, k, Y, ldy, c, Rinv=None, H=None, Yout=None, ldyo=0):
+    """Block kernel (mode 0 GRAM, 1 UPD, 2 SPMM) on device blocks U (k columns) and Y (c columns);
+    returns (HV k x c, G c x c) as numpy arrays."""
+    HV = np.zeros((k, c), order="F")
+    G = np.zeros((c, c), order="F")
+    R = None if Rinv is None else np.asfortranarray(Rinv, np.float64)
+    Hh = None if H is None else np.asfortranarray(H, np.float64)
+    ctx.check(_lib.trplk_k_block(ctx.handle, int(mode), _ptr(U), ldu, k, _ptr(Y), ldy, c, _ptr(R), _ptr(Hh),
+                                 _ptr(Yout), ldyo, _ptr(HV), _ptr(G)))
+    return HV, G

@@ -290,3 +290,48 @@ def test_step1_pipe_full_slab(orc, gen, k):
     assert np.all(np.abs(h1 - h_o) <= 1e-12 * un * nw)
     assert abs(wn - orc.dot(w_o, w_o)) <= 1e-12 * nw * nw
     ctx.close()
+
+
+@pytest.mark.parametrize("case", ["C2-19", "C2-40", "C1-None"])
+@pytest.mark.parametrize("k,c", [(1, 1), (7, 2), (22, 2), (45, 3), (64, 8), (30, 5)])
+def test_block_kernels_gram_upd_spmm(orc, problems, case, k, c):
+    """The block +K kernels (block.cuh) against the oracle's primitives: GRAM U^T Y and Y^T Y,
+    UPD Y' = Y R^-1 - U H with its U^T Y', Y'^T Y', SPMM U^T (A Y) -- dots within
+    1e-12 ||u|| ||v||, vectors normwise 1e-12; ragged row tails and every DMMA chunk width."""
+    torch, trplk = need_gpu()
+    P = problems[case]
+    n = P.A.n
+    if k + c > n:
+        pytest.skip("block wider than the problem")
+    ctx = _ctx(trplk, P)
+    rng = np.random.default_rng(1000 + 10 * k + c)
+    U = rng.standard_normal((n, k)) / np.sqrt(n)
+    Y = rng.standard_normal((n, c))
+    Ud, Yd = to_dev(torch, U, ctx.ld), to_dev(torch, Y, ctx.ld)
+    un, yn = np.linalg.norm(U, axis=0), np.linalg.norm(Y, axis=0)
+    # GRAM
+    HV, G = trplk.trplk_k_block(ctx, 0, Ud, ctx.ld, k, Yd, ctx.ld, c)
+    HVo = np.array([[orc.dot(U[:, i], Y[:, j]) for j in range(c)] for i in range(k)])
+    Go = np.array([[orc.dot(Y[:, i], Y[:, j]) for j in range(c)] for i in range(c)])
+    assert np.all(np.abs(HV - HVo) <= 1e-12 * np.outer(un, yn))
+    assert np.all(np.abs(G - Go) <= 1e-12 * np.outer(yn, yn))
+    # UPD with an upper-triangular R^-1 and coefficients H
+    R = np.triu(rng.standard_normal((c, c))) + 3 * np.eye(c)
+    H = rng.standard_normal((k, c))
+    Yo = torch.zeros((c, ctx.ld), dtype=torch.float64, device="cuda")
+    HV, G = trplk.trplk_k_block(ctx, 1, Ud, ctx.ld, k, Yd, ctx.ld, c, Rinv=R, H=H, Yout=Yo, ldyo=ctx.ld)
+    Q = Y @ R  # Q = Y Rinv with Rinv := R here
+    Yp = Q - U @ H
+    Ypg = Yo.cpu().numpy()[:, :n].T
+    assert normwise(Ypg, Yp) <= 1e-12
+    ypn = np.linalg.norm(Yp, axis=0)
+    HVo = np.array([[orc.dot(U[:, i], Yp[:, j]) for j in range(c)] for i in range(k)])
+    Go = np.array([[orc.dot(Yp[:, i], Yp[:, j]) for j in range(c)] for i in range(c)])
+    assert np.all(np.abs(HV - HVo) <= 1e-11 * np.outer(un, ypn))
+    assert np.all(np.abs(G - Go) <= 1e-11 * np.outer(ypn, ypn))
+    # SPMM
+    HV, _ = trplk.trplk_k_block(ctx, 2, Ud, ctx.ld, k, Yd, ctx.ld, c)
+    Z = np.stack([orc.spmv(P.A, Y[:, j]) for j in range(c)], axis=1)
+    HVo = np.array([[orc.dot(U[:, i], Z[:, j]) for j in range(c)] for i in range(k)])
+    assert np.all(np.abs(HV - HVo) <= 1e-12 * np.outer(un, np.linalg.norm(Z, axis=0)))
+    ctx.close()

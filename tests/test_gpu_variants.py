@@ -11,6 +11,8 @@ set (the switches are read once per process):
   TRPLK_NO_SMALL=1  the multi-kernel inner step also for n <= 8192 (C1)
   TRPLK_GRID=1      the cooperative grid-wide inner loop (inner_grid.cuh)
   TRPLK_EIG=tri     the tridiagonal RR eigensolver (eig_tri.cu) instead of one-CTA Jacobi
+  TRPLK_K1=tpdots   the thread-per-row kernel for the first-pass CGS dots of the seed / +K vectors
+  TRPLK_KPLUS=col   the +K columns one at a time (CGS2 + SpMV each) instead of the block kernels
 """
 import os
 import subprocess
@@ -23,15 +25,15 @@ from gpu_util import need_gpu
 pytestmark = pytest.mark.gpu
 HERE = os.path.dirname(os.path.abspath(__file__))
 
-VARIANTS = [("TRPLK_K1", "pipe"), ("TRPLK_K1", "rs"), ("TRPLK_NO_COOP3", "1"), ("TRPLK_NO_SMALL", "1"),
-            ("TRPLK_GRID", "1"), ("TRPLK_EIG", "tri")]
+VARIANTS = [("TRPLK_K1", "pipe"), ("TRPLK_K1", "rs"), ("TRPLK_K1", "tpdots"), ("TRPLK_NO_COOP3", "1"),
+            ("TRPLK_NO_SMALL", "1"), ("TRPLK_GRID", "1"), ("TRPLK_EIG", "tri"), ("TRPLK_KPLUS", "col")]
 
 
 @pytest.mark.parametrize("var,val", VARIANTS)
 def test_variant_parity_suite(var, val):
     need_gpu()
     env = dict(os.environ, **{var: val})
-    sel = "not full_slab and not widest"  # the 2^24-row and q > 48 cases are default-path checks
+    sel = "not full_slab and not widest and not block_kernels"  # the 2^24-row and q > 48 cases are default-path checks
     cmd = [sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider", "-m", "gpu", "-k", sel,
            os.path.join(HERE, "test_gpu_kernels.py"), os.path.join(HERE, "test_gpu_solve.py")]
     r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=1200)

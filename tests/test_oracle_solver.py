@@ -317,3 +317,52 @@ def test_trlan_baseline_m_identity(orc, gen):
                 v = C @ cols[-1][:, 0]
             th = _rr_dense(A, B, np.hstack(cols), p)
             assert np.max(np.abs(th - r["log"]["thetas"][c][:p]) / np.abs(th)) <= 1e-10, (name, c)
+
+
+@pytest.mark.parametrize("b", [2, 3])
+def test_block_trplk_subspace_multishift(orc, gen, b):
+    """NEXT-3, block TRPL+K (reading B1): per cycle the RR space is
+    span{X, u_0, C u_0, .., u_1, C u_1, ..} -- the block Krylov space of eq 3.2's C =
+    (I - X X^T B) M (A - theta_t B) from the seeds u_i = (I - X X^T B) M r_{t+i}, i < b_e =
+    min(b, p^ - t + 1) (r_{t+i} with its own Ritz value); the m inner columns are produced
+    round-robin (seed i's powers: ceil((m - i) / b_e) columns).  Rebuilt densely from explicit
+    powers per cycle (Ritz values = Rayleigh quotients of the dumped X), compared with the oracle's
+    Ritz values; also the matvec accounting m + b_e per cycle (+1 per lock) and that b = 1 is
+    Algorithm 1 bit for bit."""
+    for name in ("C2", "C4"):
+        P = gen.make(name, N=5)
+        A, B = _dense_pencil(P)
+        Bm = np.eye(A.shape[0]) if B is None else B
+        Md = 1.0 / np.abs(np.diag(A))
+        p, m = 3, 6
+        r = orc.solve(P.A, P.B, p, p + m, 0, 1e-13, dump_cycles=5, max_cycles=5, block=b)
+        d = r["dump"]
+        for c in range(len(d["rho"])):
+            X, t = d["X"][c], d["t"][c]
+            be = min(b, p - t + 1, m)
+            Pj = np.eye(len(Md)) - X @ X.T @ Bm
+            cols = [X]
+            xt = X[:, t - 1]
+            C = Pj @ (Md[:, None] * (A - (xt @ A @ xt) / (xt @ Bm @ xt) * Bm))
+            for i in range(be):
+                x = X[:, t - 1 + i]
+                th = (x @ A @ x) / (x @ Bm @ x)
+                Ci = C
+                v = Pj @ (Md * (A @ x - th * (Bm @ x)))
+                for _ in range(-(-(m - i) // be)):
+                    cols.append((v / np.linalg.norm(v))[:, None])
+                    v = Ci @ cols[-1][:, 0]
+            thr = _rr_dense(A, B, np.hstack(cols), p)
+            assert np.max(np.abs(thr - r["log"]["thetas"][c][:p]) / np.abs(thr)) <= 1e-10, (name, b, c)
+        lg = r["log"]
+        mv = np.diff(np.r_[p, lg["mv"]])
+        for c in range(len(mv) - 1):
+            # the b_e - 1 extra seed residuals of cycle c were computed at the end of cycle c - 1
+            # (cycle 0's from the start-up's A X: no matvec); +1 per lock after the RR
+            be = min(b, p - lg["t"][c] + 1, m) if c > 0 else 1
+            locks = lg["t"][c + 1] - lg["t"][c]
+            assert mv[c] == m + 1 + (be - 1) + locks, (name, b, c)
+    P = gen.make("C2", N=8)
+    r0 = orc.solve(P.A, None, P.p, P.q, P.l, P.tol, block=0)
+    r1 = orc.solve(P.A, None, P.p, P.q, P.l, P.tol, block=1)
+    assert np.array_equal(r0["eigenvalues"], r1["eigenvalues"]) and r0["a_matvecs"] == r1["a_matvecs"]
