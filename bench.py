@@ -60,6 +60,8 @@ def parse():
     ap.add_argument("--precond", default="jacobi", choices=["jacobi", "none"],
                     help="none: M = I (with --k-plus 0: the thick-restart Lanczos baseline, eq 2.1)")
     ap.add_argument("--k-plus", type=int, default=None, help="override the config's k_plus (l)")
+    ap.add_argument("--block", type=int, default=1,
+                    help="block TRPL+K (options.block, NEXT-3): b vectors per SpMM in the inner loop")
     ap.add_argument("--profile-last-only", action="store_true",
                     help="kernel-profile events on the last timed step only (default: every timed step)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -132,10 +134,10 @@ def plane_of(P):
 FULL_SOLVE_CFGS = ("C1", "C2")  # oracle full solve in seconds; C3/C4 take 20-30 min, C5 hours
 
 
-def static_config(name, P, n, world, precond="Jacobi", comm="nccl"):
+def static_config(name, P, n, world, precond="Jacobi", comm="nccl", block=1):
     """The `config` object of both arms (identical keys and values)."""
     return {"workload": f"{name}: {P.desc}; p={P.p}, max_basis={P.q}, k_plus={P.l}, tol={P.tol}, "
-                        f"{precond} preconditioner, seed 12",
+                        f"{precond} preconditioner, seed 12" + (f", block TRPL+K b={block}" if block > 1 else ""),
             "n": n, "step": "one full trplk_solve (time to p eigenpairs)",
             "l2": "inputs larger than L2 at C3-C5; a 256 MiB buffer is written between timed steps",
             "parallelism": f"z-slab row partition x{world}" + (" (host-staged gloo exchanges)" if comm == "host" else "")}
@@ -371,7 +373,7 @@ def main():
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
 
     def solve(**kw):
-        return trplk.trplk_solve(ctx, P.p, P.q, P.l, P.tol, evecs_out=evecs, precond=prec, **kw)
+        return trplk.trplk_solve(ctx, P.p, P.q, P.l, P.tol, evecs_out=evecs, precond=prec, block=args.block, **kw)
 
     for w in range(args.warmup):
         # the last warm-up solve runs with the profile on too, so the timed region finds the
@@ -473,7 +475,8 @@ def main():
             e0.record(stream)
             c2 = trplk.trplk_create(HA, HB, P.sigma, n_global=n, row_begin=rb, row_end=re, group=group,
                                     comm=args.comm)
-            ev2, _, rs2, st2 = trplk.trplk_solve(c2, P.p, P.q, P.l, P.tol, evecs_out=host_evecs, precond=prec)
+            ev2, _, rs2, st2 = trplk.trplk_solve(c2, P.p, P.q, P.l, P.tol, evecs_out=host_evecs, precond=prec,
+                                                 block=args.block)
             c2.close()
             e1.record(stream)
             torch.cuda.synchronize()
@@ -497,7 +500,8 @@ def main():
                "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
                "scaling": "strong", "vs_baseline": None, "dtype": "f64",
                "data": "synthetic (seeded generator, BASELINE configs; paper matrices unavailable)",
-               "config": static_config(args.config, P, n, world, "no (M = I)" if prec else "Jacobi", args.comm),
+               "config": static_config(args.config, P, n, world, "no (M = I)" if prec else "Jacobi", args.comm,
+                                       args.block),
                "solve": {"a_matvecs_per_solve": mv, "cycles": stats[-1]["cycles"],
                          "time_to_p_eigenpairs_ms": round(ms_per_step, 4),
                          "status": stats[-1]["status"]},

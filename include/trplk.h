@@ -81,7 +81,10 @@ typedef struct {
     int use_graphs;     /* 1 (default): one CUDA graph per cycle; 0: eager launches */
     int precond;        /* 0 (default): Jacobi M on A - sigma B (R12); 1: none, M = I -- with
                            k_plus = 0 the thick-restart Lanczos baseline (eq 2.1, PAPER.md:77-80,
-                           "cannot use preconditioning directly"), with m = 1, p = k_plus = 1 LOPCG */
+                           "cannot use preconditioning directly"), with m = 1, p = k_plus = 1 LOPCG;
+                           2: Jacobi of A - rho_i B with the cycle's shift rho_i ("M may change at
+                           every cycle with the goal to approximate (A - rho_i I)^-1", PAPER.md:171;
+                           NEXT-2, reading P2c); not with block > 1 */
     int block;          /* b = 1 (default): Algorithm 1.  2..8: block TRPL+K ("A block
                            TRPL+K is also possible"; reading B1 of DESIGN.md): the inner space is the
                            block Krylov space of eq 3.2's C from the seeds M r_t .. M r_{t+b_e-1}

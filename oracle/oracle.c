@@ -332,7 +332,8 @@ int orc_trplk_solve(const orc_problem* P, double* evals, double* evecs, double* 
     const int ph = P->restart_size > 0 ? P->restart_size : p; /* R5: p^ = p by default */
     if (rep) { rep->status = 1; rep->cycles = 0; rep->log_len = 0; }
     if (n < 1 || p < 1 || l < 0 || ph < p || q - ph - l < 1 || !(P->tol > 0.0) || ph + 1 > n ||
-        P->max_cycles < 1 || P->block > 8 || q > 64)
+        P->max_cycles < 1 || P->block > 8 || q > 64 || P->precond < 0 || P->precond > 2 ||
+        (P->precond == 2 && P->block > 1))
         return 1; /* EINVAL */
     const int m = q - ph - l; /* inner steps per cycle (R5) */
 
@@ -392,6 +393,8 @@ int orc_trplk_solve(const orc_problem* P, double* evals, double* evecs, double* 
     for (int i = 0; i < ph; ++i) T[i + (size_t)q * i] = th[i];
     int t = 1; /* target, 1-based */
     double rho = th[0];
+    if (P->precond == 2) /* M ~ (A - rho_i B)^-1 re-formed for every cycle's shift */
+        orc_jacobi_diag(n, P->a_rowptr, P->a_col, P->a_val, P->b_rowptr, P->b_col, P->b_val, rho, 1e-8, M);
     applyB(&c, U, s);
     for (int64_t i = 0; i < n; ++i) r[i] = W[i] - rho * s[i];
     for (int64_t i = 0; i < n; ++i) u[i] = M[i] * r[i];
@@ -557,6 +560,8 @@ int orc_trplk_solve(const orc_problem* P, double* evals, double* evecs, double* 
             all_conv = 0;
         }
         rho = th[t - 1];
+        if (P->precond == 2)
+            orc_jacobi_diag(n, P->a_rowptr, P->a_col, P->a_val, P->b_rowptr, P->b_col, P->b_val, rho, 1e-8, M);
         for (int64_t i = 0; i < n; ++i) u[i] = M[i] * r[i];
         c.prec++;
         if (b > 1) { /* residuals of the next targets: one A-matvec each (B1) */

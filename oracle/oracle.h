@@ -60,7 +60,8 @@ typedef struct {
     int lock_mode;          /* 0 IF (Alg. 1 step 12, R7), 1 WHILE */
     int debug;              /* 1: log ||T - U^T A U||_max and ||U^T B U - I||_max per cycle */
     int precond;            /* 0 Jacobi (R12); 1 none, M = I: with l = 0 thick-restart Lanczos (eq 2.1,
-                               PAPER.md:77-80), with m = p = l = 1 LOPCG (eq 2.2 with p = 1) */
+                               PAPER.md:77-80), with m = p = l = 1 LOPCG (eq 2.2 with p = 1);
+                               2 Jacobi of A - rho_i B re-formed every cycle (reading P2c) */
     int block;              /* b <= 8: block TRPL+K ("A block TRPL+K is also possible", reading
                                B1): the inner space is the block Krylov space of eq 3.2's operator C
                                (one shift rho = theta_t) from the b_e = min(b, p^-t+1, m) seeds

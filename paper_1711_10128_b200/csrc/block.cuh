@@ -68,8 +68,15 @@ __device__ void blk_finalize(const BlkArgs& a, const double* r, int k, int c) {
         for (int v = threadIdx.x; v < c * c; v += blockDim.x) a.G[(v % c) + BC * (v / c)] = r[nkc + v];
 }
 
-template <int KMAX, int MODE>
-__global__ void __launch_bounds__(CTA, 1) k_blk(const BlkArgs a) {
+// fp64 DMMA without `volatile`: the compiler may interleave independent accumulator chains
+__device__ __forceinline__ void dmma884_nv(double (&d)[2], double a, double b) {
+    asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+        : "+d"(d[0]), "+d"(d[1])
+        : "d"(a), "d"(b));
+}
+
+template <int KMAX, int MODE, int LB>
+__global__ void __launch_bounds__(CTA, LB) k_blk(const BlkArgs a) {
     Ctl* ctl = a.ctl;
     if ((ctl->flags & a.gate) != a.gate) return;
     const int k = a.k_from_ctl ? ctl->k + a.k_off : a.k;
@@ -107,7 +114,7 @@ __global__ void __launch_bounds__(CTA, 1) k_blk(const BlkArgs a) {
     // KMAX <= 32: the next tile's basis rows are loaded while this tile is contracted (one tile of
     // loads always in flight per warp; measured necessary: without it a warp's loads and its DMMA /
     // shared-memory phase alternate and the kernel streamed at ~1/3 of the DRAM peak at C5)
-    constexpr bool PF = KMAX <= 32;
+    constexpr bool PF = KMAX <= 32 && LB == 1;
     double un[PF ? KMAX : 1];
     if (PF) {
         const int64_t t0 = (int64_t)blockIdx.x * WARPS + warp, row0 = t0 * 32 + lane;
@@ -171,11 +178,17 @@ __global__ void __launch_bounds__(CTA, 1) k_blk(const BlkArgs a) {
         }
         __syncwarp();
         if (MODE == BM_UPD) {  // Y' = Q - U H: (H^T U^T) per 8-row block, lane: vector fi, rows 2 fj, 2 fj + 1
+            // the four 8-row blocks' accumulators interleaved: four independent DMMA chains
+            double d4[4][2];
+#pragma unroll
+            for (int rb = 0; rb < 4; ++rb) d4[rb][0] = d4[rb][1] = 0.0;
+#pragma unroll
+            for (int ks = 0; ks < KMAX / 4; ++ks)
+#pragma unroll
+                for (int rb = 0; rb < 4; ++rb) dmma884_nv(d4[rb], hf[ks], Wt[(4 * ks + fj) * WLD + 8 * rb + fi]);
 #pragma unroll
             for (int rb = 0; rb < 4; ++rb) {
-                double d2[2] = {0.0, 0.0};
-#pragma unroll
-                for (int ks = 0; ks < KMAX / 4; ++ks) dmma884_s(d2, hf[ks], Wt[(4 * ks + fj) * WLD + 8 * rb + fi]);
+                const double* d2 = d4[rb];
                 const int rr = 8 * rb + 2 * fj;
                 const double y0 = Vs[fi * WLD + rr] - d2[0], y1 = Vs[fi * WLD + rr + 1] - d2[1];
                 Vs[fi * WLD + rr] = y0;
@@ -188,24 +201,24 @@ __global__ void __launch_bounds__(CTA, 1) k_blk(const BlkArgs a) {
             }
             __syncwarp();
         }
-        // dots: U^T V (basis chunk g, vectors) and V^T V on DMMA over the 32 rows (8 k-steps of 4)
+        // dots: U^T V (basis chunk g, vectors) and V^T V on DMMA over the 32 rows (8 k-steps of 4);
+        // the chunks' accumulators (independent chains) interleaved per k-step
 #pragma unroll
-        for (int g = 0; g < KMAX / 8; ++g) {
-            if (8 * g < k) {
+        for (int q = 0; q < 8; ++q) {
+            const double bv = Vs[fi * WLD + 4 * q + fj];  // B operand (vector fi, row 4q + fj) = A of V^T V
+            const double bw = SPW ? Ws[fi * WLD + 4 * q + fj] : 0.0;
 #pragma unroll
-                for (int q = 0; q < 8; ++q)
-                    dmma884_s(cacc[g], Wt[(8 * g + fi) * WLD + 4 * q + fj], Vs[fi * WLD + 4 * q + fj]);
-                if (SPW) {
-#pragma unroll
-                    for (int q = 0; q < 8; ++q)
-                        dmma884_s(wacc[SPW ? g : 0], Wt[(8 * g + fi) * WLD + 4 * q + fj], Ws[fi * WLD + 4 * q + fj]);
+            for (int g = 0; g < KMAX / 8; ++g) {
+                if (8 * g < k) {
+                    const double au = Wt[(8 * g + fi) * WLD + 4 * q + fj];
+                    dmma884_nv(cacc[g], au, bv);
+                    if (SPW) dmma884_nv(wacc[SPW ? g : 0], au, bw);
                 }
             }
-        }
-        if (MODE != BM_SPMM) {
-            const double* G2 = SPW ? Ws : Vs;
-#pragma unroll
-            for (int q = 0; q < 8; ++q) dmma884_s(gacc, G2[fi * WLD + 4 * q + fj], G2[fi * WLD + 4 * q + fj]);
+            if (MODE != BM_SPMM) {
+                const double b2 = SPW ? bw : bv;
+                dmma884_nv(gacc, b2, b2);
+            }
         }
         __syncwarp();
     }
@@ -243,10 +256,22 @@ __global__ void __launch_bounds__(CTA, 1) k_blk(const BlkArgs a) {
     blk_finalize(a, res, k, c);
 }
 
-template <int KMAX, int MODE>
-static void launch_blk_k(const BlkArgs& a, cudaStream_t s) {
+// k <= 24: two CTAs per SM (<= 128 registers, no register prefetch) -- measured at C5 (k = 24,
+// c = 2, through trplk_k_block): GRAM 5.5 -> 6.2 TB/s, UPD 3.1 -> 4.2, SPMM 3.2 -> 4.4 against
+// one CTA with the next tile's rows prefetched into registers.  TRPLK_BLK_LB=1 selects the latter.
+static int blk_lb() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("TRPLK_BLK_LB");
+        v = (e && e[0] == '1') ? 1 : 2;
+    }
+    return v;
+}
+
+template <int KMAX, int MODE, int LB>
+static void launch_blk_kl(const BlkArgs& a, cudaStream_t s) {
     const int smem = WARPS * (KMAX + (MODE == BM_SPMW ? 2 : 1) * BC) * WLD * (int)sizeof(double);
-    auto kern = k_blk<KMAX, MODE>;
+    auto kern = k_blk<KMAX, MODE, LB>;
     static bool init = false;
     static int grid_cap = 0;
     if (!init) {
@@ -262,6 +287,12 @@ static void launch_blk_k(const BlkArgs& a, cudaStream_t s) {
     if (g < 1) g = 1;
     NOTE_KERN(kern);
     kern<<<(int)g, CTA, smem, s>>>(a);
+}
+
+template <int KMAX, int MODE>
+static void launch_blk_k(const BlkArgs& a, cudaStream_t s) {
+    if (KMAX <= 24 && blk_lb() == 2) launch_blk_kl<KMAX, MODE, 2>(a, s);
+    else launch_blk_kl<KMAX, MODE, 1>(a, s);
 }
 
 template <int MODE>

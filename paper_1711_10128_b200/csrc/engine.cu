@@ -67,6 +67,7 @@ struct trplk_ctx {
     bool hasB = false;
     double sigma = 0.0, mfloor = 0.0, normF = 0.0, amax = 0.0;
     double mfloor_solve = 0.0;  // the value kernels get: mfloor, or -1 for M = I (options.precond = 1)
+    int pmode = 0;              // options.precond of the solve (2: per-cycle shifted Jacobi)
     Sell A, B;
     int64_t sellA_bytes = 0, sellB_bytes = 0, nnzA = 0, nnzB = 0;
     // halo plan (nranks > 1): per peer, recv range in the ghost tail and send rows
@@ -601,6 +602,7 @@ SdotsArgs sd_base(trplk_ctx* ctx) {
     a.tcol_fixed = -1;
     a.sigma = ctx->sigma;
     a.mfloor = ctx->mfloor_solve;
+    a.pmode = ctx->pmode;
     a.ctl = ctx->ctl;
     a.T = ctx->T;
     a.ldT = QMAX;
@@ -1184,6 +1186,7 @@ trplk_status issue_cycle(trplk_ctx* ctx, const Sizes& S, int cur, int nprev, int
         sa.m = S.m;
         sa.sigma = ctx->sigma;
         sa.mfloor = ctx->mfloor_solve;
+        sa.pmode = ctx->pmode;
         sa.gate = F_CYCLE | F_INNER;
         sa.clear = F_INNER;
         sa.force3 = ctx->force3;
@@ -1339,7 +1342,7 @@ static std::string graph_fingerprint(const trplk_ctx* ctx, uint64_t key, const S
         put(&M->dval, sizeof(M->dval));
         put(M->offs, sizeof(M->offs));
     }
-    const double sc[4] = {ctx->sigma, ctx->mfloor, ctx->normF, ctx->mfloor_solve};
+    const double sc[5] = {ctx->sigma, ctx->mfloor, ctx->normF, ctx->mfloor_solve, (double)ctx->pmode};
     put(sc, sizeof(sc));
     const int64_t iv[6] = {ctx->n_loc, ctx->ld, ctx->row_begin, ctx->n_global, (int64_t)ctx->force3,
                            (int64_t)ctx->grid_on};
@@ -1828,11 +1831,12 @@ static trplk_status solve_impl(trplk_ctx* ctx, int p, int q, int l, double tol, 
         ctx->err = "NULL output";
         return TRPLK_EINVAL;
     }
-    if (opt.precond != 0 && opt.precond != 1) {
-        ctx->err = "options.precond must be 0 (Jacobi) or 1 (none)";
+    if (opt.precond < 0 || opt.precond > 2 || (opt.precond == 2 && opt.block > 1)) {
+        ctx->err = "options.precond must be 0 (Jacobi), 1 (none) or 2 (Jacobi of A - rho_i B; block = 1)";
         return TRPLK_EINVAL;
     }
     ctx->mfloor_solve = opt.precond == 1 ? -1.0 : ctx->mfloor;
+    ctx->pmode = opt.precond;
     const int blk = opt.block > 1 ? opt.block : 1;
     if (blk > 1 && (blk > BC || ctx->hasB || ctx->nranks > 1)) {
         ctx->err = "options.block: 1..8, B = I and one rank on the device";
@@ -2037,7 +2041,7 @@ static trplk_status solve_impl(trplk_ctx* ctx, int p, int q, int l, double tol, 
                 }
                 ctx->phase_count++;
             }
-            if (ctx->prof_on) {  // live inner-step profile (events recorded inside the cycle)
+            if (ctx->prof_on && !(blk > 1)) {  // live inner-step profile (events inside the cycle; Alg. 1 path)
                 const int jmid = std::max(1, std::min(m - 1, m / 2));
                 if (m >= 2 && G > jmid) {
                     float e[3];

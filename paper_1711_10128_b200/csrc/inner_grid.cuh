@@ -113,7 +113,7 @@ __device__ __forceinline__ void grid_phase1(const SmallArgs& a, int k, bool cgs,
         double ad = 1.0;
         double z = mat_row<false>(a.A, sl, lane, g, ad);
         const double xr = ok ? __ldcg(g + row) : 0.0;
-        double o = jacobi_minv(ad, 1.0, a.sigma, a.mfloor) * (z - rho * xr);  // w = M (z - rho g), R1
+        double o = jacobi_minv(ad, 1.0, a.pmode == 2 ? rho : a.sigma, a.mfloor) * (z - rho * xr);  // w = M (z - rho g), R1
         if (!ok) {
             z = 0.0;
             o = 0.0;

@@ -74,7 +74,7 @@ __global__ void __launch_bounds__(CTA, 2) k_step1_pipe(const SdotsArgs a) {
         for (int d = 0; d < 8; ++d) z = fma(v[d], xv[d], z);
         double o = 0.0;
         if (a.out_mode == 2) {
-            o = jacobi_minv(dg, 1.0, a.sigma, a.mfloor) * (z - rho * xr);  // w = M (z - rho g), R1
+            o = jacobi_minv(dg, 1.0, a.pmode == 2 ? rho : a.sigma, a.mfloor) * (z - rho * xr);  // w = M (z - rho g), R1
         } else if (a.out_mode == 1) {
             o = z;
         }

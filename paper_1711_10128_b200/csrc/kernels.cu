@@ -307,7 +307,7 @@ __global__ void __launch_bounds__(CTA, 3) k_spmv_nd(const SdotsArgs a) {
             }
             double o = 0.0, minv = 1.0;
             if (a.out_mode >= 2) {
-                minv = jacobi_minv(ad, bd, a.sigma, a.mfloor);  // M_ii
+                minv = jacobi_minv(ad, bd, a.pmode == 2 ? (a.out_mode == 2 ? rho : theta) : a.sigma, a.mfloor);  // M_ii
             }
             switch (a.out_mode) {
                 case 1: o = z; break;
@@ -403,7 +403,7 @@ __global__ void __launch_bounds__(CTA, 2) k_sdots_mma(const SdotsArgs a) {
         }
         double o = 0.0, minv = 1.0;
         if (a.out_mode >= 2) {
-            minv = jacobi_minv(ad, bd, a.sigma, a.mfloor);  // M_ii
+            minv = jacobi_minv(ad, bd, a.pmode == 2 ? (a.out_mode == 2 ? rho : theta) : a.sigma, a.mfloor);  // M_ii
         }
         if (a.out_mode == 1) o = z;
         else if (a.out_mode == 2) o = minv * (z - rho * sv);  // w = M (z - rho B g), R1

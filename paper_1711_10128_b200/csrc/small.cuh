@@ -71,7 +71,7 @@ __global__ void __launch_bounds__(SMALL_CTA, 1) k_inner_small(const SmallArgs a)
         for (int64_t row = tid; row < n; row += SMALL_CTA) {
             double ad = 1.0;
             const double z = mat_row(a.A, row >> 5, (int)(row & 31), g, ad);
-            const double w = jacobi_minv(ad, 1.0, a.sigma, a.mfloor) * (z - rho * g[row]);  // w = M (z - rho g), R1
+            const double w = jacobi_minv(ad, 1.0, a.pmode == 2 ? rho : a.sigma, a.mfloor) * (z - rho * g[row]);  // w = M (z - rho g), R1
             if (cgs) a.w[row] = w;
 #pragma unroll
             for (int c = 0; c < KMAX; ++c) {

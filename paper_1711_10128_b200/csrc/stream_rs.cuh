@@ -83,7 +83,7 @@ __global__ void __launch_bounds__(CTA, 2) k_step1_rs2(const SdotsArgs a) {
             if (a.out_mode == 2) {
                 if (a.B.nrows) sv = mat_row(a.B, sl, lane, X, bd);
                 else sv = xr;
-                o = jacobi_minv(ad, bd, a.sigma, a.mfloor) * (z - rho * sv);  // w = M (z - rho B g), R1
+                o = jacobi_minv(ad, bd, a.pmode == 2 ? rho : a.sigma, a.mfloor) * (z - rho * sv);  // w = M (z - rho B g), R1
             } else if (a.out_mode == 1) {
                 o = z;
             }

@@ -91,7 +91,7 @@ __global__ void __launch_bounds__(CTA, 1) k_step1_tp(const SdotsArgs a) {
             if (a.out_mode >= 2) sv = a.B.nrows ? mat_row_at(a.B, row, X, bd) : xr;
             double minv = 1.0;
             if (a.out_mode >= 2) {
-                minv = jacobi_minv(ad, bd, a.sigma, a.mfloor);  // M_ii
+                minv = jacobi_minv(ad, bd, a.pmode == 2 ? (a.out_mode == 2 ? rho : theta) : a.sigma, a.mfloor);  // M_ii
             }
             if (a.out_mode == 1) o = z;
             else if (a.out_mode == 2) o = minv * (z - rho * sv);  // w = M (z - rho B g), R1

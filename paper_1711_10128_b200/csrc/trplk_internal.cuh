@@ -97,6 +97,7 @@ struct SdotsArgs {
     unsigned gate;
     int gate_pass3;
     double sigma, mfloor;
+    int pmode;         // 2: M = Jacobi of A - rho B with this cycle's shift (w) / the residual's theta (u = M r)
     int count_prec;    // reserved
     Ctl* ctl;
     double* T;
@@ -209,6 +210,7 @@ struct SmallArgs {
     int ldT;
     int m;  // inner steps of the cycle
     double sigma, mfloor;
+    int pmode;  // as SdotsArgs::pmode
     unsigned gate, clear;
     int force3;
 };

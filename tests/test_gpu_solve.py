@@ -316,23 +316,27 @@ def test_graph_cache_across_contexts(gen):
         assert st["a_matvecs"] == st0["a_matvecs"]
 
 
-@pytest.mark.parametrize("name,N,l", [("C2", 12, 0), ("C2", 24, 0), ("C4", 8, 0), ("C1", None, 0), ("C2", 16, 2)])
-def test_no_preconditioner_trlan_baseline(orc, gen, name, N, l):
+@pytest.mark.parametrize("name,N,l,pc", [("C2", 12, 0, 1), ("C2", 24, 0, 1), ("C4", 8, 0, 1), ("C1", None, 0, 1),
+                                         ("C2", 16, 2, 1), ("C2", 16, 2, 2), ("C2", 24, 2, 2), ("C4", 8, 2, 2),
+                                         ("C5", 16, 2, 2)])
+def test_no_preconditioner_trlan_baseline(orc, gen, name, N, l, pc):
     """options.precond = 1 (M = I): with k_plus = 0 the thick-restart Lanczos baseline of eq 2.1
     (NEXT-4; the oracle pins its space per cycle in test_oracle_solver.py), the same parity as
     the preconditioned solve against the oracle run with precond = 1.  C1 (n = 1000) runs the
-    single-CTA path, C2-24 the multi-kernel one, C4 the pencil."""
+    single-CTA path, C2-24 the multi-kernel one, C4 the pencil.  pc = 2: the per-cycle shifted
+    Jacobi of NEXT-2 against the oracle's."""
     torch, trplk = need_gpu()
     P = gen.make(name, N=N)
     P.l = l
     P.q = P.q if name != "C1" else 12
-    g = gpu_solve(trplk, P, precond=1)
-    o = oracle_solve(orc, P, precond=1)
+    g = gpu_solve(trplk, P, precond=pc)
+    o = oracle_solve(orc, P, precond=pc)
     check_parity(g, o, P)
     assert g["stats"]["precond_applies"] >= 0
 
 
 @pytest.mark.parametrize("name,N,b,over", [("C2", 12, 2, {}), ("C2", 24, 2, {}), ("C2", 16, 3, {}),
+                                           ("C2", 12, 4, {"p": 4, "q": 12, "l": 4}),
                                            ("C3", 12, 2, {"p": 10, "q": 24, "l": 3}), ("C5", 16, 2, {}),
                                            ("C1", None, 2, {}), ("C2", 16, 4, {"l": 0})])
 def test_block_trplk_parity(orc, gen, name, N, b, over):

@@ -366,3 +366,58 @@ def test_block_trplk_subspace_multishift(orc, gen, b):
     r0 = orc.solve(P.A, None, P.p, P.q, P.l, P.tol, block=0)
     r1 = orc.solve(P.A, None, P.p, P.q, P.l, P.tol, block=1)
     assert np.array_equal(r0["eigenvalues"], r1["eigenvalues"]) and r0["a_matvecs"] == r1["a_matvecs"]
+
+
+def test_lobpcg_baseline_block_eq22(orc, gen):
+    """NEXT-4 baseline: LOBPCG (eq 2.2: "m = p = l") is block TRPL+K with block = p, m = p
+    and k_plus = p -- per cycle the RR space span{X_i, M R_i, X_{i-1}} with R_i = A X_i - B X_i Theta_i
+    the residuals of all p Ritz vectors and X_{i-1} the previous cycle's Ritz vectors.  Pinned by a
+    dense LOBPCG step per cycle (explicit residual block, Jacobi M, SVD orthonormalisation, dense RR)
+    while no pair is locked (t = 1), on C2 and the pencil C4."""
+    for name in ("C2", "C4"):
+        P = gen.make(name, N=5)
+        A, B = _dense_pencil(P)
+        Bm = np.eye(A.shape[0]) if B is None else B
+        Md = 1.0 / np.abs(np.diag(A))
+        p = 3
+        r = orc.solve(P.A, P.B, p, 3 * p, p, 1e-12, dump_cycles=8, max_cycles=8, block=p)
+        d = r["dump"]
+        checked = 0
+        for c in range(len(d["rho"])):
+            if d["t"][c] != 1:
+                break
+            X = d["X"][c]
+            th = np.array([(X[:, j] @ A @ X[:, j]) / (X[:, j] @ Bm @ X[:, j]) for j in range(p)])
+            R = A @ X - (Bm @ X) * th
+            cols = [X, Md[:, None] * R] + ([d["X"][c - 1]] if c > 0 else [])
+            thr = _rr_dense(A, B, np.hstack(cols), p)
+            assert np.max(np.abs(thr - r["log"]["thetas"][c][:p]) / np.abs(thr)) <= 1e-10, (name, c)
+            checked += 1
+        assert checked >= 3
+
+
+def test_shifted_jacobi_per_cycle(orc, gen):
+    """NEXT-2 (per-cycle shift, "M may change at every cycle with the goal to approximate
+    (A - rho_i I)^-1", reading P2c): precond = 2 re-forms the Jacobi M of A - rho_i B with the
+    cycle's shift; pinned by the eq 3.2 space rebuilt densely with that M, per cycle, C2 and C4."""
+    for name in ("C2", "C4"):
+        P = gen.make(name, N=4)
+        A, B = _dense_pencil(P)
+        Bm = np.eye(A.shape[0]) if B is None else B
+        p, m, l = 3, 3, 2
+        r = orc.solve(P.A, P.B, p, p + m + l, l, 1e-13, dump_cycles=6, max_cycles=6, precond=2)
+        d = r["dump"]
+        assert np.all(d["t"] == 1)
+        for c in range(len(d["rho"])):
+            X, rho = d["X"][c], d["rho"][c]
+            Md = 1.0 / np.maximum(np.abs(np.diag(A) - rho * np.diag(Bm)), 1e-8 * np.max(np.abs(np.diag(A))))
+            C = (np.eye(len(Md)) - X @ X.T @ Bm) @ (Md[:, None] * (A - rho * Bm))
+            cols = [X]
+            v = C @ X[:, 0]
+            for _ in range(m):
+                cols.append((v / np.linalg.norm(v))[:, None])
+                v = C @ cols[-1][:, 0]
+            if c > 0:
+                cols.append(d["X"][c - 1][:, :l])
+            th = _rr_dense(A, B, np.hstack(cols), p)
+            assert np.max(np.abs(th - r["log"]["thetas"][c][:p]) / np.abs(th)) <= 1e-10, (name, c)
