@@ -974,14 +974,18 @@ trplk_status run_block(trplk_ctx* ctx, BlkArgs a, int kmax, double bytes) {
 // +K as one block (B = I): block CGS2 of the c = nprev X^prev columns against U with Cholesky-QR
 // inside the block (BCGS2, third pass gated by R3's rule, dependent columns dropped by R16's
 // threshold), the accepted vectors appended, then one SpMM for their T columns (eq 3.1).  Four
-// passes over U for the whole block instead of four per column.  TRPLK_KPLUS=col: per column.
+// passes over U for the whole block instead of four per column.  Default for c >= 3 (measured:
+// C3, l = 3: +K 1.45 -> 1.23 ms per cycle, solve 3.59 -> 3.47 s); at c = 2 the per-column path is
+// as fast at C5 (29.9 vs 30.5 ms per cycle) and faster at C2 (0.100 vs 0.161 ms: fewer, shorter
+// launches).  TRPLK_KPLUS=col / =block force one of them.
 bool block_kplus(const trplk_ctx* ctx, int nprev) {
     static int v = -1;
     if (v < 0) {
         const char* e = getenv("TRPLK_KPLUS");
-        v = (e && !strcmp(e, "col")) ? 0 : 1;
+        v = (e && !strcmp(e, "col")) ? 0 : ((e && !strcmp(e, "block")) ? 2 : 1);
     }
-    return v == 1 && !ctx->hasB && nprev >= 1 && nprev <= BC;
+    if (v == 0 || ctx->hasB || nprev < 1 || nprev > BC) return false;
+    return v == 2 || nprev >= 3;
 }
 
 // Block CGS2 (BCGS2 with Cholesky-QR inside the block) of the c vectors Y against the current basis

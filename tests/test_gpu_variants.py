@@ -12,7 +12,8 @@ set (the switches are read once per process):
   TRPLK_GRID=1      the cooperative grid-wide inner loop (inner_grid.cuh)
   TRPLK_EIG=tri     the tridiagonal RR eigensolver (eig_tri.cu) instead of one-CTA Jacobi
   TRPLK_K1=tpdots   the thread-per-row kernel for the first-pass CGS dots of the seed / +K vectors
-  TRPLK_KPLUS=col   the +K columns one at a time (CGS2 + SpMV each) instead of the block kernels
+  TRPLK_KPLUS=col   the +K columns one at a time (CGS2 + SpMV each), also for k_plus >= 3
+  TRPLK_KPLUS=block the block +K kernels (block.cuh) also for k_plus <= 2
 """
 import os
 import subprocess
@@ -26,7 +27,7 @@ pytestmark = pytest.mark.gpu
 HERE = os.path.dirname(os.path.abspath(__file__))
 
 VARIANTS = [("TRPLK_K1", "pipe"), ("TRPLK_K1", "rs"), ("TRPLK_K1", "tpdots"), ("TRPLK_NO_COOP3", "1"),
-            ("TRPLK_NO_SMALL", "1"), ("TRPLK_GRID", "1"), ("TRPLK_EIG", "tri"), ("TRPLK_KPLUS", "col")]
+            ("TRPLK_NO_SMALL", "1"), ("TRPLK_GRID", "1"), ("TRPLK_EIG", "tri"), ("TRPLK_KPLUS", "col"), ("TRPLK_KPLUS", "block")]
 
 
 @pytest.mark.parametrize("var,val", VARIANTS)
