@@ -68,13 +68,6 @@ __device__ void blk_finalize(const BlkArgs& a, const double* r, int k, int c) {
         for (int v = threadIdx.x; v < c * c; v += blockDim.x) a.G[(v % c) + BC * (v / c)] = r[nkc + v];
 }
 
-// fp64 DMMA without `volatile`: the compiler may interleave independent accumulator chains
-__device__ __forceinline__ void dmma884_nv(double (&d)[2], double a, double b) {
-    asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
-        : "+d"(d[0]), "+d"(d[1])
-        : "d"(a), "d"(b));
-}
-
 template <int KMAX, int MODE, int LB>
 __global__ void __launch_bounds__(CTA, LB) k_blk(const BlkArgs a) {
     Ctl* ctl = a.ctl;

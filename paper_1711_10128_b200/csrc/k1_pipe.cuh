@@ -12,6 +12,7 @@ namespace trplk {
 
 template <int KMAX, bool TWO>
 __global__ void __launch_bounds__(CTA, 2) k_step1_pipe(const SdotsArgs a) {
+    pdl_wait();
     static_assert(KMAX <= 24, "one slab chunk");
     Ctl* ctl = a.ctl;
     if ((ctl->flags & a.gate) != a.gate) return;
@@ -98,13 +99,13 @@ __global__ void __launch_bounds__(CTA, 2) k_step1_pipe(const SdotsArgs a) {
             const double t2 = TWO ? __shfl_sync(0xffffffffu, o, 4 * q + fj) : 0.0;
             bq[q] = fi == 0 ? t1 : (fi == 1 ? t2 : 0.0);
         }
+        // the basis chunks' accumulators are independent DMMA chains: interleaved per k-step
+        // (non-volatile asm, so the compiler may schedule them) instead of one chain after another
 #pragma unroll
-        for (int g = 0; g < KMAX / 8; ++g) {
-            if (8 * g < kmx) {
-                const double* sp = W + (8 * g + fi) * WLD + fj;
+        for (int q = 0; q < 8; ++q) {
 #pragma unroll
-                for (int q = 0; q < 8; ++q) dmma884_s(cacc[g], sp[4 * q], bq[q]);
-            }
+            for (int g = 0; g < KMAX / 8; ++g)
+                if (8 * g < kmx) dmma884_nv(cacc[g], W[(8 * g + fi) * WLD + fj + 4 * q], bq[q]);
         }
         __syncwarp();
     }
@@ -131,6 +132,7 @@ __global__ void __launch_bounds__(CTA, 2) k_step1_pipe(const SdotsArgs a) {
         res[vv] = s;
     }
     __syncthreads();
+    pdl_trigger();
     if (!grid_reduce(res, nv, a.part, a.gpart, a.counter, a.maxcta, res)) return;
     if (a.red_local) {
         for (int vv = threadIdx.x; vv < nv; vv += CTA) a.red_local[vv] = res[vv];
@@ -144,7 +146,7 @@ static void launch_step1_pipe_k(const SdotsArgs& a, cudaStream_t s) {
     const int smem = WARPS * KMAX * WLD * (int)sizeof(double);
     auto kern = k_step1_pipe<KMAX, TWO>;
     NOTE_KERN(kern);
-    kern<<<rs_grid(kern, smem, a.nrows), CTA, smem, s>>>(a);
+    launch_pdl(kern, rs_grid(kern, smem, a.nrows), CTA, smem, s, a);
 }
 
 bool launch_step1_pipe(const SdotsArgs& a, int kmax, cudaStream_t s) {

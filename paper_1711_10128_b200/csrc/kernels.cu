@@ -490,7 +490,9 @@ __device__ void upd_finalize(const UpdArgs& a, const double* r, int kv) {
 }
 
 // Third CGS pass inside a cooperatively launched FINAL kernel (reading R3; one rank, B = I):
-// w2 = w1 - U h2 is already in a.out for this CTA's rows; h3 = U^T w2 and ||w2||^2 are reduced
+// w2 = w1 - U h2 is in a.out (written by all CTAs; the grid barrier below makes every row
+// visible before any CTA reads it -- a CTA's rows are not the rows it wrote with the two-tile
+// mapping); h3 = U^T w2 and ||w2||^2 are reduced
 // over the grid (per-CTA partials, grid barrier, the same fixed-order sum in every CTA), then
 // g = (w2 - U h3) / beta3 with beta3^2 = ||w2||^2 - ||h3||^2.  Rare path (a second pass that
 // loses more than half the norm): written for few registers, not speed.  Returns breakdown.
@@ -1046,7 +1048,7 @@ void launch_sdots(const SdotsArgs& a, int kmax, cudaStream_t s) {
             NOTE_KERN(kern);                                       \
             if (a.mode == 2 && a.coop) {                           \
                 cudaLaunchConfig_t cfg{};                          \
-                cfg.gridDim = stream_grid(kern, a.nrows);          \
+                cfg.gridDim = stream_grid(kern, KM <= 24 ? (a.nrows + 1) / 2 : a.nrows); \
                 cfg.blockDim = CTA;                                \
                 cfg.stream = s;                                    \
                 cudaLaunchAttribute at[1];                         \
@@ -1055,8 +1057,8 @@ void launch_sdots(const SdotsArgs& a, int kmax, cudaStream_t s) {
                 cfg.attrs = at;                                    \
                 cfg.numAttrs = 1;                                  \
                 cudaLaunchKernelEx(&cfg, kern, a);                 \
-            } else {                                               \
-                kern<<<stream_grid(kern, a.nrows), CTA, 0, s>>>(a); \
+            } else {  /* k <= 24: two 32-row tiles per warp iteration */ \
+                kern<<<stream_grid(kern, KM <= 24 ? (a.nrows + 1) / 2 : a.nrows), CTA, 0, s>>>(a); \
             }                                                      \
         }                                                          \
     } break;

@@ -23,6 +23,13 @@ __device__ __forceinline__ void dmma884_s(double (&d)[2], double a, double b) {
                  : "d"(a), "d"(b));
 }
 
+// fp64 DMMA without `volatile`: the compiler may interleave independent accumulator chains
+__device__ __forceinline__ void dmma884_nv(double (&d)[2], double a, double b) {
+    asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+        : "+d"(d[0]), "+d"(d[1])
+        : "d"(a), "d"(b));
+}
+
 __device__ __forceinline__ double warp_sum_s(double v) {
 #pragma unroll
     for (int o = 16; o >= 1; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -47,6 +54,7 @@ __host__ __device__ constexpr int rs_chunk(int kmax) { return kmax < 24 ? kmax :
 // one slab per tile.  C2: K1 24.5 -> 22.6 us, solve -2.7 %; C3: K1 145 -> 135 us, -2.9 %.
 template <int KMAX, bool TWO>
 __global__ void __launch_bounds__(CTA, 2) k_step1_rs2(const SdotsArgs a) {
+    pdl_wait();
     Ctl* ctl = a.ctl;
     if ((ctl->flags & a.gate) != a.gate) return;
     if (a.gate_pass3 && ctl->pass3 == 0) return;
@@ -66,9 +74,14 @@ __global__ void __launch_bounds__(CTA, 2) k_step1_rs2(const SdotsArgs a) {
     const int fi = lane >> 2, fj = lane & 3;
     double* W0 = wsm + (size_t)warp * 2 * CH * WLD;
     double* W1 = W0 + CH * WLD;
-    double cacc[KMAX / 8][2];
+    // k <= 32: the two tiles accumulate separately (two interleaved DMMA chains); wider blocks
+    // share one accumulator set (the register budget of 2 CTAs per SM)
+    constexpr bool DUAL = KMAX <= 32;
+    double cacc[KMAX / 8][2], cacc1[DUAL ? KMAX / 8 : 1][2];
 #pragma unroll
     for (int g = 0; g < KMAX / 8; ++g) cacc[g][0] = cacc[g][1] = 0.0;
+#pragma unroll
+    for (int g = 0; g < (DUAL ? KMAX / 8 : 1); ++g) cacc1[g][0] = cacc1[g][1] = 0.0;
     double n1 = 0.0;
     const int64_t nslices = (a.nrows + 31) >> 5;
     const int64_t npairs = (nslices + 1) >> 1;
@@ -145,10 +158,13 @@ __global__ void __launch_bounds__(CTA, 2) k_step1_rs2(const SdotsArgs a) {
             if (cb < kmx) {
                 const double* sp0 = W0 + fi * WLD + fj;
                 const double* sp1 = W1 + fi * WLD + fj;
+                // the two tiles into separate accumulators, interleaved: two independent DMMA
+                // chains of 8 instead of one of 16 (added together after the loop)
 #pragma unroll
-                for (int q = 0; q < 8; ++q) dmma884_s(cacc[cb / 8], sp0[4 * q], bq0[q]);
-#pragma unroll
-                for (int q = 0; q < 8; ++q) dmma884_s(cacc[cb / 8], sp1[4 * q], bq1[q]);
+                for (int q = 0; q < 8; ++q) {
+                    dmma884_nv(cacc[cb / 8], sp0[4 * q], bq0[q]);
+                    dmma884_nv(DUAL ? cacc1[DUAL ? cb / 8 : 0] : cacc[cb / 8], sp1[4 * q], bq1[q]);
+                }
             }
             if (more) {
                 __syncwarp();
@@ -167,8 +183,8 @@ __global__ void __launch_bounds__(CTA, 2) k_step1_rs2(const SdotsArgs a) {
 #pragma unroll
         for (int g = 0; g < KMAX / 8; ++g) {
             const int c = 8 * g + fi;
-            if (c < k1) acc[warp][c] = cacc[g][0];
-            if (TWO && c < k2) acc[warp][k1 + c] = cacc[g][1];
+            if (c < k1) acc[warp][c] = DUAL ? cacc[g][0] + cacc1[DUAL ? g : 0][0] : cacc[g][0];
+            if (TWO && c < k2) acc[warp][k1 + c] = DUAL ? cacc[g][1] + cacc1[DUAL ? g : 0][1] : cacc[g][1];
         }
     }
     if (nn) {
@@ -184,6 +200,7 @@ __global__ void __launch_bounds__(CTA, 2) k_step1_rs2(const SdotsArgs a) {
         res[v] = s;
     }
     __syncthreads();
+    pdl_trigger();
     if (!grid_reduce(res, nv, a.part, a.gpart, a.counter, a.maxcta, res)) return;
     if (a.red_local) {
         for (int v = threadIdx.x; v < nv; v += CTA) a.red_local[v] = res[v];
@@ -229,7 +246,7 @@ static void launch_step1_rs_k(const SdotsArgs& a, cudaStream_t s) {
     const int smem2 = WARPS * 2 * 8 * WLD * (int)sizeof(double);
     auto kern2 = k_step1_rs2<KMAX, TWO>;
     NOTE_KERN(kern2);
-    kern2<<<rs_grid(kern2, smem2, (a.nrows + 1) / 2), CTA, smem2, s>>>(a);
+    launch_pdl(kern2, rs_grid(kern2, smem2, (a.nrows + 1) / 2), CTA, smem2, s, a);
 }
 
 bool launch_step1_rs(const SdotsArgs& a, int kmax, cudaStream_t s) {

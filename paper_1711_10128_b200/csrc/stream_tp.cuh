@@ -213,6 +213,7 @@ bool launch_step1_tp(const SdotsArgs& a, int kmax, cudaStream_t s) {
 // the one-tile kernel measured slower and was removed).
 template <int KS, int G>
 __global__ void __launch_bounds__(CTA, 2) k_upd2_wp2(const UpdArgs a) {
+    pdl_wait();
     constexpr int NGR = WARPS / G;
     Ctl* ctl = a.ctl;
     if ((ctl->flags & a.gate) != a.gate) return;
@@ -297,6 +298,7 @@ __global__ void __launch_bounds__(CTA, 2) k_upd2_wp2(const UpdArgs a) {
         res[v] = sum;
     }
     __syncthreads();
+    pdl_trigger();
     if (!grid_reduce(res, nv, a.part, a.gpart, a.counter, a.maxcta, res)) return;
     if (a.red_local) {
         for (int v = threadIdx.x; v < nv; v += CTA) a.red_local[v] = res[v];
@@ -309,7 +311,7 @@ template <int KS, int G>
 static void launch_upd2_wp_k(const UpdArgs& a, cudaStream_t s) {
     auto kern2 = k_upd2_wp2<KS, G>;
     NOTE_KERN(kern2);
-    kern2<<<tp_grid(kern2, (a.nrows + 1) / 2, 8 * G), CTA, 0, s>>>(a);
+    launch_pdl(kern2, tp_grid(kern2, (a.nrows + 1) / 2, 8 * G), CTA, 0, s, a);
 }
 
 bool launch_upd2_wp(const UpdArgs& a, int kmax, cudaStream_t s) {

@@ -1,6 +1,7 @@
 // Internal declarations of the TRPL+K device path (kernels + engine).
 // Not part of the ABI; see include/trplk.h for the boundary.
 #pragma once
+#include <cstdlib>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -276,6 +277,43 @@ __device__ __forceinline__ double jacobi_minv(double ad, double bd, double sigma
     double d = fabs(ad - sigma * bd);
     d = d > mfloor ? d : mfloor;
     return 1.0 / d;
+}
+
+// Programmatic dependent launch (sm_90+): a kernel launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization may start while its predecessor finishes;
+// griddepcontrol.wait blocks until the predecessor grid has completed and its writes are visible
+// (a no-op when launched normally), launch_dependents lets the successor launch early.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+// Launch with programmatic stream serialization (the kernel calls pdl_wait before touching its
+// predecessor's results).  TRPLK_PDL=0: plain launches.
+inline bool pdl_on() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("TRPLK_PDL");
+        v = (e && e[0] == '0') ? 0 : 1;
+    }
+    return v == 1;
+}
+
+template <typename A>
+inline void launch_pdl(void (*kern)(A), int grid, int block, int smem, cudaStream_t s, const A& a) {
+    if (!pdl_on()) {
+        kern<<<grid, block, smem, s>>>(a);
+        return;
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3((unsigned)block);
+    cfg.dynamicSmemBytes = (size_t)smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, kern, a);
 }
 
 // The kernel function most recently launched by this host thread (measurement: bench.py and the

@@ -15,7 +15,7 @@ from typing import Optional
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "lib", "libtrplk.so")
+LIB_PATH = os.environ.get("TRPLK_LIB_OVERRIDE") or os.path.join(_PKG, "lib", "libtrplk.so")  # override: A/B tools
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"libtrplk.so not built ({LIB_PATH}); run `python -m paper_1711_10128_b200.build`")

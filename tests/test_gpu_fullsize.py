@@ -71,6 +71,12 @@ def test_fullsize_vs_oracle_golden(gen, name):
             ok = _near_tie(g["log_thetas"][c], lo["res"][c], P.tol) or any(
                 _emergence(L, cc) for L in (lo, log) for cc in range(max(c - 1, 1), min(c + 2, n)))
             assert ok, f"diverged at cycle {c} without a near-tie or an emergence event"
+            # reported, and bounded: after the divergence both runs converge to the same clusters;
+            # the total work may differ by the cycles the later emergence costs (<= 5 %)
+            print(f"{name}: trajectories part at cycle {c} (t {lo['t'][c]} / {log['t'][c]}, theta_t "
+                  f"{lo['theta_t'][c]:.16e} / {log['theta_t'][c]:.16e}); cycles oracle {g['cycles']} GPU "
+                  f"{st['cycles']}, A-matvecs {g['a_matvecs']} / {st['a_matvecs']}")
+            assert abs(st["cycles"] - g["cycles"]) <= 0.05 * g["cycles"]
             break
     else:
         assert st["a_matvecs"] == g["a_matvecs"]

@@ -149,3 +149,22 @@ def test_pl1_loopback_ranks(gen, orc, name, N, nranks):
     B = None if P.B is None else P.B.to_scipy()
     Bx = x if B is None else B @ x
     assert abs(abs(Bx @ r["x"]) - 1) <= 1e-8
+
+
+@pytest.mark.parametrize("nranks", [2, 3])
+def test_loopback_ranks_block_kplus(gen, nranks):
+    """k_plus = 3: the +K block path (block.cuh: GRAM / UPD / SPMM reductions through the rank
+    allgather + rank-ordered finalize, halo of the appended block) on 2 and 3 ranks reproduces the
+    1-rank solve (same trajectory and A-matvec count, eigenvalues within 1e-10)."""
+    torch, trplk = need_gpu()
+    P = gen.make("C2", N=15, l=3)
+    ctx = trplk.trplk_create(P.A, P.B, P.sigma)
+    ev1, X1, rs1, st1 = trplk.trplk_solve(ctx, P.p, P.q, P.l, P.tol)
+    log1 = trplk.trplk_get_log(ctx, ph=P.p)
+    ctx.close()
+    outs = _multirank(trplk, gen, "C2", 15, nranks, l=3)
+    o0 = outs[0]
+    assert o0["st"]["status"] == "OK"
+    assert o0["st"]["a_matvecs"] == st1["a_matvecs"]
+    assert list(o0["log"]["nprev"]) == list(log1["nprev"]) and max(log1["nprev"]) == 3
+    assert np.max(np.abs(o0["ev"] - ev1) / np.abs(ev1)) <= 1e-10

@@ -331,6 +331,17 @@ def test_no_preconditioner_trlan_baseline(orc, gen, name, N, l, pc):
     P.q = P.q if name != "C1" else 12
     g = gpu_solve(trplk, P, precond=pc)
     o = oracle_solve(orc, P, precond=pc)
+    if pc == 2:
+        # the per-cycle M depends on theta_t, so rounding-level differences in theta_t feed back
+        # into the operator every cycle: the trajectories agree to 1e-10 for dozens of cycles and
+        # then drift (C2-24: cycle 56, 2e-10); the protocol's "GPU = oracle +-1 cycle" + results
+        assert g["stats"]["status"] == o["status"] == "OK"
+        assert np.all(g["residuals"] <= P.tol)
+        c = first_divergence(g, o, norm_inf(P))
+        assert c is None or c >= 20, c
+        assert abs(g["stats"]["cycles"] - o["cycles"]) <= 1
+        assert np.max(np.abs(g["eigenvalues"] - o["eigenvalues"]) / np.abs(o["eigenvalues"])) <= 1e-9
+        return
     check_parity(g, o, P)
     assert g["stats"]["precond_applies"] >= 0
 

@@ -13,7 +13,8 @@ for r in rows[i + 1:]:
     if len(r) <= mv:
         continue
     v = float(r[mv].replace(",", ""))
-    v = v / 1e3 if r[mu] == "nsecond" else (v if r[mu] == "usecond" else v * 1e3)
+    unit = r[mu]
+    v = v / 1e3 if unit in ("nsecond", "ns") else (v if unit in ("usecond", "us") else v * 1e3)
     name = r[kn].split("(")[0]
     tot[name] += v
     cnt[name] += 1
