@@ -107,6 +107,8 @@ def lib():
         L.orc_inner_steps.restype = ctypes.c_int
         L.orc_inner_steps.argtypes = [ctypes.POINTER(_Problem), _P, ctypes.c_double, _P, ctypes.c_int,
                                       ctypes.c_int, _P, ctypes.c_int, _P]
+        L.orc_ic0.restype = _I64
+        L.orc_ic0.argtypes = [ctypes.POINTER(_Problem), ctypes.c_double, _P, _P, _P, _I64]
         L.orc_pl1_solve.restype = ctypes.c_int
         L.orc_pl1_solve.argtypes = [ctypes.POINTER(_Pl1Problem), _P, ctypes.POINTER(_Pl1Report)]
         _lib = L
@@ -272,6 +274,22 @@ def inner_steps(A, B, M, rho, U, k0, nsteps, T=None, work=None):
     done = lib().orc_inner_steps(ctypes.byref(prob), _ptr(M), float(rho), _ptr(U), k0, nsteps, _ptr(T), q,
                                  _ptr(work))
     return done, T
+
+
+def ic0(A, B=None, sigma=0.0):
+    """IC(0) factor of A - sigma B (orc_ic0) as a scipy CSR lower-triangular matrix."""
+    import scipy.sparse as sp
+    ra, ca, va = _csr(A)
+    rb, cb, vb = _csr(B)
+    n = len(ra) - 1
+    prob = _Problem(n, _ptr(ra), _ptr(ca), _ptr(va), _ptr(rb), _ptr(cb), _ptr(vb), sigma,
+                    1, 2, 0, 1.0, 0, 12, 1, 0, 0, 0, 3, 1)
+    nnz = lib().orc_ic0(ctypes.byref(prob), sigma, None, None, None, 0)
+    rp = np.zeros(n + 1, np.int64)
+    ci = np.zeros(nnz, np.int64)
+    v = np.zeros(nnz)
+    lib().orc_ic0(ctypes.byref(prob), sigma, _ptr(rp), _ptr(ci), _ptr(v), nnz)
+    return sp.csr_matrix((v, ci, rp), shape=(n, n))
 
 
 def pl1_solve(A, B=None, m=4, tol=1e-8, sigma=0.0, seed=12, x0=None, max_cycles=2000, variant=0,

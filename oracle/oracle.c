@@ -284,7 +284,112 @@ static void rotate_rows_inplace(int64_t n, int k, double* U, const double* Y, in
 /* One inner step of eq 3.1 on the basis U(:,0:k), g_j = U(:,k-1):
  *   z = A g_j;  T(1:k,k) = U^T z (mirrored);  if `next`: w = M(z - rho B g_j) (R1), CGS2_B of w
  *   against U(:,0:k) (R2, R3) and g_{j+1} = w/beta into U(:,k).  Returns 1 on a breakdown (R16). */
-static int inner_step_at(ctx_t* c, const double* M, double rho, int next, double* U, int k, int gpos, double* T,
+/* ------------------------------------------------ preconditioner M (R12; P2c; NEXT-2 IC(0))
+ * Either the diagonal M (Jacobi, R12 / P2c) or M = (L L^T)^-1 with L the IC(0) factor of
+ * K = A - sigma B (reading P2a): L has the sparsity of K's lower triangle (no fill);
+ *   L_ij = (K_ij - sum_{k<j} L_ik L_jk) / L_jj  (j < i, k over the common lower pattern),
+ *   L_ii = sqrt(K_ii - sum_{j<i} L_ij^2),  a pivot <= 0 replaced by eps_d max_j|K_jj| (R12 floor);
+ * applied by a forward solve L y = v and a backward solve L^T w = y, in row order. */
+typedef struct {
+    const double* M;         /* diagonal, or NULL */
+    int64_t n;
+    int64_t *rp, *ci;        /* IC(0) factor (CSR, columns ascending, diagonal last) */
+    double* val;
+    double* tmp;
+} prec_t;
+
+static void prec_apply(const prec_t* pc, double* v) {
+    const int64_t n = pc->n;
+    if (pc->M) {
+        for (int64_t i = 0; i < n; ++i) v[i] = pc->M[i] * v[i];
+        return;
+    }
+    for (int64_t i = 0; i < n; ++i) { /* L y = v */
+        double s = v[i];
+        const int64_t e = pc->rp[i + 1] - 1; /* diagonal */
+        for (int64_t p = pc->rp[i]; p < e; ++p) s -= pc->val[p] * v[pc->ci[p]];
+        v[i] = s / pc->val[e];
+    }
+    for (int64_t i = n - 1; i >= 0; --i) { /* L^T w = y, column-oriented */
+        const int64_t e = pc->rp[i + 1] - 1;
+        v[i] /= pc->val[e];
+        for (int64_t p = pc->rp[i]; p < e; ++p) v[pc->ci[p]] -= pc->val[p] * v[i];
+    }
+}
+
+/* IC(0) of K = A - sigma B on A's lower pattern (B's entries outside it are ignored). */
+static int ic0_build(const orc_problem* P, double sigma, prec_t* pc) {
+    const int64_t n = P->n;
+    int64_t* rp = (int64_t*)malloc((size_t)(n + 1) * sizeof(int64_t));
+    rp[0] = 0;
+    for (int64_t i = 0; i < n; ++i) {
+        int64_t cnt = 0;
+        for (int64_t p = P->a_rowptr[i]; p < P->a_rowptr[i + 1]; ++p)
+            if (P->a_col[p] < i) ++cnt;
+        rp[i + 1] = rp[i] + cnt + 1;
+    }
+    int64_t* ci = (int64_t*)malloc((size_t)rp[n] * sizeof(int64_t));
+    double* val = (double*)malloc((size_t)rp[n] * sizeof(double));
+    double amax = 0.0;
+    for (int64_t i = 0; i < n; ++i) {
+        int64_t q = rp[i];
+        double kd = 0.0;
+        for (int64_t p = P->a_rowptr[i]; p < P->a_rowptr[i + 1]; ++p) {
+            const int64_t j = P->a_col[p];
+            double kij = P->a_val[p];
+            if (P->b_rowptr)
+                for (int64_t t = P->b_rowptr[i]; t < P->b_rowptr[i + 1]; ++t)
+                    if (P->b_col[t] == j) kij -= sigma * P->b_val[t];
+            if (!P->b_rowptr && j == i) kij -= sigma;
+            if (j < i) { ci[q] = j; val[q] = kij; ++q; }
+            if (j == i) kd = kij;
+        }
+        ci[q] = i;
+        val[q] = kd;
+        if (fabs(kd) > amax) amax = fabs(kd);
+    }
+    for (int64_t i = 0; i < n; ++i) {
+        const int64_t e = rp[i + 1] - 1;
+        for (int64_t p = rp[i]; p < e; ++p) {
+            const int64_t j = ci[p];
+            /* s = K_ij - sum_{k < j} L_ik L_jk over the common pattern (both rows ascending) */
+            double s = val[p];
+            int64_t a = rp[i], b = rp[j];
+            const int64_t be = rp[j + 1] - 1;
+            while (a < p && b < be) {
+                if (ci[a] == ci[b]) { s -= val[a] * val[b]; ++a; ++b; }
+                else if (ci[a] < ci[b]) ++a;
+                else ++b;
+            }
+            val[p] = s / val[rp[j + 1] - 1];
+        }
+        double d = val[e];
+        for (int64_t p = rp[i]; p < e; ++p) d -= val[p] * val[p];
+        if (!(d > 1e-8 * amax)) d = 1e-8 * amax;
+        val[e] = sqrt(d);
+    }
+    pc->M = NULL;
+    pc->n = n;
+    pc->rp = rp;
+    pc->ci = ci;
+    pc->val = val;
+    return 0;
+}
+
+int64_t orc_ic0(const orc_problem* P, double sigma, int64_t* rp_out, int64_t* ci_out, double* val_out, int64_t cap) {
+    prec_t pc;
+    ic0_build(P, sigma, &pc);
+    const int64_t nnz = pc.rp[P->n];
+    if (rp_out && ci_out && val_out && cap >= nnz) {
+        memcpy(rp_out, pc.rp, (size_t)(P->n + 1) * sizeof(int64_t));
+        memcpy(ci_out, pc.ci, (size_t)nnz * sizeof(int64_t));
+        memcpy(val_out, pc.val, (size_t)nnz * sizeof(double));
+    }
+    free(pc.rp); free(pc.ci); free(pc.val);
+    return nnz;
+}
+
+static int inner_step_at(ctx_t* c, const prec_t* pc, double rho, int next, double* U, int k, int gpos, double* T,
                          int q, double* z, double* s, double* w, double* Bw) {
     /* g = U(:, gpos) of a basis of width k; its T column covers rows 0..k-1 (mirrored), its
      * preconditioned image is CGS2-orthogonalised against all k columns and appended at k */
@@ -299,16 +404,17 @@ static int inner_step_at(ctx_t* c, const double* M, double rho, int next, double
     }
     if (!next) return 0;
     applyB(c, g, s);
-    for (int64_t i = 0; i < n; ++i) w[i] = M[i] * (z[i] - rho * s[i]); /* R1 */
+    for (int64_t i = 0; i < n; ++i) w[i] = z[i] - rho * s[i];
+    prec_apply(pc, w); /* w = M (z - rho B g), R1 */
     c->prec++;
     if (cgs2_ctx(c, k, U, w, Bw, NULL, &beta, NULL)) return 1;
     scal_copy(n, 1.0 / beta, w, U + (size_t)n * k);
     return 0;
 }
 
-static int inner_step(ctx_t* c, const double* M, double rho, int next, double* U, int k, double* T, int q,
+static int inner_step(ctx_t* c, const prec_t* pc, double rho, int next, double* U, int k, double* T, int q,
                       double* z, double* s, double* w, double* Bw) {
-    return inner_step_at(c, M, rho, next, U, k, k - 1, T, q, z, s, w, Bw);
+    return inner_step_at(c, pc, rho, next, U, k, k - 1, T, q, z, s, w, Bw);
 }
 
 int orc_inner_steps(const orc_problem* P, const double* M, double rho, double* U, int k0, int nsteps,
@@ -320,7 +426,8 @@ int orc_inner_steps(const orc_problem* P, const double* M, double rho, double* U
     int done = 0;
     for (int j = 0; j < nsteps; ++j) {
         ++done;
-        if (inner_step(&c, M, rho, 1, U, k0 + j, T, ldT, z, s, w, Bw)) break;
+        prec_t pc = {M, n, NULL, NULL, NULL, NULL};
+        if (inner_step(&c, &pc, rho, 1, U, k0 + j, T, ldT, z, s, w, Bw)) break;
     }
     if (!work) free(wk);
     return done;
@@ -332,7 +439,7 @@ int orc_trplk_solve(const orc_problem* P, double* evals, double* evecs, double* 
     const int ph = P->restart_size > 0 ? P->restart_size : p; /* R5: p^ = p by default */
     if (rep) { rep->status = 1; rep->cycles = 0; rep->log_len = 0; }
     if (n < 1 || p < 1 || l < 0 || ph < p || q - ph - l < 1 || !(P->tol > 0.0) || ph + 1 > n ||
-        P->max_cycles < 1 || P->block > 8 || q > 64 || P->precond < 0 || P->precond > 2 ||
+        P->max_cycles < 1 || P->block > 8 || q > 64 || P->precond < 0 || P->precond > 3 ||
         (P->precond == 2 && P->block > 1))
         return 1; /* EINVAL */
     const int m = q - ph - l; /* inner steps per cycle (R5) */
@@ -345,6 +452,8 @@ int orc_trplk_solve(const orc_problem* P, double* evals, double* evecs, double* 
                     1e-8, M);
     if (P->precond == 1) /* no preconditioning: the TRLan / LOPCG baselines of PAPER.md:77-95 */
         for (int64_t i = 0; i < n; ++i) M[i] = 1.0;
+    prec_t pc = {M, n, NULL, NULL, NULL, NULL};
+    if (P->precond == 3) ic0_build(P, P->sigma, &pc); /* IC(0) of A - sigma B (P2a) */
     double tau = P->tol;
     if (P->tol_mode == 1) tau = P->tol * orc_frobenius(P->a_rowptr[n], P->a_val); /* eq 5.1 */
 
@@ -397,7 +506,8 @@ int orc_trplk_solve(const orc_problem* P, double* evals, double* evecs, double* 
         orc_jacobi_diag(n, P->a_rowptr, P->a_col, P->a_val, P->b_rowptr, P->b_col, P->b_val, rho, 1e-8, M);
     applyB(&c, U, s);
     for (int64_t i = 0; i < n; ++i) r[i] = W[i] - rho * s[i];
-    for (int64_t i = 0; i < n; ++i) u[i] = M[i] * r[i];
+    for (int64_t i = 0; i < n; ++i) u[i] = r[i];
+    prec_apply(&pc, u);
     c.prec++;
     /* block TRPL+K (NEXT-3; reading B1): seeds M r_{t+i} of the next b-1 targets too */
     const int b = P->block > 1 ? P->block : 1;
@@ -409,7 +519,8 @@ int orc_trplk_solve(const orc_problem* P, double* evals, double* evecs, double* 
         for (int i = 1; i <= nub; ++i) { /* r_i = A x_i - theta_i B x_i from W (no matvec) */
             double* ui = ub + (size_t)n * (i - 1);
             applyB(&c, U + (size_t)n * i, s);
-            for (int64_t j = 0; j < n; ++j) ui[j] = M[j] * (W[j + (size_t)n * i] - th[i] * s[j]);
+            for (int64_t j = 0; j < n; ++j) ui[j] = W[j + (size_t)n * i] - th[i] * s[j];
+            prec_apply(&pc, ui);
             c.prec++;
         }
     }
@@ -443,7 +554,7 @@ int orc_trplk_solve(const orc_problem* P, double* evals, double* evecs, double* 
             for (int j = 1; j <= m; ++j) {
                 k += 1; /* k = p^ + j */
                 ++inner_steps;
-                if (inner_step(&c, M, rho, j < m, U, k, T, q, z, s, w, Bw)) break; /* R16: basis ends early */
+                if (inner_step(&c, &pc, rho, j < m, U, k, T, q, z, s, w, Bw)) break; /* R16: basis ends early */
             }
         } else {
             /* ---- block version (B1): seeds M r_{t+i}, i < b_e, CGS2_B against [X, earlier seeds]
@@ -461,7 +572,7 @@ int orc_trplk_solve(const orc_problem* P, double* evals, double* evecs, double* 
             for (int next = ph; next < width; ++next) {
                 ++inner_steps;
                 const int produce = width < ph + m;
-                if (!inner_step_at(&c, M, rho, produce, U, width, next, T, q, z, s, w, Bw) && produce) ++width;
+                if (!inner_step_at(&c, &pc, rho, produce, U, width, next, T, q, z, s, w, Bw) && produce) ++width;
             }
             k = width;
         }
@@ -562,7 +673,8 @@ int orc_trplk_solve(const orc_problem* P, double* evals, double* evecs, double* 
         rho = th[t - 1];
         if (P->precond == 2)
             orc_jacobi_diag(n, P->a_rowptr, P->a_col, P->a_val, P->b_rowptr, P->b_col, P->b_val, rho, 1e-8, M);
-        for (int64_t i = 0; i < n; ++i) u[i] = M[i] * r[i];
+        for (int64_t i = 0; i < n; ++i) u[i] = r[i];
+        prec_apply(&pc, u);
         c.prec++;
         if (b > 1) { /* residuals of the next targets: one A-matvec each (B1) */
             nub = b - 1 < ph - t ? b - 1 : ph - t;
@@ -570,7 +682,8 @@ int orc_trplk_solve(const orc_problem* P, double* evals, double* evecs, double* 
             for (int i = 1; i <= nub; ++i) {
                 double* ui = ub + (size_t)n * (i - 1);
                 residual(&c, U + (size_t)n * (t - 1 + i), th[t - 1 + i], w, s);
-                for (int64_t j = 0; j < n; ++j) ui[j] = M[j] * w[j];
+                for (int64_t j = 0; j < n; ++j) ui[j] = w[j];
+                prec_apply(&pc, ui);
                 c.prec++;
             }
         }
@@ -604,6 +717,7 @@ done:
         rep->random_draws = draws;
     }
     free(ub);
+    free(pc.rp); free(pc.ci); free(pc.val);
     free(M); free(U); free(W); free(Xp); free(w); free(Bw); free(z);
     free(s); free(r); free(u); free(T); free(Tk); free(Y); free(th);
     return status;

@@ -61,7 +61,8 @@ typedef struct {
     int debug;              /* 1: log ||T - U^T A U||_max and ||U^T B U - I||_max per cycle */
     int precond;            /* 0 Jacobi (R12); 1 none, M = I: with l = 0 thick-restart Lanczos (eq 2.1,
                                PAPER.md:77-80), with m = p = l = 1 LOPCG (eq 2.2 with p = 1);
-                               2 Jacobi of A - rho_i B re-formed every cycle (reading P2c) */
+                               2 Jacobi of A - rho_i B re-formed every cycle (reading P2c);
+                               3 IC(0) of A - sigma B ("incomplete ... factorization", P2a) */
     int block;              /* b <= 8: block TRPL+K ("A block TRPL+K is also possible", reading
                                B1): the inner space is the block Krylov space of eq 3.2's operator C
                                (one shift rho = theta_t) from the b_e = min(b, p^-t+1, m) seeds
@@ -103,6 +104,10 @@ typedef struct {
  * bench.py to time a bounded sample of the oracle at sizes where a full solve takes hours. */
 int orc_inner_steps(const orc_problem* P, const double* M, double rho, double* U, int k0, int nsteps,
                     double* T, int ldT, double* work /* 4n scratch, or NULL */);
+
+/* IC(0) factor L (CSR: rows ascending by column, the diagonal last) of A - sigma B on A's lower
+ * pattern (reading P2a, see oracle.c).  Returns nnz(L); copies into the outputs when cap >= nnz. */
+int64_t orc_ic0(const orc_problem* P, double sigma, int64_t* rp_out, int64_t* ci_out, double* val_out, int64_t cap);
 
 /* Algorithm 1 in full.  evals[p], resid[p] ascending; evecs n x p column-major. */
 int orc_trplk_solve(const orc_problem* prob, double* evals, double* evecs, double* resid,

@@ -99,13 +99,14 @@ __global__ void __launch_bounds__(CTA, 2) k_step1_pipe(const SdotsArgs a) {
             const double t2 = TWO ? __shfl_sync(0xffffffffu, o, 4 * q + fj) : 0.0;
             bq[q] = fi == 0 ? t1 : (fi == 1 ? t2 : 0.0);
         }
-        // the basis chunks' accumulators are independent DMMA chains: interleaved per k-step
-        // (non-volatile asm, so the compiler may schedule them) instead of one chain after another
+        // (interleaving the chunks' DMMA chains measured 1 % slower here: 4.84 vs 4.79 ms at C5)
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
+        for (int g = 0; g < KMAX / 8; ++g) {
+            if (8 * g < kmx) {
+                const double* sp = W + (8 * g + fi) * WLD + fj;
 #pragma unroll
-            for (int g = 0; g < KMAX / 8; ++g)
-                if (8 * g < kmx) dmma884_nv(cacc[g], W[(8 * g + fi) * WLD + fj + 4 * q], bq[q]);
+                for (int q = 0; q < 8; ++q) dmma884_s(cacc[g], sp[4 * q], bq[q]);
+            }
         }
         __syncwarp();
     }
