@@ -57,8 +57,9 @@ def parse():
     ap.add_argument("--comm", default="nccl", choices=["nccl", "host"],
                     help="N>1 exchanges: nccl (production) or host (host-staged through a gloo group; "
                          "lets several ranks share one GPU -- tests of the multi-process path only)")
-    ap.add_argument("--precond", default="jacobi", choices=["jacobi", "none"],
-                    help="none: M = I (with --k-plus 0: the thick-restart Lanczos baseline, eq 2.1)")
+    ap.add_argument("--precond", default="jacobi", choices=["jacobi", "none", "shifted", "ic0"],
+                    help="none: M = I (with --k-plus 0: the thick-restart Lanczos baseline, eq 2.1); "
+                         "shifted: Jacobi of A - rho_i B per cycle (P:171); ic0: IC(0) of A - sigma B")
     ap.add_argument("--k-plus", type=int, default=None, help="override the config's k_plus (l)")
     ap.add_argument("--block", type=int, default=1,
                     help="block TRPL+K (options.block, NEXT-3): b vectors per SpMM in the inner loop")
@@ -360,7 +361,7 @@ def main():
     P = inputs.make(args.config, row_begin=rb, row_end=re)
     if args.k_plus is not None:
         P.l = args.k_plus
-    prec = 1 if args.precond == "none" else 0
+    prec = {"jacobi": 0, "none": 1, "shifted": 2, "ic0": 3}[args.precond]
     stream = torch.cuda.current_stream()
 
     def barrier():
@@ -500,8 +501,9 @@ def main():
                "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
                "scaling": "strong", "vs_baseline": None, "dtype": "f64",
                "data": "synthetic (seeded generator, BASELINE configs; paper matrices unavailable)",
-               "config": static_config(args.config, P, n, world, "no (M = I)" if prec else "Jacobi", args.comm,
-                                       args.block),
+               "config": static_config(args.config, P, n, world,
+                                       {0: "Jacobi", 1: "no (M = I)", 2: "per-cycle shifted Jacobi", 3: "IC(0)"}[prec],
+                                       args.comm, args.block),
                "solve": {"a_matvecs_per_solve": mv, "cycles": stats[-1]["cycles"],
                          "time_to_p_eigenpairs_ms": round(ms_per_step, 4),
                          "status": stats[-1]["status"]},

@@ -90,6 +90,10 @@ struct trplk_ctx {
            *bred_all = nullptr;
     unsigned* bcounter = nullptr;
     int blk_cols = 0;  // columns of wblk / xkb
+    // IC(0) (options.precond = 3): factor, forward-solve scratch, chunk flags
+    double *icL = nullptr, *ictmp = nullptr;
+    int* icflags = nullptr;
+    Ic0Args ic{};
     double* gridpart = nullptr;
     unsigned long long* gtrace = nullptr;  // TRPLK_GRID_TRACE: per-step phase timestamps
     cudaEvent_t ctev[2] = {nullptr, nullptr};  // TRPLK_CYCLE_TRACE
@@ -687,7 +691,7 @@ bool small_path(const trplk_ctx* ctx, const Sizes& S) {
         const char* e = getenv("TRPLK_NO_SMALL");
         v = (e && e[0] == '1') ? 0 : 1;
     }
-    return v == 1 && ctx->nranks == 1 && !ctx->hasB && ctx->n_loc <= SMALL_NMAX && S.q <= 24;
+    return v == 1 && ctx->nranks == 1 && !ctx->hasB && ctx->n_loc <= SMALL_NMAX && S.q <= 24 && S.prec != 3;
 }
 
 // Mid-size latency path: one cooperative grid-wide kernel runs all m steps (inner_grid.cuh) for
@@ -701,7 +705,8 @@ bool grid_path(const trplk_ctx* ctx, const Sizes& S) {
         env = (e && e[0] == '1') ? 1 : 0;
     }
     const bool on = ctx->grid_on < 0 ? env == 1 : ctx->grid_on == 1;
-    return on && !small_path(ctx, S) && ctx->nranks == 1 && !ctx->hasB && S.q <= 32 && ctx->gridpart != nullptr;
+    return on && !small_path(ctx, S) && ctx->nranks == 1 && !ctx->hasB && S.q <= 32 && ctx->gridpart != nullptr &&
+           S.prec != 3;
 }
 
 // One rank and B = I: the FINAL kernel is launched cooperatively and runs a third pass itself
@@ -878,6 +883,74 @@ trplk_status cgs2(trplk_ctx* ctx, const CgsSpec& c) {
     return TRPLK_OK;
 }
 
+// IC(0) (reading P2a): v <- (L L^T)^-1 v by the forward and the backward sync-free solve
+trplk_status ic0_apply(trplk_ctx* ctx, double* v, unsigned gate) {
+    Ic0Args f = ctx->ic;
+    f.v = v;
+    f.y = ctx->ictmp;
+    f.trans = 0;
+    f.ctl = ctx->ctl;
+    f.gate = gate;
+    launch_ic0_solve(f, ctx->stream);
+    Ic0Args b = f;
+    b.v = ctx->ictmp;
+    b.y = v;
+    b.trans = 1;
+    launch_ic0_solve(b, ctx->stream);
+    ctx->launches += 2;
+    ctx->model_bytes += 2.0 * (8.0 * ctx->n_loc * (ctx->ic.nlow + 1) + 2 * vec_bytes(ctx));
+    CK(cudaGetLastError());
+    return TRPLK_OK;
+}
+
+// the IC(0) factor of A - sigma I for this solve (buffers on first use)
+trplk_status ic0_setup(trplk_ctx* ctx) {
+    if (ctx->A.fmt != 1 || ctx->hasB || ctx->nranks > 1) {
+        ctx->err = "options.precond = 3 (IC(0)): DIA matrix, B = I and one rank on the device";
+        return TRPLK_EINVAL;
+    }
+    Ic0Args& a = ctx->ic;
+    a = Ic0Args{};
+    a.A = ctx->A;
+    a.sigma = ctx->sigma;
+    a.floor = ctx->mfloor;
+    a.n = ctx->n_loc;
+    a.ldl = ctx->ld;
+    int lo[DIA_MAX], ls[DIA_MAX], nl = 0;
+    for (int d = 0; d < ctx->A.ndiag; ++d)
+        if (ctx->A.offs[d] < 0) {
+            lo[nl] = ctx->A.offs[d];
+            ls[nl] = d;
+            ++nl;
+        }
+    for (int x = 1; x < nl; ++x)  // ascending offsets (the oracle's column order)
+        for (int y = x; y > 0 && lo[y - 1] > lo[y]; --y) {
+            std::swap(lo[y - 1], lo[y]);
+            std::swap(ls[y - 1], ls[y]);
+        }
+    a.nlow = nl;
+    for (int d = 0; d < nl; ++d) {
+        a.loff[d] = lo[d];
+        a.lslot[d] = ls[d];
+        for (int b = 0; b < DIA_MAX; ++b) a.pair[d][b] = -1;
+        for (int b = 0; b < d; ++b)
+            for (int e2 = 0; e2 < nl; ++e2)
+                if (lo[e2] == lo[b] - lo[d]) a.pair[d][b] = e2;
+    }
+    if (!ctx->icL) {
+        ST(dalloc(ctx, &ctx->icL, (size_t)ctx->ld * (DIA_MAX + 1)));
+        ST(dalloc(ctx, &ctx->ictmp, (size_t)ctx->ld));
+        ST(dalloc(ctx, &ctx->icflags, (size_t)(ctx->n_loc + 31) / 32 + 8));
+    }
+    a.L = ctx->icL;
+    a.flags = ctx->icflags;
+    a.ctl = nullptr;
+    launch_ic0_factor(a, ctx->stream);
+    ctx->launches += 1;
+    CK(cudaGetLastError());
+    return TRPLK_OK;
+}
+
 // r = A x - theta B x, u = M r, N_RES2 = ||r||^2  (Alg.1 steps 12/15)
 trplk_status residual(trplk_ctx* ctx, const double* x, int x_dyn, int theta_idx, double* uout, unsigned gate) {
     if (x_dyn == 0) ST(halo(ctx, x));
@@ -893,6 +966,7 @@ trplk_status residual(trplk_ctx* ctx, const double* x, int x_dyn, int theta_idx,
     a.theta_idx = theta_idx;
     a.gate = gate;
     ST(run_sdots(ctx, a, 0));
+    if (ctx->pmode == 3 && uout) ST(ic0_apply(ctx, uout, gate));  // u = (L L^T)^-1 r
     return TRPLK_OK;
 }
 
@@ -1237,9 +1311,10 @@ trplk_status issue_cycle(trplk_ctx* ctx, const Sizes& S, int cur, int nprev, int
         if (j < S.m) {
             a.out_mode = 2;  // w = M (z - rho B g)
             a.out = ctx->w;
+            const bool ic0 = ctx->pmode == 3;
             if (ctx->hasB) {
                 a.B = ctx->B;
-            } else {
+            } else if (!ic0) {
                 a.set2 = 2;  // h0 = U^T w
                 a.dest2 = D_H0 + 0;
                 a.norm1 = 1;  // ||w||^2
@@ -1248,6 +1323,7 @@ trplk_status issue_cycle(trplk_ctx* ctx, const Sizes& S, int cur, int nprev, int
             if (prof) CK(record_event(ctx, ctx->pev[0]));
             ST(run_sdots(ctx, a, k));
             if (prof) ctx->prof_kern[0] = g_last_kern;
+            if (ic0) ST(ic0_apply(ctx, ctx->w, F_CYCLE | F_INNER));  // w = (L L^T)^-1 (z - rho g)
             if (prof) CK(record_event(ctx, ctx->pev[1]));
             CgsSpec c{};
             if (prof) c.mark_final = ctx->pev[2];
@@ -1255,7 +1331,7 @@ trplk_status issue_cycle(trplk_ctx* ctx, const Sizes& S, int cur, int nprev, int
             c.V = Uc;
             c.kv = -1;
             c.k_nominal = k;
-            c.first_done = !ctx->hasB;
+            c.first_done = !ctx->hasB && ctx->pmode != 3;
             c.dest = Uc;
             c.dest_dyn = 1;
             c.gate = F_CYCLE | F_INNER;
@@ -1835,11 +1911,12 @@ static trplk_status solve_impl(trplk_ctx* ctx, int p, int q, int l, double tol, 
         ctx->err = "NULL output";
         return TRPLK_EINVAL;
     }
-    if (opt.precond < 0 || opt.precond > 2 || (opt.precond == 2 && opt.block > 1)) {
-        ctx->err = "options.precond must be 0 (Jacobi), 1 (none) or 2 (Jacobi of A - rho_i B; block = 1)";
+    if (opt.precond < 0 || opt.precond > 3 || (opt.precond >= 2 && opt.block > 1)) {
+        ctx->err = "options.precond must be 0 (Jacobi), 1 (none), 2 (Jacobi of A - rho_i B) or 3 (IC(0)); "
+                   "2 and 3 with block = 1";
         return TRPLK_EINVAL;
     }
-    ctx->mfloor_solve = opt.precond == 1 ? -1.0 : ctx->mfloor;
+    ctx->mfloor_solve = (opt.precond == 1 || opt.precond == 3) ? -1.0 : ctx->mfloor;  // IC(0): kernels apply I
     ctx->pmode = opt.precond;
     const int blk = opt.block > 1 ? opt.block : 1;
     if (blk > 1 && (blk > BC || ctx->hasB || ctx->nranks > 1)) {
@@ -1849,6 +1926,7 @@ static trplk_status solve_impl(trplk_ctx* ctx, int p, int q, int l, double tol, 
     const Sizes S{p, q, l, ph, m, opt.precond, blk};
     PhaseTimer pt("solve");
     ST(ensure_buffers(ctx, q, ph));
+    if (ctx->pmode == 3) ST(ic0_setup(ctx));
     if (!ctx->hasB && std::max(l <= BC ? l : 0, blk > 1 ? blk : 0) > 0)
         ST(ensure_block_buffers(ctx, std::max(l <= BC ? l : 0, blk > 1 ? blk : 0)));
     pt.mark("buffers");
@@ -1957,6 +2035,7 @@ static trplk_status solve_impl(trplk_ctx* ctx, int p, int q, int l, double tol, 
         a.nslot1 = N_RES2;
         a.theta_idx = 0;
         ST(run_sdots(ctx, a, 0));
+        if (ctx->pmode == 3) ST(ic0_apply(ctx, ctx->u, 0));
         if (ctx->hasB) ctx->b_mv++;
         ctx->prec++;
         // block (B1): seeds of targets 2 .. b_e from A X as well (no matvec)

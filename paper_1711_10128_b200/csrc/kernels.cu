@@ -909,6 +909,7 @@ __global__ void k_gather(const double* x, const int* idx, int64_t n, double* out
 #include "stream_tp.cuh"   // thread-per-row K1 / K2
 #include "rotate.cuh"      // shared-memory-staged DMMA rotation (default)
 #include "block.cuh"       // multi-vector Gram / update / SpMM (block +K)
+#include "ic0.cuh"         // IC(0) factor and sync-free triangular solves (NEXT-2)
 #include "k1_pipe.cuh"     // software-pipelined K1 (DIA, B = I, k <= 24)
 #include "small.cuh"       // single-CTA inner loop for small n (latency path)
 #include "inner_grid.cuh"  // cooperative grid-wide inner loop for mid-size n (latency path)

@@ -197,6 +197,27 @@ struct BlkArgs {
     double* red_local;
 };
 
+// IC(0) preconditioner (ic0.cuh)
+struct Ic0Args {
+    Sell A;                 // DIA (fmt 1)
+    double sigma, floor;    // K = A - sigma I; pivot floor eps_d max|K_jj|
+    double* L;              // [nlow + 1][ldl]: lower diagonals in A's offset order, then the diagonal
+    int64_t n, ldl;
+    int nlow;
+    int lslot[DIA_MAX];     // A's diagonal slot of lower diagonal a
+    int loff[DIA_MAX];      // its offset (< 0), ascending
+    int pair[DIA_MAX][DIA_MAX];  // factor: lower diagonal index of offset loff[b] - loff[a] (b < a), or -1
+    int* flags;             // per chunk done flag (zeroed before every launch); flags[nchunk] = ticket
+    const double* v;        // solve: right-hand side
+    double* y;              // solve: result
+    int trans;              // 0: L y = v, 1: L^T y = v
+    const Ctl* ctl;         // gate: the launch is a no-op unless (ctl->flags & gate) == gate
+    unsigned gate;
+};
+
+void launch_ic0_factor(const Ic0Args& a, cudaStream_t s);
+void launch_ic0_solve(const Ic0Args& a, cudaStream_t s);
+
 // Single-CTA inner loop of the small-n latency path (small.cuh)
 constexpr int SMALL_NMAX = 8192;  // rows handled by the small path (32 per thread)
 

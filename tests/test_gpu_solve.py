@@ -318,13 +318,15 @@ def test_graph_cache_across_contexts(gen):
 
 @pytest.mark.parametrize("name,N,l,pc", [("C2", 12, 0, 1), ("C2", 24, 0, 1), ("C4", 8, 0, 1), ("C1", None, 0, 1),
                                          ("C2", 16, 2, 1), ("C2", 16, 2, 2), ("C2", 24, 2, 2), ("C4", 8, 2, 2),
-                                         ("C5", 16, 2, 2)])
+                                         ("C5", 16, 2, 2), ("C2", 12, 2, 3), ("C2", 24, 2, 3), ("C3", 12, 3, 3),
+                                         ("C5", 20, 2, 3), ("C1", None, 1, 3), ("C2", 40, 2, 3)])
 def test_no_preconditioner_trlan_baseline(orc, gen, name, N, l, pc):
     """options.precond = 1 (M = I): with k_plus = 0 the thick-restart Lanczos baseline of eq 2.1
     (NEXT-4; the oracle pins its space per cycle in test_oracle_solver.py), the same parity as
     the preconditioned solve against the oracle run with precond = 1.  C1 (n = 1000) runs the
     single-CTA path, C2-24 the multi-kernel one, C4 the pencil.  pc = 2: the per-cycle shifted
-    Jacobi of NEXT-2 against the oracle's."""
+    Jacobi of NEXT-2 against the oracle's.  pc = 3: IC(0) of NEXT-2 (reading P2a; the
+    device factor and sync-free triangular solves against the oracle's row-order ones)."""
     torch, trplk = need_gpu()
     P = gen.make(name, N=N)
     P.l = l

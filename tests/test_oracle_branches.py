@@ -144,3 +144,33 @@ def test_inner_steps_entry_matches_bookkeeping(orc, gen):
     AU = P.A.to_scipy() @ U
     for j in range(k0 - 1, k0 + s - 1):  # columns k0-1 .. k0+s-2 had their T column filled
         assert np.max(np.abs(T[: j + 1, j] - U[:, : j + 1].T @ AU[:, j])) <= 1e-12
+
+
+@pytest.mark.parametrize("cfg,N", [("C2", 6), ("C4", 5), ("C3", 7)])
+def test_ic0_defining_property(orc, gen, cfg, N):
+    """NEXT-2, IC(0) of K = A - sigma B (reading P2a): L has K's lower pattern and (L L^T)_ij =
+    K_ij on that pattern -- the definition of the no-fill incomplete Cholesky factor; outside the
+    pattern L L^T carries the dropped fill."""
+    P = gen.make(cfg, N=N)
+    sigma = 0.7
+    L = orc.ic0(P.A, P.B, sigma)
+    A = P.A.to_scipy().toarray()
+    K = A - sigma * (np.eye(len(A)) if P.B is None else P.B.to_scipy().toarray())
+    Ld = L.toarray()
+    assert np.array_equal(Ld != 0, np.tril(A) != 0)
+    LL = Ld @ Ld.T
+    on = np.tril(A) != 0
+    assert np.max(np.abs(LL - K)[on]) <= 1e-13 * np.max(np.abs(K))
+
+
+def test_ic0_tridiagonal_is_cholesky_and_solve(orc, gen):
+    """For a tridiagonal matrix IC(0) drops nothing: L L^T = A (numpy Cholesky), and the IC(0)
+    preconditioned solve is exact -- the C1 oracle converges in a handful of cycles."""
+    P = gen.make("C1", N=60)
+    L = orc.ic0(P.A).toarray()
+    A = P.A.to_scipy().toarray()
+    assert np.max(np.abs(L - np.linalg.cholesky(A))) <= 1e-14
+    r = orc.solve(P.A, None, 3, 10, 1, 1e-10, precond=3)
+    assert r["status"] == "OK"
+    c = 2 - 2 * np.cos(np.arange(1, 4) * np.pi / 61)
+    assert np.max(np.abs(r["eigenvalues"] - c) / c) <= 1e-9

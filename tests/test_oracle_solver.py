@@ -421,3 +421,33 @@ def test_shifted_jacobi_per_cycle(orc, gen):
                 cols.append(d["X"][c - 1][:, :l])
             th = _rr_dense(A, B, np.hstack(cols), p)
             assert np.max(np.abs(th - r["log"]["thetas"][c][:p]) / np.abs(th)) <= 1e-10, (name, c)
+
+
+def test_ic0_preconditioned_space(orc, gen):
+    """NEXT-2, IC(0) (precond = 3, reading P2a): eq 3.2's space per cycle with M = (L L^T)^-1,
+    L = the oracle's IC(0) factor (pinned in test_oracle_branches.py), rebuilt densely, C2 and C4."""
+    for name in ("C2", "C4"):
+        P = gen.make(name, N=4)
+        A, B = _dense_pencil(P)
+        Bm = np.eye(A.shape[0]) if B is None else B
+        L = orc.ic0(P.A, P.B, 0.0).toarray()
+        Mfull = np.linalg.inv(L @ L.T)
+        p, m, l = 3, 3, 2
+        r = orc.solve(P.A, P.B, p, p + m + l, l, 1e-13, dump_cycles=6, max_cycles=6, precond=3)
+        d = r["dump"]
+        # the first 4 cycles: IC(0) converges fast, and once the residual is tiny the explicit
+        # power basis of the dense rebuild loses its conditioning (not the oracle's orthogonalised one)
+        for c in range(min(4, len(d["rho"]))):
+            if d["t"][c] != 1:
+                break
+            X, rho = d["X"][c], d["rho"][c]
+            C = (np.eye(len(A)) - X @ X.T @ Bm) @ (Mfull @ (A - rho * Bm))
+            cols = [X]
+            v = C @ X[:, 0]
+            for _ in range(m):
+                cols.append((v / np.linalg.norm(v))[:, None])
+                v = C @ cols[-1][:, 0]
+            if c > 0:
+                cols.append(d["X"][c - 1][:, :l])
+            th = _rr_dense(A, B, np.hstack(cols), p)
+            assert np.max(np.abs(th - r["log"]["thetas"][c][:p]) / np.abs(th)) <= 1e-10, (name, c)
