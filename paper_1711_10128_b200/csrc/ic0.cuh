@@ -19,11 +19,30 @@
 namespace trplk {
 
 
+// spin on a done-flag; a dependency that never completes (a scheduling bug) traps after ~10 s
+// instead of hanging the device
 __device__ __forceinline__ int ic0_chunk_wait(const int* flags, int64_t c) {
     if (c < 0) return 1;
     const volatile int* f = flags + c;
-    while (*f == 0) __nanosleep(64);
+    unsigned long long spins = 0;
+    while (*f == 0) {
+        __nanosleep(64);
+        if (++spins > (1ull << 27)) __trap();
+    }
     return 1;
+}
+
+// the warp waits for every chunk (other than its own) that one of its lanes depends on:
+// lane-specific chunk ids, deduplicated by a ballot loop; reverse = the chunks after c (L^T)
+__device__ __forceinline__ void ic0_wait_deps(const int* flags, int64_t c, int64_t dc, bool reverse, int64_t nchunk) {
+    const bool need = dc >= 0 && (reverse ? (dc > c && dc < nchunk) : dc < c);
+    unsigned m = __ballot_sync(0xffffffffu, need);
+    while (m) {
+        const int src = __ffs(m) - 1;
+        const int64_t w = __shfl_sync(0xffffffffu, dc, src);
+        if ((threadIdx.x & 31) == 0) ic0_chunk_wait(flags, w);
+        m &= ~__ballot_sync(0xffffffffu, need && dc == w);
+    }
 }
 
 // ----------------------------------------------------------------------------- factorization
@@ -39,13 +58,12 @@ __global__ void __launch_bounds__(256) k_ic0_factor(const Ic0Args a) {
         if (c >= nchunk) return;
         const int64_t r0 = c * 32, i = r0 + lane;
         const bool ok = i < a.n;
-        // dependencies on earlier chunks: rows i + o_a lie in chunks (r0 + o) >> 5 .. (r0 + 31 + o) >> 5
+        // dependencies on earlier chunks, only where the entry exists (K_ij != 0): a Dirichlet
+        // boundary row has no left neighbour, so a grid line does not wait for the previous one
         for (int d = 0; d < a.nlow; ++d) {
-            const int64_t lo = (r0 + a.loff[d]) >> 5, hi = (r0 + 31 + a.loff[d]) >> 5;
-            if (lane == 0) {
-                if (lo >= 0 && lo < c) ic0_chunk_wait(a.flags, lo);
-                if (hi >= 0 && hi < c && hi != lo) ic0_chunk_wait(a.flags, hi);
-            }
+            const int64_t j = i + a.loff[d];
+            const bool dep = ok && j >= 0 && __ldg(a.A.dval + (int64_t)a.lslot[d] * a.A.ldv + i) != 0.0;
+            ic0_wait_deps(a.flags, c, dep ? (j >> 5) : -1, false, (int64_t)0);
         }
         __syncwarp();
         __threadfence();
@@ -110,17 +128,15 @@ __global__ void __launch_bounds__(256) k_ic0_solve(const Ic0Args a) {
         const int64_t c = a.trans ? nchunk - 1 - t : t;
         const int64_t r0 = c * 32, i = r0 + lane;
         const bool ok = i < a.n;
-        for (int d = 0; d < a.nlow; ++d) {
-            const int64_t o = a.trans ? -a.loff[d] : a.loff[d];
-            const int64_t lo = (r0 + o) >> 5, hi = (r0 + 31 + o) >> 5;
-            if (lane == 0) {
-                if (!a.trans) {
-                    if (lo >= 0 && lo < c) ic0_chunk_wait(a.flags, lo);
-                    if (hi >= 0 && hi < c && hi != lo) ic0_chunk_wait(a.flags, hi);
-                } else {
-                    if (lo > c && lo < nchunk) ic0_chunk_wait(a.flags, lo);
-                    if (hi > c && hi < nchunk && hi != lo) ic0_chunk_wait(a.flags, hi);
-                }
+        for (int d = 0; d < a.nlow; ++d) {  // only the entries of L that exist (L != 0)
+            if (!a.trans) {
+                const int64_t j = i + a.loff[d];
+                const bool dep = ok && j >= 0 && __ldg(a.L + (int64_t)d * a.ldl + i) != 0.0;
+                ic0_wait_deps(a.flags, c, dep ? (j >> 5) : -1, false, nchunk);
+            } else {
+                const int64_t k = i - a.loff[d];
+                const bool dep = ok && k < a.n && __ldg(a.L + (int64_t)d * a.ldl + k) != 0.0;
+                ic0_wait_deps(a.flags, c, dep ? (k >> 5) : -1, true, nchunk);
             }
         }
         __syncwarp();
@@ -134,6 +150,7 @@ __global__ void __launch_bounds__(256) k_ic0_solve(const Ic0Args a) {
                 const int64_t j = i + a.loff[d];
                 if (!ok || j < 0) continue;
                 const double lij = __ldg(a.L + (int64_t)d * a.ldl + i);
+                if (lij == 0.0) continue;  // no entry: y_j was not waited for
                 if (j >= r0) {  // inside this chunk
                     if (d == dm1 && !seq) bcoef = lij;
                     continue;
@@ -145,6 +162,7 @@ __global__ void __launch_bounds__(256) k_ic0_solve(const Ic0Args a) {
                 const int64_t k = i - a.loff[d];
                 if (!ok || k >= a.n) continue;
                 const double lki = __ldg(a.L + (int64_t)d * a.ldl + k);
+                if (lki == 0.0) continue;
                 if (k < r0 + 32) {
                     if (d == dm1 && !seq) bcoef = lki;
                     continue;
@@ -176,10 +194,16 @@ __global__ void __launch_bounds__(256) k_ic0_solve(const Ic0Args a) {
                     for (int d = 0; d < a.nlow; ++d) {
                         if (!a.trans) {
                             const int64_t j = i + a.loff[d];
-                            if (j >= r0 && j >= 0) ss -= __ldg(a.L + (int64_t)d * a.ldl + i) * __ldcg(a.y + j);
+                            if (j >= r0 && j >= 0) {
+                                const double lij = __ldg(a.L + (int64_t)d * a.ldl + i);
+                                if (lij != 0.0) ss -= lij * __ldcg(a.y + j);
+                            }
                         } else {
                             const int64_t k = i - a.loff[d];
-                            if (k < r0 + 32 && k < a.n) ss -= __ldg(a.L + (int64_t)d * a.ldl + k) * __ldcg(a.y + k);
+                            if (k < r0 + 32 && k < a.n) {
+                                const double lki = __ldg(a.L + (int64_t)d * a.ldl + k);
+                                if (lki != 0.0) ss -= lki * __ldcg(a.y + k);
+                            }
                         }
                     }
                     a.y[i] = ss / lii;
