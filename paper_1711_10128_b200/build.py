@@ -41,20 +41,36 @@ def needs_build() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
+    """One nvcc process per translation unit (in parallel; kernels.cu dominates), then one link."""
     if not force and not needs_build():
         return LIB
+    from concurrent.futures import ThreadPoolExecutor
     os.makedirs(LIBDIR, exist_ok=True)
     inc, libd = _nccl_dirs()
     cus = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
-    cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC,-fopenmp",
-           "-Xptxas", "-v" if verbose else "-O3", "-I", INCLUDE, "-I", CSRC, "-I", inc, *cus,
-           "-o", LIB + ".tmp", "-L", libd, "-l:libnccl.so.2", "-Xlinker", f"-rpath,{libd}", "-lgomp"]
+    objdir = os.path.join(LIBDIR, "obj")
+    os.makedirs(objdir, exist_ok=True)
+    common = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-fopenmp",
+              "-Xptxas", "-v" if verbose else "-O3", "-I", INCLUDE, "-I", CSRC, "-I", inc]
+
+    def compile_one(cu):
+        obj = os.path.join(objdir, os.path.basename(cu) + ".o")
+        return subprocess.run(common + ["-c", cu, "-o", obj], capture_output=True, text=True), obj
+
+    with ThreadPoolExecutor(max_workers=len(cus)) as ex:
+        results = list(ex.map(compile_one, cus))
+    for r, _ in results:
+        if r.returncode != 0:
+            sys.stderr.write(r.stdout + r.stderr)
+            raise RuntimeError("nvcc failed building libtrplk.so")
+        if verbose:
+            sys.stderr.write(r.stderr)
+    cmd = [NVCC, *ARCH, "-shared", "-Xcompiler", "-fPIC,-fopenmp", *[o for _, o in results], "-o", LIB + ".tmp",
+           "-L", libd, "-l:libnccl.so.2", "-Xlinker", f"-rpath,{libd}", "-lgomp"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
-        raise RuntimeError("nvcc failed building libtrplk.so")
-    if verbose:
-        sys.stderr.write(r.stderr)
+        raise RuntimeError("nvcc failed linking libtrplk.so")
     os.replace(LIB + ".tmp", LIB)
     return LIB
 

@@ -43,12 +43,14 @@ __global__ void __launch_bounds__(CTA, 2) k_step1_pipe(const SdotsArgs a) {
     const int64_t stride = (int64_t)gridDim.x * WARPS;
     // registers of the tile in flight: basis row, DIA values, gathered x, diagonal, own x
     double ur[KMAX], v[8], xv[8], dg = 0.0, xr = 0.0;
+    unsigned pm = 0;  // DIA-C presence word of the tile's row (constant diagonals are decoded at use)
     auto issue = [&](int64_t sl) {
         const int64_t row = sl * 32 + lane;
         const bool ok = sl < nslices && row < a.nrows;
 #pragma unroll
         for (int c = 0; c < KMAX; ++c) ur[c] = (ok && c < kmx) ? __ldg(a.U + (int64_t)c * a.ldu + row) : 0.0;
         const double* dv = M.dval + row;
+        pm = (ok && M.cmask) ? dia_pmask(M, row) : 0u;
 #pragma unroll
         for (int d = 0; d < 8; ++d) {
             v[d] = 0.0;
@@ -57,11 +59,11 @@ __global__ void __launch_bounds__(CTA, 2) k_step1_pipe(const SdotsArgs a) {
                 int idx = (int)row + M.offs[d];
                 if (halo) idx = idx < 0 ? idx + nl + glo : (idx >= nl ? idx + glo : idx);
                 idx = idx < 0 ? 0 : (idx > top ? top : idx);
-                v[d] = __ldg(dv + (int64_t)d * M.ldv);
+                if (!((M.cmask >> d) & 1u)) v[d] = __ldg(dv + (int64_t)d * M.ldv);
                 xv[d] = __ldg(X + idx);
             }
         }
-        dg = ok ? __ldg(dv + (int64_t)M.diag_slot * M.ldv) : 1.0;
+        dg = (ok && !((M.cmask >> M.diag_slot) & 1u)) ? __ldg(dv + (int64_t)M.diag_slot * M.ldv) : 1.0;
         xr = ok ? X[row] : 0.0;
     };
     int64_t sl = (int64_t)blockIdx.x * WARPS + warp;
@@ -71,6 +73,12 @@ __global__ void __launch_bounds__(CTA, 2) k_step1_pipe(const SdotsArgs a) {
         const bool ok = row < a.nrows;
         // SpMV of this tile (ascending column order, as mat_row)
         double z = 0.0;
+        if (M.cmask) {
+#pragma unroll
+            for (int d = 0; d < 8; ++d)
+                if (d < nd && ((M.cmask >> d) & 1u)) v[d] = ((pm >> d) & 1u) ? __ldg(M.cval + d) : 0.0;
+            if (ok && ((M.cmask >> M.diag_slot) & 1u)) dg = ((pm >> M.diag_slot) & 1u) ? __ldg(M.cval + M.diag_slot) : 0.0;
+        }
 #pragma unroll
         for (int d = 0; d < 8; ++d) z = fma(v[d], xv[d], z);
         double o = 0.0;

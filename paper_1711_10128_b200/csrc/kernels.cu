@@ -70,7 +70,8 @@ __device__ __forceinline__ double mat_row(const Sell& M, int64_t s, int lane, co
         const int nl = (int)M.nrows, top = (int)(M.nrows + M.nghost - 1), glo = (int)M.glo;
         const bool halo = M.nghost != 0;
         const double* dv = M.dval + row;
-        diag = __ldg(dv + (int64_t)M.diag_slot * M.ldv);
+        const unsigned pm = M.cmask ? dia_pmask(M, row) : 0u;
+        diag = dia_val(M, M.diag_slot, pm, dv);
         for (int d0 = 0; d0 < M.ndiag; d0 += 8) {
             double v[8], xv[8];
 #pragma unroll
@@ -82,7 +83,7 @@ __device__ __forceinline__ double mat_row(const Sell& M, int64_t s, int lane, co
                     int idx = (int)row + M.offs[d];  // local rows + ghosts < 2^31 (checked at create)
                     if (halo) idx = idx < 0 ? idx + nl + glo : (idx >= nl ? idx + glo : idx);
                     idx = idx < 0 ? 0 : (idx > top ? top : idx);  // out-of-matrix slots hold 0
-                    v[u] = __ldg(dv + (int64_t)d * M.ldv);
+                    v[u] = dia_val(M, d, pm, dv);
                     xv[u] = XNC ? __ldg(x + idx) : __ldcg(x + idx);
                 }
             }
@@ -116,7 +117,10 @@ __device__ __forceinline__ double mat_row(const Sell& M, int64_t s, int lane, co
 
 // Diagonal entry of row 32 s + lane (DIA: the offset-0 array; SELL: slot 0).
 __device__ __forceinline__ double mat_diag(const Sell& M, int64_t s, int lane) {
-    if (M.fmt == 1) return __ldg(M.dval + (int64_t)M.diag_slot * M.ldv + s * 32 + lane);
+    if (M.fmt == 1) {
+        const int64_t row = s * 32 + lane;
+        return dia_val(M, M.diag_slot, M.cmask ? dia_pmask(M, row) : 0u, M.dval + row);
+    }
     return __ldg(M.val + __ldg(M.sptr + s) + lane);
 }
 
@@ -1162,6 +1166,66 @@ void launch_csr_to_dia(const int64_t* rp, const int64_t* ci, const double* va, i
     if (g > 148 * 16) g = 148 * 16;
     if (g < 1) g = 1;
     k_csr_to_dia<<<(int)g, 256, 0, s>>>(rp, ci, va, nrows, row0, o, nd, ldv, dval);
+}
+
+// DIA-C detection: per diagonal, the min and max bit pattern of its stored (non-+0.0) entries.
+__global__ void k_dia_const_scan(const double* __restrict__ dval, int64_t nrows, int64_t ldv, int nd,
+                                 unsigned long long* __restrict__ mnmx) {
+    const int d = blockIdx.y;
+    unsigned long long mn = ~0ull, mx = 0ull;
+    const unsigned long long* v = reinterpret_cast<const unsigned long long*>(dval + (int64_t)d * ldv);
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < nrows; r += (int64_t)gridDim.x * blockDim.x) {
+        const unsigned long long b = __ldg(v + r);
+        if (b != 0ull) {
+            mn = b < mn ? b : mn;
+            mx = b > mx ? b : mx;
+        }
+    }
+    for (int o = 16; o >= 1; o >>= 1) {
+        const unsigned long long a = __shfl_xor_sync(0xffffffffu, mn, o), b = __shfl_xor_sync(0xffffffffu, mx, o);
+        mn = a < mn ? a : mn;
+        mx = b > mx ? b : mx;
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicMin(mnmx + 2 * d, mn);
+        atomicMax(mnmx + 2 * d + 1, mx);
+    }
+}
+
+// DIA-C presence words: bit d of row r = stored entry of constant diagonal d (rows >= nrows: 0).
+template <typename T>
+__global__ void k_dia_pmask(const double* __restrict__ dval, int64_t nrows, int64_t ldv, int nd, unsigned cmask,
+                            T* __restrict__ pm) {
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < ldv; r += (int64_t)gridDim.x * blockDim.x) {
+        unsigned m = 0;
+        if (r < nrows)
+            for (int d = 0; d < nd; ++d)
+                if (((cmask >> d) & 1u) &&
+                    __double_as_longlong(__ldg(dval + (int64_t)d * ldv + r)) != 0ll)
+                    m |= 1u << d;
+        pm[r] = (T)m;
+    }
+}
+
+void launch_dia_const_scan(const double* dval, int64_t nrows, int64_t ldv, int nd, unsigned long long* mnmx,
+                           cudaStream_t s) {
+    int64_t g = (nrows + 255) / 256;
+    if (g > 148 * 4) g = 148 * 4;
+    if (g < 1) g = 1;
+    k_dia_const_scan<<<dim3((unsigned)g, (unsigned)nd), 256, 0, s>>>(dval, nrows, ldv, nd, mnmx);
+}
+
+void launch_dia_pmask(const double* dval, int64_t nrows, int64_t ldv, int nd, unsigned cmask, int mbytes,
+                      void* pm, cudaStream_t s) {
+    int64_t g = (ldv + 255) / 256;
+    if (g > 148 * 16) g = 148 * 16;
+    if (g < 1) g = 1;
+    if (mbytes == 1)
+        k_dia_pmask<unsigned char><<<(int)g, 256, 0, s>>>(dval, nrows, ldv, nd, cmask, static_cast<unsigned char*>(pm));
+    else if (mbytes == 2)
+        k_dia_pmask<unsigned short><<<(int)g, 256, 0, s>>>(dval, nrows, ldv, nd, cmask, static_cast<unsigned short*>(pm));
+    else
+        k_dia_pmask<unsigned><<<(int)g, 256, 0, s>>>(dval, nrows, ldv, nd, cmask, static_cast<unsigned*>(pm));
 }
 
 void launch_gather(const double* x, const int* idx, int64_t n, double* out, cudaStream_t s) {

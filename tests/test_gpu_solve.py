@@ -366,3 +366,37 @@ def test_block_trplk_parity(orc, gen, name, N, b, over):
     check_parity(g, o, P, allow_tie_divergence=(name == "C3"))
     X = g["X"]
     assert np.max(np.abs(X.T @ X - np.eye(P.p))) <= 1e-10
+
+
+@pytest.mark.parametrize("name,N", [("C2", 16), ("C3", 12), ("C4", 8), ("C5", 20), ("C1", None)])
+def test_dia_constant_diagonals_bitwise(gen, name, N):
+    """DIA-C (constant diagonals read as a presence bit + the constant, trplk_internal.cuh Sell):
+    the decoded values are the stored ones bit for bit, so a solve with DIA-C is bitwise the
+    solve with every diagonal stored (TRPLK_DIAC=0) -- eigenvalues, eigenvectors, residuals and
+    matvec count -- and reads fewer matrix bytes (C2/C5: the six -1 couplings; C3: all seven
+    diagonals; C4: A's 26 couplings and all of B)."""
+    import os
+    torch, trplk = need_gpu()
+    P = gen.make(name, N=N)
+    out = {}
+    for v in ("0", "1"):
+        os.environ["TRPLK_DIAC"] = v
+        try:
+            ctx = trplk.trplk_create(P.A, P.B, P.sigma)
+        finally:
+            os.environ.pop("TRPLK_DIAC", None)
+        info = trplk.trplk_info(ctx)
+        ev, X, rs, st = trplk.trplk_solve(ctx, P.p, P.q, P.l, P.tol, use_graphs=0)
+        out[v] = (ev, X.cpu().numpy().copy(), rs, st["a_matvecs"], info)
+        ctx.close()
+    (e0, X0, r0, m0, i0), (e1, X1, r1, m1, i1) = out["0"], out["1"]
+    assert np.array_equal(e0, e1) and np.array_equal(X0, X1) and np.array_equal(r0, r1) and m0 == m1
+    n = P.A.n
+    if name == "C1":  # tridiag(-1, 2, -1): every diagonal constant, 1 byte of presence bits per row
+        assert i1["sell_bytes_a"] == n and i0["sell_bytes_a"] == 24 * n
+    elif name == "C3":
+        assert i1["sell_bytes_a"] == n and i0["sell_bytes_a"] == 56 * n
+    elif name == "C4":
+        assert i1["sell_bytes_a"] == 8 * n + 4 * n and i1["sell_bytes_b"] == n
+    else:
+        assert i1["sell_bytes_a"] == 8 * n + n and i0["sell_bytes_a"] == 56 * n

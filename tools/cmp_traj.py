@@ -4,7 +4,9 @@ sys.path.insert(0, "."); sys.path.insert(0, "./tests")
 from paper_1711_10128_b200 import build, inputs, trplk
 import oracle; oracle.build()
 build.build()
-P = inputs.make("C2", N=24, q=22)
+N = int(sys.argv[1]) if len(sys.argv) > 1 else 24
+q = int(sys.argv[2]) if len(sys.argv) > 2 else 22
+P = inputs.make("C2", N=N, q=q)
 o = oracle.solve(P.A, P.B, P.p, P.q, P.l, P.tol, P.sigma, want_vectors=False)
 lo = o["log"]
 for dbg in (0, 2):
@@ -17,4 +19,10 @@ for dbg in (0, 2):
     first = next((c for c in range(n) if lg["t"][c] != lo["t"][c] or lg["k"][c] != lo["k"][c]), None)
     print("debug", dbg, "matvecs", st["a_matvecs"], o["a_matvecs"], "cycles", len(lg["t"]), len(lo["t"]),
           "first struct div", first, "max rel theta diff", max(rel), "at", int(np.argmax(rel)))
+    if first is not None:
+        for c in range(max(0, first - 2), min(n, first + 2)):
+            th = lo["thetas"][c]
+            gap = float(np.min(np.abs(np.diff(th)) / np.abs(th[1:])))
+            print("  cycle", c, "gpu t,k,res", lg["t"][c], lg["k"][c], lg["res"][c], "oracle", lo["t"][c], lo["k"][c],
+                  lo["res"][c], "tol", P.tol, "min rel Ritz gap", gap)
     ctx.close()
