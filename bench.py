@@ -418,6 +418,9 @@ def main():
     # roofline: inner-step kernel group with the largest share (live CUDA events, per launch)
     groups = ["K1 (SpMV + Jacobi + T-column / h1 dots)", "K2 (CGS pass 2: update + dots)",
               "K3 (CGS final update + normalisation)"]
+    if kern_names and "k_fin_step1" in kern_names[0]:  # fused step: [K3 of step j + K1 of step j+1, K2, -]
+        groups = ["K3+K1 (CGS final update of step j + SpMV/Jacobi/T-column/h1 dots of step j+1)",
+                  "K2 (CGS pass 2: update + dots)", "-"]
     peak, peak_src = peaks()
     cnt = max(prof["count"], 1)
     per_ms = prof["ms"] / cnt

@@ -95,6 +95,10 @@ struct trplk_ctx {
     int* icflags = nullptr;
     Ic0Args ic{};
     double* gridpart = nullptr;
+    unsigned* rcnt = nullptr;  // fused K3 + K1 (fused.cuh): per-round completion counters
+    int64_t rcnt_cap = 0;
+    bool prof_fused = false;   // the live profile's slots are [K3 + K1 fused, K2, -]
+    bool fuse_on = true;       // TRPLK_FUSE=0 at create: the three-kernel inner step
     unsigned long long* gtrace = nullptr;  // TRPLK_GRID_TRACE: per-step phase timestamps
     cudaEvent_t ctev[2] = {nullptr, nullptr};  // TRPLK_CYCLE_TRACE
     double ctrace_busy = 0.0;
@@ -791,6 +795,36 @@ static cudaError_t record_event(trplk_ctx* ctx, cudaEvent_t ev) {
                                                : cudaEventRecord(ev, ctx->stream);
 }
 
+// K3 of inner step j + K1 of step j+1 as one kernel (fused.cuh): one rank, B = I, a DIA matrix
+// of <= 8 diagonals, Jacobi / none / shifted preconditioner, the multi-kernel inner step (not the
+// latency paths).  TRPLK_FUSE=0 keeps the three-kernel step; TRPLK_FUSE_SLACK = rounds of slack
+// between a tile's stencil reach and its K1 (default 1).
+bool fuse_path(const trplk_ctx* ctx, const Sizes& S) {
+    return ctx->fuse_on && ctx->nranks == 1 && !ctx->hasB && ctx->A.fmt == 1 && ctx->A.ndiag <= 8 && ctx->rcnt &&
+           S.prec != 3 && S.q <= 48 && !small_path(ctx, S) && !grid_path(ctx, S);
+}
+
+bool run_fused(trplk_ctx* ctx, const UpdArgs& u, const SdotsArgs& a, int kn, int k_next) {
+    static int slack = -1;
+    if (slack < 0) {
+        const char* sl = getenv("TRPLK_FUSE_SLACK");
+        slack = sl ? std::max(0, atoi(sl)) : 1;
+    }
+    if (u.dest2 || !u.dest_dyn || u.mode != 2) return false;
+    FusedArgs f{};
+    f.u = u;
+    f.a = a;
+    f.rcnt = ctx->rcnt;
+    f.rcnt_cap = ctx->rcnt_cap;
+    int maxoff = 0;
+    for (int d = 0; d < ctx->A.ndiag; ++d) maxoff = std::max(maxoff, std::abs(ctx->A.offs[d]));
+    if (!launch_fin_step1(f, kmax_bucket(std::max(k_next, 1)), maxoff, slack, ctx->stream)) return false;
+    // bytes: FINAL (U(:, 1:kn), w', g) + the K1 without its U / g re-reads (L2): A, w
+    ctx->model_bytes += vec_bytes(ctx) * (kn + 2) + mat_bytes(ctx, false) + (a.out ? vec_bytes(ctx) : 0.0);
+    ctx->launches += 1;
+    return true;
+}
+
 // CGS2 in the B-inner product (R3) of x against V = Ubase(:, 0:kv) (kv = -1: ctl->k), result
 // normalised into Ubase(:, ctl->k) (dest_dyn) or `dest`, ctl->k += 1 on success.
 struct CgsSpec {
@@ -807,6 +841,8 @@ struct CgsSpec {
     unsigned gate, clear;
     int inc_k;
     cudaEvent_t mark_final = nullptr;  // profiling: recorded just before the FINAL update
+    const SdotsArgs* fuse_next = nullptr;  // FINAL fused with this K1 of the next inner step (fused.cuh)
+    int k_next = 0;                        // its nominal basis width
 };
 
 trplk_status cgs2(trplk_ctx* ctx, const CgsSpec& c) {
@@ -891,6 +927,10 @@ trplk_status cgs2(trplk_ctx* ctx, const CgsSpec& c) {
         u.clear_on_brk = c.clear;
         u.force3 = ctx->force3;
         u.coop = coop3(ctx);
+        if (c.fuse_next && run_fused(ctx, u, *c.fuse_next, kn, c.k_next)) {
+            if (c.mark_final) ctx->prof_kern[0] = g_last_kern;
+            return TRPLK_OK;
+        }
         ST(run_upd(ctx, u, kn));
         if (c.mark_final) ctx->prof_kern[2] = g_last_kern;
         if (u.coop) return TRPLK_OK;  // the third pass, when needed, ran inside the FINAL kernel
@@ -1348,14 +1388,13 @@ trplk_status issue_cycle(trplk_ctx* ctx, const Sizes& S, int cur, int nprev, int
             if (j < S.m) ctx->model_bytes += 2 * vec_bytes(ctx) * (k + 2);
         }
     }
-    for (int j = 1; j <= S.m && !fused; ++j) {
-        const int k = S.ph + j;  // nominal width incl. g_j
-        const bool prof = ctx->prof_on && j == jmid && j < S.m;
-        const double* g = Uc + ld * (k - 1);
-        ST(halo(ctx, g));
+    // K1 arguments of inner step j (eq 3.1: z = A g_j, T(1:k,k) = U^T z, w = M (z - rho B g_j),
+    // h0 = U^T w, ||w||^2)
+    auto k1_args = [&](int j) {
+        const int k = S.ph + j;
         SdotsArgs a = sd_base(ctx);
         a.A = ctx->A;
-        a.x = g;
+        a.x = Uc + ld * (k - 1);
         a.U = Uc;
         a.k_from_ctl = 1;
         a.set1 = 1;  // T(1:k,k) = U^T z
@@ -1364,22 +1403,42 @@ trplk_status issue_cycle(trplk_ctx* ctx, const Sizes& S, int cur, int nprev, int
         if (j < S.m) {
             a.out_mode = 2;  // w = M (z - rho B g)
             a.out = ctx->w;
-            const bool ic0 = ctx->pmode == 3;
             if (ctx->hasB) {
                 a.B = ctx->B;
-            } else if (!ic0) {
+            } else if (ctx->pmode != 3) {
                 a.set2 = 2;  // h0 = U^T w
                 a.dest2 = D_H0 + 0;
                 a.norm1 = 1;  // ||w||^2
                 a.nslot1 = N_IN2;
             }
-            if (prof) CK(record_event(ctx, ctx->pev[0]));
-            ST(run_sdots(ctx, a, k));
-            if (prof) ctx->prof_kern[0] = g_last_kern;
+        }
+        return a;
+    };
+    // fz: the FINAL of step j and the K1 of step j+1 run as one kernel (fused.cuh)
+    const bool fz = !fused && fuse_path(ctx, S);
+    ctx->prof_fused = fz;
+    for (int j = 1; j <= S.m && !fused; ++j) {
+        const int k = S.ph + j;  // nominal width incl. g_j
+        const bool prof = ctx->prof_on && j == jmid && j < S.m;
+        const double* g = Uc + ld * (k - 1);
+        ST(halo(ctx, g));
+        SdotsArgs a = k1_args(j);
+        const bool k1_done = fz && j > 1;  // ran inside the previous step's fused kernel
+        if (j < S.m) {
+            const bool ic0 = ctx->pmode == 3;
+            if (prof && !fz) CK(record_event(ctx, ctx->pev[0]));
+            if (!k1_done) ST(run_sdots(ctx, a, k));
+            if (prof && !fz) ctx->prof_kern[0] = g_last_kern;
             if (ic0) ST(ic0_apply(ctx, ctx->w, F_CYCLE | F_INNER));  // w = (L L^T)^-1 (z - rho g)
-            if (prof) CK(record_event(ctx, ctx->pev[1]));
+            if (prof) CK(record_event(ctx, ctx->pev[fz ? 0 : 1]));
             CgsSpec c{};
-            if (prof) c.mark_final = ctx->pev[2];
+            SdotsArgs an{};
+            if (fz) {
+                an = k1_args(j + 1);
+                c.fuse_next = &an;
+                c.k_next = k + 1;
+            }
+            if (prof) c.mark_final = ctx->pev[fz ? 1 : 2];
             c.x = ctx->w;
             c.V = Uc;
             c.kv = -1;
@@ -1391,8 +1450,11 @@ trplk_status issue_cycle(trplk_ctx* ctx, const Sizes& S, int cur, int nprev, int
             c.clear = F_INNER;
             c.inc_k = 1;
             ST(cgs2(ctx, c));
-            if (prof) CK(record_event(ctx, ctx->pev[3]));
-        } else {
+            if (prof) {
+                CK(record_event(ctx, ctx->pev[fz ? 2 : 3]));
+                if (fz) CK(record_event(ctx, ctx->pev[3]));
+            }
+        } else if (!k1_done) {
             ST(run_sdots(ctx, a, k));
         }
     }
@@ -1748,6 +1810,15 @@ static trplk_status create_impl(trplk_ctx* ctx, int64_t n_global, const int64_t*
     CK(cudaMemsetAsync(ctx->bcounter, 0, sizeof(unsigned) * NCOUNTERS, ctx->stream));
     CK(cudaMemsetAsync(ctx->blk, 0, sizeof(BlkCtl), ctx->stream));
     if (ctx->nranks == 1 && !ctx->hasB) ST(dalloc(ctx, &ctx->gridpart, (size_t)2 * GRID_MAXCTA * GRID_NVP));
+    {
+        const char* e = getenv("TRPLK_FUSE");
+        ctx->fuse_on = !(e && e[0] == '0');
+    }
+    if (ctx->nranks == 1 && !ctx->hasB && ctx->A.fmt == 1) {
+        ctx->rcnt_cap = (ctx->n_loc + 31) / 32 / (148 * WARPS) + 64;
+        ST(dalloc(ctx, &ctx->rcnt, (size_t)ctx->rcnt_cap));
+        CK(cudaMemsetAsync(ctx->rcnt, 0, sizeof(unsigned) * ctx->rcnt_cap, ctx->stream));
+    }
     ST(dalloc(ctx, &ctx->ctl, 1));
     CK(cudaMemsetAsync(ctx->counter, 0, sizeof(unsigned) * NCOUNTERS, ctx->stream));
     CK(cudaMemsetAsync(ctx->ctl, 0, sizeof(Ctl), ctx->stream));
@@ -2200,6 +2271,17 @@ static trplk_status solve_impl(trplk_ctx* ctx, int p, int q, int l, double tol, 
                     }
                     const double b3 = 8.0 * n * (k + 2);  // U, w', g_{j+1}
                     double bb[3] = {b1, b2, b3};
+                    if (ctx->prof_fused) {
+                        // slots [K3 of step jmid + K1 of step jmid+1, K2, -]: the fused kernel moves the
+                        // FINAL's bytes and the K1's A and w (its U and g re-reads come from L2)
+                        const float ek2 = e[0];
+                        e[0] = e[1];
+                        e[1] = ek2;
+                        e[2] = 0.0f;
+                        bb[0] = b3 + spA + 8.0 * n;
+                        bb[1] = b2;
+                        bb[2] = 0.0;
+                    }
                     if (fused) {  // one launch for all G steps: its time, the bytes of all G steps
                         double tot = 0.0;
                         for (int j = 1; j <= G; ++j) {
@@ -2997,7 +3079,8 @@ trplk_status trplk_profile_kernels(const trplk_ctx* ctx, char* buf, size_t len) 
     std::string out;
     for (int i = 0; i < 3; ++i) {
         const char* name = nullptr;
-        if (ctx->prof_kern[i] && cudaFuncGetName(&name, ctx->prof_kern[i]) != cudaSuccess) name = nullptr;
+        const void* kf = (ctx->prof_fused && i == 2) ? nullptr : ctx->prof_kern[i];  // fused: no third group
+        if (kf && cudaFuncGetName(&name, kf) != cudaSuccess) name = nullptr;
         std::string nm = name ? name : "";
         if (name) {
             int stt = 0;

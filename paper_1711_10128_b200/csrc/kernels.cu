@@ -918,6 +918,7 @@ __global__ void k_gather(const double* x, const int* idx, int64_t n, double* out
 #include "small.cuh"       // single-CTA inner loop for small n (latency path)
 #include "inner_grid.cuh"  // cooperative grid-wide inner loop for mid-size n (latency path)
 #include "pl1.cuh"         // PL+1 (Algorithm 2) small kernels
+#include "fused.cuh"       // K3 of step j + K1 of step j+1 in one kernel (lagged rounds)
 
 namespace trplk {
 

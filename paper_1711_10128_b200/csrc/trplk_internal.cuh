@@ -164,6 +164,17 @@ struct UpdArgs {
     int force3; // debug: take the third CGS pass unconditionally (tests of the pass-3 path)
 };
 
+// K3 of inner step j fused with K1 of step j + 1 (fused.cuh): FINAL update args, K1 args, the
+// per-round completion counters (zero between launches) and the round lag (set at launch).
+struct FusedArgs {
+    UpdArgs u;
+    SdotsArgs a;
+    unsigned* rcnt;
+    int64_t rcnt_cap;
+    int dn, lag;  // rounds a tile's stencil reaches past its own; rounds between FINAL and K1
+};
+bool launch_fin_step1(const FusedArgs& f, int kmax, int maxoff, int slack, cudaStream_t s);
+
 // ------------------------------------------------------------- block kernels (block.cuh)
 constexpr int BC = 8;                                // vectors per block launch (DMMA n = 8)
 constexpr int BLK_NV = 2 * QMAX * BC + BC * BC;      // reduction values of one block launch

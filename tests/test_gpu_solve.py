@@ -199,7 +199,7 @@ def test_full_C2_parity(orc, gen):
     check_parity(g, o, P, allow_tie_divergence=True)
 
 
-@pytest.mark.parametrize("name,N", [("C2", 12), ("C4", 8)])
+@pytest.mark.parametrize("name,N", [("C2", 12), ("C4", 8), ("C2", 24), ("C5", 24)])
 def test_solve_with_forced_third_pass(orc, gen, name, N):
     """Every CGS2 of the solve takes the third pass (options.debug_checks bit 1): the same
     trajectory as the oracle's two-pass run (the third projection is rounding-level), so the
