@@ -351,8 +351,12 @@ __global__ void __launch_bounds__(EIG1_THREADS) k_eig(Ctl* ctl, double* T, int l
             for (int idx = tid; idx < k * k; idx += EIG1_THREADS) {
                 const int pr = idx % k, qr = idx / k;
                 if (pr < qr) {
-                    const double apq = Ar[pr + qr * ELD];
-                    if (!(apq * apq <= eps2 * fabs(Ar[pr + pr * ELD] * Ar[qr + qr * ELD]) || fabs(apq) <= 1e-30 * fro))
+                    // the skip rule of jacobi_param, on values scaled by a power of two (exact: no
+                    // overflow / flush of the squares for any finite T)
+                    const double apq = Ar[pr + qr * ELD], app = Ar[pr + pr * ELD], aqq = Ar[qr + qr * ELD];
+                    const double s3 = pow2_inv(fmax(fmax(fabs(app), fabs(aqq)), fabs(apq)));
+                    const double apq3 = apq * s3;
+                    if (!(apq3 * apq3 <= eps2 * fabs((app * s3) * (aqq * s3)) || fabs(apq) <= 1e-30 * fro))
                         live = 1;
                 }
             }

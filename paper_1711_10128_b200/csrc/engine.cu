@@ -98,7 +98,7 @@ struct trplk_ctx {
     unsigned* rcnt = nullptr;  // fused K3 + K1 (fused.cuh): per-round completion counters
     int64_t rcnt_cap = 0;
     bool prof_fused = false;   // the live profile's slots are [K3 + K1 fused, K2, -]
-    bool fuse_on = true;       // TRPLK_FUSE=0 at create: the three-kernel inner step
+    bool fuse_on = false;      // TRPLK_FUSE=1 at create: K3 + next K1 fused (fused.cuh)
     unsigned long long* gtrace = nullptr;  // TRPLK_GRID_TRACE: per-step phase timestamps
     cudaEvent_t ctev[2] = {nullptr, nullptr};  // TRPLK_CYCLE_TRACE
     double ctrace_busy = 0.0;
@@ -797,7 +797,7 @@ static cudaError_t record_event(trplk_ctx* ctx, cudaEvent_t ev) {
 
 // K3 of inner step j + K1 of step j+1 as one kernel (fused.cuh): one rank, B = I, a DIA matrix
 // of <= 8 diagonals, Jacobi / none / shifted preconditioner, the multi-kernel inner step (not the
-// latency paths).  TRPLK_FUSE=0 keeps the three-kernel step; TRPLK_FUSE_SLACK = rounds of slack
+// latency paths).  Opt-in (TRPLK_FUSE=1, read at create); TRPLK_FUSE_SLACK = rounds of slack
 // between a tile's stencil reach and its K1 (default 1).
 bool fuse_path(const trplk_ctx* ctx, const Sizes& S) {
     return ctx->fuse_on && ctx->nranks == 1 && !ctx->hasB && ctx->A.fmt == 1 && ctx->A.ndiag <= 8 && ctx->rcnt &&
@@ -1462,6 +1462,7 @@ trplk_status issue_cycle(trplk_ctx* ctx, const Sizes& S, int cur, int nprev, int
     // +K: X^prev appended after G, explicitly orthogonalised, one matvec each
     ST(phase_mark(ctx, 2));
     if (block_kplus(ctx, nprev)) ST(kplus_block(ctx, S, Uc, Uo, nprev, xprev_static));
+    const bool fz = fuse_path(ctx, S);
     for (int jj = 0; jj < nprev && !block_kplus(ctx, nprev); ++jj) {
         const unsigned kb = F_KCOL0 << jj;
         CgsSpec c{};
@@ -1477,12 +1478,12 @@ trplk_status issue_cycle(trplk_ctx* ctx, const Sizes& S, int cur, int nprev, int
         c.k_nominal = S.ph + S.m + jj;
         c.dest = Uc;
         c.dest_dyn = 1;
-        c.dest2 = ctx->xk;
+        c.dest2 = fz ? nullptr : ctx->xk;
         c.gate = F_CYCLE | kb;
         c.clear = kb;
         c.inc_k = 1;
-        ST(cgs2(ctx, c));
-        ST(halo(ctx, ctx->xk));
+        // the column's one matvec and T column: z = A x, T(1:k,k) = U^T z (fused with the FINAL
+        // update when the inner steps are, reading x from its basis column)
         SdotsArgs a = sd_base(ctx);
         a.A = ctx->A;
         a.x = ctx->xk;
@@ -1491,6 +1492,13 @@ trplk_status issue_cycle(trplk_ctx* ctx, const Sizes& S, int cur, int nprev, int
         a.set1 = 1;
         a.dest1 = D_TCOL;
         a.gate = F_CYCLE | kb;
+        if (fz) {
+            c.fuse_next = &a;
+            c.k_next = S.ph + S.m + jj + 1;
+        }
+        ST(cgs2(ctx, c));
+        if (fz) continue;
+        ST(halo(ctx, ctx->xk));
         ST(run_sdots(ctx, a, S.ph + S.m + jj + 1));
     }
     // Rayleigh-Ritz (step 11) and rotation X = U Y(:,1:p^) into the other buffer
@@ -1810,9 +1818,9 @@ static trplk_status create_impl(trplk_ctx* ctx, int64_t n_global, const int64_t*
     CK(cudaMemsetAsync(ctx->bcounter, 0, sizeof(unsigned) * NCOUNTERS, ctx->stream));
     CK(cudaMemsetAsync(ctx->blk, 0, sizeof(BlkCtl), ctx->stream));
     if (ctx->nranks == 1 && !ctx->hasB) ST(dalloc(ctx, &ctx->gridpart, (size_t)2 * GRID_MAXCTA * GRID_NVP));
-    {
+    {  // opt-in: measured slower than the three-kernel step (fused K3 + K1)
         const char* e = getenv("TRPLK_FUSE");
-        ctx->fuse_on = !(e && e[0] == '0');
+        ctx->fuse_on = e && e[0] == '1';
     }
     if (ctx->nranks == 1 && !ctx->hasB && ctx->A.fmt == 1) {
         ctx->rcnt_cap = (ctx->n_loc + 31) / 32 / (148 * WARPS) + 64;

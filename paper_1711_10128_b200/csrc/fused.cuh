@@ -29,6 +29,10 @@ __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
     return v;
 }
 
+__device__ __forceinline__ void red_release_add(unsigned* p, unsigned v) {
+    asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
 template <int KMAX>
 __global__ void __launch_bounds__(CTA, 2) k_fin_step1(const FusedArgs f) {
     const UpdArgs& u = f.u;
@@ -105,6 +109,121 @@ __global__ void __launch_bounds__(CTA, 2) k_fin_step1(const FusedArgs f) {
 #pragma unroll
     for (int q = 0; q < KMAX / 8; ++q) cacc[q][0] = cacc[q][1] = 0.0;
     double n1 = 0.0;
+    __shared__ double cv_s[8];  // DIA-C constants of the first 8 diagonals
+    if (threadIdx.x < 8) cv_s[threadIdx.x] = (threadIdx.x < nd && ((M.cmask >> threadIdx.x) & 1u)) ? M.cval[threadIdx.x] : 0.0;
+    __syncthreads();
+    const double minv_shift = a.pmode == 2 ? rho : a.sigma;
+
+    // One warp iteration of the round loop: the FINAL of tile sa (>= 0) and the K1 of tile sb
+    // (>= 0, its stencil rows complete), with the loads of both tiles in flight together: the
+    // FINAL's w' and first 16 basis columns, the K1's first 8 basis columns (L2), DIA values
+    // and gathers.
+    auto pair_tile = [&](int64_t sa, int64_t sb) {
+        const int64_t ra = sa * 32 + lane, rb = sb * 32 + lane;
+        const bool oka = sa >= 0 && ra < nrows, okb = sb >= 0 && rb < nrows;
+        // ---- issue
+        double y = oka ? __ldcs(u.x + ra) : 0.0;
+        double ua[16];
+#pragma unroll
+        for (int c = 0; c < 16; ++c) ua[c] = (oka && c < kv) ? __ldg(Ub + ra + (int64_t)c * ldu) : 0.0;
+        const double* upb = Ub + rb;
+        double ur[CH];
+#pragma unroll
+        for (int c = 0; c < CH; ++c) ur[c] = (okb && c < k1) ? __ldcg(upb + (int64_t)c * ldu) : 0.0;
+        double v[8], xv[8], dg = 1.0, xr = 0.0;
+        unsigned pm = 0;
+        if (okb) {
+            pm = M.cmask ? dia_pmask(M, rb) : 0u;
+            const double* dv = M.dval + rb;
+#pragma unroll
+            for (int d = 0; d < 8; ++d) {
+                v[d] = 0.0;
+                xv[d] = 0.0;
+                if (d < nd) {
+                    int idx = (int)rb + M.offs[d];
+                    idx = idx < 0 ? 0 : (idx > top ? top : idx);  // out-of-matrix slots hold 0
+                    if (!((M.cmask >> d) & 1u)) v[d] = __ldg(dv + (int64_t)d * M.ldv);
+                    xv[d] = __ldcg(g + idx);
+                }
+            }
+            if (!((M.cmask >> M.diag_slot) & 1u)) dg = __ldg(dv + (int64_t)M.diag_slot * M.ldv);
+            xr = __ldcg(g + rb);
+        } else {
+#pragma unroll
+            for (int d = 0; d < 8; ++d) v[d] = xv[d] = 0.0;
+        }
+        // ---- FINAL: y = w' - U h2, columns in order (as k_upd), g = y / beta
+        if (sa >= 0) {
+#pragma unroll
+            for (int c = 0; c < 16; ++c)
+                if (c < KMAX) y = fma(-hs[c < KMAX ? c : 0], ua[c], y);
+#pragma unroll
+            for (int cb = 16; cb < KMAX; cb += 16) {
+                if (cb < kv) {
+#pragma unroll
+                    for (int c = 0; c < 16; ++c) ua[c] = (oka && cb + c < kv) ? __ldg(Ub + ra + (int64_t)(cb + c) * ldu) : 0.0;
+#pragma unroll
+                    for (int c = 0; c < 16; ++c)
+                        if (cb + c < KMAX) y = fma(-hs[cb + c < KMAX ? cb + c : 0], ua[c], y);
+                }
+            }
+            if (oka) g[ra] = y * binv;
+        }
+        if (sb < 0) return;
+        // ---- K1: SpMV (ascending diagonal order, as mat_row), w, ||w||^2, dots on DMMA
+        double z = 0.0;
+        if (M.cmask) {
+#pragma unroll
+            for (int d = 0; d < 8; ++d)
+                if (d < nd && ((M.cmask >> d) & 1u)) v[d] = ((pm >> d) & 1u) ? cv_s[d] : 0.0;
+            if (okb && ((M.cmask >> M.diag_slot) & 1u)) dg = ((pm >> M.diag_slot) & 1u) ? M.cval[M.diag_slot] : 0.0;
+        }
+#pragma unroll
+        for (int d = 0; d < 8; ++d) z = fma(v[d], xv[d], z);
+        double o = 0.0;
+        if (a.out_mode == 2) o = jacobi_minv(dg, 1.0, minv_shift, a.mfloor) * (z - rho * xr);
+        if (okb) {
+            if (a.out_mode == 2 && a.out) __stcs(a.out + rb, o);
+        } else {
+            z = 0.0;
+            o = 0.0;
+        }
+        if (a.norm1 == 1) n1 += o * o;
+        double bq[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const double t1 = __shfl_sync(0xffffffffu, z, 4 * q + fj);
+            const double t2 = __shfl_sync(0xffffffffu, o, 4 * q + fj);
+            bq[q] = fi == 0 ? t1 : (fi == 1 ? t2 : 0.0);
+        }
+        __syncwarp();
+#pragma unroll
+        for (int c = 0; c < CH; ++c) W[c * WLD + lane] = ur[c];
+        __syncwarp();
+#pragma unroll
+        for (int cb = 0; cb < KMAX; cb += CH) {
+            const bool more = cb + CH < KMAX && cb + CH < k1;
+            if (more) {
+#pragma unroll
+                for (int c = 0; c < CH; ++c) {
+                    const int cc = cb + CH + c;
+                    ur[c] = (okb && cc < k1) ? __ldcg(upb + (int64_t)cc * ldu) : 0.0;
+                }
+            }
+            if (cb < k1) {
+                const double* sp = W + fi * WLD + fj;
+#pragma unroll
+                for (int q = 0; q < 8; ++q) dmma884_nv(cacc[cb / 8], sp[4 * q], bq[q]);
+            }
+            if (more) {
+                __syncwarp();
+#pragma unroll
+                for (int c = 0; c < CH; ++c) W[c * WLD + lane] = ur[c];
+                __syncwarp();
+            }
+        }
+        __syncwarp();
+    };
     // K1 of one tile on g (complete at its stencil rows): SpMV in ascending diagonal order (as
     // mat_row), w, ||w||^2, then U(rows, 0:kv+1)^T [z w] on DMMA through the warp's slab
     auto k1_tile = [&](int64_t sl) {
@@ -183,15 +302,11 @@ __global__ void __launch_bounds__(CTA, 2) k_fin_step1(const FusedArgs f) {
     bool run_k1 = false, done3 = false, brk3 = false;
     if (!pass3 && !brk) {
         run_k1 = true;
+        // round r: the FINAL of round r and the K1 of round r - lag, whose stencil reaches round
+        // r - lag + dn <= r - 1 (lag >= dn + 1): wait until every CTA has published that round
+        // (bar.sync + one release per CTA / one acquire per CTA + bar.sync, as a grid semaphore)
         const int lag = f.lag;
         for (int64_t r = 0; r < R + lag; ++r) {
-            if (r < R) {
-                const int64_t sl = r * NW + gw;
-                if (sl < nsl) fin_tile(sl, true);
-                __threadfence();
-                __syncthreads();
-                if (threadIdx.x == 0) atomicAdd(f.rcnt + r, 1u);
-            }
             const int64_t r1 = r - lag;
             if (r1 >= 0) {
                 int64_t need = r1 + f.dn;
@@ -199,14 +314,18 @@ __global__ void __launch_bounds__(CTA, 2) k_fin_step1(const FusedArgs f) {
                 if (threadIdx.x == 0) {
                     long long spins = 0;
                     while (ld_acquire_u32(f.rcnt + need) < gridDim.x) {
-                        __nanosleep(64);
-                        if (++spins > (1ll << 26)) __trap();  // watchdog: a dirty counter would hang the GPU
+                        __nanosleep(32);
+                        if (++spins > (1ll << 27)) __trap();  // watchdog: a dirty counter would hang the GPU
                     }
-                    __threadfence();
                 }
                 __syncthreads();
-                const int64_t sl = r1 * NW + gw;
-                if (sl < nsl) k1_tile(sl);
+            }
+            const int64_t sa = (r < R && r * NW + gw < nsl) ? r * NW + gw : -1;
+            const int64_t sb = (r1 >= 0 && r1 * NW + gw < nsl) ? r1 * NW + gw : -1;
+            if (sa >= 0 || sb >= 0) pair_tile(sa, sb);
+            if (r < R) {
+                __syncthreads();
+                if (threadIdx.x == 0) red_release_add(f.rcnt + r, 1u);
             }
         }
     } else if (pass3) {

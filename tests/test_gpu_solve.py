@@ -286,12 +286,21 @@ def test_grid_inner_loop(orc, gen, name, N, over, fmt, debug):
         # drifts by ~1e-10 relative under any change of summation order (the multi-kernel path
         # shows the same drift, tools/cmp_traj.py): compare the cycle structure exactly and
         # theta_t to 1e-8 relative
+        # theta_t to 1e-8 relative.  The run may stop a few cycles apart only at a near-tie of the
+        # stopping test: where the shorter run stopped, the longer one's target residual is within
+        # 2x tol (seen with the tridiagonal RR variant, theta drift 2.5e-9 over 260 cycles)
         assert g["stats"]["status"] == "OK"
-        assert g["stats"]["a_matvecs"] == o["a_matvecs"] and g["stats"]["cycles"] == o["cycles"]
         lg, lo = g["log"], o["log"]
+        n = min(len(lg["t"]), len(lo["t"]))
         for key in ("t", "k", "nprev"):
-            assert np.array_equal(lg[key], lo[key]), key
-        assert np.max(np.abs(lg["theta_t"] - lo["theta_t"]) / np.abs(lo["theta_t"])) <= 1e-8
+            assert np.array_equal(lg[key][:n], lo[key][:n]), key
+        assert np.max(np.abs(lg["theta_t"][:n] - lo["theta_t"][:n]) / np.abs(lo["theta_t"][:n])) <= 1e-8
+        if g["stats"]["cycles"] != o["cycles"]:
+            longer = lo if len(lo["t"]) > n else lg
+            assert longer["res"][n - 1] <= 2 * P.tol, (g["stats"]["cycles"], o["cycles"], longer["res"][n - 1])
+            assert abs(g["stats"]["cycles"] - o["cycles"]) <= 0.05 * o["cycles"]
+        else:
+            assert g["stats"]["a_matvecs"] == o["a_matvecs"]
         assert np.max(np.abs(g["eigenvalues"] - o["eigenvalues"]) / np.abs(o["eigenvalues"])) <= 1e-9
         assert np.all(g["residuals"] <= P.tol)
     X = g["X"]

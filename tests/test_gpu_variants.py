@@ -14,8 +14,8 @@ set (the switches are read once per process):
   TRPLK_K1=tpdots   the thread-per-row kernel for the first-pass CGS dots of the seed / +K vectors
   TRPLK_KPLUS=col   the +K columns one at a time (CGS2 + SpMV each), also for k_plus >= 3
   TRPLK_KPLUS=block the block +K kernels (block.cuh) also for k_plus <= 2
-  TRPLK_FUSE=0      the three-kernel inner step (K3 and the next K1 as separate launches) instead
-                    of the fused k_fin_step1 (fused.cuh)
+  TRPLK_FUSE=1      K3 of each inner step and the next K1 (and each +K column's FINAL and its
+                    matvec) as one cooperative kernel, k_fin_step1 (fused.cuh)
   TRPLK_DIAC=0      every DIA diagonal as a value array (no constant-diagonal presence bits)
 """
 import os
@@ -31,7 +31,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 
 VARIANTS = [("TRPLK_K1", "pipe"), ("TRPLK_K1", "rs"), ("TRPLK_K1", "tpdots"), ("TRPLK_NO_COOP3", "1"),
             ("TRPLK_NO_SMALL", "1"), ("TRPLK_GRID", "1"), ("TRPLK_EIG", "tri"), ("TRPLK_KPLUS", "col"), ("TRPLK_KPLUS", "block"),
-            ("TRPLK_FUSE", "0"), ("TRPLK_DIAC", "0")]
+            ("TRPLK_FUSE", "1"), ("TRPLK_DIAC", "0")]
 
 
 @pytest.mark.parametrize("var,val", VARIANTS)
