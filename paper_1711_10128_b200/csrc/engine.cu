@@ -505,13 +505,13 @@ static bool host_pinned(const void* p) {
 // are read as one presence bit per row plus the constant, instead of 8 bytes per row.  One
 // device scan of the value arrays (min / max stored bit pattern per diagonal) decides; the
 // decoded values are bit-identical to the stored ones, so the arithmetic does not change.
-// TRPLK_DIAC=0 keeps every diagonal as a value array (A/B measurements, parity tests).
+// Opt-in (TRPLK_DIAC=1 at create): measured slower on the default kernels.
 trplk_status dia_compress(trplk_ctx* ctx, Sell& S, int64_t& bytes) {
     const char* e = getenv("TRPLK_DIAC");
-    if ((e && e[0] == '0') || S.nrows == 0) return TRPLK_OK;
-    const int nd = S.ndiag;
+    if (!(e && e[0] == '1') || S.nrows == 0) return TRPLK_OK;  // opt-in (measured)
+    const int nd = S.ndiag < 8 ? S.ndiag : 8;
     double* tmp;
-    ST(dalloc(ctx, &tmp, (size_t)2 * nd + DIA_MAX));
+    ST(dalloc(ctx, &tmp, (size_t)2 * nd));
     unsigned long long* mm = reinterpret_cast<unsigned long long*>(tmp);
     std::vector<unsigned long long> h(2 * (size_t)nd);
     for (int d = 0; d < nd; ++d) {
@@ -523,34 +523,26 @@ trplk_status dia_compress(trplk_ctx* ctx, Sell& S, int64_t& bytes) {
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(h.data(), mm, 16 * (size_t)nd, cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
+    dev_free(ctx, tmp);
     unsigned cm = 0;
-    double cv[DIA_MAX] = {};
-    int top = -1;
+    double cv[8] = {};
     for (int d = 0; d < nd; ++d) {
         if (h[2 * d] == h[2 * d + 1] || (h[2 * d] == ~0ull && h[2 * d + 1] == 0ull)) {  // one pattern, or none
             cm |= 1u << d;
             const unsigned long long b = h[2 * d] == ~0ull ? 0ull : h[2 * d];
             std::memcpy(&cv[d], &b, 8);
-            top = d;
         }
     }
-    if (cm == 0) {
-        dev_free(ctx, tmp);
-        return TRPLK_OK;
-    }
-    const int mb = top < 8 ? 1 : (top < 16 ? 2 : 4);
-    double* pm;
-    ST(dalloc(ctx, &pm, ((size_t)S.ldv * mb + 7) / 8));
-    launch_dia_pmask(S.dval, S.nrows, S.ldv, nd, cm, mb, pm, ctx->stream);
+    if (cm == 0) return TRPLK_OK;
+    unsigned char* pm;
+    ST(dalloc(ctx, &pm, (size_t)S.ldv));
+    launch_dia_pmask(S.dval, S.nrows, S.ldv, nd, cm, pm, ctx->stream);
     CK(cudaGetLastError());
-    double* cvd = tmp + 2 * nd;
-    CK(cudaMemcpyAsync(cvd, cv, sizeof(cv), cudaMemcpyHostToDevice, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
     S.cmask = cm;
-    S.mbytes = mb;
     S.pmask = pm;
-    S.cval = cvd;
-    bytes = (int64_t)(nd - __builtin_popcount(cm)) * S.nrows * 8 + (int64_t)mb * S.nrows;
+    for (int d = 0; d < 8; ++d) S.cv[d] = cv[d];
+    bytes = (int64_t)(S.ndiag - __builtin_popcount(cm)) * S.nrows * 8 + S.nrows;
     return TRPLK_OK;
 }
 
@@ -1544,8 +1536,9 @@ static std::string graph_fingerprint(const trplk_ctx* ctx, uint64_t key, const S
         put(v, sizeof(v));
         put(&M->dval, sizeof(M->dval));
         put(M->offs, sizeof(M->offs));
-        const int64_t c[4] = {(int64_t)M->cmask, M->mbytes, (int64_t)(uintptr_t)M->pmask, (int64_t)(uintptr_t)M->cval};
+        const int64_t c[2] = {(int64_t)M->cmask, (int64_t)(uintptr_t)M->pmask};
         put(c, sizeof(c));
+        put(M->cv, sizeof(M->cv));
     }
     const double sc[5] = {ctx->sigma, ctx->mfloor, ctx->normF, ctx->mfloor_solve, (double)ctx->pmode};
     put(sc, sizeof(sc));

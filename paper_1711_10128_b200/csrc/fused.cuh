@@ -110,7 +110,7 @@ __global__ void __launch_bounds__(CTA, 2) k_fin_step1(const FusedArgs f) {
     for (int q = 0; q < KMAX / 8; ++q) cacc[q][0] = cacc[q][1] = 0.0;
     double n1 = 0.0;
     __shared__ double cv_s[8];  // DIA-C constants of the first 8 diagonals
-    if (threadIdx.x < 8) cv_s[threadIdx.x] = (threadIdx.x < nd && ((M.cmask >> threadIdx.x) & 1u)) ? M.cval[threadIdx.x] : 0.0;
+    if (threadIdx.x < 8) cv_s[threadIdx.x] = (threadIdx.x < nd && ((M.cmask >> threadIdx.x) & 1u)) ? M.cv[threadIdx.x] : 0.0;
     __syncthreads();
     const double minv_shift = a.pmode == 2 ? rho : a.sigma;
 
@@ -176,7 +176,7 @@ __global__ void __launch_bounds__(CTA, 2) k_fin_step1(const FusedArgs f) {
 #pragma unroll
             for (int d = 0; d < 8; ++d)
                 if (d < nd && ((M.cmask >> d) & 1u)) v[d] = ((pm >> d) & 1u) ? cv_s[d] : 0.0;
-            if (okb && ((M.cmask >> M.diag_slot) & 1u)) dg = ((pm >> M.diag_slot) & 1u) ? M.cval[M.diag_slot] : 0.0;
+            if (okb && ((M.cmask >> M.diag_slot) & 1u)) dg = ((pm >> M.diag_slot) & 1u) ? cv_s[M.diag_slot] : 0.0;
         }
 #pragma unroll
         for (int d = 0; d < 8; ++d) z = fma(v[d], xv[d], z);

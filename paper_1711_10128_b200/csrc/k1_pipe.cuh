@@ -76,8 +76,8 @@ __global__ void __launch_bounds__(CTA, 2) k_step1_pipe(const SdotsArgs a) {
         if (M.cmask) {
 #pragma unroll
             for (int d = 0; d < 8; ++d)
-                if (d < nd && ((M.cmask >> d) & 1u)) v[d] = ((pm >> d) & 1u) ? __ldg(M.cval + d) : 0.0;
-            if (ok && ((M.cmask >> M.diag_slot) & 1u)) dg = ((pm >> M.diag_slot) & 1u) ? __ldg(M.cval + M.diag_slot) : 0.0;
+                if (d < nd && ((M.cmask >> d) & 1u)) v[d] = ((pm >> d) & 1u) ? M.cv[d] : 0.0;
+            if (ok && ((M.cmask >> M.diag_slot) & 1u)) dg = ((pm >> M.diag_slot) & 1u) ? M.cv[M.diag_slot & 7] : 0.0;
         }
 #pragma unroll
         for (int d = 0; d < 8; ++d) z = fma(v[d], xv[d], z);

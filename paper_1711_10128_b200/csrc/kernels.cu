@@ -919,6 +919,7 @@ __global__ void k_gather(const double* x, const int* idx, int64_t n, double* out
 #include "inner_grid.cuh"  // cooperative grid-wide inner loop for mid-size n (latency path)
 #include "pl1.cuh"         // PL+1 (Algorithm 2) small kernels
 #include "fused.cuh"       // K3 of step j + K1 of step j+1 in one kernel (lagged rounds)
+#include "lean_k1.cuh"     // thread-per-row K1 (register accumulators) for k <= 24
 
 namespace trplk {
 
@@ -931,7 +932,8 @@ static int k1var() {
     static int v = -1;
     if (v < 0) {
         const char* e = getenv("TRPLK_K1");
-        v = (e && !strcmp(e, "pipe")) ? 2 : (e && !strcmp(e, "rs")) ? 1 : (e && !strcmp(e, "tpdots")) ? 3 : 0;
+        v = (e && !strcmp(e, "pipe")) ? 2 : (e && !strcmp(e, "rs")) ? 1 : (e && !strcmp(e, "tpdots")) ? 3
+            : (e && !strcmp(e, "lean")) ? 4 : 0;
     }
     return v;
 }
@@ -1003,6 +1005,7 @@ void launch_sdots(const SdotsArgs& a, int kmax, cudaStream_t s) {
     const bool k1_shape = a.A.nrows && a.out_mode <= 2 && a.set1 == 1 && (a.set2 == 0 || a.set2 == 2) &&
                           (a.norm1 >= 0 && a.norm1 <= 2) && a.norm2 == 0 && a.x_dyn == 0 && a.uout == nullptr;
     if (kmax > 0 && k1_shape) {
+        if (k1var() == 4 && kmax <= 24 && launch_step1_lean(a, kmax, s)) return;
         // pipelined K1: measured faster on long tile loops with a register-resident row (C5,
         // k <= 16: 10.98 vs 11.53 ms per inner step); equal or slower elsewhere
         if ((k1var() == 2 || (k1var() == 0 && kmax <= 16 && a.nrows >= (int64_t)1 << 24)) &&
@@ -1216,17 +1219,12 @@ void launch_dia_const_scan(const double* dval, int64_t nrows, int64_t ldv, int n
     k_dia_const_scan<<<dim3((unsigned)g, (unsigned)nd), 256, 0, s>>>(dval, nrows, ldv, nd, mnmx);
 }
 
-void launch_dia_pmask(const double* dval, int64_t nrows, int64_t ldv, int nd, unsigned cmask, int mbytes,
-                      void* pm, cudaStream_t s) {
+void launch_dia_pmask(const double* dval, int64_t nrows, int64_t ldv, int nd, unsigned cmask, unsigned char* pm,
+                      cudaStream_t s) {
     int64_t g = (ldv + 255) / 256;
     if (g > 148 * 16) g = 148 * 16;
     if (g < 1) g = 1;
-    if (mbytes == 1)
-        k_dia_pmask<unsigned char><<<(int)g, 256, 0, s>>>(dval, nrows, ldv, nd, cmask, static_cast<unsigned char*>(pm));
-    else if (mbytes == 2)
-        k_dia_pmask<unsigned short><<<(int)g, 256, 0, s>>>(dval, nrows, ldv, nd, cmask, static_cast<unsigned short*>(pm));
-    else
-        k_dia_pmask<unsigned><<<(int)g, 256, 0, s>>>(dval, nrows, ldv, nd, cmask, static_cast<unsigned*>(pm));
+    k_dia_pmask<unsigned char><<<(int)g, 256, 0, s>>>(dval, nrows, ldv, nd, cmask, pm);
 }
 
 void launch_gather(const double* x, const int* idx, int64_t n, double* out, cudaStream_t s) {

@@ -25,12 +25,12 @@ constexpr int DIA_MAX = 32;       // most diagonals a DIA matrix may have
 //         dval[d*ldv + row] (0 where no entry).  Requires the ghost tail to be the contiguous
 //         global ranges [row_begin-glo, row_begin) then [row_end, row_end+nghost-glo), so the
 //         local index of row+off is computed, not loaded.  diag_slot = index of offset 0.
-//         Constant diagonals (DIA-C): bit d of cmask set = every stored entry of diagonal d has
-//         the same bit pattern cval[d] (device array); the kernels then read, instead of the
-//         d-th value array, bit d of the row's presence word pmask[row] (mbytes = 1, 2 or 4
-//         bytes per row, 0 past the last row) and use cval[d] where it is set, +0.0 elsewhere
-//         -- exactly the stored values (a stencil's -1 / 1/12 couplings: 8 bytes per row and
-//         diagonal become one bit).  dval stays fully populated (IC(0) factors from it).
+//         Constant diagonals (DIA-C, opt-in): bit d (d < 8) of cmask set = every stored entry of
+//         diagonal d has the same bit pattern cv[d] (kept in the descriptor, i.e. in the kernel
+//         parameters); the kernels then read, instead of the d-th value array, bit d of the
+//         row's presence byte pmask[row] (0 past the last row) and use cv[d] where it is set,
+//         +0.0 elsewhere -- exactly the stored values (a stencil's -1 couplings: 8 bytes per
+//         row and diagonal become one bit).  dval stays fully populated (IC(0) factors from it).
 struct Sell {
     int fmt = 0;
     int64_t nrows = 0;
@@ -43,20 +43,15 @@ struct Sell {
     const double* dval = nullptr;
     int offs[DIA_MAX] = {};
     unsigned cmask = 0;
-    int mbytes = 0;
-    const void* pmask = nullptr;
-    const double* cval = nullptr;
+    const unsigned char* pmask = nullptr;
+    double cv[8] = {};
 };
 
 // Presence word of a DIA-C row (bit d = entry of constant diagonal d stored).
-__device__ __forceinline__ unsigned dia_pmask(const Sell& M, int64_t row) {
-    if (M.mbytes == 1) return __ldg(static_cast<const unsigned char*>(M.pmask) + row);
-    if (M.mbytes == 2) return __ldg(static_cast<const unsigned short*>(M.pmask) + row);
-    return __ldg(static_cast<const unsigned*>(M.pmask) + row);
-}
+__device__ __forceinline__ unsigned dia_pmask(const Sell& M, int64_t row) { return __ldg(M.pmask + row); }
 // Value of diagonal d at a row: the stored array, or the constant where the row's bit is set.
 __device__ __forceinline__ double dia_val(const Sell& M, int d, unsigned pm, const double* dv) {
-    if ((M.cmask >> d) & 1u) return ((pm >> d) & 1u) ? __ldg(M.cval + d) : 0.0;
+    if (d < 8 && ((M.cmask >> d) & 1u)) return ((pm >> d) & 1u) ? M.cv[d < 8 ? d : 0] : 0.0;
     return __ldg(dv + (int64_t)d * M.ldv);
 }
 
@@ -174,6 +169,7 @@ struct FusedArgs {
     int dn, lag;  // rounds a tile's stencil reaches past its own; rounds between FINAL and K1
 };
 bool launch_fin_step1(const FusedArgs& f, int kmax, int maxoff, int slack, cudaStream_t s);
+bool launch_step1_lean(const SdotsArgs& a, int kmax, cudaStream_t s);
 
 // ------------------------------------------------------------- block kernels (block.cuh)
 constexpr int BC = 8;                                // vectors per block launch (DMMA n = 8)
@@ -415,8 +411,8 @@ void launch_copy_cols(const double* src, int64_t lds, double* dst, int64_t ldd, 
 // initialised to {~0, 0}), then the presence words of the diagonals in cmask.
 void launch_dia_const_scan(const double* dval, int64_t nrows, int64_t ldv, int nd, unsigned long long* mnmx,
                            cudaStream_t s);
-void launch_dia_pmask(const double* dval, int64_t nrows, int64_t ldv, int nd, unsigned cmask, int mbytes,
-                      void* pm, cudaStream_t s);
+void launch_dia_pmask(const double* dval, int64_t nrows, int64_t ldv, int nd, unsigned cmask, unsigned char* pm,
+                      cudaStream_t s);
 void launch_csr_to_dia(const int64_t* rp, const int64_t* ci, const double* va, int64_t nrows, int64_t row0,
                        const int* offs, int nd, int64_t ldv, double* dval, cudaStream_t s);
 int kmax_bucket(int k);

@@ -12,6 +12,8 @@ set (the switches are read once per process):
   TRPLK_GRID=1      the cooperative grid-wide inner loop (inner_grid.cuh)
   TRPLK_EIG=tri     the tridiagonal RR eigensolver (eig_tri.cu) instead of one-CTA Jacobi
   TRPLK_K1=tpdots   the thread-per-row kernel for the first-pass CGS dots of the seed / +K vectors
+  TRPLK_K1=lean     the thread-per-row inner-step K1 with register dot accumulators (lean_k1.cuh)
+                    for k <= 24
   TRPLK_KPLUS=col   the +K columns one at a time (CGS2 + SpMV each), also for k_plus >= 3
   TRPLK_KPLUS=block the block +K kernels (block.cuh) also for k_plus <= 2
   TRPLK_FUSE=1      K3 of each inner step and the next K1 (and each +K column's FINAL and its
@@ -29,7 +31,7 @@ from gpu_util import need_gpu
 pytestmark = pytest.mark.gpu
 HERE = os.path.dirname(os.path.abspath(__file__))
 
-VARIANTS = [("TRPLK_K1", "pipe"), ("TRPLK_K1", "rs"), ("TRPLK_K1", "tpdots"), ("TRPLK_NO_COOP3", "1"),
+VARIANTS = [("TRPLK_K1", "pipe"), ("TRPLK_K1", "rs"), ("TRPLK_K1", "tpdots"), ("TRPLK_K1", "lean"), ("TRPLK_NO_COOP3", "1"),
             ("TRPLK_NO_SMALL", "1"), ("TRPLK_GRID", "1"), ("TRPLK_EIG", "tri"), ("TRPLK_KPLUS", "col"), ("TRPLK_KPLUS", "block"),
             ("TRPLK_FUSE", "1"), ("TRPLK_DIAC", "0")]
 
