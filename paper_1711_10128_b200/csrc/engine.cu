@@ -99,6 +99,12 @@ struct trplk_ctx {
     int64_t rcnt_cap = 0;
     bool prof_fused = false;   // the live profile's slots are [K3 + K1 fused, K2, -]
     bool fuse_on = false;      // TRPLK_FUSE=1 at create: K3 + next K1 fused (fused.cuh)
+    // halo overlap (nranks > 1, DIA, B = I): the exchange on hstream while K1 runs the interior
+    // rows [hb0, hb1), then the boundary rows; TRPLK_HALO_OVERLAP=0 at create: exchange first
+    cudaStream_t hstream = nullptr;
+    cudaEvent_t hev_fork = nullptr, hev_done = nullptr;
+    int64_t hb0 = 0, hb1 = 0;
+    bool hov = false;
     unsigned long long* gtrace = nullptr;  // TRPLK_GRID_TRACE: per-step phase timestamps
     cudaEvent_t ctev[2] = {nullptr, nullptr};  // TRPLK_CYCLE_TRACE
     double ctrace_busy = 0.0;
@@ -622,13 +628,14 @@ trplk_status try_dia(trplk_ctx* ctx, const int64_t* rp, const int64_t* ci, const
 }
 
 // ----------------------------------------------------------------- halo exchange
-trplk_status halo(trplk_ctx* ctx, const double* xconst) {
+trplk_status halo(trplk_ctx* ctx, const double* xconst, cudaStream_t hs = nullptr) {
     if (ctx->nranks == 1 || ctx->peers.empty()) return TRPLK_OK;
+    cudaStream_t st = hs ? hs : ctx->stream;
     double* x = const_cast<double*>(xconst);
     int64_t off = 0;
     for (size_t i = 0; i < ctx->peers.size(); ++i) {
         if (ctx->send_cnt[i] > 0 && ctx->send_start[i] < 0) {
-            launch_gather(x, ctx->send_idx[i], ctx->send_cnt[i], ctx->sendbuf + off, ctx->stream);
+            launch_gather(x, ctx->send_idx[i], ctx->send_cnt[i], ctx->sendbuf + off, st);
         }
         off += ctx->send_cnt[i];
     }
@@ -643,7 +650,7 @@ trplk_status halo(trplk_ctx* ctx, const double* xconst) {
         }
         off += ctx->send_cnt[i];
     }
-    CM(ctx->cm->sendrecv(sends, recvs, 8, ctx->stream));
+    CM(ctx->cm->sendrecv(sends, recvs, 8, st));
     return TRPLK_OK;
 }
 
@@ -711,6 +718,55 @@ trplk_status run_sdots(trplk_ctx* ctx, SdotsArgs a, int kbytes_cols, bool count_
     } else {
         launch_sdots(a, kmax, ctx->stream);
     }
+    CK(cudaGetLastError());
+    return TRPLK_OK;
+}
+
+// Inner-step K1 of a row slab with the halo exchange overlapped: the exchange of
+// g's boundary rows runs on hstream while K1 covers the interior rows [hb0, hb1), which read no
+// ghost; then K1 covers [0, hb0) and [hb1, n).  The three launches are partial slots of ONE
+// deterministic grid reduction (fixed slot order), finished by the last launch's last CTA.
+bool k1_overlap_ok(const trplk_ctx* ctx, const SdotsArgs& a, int k) {
+    return ctx->hov && a.A.nrows && !a.B.nrows && a.out_mode <= 2 && a.set1 == 1 && a.norm2 == 0 && a.x_dyn == 0 &&
+           kmax_bucket(std::max(k, 1)) <= 48;
+}
+
+trplk_status run_k1_overlap(trplk_ctx* ctx, SdotsArgs a, int k) {
+    const int kmax = kmax_bucket(std::max(k, 1));
+    CK(cudaEventRecord(ctx->hev_fork, ctx->stream));
+    CK(cudaStreamWaitEvent(ctx->hstream, ctx->hev_fork, 0));
+    const int64_t n = ctx->n_loc;
+    const int64_t rr[3][2] = {{ctx->hb0, ctx->hb1}, {0, ctx->hb0}, {ctx->hb1, n}};
+    int g[3], tot = 0;
+    for (int i = 0; i < 3; ++i) {  // one tile pair per warp, 2 CTAs per SM at most
+        const int64_t tiles = (rr[i][1] - rr[i][0] + 31) / 32;
+        int64_t need = (tiles + 2 * WARPS - 1) / (2 * WARPS);
+        const int64_t cap = 2 * 148;
+        g[i] = (int)std::max<int64_t>(1, std::min(need, cap));
+        tot += g[i];
+    }
+    ctx->model_bytes += mat_bytes(ctx, false) + vec_bytes(ctx) * (k + 2 + (a.out ? 1 : 0));
+    ctx->launches += 5;
+    a.red_local = ctx->red_local;
+    a.cta_tot = tot;
+    int off = 0;
+    for (int i = 0; i < 3; ++i) {
+        SdotsArgs b = a;
+        b.row0 = rr[i][0];
+        b.nrows = rr[i][1];
+        b.cta_off = off;
+        b.grid_force = g[i];
+        off += g[i];
+        if (i == 1) {  // boundary rows: after the exchange
+            CK(cudaEventRecord(ctx->hev_done, ctx->hstream));
+            CK(cudaStreamWaitEvent(ctx->stream, ctx->hev_done, 0));
+        }
+        launch_sdots(b, kmax, ctx->stream);
+        CK(cudaGetLastError());
+        if (i == 0) ST(halo(ctx, a.x, ctx->hstream));  // enqueued after the interior launch
+    }
+    CM(ctx->cm->allgather(ctx->red_local, ctx->red_all, NV_MAX, 8, ctx->stream));
+    launch_finalize_sdots_multi(a, ctx->red_all, ctx->nranks, NV_MAX, ctx->stream);
     CK(cudaGetLastError());
     return TRPLK_OK;
 }
@@ -1413,13 +1469,14 @@ trplk_status issue_cycle(trplk_ctx* ctx, const Sizes& S, int cur, int nprev, int
         const int k = S.ph + j;  // nominal width incl. g_j
         const bool prof = ctx->prof_on && j == jmid && j < S.m;
         const double* g = Uc + ld * (k - 1);
-        ST(halo(ctx, g));
         SdotsArgs a = k1_args(j);
         const bool k1_done = fz && j > 1;  // ran inside the previous step's fused kernel
+        const bool ov = !k1_done && k1_overlap_ok(ctx, a, k);
+        if (!ov) ST(halo(ctx, g));
         if (j < S.m) {
             const bool ic0 = ctx->pmode == 3;
             if (prof && !fz) CK(record_event(ctx, ctx->pev[0]));
-            if (!k1_done) ST(run_sdots(ctx, a, k));
+            if (!k1_done) ST(ov ? run_k1_overlap(ctx, a, k) : run_sdots(ctx, a, k));
             if (prof && !fz) ctx->prof_kern[0] = g_last_kern;
             if (ic0) ST(ic0_apply(ctx, ctx->w, F_CYCLE | F_INNER));  // w = (L L^T)^-1 (z - rho g)
             if (prof) CK(record_event(ctx, ctx->pev[fz ? 0 : 1]));
@@ -1447,7 +1504,7 @@ trplk_status issue_cycle(trplk_ctx* ctx, const Sizes& S, int cur, int nprev, int
                 if (fz) CK(record_event(ctx, ctx->pev[3]));
             }
         } else if (!k1_done) {
-            ST(run_sdots(ctx, a, k));
+            ST(ov ? run_k1_overlap(ctx, a, k) : run_sdots(ctx, a, k));
         }
     }
     }  // seed + inner loop of Algorithm 1
@@ -1815,6 +1872,22 @@ static trplk_status create_impl(trplk_ctx* ctx, int64_t n_global, const int64_t*
         const char* e = getenv("TRPLK_FUSE");
         ctx->fuse_on = e && e[0] == '1';
     }
+    if (ctx->nranks > 1 && !ctx->hasB && ctx->A.fmt == 1) {  // halo overlap: interior rows of the slab
+        const char* e = getenv("TRPLK_HALO_OVERLAP");
+        int lo = 0, hi = 0;
+        for (int d = 0; d < ctx->A.ndiag; ++d) {
+            lo = std::max(lo, -ctx->A.offs[d]);
+            hi = std::max(hi, ctx->A.offs[d]);
+        }
+        ctx->hb0 = ((int64_t)lo + 31) / 32 * 32;
+        ctx->hb1 = (ctx->n_loc - hi) / 32 * 32;
+        ctx->hov = !(e && e[0] == '0') && ctx->hb1 - ctx->hb0 >= 64;
+        if (ctx->hov && !ctx->hstream) {
+            CK(cudaStreamCreateWithFlags(&ctx->hstream, cudaStreamNonBlocking));
+            CK(cudaEventCreateWithFlags(&ctx->hev_fork, cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&ctx->hev_done, cudaEventDisableTiming));
+        }
+    }
     if (ctx->nranks == 1 && !ctx->hasB && ctx->A.fmt == 1) {
         ctx->rcnt_cap = (ctx->n_loc + 31) / 32 / (148 * WARPS) + 64;
         ST(dalloc(ctx, &ctx->rcnt, (size_t)ctx->rcnt_cap));
@@ -1980,6 +2053,9 @@ void trplk_destroy(trplk_ctx* ctx) {
     if (!ctx->has_alloc) trim_pool();
     ctl_host_free(ctx->ctl_h);
     if (ctx->ev_in) cudaEventDestroy(ctx->ev_in);
+    if (ctx->hev_fork) cudaEventDestroy(ctx->hev_fork);
+    if (ctx->hev_done) cudaEventDestroy(ctx->hev_done);
+    if (ctx->hstream) cudaStreamDestroy(ctx->hstream);
     for (auto& e : ctx->pev)
         if (e) cudaEventDestroy(e);
     for (auto& e : ctx->phev)

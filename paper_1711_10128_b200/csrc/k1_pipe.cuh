@@ -40,6 +40,7 @@ __global__ void __launch_bounds__(CTA, 2) k_step1_pipe(const SdotsArgs a) {
     const int nl = (int)M.nrows, top = (int)(M.nrows + M.nghost - 1), glo = (int)M.glo;
     const bool halo = M.nghost != 0;
     const int64_t nslices = (a.nrows + 31) >> 5;
+    const int64_t sbeg = a.row0 >> 5;  // first tile of the row range
     const int64_t stride = (int64_t)gridDim.x * WARPS;
     // registers of the tile in flight: basis row, DIA values, gathered x, diagonal, own x
     double ur[KMAX], v[8], xv[8], dg = 0.0, xr = 0.0;
@@ -66,7 +67,7 @@ __global__ void __launch_bounds__(CTA, 2) k_step1_pipe(const SdotsArgs a) {
         dg = (ok && !((M.cmask >> M.diag_slot) & 1u)) ? __ldg(dv + (int64_t)M.diag_slot * M.ldv) : 1.0;
         xr = ok ? X[row] : 0.0;
     };
-    int64_t sl = (int64_t)blockIdx.x * WARPS + warp;
+    int64_t sl = sbeg + (int64_t)blockIdx.x * WARPS + warp;
     if (sl < nslices) issue(sl);
     for (; sl < nslices; sl += stride) {
         const int64_t row = sl * 32 + lane;
@@ -142,7 +143,7 @@ __global__ void __launch_bounds__(CTA, 2) k_step1_pipe(const SdotsArgs a) {
     }
     __syncthreads();
     pdl_trigger();
-    if (!grid_reduce(res, nv, a.part, a.gpart, a.counter, a.maxcta, res)) return;
+    if (!grid_reduce(res, nv, a.part, a.gpart, a.counter, a.maxcta, res, a.cta_off, a.cta_tot)) return;
     if (a.red_local) {
         for (int vv = threadIdx.x; vv < nv; vv += CTA) a.red_local[vv] = res[vv];
     } else {
@@ -155,7 +156,7 @@ static void launch_step1_pipe_k(const SdotsArgs& a, cudaStream_t s) {
     const int smem = WARPS * KMAX * WLD * (int)sizeof(double);
     auto kern = k_step1_pipe<KMAX, TWO>;
     NOTE_KERN(kern);
-    launch_pdl(kern, rs_grid(kern, smem, a.nrows), CTA, smem, s, a);
+    launch_pdl(kern, a.grid_force > 0 ? a.grid_force : rs_grid(kern, smem, a.nrows - a.row0), CTA, smem, s, a);
 }
 
 bool launch_step1_pipe(const SdotsArgs& a, int kmax, cudaStream_t s) {

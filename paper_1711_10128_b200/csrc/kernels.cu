@@ -133,10 +133,12 @@ __device__ __forceinline__ double mat_diag(const Sell& M, int64_t s, int lane) {
 constexpr int RG = 32;
 constexpr int ONE_LEVEL_MAX = 1024;
 __device__ bool grid_reduce(const double* mine, int nv, double* part, double* gpart, unsigned* cnt, int maxcta,
-                            double* out) {
+                            double* out, int bid_off = 0, int ncta_tot = 0) {
     __shared__ bool flag;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int bid = blockIdx.x, ncta = gridDim.x;
+    // a reduction may span several launches in stream order (halo overlap: interior rows, then
+    // the boundary rows): CTA slots bid_off.. of ncta_tot; the last CTA to arrive is in the last one
+    const int bid = blockIdx.x + bid_off, ncta = ncta_tot > 0 ? ncta_tot : (int)gridDim.x;
     // only the threads that wrote partials fence (a fence waits for ALL of the thread's
     // outstanding stores, e.g. its rows of the output vector, which need no ordering here)
     if (tid < nv) {
@@ -1005,7 +1007,8 @@ void launch_sdots(const SdotsArgs& a, int kmax, cudaStream_t s) {
     const bool k1_shape = a.A.nrows && a.out_mode <= 2 && a.set1 == 1 && (a.set2 == 0 || a.set2 == 2) &&
                           (a.norm1 >= 0 && a.norm1 <= 2) && a.norm2 == 0 && a.x_dyn == 0 && a.uout == nullptr;
     if (kmax > 0 && k1_shape) {
-        if (k1var() == 4 && kmax <= 24 && launch_step1_lean(a, kmax, s)) return;
+        const bool split = a.row0 != 0 || a.cta_tot != 0;  // row-range launches: rs2 / pipe only
+        if (!split && k1var() == 4 && kmax <= 24 && launch_step1_lean(a, kmax, s)) return;
         // pipelined K1: measured faster on long tile loops with a register-resident row (C5,
         // k <= 16: 10.98 vs 11.53 ms per inner step); equal or slower elsewhere
         if ((k1var() == 2 || (k1var() == 0 && kmax <= 16 && a.nrows >= (int64_t)1 << 24)) &&

@@ -84,7 +84,8 @@ __global__ void __launch_bounds__(CTA, 2) k_step1_rs2(const SdotsArgs a) {
     for (int g = 0; g < (DUAL ? KMAX / 8 : 1); ++g) cacc1[g][0] = cacc1[g][1] = 0.0;
     double n1 = 0.0;
     const int64_t nslices = (a.nrows + 31) >> 5;
-    const int64_t npairs = (nslices + 1) >> 1;
+    const int64_t sbeg = a.row0 >> 5;  // first tile of the row range
+    const int64_t npairs = (nslices - sbeg + 1) >> 1;
     auto tile = [&](int64_t sl, bool live, double& v1, double& o) {
         const int64_t row = sl * 32 + lane;
         const bool ok = live && row < a.nrows;
@@ -112,7 +113,7 @@ __global__ void __launch_bounds__(CTA, 2) k_step1_rs2(const SdotsArgs a) {
         v1 = a.set1 == 1 ? z : o;
     };
     for (int64_t pr = (int64_t)blockIdx.x * WARPS + warp; pr < npairs; pr += (int64_t)gridDim.x * WARPS) {
-        const int64_t s0 = 2 * pr, s1 = 2 * pr + 1;
+        const int64_t s0 = sbeg + 2 * pr, s1 = s0 + 1;
         const bool has1 = s1 < nslices;
         const int64_t r0 = s0 * 32 + lane, r1 = s1 * 32 + lane;
         const bool ok0 = r0 < a.nrows, ok1 = has1 && r1 < a.nrows;
@@ -201,7 +202,7 @@ __global__ void __launch_bounds__(CTA, 2) k_step1_rs2(const SdotsArgs a) {
     }
     __syncthreads();
     pdl_trigger();
-    if (!grid_reduce(res, nv, a.part, a.gpart, a.counter, a.maxcta, res)) return;
+    if (!grid_reduce(res, nv, a.part, a.gpart, a.counter, a.maxcta, res, a.cta_off, a.cta_tot)) return;
     if (a.red_local) {
         for (int v = threadIdx.x; v < nv; v += CTA) a.red_local[v] = res[v];
     } else {
@@ -246,7 +247,7 @@ static void launch_step1_rs_k(const SdotsArgs& a, cudaStream_t s) {
     const int smem2 = WARPS * 2 * 8 * WLD * (int)sizeof(double);
     auto kern2 = k_step1_rs2<KMAX, TWO>;
     NOTE_KERN(kern2);
-    launch_pdl(kern2, rs_grid(kern2, smem2, (a.nrows + 1) / 2), CTA, smem2, s, a);
+    launch_pdl(kern2, a.grid_force > 0 ? a.grid_force : rs_grid(kern2, smem2, (a.nrows - a.row0 + 1) / 2), CTA, smem2, s, a);
 }
 
 bool launch_step1_rs(const SdotsArgs& a, int kmax, cudaStream_t s) {

@@ -125,6 +125,11 @@ struct SdotsArgs {
     unsigned* counter; // [NCOUNTERS]
     int maxcta;
     double* red_local; // multi-rank: local sums instead of finalize (nullptr => finalize)
+    // row range split (halo overlap, K1 kernels k_step1_rs2 / k_step1_pipe): rows [row0, nrows)
+    // (row0 a multiple of 32); this launch's CTAs are partial slots cta_off.. of a reduction over
+    // cta_tot CTAs in several launches (0: this grid alone); grid_force > 0 fixes the grid size
+    int64_t row0;
+    int cta_off, cta_tot, grid_force;
 };
 
 // Arguments of the CGS update kernel (K2 / K3 / fix-up).

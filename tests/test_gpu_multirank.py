@@ -168,3 +168,32 @@ def test_loopback_ranks_block_kplus(gen, nranks):
     assert o0["st"]["a_matvecs"] == st1["a_matvecs"]
     assert list(o0["log"]["nprev"]) == list(log1["nprev"]) and max(log1["nprev"]) == 3
     assert np.max(np.abs(o0["ev"] - ev1) / np.abs(ev1)) <= 1e-10
+
+
+@pytest.mark.parametrize("name,N,nranks", [("C2", 24, 2), ("C5", 24, 3)])
+def test_loopback_halo_overlap(gen, orc, name, N, nranks):
+    """Halo overlap (engine run_k1_overlap): the exchange of g's boundary rows on a side stream
+    while K1 covers the interior rows, then K1 over the two boundary row ranges -- three launches
+    feeding one grid reduction.  Against the exchange-first K1 (TRPLK_HALO_OVERLAP=0): same matvec
+    count and trajectory structure, eigenvalues within 1e-10 relative (only the reduction's CTA
+    grouping differs), and against the oracle within 1e-9."""
+    import os
+    torch, trplk = need_gpu()
+    os.environ["TRPLK_HALO_OVERLAP"] = "0"
+    try:
+        off = _multirank(trplk, gen, name, N, nranks)
+    finally:
+        os.environ.pop("TRPLK_HALO_OVERLAP", None)
+    on = _multirank(trplk, gen, name, N, nranks)
+    a, b = on[0], off[0]
+    assert a["st"]["status"] == b["st"]["status"] == "OK"
+    assert a["st"]["a_matvecs"] == b["st"]["a_matvecs"]
+    for key in ("t", "k", "nprev"):
+        assert np.array_equal(a["log"][key], b["log"][key]), key
+    assert np.max(np.abs(a["ev"] - b["ev"]) / np.abs(b["ev"])) <= 1e-10
+    for o in on[1:]:
+        assert np.array_equal(o["ev"], a["ev"])
+    P = gen.make(name, N=N)
+    ro = orc.solve(P.A, P.B, P.p, P.q, P.l, P.tol, P.sigma, want_vectors=False)
+    assert np.max(np.abs(a["ev"] - ro["eigenvalues"]) / np.abs(ro["eigenvalues"])) <= 1e-9
+    assert np.all(a["rs"] <= P.tol)
