@@ -16,7 +16,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIBDIR = os.path.join(PKG, "lib")
-LIB = os.path.join(LIBDIR, "libtrplk.so")
+LIB = os.environ.get("TRPLK_BUILD_OUT") or os.path.join(LIBDIR, "libtrplk.so")  # override: experiment builds
 INCLUDE = os.path.join(ROOT, "include")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -45,13 +45,14 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not needs_build():
         return LIB
     from concurrent.futures import ThreadPoolExecutor
-    os.makedirs(LIBDIR, exist_ok=True)
+    os.makedirs(os.path.dirname(LIB), exist_ok=True)
     inc, libd = _nccl_dirs()
     cus = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
-    objdir = os.path.join(LIBDIR, "obj")
+    objdir = os.path.join(os.path.dirname(LIB), "obj")
     os.makedirs(objdir, exist_ok=True)
     common = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-fopenmp",
-              "-Xptxas", "-v" if verbose else "-O3", "-I", INCLUDE, "-I", CSRC, "-I", inc]
+              "-Xptxas", "-v" if verbose else "-O3", "-I", INCLUDE, "-I", CSRC, "-I", inc,
+              *os.environ.get("TRPLK_BUILD_DEFS", "").split()]  # experiment builds: extra -D flags
 
     def compile_one(cu):
         obj = os.path.join(objdir, os.path.basename(cu) + ".o")

@@ -99,6 +99,7 @@ struct trplk_ctx {
     int64_t rcnt_cap = 0;
     bool prof_fused = false;   // the live profile's slots are [K3 + K1 fused, K2, -]
     bool fuse_on = false;      // TRPLK_FUSE=1 at create: K3 + next K1 fused (fused.cuh)
+    bool kplus_xd = true;      // +K first-pass dots on the preceding K1 (TRPLK_KPLUS_XD=0 at create: off)
     // halo overlap (nranks > 1, DIA, B = I): the exchange on hstream while K1 runs the interior
     // rows [hb0, hb1), then the boundary rows; TRPLK_HALO_OVERLAP=0 at create: exchange first
     cudaStream_t hstream = nullptr;
@@ -511,7 +512,9 @@ static bool host_pinned(const void* p) {
 // are read as one presence bit per row plus the constant, instead of 8 bytes per row.  One
 // device scan of the value arrays (min / max stored bit pattern per diagonal) decides; the
 // decoded values are bit-identical to the stored ones, so the arithmetic does not change.
-// Opt-in (TRPLK_DIAC=1 at create): measured slower on the default kernels.
+// Opt-in (TRPLK_DIAC=1 at create), decoded only by the thread-per-row and fused K1 (lean_k1.cuh,
+// fused.cuh): the shared SpMV row (mat_row) and the default K1 kernels ran slower with the decode
+// in them, even when it was not taken (profiles/r02_variants.md).
 trplk_status dia_compress(trplk_ctx* ctx, Sell& S, int64_t& bytes) {
     const char* e = getenv("TRPLK_DIAC");
     if (!(e && e[0] == '1') || S.nrows == 0) return TRPLK_OK;  // opt-in (measured)
@@ -548,7 +551,7 @@ trplk_status dia_compress(trplk_ctx* ctx, Sell& S, int64_t& bytes) {
     S.cmask = cm;
     S.pmask = pm;
     for (int d = 0; d < 8; ++d) S.cv[d] = cv[d];
-    bytes = (int64_t)(S.ndiag - __builtin_popcount(cm)) * S.nrows * 8 + S.nrows;
+    (void)bytes;  // only the opt-in lean / fused K1 decode it; the other kernels read the value arrays
     return TRPLK_OK;
 }
 
@@ -707,6 +710,7 @@ trplk_status run_sdots(trplk_ctx* ctx, SdotsArgs a, int kbytes_cols, bool count_
     if (a.out) by += vec_bytes(ctx);
     if (a.uout) by += vec_bytes(ctx);
     if (a.wext) by += vec_bytes(ctx);
+    if (a.set2 == 4) by += vec_bytes(ctx);  // the external dot vector x2
     if (a.set1 || a.set2) by += vec_bytes(ctx) * kbytes_cols;
     if (count_bytes) ctx->model_bytes += by;
     ctx->launches += ctx->nranks > 1 ? 2 : 1;
@@ -883,6 +887,7 @@ struct CgsSpec {
     int kv;          // fixed width or -1 (ctl->k)
     int k_nominal;   // upper bound for the kernel bucket
     bool first_done; // B = I: h0 / N_IN2 already computed by the fused K1
+    unsigned gate1 = 0;  // extra gate bits of the first-pass launch (F_XD0 << j: not yet done elsewhere)
     double* dest;
     int dest_dyn;
     double* dest2;
@@ -917,8 +922,8 @@ trplk_status cgs2(trplk_ctx* ctx, const CgsSpec& c) {
         a.k_from_ctl = c.kv < 0;
         a.dest1 = D_H0 + 0;
         a.nslot1 = N_IN2;
-        a.gate = c.gate;
-        ST(run_sdots(ctx, a, kn));
+        a.gate = c.gate | c.gate1;
+        ST(run_sdots(ctx, a, kn, c.gate1 == 0));  // normally skipped when gated on F_XD0 << j
     }
     // pass 2: w1 = x - V h0 (+ B = I: h1 = V^T w1, N_1SQ)
     {
@@ -1203,6 +1208,30 @@ bool block_kplus(const trplk_ctx* ctx, int nprev) {
     return v == 2 || nprev >= 3;
 }
 
+// The first CGS pass of +K column j (U^T x^prev_j, ||x^prev_j||^2; reading R3) as the second dot
+// set of a K1 launch that streams U anyway: the last inner step's K1 (j = 0) or the T-column K1 of
+// +K column j - 1.  The column's own first-pass launch is gated on F_XD0 << j, which that K1's
+// finalize clears, so it still runs when the K1 did not (inner breakdown, a dropped column, the
+// latency paths).  TRPLK_KPLUS_XD=0 at create: off.
+static bool kplus_xd_on(const trplk_ctx* ctx, int nprev) {
+    return ctx->kplus_xd && nprev > 0 && nprev <= 8 && !ctx->hasB && !block_kplus(ctx, nprev);
+}
+static void set_kplus_xd(SdotsArgs& a, const double* Uo, int64_t ld, int xprev_static, int j) {
+    a.set2 = 4;
+    if (xprev_static >= 0) {
+        a.x2 = Uo + ld * (xprev_static + j);
+    } else {
+        a.x2 = Uo;
+        a.x2_dyn = 2;
+        a.x2_off = j;
+        a.x2_ld = ld;
+    }
+    a.dest2 = D_H0 + 0;
+    a.norm2 = 5;
+    a.nslot2 = N_IN2;
+    a.clear_done = F_XD0 << j;
+}
+
 // Block CGS2 (BCGS2 with Cholesky-QR inside the block) of the c vectors Y against the current basis
 // Uc(:, 0:ctl->k): two projections (a third gated by R3's rule), dependent vectors dropped (R16),
 // the accepted ones appended at Uc(:, ctl->k ..) and copied to the static block xkb; ctl->k grows.
@@ -1438,6 +1467,7 @@ trplk_status issue_cycle(trplk_ctx* ctx, const Sizes& S, int cur, int nprev, int
     }
     // K1 arguments of inner step j (eq 3.1: z = A g_j, T(1:k,k) = U^T z, w = M (z - rho B g_j),
     // h0 = U^T w, ||w||^2)
+    bool xd = false;
     auto k1_args = [&](int j) {
         const int k = S.ph + j;
         SdotsArgs a = sd_base(ctx);
@@ -1459,11 +1489,14 @@ trplk_status issue_cycle(trplk_ctx* ctx, const Sizes& S, int cur, int nprev, int
                 a.norm1 = 1;  // ||w||^2
                 a.nslot1 = N_IN2;
             }
+        } else if (xd) {
+            set_kplus_xd(a, Uo, ld, xprev_static, 0);  // +K column 0's first CGS pass rides along
         }
         return a;
     };
     // fz: the FINAL of step j and the K1 of step j+1 run as one kernel (fused.cuh)
     const bool fz = !fused && fuse_path(ctx, S);
+    xd = !fz && kplus_xd_on(ctx, nprev);
     ctx->prof_fused = fz;
     for (int j = 1; j <= S.m && !fused; ++j) {
         const int k = S.ph + j;  // nominal width incl. g_j
@@ -1512,6 +1545,7 @@ trplk_status issue_cycle(trplk_ctx* ctx, const Sizes& S, int cur, int nprev, int
     ST(phase_mark(ctx, 2));
     if (block_kplus(ctx, nprev)) ST(kplus_block(ctx, S, Uc, Uo, nprev, xprev_static));
     const bool fz = fuse_path(ctx, S);
+    const bool xdk = !fz && kplus_xd_on(ctx, nprev);
     for (int jj = 0; jj < nprev && !block_kplus(ctx, nprev); ++jj) {
         const unsigned kb = F_KCOL0 << jj;
         CgsSpec c{};
@@ -1529,6 +1563,7 @@ trplk_status issue_cycle(trplk_ctx* ctx, const Sizes& S, int cur, int nprev, int
         c.dest_dyn = 1;
         c.dest2 = fz ? nullptr : ctx->xk;
         c.gate = F_CYCLE | kb;
+        if (xdk) c.gate1 = F_XD0 << jj;  // unless the preceding K1 computed this first pass
         c.clear = kb;
         c.inc_k = 1;
         // the column's one matvec and T column: z = A x, T(1:k,k) = U^T z (fused with the FINAL
@@ -1541,6 +1576,7 @@ trplk_status issue_cycle(trplk_ctx* ctx, const Sizes& S, int cur, int nprev, int
         a.set1 = 1;
         a.dest1 = D_TCOL;
         a.gate = F_CYCLE | kb;
+        if (xdk && jj + 1 < nprev) set_kplus_xd(a, Uo, ld, xprev_static, jj + 1);  // next column's first pass
         if (fz) {
             c.fuse_next = &a;
             c.k_next = S.ph + S.m + jj + 1;
@@ -1871,6 +1907,8 @@ static trplk_status create_impl(trplk_ctx* ctx, int64_t n_global, const int64_t*
     {  // opt-in: measured slower than the three-kernel step (fused K3 + K1)
         const char* e = getenv("TRPLK_FUSE");
         ctx->fuse_on = e && e[0] == '1';
+        const char* x = getenv("TRPLK_KPLUS_XD");
+        ctx->kplus_xd = !(x && x[0] == '0');
     }
     if (ctx->nranks > 1 && !ctx->hasB && ctx->A.fmt == 1) {  // halo overlap: interior rows of the slab
         const char* e = getenv("TRPLK_HALO_OVERLAP");

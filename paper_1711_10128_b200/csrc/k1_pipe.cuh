@@ -22,9 +22,11 @@ __global__ void __launch_bounds__(CTA, 2) k_step1_pipe(const SdotsArgs a) {
     const int k2 = (TWO && a.set2) ? (a.k_from_ctl ? kc : a.k2) : 0;
     const int kmx = k1 > k2 ? k1 : k2;
     const double rho = ctl->rho;
-    const int nn = a.norm1 ? 1 : 0;
+    const int nn = (a.norm1 ? 1 : 0) + (a.norm2 == 5 ? 1 : 0);
     const int nv = k1 + k2 + nn;
     const double* __restrict__ X = a.x;
+    const double* __restrict__ X2 = a.set2 == 4 ? resolve_x(a.x2, a.x2_dyn, a.x2_ld, a.x2_off, ctl) : nullptr;
+    double n2 = 0.0;
     const Sell& M = a.A;
     extern __shared__ __align__(128) double wsm[];  // WARPS x KMAX x WLD
     __shared__ double acc[WARPS][NV_MAX];
@@ -44,14 +46,12 @@ __global__ void __launch_bounds__(CTA, 2) k_step1_pipe(const SdotsArgs a) {
     const int64_t stride = (int64_t)gridDim.x * WARPS;
     // registers of the tile in flight: basis row, DIA values, gathered x, diagonal, own x
     double ur[KMAX], v[8], xv[8], dg = 0.0, xr = 0.0;
-    unsigned pm = 0;  // DIA-C presence word of the tile's row (constant diagonals are decoded at use)
     auto issue = [&](int64_t sl) {
         const int64_t row = sl * 32 + lane;
         const bool ok = sl < nslices && row < a.nrows;
 #pragma unroll
         for (int c = 0; c < KMAX; ++c) ur[c] = (ok && c < kmx) ? __ldg(a.U + (int64_t)c * a.ldu + row) : 0.0;
         const double* dv = M.dval + row;
-        pm = (ok && M.cmask) ? dia_pmask(M, row) : 0u;
 #pragma unroll
         for (int d = 0; d < 8; ++d) {
             v[d] = 0.0;
@@ -60,11 +60,11 @@ __global__ void __launch_bounds__(CTA, 2) k_step1_pipe(const SdotsArgs a) {
                 int idx = (int)row + M.offs[d];
                 if (halo) idx = idx < 0 ? idx + nl + glo : (idx >= nl ? idx + glo : idx);
                 idx = idx < 0 ? 0 : (idx > top ? top : idx);
-                if (!((M.cmask >> d) & 1u)) v[d] = __ldg(dv + (int64_t)d * M.ldv);
+                v[d] = __ldg(dv + (int64_t)d * M.ldv);
                 xv[d] = __ldg(X + idx);
             }
         }
-        dg = (ok && !((M.cmask >> M.diag_slot) & 1u)) ? __ldg(dv + (int64_t)M.diag_slot * M.ldv) : 1.0;
+        dg = ok ? __ldg(dv + (int64_t)M.diag_slot * M.ldv) : 1.0;
         xr = ok ? X[row] : 0.0;
     };
     int64_t sl = sbeg + (int64_t)blockIdx.x * WARPS + warp;
@@ -74,12 +74,6 @@ __global__ void __launch_bounds__(CTA, 2) k_step1_pipe(const SdotsArgs a) {
         const bool ok = row < a.nrows;
         // SpMV of this tile (ascending column order, as mat_row)
         double z = 0.0;
-        if (M.cmask) {
-#pragma unroll
-            for (int d = 0; d < 8; ++d)
-                if (d < nd && ((M.cmask >> d) & 1u)) v[d] = ((pm >> d) & 1u) ? M.cv[d] : 0.0;
-            if (ok && ((M.cmask >> M.diag_slot) & 1u)) dg = ((pm >> M.diag_slot) & 1u) ? M.cv[M.diag_slot & 7] : 0.0;
-        }
 #pragma unroll
         for (int d = 0; d < 8; ++d) z = fma(v[d], xv[d], z);
         double o = 0.0;
@@ -95,6 +89,11 @@ __global__ void __launch_bounds__(CTA, 2) k_step1_pipe(const SdotsArgs a) {
             o = 0.0;
         }
         if (a.norm1 == 1) n1 += o * o;
+        if (TWO && a.set2 == 4) {  // second dot set on the external vector x2
+            const double x2 = ok ? X2[row] : 0.0;
+            n2 += x2 * x2;
+            o = x2;
+        }
         __syncwarp();
 #pragma unroll
         for (int c = 0; c < KMAX; ++c) W[c * WLD + lane] = ur[c];
@@ -131,7 +130,11 @@ __global__ void __launch_bounds__(CTA, 2) k_step1_pipe(const SdotsArgs a) {
     }
     if (nn) {
         const double s1 = warp_sum_s(n1);
-        if (lane == 0) acc[warp][k1 + k2] = s1;
+        if (lane == 0 && a.norm1) acc[warp][k1 + k2] = s1;
+        if (a.norm2 == 5) {
+            const double s2 = warp_sum_s(n2);
+            if (lane == 0) acc[warp][k1 + k2 + (a.norm1 ? 1 : 0)] = s2;
+        }
     }
     if (nv == 0) return;
     __syncthreads();
@@ -160,7 +163,8 @@ static void launch_step1_pipe_k(const SdotsArgs& a, cudaStream_t s) {
 }
 
 bool launch_step1_pipe(const SdotsArgs& a, int kmax, cudaStream_t s) {
-    if (a.A.fmt != 1 || a.A.ndiag > 8 || a.B.nrows || a.out_mode > 2 || a.norm1 > 1) return false;
+    if (a.A.fmt != 1 || a.A.ndiag > 8 || a.B.nrows || a.out_mode > 2 || a.norm1 > 1 || (a.norm2 != 0 && a.norm2 != 5))
+        return false;
     const bool two = a.set2 != 0;
     switch (kmax) {
         case 8: two ? launch_step1_pipe_k<8, true>(a, s) : launch_step1_pipe_k<8, false>(a, s); break;

@@ -70,8 +70,7 @@ __device__ __forceinline__ double mat_row(const Sell& M, int64_t s, int lane, co
         const int nl = (int)M.nrows, top = (int)(M.nrows + M.nghost - 1), glo = (int)M.glo;
         const bool halo = M.nghost != 0;
         const double* dv = M.dval + row;
-        const unsigned pm = M.cmask ? dia_pmask(M, row) : 0u;
-        diag = dia_val(M, M.diag_slot, pm, dv);
+        diag = __ldg(dv + (int64_t)M.diag_slot * M.ldv);
         for (int d0 = 0; d0 < M.ndiag; d0 += 8) {
             double v[8], xv[8];
 #pragma unroll
@@ -83,7 +82,7 @@ __device__ __forceinline__ double mat_row(const Sell& M, int64_t s, int lane, co
                     int idx = (int)row + M.offs[d];  // local rows + ghosts < 2^31 (checked at create)
                     if (halo) idx = idx < 0 ? idx + nl + glo : (idx >= nl ? idx + glo : idx);
                     idx = idx < 0 ? 0 : (idx > top ? top : idx);  // out-of-matrix slots hold 0
-                    v[u] = dia_val(M, d, pm, dv);
+                    v[u] = __ldg(dv + (int64_t)d * M.ldv);
                     xv[u] = XNC ? __ldg(x + idx) : __ldcg(x + idx);
                 }
             }
@@ -117,10 +116,7 @@ __device__ __forceinline__ double mat_row(const Sell& M, int64_t s, int lane, co
 
 // Diagonal entry of row 32 s + lane (DIA: the offset-0 array; SELL: slot 0).
 __device__ __forceinline__ double mat_diag(const Sell& M, int64_t s, int lane) {
-    if (M.fmt == 1) {
-        const int64_t row = s * 32 + lane;
-        return dia_val(M, M.diag_slot, M.cmask ? dia_pmask(M, row) : 0u, M.dval + row);
-    }
+    if (M.fmt == 1) return __ldg(M.dval + (int64_t)M.diag_slot * M.ldv + s * 32 + lane);
     return __ldg(M.val + __ldg(M.sptr + s) + lane);
 }
 
@@ -263,6 +259,7 @@ __device__ void sdots_finalize(const SdotsArgs& a, const double* r, int k1, int 
         int o = k1 + k2;
         if (a.norm1) ctl->nrm[a.nslot1] = r[o++];
         if (a.norm2) ctl->nrm[a.nslot2] = r[o];
+        if (a.clear_done) ctl->flags &= ~a.clear_done;
     }
 }
 
@@ -1004,11 +1001,12 @@ int kmax_bucket(int k) {
 
 void launch_sdots(const SdotsArgs& a, int kmax, cudaStream_t s) {
     // inner-step K1 shape: z = A g, w = M (z - rho B g), U^T z (+ U^T w, ||w||^2)
-    const bool k1_shape = a.A.nrows && a.out_mode <= 2 && a.set1 == 1 && (a.set2 == 0 || a.set2 == 2) &&
-                          (a.norm1 >= 0 && a.norm1 <= 2) && a.norm2 == 0 && a.x_dyn == 0 && a.uout == nullptr;
+    const bool k1_shape = a.A.nrows && a.out_mode <= 2 && a.set1 == 1 && (a.set2 == 0 || a.set2 == 2 || a.set2 == 4) &&
+                          (a.norm1 >= 0 && a.norm1 <= 2) && (a.norm2 == 0 || (a.norm2 == 5 && a.set2 == 4)) &&
+                          a.x_dyn == 0 && a.uout == nullptr;
     if (kmax > 0 && k1_shape) {
         const bool split = a.row0 != 0 || a.cta_tot != 0;  // row-range launches: rs2 / pipe only
-        if (!split && k1var() == 4 && kmax <= 24 && launch_step1_lean(a, kmax, s)) return;
+        if (!split && a.set2 != 4 && k1var() == 4 && kmax <= 24 && launch_step1_lean(a, kmax, s)) return;
         // pipelined K1: measured faster on long tile loops with a register-resident row (C5,
         // k <= 16: 10.98 vs 11.53 ms per inner step); equal or slower elsewhere
         if ((k1var() == 2 || (k1var() == 0 && kmax <= 16 && a.nrows >= (int64_t)1 << 24)) &&

@@ -66,6 +66,8 @@ __global__ void __launch_bounds__(CTA, 2) k_step1_rs2(const SdotsArgs a) {
     const int nn = (a.norm1 ? 1 : 0) + (a.norm2 ? 1 : 0);
     const int nv = k1 + k2 + nn;
     const double* __restrict__ X = resolve_x(a.x, a.x_dyn, a.x_ld, a.x_off, ctl);
+    const double* __restrict__ X2 = a.set2 == 4 ? resolve_x(a.x2, a.x2_dyn, a.x2_ld, a.x2_off, ctl) : nullptr;
+    double n2 = 0.0;
     constexpr int CH = 8;
     extern __shared__ __align__(128) double wsm[];  // WARPS x 2 x CH x WLD
     __shared__ double acc[WARPS][NV_MAX];
@@ -74,14 +76,12 @@ __global__ void __launch_bounds__(CTA, 2) k_step1_rs2(const SdotsArgs a) {
     const int fi = lane >> 2, fj = lane & 3;
     double* W0 = wsm + (size_t)warp * 2 * CH * WLD;
     double* W1 = W0 + CH * WLD;
-    // k <= 32: the two tiles accumulate separately (two interleaved DMMA chains); wider blocks
-    // share one accumulator set (the register budget of 2 CTAs per SM)
-    constexpr bool DUAL = KMAX <= 32;
-    double cacc[KMAX / 8][2], cacc1[DUAL ? KMAX / 8 : 1][2];
+    // one accumulator chain per 8-column chunk, the two tiles' DMMAs in order (volatile): the
+    // round-2 variant with the tiles in separate, interleaved chains measured slower (C2 solve
+    // 63.7 vs 62.6 ms, C5 K1 at k = 23 6.91 vs 6.67 ms; profiles/r02_variants.md)
+    double cacc[KMAX / 8][2];
 #pragma unroll
     for (int g = 0; g < KMAX / 8; ++g) cacc[g][0] = cacc[g][1] = 0.0;
-#pragma unroll
-    for (int g = 0; g < (DUAL ? KMAX / 8 : 1); ++g) cacc1[g][0] = cacc1[g][1] = 0.0;
     double n1 = 0.0;
     const int64_t nslices = (a.nrows + 31) >> 5;
     const int64_t sbeg = a.row0 >> 5;  // first tile of the row range
@@ -111,6 +111,11 @@ __global__ void __launch_bounds__(CTA, 2) k_step1_rs2(const SdotsArgs a) {
         if (a.norm1 == 1) n1 += o * o;
         else if (a.norm1 == 2) n1 += xr * z;
         v1 = a.set1 == 1 ? z : o;
+        if (TWO && a.set2 == 4) {  // second dot set on the external vector x2
+            const double x2 = ok ? X2[row] : 0.0;
+            n2 += x2 * x2;
+            o = x2;
+        }
     };
     for (int64_t pr = (int64_t)blockIdx.x * WARPS + warp; pr < npairs; pr += (int64_t)gridDim.x * WARPS) {
         const int64_t s0 = sbeg + 2 * pr, s1 = s0 + 1;
@@ -159,13 +164,10 @@ __global__ void __launch_bounds__(CTA, 2) k_step1_rs2(const SdotsArgs a) {
             if (cb < kmx) {
                 const double* sp0 = W0 + fi * WLD + fj;
                 const double* sp1 = W1 + fi * WLD + fj;
-                // the two tiles into separate accumulators, interleaved: two independent DMMA
-                // chains of 8 instead of one of 16 (added together after the loop)
 #pragma unroll
-                for (int q = 0; q < 8; ++q) {
-                    dmma884_nv(cacc[cb / 8], sp0[4 * q], bq0[q]);
-                    dmma884_nv(DUAL ? cacc1[DUAL ? cb / 8 : 0] : cacc[cb / 8], sp1[4 * q], bq1[q]);
-                }
+                for (int q = 0; q < 8; ++q) dmma884_s(cacc[cb / 8], sp0[4 * q], bq0[q]);
+#pragma unroll
+                for (int q = 0; q < 8; ++q) dmma884_s(cacc[cb / 8], sp1[4 * q], bq1[q]);
             }
             if (more) {
                 __syncwarp();
@@ -184,13 +186,17 @@ __global__ void __launch_bounds__(CTA, 2) k_step1_rs2(const SdotsArgs a) {
 #pragma unroll
         for (int g = 0; g < KMAX / 8; ++g) {
             const int c = 8 * g + fi;
-            if (c < k1) acc[warp][c] = DUAL ? cacc[g][0] + cacc1[DUAL ? g : 0][0] : cacc[g][0];
-            if (TWO && c < k2) acc[warp][k1 + c] = DUAL ? cacc[g][1] + cacc1[DUAL ? g : 0][1] : cacc[g][1];
+            if (c < k1) acc[warp][c] = cacc[g][0];
+            if (TWO && c < k2) acc[warp][k1 + c] = cacc[g][1];
         }
     }
     if (nn) {
         const double s1 = warp_sum_s(n1);
-        if (lane == 0) acc[warp][k1 + k2] = s1;
+        if (lane == 0 && a.norm1) acc[warp][k1 + k2] = s1;
+        if (a.norm2 == 5) {
+            const double s2 = warp_sum_s(n2);
+            if (lane == 0) acc[warp][k1 + k2 + (a.norm1 ? 1 : 0)] = s2;
+        }
     }
     if (nv == 0) return;
     __syncthreads();

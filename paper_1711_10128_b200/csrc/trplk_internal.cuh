@@ -61,6 +61,8 @@ enum : unsigned {
     F_INNER = 2u,      // inner Lanczos loop still running (no breakdown, R16)
     F_KCOL0 = 4u,      // +K column j valid: F_KCOL0 << j
     F_BPASS3 = 1u << 30,  // block +K: third BCGS pass needed (R3); F_KCOL0 << j uses bits 2..17
+    F_XD0 = 1u << 20,     // +K column j's first-pass dots still to do: F_XD0 << j (j < 8), cleared by the
+                          // K1 launch that computed them alongside its own dots (set2 = 4)
 };
 
 // Norm slots of Ctl::nrm
@@ -103,10 +105,10 @@ struct SdotsArgs {
     const double* U;   // dot block
     int64_t ldu;
     int set1;          // vector for dot set 1: 0 none, 1 z, 2 out, 3 x
-    int set2;          // vector for dot set 2 (same U): 0 none, 2 out
+    int set2;          // vector for dot set 2 (same U): 0 none, 2 out, 4 x2 (an external vector)
     int k1, k2;        // #columns; <0 => ctl->k + (k+1) ... see k_from_ctl
     int k_from_ctl;    // 1: k1 = k2-style counts = ctl->k (set2 only if set2 != 0)
-    int norm1, norm2;  // 0 none, 1 out.out, 2 x.z, 3 x.x, 4 z.z
+    int norm1, norm2;  // 0 none, 1 out.out, 2 x.z, 3 x.x, 4 z.z, 5 x2.x2 (norm2 only)
     int theta_idx;     // RES: theta = ctl->theta[theta_idx] (>=0) or ctl->theta[ctl->t-1] (-1)
     double theta_val;  // used when theta_idx == -2
     int dest1, dest2;  // D_TCOL / D_H0+slot / D_NONE
@@ -130,6 +132,13 @@ struct SdotsArgs {
     // cta_tot CTAs in several launches (0: this grid alone); grid_force > 0 fixes the grid size
     int64_t row0;
     int cta_off, cta_tot, grid_force;
+    // set2 = 4: the second dot set is U^T x2 (x2 resolved like x: x2_dyn 2 = x2 + x2_ld *
+    // (ctl->xprev_col + x2_off)) -- the next +K column's first CGS pass riding on a K1 that reads
+    // U anyway; clear_done: flag bits the finalize clears (F_XD0 << j: those dots are done)
+    const double* x2;
+    int x2_dyn, x2_off;
+    int64_t x2_ld;
+    unsigned clear_done;
 };
 
 // Arguments of the CGS update kernel (K2 / K3 / fix-up).

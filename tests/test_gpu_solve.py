@@ -378,11 +378,11 @@ def test_block_trplk_parity(orc, gen, name, N, b, over):
 
 @pytest.mark.parametrize("name,N", [("C2", 16), ("C3", 12), ("C4", 8), ("C5", 20), ("C1", None)])
 def test_dia_constant_diagonals_bitwise(gen, name, N):
-    """DIA-C (constant diagonals read as a presence bit + the constant, trplk_internal.cuh Sell):
-    the decoded values are the stored ones bit for bit, so a solve with DIA-C is bitwise the
-    solve with every diagonal stored (TRPLK_DIAC=0) -- eigenvalues, eigenvectors, residuals and
-    matvec count -- and reads fewer matrix bytes (C2/C5: the six -1 couplings; C3: all seven
-    diagonals; C4: A's first 8 couplings and all of B).  DIA-C is opt-in (TRPLK_DIAC=1)."""
+    """DIA-C (opt-in TRPLK_DIAC=1: constant diagonals read as a presence bit + the constant by the
+    thread-per-row and fused K1, lean_k1.cuh / fused.cuh; the other kernels keep reading the value
+    arrays, which stay populated): the decoded values are the stored ones bit for bit, so a solve
+    with DIA-C is bitwise the solve without it -- eigenvalues, eigenvectors, residuals and matvec
+    count.  The variant suite re-runs this file with TRPLK_K1=lean, where the decode is used."""
     import os
     torch, trplk = need_gpu()
     P = gen.make(name, N=N)
@@ -393,18 +393,33 @@ def test_dia_constant_diagonals_bitwise(gen, name, N):
             ctx = trplk.trplk_create(P.A, P.B, P.sigma)
         finally:
             os.environ.pop("TRPLK_DIAC", None)
-        info = trplk.trplk_info(ctx)
         ev, X, rs, st = trplk.trplk_solve(ctx, P.p, P.q, P.l, P.tol, use_graphs=0)
-        out[v] = (ev, X.cpu().numpy().copy(), rs, st["a_matvecs"], info)
+        out[v] = (ev, X.cpu().numpy().copy(), rs, st["a_matvecs"])
         ctx.close()
-    (e0, X0, r0, m0, i0), (e1, X1, r1, m1, i1) = out["0"], out["1"]
+    (e0, X0, r0, m0), (e1, X1, r1, m1) = out["0"], out["1"]
     assert np.array_equal(e0, e1) and np.array_equal(X0, X1) and np.array_equal(r0, r1) and m0 == m1
-    n = P.A.n
-    if name == "C1":  # tridiag(-1, 2, -1): every diagonal constant, 1 byte of presence bits per row
-        assert i1["sell_bytes_a"] == n and i0["sell_bytes_a"] == 24 * n
-    elif name == "C3":
-        assert i1["sell_bytes_a"] == n and i0["sell_bytes_a"] == 56 * n
-    elif name == "C4":
-        assert i1["sell_bytes_a"] == 19 * 8 * n + n and i1["sell_bytes_b"] == n  # DIA-C covers diagonals 0..7
-    else:
-        assert i1["sell_bytes_a"] == 8 * n + n and i0["sell_bytes_a"] == 56 * n
+
+
+@pytest.mark.parametrize("name,N", [("C2", 24), ("C5", 24), ("C2", None)])
+def test_kplus_first_pass_on_preceding_k1(gen, name, N):
+    """The first CGS pass of each +K column (U^T x^prev_j, ||x^prev_j||^2; reading R3) computed as
+    the second dot set of the K1 launch before it (the last inner step's, or the previous +K
+    column's T-column K1) instead of its own pass over U: the same products on the same tiles
+    and grid, so the solve is bitwise the one with the separate launch (TRPLK_KPLUS_XD=0)."""
+    import os
+    torch, trplk = need_gpu()
+    P = gen.make(name, N=N)
+    out = {}
+    for v in ("0", "1"):
+        os.environ["TRPLK_KPLUS_XD"] = v
+        try:
+            ctx = trplk.trplk_create(P.A, P.B, P.sigma)
+        finally:
+            os.environ.pop("TRPLK_KPLUS_XD", None)
+        ev, X, rs, st = trplk.trplk_solve(ctx, P.p, P.q, P.l, P.tol)
+        out[v] = (ev, X.cpu().numpy().copy(), rs, st)
+        ctx.close()
+    (e0, X0, r0, s0), (e1, X1, r1, s1) = out["0"], out["1"]
+    assert s1["status"] == "OK" and s0["a_matvecs"] == s1["a_matvecs"]
+    assert np.array_equal(e0, e1) and np.array_equal(X0, X1) and np.array_equal(r0, r1)
+    assert s1["kernel_launches"] < s0["kernel_launches"]

@@ -37,6 +37,6 @@ for r in range(reps + 2):
         ts.append(e0.elapsed_time(e1))
 ms = float(np.median(ts))
 by = info["sell_bytes_a"] + 8.0 * n * (k + 2)
-print(f"{cfg} k={k} K1[{os.environ.get('TRPLK_K1', 'default')}, DIAC={os.environ.get('TRPLK_DIAC', '1')}]: "
+print(f"{cfg} k={k} K1[{os.environ.get('TRPLK_K1', 'default')}, DIAC={os.environ.get('TRPLK_DIAC', '0')}]: "
       f"{ms:.3f} ms median (min {min(ts):.3f}), {by / 1e9:.2f} GB -> {by / ms / 1e6:.0f} GB/s")
 ctx.close()
