@@ -512,12 +512,13 @@ static bool host_pinned(const void* p) {
 // are read as one presence bit per row plus the constant, instead of 8 bytes per row.  One
 // device scan of the value arrays (min / max stored bit pattern per diagonal) decides; the
 // decoded values are bit-identical to the stored ones, so the arithmetic does not change.
-// Opt-in (TRPLK_DIAC=1 at create), decoded only by the thread-per-row and fused K1 (lean_k1.cuh,
-// fused.cuh): the shared SpMV row (mat_row) and the default K1 kernels ran slower with the decode
-// in them, even when it was not taken (profiles/r02_variants.md).
+// Decoded only by the thread-per-row and fused K1 (lean_k1.cuh, fused.cuh): the shared SpMV row
+// (mat_row) and the other K1 kernels ran slower with the decode in them, even when it was not
+// taken (profiles/r02_variants.md); they read the value arrays, which stay populated.
+// TRPLK_DIAC=0 at create: no presence bits.
 trplk_status dia_compress(trplk_ctx* ctx, Sell& S, int64_t& bytes) {
     const char* e = getenv("TRPLK_DIAC");
-    if (!(e && e[0] == '1') || S.nrows == 0) return TRPLK_OK;  // opt-in (measured)
+    if ((e && e[0] == '0') || S.nrows == 0) return TRPLK_OK;  // TRPLK_DIAC=0: off
     const int nd = S.ndiag < 8 ? S.ndiag : 8;
     double* tmp;
     ST(dalloc(ctx, &tmp, (size_t)2 * nd));

@@ -1006,7 +1006,11 @@ void launch_sdots(const SdotsArgs& a, int kmax, cudaStream_t s) {
                           a.x_dyn == 0 && a.uout == nullptr;
     if (kmax > 0 && k1_shape) {
         const bool split = a.row0 != 0 || a.cta_tot != 0;  // row-range launches: rs2 / pipe only
-        if (!split && a.set2 != 4 && k1var() == 4 && kmax <= 24 && launch_step1_lean(a, kmax, s)) return;
+        // thread-per-row K1 with the DIA-C decode: default for k <= 16 on slabs of >= 2^24 rows with
+        // constant diagonals (C5: 4.46 vs 4.72 ms for the pipelined kernel at k = 15), or forced
+        const bool lean_default = k1var() == 0 && kmax <= 16 && a.nrows >= ((int64_t)1 << 24) && a.A.cmask;
+        if (!split && a.set2 != 4 && (k1var() == 4 || lean_default) && kmax <= 24 && launch_step1_lean(a, kmax, s))
+            return;
         // pipelined K1: measured faster on long tile loops with a register-resident row (C5,
         // k <= 16: 10.98 vs 11.53 ms per inner step); equal or slower elsewhere
         if ((k1var() == 2 || (k1var() == 0 && kmax <= 16 && a.nrows >= (int64_t)1 << 24)) &&

@@ -262,17 +262,24 @@ def test_random_start_block_bit_exact(orc, problems):
         assert np.array_equal(x.cpu().numpy(), ref)
 
 
+@pytest.mark.parametrize("diac", ["1", "0"])
 @pytest.mark.parametrize("k", [8, 13, 16])
-def test_step1_pipe_full_slab(orc, gen, k):
-    """The K1 that C5 runs (k_step1_pipe: DIA, B = I, k <= 16, selected by default on slabs of
-    >= 2^24 rows) at a size that selects it: 257^3 = 16,974,593 rows (ragged last 32-row tile),
-    C5's matrix shape (7-pt + diag(d), d~U[0,10)).  Every output against the oracle's SpMV and
-    blocked dots over all rows: w normwise <= 1e-12, dots <= 1e-12 ||u|| ||v||."""
+def test_step1_pipe_full_slab(orc, gen, k, diac):
+    """The K1 that C5 runs for k <= 16 on slabs of >= 2^24 rows: the thread-per-row k_step1_lean
+    with the DIA-C decode (default), or k_step1_pipe when the matrix has no presence bits
+    (TRPLK_DIAC=0) -- at a size that selects them: 257^3 = 16,974,593 rows (ragged last 32-row
+    tile), C5's matrix shape (7-pt + diag(d), d~U[0,10)).  Every output against the oracle's SpMV
+    and blocked dots over all rows: w normwise <= 1e-12, dots <= 1e-12 ||u|| ||v||."""
+    import os
     torch, trplk = need_gpu()
     P = gen.make("C5", N=257)
     n = P.A.n
     assert n >= 1 << 24
-    ctx = trplk.trplk_create(P.A, P.B)
+    os.environ["TRPLK_DIAC"] = diac
+    try:
+        ctx = trplk.trplk_create(P.A, P.B)
+    finally:
+        os.environ.pop("TRPLK_DIAC", None)
     rng = np.random.default_rng(100 + k)
     U = np.asfortranarray(rng.standard_normal((n, k)) / np.sqrt(n))
     g = U[:, k - 1]
