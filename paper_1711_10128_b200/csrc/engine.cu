@@ -70,6 +70,7 @@ struct trplk_ctx {
     int pmode = 0;              // options.precond of the solve (2: per-cycle shifted Jacobi)
     Sell A, B;
     int64_t sellA_bytes = 0, sellB_bytes = 0, nnzA = 0, nnzB = 0;
+    int64_t sellA_bytes_dc = 0;  // A's bytes as read by the DIA-C kernels (kern_reads_diac)
     // halo plan (nranks > 1): per peer, recv range in the ghost tail and send rows
     std::vector<int> peers;
     std::vector<int64_t> recv_off, recv_cnt, send_cnt, send_start;
@@ -552,7 +553,10 @@ trplk_status dia_compress(trplk_ctx* ctx, Sell& S, int64_t& bytes) {
     S.cmask = cm;
     S.pmask = pm;
     for (int d = 0; d < 8; ++d) S.cv[d] = cv[d];
-    (void)bytes;  // only the opt-in lean / fused K1 decode it; the other kernels read the value arrays
+    // `bytes` stays the value arrays' (what every other kernel reads); the DIA-C kernels' count:
+    ctx->sellA_bytes_dc = (&S == &ctx->A) ? (int64_t)(S.ndiag - __builtin_popcount(cm)) * S.nrows * 8 + S.nrows
+                                          : ctx->sellA_bytes_dc;
+    (void)bytes;
     return TRPLK_OK;
 }
 
@@ -723,6 +727,8 @@ trplk_status run_sdots(trplk_ctx* ctx, SdotsArgs a, int kbytes_cols, bool count_
     } else {
         launch_sdots(a, kmax, ctx->stream);
     }
+    if (count_bytes && a.A.nrows && a.out_mode != 4 && kern_reads_diac(g_last_kern))
+        ctx->model_bytes -= (double)(ctx->sellA_bytes - ctx->sellA_bytes_dc);
     CK(cudaGetLastError());
     return TRPLK_OK;
 }
@@ -873,7 +879,7 @@ bool run_fused(trplk_ctx* ctx, const UpdArgs& u, const SdotsArgs& a, int kn, int
     for (int d = 0; d < ctx->A.ndiag; ++d) maxoff = std::max(maxoff, std::abs(ctx->A.offs[d]));
     if (!launch_fin_step1(f, kmax_bucket(std::max(k_next, 1)), maxoff, slack, ctx->stream)) return false;
     // bytes: FINAL (U(:, 1:kn), w', g) + the K1 without its U / g re-reads (L2): A, w
-    ctx->model_bytes += vec_bytes(ctx) * (kn + 2) + mat_bytes(ctx, false) + (a.out ? vec_bytes(ctx) : 0.0);
+    ctx->model_bytes += vec_bytes(ctx) * (kn + 2) + (double)ctx->sellA_bytes_dc + (a.out ? vec_bytes(ctx) : 0.0);
     ctx->launches += 1;
     return true;
 }
@@ -1880,6 +1886,7 @@ static trplk_status create_impl(trplk_ctx* ctx, int64_t n_global, const int64_t*
         }
     }
 
+    if (ctx->A.cmask == 0) ctx->sellA_bytes_dc = ctx->sellA_bytes;
     pt.mark("format");
     // fixed device buffers
     const size_t ld = (size_t)ctx->ld;
@@ -2378,11 +2385,12 @@ static trplk_status solve_impl(trplk_ctx* ctx, int p, int q, int l, double tol, 
                     // matrix bytes of the device format (DIA: 8 ndiag n; SELL: 12 per slot + slice ptrs)
                     const double spA = (double)ctx->sellA_bytes, spB = (double)ctx->sellB_bytes;
                     double b1, b2;
+                    const double spA1 = kern_reads_diac(ctx->prof_kern[0]) ? (double)ctx->sellA_bytes_dc : spA;
                     if (ctx->hasB) {
                         b1 = spA + spB + 8.0 * n * (k + 2);
                         b2 = 2 * (spB + 8.0 * n * (k + 1)) + 8.0 * n * (k + 2);
                     } else {
-                        b1 = spA + 8.0 * n * (k + 2);  // A, g, U(:,1:k), w (M folded from diag)
+                        b1 = spA1 + 8.0 * n * (k + 2);  // A (as the launched K1 reads it), g, U(:,1:k), w
                         b2 = 8.0 * n * (k + 2);        // U, w, w'
                     }
                     const double b3 = 8.0 * n * (k + 2);  // U, w', g_{j+1}
@@ -2394,7 +2402,7 @@ static trplk_status solve_impl(trplk_ctx* ctx, int p, int q, int l, double tol, 
                         e[0] = e[1];
                         e[1] = ek2;
                         e[2] = 0.0f;
-                        bb[0] = b3 + spA + 8.0 * n;
+                        bb[0] = b3 + (double)ctx->sellA_bytes_dc + 8.0 * n;
                         bb[1] = b2;
                         bb[2] = 0.0;
                     }

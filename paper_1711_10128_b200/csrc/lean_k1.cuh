@@ -148,6 +148,18 @@ static void launch_step1_lean_k(const SdotsArgs& a, cudaStream_t s) {
     launch_pdl(kern, rs_grid(kern, 0, a.nrows), CTA, 0, s, a);
 }
 
+bool kern_reads_diac(const void* k) {
+    const void* ks[] = {
+        (const void*)k_step1_lean<8, true, true>,    (const void*)k_step1_lean<8, false, true>,
+        (const void*)k_step1_lean<16, true, false>,  (const void*)k_step1_lean<16, false, false>,
+        (const void*)k_step1_lean<24, true, false>,  (const void*)k_step1_lean<24, false, false>,
+        (const void*)k_fin_step1<8>,  (const void*)k_fin_step1<16>, (const void*)k_fin_step1<24>,
+        (const void*)k_fin_step1<32>, (const void*)k_fin_step1<40>, (const void*)k_fin_step1<48>};
+    for (const void* x : ks)
+        if (x == k) return true;
+    return false;
+}
+
 // DIA (<= 8 diagonals), B = I, out_mode 0 / 2, ||w||^2 only; k <= 24.  PF for k <= 16.
 bool launch_step1_lean(const SdotsArgs& a, int kmax, cudaStream_t s) {
     if (a.A.fmt != 1 || a.A.ndiag > 8 || a.B.nrows || a.out_mode == 1 || a.out_mode > 2 || a.norm1 > 1 ||

@@ -184,6 +184,9 @@ struct FusedArgs {
 };
 bool launch_fin_step1(const FusedArgs& f, int kmax, int maxoff, int slack, cudaStream_t s);
 bool launch_step1_lean(const SdotsArgs& a, int kmax, cudaStream_t s);
+// true for the kernels that read a DIA-C matrix's presence bits instead of its constant diagonals
+// (k_step1_lean, k_fin_step1): their algorithmic matrix bytes are the compressed ones
+bool kern_reads_diac(const void* kern);
 
 // ------------------------------------------------------------- block kernels (block.cuh)
 constexpr int BC = 8;                                // vectors per block launch (DMMA n = 8)
