@@ -74,7 +74,8 @@ class _Pl1Report(ctypes.Structure):
                 ("rho", ctypes.c_double), ("resid", ctypes.c_double),
                 ("log_cap", ctypes.c_int), ("log_len", ctypes.c_int),
                 ("log_rho", _P), ("log_res", _P), ("log_conj", _P), ("log_ritz", _P),
-                ("log_mg", _P), ("log_nq", _P)]
+                ("log_mg", _P), ("log_nq", _P),
+                ("qopt_cap", ctypes.c_int), ("log_qopt", _P), ("log_qdim", _P), ("log_g", _P)]
 
 
 _lib = None
@@ -293,9 +294,11 @@ def ic0(A, B=None, sigma=0.0):
 
 
 def pl1_solve(A, B=None, m=4, tol=1e-8, sigma=0.0, seed=12, x0=None, max_cycles=2000, variant=0,
-              use_precond=True):
+              use_precond=True, qopt_cap=0, want_g=False):
     """Run Algorithm 2 (PL+1) for the lowest eigenpair of (A, B), readings P1-P6.  Returns a dict
-    with rho, x (B-normalised), residual norm, counters and the per-iteration log."""
+    with rho, x (B-normalised), residual norm, counters and the per-iteration log.  qopt_cap > 0:
+    also the quasi-optimality diagnostic (P7, Def. defnglbopt) in log["qopt"]
+    (rho(y*_k) over U_k) and log["qdim"] (dim U_k) for k < qopt_cap; want_g: g_k in "g" (n x cap)."""
     ra, ca, va = _csr(A)
     rb, cb, vb = _csr(B)
     n = len(ra) - 1
@@ -305,11 +308,22 @@ def pl1_solve(A, B=None, m=4, tol=1e-8, sigma=0.0, seed=12, x0=None, max_cycles=
     cap = max_cycles + 1
     logs = {"rho": np.zeros(cap), "res": np.zeros(cap), "conj": np.zeros(cap), "ritz": np.zeros(cap),
             "mg": np.zeros(cap, np.int32), "nq": np.zeros(cap, np.int32)}
+    qo = np.zeros(max(qopt_cap, 1))
+    qd = np.zeros(max(qopt_cap, 1), np.int32)
+    gl = np.zeros((max(qopt_cap, 1), n)) if (want_g and qopt_cap > 0) else None
     rep = _Pl1Report(0, 0, 0, 0, 0.0, 0.0, cap, 0, _ptr(logs["rho"]), _ptr(logs["res"]),
-                     _ptr(logs["conj"]), _ptr(logs["ritz"]), _ptr(logs["mg"]), _ptr(logs["nq"]))
+                     _ptr(logs["conj"]), _ptr(logs["ritz"]), _ptr(logs["mg"]), _ptr(logs["nq"]),
+                     qopt_cap, _ptr(qo), _ptr(qd), _ptr(gl))
     x = np.zeros(n)
     st = lib().orc_pl1_solve(ctypes.byref(prob), _ptr(x), ctypes.byref(rep))
     L = rep.log_len
-    return {"status": STATUS.get(st, st), "rho": rep.rho, "x": x, "residual": rep.resid,
-            "cycles": rep.cycles, "a_matvecs": rep.a_matvecs, "b_matvecs": rep.b_matvecs,
-            "log": {k_: v[:L].copy() for k_, v in logs.items()}}
+    out = {"status": STATUS.get(st, st), "rho": rep.rho, "x": x, "residual": rep.resid,
+           "cycles": rep.cycles, "a_matvecs": rep.a_matvecs, "b_matvecs": rep.b_matvecs,
+           "log": {k_: v[:L].copy() for k_, v in logs.items()}}
+    if qopt_cap > 0:
+        Lq = min(L, qopt_cap)
+        out["log"]["qopt"] = qo[:Lq].copy()
+        out["log"]["qdim"] = qd[:Lq].copy()
+        if gl is not None:
+            out["g"] = gl[:max(Lq - 1, 0)].T.copy()
+    return out

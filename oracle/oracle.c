@@ -743,6 +743,10 @@ done:
  *     explicit product when Q_k is formed.  A-matvecs: 1 (x_0) + per iteration m (A g_j) +
  *     1 (A x_{k+1}) + [k > 0] (A p_{k-1}).
  *  P6 x_0(i) = u01(seed, 3, i) (R13 generator, stream 3), then B-normalised (step 2).
+ *  P7 quasi-optimality diagnostic (Def. defnglbopt): rho(y*_k) = min of the
+ *     Rayleigh quotient over U_k = span{x_0} + span{g_0..g_{k-1}}, from a
+ *     B-orthonormal basis of U_k (CGS2_B, g_j dropped at the R16 threshold) and the smallest
+ *     eigenvalue of Z^T A Z.  lambda_1 of the ratio is the caller's (e.g. the converged rho).
  * ===================================================================================== */
 
 /* S = L L^T in place (lower triangle of L, column-major nq x nq); returns the index of the
@@ -807,6 +811,23 @@ int orc_pl1_solve(const orc_pl1_problem* P, double* x_out, orc_pl1_report* rep) 
     double res = sqrt(orc_dot(n, r, r));
     double rho_prev = rho;  /* rho(x_{k-1}) for step 7 (P4) */
     double conj_next = 0.0;
+    /* quasi-optimality diagnostic (P7): B-orthonormal basis Z of U_k, Hz = Z^T A Z */
+    const int qcap = (rep && rep->log_qopt && rep->log_qdim) ? rep->qopt_cap : 0;
+    ctx_t cq = {&Q, n, 0, 0, 0};  /* its own counters: not the algorithm's matvecs */
+    double *Z = NULL, *Hz = NULL, *Tq = NULL, *Yq = NULL, *thq = NULL, *vq = NULL, *Bvq = NULL, *Azq = NULL;
+    int dq = 0;
+    if (qcap > 0) {
+        Z = malloc(nb * qcap); Hz = calloc((size_t)qcap * qcap, sizeof(double));
+        Tq = malloc(sizeof(double) * qcap * qcap); Yq = malloc(sizeof(double) * qcap * qcap);
+        thq = malloc(sizeof(double) * qcap);
+        vq = malloc(nb); Bvq = malloc(nb); Azq = malloc(nb);
+        memcpy(Z, x, nb);  /* U_0 = span{x_0}, x_0 B-normalised */
+        applyA(&cq, Z, Azq);
+        Hz[0] = orc_dot(n, Z, Azq);
+        dq = 1;
+        rep->log_qopt[0] = Hz[0];
+        rep->log_qdim[0] = 1;
+    }
 
     for (k = 0;; ++k) {
         if (rep && k < rep->log_cap) {
@@ -903,6 +924,23 @@ int orc_pl1_solve(const orc_pl1_problem* P, double* x_out, orc_pl1_report* rep) 
             g[i] = s;
             xt[i] = w[0] * x[i] + s + (use_p ? w[nq - 1] * p[i] : 0.0);
         }
+        if (qcap > 0 && k + 1 < qcap) {  /* U_{k+1} = U_k + span{g_k} (P7) */
+            if (rep->log_g) memcpy(rep->log_g + (size_t)n * k, g, nb);
+            memcpy(vq, g, nb);
+            double bq;
+            if (!cgs2_ctx(&cq, dq, Z, vq, Bvq, NULL, &bq, NULL)) {
+                double* zd = Z + (size_t)n * dq;
+                for (int64_t i = 0; i < n; ++i) zd[i] = vq[i] / bq;
+                applyA(&cq, zd, Azq);
+                for (int i = 0; i <= dq; ++i) Hz[i + qcap * dq] = Hz[dq + qcap * i] = orc_dot(n, Z + (size_t)n * i, Azq);
+                ++dq;
+            }
+            for (int jj = 0; jj < dq; ++jj)
+                for (int i = 0; i < dq; ++i) Tq[i + dq * jj] = Hz[i + qcap * jj];
+            if (orc_sym_eig(dq, Tq, thq, Yq) < 0) { status = 3; break; }
+            rep->log_qopt[k + 1] = thq[0];
+            rep->log_qdim[k + 1] = dq;
+        }
         applyB(&c, xt, tmp);
         const double nxt = sqrt(orc_dot(n, xt, tmp));
         const double rho_k = rho;
@@ -948,5 +986,6 @@ int orc_pl1_solve(const orc_pl1_problem* P, double* x_out, orc_pl1_report* rep) 
     (void)qmax;
     free(M); free(x); free(Ax); free(Bx); free(r); free(p); free(Ap); free(Bp); free(v); free(tmp);
     free(g); free(xt); free(d); free(G); free(AG); free(BG);
+    free(Z); free(Hz); free(Tq); free(Yq); free(thq); free(vq); free(Bvq); free(Azq);
     return status;
 }

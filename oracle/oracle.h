@@ -143,6 +143,16 @@ typedef struct {
     double* log_ritz;       /* lowest Ritz value of step 5 at iteration k (entry k), or 0 */
     int* log_mg;            /* columns of G_k built at iteration k (entry k; < m after a breakdown) */
     int* log_nq;            /* columns of Q_k used in the RR at iteration k (p dropped if dependent) */
+    /* Global quasi-optimality diagnostic (Definition defnglbopt; reading P7):
+     * U_k = span{x_0} + W_k, W_k = span{g_0, ..., g_{k-1}}.  Entry k (k <
+     * qopt_cap): log_qopt[k] = rho(y*_k), the minimum of the Rayleigh quotient over U_k;
+     * log_qdim[k] = dim U_k as built (g_j B-orthonormalised by CGS2 against the earlier basis and
+     * dropped when dependent, the R16 threshold).  log_g (optional, n x qopt_cap column-major):
+     * column k = g_k of step 6.  qopt_cap = 0: off.  The diagnostic's matvecs are not counted. */
+    int qopt_cap;
+    double* log_qopt;
+    int* log_qdim;
+    double* log_g;
 } orc_pl1_report;
 
 /* Algorithm 2.  x_out (n, may be NULL): the final B-normalised iterate. */

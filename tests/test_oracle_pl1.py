@@ -149,3 +149,69 @@ def test_matvec_accounting(orc, gen):
     K = r["cycles"]
     assert np.all(r["log"]["mg"][:K] == m)
     assert r["a_matvecs"] == 1 + K * (m + 1) + (K - 1)
+
+
+# ---------------------------------------------------------------- quasi-optimality diagnostic (P7)
+# Definition defnglbopt: rho(y*_k) = min of the Rayleigh quotient over
+# U_k = span{x_0} + span{g_0, ..., g_{k-1}}.
+
+
+def test_qopt_brute_force_generalized(orc, gen):
+    """rho(y*_k) of the oracle = the lowest Ritz value of (A, B) on the explicitly stacked
+    [x_0, g_0, ..., g_{k-1}] (numpy QR + scipy generalized eigh), C4-shaped pencil (B != I)."""
+    P = gen.make("C4", N=6)
+    A = P.A.to_scipy().toarray()
+    B = P.B.to_scipy().toarray()
+    n = A.shape[0]
+    x0 = np.random.default_rng(7).random(n)
+    cap = 10
+    r = orc.pl1_solve(P.A, P.B, m=2, tol=1e-300, sigma=P.sigma, max_cycles=cap - 1, x0=x0,
+                      qopt_cap=cap, want_g=True)
+    q, dim, G = r["log"]["qopt"], r["log"]["qdim"], r["g"]
+    assert len(q) == cap and G.shape == (n, cap - 1)
+    assert np.array_equal(dim, np.arange(1, cap + 1))
+    for k in range(cap):
+        ref = _min_rq(A, B, np.column_stack([x0] + [G[:, j] for j in range(k)]))
+        assert abs(q[k] - ref) <= 1e-10 * abs(ref), (k, q[k], ref)
+
+
+@pytest.mark.parametrize("m", [1, 3])
+def test_qopt_special_cases(orc, gen, m):
+    """rho(y*_0) = rho_0 (U_0 = span{x_0}); x_1 is the RR minimiser over span{x_0, G_0} which
+    contains U_1, so rho(y*_1) = rho_1; for m = 1, U_2 = span{x_1, g_1, p_0} (section 4.3), so
+    rho(y*_2) = rho_2; always lambda_1 <= rho(y*_k) <= rho_k and rho(y*_k) nonincreasing.  The
+    diagnostic leaves the trajectory and the matvec counts untouched."""
+    P = gen.make("C2", N=8)
+    A = P.A.to_scipy().toarray()
+    lam1 = np.linalg.eigvalsh(A)[0]
+    base = orc.pl1_solve(P.A, None, m=m, tol=1e-9, sigma=P.sigma)
+    r = orc.pl1_solve(P.A, None, m=m, tol=1e-9, sigma=P.sigma, qopt_cap=64)
+    assert r["a_matvecs"] == base["a_matvecs"] and r["b_matvecs"] == base["b_matvecs"]
+    assert np.array_equal(r["log"]["rho"], base["log"]["rho"])
+    rho, q = r["log"]["rho"], r["log"]["qopt"]
+    K = len(q)
+    assert K == min(len(rho), 64) and K >= 4
+    eps = 1e-13 * abs(lam1)
+    assert abs(q[0] - rho[0]) <= eps
+    assert abs(q[1] - rho[1]) <= eps
+    if m == 1:
+        assert abs(q[2] - rho[2]) <= eps
+    assert np.all(q <= rho[:K] + eps) and np.all(q >= lam1 - eps)
+    assert np.all(np.diff(q) <= eps)
+
+
+def test_qopt_full_space(orc):
+    """Dense n = 6, m = 1: once dim U_k = n, rho(y*_k) = lambda_1 to rounding, and later g_k
+    (inside U_k) are dropped by the R16 dependence test so dim U_k stays n."""
+    rng = np.random.default_rng(11)
+    n = 6
+    Q, _ = np.linalg.qr(rng.standard_normal((n, n)))
+    lam = np.array([1.0, 1.5, 2.0, 3.0, 5.0, 8.0])
+    A = Q @ np.diag(lam) @ Q.T
+    A = 0.5 * (A + A.T)
+    r = orc.pl1_solve(_csr_dense(A), None, m=1, tol=1e-300, max_cycles=12, use_precond=False,
+                      x0=rng.random(n), qopt_cap=13)
+    q, dim = r["log"]["qopt"], r["log"]["qdim"]
+    full = np.nonzero(dim == n)[0]
+    assert len(full) >= 2 and np.all(dim <= n) and np.all(np.diff(dim) >= 0)
+    assert np.all(np.abs(q[full] - lam[0]) <= 1e-13 * lam[0])
