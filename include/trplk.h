@@ -164,6 +164,22 @@ trplk_status trplk_pl1_solve(trplk_ctx* ctx, int m, double tol, int variant, int
                              int log_cap, double* log_rho, double* log_res, double* log_conj, int* log_len,
                              trplk_stats* stats);
 
+/* PL+1 global quasi-optimality diagnostic (Definition defnglbopt; reading P7
+ * of DESIGN.md).  trplk_pl1_set_qopt(ctx, cap), 0 <= cap <= 64 (0 = off, the default), arms it
+ * for the context's later trplk_pl1_solve calls: entry k < cap records rho(y*_k), the minimum of
+ * the Rayleigh quotient over U_k = span{x_0} + span{g_0, ..., g_{k-1}} (g_k of
+ * Alg. 2 step 6), from a B-orthonormal basis of U_k kept on the device (CGS2_B; g_k dropped on
+ * the R16 breakdown test) and the lowest eigenvalue of Z^T A Z (the Jacobi eig kernel).  Costs,
+ * per iteration, one CGS2_B, one A-SpMV and one Gram column (eager launches between the
+ * iteration graphs, not counted in stats), plus 8 n_local x cap bytes of device memory.
+ * Returns EINVAL for cap outside [0, 64].
+ * trplk_pl1_get_qopt: of the last PL+1 solve, entries k = 0 .. ret-1 (ret <= cap):
+ *   rho_star[k] = rho(y*_k);  dim[k] = dim U_k;  ratio[k] = (rho_k - rho(y*_k)) / (rho_k - lambda1),
+ *   NaN where rho_k <= lambda1 (lambda1 = NaN: the solve's last rho_k).  Any pointer may be NULL
+ *   (host arrays).  Returns 0 when the diagnostic was off. */
+trplk_status trplk_pl1_set_qopt(trplk_ctx* ctx, int cap);
+int trplk_pl1_get_qopt(const trplk_ctx* ctx, int cap, double lambda1, double* rho_star, int* dim, double* ratio);
+
 /* Per-cycle log of the last solve (SURVEY 8(c.2) "Log per cycle"); any pointer may be NULL.
  * Arrays have capacity cap (thetas: cap x p^, row-major).  Returns the number of cycles logged. */
 int trplk_get_log(const trplk_ctx* ctx, int cap, int* t, int64_t* mv, double* theta_t,

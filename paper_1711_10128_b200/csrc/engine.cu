@@ -135,6 +135,10 @@ struct trplk_ctx {
     double phase_ms[6] = {0, 0, 0, 0, 0, 0};
     int64_t phase_count = 0;
     int prof_k = 0;
+    // PL+1 quasi-optimality diagnostic (P7): capacity (0 = off) and the last solve's log
+    int qopt_cap = 0;
+    std::vector<double> qopt_star, qopt_rho;
+    std::vector<int> qopt_dim;
 };
 
 namespace {
@@ -2671,6 +2675,44 @@ static trplk_status pl1_impl(trplk_ctx* ctx, int m, double tol, int variant, int
     pl1_res(n, Ax, Bx, sc + 1, sc + 2, r, st);
     ST(dots({{{r, r}, 3}}));
     pl1_shift_rho(dv, sc, st);  // rho_cur = rho_0
+    // quasi-optimality diagnostic (P7, Def. defnglbopt): B-orthonormal basis Z
+    // of U_k = span{x_0} + span{g_0..g_{k-1}} and Hz = Z^T A Z, extended between iterations
+    // (eager launches outside the iteration graphs; matvecs, launches and bytes not counted)
+    const int qcap = std::min(ctx->qopt_cap, QMAX);
+    double *Z = nullptr, *Hz = nullptr, *Azq = nullptr, *qstar = nullptr;
+    int dq = 0;
+    ctx->qopt_star.clear();
+    ctx->qopt_rho.clear();
+    ctx->qopt_dim.clear();
+    auto gram_col = [&](const double* Az, int col) -> trplk_status {  // Hz(0:col, col) = Z^T (A z_col)
+        SdotsArgs a = sd_base(ctx);
+        a.x = Az;
+        a.set1 = 3;
+        a.U = Z;
+        a.k1 = col + 1;
+        a.dest1 = D_TCOL;
+        a.tcol_fixed = col;
+        a.T = Hz;
+        a.ldT = QMAX;
+        return run_sdots(ctx, a, col + 1, false);
+    };
+    if (qcap > 0) {
+        ST(dalloc(ctx, &Z, (size_t)ld * qcap));
+        ST(dalloc(ctx, &Hz, (size_t)QMAX * QMAX));
+        ST(dalloc(ctx, &Azq, (size_t)ld));
+        ST(dalloc(ctx, &qstar, (size_t)qcap));
+        CK(cudaMemsetAsync(Z, 0, 8 * (size_t)ld * qcap, st));
+        CK(cudaMemsetAsync(Hz, 0, 8 * (size_t)QMAX * QMAX, st));
+        CK(cudaMemsetAsync(Azq, 0, 8 * (size_t)ld, st));
+        CK(cudaMemcpyAsync(Z, x, 8 * (size_t)n, cudaMemcpyDeviceToDevice, st));  // U_0 = span{x_0}
+        const double mb = ctx->model_bytes;
+        const int64_t la = ctx->launches;
+        ST(gram_col(Ax, 0));
+        ctx->model_bytes = mb;
+        ctx->launches = la;
+        dq = 1;
+        ctx->qopt_dim.push_back(1);
+    }
     ST(read_sc());
     double rho = h[1] / h[2], res = std::sqrt(h[3]);
     double rho_prev = rho, conj_next = 0.0;
@@ -2681,6 +2723,7 @@ static trplk_status pl1_impl(trplk_ctx* ctx, int m, double tol, int variant, int
     double gbytes[2] = {0.0, 0.0};
     int64_t glaunch[2] = {0, 0}, gamv[2] = {0, 0}, gbmv[2] = {0, 0};
     for (k = 0;; ++k) {
+        if (k < qcap) ctx->qopt_rho.push_back(rho);
         if (k < log_cap) {
             if (log_rho) log_rho[k] = rho;
             if (log_res) log_res[k] = res;
@@ -2845,6 +2888,57 @@ static trplk_status pl1_impl(trplk_ctx* ctx, int m, double tol, int variant, int
         rho_prev = rho;
         rho = h[1] / h[2];
         res = std::sqrt(h[3]);
+        if (k + 1 < qcap) {  // P7: U_{k+1} = U_k + span{g_k}; g_k dropped on a CGS2 breakdown (R16)
+            const double mb = ctx->model_bytes;
+            const int64_t la = ctx->launches;
+            const int brk0 = H.brk;
+            CgsSpec cs{};
+            cs.x = g;
+            cs.V = Z;
+            cs.kv = dq;
+            cs.k_nominal = dq;
+            cs.dest = Z + ld * dq;
+            cs.dest_dyn = 0;
+            cs.gate = 0;
+            cs.clear = 0;
+            cs.inc_k = 0;
+            ST(cgs2(ctx, cs));
+            ST(ctl_pull(ctx));
+            if (H.brk == brk0) {
+                ST(halo(ctx, Z + ld * dq));
+                SdotsArgs a = sd_base(ctx);
+                a.A = ctx->A;
+                a.x = Z + ld * dq;
+                a.out_mode = 1;
+                a.out = Azq;
+                ST(run_sdots(ctx, a, 0, false));
+                ST(gram_col(Azq, dq));
+                ++dq;
+            }
+            ctx->qopt_dim.push_back(dq);
+            ctx->model_bytes = mb;
+            ctx->launches = la;
+        }
+    }
+    if (qcap > 0) {  // rho(y*_k) = lowest eigenvalue of the leading dim(U_k) block of Hz (P7)
+        const int nq = (int)ctx->qopt_dim.size();
+        pl1_qmirror(Hz, QMAX, dq, st);
+        for (int j = 0; j < nq; ++j) {
+            const int d = ctx->qopt_dim[j];
+            if (j > 0 && d == ctx->qopt_dim[j - 1]) {
+                CK(cudaMemcpyAsync(qstar + j, qstar + j - 1, 8, cudaMemcpyDeviceToDevice, st));
+            } else if (d == 1) {
+                CK(cudaMemcpyAsync(qstar + j, Hz, 8, cudaMemcpyDeviceToDevice, st));
+            } else {
+                launch_eig(ctx->ctl, Hz, QMAX, ctx->Yg, QMAX, 0, d, 0, st);
+                CK(cudaMemcpyAsync(qstar + j, &ctx->ctl->theta[0], 8, cudaMemcpyDeviceToDevice, st));
+            }
+        }
+        ctx->qopt_star.resize(nq);
+        CK(cudaMemcpyAsync(ctx->qopt_star.data(), qstar, 8 * (size_t)nq, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        ctx->qopt_rho.resize(std::min(ctx->qopt_rho.size(), (size_t)nq));
+        for (void* b : {(void*)Z, (void*)Hz, (void*)Azq, (void*)qstar}) dev_free(ctx, b);
     }
     CK(cudaEventRecord(e1, st));
     CK(cudaEventSynchronize(e1));
@@ -2890,6 +2984,32 @@ trplk_status trplk_pl1_solve(trplk_ctx* ctx, int m, double tol, int variant, int
                                     log_cap, log_rho, log_res, log_conj, log_len, stats);
     leave_stream(ctx);
     return s;
+}
+
+trplk_status trplk_pl1_set_qopt(trplk_ctx* ctx, int cap) {
+    if (!ctx) return TRPLK_EINVAL;
+    if (cap < 0 || cap > QMAX) {
+        ctx->err = "PL+1 quasi-optimality diagnostic: needs 0 <= cap <= 64";
+        return TRPLK_EINVAL;
+    }
+    ctx->qopt_cap = cap;
+    return TRPLK_OK;
+}
+
+int trplk_pl1_get_qopt(const trplk_ctx* ctx, int cap, double lambda1, double* rho_star, int* dim, double* ratio) {
+    if (!ctx) return 0;
+    const int n = std::min<int>(cap, (int)std::min(ctx->qopt_star.size(), ctx->qopt_rho.size()));
+    if (n <= 0) return 0;
+    const double lam = std::isnan(lambda1) ? ctx->qopt_rho[n - 1] : lambda1;
+    for (int j = 0; j < n; ++j) {
+        if (rho_star) rho_star[j] = ctx->qopt_star[j];
+        if (dim) dim[j] = ctx->qopt_dim[j];
+        if (ratio) {
+            const double den = ctx->qopt_rho[j] - lam;
+            ratio[j] = den > 0.0 ? (ctx->qopt_rho[j] - ctx->qopt_star[j]) / den : NAN;
+        }
+    }
+    return n;
 }
 
 // ------------------------------------------------------------ kernel-level entry points

@@ -324,6 +324,15 @@ __global__ void k_pl1_dvec(int64_t n, const double* Ap, const double* Bp, const 
         v[i] = Ap[i] - r * Bp[i];
 }
 
+// quasi-optimality diagnostic (P7): H(j, i) = H(i, j) for i < j < d (the Gram columns fill i <= j)
+__global__ void k_pl1_qmirror(double* H, int ldH, int d) {
+    for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < d * d; idx += gridDim.x * blockDim.x) {
+        const int i = idx % d, j = idx / d;
+        if (i < j) H[j + (int64_t)i * ldH] = H[i + (int64_t)j * ldH];
+    }
+}
+
+void pl1_qmirror(double* H, int ldH, int d, cudaStream_t st) { k_pl1_qmirror<<<4, 256, 0, st>>>(H, ldH, d); }
 void pl1_begin(Ctl* ctl, cudaStream_t st) { k_pl1_begin<<<1, 1, 0, st>>>(ctl); }
 void pl1_shift_rho(Pl1Dev* d, const double* sc, cudaStream_t st) { k_pl1_shift_rho<<<1, 1, 0, st>>>(d, sc); }
 void pl1_dvec(int64_t n, const double* Ap, const double* Bp, const Pl1Dev* d, double* v, cudaStream_t st) {

@@ -314,6 +314,7 @@ struct Pl1Pairs {
 constexpr int PL1_PART = 296 * 72;  // partials of pl1_dots / pl1_gram (296 CTAs x 2 NT, NC <= 8)
 void pl1_prec(const Sell& A, const Sell& B, int64_t n, double sigma, double mfloor, const double* z,
               const double* s, const double* rho, double* v, int prec, cudaStream_t st);
+void pl1_qmirror(double* H, int ldH, int d, cudaStream_t st);     // mirror the upper d x d triangle (P7)
 void pl1_begin(Ctl* ctl, cudaStream_t st);                         // ctl->k = 0, flags = ~0, pass3 = 0
 void pl1_shift_rho(Pl1Dev* d, const double* sc, cudaStream_t st);  // rho_prev = rho_cur; rho_cur = sc1/sc2
 void pl1_dvec(int64_t n, const double* Ap, const double* Bp, const Pl1Dev* d, double* v, cudaStream_t st);

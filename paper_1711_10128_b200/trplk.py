@@ -107,6 +107,8 @@ _sig("trplk_profile_phases", _I, [_P, _P, ctypes.POINTER(_I64)])
 _sig("trplk_k_block", _I, [_P, _I, _P, _I64, _I, _P, _I64, _I, _P, _P, _P, _I64, _P, _P])
 _sig("trplk_pl1_solve", _I, [_P, _I, _D, _I, _I, _I, ctypes.c_uint64, _P, _P, _P, _P, _I, _P, _P, _P, _P,
                              ctypes.POINTER(Stats)])
+_sig("trplk_pl1_set_qopt", _I, [_P, _I])
+_sig("trplk_pl1_get_qopt", _I, [_P, _I, _D, _P, _P, _P])
 
 EXPORTED = ["trplk_options_default", "trplk_nccl_unique_id", "trplk_create", "trplk_solve",
             "trplk_get_log", "trplk_info", "trplk_destroy", "trplk_last_error", "trplk_k_spmv",
@@ -114,7 +116,7 @@ EXPORTED = ["trplk_options_default", "trplk_nccl_unique_id", "trplk_create", "tr
             "trplk_k_residual", "trplk_k_random", "trplk_profile", "trplk_profile_read",
             "trplk_plan_ghosts", "trplk_k_sym_eig_time", "trplk_loopback_create", "trplk_loopback_destroy",
             "trplk_set_debug", "trplk_pl1_solve", "trplk_profile_kernels", "trplk_create_ex",
-            "trplk_profile_phases", "trplk_k_block"]
+            "trplk_profile_phases", "trplk_k_block", "trplk_pl1_set_qopt", "trplk_pl1_get_qopt"]
 
 
 class TrplkError(RuntimeError):
@@ -418,6 +420,18 @@ def trplk_pl1_solve(ctx: Context, m: int, tol: float, variant: int = 0, use_prec
         ctx.check(st)
     L = nlog.value
     return rho.value, res.value, x, stats.as_dict(), {"rho": lr[:L], "res": ls[:L], "conj": lc[:L]}
+
+
+def trplk_pl1_set_qopt(ctx: Context, cap: int):
+    """Arm (cap > 0, <= 64) or disarm (0) the PL+1 quasi-optimality diagnostic (reading P7)."""
+    ctx.check(_lib.trplk_pl1_set_qopt(ctx.handle, int(cap)))
+
+
+def trplk_pl1_get_qopt(ctx: Context, cap: int = 64, lambda1: float = float("nan")):
+    """Of the last PL+1 solve: {rho_star, dim, ratio} per iteration (entry k = U_k)."""
+    rs, dm, ra = np.zeros(cap), np.zeros(cap, np.int32), np.zeros(cap)
+    L = _lib.trplk_pl1_get_qopt(ctx.handle, int(cap), float(lambda1), _ptr(rs), _ptr(dm), _ptr(ra))
+    return {"rho_star": rs[:L], "dim": dm[:L], "ratio": ra[:L]}
 
 
 def trplk_get_log(ctx: Context, cap: int = 100000, ph: Optional[int] = None):

@@ -111,8 +111,10 @@ def _pl1_rank(trplk, inputs, name, N, hub, rank, nranks, out, m):
     try:
         ctx = trplk.trplk_create(P.A, P.B, P.sigma, n_global=n, row_begin=rb, row_end=re,
                                  loopback=(hub, rank, nranks))
+        trplk.trplk_pl1_set_qopt(ctx, 40)  # the P7 diagnostic rides along (rank reductions)
         rho, res, x, st, log = trplk.trplk_pl1_solve(ctx, m, P.tol)
-        out[rank] = {"rho": rho, "res": res, "x": x.cpu().numpy().copy(), "st": st, "log": log}
+        out[rank] = {"rho": rho, "res": res, "x": x.cpu().numpy().copy(), "st": st, "log": log,
+                     "qopt": trplk.trplk_pl1_get_qopt(ctx)}
         ctx.close()
     except Exception as e:  # reported by the main thread
         out[rank] = e
@@ -140,8 +142,13 @@ def test_pl1_loopback_ranks(gen, orc, name, N, nranks):
     for o in out[1:]:
         assert o["rho"] == out[0]["rho"] and o["st"]["cycles"] == out[0]["st"]["cycles"]
     P = gen.make(name, N=N)
-    r = orc.pl1_solve(P.A, P.B, m=m, tol=P.tol, sigma=P.sigma)
+    r = orc.pl1_solve(P.A, P.B, m=m, tol=P.tol, sigma=P.sigma, qopt_cap=40)
     o0 = out[0]
+    for o in out[1:]:
+        assert np.array_equal(o["qopt"]["rho_star"], o0["qopt"]["rho_star"])
+    assert np.array_equal(o0["qopt"]["dim"], r["log"]["qdim"])
+    rq = r["log"]["qopt"]
+    assert np.max(np.abs(o0["qopt"]["rho_star"] - rq) / np.abs(rq)) <= 1e-10
     assert o0["st"]["status"] == "OK" and r["status"] == "OK"
     assert o0["st"]["cycles"] == r["cycles"] and o0["st"]["a_matvecs"] == r["a_matvecs"]
     assert abs(o0["rho"] - r["rho"]) <= 1e-12 * abs(r["rho"])

@@ -107,3 +107,36 @@ def test_pl1_wide_block_and_breakdown(orc, gen):
     assert o["log"]["mg"][0] == 2
     assert st["cycles"] == o["cycles"] == 0 and st["a_matvecs"] == o["a_matvecs"]
     assert abs(rho - o["rho"]) <= 1e-14
+
+
+@pytest.mark.parametrize("name,N,m", [("C2", 16, 4), ("C2", 12, 1), ("C4", 8, 2), ("C3", 10, 3)])
+def test_pl1_quasi_optimality(orc, gen, name, N, m):
+    """Global quasi-optimality diagnostic (reading P7, Def. defnglbopt) on the
+    device against the oracle: the same dim U_k sequence, rho(y*_k) to 1e-10 relative, the ratio
+    (rho_k - rho(y*_k)) / (rho_k - lambda_1) to 1e-5 where rho_k - lambda_1 > 1e-4 |lambda_1|;
+    arming it leaves the PL+1 trajectory bit-identical."""
+    torch, trplk = need_gpu()
+    P = gen.make(name, N=N)
+    tol = 1e-9
+    ctx = trplk.trplk_create(P.A, P.B, P.sigma)
+    rho0, _, x0, st0, log0 = trplk.trplk_pl1_solve(ctx, m, tol)
+    x0 = x0.cpu().numpy().copy()
+    assert trplk.trplk_pl1_get_qopt(ctx)["rho_star"].size == 0  # off by default
+    trplk.trplk_pl1_set_qopt(ctx, 64)
+    rho, _, x, st, log = trplk.trplk_pl1_solve(ctx, m, tol)
+    q = trplk.trplk_pl1_get_qopt(ctx)
+    ctx.close()
+    assert rho == rho0 and np.array_equal(log["rho"], log0["rho"])
+    assert np.array_equal(x.cpu().numpy(), x0)
+    assert st["a_matvecs"] == st0["a_matvecs"] and st["kernel_launches"] == st0["kernel_launches"]
+    o = orc.pl1_solve(P.A, P.B, m=m, tol=tol, sigma=P.sigma, qopt_cap=64)
+    oq, od = o["log"]["qopt"], o["log"]["qdim"]
+    assert len(q["rho_star"]) == len(oq) == min(len(log["rho"]), 64) >= 3
+    assert np.array_equal(q["dim"], od)
+    assert np.max(np.abs(q["rho_star"] - oq) / np.abs(oq)) <= 1e-10
+    lam = o["rho"]
+    orat = (o["log"]["rho"][:len(oq)] - oq) / (o["log"]["rho"][:len(oq)] - lam)
+    sel = (o["log"]["rho"][:len(oq)] - lam) > 1e-4 * abs(lam)
+    assert sel.sum() >= 2
+    assert np.max(np.abs(q["ratio"][sel] - orat[sel])) <= 1e-5
+    assert np.all(q["ratio"][sel] >= -1e-6) and np.all(q["ratio"][sel] <= 1 + 1e-6)
