@@ -7,7 +7,9 @@
 // block with mma.sync.m8n8k4.f64: the A operand (Y^T, <= 3 x 16 fragments) stays in registers
 // for the whole kernel, the B operand (U^T: lane (kk, n) = U[8 rb + n, 4 ks + kk]) comes from
 // the slab, and the accumulator holds 2 consecutive rows of one output column per lane,
-// written as one 16-byte store.  The ncu capture of the register-fragment version at C5 showed
+// written as one 16-byte store.  The slab is double-buffered and filled by cp.async, so the next
+// tile streams in during the current tile's DMMA (round 2; C3 k_rotate_s<3,48> was at 0.62 of
+// the copy peak with alternating load / compute phases).  The ncu capture of the register-fragment version at C5 showed
 // lg_throttle + long_scoreboard stalls: its loads touched 4 columns x 64 bytes per instruction.
 // Included by kernels.cu after stream_rs.cuh (WLD, dmma884_s).
 #pragma once
@@ -15,7 +17,7 @@
 namespace trplk {
 
 template <int NJ, int KMAX>
-__global__ void __launch_bounds__(CTA, (NJ * KMAX > 64) ? 1 : 2) k_rotate_s(const double* __restrict__ U, int64_t ldu, int64_t nrows,
+__global__ void __launch_bounds__(CTA, (NJ * KMAX > 64 || KMAX >= 32) ? 1 : 2) k_rotate_s(const double* __restrict__ U, int64_t ldu, int64_t nrows,
                                                      const Ctl* ctl, int k_fixed, const double* __restrict__ Y,
                                                      int ldY, int ncol, double* __restrict__ X, int64_t ldx,
                                                      unsigned gate) {
@@ -36,15 +38,34 @@ __global__ void __launch_bounds__(CTA, (NJ * KMAX > 64) ? 1 : 2) k_rotate_s(cons
         }
     const bool vec = ((reinterpret_cast<uintptr_t>(X) & 15) == 0) && ((ldx & 1) == 0);
     const int64_t ntile = (nrows + 31) >> 5;
-    for (int64_t t = (int64_t)blockIdx.x * WARPS + warp; t < ntile; t += (int64_t)gridDim.x * WARPS) {
-        const int64_t r0 = t * 32, row = r0 + lane;
+    const int64_t tstride = (int64_t)gridDim.x * WARPS;
+    // Two slabs per warp, filled by cp.async (LDGSTS, no register staging): the next tile's
+    // KMAX x 256 B are in flight while the current one goes through the DMMA.  Columns >= k and
+    // rows >= nrows are zero-filled (src-size 0).
+    auto fill = [&](int64_t t, double* Wb) {
+        const int64_t row = t * 32 + lane;
         const bool ok = row < nrows;
-        double ur[KMAX];
 #pragma unroll
-        for (int c = 0; c < KMAX; ++c) ur[c] = (ok && c < k) ? __ldg(U + (int64_t)c * ldu + row) : 0.0;
-        __syncwarp();
-#pragma unroll
-        for (int c = 0; c < KMAX; ++c) W[c * WLD + lane] = ur[c];
+        for (int c = 0; c < KMAX; ++c) {
+            const bool v = ok && c < k;
+            const double* src = v ? U + (int64_t)c * ldu + row : U;
+            const unsigned dst = (unsigned)__cvta_generic_to_shared(Wb + c * WLD + lane);
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(dst), "l"(src), "r"(v ? 8 : 0)
+                         : "memory");
+        }
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+    };
+    int64_t t = (int64_t)blockIdx.x * WARPS + warp;
+    if (t < ntile) fill(t, W);
+    for (int it = 0; t < ntile; t += tstride, ++it) {
+        const int64_t r0 = t * 32;
+        double* Wc = W + (it & 1) * (WARPS * KMAX * WLD);
+        if (t + tstride < ntile) {
+            fill(t + tstride, W + ((it + 1) & 1) * (WARPS * KMAX * WLD));
+            asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+        } else {
+            asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+        }
         __syncwarp();
 #pragma unroll
         for (int rb = 0; rb < 4; ++rb) {
@@ -53,7 +74,7 @@ __global__ void __launch_bounds__(CTA, (NJ * KMAX > 64) ? 1 : 2) k_rotate_s(cons
             for (int jb = 0; jb < NJ; ++jb) acc[jb][0] = acc[jb][1] = 0.0;
 #pragma unroll
             for (int ks = 0; ks < KS4; ++ks) {
-                const double b = W[(4 * ks + lq) * WLD + 8 * rb + lr];
+                const double b = Wc[(4 * ks + lq) * WLD + 8 * rb + lr];
 #pragma unroll
                 for (int jb = 0; jb < NJ; ++jb) dmma884_s(acc[jb], yf[jb][ks], b);
             }
@@ -72,6 +93,7 @@ __global__ void __launch_bounds__(CTA, (NJ * KMAX > 64) ? 1 : 2) k_rotate_s(cons
                 }
             }
         }
+        __syncwarp();  // every lane is done with Wc before the next iteration refills it
     }
 }
 
@@ -79,7 +101,7 @@ template <int NJ, int KMAX>
 static void rot_s(const double* U, int64_t ldu, int64_t nrows, const Ctl* ctl, int k_fixed, const double* Y,
                   int ldY, int ncol, double* X, int64_t ldx, unsigned gate, cudaStream_t s) {
     auto kern = k_rotate_s<NJ, KMAX>;
-    const int smem = WARPS * KMAX * WLD * (int)sizeof(double);
+    const int smem = 2 * WARPS * KMAX * WLD * (int)sizeof(double);  // two slabs per warp
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     int occ = 1, nsm = 148, dev = 0;
     cudaGetDevice(&dev);

@@ -342,3 +342,22 @@ def test_block_kernels_gram_upd_spmm(orc, problems, case, k, c):
     HVo = np.array([[orc.dot(U[:, i], Z[:, j]) for j in range(c)] for i in range(k)])
     assert np.all(np.abs(HV - HVo) <= 1e-12 * np.outer(un, np.linalg.norm(Z, axis=0)))
     ctx.close()
+
+
+@pytest.mark.parametrize("ncol,k", [(20, 48), (24, 40), (8, 32), (10, 24), (3, 16)])
+def test_rotate_dmma_pipelined(orc, gen, ncol, k):
+    """K5 with several 32-row tiles per warp (the cp.async double-buffered slab: the next tile
+    streams in while the current one is in the DMMA) and a ragged tail (65^3 = 274,625 rows,
+    one row past a tile boundary), against the oracle's triple loop."""
+    torch, trplk = need_gpu()
+    P = gen.make("C2", N=65)
+    n = P.A.n
+    assert n % 32 == 1
+    ctx = _ctx(trplk, P)
+    rng = np.random.default_rng(ncol * 1000 + k)
+    U = rng.standard_normal((n, k))
+    Y = rng.standard_normal((k, ncol))
+    X = torch.zeros((ncol, ctx.ld), dtype=torch.float64, device="cuda")
+    trplk.trplk_k_rotate(ctx, to_dev(torch, U, ctx.ld), ctx.ld, k, Y, ncol, X, ctx.ld)
+    Xo = orc.rotate(U, Y)
+    assert normwise(X.cpu().numpy()[:, :n].T, Xo) <= 1e-13
