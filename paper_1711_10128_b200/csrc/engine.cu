@@ -138,6 +138,7 @@ struct trplk_ctx {
     // PL+1 quasi-optimality diagnostic (P7): capacity (0 = off) and the last solve's log
     int qopt_cap = 0;
     std::vector<double> qopt_star, qopt_rho;
+    double qopt_last = 0.0;  // the solve's last rho_k (the default lambda1 of trplk_pl1_get_qopt)
     std::vector<int> qopt_dim;
 };
 
@@ -2724,6 +2725,7 @@ static trplk_status pl1_impl(trplk_ctx* ctx, int m, double tol, int variant, int
     int64_t glaunch[2] = {0, 0}, gamv[2] = {0, 0}, gbmv[2] = {0, 0};
     for (k = 0;; ++k) {
         if (k < qcap) ctx->qopt_rho.push_back(rho);
+        ctx->qopt_last = rho;
         if (k < log_cap) {
             if (log_rho) log_rho[k] = rho;
             if (log_res) log_res[k] = res;
@@ -2950,6 +2952,7 @@ static trplk_status pl1_impl(trplk_ctx* ctx, int m, double tol, int variant, int
         if (ge) cudaGraphExecDestroy(ge);
     if (x_out) CK(cudaMemcpyAsync(x_out, x, 8 * (size_t)n, cudaMemcpyDefault, st));
     CK(cudaStreamSynchronize(st));
+    ctx->qopt_last = rho;
     if (rho_out) *rho_out = rho;
     if (resid_out) *resid_out = res;
     if (log_len) *log_len = nlog;
@@ -3000,7 +3003,7 @@ int trplk_pl1_get_qopt(const trplk_ctx* ctx, int cap, double lambda1, double* rh
     if (!ctx) return 0;
     const int n = std::min<int>(cap, (int)std::min(ctx->qopt_star.size(), ctx->qopt_rho.size()));
     if (n <= 0) return 0;
-    const double lam = std::isnan(lambda1) ? ctx->qopt_rho[n - 1] : lambda1;
+    const double lam = std::isnan(lambda1) ? ctx->qopt_last : lambda1;
     for (int j = 0; j < n; ++j) {
         if (rho_star) rho_star[j] = ctx->qopt_star[j];
         if (dim) dim[j] = ctx->qopt_dim[j];

@@ -7,9 +7,11 @@
 // block with mma.sync.m8n8k4.f64: the A operand (Y^T, <= 3 x 16 fragments) stays in registers
 // for the whole kernel, the B operand (U^T: lane (kk, n) = U[8 rb + n, 4 ks + kk]) comes from
 // the slab, and the accumulator holds 2 consecutive rows of one output column per lane,
-// written as one 16-byte store.  The slab is double-buffered and filled by cp.async, so the next
-// tile streams in during the current tile's DMMA (round 2; C3 k_rotate_s<3,48> was at 0.62 of
-// the copy peak with alternating load / compute phases).  The ncu capture of the register-fragment version at C5 showed
+// written as one 16-byte store.  For KMAX >= 32 the slab is double-buffered and filled by
+// cp.async, so the next tile streams in during the current tile's DMMA (round 2; measured alone:
+// C3 k = 32 3.98 -> 4.54 TB/s, k = 48 3.83 -> 3.88, C2 k = 30 1.51 -> 1.58; narrower bases keep
+// the register-staged single slab, two CTAs per SM: C5 k = 24 5.43 TB/s against 4.91 pipelined).
+// The ncu capture of the register-fragment version at C5 showed
 // lg_throttle + long_scoreboard stalls: its loads touched 4 columns x 64 bytes per instruction.
 // Included by kernels.cu after stream_rs.cuh (WLD, dmma884_s).
 #pragma once
@@ -39,9 +41,12 @@ __global__ void __launch_bounds__(CTA, (NJ * KMAX > 64 || KMAX >= 32) ? 1 : 2) k
     const bool vec = ((reinterpret_cast<uintptr_t>(X) & 15) == 0) && ((ldx & 1) == 0);
     const int64_t ntile = (nrows + 31) >> 5;
     const int64_t tstride = (int64_t)gridDim.x * WARPS;
-    // Two slabs per warp, filled by cp.async (LDGSTS, no register staging): the next tile's
-    // KMAX x 256 B are in flight while the current one goes through the DMMA.  Columns >= k and
-    // rows >= nrows are zero-filled (src-size 0).
+    // KMAX >= 32: two slabs per warp, filled by cp.async (LDGSTS, no register staging): the next
+    // tile's KMAX x 256 B are in flight while the current one goes through the DMMA.  Columns >= k
+    // and rows >= nrows are zero-filled (src-size 0).  KMAX < 32: one slab filled through
+    // registers, two CTAs per SM (measured: C5 k = 24 rotation 5.4 TB/s against 4.9 pipelined,
+    // C3 k = 32 4.5 against 4.0 the other way; profiles/r02_variants.md).
+    constexpr bool PIPE = KMAX >= 32;
     auto fill = [&](int64_t t, double* Wb) {
         const int64_t row = t * 32 + lane;
         const bool ok = row < nrows;
@@ -56,15 +61,26 @@ __global__ void __launch_bounds__(CTA, (NJ * KMAX > 64 || KMAX >= 32) ? 1 : 2) k
         asm volatile("cp.async.commit_group;\n" ::: "memory");
     };
     int64_t t = (int64_t)blockIdx.x * WARPS + warp;
-    if (t < ntile) fill(t, W);
+    if (PIPE && t < ntile) fill(t, W);
     for (int it = 0; t < ntile; t += tstride, ++it) {
         const int64_t r0 = t * 32;
-        double* Wc = W + (it & 1) * (WARPS * KMAX * WLD);
-        if (t + tstride < ntile) {
-            fill(t + tstride, W + ((it + 1) & 1) * (WARPS * KMAX * WLD));
-            asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+        double* Wc = PIPE ? W + (it & 1) * (WARPS * KMAX * WLD) : W;
+        if (PIPE) {
+            if (t + tstride < ntile) {
+                fill(t + tstride, W + ((it + 1) & 1) * (WARPS * KMAX * WLD));
+                asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+            } else {
+                asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+            }
         } else {
-            asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+            const int64_t row = r0 + lane;
+            const bool ok = row < nrows;
+            double ur[PIPE ? 1 : KMAX];
+#pragma unroll
+            for (int c = 0; c < (PIPE ? 1 : KMAX); ++c) ur[c] = (ok && c < k) ? __ldg(U + (int64_t)c * ldu + row) : 0.0;
+            __syncwarp();
+#pragma unroll
+            for (int c = 0; c < (PIPE ? 1 : KMAX); ++c) W[c * WLD + lane] = ur[c];
         }
         __syncwarp();
 #pragma unroll
@@ -101,7 +117,7 @@ template <int NJ, int KMAX>
 static void rot_s(const double* U, int64_t ldu, int64_t nrows, const Ctl* ctl, int k_fixed, const double* Y,
                   int ldY, int ncol, double* X, int64_t ldx, unsigned gate, cudaStream_t s) {
     auto kern = k_rotate_s<NJ, KMAX>;
-    const int smem = 2 * WARPS * KMAX * WLD * (int)sizeof(double);  // two slabs per warp
+    const int smem = (KMAX >= 32 ? 2 : 1) * WARPS * KMAX * WLD * (int)sizeof(double);  // KMAX >= 32: two slabs per warp
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     int occ = 1, nsm = 148, dev = 0;
     cudaGetDevice(&dev);
