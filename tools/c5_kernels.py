@@ -1,7 +1,8 @@
 """The inner-step kernels at the C5 size, launched alone through the kernel-level C ABI
 (include/trplk_kernels.h) -- for ncu --set full captures (a full C5 solve has ~5,700 launches, too
 many to run under the profiler's interception).  Same instantiations the C5 solve runs:
-  K1  trplk_k_step1 at k = 15           -> k_step1_pipe<16, 1>   (z = A g, w = M(z - rho g), U^T [z w])
+  K1  trplk_k_step1 at k = 15           -> k_step1_lean<16, 1, 0> (z = A g, w = M(z - rho g), U^T [z w]; DIA-C)
+  K1  trplk_k_step1 at k = 23           -> k_step1_rs2<24, 1>
   K2  trplk_k_cgs2 at k = 15, pass 2    -> k_upd2_wp2<8, 2>     (w' = w - U h1, U^T w', ||w'||^2)
   K3  trplk_k_cgs2 at k = 15, final     -> k_upd<16, 0>         (g = (w' - U h2) / beta)
   +K  trplk_k_cgs2 at k = 23, pass 1    -> k_step1_tp<24, 1, 0, 0> (U^T x, the +K / seed dots)
@@ -39,6 +40,7 @@ def main(reps):
         trplk.trplk_k_cgs2(ctx, U, ld, 15, w, out)
         trplk.trplk_k_cgs2(ctx, U, ld, 23, w, out)
         trplk.trplk_k_rotate(ctx, U, ld, 24, Y, 8, X, ld)
+        trplk.trplk_k_step1(ctx, U, ld, 23, U[22], 2.5, w)  # k > 16: k_step1_rs2<24, 1>
         torch.cuda.synchronize()
         print(f"round {time.perf_counter() - t0:.3f} s", flush=True)
     ctx.close()
