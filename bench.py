@@ -387,9 +387,12 @@ def main():
     times, stats = [], []
     for it in range(args.steps):
         # the live kernel profile (CUDA event nodes around the middle inner step of every cycle)
-        # serialises that step's kernels; it runs on every timed step (the headline carries its
-        # cost: +2 % at C2, below 0.1 % at C5), or on the last one with --profile-last-only
-        if it == (args.steps - 1 if args.profile_last_only else 0):
+        # serialises that step's kernels.  HBM-sized problems (n >= 2^21: C3-C5; cost below
+        # 0.3 %): on every timed step.  The latency-bound ones (C1, C2), whose kernels otherwise
+        # overlap inside the cycle graph (C2: 65.0 ms with it on every step against 60.4 ms,
+        # profiles/r02_variants.md): on the last timed step only, as with --profile-last-only
+        last_only = args.profile_last_only or n < (1 << 21)
+        if it == (args.steps - 1 if last_only else 0):
             trplk.trplk_profile(ctx, True)
         flush.fill_(1.0)
         barrier()
